@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""FaSE throughput on B200: extrapolated blocks/s (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
+
+A *step* is one pass of the hot path over one batch: BASELINE config 1 by
+default -- 1,024 independent 48x48 areas per GPU with a centred 16x16 loss,
+DCT u Hadamard-48 (K = 4608), 200 iterations, FP64. Per step: batched initial
+products (DMMA GEMM), the FaSE recursion, synthesis of the lost samples. The
+shared Gram table is built once before the clock, exactly as the reference's
+own benchmark does (pkg/src/fase/bench.py:6-9,118-119); its build time is
+reported as ``gram_ms``.
+
+``value``: device-resident throughput (signals already in HBM), CUDA events
+per step on the launching stream, L2 flushed (256 MiB write) between steps.
+``e2e``: the same batch through ExtrapolationPlan.run_host -- pinned host
+signals -> device, kernels, selections / coefficients / lost samples -> pinned
+host -- all inside the timed region.
+
+Multi-GPU (torchrun): one process per GPU, each rank extrapolates its own 1,024
+blocks (weak scaling; blocks are independent, so no collective in the data
+path); time = max over ranks.
+
+--impl reference: the reference algorithm's CPU path (the oracle port of the
+pure-Python reference, oracle/fase_oracle.py) on all host cores, one process
+per core with one BLAS thread each; each step is a bounded sample of the same
+workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+from paper_2204_14194_b200 import workloads as wl  # noqa: E402
+from paper_2204_14194_b200.shard import dist_env  # noqa: E402
+
+HBM_FALLBACK_GBS = 6650.0
+FP64_FALLBACK_TFLOPS = 35.4
+REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x40: "sw_thermal_slowdown",
+           0x80: "hw_thermal_slowdown", 0x100: "hw_power_brake_slowdown",
+           0x2: "applications_clocks_setting", 0x20: "sync_boost"}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 4])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target wall seconds of the bounded CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- CPU reference
+
+
+_CPU = {}
+
+
+def _cpu_worker(args):
+    """Extrapolate blocks [first, first+n) of the workload with the oracle port."""
+    cid, first, n = args
+    from threadpoolctl import threadpool_limits
+
+    from oracle import fase_oracle as orc
+
+    w = wl.WORKLOADS[cid]
+    vals, mask, tables = _CPU["vals"], _CPU["mask"], _CPU["tables"]
+    nb = w.n_blocks
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        for i in range(n):
+            b = (first + i) % nb
+            sig = wl.block_signals(cid, 1, *w.area, first=b)[0]
+            orc.extrapolate_block(sig, mask, vals, w.config.gamma, w.config.iterations,
+                                  w.config.rho_hat, tables=tables)
+        return n, time.perf_counter() - t0
+
+
+def cpu_prepare(cid: int):
+    from oracle import fase_oracle as orc
+
+    w = wl.WORKLOADS[cid]
+    d = w.dictionary()
+    vals = d.real_values().astype(np.complex128)
+    mask = wl.central_loss_mask(*w.area, *w.loss)
+    tables = orc.gram(vals.reshape(len(vals), -1), orc.weight_field(mask, w.config.rho_hat))
+    _CPU.update(vals=vals, mask=mask, tables=tables)
+
+
+def cpu_sample(cid: int, seconds: float, pool, procs: int, per_block_s: float):
+    """One bounded sample: every worker extrapolates ~seconds worth of blocks."""
+    n = max(1, int(seconds / max(per_block_s, 1e-4)))
+    t0 = time.perf_counter()
+    out = pool.map(_cpu_worker, [(cid, p * n, n) for p in range(procs)])
+    wall = time.perf_counter() - t0
+    blocks = sum(o[0] for o in out)
+    return blocks / wall, blocks, wall
+
+
+def cpu_baseline(cid: int, seconds: float, steps: int = 1, warmup: int = 0):
+    import multiprocessing as mp
+
+    cpu_prepare(cid)
+    procs = os.cpu_count() or 1
+    # calibrate one block on one core
+    n1, t1 = _cpu_worker((cid, 0, 1))
+    per_block = t1 / n1
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        for _ in range(warmup):
+            cpu_sample(cid, seconds, pool, procs, per_block)
+        vals = [cpu_sample(cid, seconds, pool, procs, per_block) for _ in range(steps)]
+    rate = float(np.median([v[0] for v in vals]))
+    blocks, wall = vals[-1][1], vals[-1][2]
+    return {"value": rate, "unit": "blocks/s", "cores": procs, "kind": "port",
+            "sample": (f"{blocks} blocks of config {cid} per step ({procs} processes x 1 BLAS "
+                       f"thread, ~{wall:.1f} s wall), oracle/fase_oracle.py port of the reference "
+                       f"fase_extrapolate+apply_model with tables prebuilt; 1-core "
+                       f"{1.0 / per_block:.1f} blocks/s")}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    w = wl.WORKLOADS[args.config]
+    base = cpu_baseline(args.config, args.cpu_seconds, steps=args.steps, warmup=args.warmup)
+    line = {
+        "impl": "reference", "metric": "extrapolated blocks/s", "value": base["value"],
+        "unit": "blocks/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded, BASELINE Appendix-A generators)",
+        "config": workload_config(w, args.gpus), "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "blocks/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+
+
+def workload_config(w, n_gpus):
+    return {"workload": w.name, "blocks_per_gpu": w.n_blocks, "area": list(w.area),
+            "K": w.n_atoms, "M": w.area[0] * w.area[1],
+            "iterations": w.config.iterations, "gamma": w.config.gamma, "rho": w.config.rho_hat,
+            "dictionary": w.dict_spec, "loss": f"{w.loss[0]}x{w.loss[1]} centred",
+            "tables": "shared Gram prebuilt before the clock (reference bench.py:118-119)",
+            "l2": "flushed between timed steps (256 MiB write)",
+            "parallelism": f"dp{n_gpus} (block sharding, no collective)"}
+
+
+class ClockSampler:
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.path = ROOT / "gpurun_out" / f"clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.path.parent.mkdir(exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.gpu_id,
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+                mask = int(parts[2], 16)
+            except ValueError:
+                continue
+            for bit, name in REASONS.items():
+                if mask & bit:
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    hbm, src = HBM_FALLBACK_GBS, "fallback"
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            hbm, src = float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except (KeyError, ValueError):
+            pass
+    fp64, fsrc = FP64_FALLBACK_TFLOPS, "cuBLAS DGEMM 8192^3 measured r01"
+    q = ROOT / "profiles" / "r01_fp64_peak.json"
+    if q.exists():
+        fp64 = float(json.loads(q.read_text())["dgemm_8192_tflops"])
+    return hbm, src, fp64, fsrc
+
+
+def ncu_traffic(kernel: str):
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(kernel, {}).get("dram_bytes_per_launch")
+    except ValueError:
+        return None
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_14194_b200 import ExtrapolationPlan, _native, build_gram_tables, build_weight_field
+
+    rank, world, local = dist_env()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, args.cpu_seconds)  # before CUDA init (fork-safe)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _native.load()
+
+    w = wl.WORKLOADS[args.config]
+    d = w.dictionary()
+    K, M, I, B = len(d), w.area[0] * w.area[1], w.config.iterations, w.n_blocks
+    mask = wl.central_loss_mask(*w.area, *w.loss)
+    d.device_matrix(dev)
+    torch.cuda.synchronize()
+    g0 = torch.cuda.Event(enable_timing=True)
+    g1 = torch.cuda.Event(enable_timing=True)
+    g0.record()
+    tables = build_gram_tables(d, build_weight_field(mask, w.config.rho_hat), device=dev)
+    g1.record()
+    torch.cuda.synchronize()
+    gram_ms = g0.elapsed_time(g1)
+    plan = ExtrapolationPlan(d, mask, B, w.config, tables, device=dev)
+
+    host = torch.from_numpy(wl.block_signals(args.config, B, *w.area, first=rank * B)).pin_memory()
+    dev_sig = host.to(dev)
+    outs = plan.host_buffers()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(max(args.warmup, 0)):
+        plan.run(dev_sig)
+        plan.run_host(host, outs)
+    torch.cuda.synchronize()
+
+    def timed(fn, split=False):
+        evs = []
+        for _ in range(args.steps):
+            _native.l2_flush(flush)
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4 if split else 2)]
+            e[0].record(stream)
+            if split:
+                plan.F[:, :M].copy_(dev_sig.reshape(B, -1), non_blocking=True)
+                _native.init_products(plan.phi, plan.F, plan.W, K, M, plan.R0)
+                e[1].record(stream)
+                _native.iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, plan.selected,
+                                plan.projections, plan.coefficients)
+                e[2].record(stream)
+                _native.synth_paste(plan.phi, plan.selected, plan.coefficients, I, plan.lost_idx,
+                                    plan.lost, n_shared=plan.n_lost, dst=plan.lost_pos)
+                e[3].record(stream)
+            else:
+                fn()
+                e[1].record(stream)
+            evs.append(e)
+        return evs
+
+    gpu_id = str(local)
+    try:
+        uuid = torch.cuda.get_device_properties(dev).uuid
+        gpu_id = f"GPU-{uuid}"
+    except AttributeError:
+        pass
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(gpu_id) as clocks:
+        t_wall0 = time.perf_counter()
+        ev_dev = timed(None, split=True)
+        ev_e2e = timed(lambda: plan.run_host(host, outs))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    dev_ms = [e[0].elapsed_time(e[3]) for e in ev_dev]
+    init_ms = [e[0].elapsed_time(e[1]) for e in ev_dev]
+    iter_ms = [e[1].elapsed_time(e[2]) for e in ev_dev]
+    synth_ms = [e[2].elapsed_time(e[3]) for e in ev_dev]
+    e2e_ms = [e[0].elapsed_time(e[1]) for e in ev_e2e]
+    tot = torch.tensor([sum(dev_ms), sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    dev_total_s, e2e_total_s = tot[0].item() / 1e3, tot[1].item() / 1e3
+
+    # correctness guard on the timed outputs (cheap; not timed)
+    sel = plan.selected
+    assert int(sel.min()) >= 0 and int(sel.max()) < K, "selection out of range"
+    assert torch.isfinite(plan.lost).all(), "non-finite reconstruction"
+
+    if rank == 0:
+        hbm, hsrc, fp64, fsrc = measured_peaks()
+        it_s = float(np.mean(iter_ms)) / 1e3
+        bytes_iter = 8.0 * K * B * I
+        achieved = bytes_iter / it_s / 1e9
+        init_s = float(np.mean(init_ms)) / 1e3
+        flops_init = 2.0 * K * M * B
+        step_ms = dev_total_s / args.steps * 1e3
+        line = {
+            "metric": "extrapolated blocks/s",
+            "value": world * B * args.steps / dev_total_s,
+            "unit": "blocks/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": step_ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded BASELINE Appendix-A generators; random atoms: none)",
+            "config": workload_config(w, world),
+            "e2e": {"value": world * B * args.steps / e2e_total_s, "unit": "blocks/s",
+                    "h2d_bytes_per_step": plan.bytes_h2d(), "d2h_bytes_per_step": plan.bytes_d2h(),
+                    "ms_per_step": e2e_total_s / args.steps * 1e3,
+                    "api": "ExtrapolationPlan.run_host (pinned host in/out, one stream)"},
+            "roofline": {"bound": "hbm", "kernel": "fase_iterate_kernel",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": ncu_traffic("fase_iterate_kernel"),
+                         "algorithmic_bytes_per_launch": bytes_iter,
+                         "ms_per_launch": it_s * 1e3, "peak_source": hsrc,
+                         "note": "8*K bytes per block-iteration (one FP64 table row); hot rows "
+                                 "hit L2, so frac can exceed DRAM-bound expectations"},
+            "roofline_init": {"bound": "tensor", "kernel": "dgemm_nt_kernel (DMMA FP64)",
+                              "achieved": flops_init / init_s / 1e12, "peak": fp64,
+                              "unit": "TFLOP/s", "frac": flops_init / init_s / 1e12 / fp64,
+                              "ms_per_launch": init_s * 1e3, "peak_source": fsrc},
+            "stage_ms": {"init_products": float(np.mean(init_ms)), "iterate": float(np.mean(iter_ms)),
+                         "synth": float(np.mean(synth_ms))},
+            "gram_ms": gram_ms,
+            "gpu_launches": args.steps * (3 + 1) + args.steps * (plan.launches_per_run + 1),
+            "clocks": clocks.summary(),
+            "wall_s": t_wall,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/*
+ * fase_b200.h -- C ABI of the B200-native FaSE hot path (libfase_b200.so).
+ *
+ * The reference (`/root/reference/pkg/src/fase`) is a pure-Python package with
+ * no FFI layer; its boundary is the Python API re-exported from
+ * `pkg/src/fase/__init__.py:14-132`. These entry points are what a ctypes /
+ * cffi binding of that API binds (INTEGRATION.md shows the stub); each one
+ * names the reference function it replaces.
+ *
+ * Conventions
+ *   - Every pointer is DEVICE memory owned by the caller (e.g. a torch tensor);
+ *     the library never allocates or frees on these paths.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Work is enqueued asynchronously; errors of the enqueue are returned.
+ *   - Matrices are row-major float64 with an explicit leading dimension
+ *     (elements). Operands read with 16-byte vector loads require an even
+ *     leading dimension and 16-byte-aligned base pointers.
+ *   - Return value: FASE_OK (0) or a negative status. Status codes map 1:1 to
+ *     the reference exception classes (`pkg/src/fase/errors.py:8-47`);
+ *     fase_last_error() gives a thread-local message for the last failure.
+ *   - No global mutable state besides that message: calls are reentrant per
+ *     stream; the caller selects the device (cudaSetDevice / torch.cuda.device).
+ */
+#ifndef FASE_B200_H
+#define FASE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FASE_API __attribute__((visibility("default")))
+#else
+#define FASE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  FASE_OK = 0,
+  FASE_ERR_SHAPE = -1,          /* ShapeError            errors.py:8  */
+  FASE_ERR_PARAMETER = -2,      /* ParameterError        errors.py:12 */
+  FASE_ERR_MASK = -3,           /* MaskError             errors.py:16 */
+  FASE_ERR_FORMAT = -4,         /* FormatError           errors.py:20 */
+  FASE_ERR_DEGENERATE = -5,     /* DegenerateAtomError   errors.py:24 */
+  FASE_ERR_NO_SELECTABLE = -6,  /* NoSelectableAtomError errors.py:37 */
+  FASE_ERR_STALE = -7,          /* StaleTableError       errors.py:41 */
+  FASE_ERR_UNSUPPORTED = -8,    /* UnsupportedDictionaryError errors.py:45 */
+  FASE_ERR_CUDA = -100          /* CUDA launch / runtime failure */
+};
+
+/* Thread-local text of the last non-OK status of this thread. */
+FASE_API const char* fase_last_error(void);
+
+/* ABI version: (major << 16) | minor. */
+FASE_API int fase_abi_version(void);
+
+/* Largest dictionary size K the iteration kernel accepts. */
+FASE_API int fase_max_atoms(void);
+
+/*
+ * Basis construction (replaces the separable branch of generate_dictionary,
+ * dictionary.py:167-178, np.einsum("um,vn->uvmn")):
+ *   phi[(row0 + u*Lc + v) * ldphi + m*Nc + n] = rows[u*Mr + m] * cols[v*Nc + n]
+ * one correctly rounded multiply per sample, bit-identical to the einsum.
+ */
+FASE_API int fase_basis_outer(const double* rows, int Lr, int Mr, const double* cols, int Lc, int Nc,
+                     double* phi, int64_t ldphi, int64_t row0, void* stream);
+
+/*
+ * Weighted Gram table (replaces build_gram_tables, fast.py:109-142):
+ *   G[k*ldg + l] = sum_m (phi[k,m] * w[m]) * phi[l,m]      for k, l < K, m < M
+ * FP64 DMMA tiles; only the upper triangle is computed and mirrored exactly,
+ * so G is bit-symmetric. `w` is a length-M vector (ldw == 0) or a K x M matrix
+ * is NOT accepted here (tables are per weight).
+ */
+FASE_API int fase_gram(const double* phi, int64_t ldphi, const double* w, int K, int M,
+              double* G, int64_t ldg, void* stream);
+
+/*
+ * Normalizers (replaces _finish_tables, fast.py:97-106):
+ *   top = max_k G[k,k];  D[k] = (top > 0 && G[k,k] > 1e-12*top) ? 1/sqrt(G[k,k]) : 0
+ * `n_alive` (device int32, may be NULL) receives the number of non-degenerate atoms.
+ */
+FASE_API int fase_gram_finish(const double* G, int64_t ldg, int K, double* D, int32_t* n_alive,
+                     void* stream);
+
+/*
+ * Batched initial scalar products (replaces initial_scalar_products,
+ * fast.py:145-157, one zgemv per block):
+ *   R0[b*ldr + k] = sum_m (f[b*ldf + m] * w[b*ldw + m]) * phi[k*ldphi + m]
+ * ldw == 0 shares one weight vector across the batch.
+ */
+FASE_API int fase_init_products(const double* phi, int64_t ldphi, const double* f, int64_t ldf,
+                       const double* w, int64_t ldw, int K, int M, int B,
+                       double* R0, int64_t ldr, void* stream);
+
+/*
+ * Per-block normalizers for per-block geometries whose table rows are
+ * G_b = G0 - sum_{j in chunks(b)} C_j (see fase_iterate):
+ *   diag_b[k] = G0[k,k] - sum_j C_j[k,k];  D[b*ldd + k] as in fase_gram_finish.
+ * n_alive[b] receives the count of non-degenerate atoms of block b.
+ */
+FASE_API int fase_block_normalizers(const double* G0, int64_t ldg, const double* chunk_tables,
+                           int64_t chunk_stride, const int32_t* chunk_ptr,
+                           const int32_t* chunk_ids, int K, int B, double* D, int64_t ldd,
+                           int32_t* n_alive, void* stream);
+
+/*
+ * The FaSE recursion for B independent blocks (replaces the loop of
+ * fase_extrapolate, fast.py:224-255, with the tie rule of reference.py:55-85):
+ *   metric_k = |R_k| * D_k  (D_k == 0: never selectable)
+ *   q = max(q, 1e-13 * max metric);  u = lowest k with metric_k >= max - q
+ *   p = R_u * (D_u * D_u);  c = gamma * p;  R_k <- R_k - c * row_u[k]
+ * row_u = G0[u, :] - sum_{j in chunks(b)} C_j[u, :]   (chunk list empty when
+ * chunk_ptr == NULL: shared geometry). One persistent CTA per block keeps R and
+ * D in registers; rows are streamed with 16-byte loads.
+ *   R0, R_out: B x ldr (R_out may be NULL or alias R0)
+ *   D: shared vector (ldd == 0) or B x ldd
+ *   sel / proj / coef: B x ldo outputs (I entries per block)
+ *   R_log: NULL or B x I x ldr record of R after every iteration
+ */
+typedef struct {
+  const double* G0;
+  int64_t ldg;
+  const double* chunk_tables; /* C_j = chunk_tables + j * chunk_stride, row stride ldg */
+  int64_t chunk_stride;
+  const int32_t* chunk_ptr;   /* B+1 offsets into chunk_ids, or NULL */
+  const int32_t* chunk_ids;
+  const double* D;
+  int64_t ldd;
+  const double* R0;
+  int64_t ldr;
+  double* R_out;
+  double* R_log;
+  int K;
+  int B;
+  int I;
+  double gamma;
+  int32_t* sel;
+  double* proj;
+  double* coef;
+  int64_t ldo;
+} fase_iterate_args;
+
+FASE_API int fase_iterate(const fase_iterate_args* args, void* stream);
+
+/*
+ * Model synthesis and paste (replaces SparseModel.materialize + apply_model,
+ * reference.py:120-125 and fast.py:267-286, evaluated on lost samples only):
+ *   g = sum_t coef[b,t] * phi[sel[b,t], m]   accumulated in selection order
+ * For output position i of block b (list position i' = idx_ptr[b] + i, or
+ * i' = i for one shared list of n_shared samples when idx_ptr == NULL; the
+ * area sample is m = idx[i']):
+ *   dst == NULL : out[b*ldout + m]        = g   (patch (B, ldout) areas in place)
+ *   dst != NULL : out[b*ldout + dst[i']]  = g   (ldout = 0: paste into a frame at
+ *                                                absolute offsets; dst = 0..n-1 with
+ *                                                ldout = n: packed lost samples)
+ */
+FASE_API int fase_synth_paste(const double* phi, int64_t ldphi, const int32_t* sel, const double* coef,
+                     int64_t ldo, int I, int B, const int32_t* idx_ptr, const int32_t* idx,
+                     int n_shared, const int64_t* dst, double* out, int64_t ldout, void* stream);
+
+/* Writes `bytes` of zeros-then-ones into `buf` to evict L2 between timed steps. */
+FASE_API int fase_l2_flush(void* buf, size_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASE_B200_H */

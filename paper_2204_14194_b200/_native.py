@@ -1,0 +1,241 @@
+"""ctypes binding of libfase_b200.so (the C ABI in include/fase_b200.h).
+
+torch tensors are used as device buffers only: this module passes raw
+``data_ptr()`` values, leading dimensions and the current CUDA stream. A
+missing or unloadable library raises NativeLibraryError -- there is no CPU or
+eager fallback for any entry point.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from . import errors
+
+_LIB_PATH = Path(__file__).resolve().parent / "libfase_b200.so"
+_lib = None
+
+_STATUS = {
+    -1: errors.ShapeError,
+    -2: errors.ParameterError,
+    -3: errors.MaskError,
+    -4: errors.FormatError,
+    -5: errors.DegenerateAtomError,
+    -6: errors.NoSelectableAtomError,
+    -7: errors.StaleTableError,
+    -8: errors.UnsupportedDictionaryError,
+}
+
+EXPORTS = (
+    "fase_last_error", "fase_abi_version", "fase_max_atoms", "fase_basis_outer", "fase_gram",
+    "fase_gram_finish", "fase_init_products", "fase_block_normalizers", "fase_iterate",
+    "fase_synth_paste", "fase_l2_flush",
+)
+
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int
+_i64 = ctypes.c_int64
+_f64 = ctypes.c_double
+
+
+class IterateArgs(ctypes.Structure):
+    """Mirror of ``fase_iterate_args`` (include/fase_b200.h)."""
+
+    _fields_ = [
+        ("G0", _vp), ("ldg", _i64), ("chunk_tables", _vp), ("chunk_stride", _i64),
+        ("chunk_ptr", _vp), ("chunk_ids", _vp), ("D", _vp), ("ldd", _i64), ("R0", _vp),
+        ("ldr", _i64), ("R_out", _vp), ("R_log", _vp), ("K", _i32), ("B", _i32), ("I", _i32),
+        ("gamma", _f64), ("sel", _vp), ("proj", _vp), ("coef", _vp), ("ldo", _i64),
+    ]
+
+
+def library_path() -> Path:
+    return Path(os.environ.get("FASE_B200_LIB", _LIB_PATH))
+
+
+def load():
+    """Load the shared library once; NativeLibraryError if it is absent or broken."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = library_path()
+    if not path.exists():
+        raise errors.NativeLibraryError(
+            f"{path} is missing: run `python -m paper_2204_14194_b200._build` "
+            "(or __graft_entry__.build()) -- there is no CPU fallback")
+    try:
+        lib = ctypes.CDLL(str(path))
+    except OSError as exc:
+        raise errors.NativeLibraryError(f"cannot load {path}: {exc}") from exc
+    lib.fase_last_error.restype = ctypes.c_char_p
+    lib.fase_last_error.argtypes = []
+    lib.fase_abi_version.restype = _i32
+    lib.fase_max_atoms.restype = _i32
+    sigs = {
+        "fase_basis_outer": [_vp, _i32, _i32, _vp, _i32, _i32, _vp, _i64, _i64, _vp],
+        "fase_gram": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp],
+        "fase_gram_finish": [_vp, _i64, _i32, _vp, _vp, _vp],
+        "fase_init_products": [_vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp],
+        "fase_block_normalizers": [_vp, _i64, _vp, _i64, _vp, _vp, _i32, _i32, _vp, _i64, _vp,
+                                   _vp],
+        "fase_iterate": [ctypes.POINTER(IterateArgs), _vp],
+        "fase_synth_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
+                             _i64, _vp],
+        "fase_l2_flush": [_vp, ctypes.c_size_t, _vp],
+    }
+    for name, args in sigs.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _i32
+    _lib = lib
+    return lib
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    msg = _lib.fase_last_error().decode("utf-8", "replace")
+    cls = _STATUS.get(status)
+    if cls is None:
+        raise errors.NativeLibraryError(f"libfase_b200 status {status}: {msg}")
+    raise cls(msg)
+
+
+def _stream(tensor) -> int:
+    import torch
+
+    return torch.cuda.current_stream(tensor.device).cuda_stream
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _require(t, name, dtype=None, ndim=None):
+    import torch
+
+    if t is None:
+        raise errors.ShapeError(f"{name} is required")
+    if not t.is_cuda:
+        raise errors.NativeLibraryError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if dtype is not None and t.dtype != dtype:
+        raise errors.ShapeError(f"{name} must be {dtype}, got {t.dtype}")
+    if ndim is not None and t.dim() != ndim:
+        raise errors.ShapeError(f"{name} must be {ndim}-D, got shape {tuple(t.shape)}")
+    if t.dim() >= 1 and t.stride(-1) != 1:
+        raise errors.ShapeError(f"{name} must be contiguous in its last dimension")
+    return t
+
+
+def _ld(t) -> int:
+    return t.stride(0) if t.dim() == 2 else 0
+
+
+# ----------------------------------------------------------------- entry points
+
+
+def basis_outer(rows, cols, phi, row0: int) -> None:
+    import torch
+
+    lib = load()
+    _require(rows, "rows", torch.float64, 2)
+    _require(cols, "cols", torch.float64, 2)
+    _require(phi, "phi", torch.float64, 2)
+    lr, mr = rows.shape
+    lc, nc = cols.shape
+    _check(lib.fase_basis_outer(_ptr(rows), lr, mr, _ptr(cols), lc, nc, _ptr(phi), _ld(phi),
+                                row0, _stream(phi)))
+
+
+def gram(phi, w, K: int, M: int, G) -> None:
+    import torch
+
+    lib = load()
+    _require(phi, "phi", torch.float64, 2)
+    _require(w, "w", torch.float64, 1)
+    _require(G, "G", torch.float64, 2)
+    _check(lib.fase_gram(_ptr(phi), _ld(phi), _ptr(w), K, M, _ptr(G), _ld(G), _stream(G)))
+
+
+def gram_finish(G, K: int, D, n_alive=None) -> None:
+    import torch
+
+    lib = load()
+    _require(G, "G", torch.float64, 2)
+    _require(D, "D", torch.float64, 1)
+    _check(lib.fase_gram_finish(_ptr(G), _ld(G), K, _ptr(D), _ptr(n_alive), _stream(G)))
+
+
+def init_products(phi, f, w, K: int, M: int, R0) -> None:
+    """R0[b] = (f[b] o w[b or shared]) @ phi.T ; f, R0 2-D; w 1-D (shared) or 2-D."""
+    import torch
+
+    lib = load()
+    _require(phi, "phi", torch.float64, 2)
+    _require(f, "f", torch.float64, 2)
+    _require(w, "w", torch.float64)
+    _require(R0, "R0", torch.float64, 2)
+    ldw = _ld(w) if w.dim() == 2 else 0
+    _check(lib.fase_init_products(_ptr(phi), _ld(phi), _ptr(f), _ld(f), _ptr(w), ldw, K, M,
+                                  f.shape[0], _ptr(R0), _ld(R0), _stream(R0)))
+
+
+def block_normalizers(G0, chunk_tables, chunk_stride: int, chunk_ptr, chunk_ids, K: int,
+                      D, n_alive) -> None:
+    import torch
+
+    lib = load()
+    _require(G0, "G0", torch.float64, 2)
+    _require(D, "D", torch.float64, 2)
+    _check(lib.fase_block_normalizers(_ptr(G0), _ld(G0), _ptr(chunk_tables), chunk_stride,
+                                      _ptr(chunk_ptr), _ptr(chunk_ids), K, D.shape[0], _ptr(D),
+                                      _ld(D), _ptr(n_alive), _stream(D)))
+
+
+def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *,
+            chunk_tables=None, chunk_stride: int = 0, chunk_ptr=None, chunk_ids=None,
+            R_out=None, R_log=None) -> None:
+    import torch
+
+    lib = load()
+    _require(G0, "G0", torch.float64, 2)
+    _require(D, "D", torch.float64)
+    _require(R0, "R0", torch.float64, 2)
+    _require(sel, "sel", torch.int32, 2)
+    _require(proj, "proj", torch.float64, 2)
+    _require(coef, "coef", torch.float64, 2)
+    args = IterateArgs(
+        G0=_ptr(G0), ldg=_ld(G0), chunk_tables=_ptr(chunk_tables), chunk_stride=chunk_stride,
+        chunk_ptr=_ptr(chunk_ptr), chunk_ids=_ptr(chunk_ids), D=_ptr(D),
+        ldd=_ld(D) if D.dim() == 2 else 0, R0=_ptr(R0), ldr=_ld(R0), R_out=_ptr(R_out),
+        R_log=_ptr(R_log), K=K, B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel),
+        proj=_ptr(proj), coef=_ptr(coef), ldo=_ld(sel))
+    if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
+        raise errors.ShapeError("sel / proj / coef must share one leading dimension")
+    _check(lib.fase_iterate(ctypes.byref(args), _stream(R0)))
+
+
+def synth_paste(phi, sel, coef, iterations: int, idx, out, *, idx_ptr=None, n_shared: int = 0,
+                dst=None) -> None:
+    import torch
+
+    lib = load()
+    _require(phi, "phi", torch.float64, 2)
+    _require(idx, "idx", torch.int32, 1)
+    _require(out, "out", torch.float64)
+    B = sel.shape[0]
+    ldout = _ld(out) if out.dim() == 2 else 0
+    _check(lib.fase_synth_paste(_ptr(phi), _ld(phi), _ptr(sel), _ptr(coef), _ld(sel), iterations,
+                                B, _ptr(idx_ptr), _ptr(idx), n_shared, _ptr(dst), _ptr(out),
+                                ldout, _stream(out)))
+
+
+def l2_flush(buf) -> None:
+    lib = load()
+    _check(lib.fase_l2_flush(_ptr(buf), buf.numel() * buf.element_size(), _stream(buf)))
+
+
+def max_atoms() -> int:
+    return int(load().fase_max_atoms())

@@ -1,0 +1,262 @@
+// C ABI plumbing plus the small kernels of libfase_b200: basis expansion,
+// table normalizers, model synthesis / paste, L2 flush.
+
+#include <cstdarg>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace fase {
+
+namespace {
+thread_local char g_last_error[512] = "";
+}
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+}
+
+namespace {
+
+// phi[(row0 + u*Lc + v) * ld + m*Nc + n] = rows[u, m] * cols[v, n]
+// (reference dictionary.py:167-178: one rounded product per sample).
+__global__ void basis_outer_kernel(const double* __restrict__ rows, int Lr, int Mr,
+                                   const double* __restrict__ cols, int Lc, int Nc,
+                                   double* __restrict__ phi, int64_t ld, int64_t row0) {
+  const int64_t area = static_cast<int64_t>(Mr) * Nc;
+  const int64_t total = static_cast<int64_t>(Lr) * Lc * area;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t atom = i / area;
+    const int64_t s = i - atom * area;
+    const int u = static_cast<int>(atom / Lc);
+    const int v = static_cast<int>(atom - static_cast<int64_t>(u) * Lc);
+    const int m = static_cast<int>(s / Nc);
+    const int n = static_cast<int>(s - static_cast<int64_t>(m) * Nc);
+    phi[(row0 + atom) * ld + s] = mul_rn(rows[u * Mr + m], cols[v * Nc + n]);
+  }
+}
+
+// Block-wide max of non-negative doubles (fmax is exact).
+template <int NT>
+__device__ double block_max(double v, double* scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  double m = scratch[0];
+#pragma unroll
+  for (int w = 1; w < NT / 32; ++w) m = fmax(m, scratch[w]);
+  return m;
+}
+
+template <int NT>
+__device__ int block_sum(int v, int* scratch) {
+  v = __reduce_add_sync(0xffffffffu, v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  int s = 0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) s += scratch[w];
+  return s;
+}
+
+// D from a table diagonal: _finish_tables (reference fast.py:97-106).
+// 1.0 / sqrt(x): IEEE sqrt and division, both correctly rounded like numpy's.
+__device__ __forceinline__ double normalizer(double diag, double top) {
+  return (top > 0.0 && diag > mul_rn(1e-12, top)) ? 1.0 / sqrt(diag) : 0.0;
+}
+
+constexpr int kFinishThreads = 1024;
+
+__global__ void __launch_bounds__(kFinishThreads) gram_finish_kernel(const double* __restrict__ G,
+                                                                     int64_t ldg, int K,
+                                                                     double* __restrict__ D,
+                                                                     int32_t* n_alive) {
+  __shared__ double s_m[kFinishThreads / 32];
+  __shared__ int s_n[kFinishThreads / 32];
+  double m = 0.0;
+  for (int k = threadIdx.x; k < K; k += kFinishThreads) m = fmax(m, G[k * ldg + k]);
+  const double top = block_max<kFinishThreads>(m, s_m);
+  int alive = 0;
+  for (int k = threadIdx.x; k < K; k += kFinishThreads) {
+    const double dk = normalizer(G[k * ldg + k], top);
+    D[k] = dk;
+    alive += dk != 0.0;
+  }
+  alive = block_sum<kFinishThreads>(alive, s_n);
+  if (n_alive && threadIdx.x == 0) *n_alive = alive;
+}
+
+constexpr int kNormThreads = 256;
+
+__device__ __forceinline__ double chunk_diag(const double* G0, int64_t ldg, const double* tabs,
+                                             int64_t stride, const int32_t* ids, int nch, int k) {
+  const int64_t off = static_cast<int64_t>(k) * ldg + k;
+  double x = G0[off];
+  for (int c = 0; c < nch; ++c) x = sub_rn(x, tabs[static_cast<int64_t>(ids[c]) * stride + off]);
+  return x;
+}
+
+__global__ void __launch_bounds__(kNormThreads) block_normalizers_kernel(
+    const double* __restrict__ G0, int64_t ldg, const double* __restrict__ tabs, int64_t stride,
+    const int32_t* __restrict__ ptr, const int32_t* __restrict__ ids, int K,
+    double* __restrict__ D, int64_t ldd, int32_t* n_alive) {
+  __shared__ double s_m[kNormThreads / 32];
+  __shared__ int s_n[kNormThreads / 32];
+  const int b = blockIdx.x;
+  const int lo = ptr ? ptr[b] : 0;
+  const int nch = ptr ? ptr[b + 1] - lo : 0;
+  const int32_t* my = ids ? ids + lo : nullptr;
+  double m = 0.0;
+  for (int k = threadIdx.x; k < K; k += kNormThreads)
+    m = fmax(m, chunk_diag(G0, ldg, tabs, stride, my, nch, k));
+  const double top = block_max<kNormThreads>(m, s_m);
+  double* Db = D + static_cast<int64_t>(b) * ldd;
+  int alive = 0;
+  for (int k = threadIdx.x; k < K; k += kNormThreads) {
+    const double dk = normalizer(chunk_diag(G0, ldg, tabs, stride, my, nch, k), top);
+    Db[k] = dk;
+    alive += dk != 0.0;
+  }
+  alive = block_sum<kNormThreads>(alive, s_n);
+  if (n_alive && threadIdx.x == 0) n_alive[b] = alive;
+}
+
+// g = sum_t coef_t * phi[sel_t, m] in selection order: SparseModel.materialize
+// (reference.py:120-125) restricted to the lost samples, then the paste of
+// apply_model (fast.py:267-286). Selection terms are staged in shared memory.
+constexpr int kSynthThreads = 256;
+constexpr int kSynthChunk = 1024;
+
+__global__ void __launch_bounds__(kSynthThreads) synth_paste_kernel(
+    const double* __restrict__ phi, int64_t ldphi, const int32_t* __restrict__ sel,
+    const double* __restrict__ coef, int64_t ldo, int I, const int32_t* __restrict__ idx_ptr,
+    const int32_t* __restrict__ idx, int n_shared, const int64_t* __restrict__ dst,
+    double* __restrict__ out, int64_t ldout) {
+  __shared__ int32_t s_sel[kSynthChunk];
+  __shared__ double s_coef[kSynthChunk];
+  const int b = blockIdx.x;
+  const int lo = idx_ptr ? idx_ptr[b] : 0;
+  const int n = idx_ptr ? idx_ptr[b + 1] - lo : n_shared;
+  const int32_t* my_idx = idx + lo;
+  const int32_t* my_sel = sel + static_cast<int64_t>(b) * ldo;
+  const double* my_coef = coef + static_cast<int64_t>(b) * ldo;
+  for (int base = 0; base < n; base += kSynthThreads) {
+    const int i = base + threadIdx.x;
+    const int m = i < n ? my_idx[i] : 0;
+    double g = 0.0;
+    for (int t0 = 0; t0 < I; t0 += kSynthChunk) {
+      const int len = min(kSynthChunk, I - t0);
+      __syncthreads();
+      for (int t = threadIdx.x; t < len; t += kSynthThreads) {
+        s_sel[t] = my_sel[t0 + t];
+        s_coef[t] = my_coef[t0 + t];
+      }
+      __syncthreads();
+      if (i < n) {
+        for (int t = 0; t < len; ++t)
+          g = add_rn(g, mul_rn(s_coef[t], __ldg(phi + static_cast<int64_t>(s_sel[t]) * ldphi + m)));
+      }
+    }
+    if (i < n) out[(dst ? dst[lo + i] : static_cast<int64_t>(m)) + static_cast<int64_t>(b) * ldout] = g;
+  }
+}
+
+__global__ void flush_kernel(uint4* buf, size_t n, unsigned salt) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    buf[i] = make_uint4(salt, salt ^ 1u, salt ^ 2u, static_cast<unsigned>(i));
+}
+
+}  // namespace
+}  // namespace fase
+
+using namespace fase;
+
+extern "C" const char* fase_last_error(void) { return g_last_error; }
+
+extern "C" int fase_abi_version(void) { return (1 << 16) | 0; }
+
+extern "C" int fase_basis_outer(const double* rows, int Lr, int Mr, const double* cols, int Lc,
+                                int Nc, double* phi, int64_t ldphi, int64_t row0, void* stream) {
+  if (Lr < 1 || Mr < 1 || Lc < 1 || Nc < 1 || row0 < 0 || ldphi < static_cast<int64_t>(Mr) * Nc) {
+    set_error("fase_basis_outer: bad sizes (Lr=%d Mr=%d Lc=%d Nc=%d ld=%lld)", Lr, Mr, Lc, Nc,
+              static_cast<long long>(ldphi));
+    return FASE_ERR_SHAPE;
+  }
+  if (!rows || !cols || !phi) {
+    set_error("fase_basis_outer: null pointer");
+    return FASE_ERR_SHAPE;
+  }
+  const int64_t total = static_cast<int64_t>(Lr) * Lc * Mr * Nc;
+  const int threads = 256;
+  const int64_t blocks = (total + threads - 1) / threads;
+  basis_outer_kernel<<<static_cast<unsigned>(blocks < 148 * 64 ? blocks : 148 * 64), threads, 0,
+                       as_stream(stream)>>>(rows, Lr, Mr, cols, Lc, Nc, phi, ldphi, row0);
+  return check_launch("fase_basis_outer");
+}
+
+extern "C" int fase_gram_finish(const double* G, int64_t ldg, int K, double* D, int32_t* n_alive,
+                                void* stream) {
+  if (K < 1 || ldg < K || !G || !D) {
+    set_error("fase_gram_finish: bad operand (K=%d)", K);
+    return FASE_ERR_SHAPE;
+  }
+  gram_finish_kernel<<<1, kFinishThreads, 0, as_stream(stream)>>>(G, ldg, K, D, n_alive);
+  return check_launch("fase_gram_finish");
+}
+
+extern "C" int fase_block_normalizers(const double* G0, int64_t ldg, const double* chunk_tables,
+                                      int64_t chunk_stride, const int32_t* chunk_ptr,
+                                      const int32_t* chunk_ids, int K, int B, double* D,
+                                      int64_t ldd, int32_t* n_alive, void* stream) {
+  if (K < 1 || B < 0 || ldg < K || ldd < K || !G0 || !D) {
+    set_error("fase_block_normalizers: bad operand (K=%d, B=%d)", K, B);
+    return FASE_ERR_SHAPE;
+  }
+  if (chunk_ptr && (!chunk_ids || !chunk_tables)) {
+    set_error("fase_block_normalizers: chunk list without chunk tables");
+    return FASE_ERR_SHAPE;
+  }
+  if (B == 0) return FASE_OK;
+  block_normalizers_kernel<<<B, kNormThreads, 0, as_stream(stream)>>>(
+      G0, ldg, chunk_tables, chunk_stride, chunk_ptr, chunk_ids, K, D, ldd, n_alive);
+  return check_launch("fase_block_normalizers");
+}
+
+extern "C" int fase_synth_paste(const double* phi, int64_t ldphi, const int32_t* sel,
+                                const double* coef, int64_t ldo, int I, int B,
+                                const int32_t* idx_ptr, const int32_t* idx, int n_shared,
+                                const int64_t* dst, double* out, int64_t ldout, void* stream) {
+  if (I < 1 || B < 0 || ldo < I || (!idx_ptr && n_shared < 0)) {
+    set_error("fase_synth_paste: bad sizes (I=%d, B=%d)", I, B);
+    return FASE_ERR_SHAPE;
+  }
+  if (B == 0 || (!idx_ptr && n_shared == 0)) return FASE_OK;
+  if (!phi || !sel || !coef || !idx || !out) {
+    set_error("fase_synth_paste: null pointer");
+    return FASE_ERR_SHAPE;
+  }
+  synth_paste_kernel<<<B, kSynthThreads, 0, as_stream(stream)>>>(
+      phi, ldphi, sel, coef, ldo, I, idx_ptr, idx, n_shared, dst, out, ldout);
+  return check_launch("fase_synth_paste");
+}
+
+extern "C" int fase_l2_flush(void* buf, size_t bytes, void* stream) {
+  if (!buf || bytes < 16) {
+    set_error("fase_l2_flush: need a buffer of at least 16 bytes");
+    return FASE_ERR_SHAPE;
+  }
+  static unsigned salt = 0;
+  flush_kernel<<<148 * 8, 512, 0, as_stream(stream)>>>(static_cast<uint4*>(buf), bytes / 16,
+                                                       ++salt);
+  return check_launch("fase_l2_flush");
+}

@@ -1,0 +1,242 @@
+// FP64 tensor-core (DMMA) contractions of the FaSE correlation stage.
+//
+//   C[i, j] = sum_k (A[i, k] * W[i, k]) * B[j, k]        ("NT": both operands
+//                                                          contraction-contiguous)
+//
+// Used for the weighted Gram table G = (Phi o w) Phi^T (build_gram_tables,
+// reference fast.py:109-142) and the batched initial products
+// R0 = (F o W) Phi^T (initial_scalar_products, fast.py:145-157, one zgemv per
+// block in the reference). The weight is applied in the producer: the scaled
+// operand is formed in shared memory, one correctly rounded multiply per
+// sample, the same rounding structure as the reference's `conj(phi)*w` /
+// `s*w` before its BLAS call.
+//
+// Why DMMA and not tcgen05: tcgen05.mma has no f64 kind on sm_100a
+// (SURVEY.md section 0, item 7); FP64 on Blackwell's tensor cores is the
+// warp-level `mma.sync ... .f64` path, which ptxas lowers to DMMA.8x8x4.
+//
+// Tiling: 128 x 128 CTA tile, BK = 16, 3-stage cp.async ring, 8 warps as
+// 2 (M) x 4 (N), warp tile 64 x 32 = 8 x 4 DMMA 8x8 accumulators (64 FP64
+// registers). Shared rows are padded to 20 doubles: the 8x4 A/B fragment a
+// half-warp reads then hits 16 distinct 8-byte bank pairs.
+// Symmetric mode (Gram) computes tiles with bm <= bn only and writes each
+// accumulator to (i, j) and (j, i): the table is bit-symmetric.
+
+#include "common.cuh"
+
+namespace fase {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int BK = 16;
+constexpr int LDS = BK + 4;
+constexpr int STAGES = 3;
+constexpr int NTHREADS = 256;
+
+struct GemmParams {
+  const double* A;
+  int64_t lda;
+  const double* W;  // nullptr: no scaling; ldw == 0: one weight row for all i
+  int64_t ldw;
+  const double* B;
+  int64_t ldb;
+  double* C;
+  int64_t ldc;
+  int m_rows;
+  int n_rows;
+  int kdim;
+};
+
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <bool kSym, bool kScale>
+__global__ void __launch_bounds__(NTHREADS, 1) dgemm_nt_kernel(const GemmParams p) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = As + STAGES * BM * LDS;
+  double* Ws = Bs + STAGES * BN * LDS;
+
+  const int bm = blockIdx.y;
+  const int bn = blockIdx.x;
+  if (kSym && bm > bn) return;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int wm = warp >> 2;
+  const int wn = warp & 3;
+  const int row0 = bm * BM;
+  const int col0 = bn * BN;
+  const int ktiles = (p.kdim + BK - 1) / BK;
+
+  auto load_stage = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * NTHREADS;
+      const int r = idx >> 3;
+      const int kc = (idx & 7) * 2;
+      const int k = k0 + kc;
+      int kb = (p.kdim - k) * 8;
+      kb = kb < 0 ? 0 : (kb > 16 ? 16 : kb);
+      {
+        const int gr = row0 + r;
+        const int nb = gr < p.m_rows ? kb : 0;
+        const double* src = nb ? p.A + static_cast<int64_t>(gr) * p.lda + k : p.A;
+        cp_async16(As + (stage * BM + r) * LDS + kc, src, nb);
+        if (kScale) {
+          const double* ws = nb ? p.W + static_cast<int64_t>(gr) * p.ldw + k : p.W;
+          cp_async16(Ws + (stage * BM + r) * LDS + kc, ws, nb);
+        }
+      }
+      {
+        const int gr = col0 + r;
+        const int nb = gr < p.n_rows ? kb : 0;
+        const double* src = nb ? p.B + static_cast<int64_t>(gr) * p.ldb + k : p.B;
+        cp_async16(Bs + (stage * BN + r) * LDS + kc, src, nb);
+      }
+    }
+  };
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  const int fr = lane >> 2;
+  const int fc = lane & 3;
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    const int st = kt % STAGES;
+    if (kScale) {
+      // each thread scales exactly the chunks it copied itself
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int idx = tid + i * NTHREADS;
+        const int r = idx >> 3;
+        const int kc = (idx & 7) * 2;
+        double2* av = reinterpret_cast<double2*>(As + (st * BM + r) * LDS + kc);
+        const double2 wv = *reinterpret_cast<const double2*>(Ws + (st * BM + r) * LDS + kc);
+        double2 x = *av;
+        x.x = mul_rn(x.x, wv.x);
+        x.y = mul_rn(x.y, wv.y);
+        *av = x;
+      }
+    }
+    __syncthreads();
+    const int nk = kt + STAGES - 1;
+    if (nk < ktiles) load_stage(nk % STAGES, nk);
+    cp_async_commit();
+
+    const double* as = As + st * BM * LDS + (wm * 64 + fr) * LDS + fc;
+    const double* bs = Bs + st * BN * LDS + (wn * 32 + fr) * LDS + fc;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[8], b[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = as[i * 8 * LDS + kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = bs[j * 8 * LDS + kk];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  const bool vec_ok = ((p.ldc & 1) == 0) && aligned16(p.C);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = row0 + wm * 64 + i * 8 + fr;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = col0 + wn * 32 + j * 8 + fc * 2;
+      if (!kSym) {
+        if (r < p.m_rows) {
+          double* dst = p.C + static_cast<int64_t>(r) * p.ldc + c;
+          if (vec_ok && c + 1 < p.n_rows) {
+            *reinterpret_cast<double2*>(dst) = make_double2(acc[i][j][0], acc[i][j][1]);
+          } else {
+            if (c < p.n_rows) dst[0] = acc[i][j][0];
+            if (c + 1 < p.n_rows) dst[1] = acc[i][j][1];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cc = c + e;
+          if (r < p.m_rows && cc < p.n_rows && r <= cc) {
+            p.C[static_cast<int64_t>(r) * p.ldc + cc] = acc[i][j][e];
+            p.C[static_cast<int64_t>(cc) * p.ldc + r] = acc[i][j][e];
+          }
+        }
+      }
+    }
+  }
+}
+
+template <bool kSym, bool kScale>
+int launch(const GemmParams& p, cudaStream_t stream, const char* what) {
+  const size_t smem = sizeof(double) * STAGES * LDS * (BM + BN + (kScale ? BM : 0));
+  // per-device attribute; cheap enough to set on every launch
+  cudaError_t e = cudaFuncSetAttribute(dgemm_nt_kernel<kSym, kScale>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) {
+    set_error("%s: cudaFuncSetAttribute: %s", what, cudaGetErrorString(e));
+    return FASE_ERR_CUDA;
+  }
+  dim3 grid((p.n_rows + BN - 1) / BN, (p.m_rows + BM - 1) / BM);
+  dgemm_nt_kernel<kSym, kScale><<<grid, NTHREADS, smem, stream>>>(p);
+  return check_launch(what);
+}
+
+bool operand_ok(const double* ptr, int64_t ld) { return ptr && aligned16(ptr) && (ld % 2 == 0); }
+
+}  // namespace
+}  // namespace fase
+
+using namespace fase;
+
+extern "C" int fase_gram(const double* phi, int64_t ldphi, const double* w, int K, int M, double* G,
+                         int64_t ldg, void* stream) {
+  if (K < 1 || M < 1) {
+    set_error("fase_gram: K and M must be positive (K=%d, M=%d)", K, M);
+    return FASE_ERR_SHAPE;
+  }
+  if (!operand_ok(phi, ldphi) || ldphi < M || !w || !aligned16(w) || !G || ldg < K) {
+    set_error("fase_gram: bad operand (null, misaligned, odd or short leading dimension)");
+    return FASE_ERR_SHAPE;
+  }
+  GemmParams p{phi, ldphi, w, 0, phi, ldphi, G, ldg, K, K, M};
+  return launch<true, true>(p, as_stream(stream), "fase_gram");
+}
+
+extern "C" int fase_init_products(const double* phi, int64_t ldphi, const double* f, int64_t ldf,
+                                  const double* w, int64_t ldw, int K, int M, int B, double* R0,
+                                  int64_t ldr, void* stream) {
+  if (K < 1 || M < 1 || B < 0) {
+    set_error("fase_init_products: bad sizes (K=%d, M=%d, B=%d)", K, M, B);
+    return FASE_ERR_SHAPE;
+  }
+  if (B == 0) return FASE_OK;
+  if (!operand_ok(phi, ldphi) || ldphi < M || !operand_ok(f, ldf) || ldf < M || !w ||
+      !aligned16(w) || (ldw != 0 && (ldw % 2 || ldw < M)) || !R0 || ldr < K) {
+    set_error("fase_init_products: bad operand (null, misaligned, odd or short leading dimension)");
+    return FASE_ERR_SHAPE;
+  }
+  GemmParams p{f, ldf, w, ldw, phi, ldphi, R0, ldr, B, K, M};
+  return launch<false, true>(p, as_stream(stream), "fase_init_products");
+}

@@ -1,0 +1,699 @@
+"""FaSE on the B200: Gram tables, initial products, the recursion, synthesis.
+
+Drop-in for the reference's fast path (``pkg/src/fase/fast.py``): the same
+names, arguments, return types and error classes --
+``GramTable``, ``provenance_hash``, ``build_gram_tables``,
+``initial_scalar_products``, ``fase_extrapolate``, ``apply_model`` -- plus the
+batched entry point the BASELINE configs need, ``fase_extrapolate_batch``.
+
+Every numeric step runs in libfase_b200.so (csrc/); this module only
+validates arguments, hashes provenance on the host (blake2b, as the
+reference), builds the host-side weight field (bit-exact ``rho ** dist``), and
+moves buffers. There is no CPU fallback: without CUDA or the library every
+entry point raises NativeLibraryError.
+
+Per-block geometries (``masks`` of shape (B, M, N)) use *chunked tables*:
+samples are grouped into classes by their lost/kept pattern across the batch;
+G0 is the table of the weight that keeps every sample some block keeps, and
+C_j the table restricted to class j. Block b's table is
+G0 - sum_{j lost in b} C_j, applied row by row inside the recursion kernel,
+so per-block tables are never materialized.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .dictionary import Dictionary
+from .errors import (
+    MaskError,
+    NativeLibraryError,
+    NoSelectableAtomError,
+    ShapeError,
+    StaleTableError,
+    UnsupportedDictionaryError,
+)
+from .grid import (
+    ExtrapConfig,
+    as_mask,
+    as_real_field,
+    base_weight,
+    build_weight_field,
+)
+from .model import BatchResult, IterationTrace, SparseModel
+
+# Chunked per-block tables beyond this many bytes switch to one table per
+# distinct geometry (see _run_grouped).
+CHUNK_TABLE_BUDGET = 48 << 30
+
+
+def _round_up(x: int, to: int) -> int:
+    return (x + to - 1) // to * to
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def resolve_device(device=None):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("a CUDA device is required: the FaSE hot path has no CPU fallback")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise NativeLibraryError(f"device {dev} is not a CUDA device (no CPU fallback)")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def provenance_hash(dictionary: Dictionary, weight) -> int:
+    """blake2b-64 binding a table to (dictionary, weight) (``fast.py:87-94``)."""
+    w = np.ascontiguousarray(weight, dtype=np.float64).ravel()
+    h = hashlib.blake2b(digest_size=8)
+    h.update(b"gram-tables/1")
+    h.update(struct.pack("<2Q", dictionary.content_hash(), w.size))
+    h.update(w.tobytes())
+    return int.from_bytes(h.digest(), "little")
+
+
+class GramTable:
+    """Weighted cross-energies C = Phi W Phi^T and normalizers D of one weight.
+
+    Reference-compatible construction ``GramTable(c, d, provenance)`` from host
+    arrays (``fast.py:55-85``), or device-born from ``build_gram_tables``.
+    On the device the table is a (K, ldg) float64 matrix, ldg = K rounded up
+    to even, exactly symmetric.
+    """
+
+    def __init__(self, c=None, d=None, provenance: int = 0, *, G=None, D=None, n_alive=None):
+        self.provenance = int(provenance)
+        self._G = G
+        self._D = D
+        self._host_c = None
+        self._host_d = None
+        self._uploaded = {}
+        if G is None:
+            c = np.asarray(c)
+            d = np.asarray(d)
+            if c.ndim != 2 or c.shape[0] != c.shape[1]:
+                raise ShapeError(f"table must be square, got {c.shape}")
+            if d.shape != (c.shape[0],):
+                raise ShapeError(f"{d.shape[0] if d.ndim == 1 else d.shape} normalizers for a "
+                                 f"{c.shape[0]}-atom table")
+            self._host_c = c
+            self._host_d = np.asarray(d, dtype=np.float64)
+            self._k = c.shape[0]
+            self._n_alive = int(np.count_nonzero(self._host_d))
+        else:
+            self._k = int(G.shape[0])
+            self._n_alive = int(n_alive) if n_alive is not None else None
+
+    @property
+    def size(self) -> int:
+        return self._k
+
+    @property
+    def n_alive(self) -> int:
+        if self._n_alive is None:
+            self._n_alive = int((self._D != 0).sum().item())
+        return self._n_alive
+
+    @property
+    def d(self) -> np.ndarray:
+        if self._host_d is None:
+            self._host_d = self._D.cpu().numpy()
+        return self._host_d
+
+    @property
+    def c(self) -> np.ndarray:
+        """Host complex128 (K, K) copy (downloads a device table on first use)."""
+        if self._host_c is None:
+            self._host_c = self._G[:, : self._k].cpu().numpy().astype(np.complex128)
+        return self._host_c
+
+    def degenerate(self) -> np.ndarray:
+        return self.d == 0.0
+
+    def device_tables(self, device):
+        """(G, D) on ``device``; host-born tables are uploaded once (real part).
+
+        Raises UnsupportedDictionaryError for a table with imaginary content.
+        """
+        torch = _torch()
+        if self._G is not None:
+            if self._G.device != device:
+                raise ShapeError(f"table lives on {self._G.device}, run requested on {device}")
+            return self._G, self._D
+        key = (device.type, device.index)
+        if key not in self._uploaded:
+            c = self._host_c
+            if np.iscomplexobj(c):
+                if np.any(c.imag != 0):
+                    raise UnsupportedDictionaryError(
+                        "complex-valued tables are not supported by the FP64 GPU path")
+                c = c.real
+            k = self._k
+            G = torch.zeros((k, _round_up(k, 2)), dtype=torch.float64, device=device)
+            G[:, :k].copy_(torch.from_numpy(np.ascontiguousarray(c, dtype=np.float64)))
+            D = torch.from_numpy(self._host_d.copy()).to(device)
+            self._uploaded[key] = (G, D)
+        return self._uploaded[key]
+
+
+def _device_vector(x: np.ndarray, length: int, device):
+    torch = _torch()
+    out = torch.zeros(length, dtype=torch.float64, device=device)
+    out[: x.size].copy_(torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64).ravel()))
+    return out
+
+
+def _gram_on_device(phi, w_dev, K: int, M: int, device):
+    torch = _torch()
+    G = torch.zeros((K, _round_up(K, 2)), dtype=torch.float64, device=device)
+    _native.gram(phi, w_dev, K, M, G)
+    return G
+
+
+def build_gram_tables(dictionary: Dictionary, weight, *, block: int = 256, counter=None,
+                      device=None) -> GramTable:
+    """C and D for one (dictionary, weight) pair (``fast.py:109-142``).
+
+    Upper-triangle DMMA tiles mirrored exactly (``C == C.T`` bit-for-bit),
+    then D = 1/sqrt(diag) with the 1e-12 relative degeneracy cutoff.
+    ``block`` is accepted for signature compatibility (the device tile is
+    fixed); it must still be positive.
+    """
+    torch = _torch()
+    w = np.asarray(weight, dtype=np.float64).ravel()
+    if w.size != dictionary.area:
+        raise ShapeError(f"weight has {w.size} samples, atoms have {dictionary.area}")
+    if block < 1:
+        raise ShapeError(f"block must be positive, got {block}")
+    dev = resolve_device(device)
+    K, M = len(dictionary), dictionary.area
+    phi = dictionary.device_matrix(dev)
+    G = _gram_on_device(phi, _device_vector(w, dictionary.ld, dev), K, M, dev)
+    D = torch.empty(K, dtype=torch.float64, device=dev)
+    alive = torch.zeros(1, dtype=torch.int32, device=dev)
+    _native.gram_finish(G, K, D, alive)
+    if counter is not None:
+        counter.table_pair_products(M, (K * K + K) // 2)
+        counter.table_normalizers(K)
+    return GramTable(G=G, D=D, provenance=provenance_hash(dictionary, w), n_alive=int(alive.item()))
+
+
+def initial_scalar_products(signal, weight, dictionary: Dictionary, *, counter=None,
+                            device=None) -> np.ndarray:
+    """R0_k = sum s * w * phi_k over the area (``fast.py:145-157``), on the GPU."""
+    torch = _torch()
+    s = as_real_field(signal)
+    w = np.asarray(weight, dtype=np.float64)
+    if w.shape != s.shape:
+        raise ShapeError(f"signal {s.shape} vs weight {w.shape}")
+    if dictionary.shape != s.shape:
+        raise ShapeError(f"signal {s.shape} vs dictionary area {dictionary.shape}")
+    dev = resolve_device(device)
+    K = len(dictionary)
+    phi = dictionary.device_matrix(dev)
+    f = _device_vector(s, dictionary.ld, dev).reshape(1, -1)
+    R0 = torch.empty((1, _round_up(K, 2)), dtype=torch.float64, device=dev)
+    _native.init_products(phi, f, _device_vector(w, dictionary.ld, dev), K, dictionary.area, R0)
+    if counter is not None:
+        counter.fase_initial(s.size, K)
+    return R0[0, :K].cpu().numpy().astype(np.complex128)
+
+
+# ----------------------------------------------------------------- batches
+
+
+def _signals_on_device(signals, dictionary: Dictionary, device):
+    """(B, ld) float64 device matrix of the block signals (a view when possible)."""
+    torch = _torch()
+    m, n = dictionary.shape
+    area = m * n
+    if isinstance(signals, torch.Tensor):
+        if signals.dim() != 3 or tuple(signals.shape[1:]) != (m, n):
+            raise ShapeError(f"signals {tuple(signals.shape)} vs dictionary area {(m, n)}")
+        if signals.dtype != torch.float64:
+            raise ShapeError(f"signals must be float64, got {signals.dtype}")
+        flat = signals.to(device).reshape(signals.shape[0], area)
+    else:
+        arr = np.asarray(signals)
+        if np.iscomplexobj(arr):
+            if np.any(arr.imag != 0):
+                raise UnsupportedDictionaryError("complex signals are not supported on the GPU path")
+            arr = arr.real
+        if arr.ndim != 3 or arr.shape[1:] != (m, n):
+            raise ShapeError(f"signals {arr.shape} vs dictionary area {(m, n)}")
+        flat = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64).reshape(-1, area))
+        flat = flat.to(device, non_blocking=True)
+    if area % 2 == 0 and flat.is_contiguous():
+        return flat
+    out = torch.zeros((flat.shape[0], dictionary.ld), dtype=torch.float64, device=device)
+    out[:, :area].copy_(flat)
+    return out
+
+
+@dataclass
+class ChunkPlan:
+    """Sample classes of a batch of per-block masks (host side).
+
+    base_lost: (M,) lost in every block; classes: list of sample-index arrays
+    of the mixed classes; ptr/ids: CSR of the classes each block loses.
+    """
+
+    base_lost: np.ndarray
+    classes: list
+    ptr: np.ndarray
+    ids: np.ndarray
+
+    @property
+    def n_classes(self) -> int:
+        return len(self.classes)
+
+
+def chunk_plan(masks: np.ndarray) -> ChunkPlan:
+    """Group samples by their lost/kept pattern across the batch."""
+    b = masks.shape[0]
+    flat = masks.reshape(b, -1)
+    lost_any = flat.any(axis=0)
+    lost_all = flat.all(axis=0)
+    mixed = np.flatnonzero(lost_any & ~lost_all)
+    if mixed.size == 0:
+        classes, member = [], np.zeros((b, 0), dtype=bool)
+    else:
+        packed = np.packbits(flat[:, mixed], axis=0).T  # (n_mixed, ceil(B/8))
+        _, first, inverse = np.unique(packed, axis=0, return_index=True, return_inverse=True)
+        inverse = inverse.ravel()
+        classes = [mixed[inverse == j] for j in range(len(first))]
+        member = flat[:, mixed[first]]  # (B, n_classes): block loses class j
+    counts = member.sum(axis=1)
+    ptr = np.zeros(b + 1, dtype=np.int32)
+    np.cumsum(counts, out=ptr[1:])
+    ids = np.nonzero(member)[1].astype(np.int32)
+    return ChunkPlan(base_lost=lost_all, classes=classes, ptr=ptr, ids=ids)
+
+
+class ChunkedTables:
+    """Device tables for a batch of per-block geometries: G0 and the class tables."""
+
+    def __init__(self, dictionary: Dictionary, masks: np.ndarray, rho_hat: float, device):
+        torch = _torch()
+        self.device = device
+        self.rho_hat = rho_hat
+        m, n = dictionary.shape
+        K, M = len(dictionary), m * n
+        self.plan = chunk_plan(masks)
+        base = base_weight(m, n, rho_hat).ravel()
+        w0 = base.copy()
+        w0[self.plan.base_lost] = 0.0
+        phi = dictionary.device_matrix(device)
+        self.G0 = _gram_on_device(phi, _device_vector(w0, dictionary.ld, device), K, M, device)
+        ldg = self.G0.shape[1]
+        nc = self.plan.n_classes
+        self.tables = torch.zeros((max(nc, 1), K, ldg), dtype=torch.float64, device=device)
+        for j, samples in enumerate(self.plan.classes):
+            cols = torch.from_numpy(samples.astype(np.int64)).to(device)
+            width = _round_up(len(samples), 2)
+            sub = torch.zeros((K, width), dtype=torch.float64, device=device)
+            sub[:, : len(samples)] = phi.index_select(1, cols)
+            wj = torch.zeros(width, dtype=torch.float64, device=device)
+            wj[: len(samples)] = torch.from_numpy(base[samples]).to(device)
+            _native.gram(sub, wj, K, len(samples), self.tables[j])
+        self.ptr = torch.from_numpy(self.plan.ptr).to(device)
+        self.ids = torch.from_numpy(self.plan.ids if self.plan.ids.size else
+                                    np.zeros(1, np.int32)).to(device)
+        self.masks = masks
+        self.key = (dictionary.content_hash(), masks.shape, hashlib.blake2b(
+            np.packbits(masks).tobytes(), digest_size=16).hexdigest(), rho_hat)
+
+    @staticmethod
+    def table_bytes(dictionary: Dictionary, masks: np.ndarray) -> int:
+        plan = chunk_plan(masks)
+        k = len(dictionary)
+        return (plan.n_classes + 1) * k * _round_up(k, 2) * 8
+
+
+def _validate_masks(masks, dictionary: Dictionary, n_blocks: int):
+    m, n = dictionary.shape
+    arr = np.asarray(masks, dtype=bool)
+    if arr.ndim == 2:
+        if arr.shape != (m, n):
+            raise ShapeError(f"mask {arr.shape} vs dictionary area {(m, n)}")
+        if arr.all():
+            raise MaskError("loss mask marks every sample lost; nothing to extrapolate from")
+        return arr, True
+    if arr.ndim != 3 or arr.shape != (n_blocks, m, n):
+        raise ShapeError(f"masks {arr.shape} vs ({n_blocks}, {m}, {n})")
+    full = arr.reshape(n_blocks, -1).all(axis=1)
+    if full.any():
+        raise MaskError(f"block {int(np.flatnonzero(full)[0])}: every sample is lost")
+    if n_blocks > 0 and (arr == arr[0]).all():
+        return arr[0], True
+    return arr, False
+
+
+def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
+                           config: ExtrapConfig = ExtrapConfig(), *, products=None,
+                           record_products: bool = False, patch: bool = True,
+                           device=None) -> BatchResult:
+    """Run FaSE on B independent blocks; equals B calls of ``fase_extrapolate``.
+
+    Args:
+        signals: (B, M, N) float64 -- numpy (host) or torch (any device).
+        masks: (M, N) shared loss mask, or (B, M, N) per-block masks.
+        dictionary: atoms over the (M, N) area (real-valued).
+        tables: shared geometry -- a GramTable for the shared weight (built
+            when None; StaleTableError on a provenance mismatch); per-block
+            geometry -- None or a ChunkedTables built for these masks.
+        config: iterations / gamma / rho_hat.
+        products: optional (B, K) initial products (skips the GEMM).
+        record_products: keep R after every iteration (B, I, K) -- test use.
+        patch: produce the patched (B, M, N) areas.
+
+    Returns:
+        BatchResult with device tensors.
+    """
+    torch = _torch()
+    if not dictionary.is_real:
+        raise UnsupportedDictionaryError("complex-valued dictionaries are not supported on the GPU path")
+    dev = resolve_device(device)
+    F = _signals_on_device(signals, dictionary, dev)
+    B = F.shape[0]
+    K, M = len(dictionary), dictionary.area
+    if K > _native.max_atoms():
+        raise UnsupportedDictionaryError(f"K={K} exceeds the iteration kernel's {_native.max_atoms()}")
+    mask, shared = _validate_masks(masks, dictionary, B)
+    I = config.iterations
+    phi = dictionary.device_matrix(dev)
+
+    chunk_args = {}
+    if shared:
+        w = build_weight_field(mask, config.rho_hat)
+        if tables is None:
+            tables = build_gram_tables(dictionary, w, device=dev)
+        elif not isinstance(tables, GramTable):
+            raise StaleTableError("per-block tables given for a shared geometry")
+        if tables.size != K:
+            raise StaleTableError(f"tables hold {tables.size} atoms, dictionary has {K}")
+        if tables.provenance != provenance_hash(dictionary, w):
+            raise StaleTableError("table provenance mismatch: tables were built for a different "
+                                  "dictionary/weight combination")
+        if tables.n_alive == 0:
+            raise NoSelectableAtomError("every atom has zero weighted energy")
+        G, D = tables.device_tables(dev)
+        W = _device_vector(w, dictionary.ld, dev)
+        lost_idx = np.flatnonzero(mask.ravel()).astype(np.int32)
+    else:
+        if tables is None:
+            if ChunkedTables.table_bytes(dictionary, mask) > CHUNK_TABLE_BUDGET:
+                return _run_grouped(F, mask, dictionary, config, dev, patch)
+            tables = ChunkedTables(dictionary, mask, config.rho_hat, dev)
+        elif not isinstance(tables, ChunkedTables) or tables.masks.shape != mask.shape or \
+                not np.array_equal(tables.masks, mask) or tables.rho_hat != config.rho_hat:
+            raise StaleTableError("chunked tables were built for other masks / rho_hat")
+        G = tables.G0
+        D = torch.empty((B, G.shape[1]), dtype=torch.float64, device=dev)
+        alive = torch.empty(B, dtype=torch.int32, device=dev)
+        stride = tables.tables[0].numel()
+        _native.block_normalizers(G, tables.tables, stride, tables.ptr, tables.ids, K, D, alive)
+        dead = torch.nonzero(alive == 0)
+        if dead.numel():
+            raise NoSelectableAtomError(f"block {int(dead[0, 0])}: every atom has zero weighted energy")
+        chunk_args = dict(chunk_tables=tables.tables, chunk_stride=stride, chunk_ptr=tables.ptr,
+                          chunk_ids=tables.ids)
+        base = torch.from_numpy(base_weight(*dictionary.shape, config.rho_hat).ravel()).to(dev)
+        mdev = torch.from_numpy(mask.reshape(B, -1)).to(dev)
+        W = torch.zeros((B, F.shape[1]), dtype=torch.float64, device=dev)
+        W[:, :M] = torch.where(mdev, torch.zeros((), dtype=torch.float64, device=dev), base)
+        lost_idx = None
+
+    ldr = _round_up(K, 2)
+    if products is None:
+        R0 = torch.empty((B, ldr), dtype=torch.float64, device=dev)
+        _native.init_products(phi, F, W, K, M, R0)
+    else:
+        R0 = _products_on_device(products, B, K, ldr, dev)
+    sel = torch.empty((B, I), dtype=torch.int32, device=dev)
+    proj = torch.empty((B, I), dtype=torch.float64, device=dev)
+    coef = torch.empty((B, I), dtype=torch.float64, device=dev)
+    R_log = torch.empty((B, I, ldr), dtype=torch.float64, device=dev) if record_products else None
+    _native.iterate(G, D, R0, K, I, config.gamma, sel, proj, coef, R_log=R_log, **chunk_args)
+
+    patched = None
+    if patch:
+        patched = F[:, :M].clone() if F.shape[1] != M else F.clone()
+        if shared:
+            if lost_idx.size:
+                idx = torch.from_numpy(lost_idx).to(dev)
+                _native.synth_paste(phi, sel, coef, I, idx, patched, n_shared=int(lost_idx.size))
+        else:
+            flat = mask.reshape(B, -1)
+            counts = flat.sum(axis=1)
+            ptr = np.zeros(B + 1, dtype=np.int32)
+            np.cumsum(counts, out=ptr[1:])
+            idx = np.nonzero(flat)[1].astype(np.int32)
+            if idx.size:
+                _native.synth_paste(phi, sel, coef, I, torch.from_numpy(idx).to(dev), patched,
+                                    idx_ptr=torch.from_numpy(ptr).to(dev))
+        patched = patched.reshape(B, *dictionary.shape)
+    prods = R_log[:, :, :K] if R_log is not None else None
+    return BatchResult(selected=sel, projections=proj, coefficients=coef, patched=patched,
+                       products=prods, dictionary=dictionary, shape=dictionary.shape)
+
+
+class ExtrapolationPlan:
+    """A prepared shared-geometry batch: validate, hash and build tables once,
+    then ``run`` only enqueues the three kernels (initial products, recursion,
+    synthesis) on the current stream -- no host work, no synchronization.
+
+    Outputs live in preallocated device buffers: ``selected`` (B, I) int32,
+    ``coefficients`` / ``projections`` (B, I) float64 and ``lost`` (B, L)
+    float64, the reconstructed lost samples in row-major mask order.
+    ``run_host`` is the end-to-end form: pinned host signals in, pinned host
+    results out, copies on the same stream.
+    """
+
+    def __init__(self, dictionary: Dictionary, mask, n_blocks: int,
+                 config: ExtrapConfig = ExtrapConfig(), tables: GramTable | None = None,
+                 device=None):
+        torch = _torch()
+        if not dictionary.is_real:
+            raise UnsupportedDictionaryError("complex-valued dictionaries are not supported on the GPU path")
+        self.device = dev = resolve_device(device)
+        self.dictionary = dictionary
+        self.config = config
+        mask = as_mask(mask)
+        if mask.shape != dictionary.shape:
+            raise ShapeError(f"mask {mask.shape} vs dictionary area {dictionary.shape}")
+        w = build_weight_field(mask, config.rho_hat)
+        if tables is None:
+            tables = build_gram_tables(dictionary, w, device=dev)
+        if tables.size != len(dictionary):
+            raise StaleTableError(f"tables hold {tables.size} atoms, dictionary has {len(dictionary)}")
+        if tables.provenance != provenance_hash(dictionary, w):
+            raise StaleTableError("table provenance mismatch")
+        if tables.n_alive == 0:
+            raise NoSelectableAtomError("every atom has zero weighted energy")
+        self.tables = tables
+        self.G, self.D = tables.device_tables(dev)
+        K, M, I = len(dictionary), dictionary.area, config.iterations
+        if K > _native.max_atoms():
+            raise UnsupportedDictionaryError(f"K={K} exceeds the iteration kernel's {_native.max_atoms()}")
+        self.K, self.M, self.I, self.B = K, M, I, int(n_blocks)
+        self.phi = dictionary.device_matrix(dev)
+        self.W = _device_vector(w, dictionary.ld, dev)
+        ldf = M if M % 2 == 0 else dictionary.ld
+        self.F = torch.zeros((self.B, ldf), dtype=torch.float64, device=dev)
+        self.R0 = torch.empty((self.B, _round_up(K, 2)), dtype=torch.float64, device=dev)
+        self.selected = torch.empty((self.B, I), dtype=torch.int32, device=dev)
+        self.projections = torch.empty((self.B, I), dtype=torch.float64, device=dev)
+        self.coefficients = torch.empty((self.B, I), dtype=torch.float64, device=dev)
+        lost = np.flatnonzero(mask.ravel()).astype(np.int32)
+        self.n_lost = int(lost.size)
+        self.lost_idx = torch.from_numpy(lost if lost.size else np.zeros(1, np.int32)).to(dev)
+        self.lost_pos = torch.arange(max(self.n_lost, 1), dtype=torch.int64, device=dev)
+        self.lost = torch.zeros((self.B, max(self.n_lost, 1)), dtype=torch.float64, device=dev)
+        self.launches_per_run = 3 if self.n_lost else 2
+
+    def run(self, signals=None):
+        """Enqueue one batch. ``signals``: None (use ``self.F`` as filled by the
+        caller) or a (B, M, N) / (B, M) float64 tensor on any device (copied
+        asynchronously into the device buffer)."""
+        if signals is not None:
+            src = signals.reshape(self.B, -1)
+            self.F[:, : self.M].copy_(src, non_blocking=True)
+        _native.init_products(self.phi, self.F, self.W, self.K, self.M, self.R0)
+        _native.iterate(self.G, self.D, self.R0, self.K, self.I, self.config.gamma, self.selected,
+                        self.projections, self.coefficients)
+        if self.n_lost:
+            _native.synth_paste(self.phi, self.selected, self.coefficients, self.I, self.lost_idx,
+                                self.lost, n_shared=self.n_lost, dst=self.lost_pos)
+        return self
+
+    def host_buffers(self):
+        """Pinned host buffers matching the outputs (for ``run_host``)."""
+        torch = _torch()
+        return {
+            "selected": torch.empty(tuple(self.selected.shape), dtype=torch.int32, pin_memory=True),
+            "coefficients": torch.empty(tuple(self.coefficients.shape), dtype=torch.float64,
+                                        pin_memory=True),
+            "lost": torch.empty(tuple(self.lost.shape), dtype=torch.float64, pin_memory=True),
+        }
+
+    def run_host(self, host_signals, out: dict):
+        """H2D of pinned ``host_signals`` (B, M, N), the batch, D2H of selections,
+        coefficients and lost samples into pinned ``out`` -- all on one stream."""
+        self.run(host_signals)
+        out["selected"].copy_(self.selected, non_blocking=True)
+        out["coefficients"].copy_(self.coefficients, non_blocking=True)
+        out["lost"].copy_(self.lost, non_blocking=True)
+        return out
+
+    def bytes_h2d(self) -> int:
+        return self.B * self.M * 8
+
+    def bytes_d2h(self) -> int:
+        return self.selected.numel() * 4 + self.coefficients.numel() * 8 + self.lost.numel() * 8
+
+
+def _products_on_device(products, B: int, K: int, ldr: int, device):
+    torch = _torch()
+    if isinstance(products, torch.Tensor):
+        p = products.to(device)
+        if p.is_complex():
+            if torch.any(p.imag != 0):
+                raise UnsupportedDictionaryError("complex products on the real GPU path")
+            p = p.real
+    else:
+        arr = np.asarray(products)
+        if np.iscomplexobj(arr):
+            if np.any(arr.imag != 0):
+                raise UnsupportedDictionaryError("complex products on the real GPU path")
+            arr = arr.real
+        p = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device)
+    p = p.reshape(-1, K) if p.dim() == 1 else p
+    if tuple(p.shape) != (B, K):
+        raise ShapeError(f"products shape {tuple(p.shape)}, expected ({B}, {K})")
+    R0 = torch.zeros((B, ldr), dtype=torch.float64, device=device)
+    R0[:, :K].copy_(p)
+    return R0
+
+
+def _run_grouped(F, masks, dictionary, config, dev, patch):
+    """One table per distinct geometry (fallback when chunk tables would not fit)."""
+    torch = _torch()
+    B = F.shape[0]
+    flat = masks.reshape(B, -1)
+    uniq, inverse = np.unique(flat, axis=0, return_inverse=True)
+    inverse = inverse.ravel()
+    I = config.iterations
+    sel = torch.empty((B, I), dtype=torch.int32, device=dev)
+    proj = torch.empty((B, I), dtype=torch.float64, device=dev)
+    coef = torch.empty((B, I), dtype=torch.float64, device=dev)
+    patched = F[:, : dictionary.area].clone() if patch else None
+    for g in range(uniq.shape[0]):
+        rows = np.flatnonzero(inverse == g)
+        ridx = torch.from_numpy(rows).to(dev)
+        sub = fase_extrapolate_batch(F.index_select(0, ridx).reshape(-1, *dictionary.shape),
+                                     uniq[g].reshape(dictionary.shape), dictionary, None, config,
+                                     patch=patch, device=dev)
+        sel[ridx] = sub.selected
+        proj[ridx] = sub.projections
+        coef[ridx] = sub.coefficients
+        if patch:
+            patched[ridx] = sub.patched.reshape(len(rows), -1)
+    if patch:
+        patched = patched.reshape(B, *dictionary.shape)
+    return BatchResult(selected=sel, projections=proj, coefficients=coef, patched=patched,
+                       dictionary=dictionary, shape=dictionary.shape)
+
+
+# ----------------------------------------------------------------- single block
+
+
+def fase_extrapolate(signal, mask, dictionary: Dictionary, tables: GramTable,
+                     config: ExtrapConfig = ExtrapConfig(), *, products=None,
+                     record_products: bool = False, counter=None, device=None):
+    """Scalar-product recursion for one area (``fast.py:160-264``).
+
+    Same checks in the same order as the reference: shapes, atom count,
+    provenance (StaleTableError), all-degenerate (NoSelectableAtomError).
+    Returns (SparseModel, IterationTrace) with host arrays.
+    """
+    s = as_real_field(signal)
+    mask = as_mask(mask)
+    if mask.shape != s.shape:
+        raise ShapeError(f"signal {s.shape} vs mask {mask.shape}")
+    if dictionary.shape != s.shape:
+        raise ShapeError(f"signal {s.shape} vs dictionary area {dictionary.shape}")
+    if tables.size != len(dictionary):
+        raise StaleTableError(f"tables hold {tables.size} atoms, dictionary has {len(dictionary)}")
+    w = build_weight_field(mask, config.rho_hat)
+    if tables.provenance != provenance_hash(dictionary, w):
+        raise StaleTableError("table provenance mismatch: tables were built for a different "
+                              "dictionary/weight combination")
+    if tables.n_alive == 0:
+        raise NoSelectableAtomError("every atom has zero weighted energy")
+    if products is not None:
+        p = np.asarray(products)
+        if p.shape != (len(dictionary),):
+            raise ShapeError(f"products shape {p.shape}, expected ({len(dictionary)},)")
+        products = p.reshape(1, -1)
+    res = fase_extrapolate_batch(s[None], mask, dictionary, tables, config, products=products,
+                                 record_products=record_products, patch=False, device=device)
+    model, trace = res.block(0)
+    if counter is not None:
+        if products is None:
+            counter.fase_initial(s.size, len(dictionary))
+        for _ in range(config.iterations):
+            counter.fase_selection(len(dictionary))
+            counter.fase_update(s.size, len(dictionary))
+    return model, trace
+
+
+def apply_model(signal, model: SparseModel, mask, *, device=None):
+    """Replace lost samples by Re(g) (``fast.py:267-286``); g on the GPU.
+
+    Returns (patched float64 field, max |Im g| over lost samples) -- the latter
+    is exactly 0.0 for the real dictionaries of the GPU path.
+    """
+    torch = _torch()
+    s = np.asarray(signal)
+    mask = as_mask(mask)
+    if s.shape != mask.shape:
+        raise ShapeError(f"signal {s.shape} vs mask {mask.shape}")
+    if tuple(model.shape) != s.shape:
+        raise ShapeError(f"signal {s.shape} vs model area {model.shape}")
+    out = s.astype(np.complex128 if np.iscomplexobj(s) else np.float64, copy=True)
+    if not mask.any():
+        return out, 0.0
+    if len(model.terms) == 0:
+        out[mask] = 0.0
+        return out, 0.0
+    dictionary = model.dictionary
+    if not dictionary.is_real:
+        raise UnsupportedDictionaryError("complex-valued models are not supported on the GPU path")
+    coefs = np.array([c for _, c in model.terms], dtype=np.complex128)
+    if np.any(coefs.imag != 0):
+        raise UnsupportedDictionaryError("complex coefficients on the real GPU path")
+    dev = resolve_device(device)
+    phi = dictionary.device_matrix(dev)
+    sel = torch.tensor([[int(k) for k, _ in model.terms]], dtype=torch.int32, device=dev)
+    coef = torch.from_numpy(coefs.real.reshape(1, -1).copy()).to(dev)
+    idx = np.flatnonzero(mask.ravel()).astype(np.int32)
+    g = torch.zeros((1, s.size), dtype=torch.float64, device=dev)
+    _native.synth_paste(phi, sel, coef, len(model.terms), torch.from_numpy(idx).to(dev), g,
+                        n_shared=int(idx.size))
+    out[mask] = g.cpu().numpy().ravel()[idx]
+    return out, 0.0

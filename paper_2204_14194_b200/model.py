@@ -1,0 +1,90 @@
+"""Result types shared by every extrapolation entry point.
+
+``IterationTrace`` and ``SparseModel`` keep the reference's field names and
+semantics (``pkg/src/fase/reference.py:88-125``) so code written against the
+reference reads results the same way. ``BatchResult`` is the batched form
+returned by ``fase_extrapolate_batch``; it holds device tensors and converts
+to per-block ``(SparseModel, IterationTrace)`` pairs on request.
+
+The selection constants are the reference's (``reference.py:36,55``); the
+device kernels hard-code the same values (csrc/iterate.cu, csrc/capi.cu).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+DEGENERACY_RTOL = 1e-12
+SELECTION_TIE_RTOL = 1e-13
+
+
+@dataclass
+class IterationTrace:
+    """Per-iteration record: selected atom, raw projection, applied coefficient.
+
+    ``products`` holds the R vector after every iteration when recording was
+    requested (the fast path never materializes residual fields, so
+    ``residuals`` stays None, as in the reference's fast path).
+    """
+
+    selected: np.ndarray
+    projections: np.ndarray
+    coefficients: np.ndarray
+    residuals: list | None = None
+    products: list | None = None
+
+    def __len__(self) -> int:
+        return len(self.selected)
+
+
+@dataclass
+class SparseModel:
+    """g = sum of c * phi_k over the selected terms, in selection order."""
+
+    shape: tuple[int, int]
+    terms: list
+    dictionary: object
+
+    def materialize(self) -> np.ndarray:
+        """Evaluate g over the full area on the host (reference.py:120-125 order)."""
+        vals = self.dictionary.values
+        g = np.zeros(self.shape, dtype=np.complex128)
+        for k, c in self.terms:
+            g += c * vals[k]
+        return g
+
+
+@dataclass
+class BatchResult:
+    """Outcome of one batched run over B blocks (device tensors).
+
+    selected: (B, I) int32; projections, coefficients: (B, I) float64;
+    patched: (B, M, N) float64 areas with lost samples replaced, or None;
+    products: (B, I, K) float64 record of R when requested, else None.
+    """
+
+    selected: object
+    projections: object
+    coefficients: object
+    patched: object = None
+    products: object = None
+    dictionary: object = None
+    shape: tuple[int, int] | None = None
+
+    def __len__(self) -> int:
+        return int(self.selected.shape[0])
+
+    def block(self, b: int) -> tuple[SparseModel, IterationTrace]:
+        """Per-block reference-style (model, trace) pair (host copies)."""
+        sel = self.selected[b].cpu().numpy().astype(np.intp)
+        proj = self.projections[b].cpu().numpy().astype(np.complex128)
+        coef = self.coefficients[b].cpu().numpy().astype(np.complex128)
+        prods = None
+        if self.products is not None:
+            prods = [p.astype(np.complex128) for p in self.products[b].cpu().numpy()]
+        terms = [(int(k), complex(c)) for k, c in zip(sel, coef)]
+        model = SparseModel(shape=self.shape, terms=terms, dictionary=self.dictionary)
+        trace = IterationTrace(selected=sel, projections=proj, coefficients=coef, products=prods)
+        return model, trace

@@ -1,0 +1,204 @@
+"""Generate the golden fixtures under tests/golden/ FROM THE REFERENCE ITSELF.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the unmodified reference package from /root/reference/pkg/src and
+calls its public API (weights, dictionaries, Gram tables, fase_extrapolate,
+se_extrapolate, apply_model) on inputs produced by this repo's seeded
+generators (paper_2204_14194_b200.workloads), then stores inputs' seeds and the
+reference outputs as small .npz files. Nothing at test / bench time reads
+/root/reference: the GPU box only sees these fixtures.
+
+Custom BASELINE families (DCT u Hadamard-48, real DFT u sign, Gaussian) are
+handed to the reference as ``fase.Dictionary(values)`` -- the reference's own
+container for numerically defined atoms (dictionary.py:59-85).
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import fase  # noqa: E402  (the reference)
+
+from paper_2204_14194_b200 import workloads as wl  # noqa: E402
+from paper_2204_14194_b200.dictionary import parse_dict_spec  # noqa: E402
+
+
+def ref_dictionary(spec: str, m: int, n: int):
+    """Reference Dictionary for a spec; custom kinds via Dictionary(values)."""
+    try:
+        return fase.parse_dict_spec(spec, m, n)
+    except ValueError:
+        ours = parse_dict_spec(spec, m, n)
+        return fase.Dictionary(ours.real_values())
+
+
+def run_block(d, signal, mask, cfg, tables=None, record=False):
+    w = fase.build_weight_field(mask, cfg.rho_hat)
+    if tables is None:
+        tables = fase.build_gram_tables(d, w)
+    r0 = fase.initial_scalar_products(signal, w, d)
+    model, trace = fase.fase_extrapolate(signal, mask, d, tables, cfg, record_products=record)
+    patched, max_imag = fase.apply_model(signal, model, mask)
+    out = {
+        "r0": r0.real.copy(),
+        "selected": np.asarray(trace.selected, dtype=np.int64),
+        "projections": trace.projections.real.copy(),
+        "coefficients": trace.coefficients.real.copy(),
+        "patched_lost": patched[mask].copy(),
+        "max_imag": np.float64(max_imag),
+        "d": tables.d.copy(),
+    }
+    if record:
+        out["products"] = np.stack([p.real for p in trace.products])
+    return out, tables
+
+
+def small_cases():
+    cases = []
+    specs = [("dct", 8, 8, (4, 4)), ("wht", 8, 8, (4, 4)), ("union:dct+wht", 8, 8, (4, 4)),
+             ("union:dct+had", 12, 12, (4, 4)), ("dct", 16, 16, (8, 8)),
+             ("union:rdft+brdft", 8, 8, (2, 2)), ("had", 12, 12, (4, 6)), ("dct", 6, 10, (2, 4))]
+    out = {}
+    for i, (spec, m, n, loss) in enumerate(specs):
+        d = ref_dictionary(spec, m, n)
+        mask = wl.central_loss_mask(m, n, *loss)
+        cfg = fase.ExtrapConfig(iterations=40, gamma=[0.5, 1.0, 0.25][i % 3], rho_hat=0.8)
+        signal = np.random.default_rng([2204, i]).uniform(0.0, 255.0, (m, n))
+        res, tables = run_block(d, signal, mask, cfg, record=True)
+        _, se_trace = fase.se_extrapolate(signal, mask, d, cfg)
+        key = f"case{i}"
+        out[f"{key}_signal"] = signal
+        out[f"{key}_mask"] = mask
+        out[f"{key}_gram"] = tables.c.real.copy()
+        out[f"{key}_se_selected"] = np.asarray(se_trace.selected, dtype=np.int64)
+        out[f"{key}_se_coefficients"] = se_trace.coefficients.real.copy()
+        for k, v in res.items():
+            out[f"{key}_{k}"] = v
+        cases.append({"key": key, "spec": spec, "m": m, "n": n, "loss": list(loss),
+                      "iterations": cfg.iterations, "gamma": cfg.gamma, "rho_hat": cfg.rho_hat,
+                      "provenance": str(tables.provenance),
+                      "content_hash": str(d.content_hash())})
+    np.savez_compressed(HERE / "small_cases.npz", **out)
+    return cases
+
+
+def weights_and_hashes():
+    rec = {"weights": [], "hashes": []}
+    arrays = {}
+    for i, (m, n, rho, loss) in enumerate([(3, 3, 0.5, (1, 1)), (48, 48, 0.8, (16, 16)),
+                                           (64, 64, 0.85, (24, 24)), (32, 32, 0.8, (8, 8)),
+                                           (5, 7, 0.3, (1, 3))]):
+        mask = wl.central_loss_mask(m, n, *loss)
+        arrays[f"w{i}"] = fase.build_weight_field(mask, rho)
+        arrays[f"mask{i}"] = mask
+        rec["weights"].append({"key": f"w{i}", "rho": rho})
+    for spec, m, n in [("dct", 4, 4), ("wht", 8, 8), ("dft", 4, 4), ("bdft", 4, 4),
+                       ("union:dct+wht", 8, 8), ("dct", 48, 48), ("dft", 6, 5),
+                       ("union:dct+had", 48, 48), ("union:rdft+brdft", 32, 32),
+                       ("union:dct+had", 12, 12)]:
+        d = ref_dictionary(spec, m, n)
+        rec["hashes"].append({"spec": spec, "m": m, "n": n, "K": len(d),
+                              "content_hash": str(d.content_hash())})
+    g = wl.WORKLOADS[4].dictionary()
+    rec["hashes"].append({"spec": wl.WORKLOADS[4].dict_spec, "m": 64, "n": 64, "K": len(g),
+                          "content_hash": str(fase.Dictionary(g.real_values()).content_hash())})
+    np.savez_compressed(HERE / "weights.npz", **arrays)
+    return rec
+
+
+def shared_config_blocks(cid: int, blocks):
+    w = wl.WORKLOADS[cid]
+    m, n = w.area
+    d = ref_dictionary(w.dict_spec, m, n)
+    mask = wl.central_loss_mask(m, n, *w.loss)
+    cfg = fase.ExtrapConfig(w.config.iterations, w.config.gamma, w.config.rho_hat)
+    sig = wl.block_signals(cid, max(blocks) + 1, m, n)
+    tables = None
+    out = {"blocks": np.asarray(blocks)}
+    t0 = time.time()
+    for b in blocks:
+        res, tables = run_block(d, sig[b], mask, cfg, tables=tables)
+        for k, v in res.items():
+            if k == "d":
+                continue
+            out[f"b{b}_{k}"] = v
+    out["d"] = tables.d.copy()
+    out["gram_diag"] = tables.c.diagonal().real.copy()
+    out["provenance"] = np.uint64(tables.provenance)
+    np.savez_compressed(HERE / f"c{cid}_blocks.npz", **out)
+    return {"config": cid, "blocks": list(blocks), "seconds": time.time() - t0}
+
+
+def frame_config_blocks(cid: int, picks: int):
+    w = wl.WORKLOADS[cid]
+    case = wl.frame_case(w)
+    signals, masks = wl.frame_areas(case.damaged(), case.lost, case.corners, case.mb, case.support)
+    # cover the per-block geometries: most neighbour losses (interior), frame
+    # edges / corners (out-of-frame samples), both at once, and a plain block
+    h, wd = case.frame.shape
+    a = case.area
+    oof = np.empty(len(masks), dtype=np.int64)
+    for i, (r, c) in enumerate(case.corners):
+        rr = np.arange(r - case.support, r - case.support + a)
+        cc = np.arange(c - case.support, c - case.support + a)
+        inside = ((rr >= 0) & (rr < h))[:, None] & ((cc >= 0) & (cc < wd))[None, :]
+        oof[i] = a * a - inside.sum()
+    neigh = masks.reshape(len(masks), -1).sum(axis=1) - oof - case.mb * case.mb
+    interior = np.flatnonzero(oof == 0)
+    chosen = [0]
+    chosen += list(interior[np.argsort(-neigh[interior], kind="stable")[:2]])
+    both = np.flatnonzero((oof > 0) & (neigh > 0))
+    if both.size:
+        chosen.append(int(both[np.argmax(neigh[both])]))
+    chosen.append(int(np.argmax(oof)))
+    plain = np.flatnonzero((oof == 0) & (neigh == 0))
+    if plain.size:
+        chosen.append(int(plain[len(plain) // 2]))
+    chosen = sorted(set(int(x) for x in chosen))[:picks]
+    m, n = w.area
+    d = ref_dictionary(w.dict_spec, m, n)
+    cfg = fase.ExtrapConfig(w.config.iterations, w.config.gamma, w.config.rho_hat)
+    out = {"blocks": np.asarray(chosen, dtype=np.int64), "n_blocks": np.int64(len(masks)),
+           "lost_total": np.int64(case.lost.sum())}
+    t0 = time.time()
+    for b in chosen:
+        res, _ = run_block(d, signals[b], masks[b], cfg)
+        for k, v in res.items():
+            out[f"b{b}_{k}"] = v
+        out[f"b{b}_mask"] = masks[b]
+        out[f"b{b}_signal_sum"] = np.float64(signals[b].sum())
+    np.savez_compressed(HERE / f"c{cid}_blocks.npz", **out)
+    return {"config": cid, "blocks": [int(x) for x in chosen], "seconds": time.time() - t0}
+
+
+def main():
+    meta = {"generator": "tests/golden/make_golden.py",
+            "reference": "/root/reference/pkg (fase 0.1.0, unmodified)",
+            "numpy": np.__version__}
+    meta.update(weights_and_hashes())
+    meta["small_cases"] = small_cases()
+    meta["c0"] = shared_config_blocks(0, [0])
+    meta["c1"] = shared_config_blocks(1, [0, 1, 2, 3])
+    meta["c4"] = shared_config_blocks(4, [0, 1])
+    meta["c3"] = frame_config_blocks(3, 6)
+    meta["c2"] = frame_config_blocks(2, 4)
+    with open(HERE / "golden.json", "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print(json.dumps({k: v for k, v in meta.items() if k.startswith("c")}, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,312 @@
+"""GPU parity: libfase_b200 against the reference (golden fixtures) and the oracle.
+
+Two gates, as in SURVEY.md section 8(c):
+  1. stage-isolated -- the oracle's own tables / initial products are fed to the
+     CUDA recursion; selections, projections and coefficients must then be
+     BIT-IDENTICAL to the reference;
+  2. end to end -- GPU-built tables and products; selections identical up to a
+     legitimate near-tie (top-two Delta-E within 1e-9 relative), coefficients
+     and reconstructed samples within 1e-6 of the run scale.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import fase_oracle as orc  # noqa: E402
+from paper_2204_14194_b200 import (  # noqa: E402
+    ExtrapConfig,
+    GramTable,
+    NoSelectableAtomError,
+    StaleTableError,
+    UnsupportedDictionaryError,
+    build_gram_tables,
+    build_weight_field,
+    fase_extrapolate,
+    fase_extrapolate_batch,
+    generate_dictionary,
+    parse_dict_spec,
+    provenance_hash,
+)
+from paper_2204_14194_b200 import _native, workloads as wl  # noqa: E402
+from paper_2204_14194_b200.dictionary import Dictionary  # noqa: E402
+from parity import COEF_REL, compare_selection, metric_fn, rel_dev  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def meta(golden_dir):
+    with open(golden_dir / "golden.json") as fh:
+        return json.load(fh)
+
+
+def host_tables(dictionary, mask, rho):
+    """Oracle tables wrapped as a reference-style GramTable (host arrays)."""
+    vals = dictionary.real_values().astype(np.complex128)
+    w = orc.weight_field(mask, rho)
+    c, d = orc.gram(vals.reshape(len(vals), -1), w)
+    return GramTable(c=c, d=d, provenance=provenance_hash(dictionary, w)), (c, d)
+
+
+# ----------------------------------------------------------------- kernels
+
+
+@pytest.mark.parametrize("spec,m,n", [("dct", 48, 48), ("union:dct+had", 48, 48),
+                                      ("union:dct+wht", 8, 8), ("had", 12, 20)])
+def test_basis_outer_bit_exact(spec, m, n):
+    d = parse_dict_spec(spec, m, n)
+    phi = d.device_matrix(DEV)[:, : m * n].cpu().numpy()
+    assert np.array_equal(phi, d.real_values().reshape(len(d), -1))
+
+
+@pytest.mark.parametrize("spec,m,n,loss", [("dct", 48, 48, (16, 16)),
+                                           ("union:dct+had", 48, 48, (16, 16)),
+                                           ("dct", 5, 7, (1, 3)), ("union:rdft+brdft", 32, 32, (8, 8))])
+def test_gram_and_normalizers(spec, m, n, loss):
+    d = parse_dict_spec(spec, m, n)
+    mask = wl.central_loss_mask(m, n, *loss)
+    w = build_weight_field(mask, 0.8)
+    t = build_gram_tables(d, w, device=DEV)
+    G = t._G[:, : len(d)].cpu().numpy()
+    assert np.array_equal(G, G.T)  # exact mirror
+    c, dd = orc.gram(d.real_values().reshape(len(d), -1).astype(np.complex128), w)
+    assert rel_dev(G, c.real) < 1e-14
+    alive = dd != 0
+    assert np.array_equal(t.d != 0, alive)
+    assert np.abs(t.d[alive] / dd[alive] - 1).max() < 1e-14
+    assert t.provenance == orc.provenance(orc.content_hash(d.values), w)
+
+
+def test_initial_products_batched():
+    w8 = wl.WORKLOADS[1]
+    d = w8.dictionary()
+    mask = wl.central_loss_mask(48, 48, 16, 16)
+    w = build_weight_field(mask, 0.8)
+    sig = wl.block_signals(1, 37, 48, 48)
+    F = torch.from_numpy(sig.reshape(37, -1)).to(DEV)
+    R0 = torch.empty((37, len(d)), dtype=torch.float64, device=DEV)
+    wd = torch.from_numpy(w.ravel()).to(DEV)
+    _native.init_products(d.device_matrix(DEV), F, wd, len(d), 2304, R0)
+    got = R0.cpu().numpy()
+    phi = d.real_values().reshape(len(d), -1).astype(np.complex128)
+    for b in (0, 17, 36):
+        want = orc.initial_products(sig[b], w, phi).real
+        assert rel_dev(got[b], want) < 1e-13
+
+
+# ----------------------------------------------------------------- stage-isolated
+
+
+def test_recursion_bit_exact_small(golden_dir, meta):
+    z = np.load(golden_dir / "small_cases.npz")
+    from test_oracle_golden import oracle_values
+
+    for case in meta["small_cases"]:
+        k = case["key"]
+        vals = oracle_values(case["spec"], case["m"], case["n"])
+        d = Dictionary(vals.real) if case["spec"] not in ("dct", "wht") else \
+            parse_dict_spec(case["spec"], case["m"], case["n"])
+        mask = z[f"{k}_mask"]
+        cfg = ExtrapConfig(case["iterations"], case["gamma"], case["rho_hat"])
+        w = orc.weight_field(mask, cfg.rho_hat)
+        tables = GramTable(c=z[f"{k}_gram"], d=z[f"{k}_d"], provenance=provenance_hash(d, w))
+        model, trace = fase_extrapolate(z[f"{k}_signal"], mask, d, tables, cfg,
+                                        products=z[f"{k}_r0"], record_products=True, device=DEV)
+        assert np.array_equal(trace.selected, z[f"{k}_selected"]), k
+        assert np.array_equal(trace.coefficients.real, z[f"{k}_coefficients"]), k
+        assert np.array_equal(trace.projections.real, z[f"{k}_projections"]), k
+        assert np.array_equal(np.stack([p.real for p in trace.products]), z[f"{k}_products"]), k
+
+
+@pytest.mark.parametrize("cid", [0, 1])
+def test_recursion_bit_exact_configs(golden_dir, cid):
+    """Reference tables + reference R0 -> the CUDA recursion reproduces the
+    reference's selections / coefficients / projections bit-for-bit."""
+    z = np.load(golden_dir / f"c{cid}_blocks.npz")
+    w8 = wl.WORKLOADS[cid]
+    d = w8.dictionary()
+    mask = wl.central_loss_mask(*w8.area, *w8.loss)
+    tables, _ = host_tables(d, mask, w8.config.rho_hat)
+    assert np.array_equal(tables.d, z["d"])
+    blocks = list(z["blocks"])
+    sig = wl.block_signals(cid, max(blocks) + 1, *w8.area)[blocks]
+    r0 = np.stack([z[f"b{b}_r0"] for b in blocks])
+    res = fase_extrapolate_batch(sig, mask, d, tables, w8.config, products=r0, device=DEV)
+    for i, b in enumerate(blocks):
+        assert np.array_equal(res.selected[i].cpu().numpy(), z[f"b{b}_selected"])
+        assert np.array_equal(res.coefficients[i].cpu().numpy(), z[f"b{b}_coefficients"])
+        assert np.array_equal(res.projections[i].cpu().numpy(), z[f"b{b}_projections"])
+        # synthesis is also bit-exact given the same terms
+        lost = res.patched[i].cpu().numpy()[mask]
+        assert np.array_equal(lost, z[f"b{b}_patched_lost"])
+
+
+# ----------------------------------------------------------------- end to end
+
+
+def _end_to_end(cid, golden_dir, tol_blocks_early=None):
+    z = np.load(golden_dir / f"c{cid}_blocks.npz")
+    w8 = wl.WORKLOADS[cid]
+    d = w8.dictionary()
+    mask = wl.central_loss_mask(*w8.area, *w8.loss)
+    blocks = list(z["blocks"])
+    sig = wl.block_signals(cid, max(blocks) + 1, *w8.area)[blocks]
+    res = fase_extrapolate_batch(sig, mask, d, None, w8.config, device=DEV)
+    vals = d.real_values()
+    tables = None
+    verdicts = []
+    for i, b in enumerate(blocks):
+        got_sel = res.selected[i].cpu().numpy()
+        want_sel = z[f"b{b}_selected"]
+
+        def metric_at(t, b=b, i=i):
+            nonlocal tables
+            if tables is None:
+                tables = orc.gram(vals.reshape(len(vals), -1).astype(np.complex128),
+                                  orc.weight_field(mask, w8.config.rho_hat))
+            _, _, _, log = orc.fase_run(z[f"b{b}_r0"], tables[0], tables[1], w8.config.gamma,
+                                        t, record=True)
+            return metric_fn(z[f"b{b}_r0"], tables[1], log)(t)
+
+        v = compare_selection(got_sel, want_sel, metric_at)
+        assert v.ok, f"block {b}: diverged at {v.stop} with Delta-E gap {v.gap}"
+        s = v.stop
+        assert rel_dev(res.coefficients[i].cpu().numpy()[:s], z[f"b{b}_coefficients"][:s]) < COEF_REL
+        if v.exact:
+            lost = res.patched[i].cpu().numpy()[mask]
+            assert rel_dev(lost, z[f"b{b}_patched_lost"]) < COEF_REL
+        verdicts.append(v)
+    return verdicts
+
+
+@pytest.mark.parametrize("cid", [0, 1, 4])
+def test_end_to_end_configs(golden_dir, cid):
+    _end_to_end(cid, golden_dir)
+
+
+def test_frame_blocks_config3(golden_dir):
+    """All 25,920 blocks of the config-3 frame in one batch (chunked per-block
+    tables); the reference's per-block results pin the sampled blocks."""
+    z = np.load(golden_dir / "c3_blocks.npz")
+    w8 = wl.WORKLOADS[3]
+    case = wl.frame_case(w8)
+    signals, masks = wl.frame_areas(case.damaged(), case.lost, case.corners, case.mb, case.support)
+    d = w8.dictionary()
+    res = fase_extrapolate_batch(signals, masks, d, None, w8.config, device=DEV)
+    vals = d.real_values().reshape(len(d), -1).astype(np.complex128)
+    exact = 0
+    for b in z["blocks"]:
+        got = res.selected[b].cpu().numpy()
+        want = z[f"b{b}_selected"]
+
+        def metric_at(t, b=b):
+            tab = orc.gram(vals, orc.weight_field(masks[b], w8.config.rho_hat))
+            r0 = orc.initial_products(signals[b], orc.weight_field(masks[b], w8.config.rho_hat), vals)
+            _, _, _, log = orc.fase_run(r0, tab[0], tab[1], w8.config.gamma, t, record=True)
+            return metric_fn(r0, tab[1], log)(t)
+
+        v = compare_selection(got, want, metric_at)
+        assert v.ok, f"block {b}: diverged at {v.stop}, gap {v.gap}"
+        s = v.stop
+        assert rel_dev(res.coefficients[b].cpu().numpy()[:s], z[f"b{b}_coefficients"][:s]) < COEF_REL
+        if v.exact:
+            exact += 1
+            lost = res.patched[b].cpu().numpy()[masks[b]]
+            assert rel_dev(lost, z[f"b{b}_patched_lost"]) < COEF_REL
+    assert exact >= len(z["blocks"]) - 1
+
+
+# ----------------------------------------------------------------- properties / edges
+
+
+def test_full_config1_properties():
+    """1,024 blocks: deterministic, support untouched, selections valid."""
+    w8 = wl.WORKLOADS[1]
+    d = w8.dictionary()
+    mask = wl.central_loss_mask(48, 48, 16, 16)
+    sig = wl.block_signals(1, 1024, 48, 48)
+    t = build_gram_tables(d, build_weight_field(mask, 0.8), device=DEV)
+    a = fase_extrapolate_batch(sig, mask, d, t, w8.config, device=DEV)
+    b = fase_extrapolate_batch(torch.from_numpy(sig).to(DEV), mask, d, t, w8.config, device=DEV)
+    assert torch.equal(a.selected, b.selected) and torch.equal(a.coefficients, b.coefficients)
+    sel = a.selected.cpu().numpy()
+    assert sel.min() >= 0 and sel.max() < len(d)
+    patched = a.patched.cpu().numpy()
+    assert np.array_equal(patched[:, ~mask], sig[:, ~mask])
+    assert np.isfinite(patched).all()
+
+
+def test_zero_signal_selects_first_atom():
+    # pkg/tests/test_reference.py:186-191: zero signal -> atom 0, coefficient 0
+    d = generate_dictionary("dct", 8, 8)
+    mask = wl.central_loss_mask(8, 8, 4, 4)
+    t = build_gram_tables(d, build_weight_field(mask, 0.8), device=DEV)
+    _, trace = fase_extrapolate(np.zeros((8, 8)), mask, d, t, ExtrapConfig(5), device=DEV)
+    assert (trace.selected == 0).all() and (trace.coefficients == 0).all()
+
+
+def test_single_atom_recovery():
+    # signal = atom 9, gamma = 1, one iteration -> term (9, 1.0) (SPEC fase-core example)
+    d = generate_dictionary("dct", 8, 8)
+    mask = np.zeros((8, 8), bool)
+    mask[3:5, 3:5] = True
+    sig = d.real_values()[9].copy()
+    t = build_gram_tables(d, build_weight_field(mask, 0.8), device=DEV)
+    _, trace = fase_extrapolate(sig, mask, d, t, ExtrapConfig(1, 1.0, 0.8), device=DEV)
+    assert trace.selected[0] == 9
+    assert abs(trace.coefficients[0] - 1.0) < 1e-13
+
+
+def test_degenerate_atoms_never_selected_and_all_dead_raises():
+    mask = wl.central_loss_mask(4, 4, 2, 2)
+    inside = np.zeros((4, 4))
+    inside[1:3, 1:3] = 1.0
+    base = generate_dictionary("dct", 4, 4).real_values()
+    d = Dictionary(np.concatenate([inside[None], base]))
+    t = build_gram_tables(d, build_weight_field(mask, 0.8), device=DEV)
+    assert t.d[0] == 0.0
+    _, trace = fase_extrapolate(np.random.default_rng(12).standard_normal((4, 4)), mask, d, t,
+                                ExtrapConfig(10), device=DEV)
+    assert (trace.selected != 0).all()
+    dead = Dictionary(inside[None])
+    td = build_gram_tables(dead, build_weight_field(mask, 0.8), device=DEV)
+    with pytest.raises(NoSelectableAtomError):
+        fase_extrapolate(np.ones((4, 4)), mask, dead, td, device=DEV)
+
+
+def test_stale_tables_detected():
+    d = generate_dictionary("dct", 4, 4)
+    mask = wl.central_loss_mask(4, 4, 2, 2)
+    other = build_gram_tables(generate_dictionary("wht", 4, 4), build_weight_field(mask, 0.8),
+                              device=DEV)
+    with pytest.raises(StaleTableError):
+        fase_extrapolate(np.ones((4, 4)), mask, d, other, device=DEV)
+    rho = build_gram_tables(d, build_weight_field(mask, 0.5), device=DEV)
+    with pytest.raises(StaleTableError):
+        fase_extrapolate(np.ones((4, 4)), mask, d, rho, device=DEV)
+
+
+def test_complex_dictionary_rejected():
+    d = generate_dictionary("dft", 4, 4)
+    with pytest.raises(UnsupportedDictionaryError):
+        fase_extrapolate_batch(np.ones((1, 4, 4)), wl.central_loss_mask(4, 4, 2, 2), d, None,
+                               device=DEV)
+
+
+def test_empty_batch_and_odd_area():
+    d = generate_dictionary("dct", 5, 7)  # K = 35, odd area
+    mask = wl.central_loss_mask(5, 7, 1, 3)
+    res = fase_extrapolate_batch(np.zeros((0, 5, 7)), mask, d, None, ExtrapConfig(3), device=DEV)
+    assert res.selected.shape == (0, 3)
+    sig = np.random.default_rng(3).uniform(0, 255, (3, 5, 7))
+    res = fase_extrapolate_batch(sig, mask, d, None, ExtrapConfig(12), device=DEV)
+    vals = d.real_values().astype(np.complex128)
+    for b in range(3):
+        ref = orc.extrapolate_block(sig[b], mask, vals, 0.5, 12, 0.8)
+        assert np.array_equal(res.selected[b].cpu().numpy(), ref["selected"])
+        assert rel_dev(res.coefficients[b].cpu().numpy(), ref["coefficients"].real) < 1e-12

@@ -1,0 +1,119 @@
+"""Pin the CPU oracle against fixtures produced by the reference itself.
+
+tests/golden/*.npz were written by tests/golden/make_golden.py calling the
+unmodified reference package. The oracle (oracle/fase_oracle.py) must
+reproduce them bit-for-bit; only then is it trusted as the GPU checker.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from oracle import fase_oracle as orc
+from paper_2204_14194_b200 import workloads as wl
+from paper_2204_14194_b200.dictionary import parse_dict_spec
+
+
+@pytest.fixture(scope="module")
+def meta(golden_dir):
+    with open(golden_dir / "golden.json") as fh:
+        return json.load(fh)
+
+
+def oracle_values(spec, m, n):
+    """Oracle dictionary: reference families restated; custom ones from the shared generator."""
+    if spec in ("dct", "wht", "dft", "bdft"):
+        return orc.family(spec, m, n)
+    if spec.startswith("union:") and all(p in ("dct", "wht", "dft", "bdft")
+                                         for p in spec[6:].split("+")):
+        return np.concatenate([orc.family(p, m, n) for p in spec[6:].split("+")])
+    return parse_dict_spec(spec, m, n).real_values().astype(np.complex128)
+
+
+def test_weight_fields_bit_exact(golden_dir, meta):
+    z = np.load(golden_dir / "weights.npz")
+    for rec in meta["weights"]:
+        k = rec["key"]
+        mask = z["mask" + k[1:]]
+        assert np.array_equal(orc.weight_field(mask, rec["rho"]), z[k])
+
+
+def test_weight_known_answer():
+    # pkg/tests/test_grid.py:18-26: w[0,0] of a 3x3 area at rho 0.5 is 0.5**sqrt(2)
+    w = orc.weight_field(np.zeros((3, 3), bool), 0.5)
+    assert w[1, 1] == 1.0
+    assert w[0, 0] == 0.5 ** np.sqrt(2)
+    assert w[0, 0] == pytest.approx(0.3752142272464817, abs=1e-15)
+    assert w[0, 0] == w[0, 2] == w[2, 0] == w[2, 2]
+
+
+def test_content_hashes(meta):
+    for rec in meta["hashes"]:
+        if rec["spec"].startswith("gauss"):
+            continue  # 256 MB; covered by test_host's package-side hash check
+        vals = oracle_values(rec["spec"], rec["m"], rec["n"])
+        assert len(vals) == rec["K"]
+        assert orc.content_hash(vals) == int(rec["content_hash"]), rec["spec"]
+
+
+def test_small_cases(golden_dir, meta):
+    z = np.load(golden_dir / "small_cases.npz")
+    for case in meta["small_cases"]:
+        k = case["key"]
+        vals = oracle_values(case["spec"], case["m"], case["n"])
+        phi = vals.reshape(len(vals), -1)
+        sig, mask = z[f"{k}_signal"], z[f"{k}_mask"]
+        w = orc.weight_field(mask, case["rho_hat"])
+        assert orc.provenance(orc.content_hash(vals), w) == int(case["provenance"])
+        c, d = orc.gram(phi, w)
+        assert np.array_equal(c.real, z[f"{k}_gram"]), k
+        assert np.array_equal(d, z[f"{k}_d"]), k
+        res = orc.extrapolate_block(sig, mask, vals, case["gamma"], case["iterations"],
+                                    case["rho_hat"], tables=(c, d), record=True)
+        assert np.array_equal(res["r0"].real, z[f"{k}_r0"]), k
+        assert np.array_equal(res["selected"], z[f"{k}_selected"]), k
+        assert np.array_equal(res["coefficients"].real, z[f"{k}_coefficients"]), k
+        assert np.array_equal(res["projections"].real, z[f"{k}_projections"]), k
+        assert np.array_equal(np.stack([p.real for p in res["log"]]), z[f"{k}_products"]), k
+        assert np.array_equal(res["patched"][mask], z[f"{k}_patched_lost"]), k
+        se_sel, _, se_coef = orc.se_run(sig, mask, phi, case["gamma"], case["iterations"],
+                                        case["rho_hat"])
+        assert np.array_equal(se_sel, z[f"{k}_se_selected"]), k
+        assert np.array_equal(se_coef.real, z[f"{k}_se_coefficients"]), k
+
+
+@pytest.mark.parametrize("cid", [0, 1])
+def test_shared_config_blocks(golden_dir, cid):
+    z = np.load(golden_dir / f"c{cid}_blocks.npz")
+    w = wl.WORKLOADS[cid]
+    m, n = w.area
+    vals = oracle_values(w.dict_spec, m, n)
+    mask = orc.central_mask(m, n, *w.loss)
+    tables = orc.gram(vals.reshape(len(vals), -1), orc.weight_field(mask, w.config.rho_hat))
+    assert np.array_equal(tables[1], z["d"])
+    sig = wl.block_signals(cid, int(z["blocks"].max()) + 1, m, n)
+    for b in z["blocks"]:
+        res = orc.extrapolate_block(sig[b], mask, vals, w.config.gamma, w.config.iterations,
+                                    w.config.rho_hat, tables=tables)
+        assert np.array_equal(res["r0"].real, z[f"b{b}_r0"])
+        assert np.array_equal(res["selected"], z[f"b{b}_selected"])
+        assert np.array_equal(res["coefficients"].real, z[f"b{b}_coefficients"])
+        assert np.array_equal(res["patched"][mask], z[f"b{b}_patched_lost"])
+
+
+def test_frame_config3_blocks(golden_dir):
+    z = np.load(golden_dir / "c3_blocks.npz")
+    w = wl.WORKLOADS[3]
+    case = wl.frame_case(w)
+    signals, masks = wl.frame_areas(case.damaged(), case.lost, case.corners, case.mb, case.support)
+    assert len(masks) == int(z["n_blocks"]) == 25920
+    vals = oracle_values(w.dict_spec, *w.area)
+    for b in z["blocks"][:3]:
+        assert np.array_equal(masks[b], z[f"b{b}_mask"])
+        assert signals[b].sum() == z[f"b{b}_signal_sum"]
+        res = orc.extrapolate_block(signals[b], masks[b], vals, w.config.gamma,
+                                    w.config.iterations, w.config.rho_hat)
+        assert np.array_equal(res["selected"], z[f"b{b}_selected"])
+        assert np.array_equal(res["coefficients"].real, z[f"b{b}_coefficients"])
+        assert np.array_equal(res["patched"][masks[b]], z[f"b{b}_patched_lost"])
