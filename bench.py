@@ -55,7 +55,7 @@ REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x40: "sw_thermal_slowdown",
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 4])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -178,10 +178,18 @@ class ClockSampler:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", self.gpu_id,
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return self
+        # the timed region starts only once the sampler is producing lines
+        t0 = time.time()
+        while time.time() - t0 < 5.0 and self.proc.poll() is None:
+            if self.path.stat().st_size > 0:
+                break
+            time.sleep(0.02)
+        self.skip = len(self.path.read_text().splitlines())  # idle samples before the region
         return self
 
     def __exit__(self, *exc):
@@ -197,7 +205,7 @@ class ClockSampler:
         if self.proc is None or not self.path.exists():
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm, smax, reasons = [], None, set()
-        for line in self.path.read_text().splitlines():
+        for line in self.path.read_text().splitlines()[getattr(self, "skip", 0):]:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 3:
                 continue
@@ -260,15 +268,22 @@ def run_gpu(args):
     K, M, I, B = len(d), w.area[0] * w.area[1], w.config.iterations, w.n_blocks
     mask = wl.central_loss_mask(*w.area, *w.loss)
     d.device_matrix(dev)
+    tables = build_gram_tables(d, build_weight_field(mask, w.config.rho_hat), device=dev)
+    plan = ExtrapolationPlan(d, mask, B, w.config, tables, device=dev)
+    # one more table build, kernels only, for the reported Gram time
+    G2 = torch.zeros_like(plan.G)
+    D2 = torch.empty_like(plan.D)
     torch.cuda.synchronize()
     g0 = torch.cuda.Event(enable_timing=True)
     g1 = torch.cuda.Event(enable_timing=True)
     g0.record()
-    tables = build_gram_tables(d, build_weight_field(mask, w.config.rho_hat), device=dev)
+    _native.gram(plan.phi, plan.W, K, M, G2)
+    _native.gram_finish(G2, K, D2)
     g1.record()
     torch.cuda.synchronize()
     gram_ms = g0.elapsed_time(g1)
-    plan = ExtrapolationPlan(d, mask, B, w.config, tables, device=dev)
+    assert torch.equal(G2, plan.G) and torch.equal(D2, plan.D), "Gram build is not deterministic"
+    del G2, D2
 
     host = torch.from_numpy(wl.block_signals(args.config, B, *w.area, first=rank * B)).pin_memory()
     dev_sig = host.to(dev)
@@ -376,6 +391,7 @@ def run_gpu(args):
             "stage_ms": {"init_products": float(np.mean(init_ms)), "iterate": float(np.mean(iter_ms)),
                          "synth": float(np.mean(synth_ms))},
             "gram_ms": gram_ms,
+            "gram_tflops": K * (K + 1) * M / (gram_ms * 1e-3) / 1e12,
             "gpu_launches": args.steps * (3 + 1) + args.steps * (plan.launches_per_run + 1),
             "clocks": clocks.summary(),
             "wall_s": t_wall,

@@ -59,6 +59,10 @@ FASE_API int fase_abi_version(void);
 /* Largest dictionary size K the iteration kernel accepts. */
 FASE_API int fase_max_atoms(void);
 
+/* Leading dimension (>= K, even) that table rows handed to fase_iterate must
+ * have, zero-padded past K; 0 if K is unsupported. */
+FASE_API int fase_table_ld(int K);
+
 /*
  * Basis construction (replaces the separable branch of generate_dictionary,
  * dictionary.py:167-178, np.einsum("um,vn->uvmn")):
@@ -115,7 +119,8 @@ FASE_API int fase_block_normalizers(const double* G0, int64_t ldg, const double*
  *   p = R_u * (D_u * D_u);  c = gamma * p;  R_k <- R_k - c * row_u[k]
  * row_u = G0[u, :] - sum_{j in chunks(b)} C_j[u, :]   (chunk list empty when
  * chunk_ptr == NULL: shared geometry). One persistent CTA per block keeps R and
- * D in registers; rows are streamed with 16-byte loads.
+ * D in registers; rows are streamed with 16-byte loads. G0 / C_j rows must be
+ * zero-padded to ldg >= fase_table_ld(K).
  *   R0, R_out: B x ldr (R_out may be NULL or alias R0)
  *   D: shared vector (ldd == 0) or B x ldd
  *   sel / proj / coef: B x ldo outputs (I entries per block)

@@ -29,7 +29,8 @@ _STATUS = {
 }
 
 EXPORTS = (
-    "fase_last_error", "fase_abi_version", "fase_max_atoms", "fase_basis_outer", "fase_gram",
+    "fase_last_error", "fase_abi_version", "fase_max_atoms", "fase_table_ld", "fase_basis_outer",
+    "fase_gram",
     "fase_gram_finish", "fase_init_products", "fase_block_normalizers", "fase_iterate",
     "fase_synth_paste", "fase_l2_flush",
 )
@@ -73,6 +74,8 @@ def load():
     lib.fase_last_error.argtypes = []
     lib.fase_abi_version.restype = _i32
     lib.fase_max_atoms.restype = _i32
+    lib.fase_table_ld.restype = _i32
+    lib.fase_table_ld.argtypes = [_i32]
     sigs = {
         "fase_basis_outer": [_vp, _i32, _i32, _vp, _i32, _i32, _vp, _i64, _i64, _vp],
         "fase_gram": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp],
@@ -239,3 +242,12 @@ def l2_flush(buf) -> None:
 
 def max_atoms() -> int:
     return int(load().fase_max_atoms())
+
+
+def table_ld(K: int) -> int:
+    """Row stride (zero-padded) the recursion kernel needs for a K-atom table."""
+    ld = int(load().fase_table_ld(K))
+    if ld <= 0:
+        raise errors.UnsupportedDictionaryError(f"K={K} exceeds the iteration kernel's "
+                                                f"{max_atoms()} atoms")
+    return ld

@@ -17,13 +17,23 @@
 // j < EPT/2, so one table row is streamed with coalesced 16-byte loads (a
 // warp reads 512 contiguous bytes per j). R and D stay in registers for the
 // whole run; nothing but the table rows comes from memory inside the loop.
+// Table rows are padded with zeros to the variant's capacity NT*EPT
+// (fase_table_ld), so row loads carry no bounds predicates.
 //
-// Reductions: metric values are non-negative doubles, so their IEEE bit
-// patterns order like int64; a dead atom is the key -1. The block max is two
-// 32-bit redux.sync steps per warp plus one shared-memory exchange; the tie
-// pass is a 32-bit redux.sync min over candidate indices, executed only by
-// warps whose own max reaches the threshold (warp-uniform skip). Two
-// __syncthreads per iteration.
+// Reductions: each thread tracks the exact max of its metrics (and the lowest
+// index attaining it) during the update pass. Non-negative doubles order like
+// their int64 bit patterns, so the warp max is three 32-bit redux.sync steps
+// (high word, low word, lowest index) and one shared-memory exchange gives
+// the block max. The tie pass is a 32-bit redux.sync min over candidate
+// indices, run only by warps whose own max reaches the threshold (warp-uniform
+// skip). Two __syncthreads per iteration.
+//
+// Row staging: after the first barrier the block knows the exact max and the
+// lowest index attaining it. That index is the selection unless a tie within
+// the quantum resolves lower (structural twins, rare), so one thread issues a
+// TMA 1-D bulk copy (cp.async.bulk + mbarrier) of that row into shared memory
+// while the tie pass and the second barrier run; no registers are held for it.
+// A mispredicted row is loaded directly from global memory.
 //
 // Per-block geometries: row_u = G0[u,:] - sum_{j in chunks(b)} C_j[u,:]
 // (chunk tables of sample classes that are lost in some blocks and not in
@@ -39,37 +49,48 @@ namespace {
 
 constexpr unsigned kNone = 0xffffffffu;
 
-__device__ __forceinline__ long long metric_key(double r, double d) {
-  return d != 0.0 ? __double_as_longlong(mul_rn(fabs(r), d)) : -1LL;
-}
-
-template <int NT, int EPT, int MINB>
+// Dead atoms (D == 0, and the padding past K) carry d = -inf in registers:
+// their metric |R| * d is -inf (NaN when R == 0), which never wins a '>'
+// comparison and never reaches a finite threshold.
+template <int NT, int EPT, int MINB, bool kChunked, bool kRecord>
 __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_iterate_args a) {
   constexpr int EP = EPT / 2;
   constexpr int NW = NT / 32;
-  __shared__ long long s_max[NW];
+  constexpr unsigned kRowBytes = NT * EPT * sizeof(double);
+  __shared__ long long s_key[NW];
+  __shared__ unsigned s_arg[NW];
   __shared__ unsigned s_u[NW];
   __shared__ double s_r[NW];
   __shared__ double s_d[NW];
+  __shared__ __align__(16) double s_dump[NW][2][EPT];  // tie-pass winner's registers
+  __shared__ __align__(8) uint64_t s_bar;
+  extern __shared__ double2 s_row[];  // staged row: pair p at s_row[p]
 
   const int b = blockIdx.x;
   const int t = threadIdx.x;
   const int lane = t & 31;
   const int warp = t >> 5;
   const int K = a.K;
+  const double kDead = __longlong_as_double(static_cast<long long>(0xfff0000000000000ULL));
+
+  if (t == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+  }
 
   const double* D = a.D + (a.ldd ? static_cast<int64_t>(b) * a.ldd : 0);
   const double* R0 = a.R0 + static_cast<int64_t>(b) * a.ldr;
   const int32_t* cids = nullptr;
   int nch = 0;
-  if (a.chunk_ptr) {
+  if (kChunked) {
     const int lo = a.chunk_ptr[b];
     nch = a.chunk_ptr[b + 1] - lo;
     cids = a.chunk_ids + lo;
   }
 
   double r[EP][2], d[EP][2];
-  long long lmax = -1;
+  double best = kDead;
+  unsigned barg = kNone;
 #pragma unroll
   for (int j = 0; j < EP; ++j) {
     const int k = 2 * (j * NT + t);
@@ -77,63 +98,97 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
     for (int e = 0; e < 2; ++e) {
       const bool in = k + e < K;
       r[j][e] = in ? R0[k + e] : 0.0;
-      d[j][e] = in ? D[k + e] : 0.0;
-      lmax = max(lmax, metric_key(r[j][e], d[j][e]));
+      const double dk = in ? D[k + e] : 0.0;
+      d[j][e] = dk != 0.0 ? dk : kDead;
+      const double m = mul_rn(fabs(r[j][e]), d[j][e]);
+      if (m > best) {
+        best = m;
+        barg = static_cast<unsigned>(k + e);
+      }
     }
   }
 
   int32_t* sel = a.sel + static_cast<int64_t>(b) * a.ldo;
   double* proj = a.proj + static_cast<int64_t>(b) * a.ldo;
   double* coef = a.coef + static_cast<int64_t>(b) * a.ldo;
+  const int64_t ldg = a.ldg;
   double q = 0.0;
 
   for (int it = 0; it < a.I; ++it) {
-    // ---- block max of the metric keys
-    const long long wmax = warp_max_i64(lmax);
-    if (lane == 0) s_max[warp] = wmax;
+    // ---- exact warp max and the lowest index attaining it
+    {
+      const long long key = __double_as_longlong(best);
+      const int kh = static_cast<int>(key >> 32);
+      const unsigned kl = static_cast<unsigned>(key);
+      const int wh = __reduce_max_sync(0xffffffffu, kh);
+      const unsigned wl = __reduce_max_sync(0xffffffffu, kh == wh ? kl : 0u);
+      const unsigned wa = __reduce_min_sync(0xffffffffu, (kh == wh && kl == wl) ? barg : kNone);
+      if (lane == 0) {
+        s_key[warp] = (static_cast<long long>(wh) << 32) | wl;
+        s_arg[warp] = wa;
+      }
+    }
     __syncthreads();
-    long long top_key = s_max[0];
-#pragma unroll
-    for (int w = 1; w < NW; ++w) top_key = max(top_key, s_max[w]);
+    // ---- block max: every warp reduces the NW slots in parallel (lane l reads slot l)
+    long long top_key;
+    unsigned guess;
+    long long wkey;
+    {
+      const long long sk = lane < NW ? s_key[lane] : LLONG_MIN;
+      const unsigned sa = lane < NW ? s_arg[lane] : kNone;
+      wkey = s_key[warp];
+      const int h = static_cast<int>(sk >> 32);
+      const unsigned l = static_cast<unsigned>(sk);
+      const int bh = __reduce_max_sync(0xffffffffu, h);
+      const unsigned bl = __reduce_max_sync(0xffffffffu, h == bh ? l : 0u);
+      guess = __reduce_min_sync(0xffffffffu, (h == bh && l == bl) ? sa : kNone);
+      top_key = (static_cast<long long>(bh) << 32) | bl;
+    }
+    // stage the likely selection's row in shared memory (one TMA bulk copy)
+    // while the tie pass and the second barrier run
+    if (t == 0) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&s_bar, kRowBytes);
+      tma_load_1d(s_row, a.G0 + static_cast<int64_t>(guess) * ldg, kRowBytes, &s_bar);
+    }
     const double top = __longlong_as_double(top_key);
     // tie_quantum: only a finite, strictly positive top moves the ratchet
     if (top_key > 0 && top_key < 0x7ff0000000000000LL) q = fmax(q, mul_rn(1e-13, top));
     const double thr = q > 0.0 ? sub_rn(top, q) : top;
 
-    // ---- lowest index reaching the threshold
+    // ---- lowest index reaching the threshold (only warps whose max reaches it)
     unsigned cand = kNone;
-    double cr = 0.0, cd = 0.0;
-    if (wmax >= 0 && __longlong_as_double(wmax) >= thr) {
+    if (wkey >= 0 && __longlong_as_double(wkey) >= thr) {  // warp-uniform
 #pragma unroll
-      for (int j = 0; j < EP; ++j) {
+      for (int j = EP - 1; j >= 0; --j)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          if (cand == kNone && d[j][e] != 0.0 && mul_rn(fabs(r[j][e]), d[j][e]) >= thr) {
-            cand = static_cast<unsigned>(2 * (j * NT + t) + e);
-            cr = r[j][e];
-            cd = d[j][e];
-          }
-        }
-      }
+        for (int e = 1; e >= 0; --e)
+          if (mul_rn(fabs(r[j][e]), d[j][e]) >= thr) cand = 2 * (j * NT + t) + e;
     }
     const unsigned wmin = __reduce_min_sync(0xffffffffu, cand);
     if (wmin == kNone) {
       if (lane == 0) s_u[warp] = kNone;
     } else if (cand == wmin) {
+      // fetch R and D of the winner through a shared scratch (no dynamic
+      // register indexing)
+#pragma unroll
+      for (int j = 0; j < EP; ++j) {
+        *reinterpret_cast<double2*>(&s_dump[warp][0][2 * j]) = make_double2(r[j][0], r[j][1]);
+        *reinterpret_cast<double2*>(&s_dump[warp][1][2 * j]) = make_double2(d[j][0], d[j][1]);
+      }
+      const int jj = (static_cast<int>(cand >> 1) - t) / NT;
+      const int ee = static_cast<int>(cand & 1u);
       s_u[warp] = cand;
-      s_r[warp] = cr;
-      s_d[warp] = cd;
+      s_r[warp] = s_dump[warp][0][2 * jj + ee];
+      s_d[warp] = s_dump[warp][1][2 * jj + ee];
     }
     __syncthreads();
-    unsigned u = s_u[0];
-    int uw = 0;
-#pragma unroll
-    for (int w = 1; w < NW; ++w) {
-      const unsigned v = s_u[w];
-      if (v < u) {
-        u = v;
-        uw = w;
-      }
+    unsigned u;
+    int uw;
+    {
+      const unsigned su = lane < NW ? s_u[lane] : kNone;
+      u = __reduce_min_sync(0xffffffffu, su);
+      uw = __ffs(__ballot_sync(0xffffffffu, su == u)) - 1;
     }
     const double ru = s_r[uw];
     const double du = s_d[uw];
@@ -145,43 +200,53 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
       coef[it] = c;
     }
 
-    // ---- stream row u (minus chunk rows) and apply the rank-1 update
-    const double* row = a.G0 + static_cast<int64_t>(u) * a.ldg;
     double g[EP][2];
-#pragma unroll
-    for (int j = 0; j < EP; ++j) {
-      const int k = 2 * (j * NT + t);
-      if (k < K) {
-        const double2 v = ldg2(row + k);
-        g[j][0] = v.x;
-        g[j][1] = v.y;
-      } else {
-        g[j][0] = g[j][1] = 0.0;
-      }
-    }
-    for (int ch = 0; ch < nch; ++ch) {
-      const double* crow = a.chunk_tables + static_cast<int64_t>(cids[ch]) * a.chunk_stride +
-                           static_cast<int64_t>(u) * a.ldg;
+    if (u == guess) {  // block-uniform
+      mbar_wait(&s_bar, it & 1);
 #pragma unroll
       for (int j = 0; j < EP; ++j) {
-        const int k = 2 * (j * NT + t);
-        if (k < K) {
-          const double2 v = ldg2(crow + k);
+        const double2 v = s_row[j * NT + t];
+        g[j][0] = v.x;
+        g[j][1] = v.y;
+      }
+    } else {  // the tie rule picked a lower twin: fetch its row directly
+      const double* row = a.G0 + static_cast<int64_t>(u) * ldg + 2 * t;
+#pragma unroll
+      for (int j = 0; j < EP; ++j) {
+        const double2 v = ldg2(row + 2 * j * NT);
+        g[j][0] = v.x;
+        g[j][1] = v.y;
+      }
+      mbar_wait(&s_bar, it & 1);  // retire the staged copy before the next one
+    }
+    if (kChunked) {
+      for (int ch = 0; ch < nch; ++ch) {
+        const double* crow = a.chunk_tables + static_cast<int64_t>(cids[ch]) * a.chunk_stride +
+                             static_cast<int64_t>(u) * ldg + 2 * t;
+#pragma unroll
+        for (int j = 0; j < EP; ++j) {
+          const double2 v = ldg2(crow + 2 * j * NT);
           g[j][0] = sub_rn(g[j][0], v.x);
           g[j][1] = sub_rn(g[j][1], v.y);
         }
       }
     }
-    lmax = -1;
+    // ---- rank-1 update fused with the next iteration's running max
+    best = kDead;
+    barg = kNone;
 #pragma unroll
     for (int j = 0; j < EP; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         r[j][e] = sub_rn(r[j][e], mul_rn(c, g[j][e]));
-        lmax = max(lmax, metric_key(r[j][e], d[j][e]));
+        const double m = mul_rn(fabs(r[j][e]), d[j][e]);
+        if (m > best) {
+          best = m;
+          barg = static_cast<unsigned>(2 * (j * NT + t) + e);
+        }
       }
     }
-    if (a.R_log) {
+    if (kRecord) {
       double* dst = a.R_log + (static_cast<int64_t>(b) * a.I + it) * a.ldr;
 #pragma unroll
       for (int j = 0; j < EP; ++j) {
@@ -208,16 +273,22 @@ using KernelFn = void (*)(const fase_iterate_args);
 struct Variant {
   int nt;
   int ept;
-  KernelFn fn;
+  KernelFn plain;    // shared geometry
+  KernelFn chunked;  // per-block geometry (chunk-corrected rows)
+  KernelFn record;   // shared geometry, R logged after every iteration
 };
 
-#define FASE_V(NT, EPT, MINB) {NT, EPT, fase_iterate_kernel<NT, EPT, MINB>}
+#define FASE_V(NT, EPT, MINB)                                                \
+  {NT, EPT, fase_iterate_kernel<NT, EPT, MINB, false, false>,                 \
+   fase_iterate_kernel<NT, EPT, MINB, true, false>,                           \
+   fase_iterate_kernel<NT, EPT, MINB, false, true>}
 // Ordered by capacity NT*EPT; the first variant that holds K is used. R and D
 // live in registers (4 registers per owned atom), which caps K at 512 x 24.
 const Variant kVariants[] = {
     FASE_V(128, 2, 4),   FASE_V(128, 4, 4),   FASE_V(128, 6, 4),   FASE_V(128, 8, 4),
     FASE_V(256, 6, 3),   FASE_V(256, 8, 3),   FASE_V(256, 10, 3),  FASE_V(256, 12, 2),
-    FASE_V(256, 14, 2),  FASE_V(256, 16, 2),  FASE_V(256, 18, 2),  FASE_V(256, 20, 2),
+    FASE_V(256, 14, 2),  FASE_V(256, 16, 2),  FASE_V(256, 18, 2),
+    FASE_V(256, 20, 2),
     FASE_V(512, 12, 1),  FASE_V(512, 14, 1),  FASE_V(512, 16, 1),  FASE_V(512, 18, 1),
     FASE_V(512, 20, 1),  FASE_V(512, 24, 1),
 };
@@ -237,6 +308,12 @@ using namespace fase;
 extern "C" int fase_max_atoms(void) {
   const Variant& last = kVariants[sizeof(kVariants) / sizeof(kVariants[0]) - 1];
   return last.nt * last.ept;
+}
+
+extern "C" int fase_table_ld(int K) {
+  if (K < 1) return 0;
+  const Variant* v = pick_variant(K);
+  return v ? v->nt * v->ept : 0;
 }
 
 extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
@@ -264,12 +341,31 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
     set_error("fase_iterate: chunk tables given without ids / aligned storage");
     return FASE_ERR_SHAPE;
   }
+  if (a.chunk_ptr && a.R_log) {
+    set_error("fase_iterate: R_log recording is not available with chunked tables");
+    return FASE_ERR_UNSUPPORTED;
+  }
   const Variant* v = pick_variant(a.K);
   if (!v) {
     set_error("fase_iterate: K=%d exceeds the largest kernel variant (%d atoms)", a.K,
               fase_max_atoms());
     return FASE_ERR_UNSUPPORTED;
   }
-  v->fn<<<a.B, v->nt, 0, as_stream(stream)>>>(a);
+  if (a.ldg < v->nt * v->ept || (a.chunk_ptr && a.chunk_stride < a.ldg * a.K)) {
+    set_error("fase_iterate: table rows must be zero-padded to fase_table_ld(K)=%d (ldg=%lld)",
+              v->nt * v->ept, static_cast<long long>(a.ldg));
+    return FASE_ERR_SHAPE;
+  }
+  KernelFn fn = a.chunk_ptr ? v->chunked : (a.R_log ? v->record : v->plain);
+  const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+    if (e != cudaSuccess) {
+      set_error("fase_iterate: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+      return FASE_ERR_CUDA;
+    }
+  }
+  fn<<<a.B, v->nt, smem, as_stream(stream)>>>(a);
   return check_launch("fase_iterate");
 }

@@ -163,7 +163,7 @@ class GramTable:
                         "complex-valued tables are not supported by the FP64 GPU path")
                 c = c.real
             k = self._k
-            G = torch.zeros((k, _round_up(k, 2)), dtype=torch.float64, device=device)
+            G = torch.zeros((k, _native.table_ld(k)), dtype=torch.float64, device=device)
             G[:, :k].copy_(torch.from_numpy(np.ascontiguousarray(c, dtype=np.float64)))
             D = torch.from_numpy(self._host_d.copy()).to(device)
             self._uploaded[key] = (G, D)
@@ -179,7 +179,7 @@ def _device_vector(x: np.ndarray, length: int, device):
 
 def _gram_on_device(phi, w_dev, K: int, M: int, device):
     torch = _torch()
-    G = torch.zeros((K, _round_up(K, 2)), dtype=torch.float64, device=device)
+    G = torch.zeros((K, _native.table_ld(K)), dtype=torch.float64, device=device)
     _native.gram(phi, w_dev, K, M, G)
     return G
 
