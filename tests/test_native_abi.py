@@ -1,0 +1,94 @@
+"""The C-ABI library loads without a GPU and exports every declared entry point.
+
+No compute is launched here: only host-side entry points (version / capacity
+queries) and argument validation paths that return before touching CUDA.
+"""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2204_14194_b200 import _build, _native, errors
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "fase_b200.h"
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _build.build()
+    return _native.load()
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"FASE_API\s+[\w\s\*]*?\b(fase_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_abi():
+    names = declared_symbols()
+    assert "fase_iterate" in names and "fase_gram" in names and "fase_synth_paste" in names
+    assert set(names) == set(_native.EXPORTS)
+
+
+def test_every_declared_symbol_is_exported(lib):
+    raw = ctypes.CDLL(str(_native.library_path()))
+    for name in declared_symbols():
+        assert hasattr(raw, name), name
+
+
+def test_host_queries(lib):
+    assert lib.fase_abi_version() == (1 << 16)
+    assert lib.fase_max_atoms() >= 8192
+    # rows padded to the kernel variant's capacity, never shorter than K, even
+    for k in (1, 35, 2048, 2304, 4608, 8192):
+        ld = _native.table_ld(k)
+        assert ld >= k and ld % 2 == 0
+    assert _native.table_ld(4608) == 4608 and _native.table_ld(8192) == 8192
+    assert _native.table_ld(2048) == 2048
+    with pytest.raises(errors.UnsupportedDictionaryError):
+        _native.table_ld(lib.fase_max_atoms() + 1)
+
+
+def test_status_codes_and_messages(lib):
+    # argument errors are reported before any CUDA call
+    assert lib.fase_iterate(None, None) == -2
+    assert b"null argument" in lib.fase_last_error()
+    assert lib.fase_gram(None, 0, None, 0, 0, None, 0, None) == -1
+    assert lib.fase_init_products(None, 0, None, 0, None, 0, 4, 4, -1, None, 0, None) == -1
+    assert lib.fase_synth_paste(None, 0, None, None, 0, 0, 1, None, None, 0, None, None, 0,
+                                None) == -1
+    args = _native.IterateArgs(K=4, B=1, I=1, gamma=2.0)
+    assert lib.fase_iterate(ctypes.byref(args), None) == -2
+    assert b"gamma" in lib.fase_last_error()
+    # empty batches are a no-op, not an error
+    args = _native.IterateArgs(K=4, B=0, I=1, gamma=0.5)
+    assert lib.fase_iterate(ctypes.byref(args), None) == 0
+
+
+def test_status_maps_to_reference_exceptions(lib):
+    assert _native._STATUS[-1] is errors.ShapeError
+    assert _native._STATUS[-2] is errors.ParameterError
+    assert _native._STATUS[-6] is errors.NoSelectableAtomError
+    assert _native._STATUS[-7] is errors.StaleTableError
+    assert all(issubclass(c, ValueError) for c in _native._STATUS.values())
+    lib.fase_iterate(None, None)
+    with pytest.raises(errors.ParameterError):
+        _native._check(-2)
+
+
+def test_iterate_args_layout_matches_header():
+    # the ctypes mirror must have the header's field order
+    text = HEADER.read_text()
+    body = text[text.index("typedef struct {"):text.index("} fase_iterate_args;")]
+    fields = re.findall(r"\b(\w+);", body)
+    assert fields == [f for f, _ in _native.IterateArgs._fields_]
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    monkeypatch.setattr(_native, "_lib", None)
+    monkeypatch.setenv("FASE_B200_LIB", str(tmp_path / "nope.so"))
+    with pytest.raises(errors.NativeLibraryError):
+        _native.load()
