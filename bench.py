@@ -277,7 +277,8 @@ def run_gpu(args):
     g0 = torch.cuda.Event(enable_timing=True)
     g1 = torch.cuda.Event(enable_timing=True)
     g0.record()
-    _native.gram(plan.phi, plan.W, K, M, G2)
+    gws = torch.empty(K * plan.phi.shape[1] + 2, dtype=torch.float64, device=dev)
+    _native.gram(plan.phi, plan.W, K, M, G2, ws=gws)
     _native.gram_finish(G2, K, D2)
     g1.record()
     torch.cuda.synchronize()
@@ -304,7 +305,7 @@ def run_gpu(args):
             e[0].record(stream)
             if split:
                 plan.F[:, :M].copy_(dev_sig.reshape(B, -1), non_blocking=True)
-                _native.init_products(plan.phi, plan.F, plan.W, K, M, plan.R0)
+                _native.init_products(plan.phi, plan.F, plan.W, K, M, plan.R0, ws=plan.ws)
                 e[1].record(stream)
                 _native.iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, plan.selected,
                                 plan.projections, plan.coefficients)

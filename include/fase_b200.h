@@ -75,12 +75,20 @@ FASE_API int fase_basis_outer(const double* rows, int Lr, int Mr, const double* 
 /*
  * Weighted Gram table (replaces build_gram_tables, fast.py:109-142):
  *   G[k*ldg + l] = sum_m (phi[k,m] * w[m]) * phi[l,m]      for k, l < K, m < M
- * FP64 DMMA tiles; only the upper triangle is computed and mirrored exactly,
- * so G is bit-symmetric. `w` is a length-M vector (ldw == 0) or a K x M matrix
- * is NOT accepted here (tables are per weight).
+ * Phi o w is formed in `ws` (fase_gram_workspace(K, M) bytes, 16-byte aligned),
+ * then FP64 DMMA tiles compute the upper triangle and mirror it exactly, so G
+ * is bit-symmetric.
  */
+FASE_API size_t fase_gram_workspace(int K, int M);
 FASE_API int fase_gram(const double* phi, int64_t ldphi, const double* w, int K, int M,
-              double* G, int64_t ldg, void* stream);
+                       double* G, int64_t ldg, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * Plain FP64 contraction C[i*ldc + j] = sum_k A[i*lda + k] * B[j*ldb + k]
+ * (the DMMA tile kernel behind fase_gram / fase_init_products).
+ */
+FASE_API int fase_gemm_nt(const double* A, int64_t lda, const double* B, int64_t ldb, int M,
+                          int N, int Kd, double* C, int64_t ldc, void* stream);
 
 /*
  * Normalizers (replaces _finish_tables, fast.py:97-106):
@@ -94,11 +102,14 @@ FASE_API int fase_gram_finish(const double* G, int64_t ldg, int K, double* D, in
  * Batched initial scalar products (replaces initial_scalar_products,
  * fast.py:145-157, one zgemv per block):
  *   R0[b*ldr + k] = sum_m (f[b*ldf + m] * w[b*ldw + m]) * phi[k*ldphi + m]
- * ldw == 0 shares one weight vector across the batch.
+ * ldw == 0 shares one weight vector across the batch. F o W is formed in `ws`
+ * (fase_init_products_workspace(M, B) bytes), then one DMMA GEMM.
  */
+FASE_API size_t fase_init_products_workspace(int M, int B);
 FASE_API int fase_init_products(const double* phi, int64_t ldphi, const double* f, int64_t ldf,
-                       const double* w, int64_t ldw, int K, int M, int B,
-                       double* R0, int64_t ldr, void* stream);
+                                const double* w, int64_t ldw, int K, int M, int B,
+                                double* R0, int64_t ldr, void* ws, size_t ws_bytes,
+                                void* stream);
 
 /*
  * Per-block normalizers for per-block geometries whose table rows are

@@ -30,7 +30,7 @@ _STATUS = {
 
 EXPORTS = (
     "fase_last_error", "fase_abi_version", "fase_max_atoms", "fase_table_ld", "fase_basis_outer",
-    "fase_gram",
+    "fase_gram", "fase_gram_workspace", "fase_gemm_nt", "fase_init_products_workspace",
     "fase_gram_finish", "fase_init_products", "fase_block_normalizers", "fase_iterate",
     "fase_synth_paste", "fase_l2_flush",
 )
@@ -76,11 +76,17 @@ def load():
     lib.fase_max_atoms.restype = _i32
     lib.fase_table_ld.restype = _i32
     lib.fase_table_ld.argtypes = [_i32]
+    lib.fase_gram_workspace.restype = ctypes.c_size_t
+    lib.fase_gram_workspace.argtypes = [_i32, _i32]
+    lib.fase_init_products_workspace.restype = ctypes.c_size_t
+    lib.fase_init_products_workspace.argtypes = [_i32, _i32]
     sigs = {
         "fase_basis_outer": [_vp, _i32, _i32, _vp, _i32, _i32, _vp, _i64, _i64, _vp],
-        "fase_gram": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp],
+        "fase_gram": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp, ctypes.c_size_t, _vp],
+        "fase_gemm_nt": [_vp, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp],
         "fase_gram_finish": [_vp, _i64, _i32, _vp, _vp, _vp],
-        "fase_init_products": [_vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp],
+        "fase_init_products": [_vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp,
+                               ctypes.c_size_t, _vp],
         "fase_block_normalizers": [_vp, _i64, _vp, _i64, _vp, _vp, _i32, _i32, _vp, _i64, _vp,
                                    _vp],
         "fase_iterate": [ctypes.POINTER(IterateArgs), _vp],
@@ -152,14 +158,41 @@ def basis_outer(rows, cols, phi, row0: int) -> None:
                                 row0, _stream(phi)))
 
 
-def gram(phi, w, K: int, M: int, G) -> None:
+def _workspace(nbytes: int, device, ws=None):
+    """A 16-byte-aligned device scratch of at least ``nbytes`` (reused when given)."""
+    import torch
+
+    if ws is not None and ws.numel() * ws.element_size() >= nbytes:
+        return ws
+    return torch.empty(max(nbytes // 8, 2), dtype=torch.float64, device=device)
+
+
+def gram(phi, w, K: int, M: int, G, ws=None) -> None:
     import torch
 
     lib = load()
     _require(phi, "phi", torch.float64, 2)
     _require(w, "w", torch.float64, 1)
     _require(G, "G", torch.float64, 2)
-    _check(lib.fase_gram(_ptr(phi), _ld(phi), _ptr(w), K, M, _ptr(G), _ld(G), _stream(G)))
+    need = int(lib.fase_gram_workspace(K, M))
+    ws = _workspace(need, G.device, ws)
+    _check(lib.fase_gram(_ptr(phi), _ld(phi), _ptr(w), K, M, _ptr(G), _ld(G), _ptr(ws),
+                         ws.numel() * 8, _stream(G)))
+
+
+def init_products_workspace(M: int, B: int) -> int:
+    return int(load().fase_init_products_workspace(M, B))
+
+
+def gemm_nt(A, B, C) -> None:
+    """C = A @ B.T in FP64 (all 2-D, contiguous rows)."""
+    import torch
+
+    lib = load()
+    for t, n in ((A, "A"), (B, "B"), (C, "C")):
+        _require(t, n, torch.float64, 2)
+    _check(lib.fase_gemm_nt(_ptr(A), _ld(A), _ptr(B), _ld(B), A.shape[0], B.shape[0], A.shape[1],
+                            _ptr(C), _ld(C), _stream(C)))
 
 
 def gram_finish(G, K: int, D, n_alive=None) -> None:
@@ -171,7 +204,7 @@ def gram_finish(G, K: int, D, n_alive=None) -> None:
     _check(lib.fase_gram_finish(_ptr(G), _ld(G), K, _ptr(D), _ptr(n_alive), _stream(G)))
 
 
-def init_products(phi, f, w, K: int, M: int, R0) -> None:
+def init_products(phi, f, w, K: int, M: int, R0, ws=None) -> None:
     """R0[b] = (f[b] o w[b or shared]) @ phi.T ; f, R0 2-D; w 1-D (shared) or 2-D."""
     import torch
 
@@ -181,8 +214,10 @@ def init_products(phi, f, w, K: int, M: int, R0) -> None:
     _require(w, "w", torch.float64)
     _require(R0, "R0", torch.float64, 2)
     ldw = _ld(w) if w.dim() == 2 else 0
-    _check(lib.fase_init_products(_ptr(phi), _ld(phi), _ptr(f), _ld(f), _ptr(w), ldw, K, M,
-                                  f.shape[0], _ptr(R0), _ld(R0), _stream(R0)))
+    B = f.shape[0]
+    ws = _workspace(int(lib.fase_init_products_workspace(M, B)), R0.device, ws)
+    _check(lib.fase_init_products(_ptr(phi), _ld(phi), _ptr(f), _ld(f), _ptr(w), ldw, K, M, B,
+                                  _ptr(R0), _ld(R0), _ptr(ws), ws.numel() * 8, _stream(R0)))
 
 
 def block_normalizers(G0, chunk_tables, chunk_stride: int, chunk_ptr, chunk_ids, K: int,

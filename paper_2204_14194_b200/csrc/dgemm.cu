@@ -1,23 +1,25 @@
 // FP64 tensor-core (DMMA) contractions of the FaSE correlation stage.
 //
-//   C[i, j] = sum_k (A[i, k] * W[i, k]) * B[j, k]        ("NT": both operands
-//                                                          contraction-contiguous)
+//   C[i, j] = sum_k A[i, k] * B[j, k]        ("NT": both operands contraction-contiguous)
 //
 // Used for the weighted Gram table G = (Phi o w) Phi^T (build_gram_tables,
 // reference fast.py:109-142) and the batched initial products
 // R0 = (F o W) Phi^T (initial_scalar_products, fast.py:145-157, one zgemv per
-// block in the reference). The weight is applied in the producer: the scaled
-// operand is formed in shared memory, one correctly rounded multiply per
-// sample, the same rounding structure as the reference's `conj(phi)*w` /
-// `s*w` before its BLAS call.
+// block in the reference). The weighted operand is formed first by a streaming
+// kernel (one correctly rounded multiply per sample, the rounding structure of
+// the reference's `conj(phi)*w` / `s*w` before its BLAS call); folding the
+// multiply into the GEMM's shared-memory stage was measured 23% slower
+// (0.88 vs 0.72 ms on the config-1 shape) because it adds a barrier and a
+// shared-memory round trip per k-tile.
 //
 // Why DMMA and not tcgen05: tcgen05.mma has no f64 kind on sm_100a
 // (SURVEY.md section 0, item 7); FP64 on Blackwell's tensor cores is the
 // warp-level `mma.sync ... .f64` path, which ptxas lowers to DMMA.8x8x4.
+// Measured DMMA issue peak on the B200: 37 TFLOP/s (tools/probes/dmma_probe.cu).
 //
 // Tiling: 128 x 128 CTA tile, BK = 16, 3-stage cp.async ring, 8 warps as
 // 2 (M) x 4 (N), warp tile 64 x 32 = 8 x 4 DMMA 8x8 accumulators (64 FP64
-// registers). Shared rows are padded to 20 doubles: the 8x4 A/B fragment a
+// registers). Shared rows are padded to 20 doubles: the 8x4 fragment a
 // half-warp reads then hits 16 distinct 8-byte bank pairs.
 // Symmetric mode (Gram) computes tiles with bm <= bn only and writes each
 // accumulator to (i, j) and (j, i): the table is bit-symmetric.
@@ -37,8 +39,6 @@ constexpr int NTHREADS = 256;
 struct GemmParams {
   const double* A;
   int64_t lda;
-  const double* W;  // nullptr: no scaling; ldw == 0: one weight row for all i
-  int64_t ldw;
   const double* B;
   int64_t ldb;
   double* C;
@@ -54,12 +54,11 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
-template <bool kSym, bool kScale>
+template <bool kSym>
 __global__ void __launch_bounds__(NTHREADS, 1) dgemm_nt_kernel(const GemmParams p) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = As + STAGES * BM * LDS;
-  double* Ws = Bs + STAGES * BN * LDS;
 
   const int bm = blockIdx.y;
   const int bn = blockIdx.x;
@@ -88,10 +87,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) dgemm_nt_kernel(const GemmParams 
         const int nb = gr < p.m_rows ? kb : 0;
         const double* src = nb ? p.A + static_cast<int64_t>(gr) * p.lda + k : p.A;
         cp_async16(As + (stage * BM + r) * LDS + kc, src, nb);
-        if (kScale) {
-          const double* ws = nb ? p.W + static_cast<int64_t>(gr) * p.ldw + k : p.W;
-          cp_async16(Ws + (stage * BM + r) * LDS + kc, ws, nb);
-        }
       }
       {
         const int gr = col0 + r;
@@ -118,23 +113,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) dgemm_nt_kernel(const GemmParams 
   const int fc = lane & 3;
   for (int kt = 0; kt < ktiles; ++kt) {
     cp_async_wait<STAGES - 2>();
-    const int st = kt % STAGES;
-    if (kScale) {
-      // each thread scales exactly the chunks it copied itself
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int idx = tid + i * NTHREADS;
-        const int r = idx >> 3;
-        const int kc = (idx & 7) * 2;
-        double2* av = reinterpret_cast<double2*>(As + (st * BM + r) * LDS + kc);
-        const double2 wv = *reinterpret_cast<const double2*>(Ws + (st * BM + r) * LDS + kc);
-        double2 x = *av;
-        x.x = mul_rn(x.x, wv.x);
-        x.y = mul_rn(x.y, wv.y);
-        *av = x;
-      }
-    }
     __syncthreads();
+    const int st = kt % STAGES;
     const int nk = kt + STAGES - 1;
     if (nk < ktiles) load_stage(nk % STAGES, nk);
     cp_async_commit();
@@ -187,11 +167,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) dgemm_nt_kernel(const GemmParams 
   }
 }
 
-template <bool kSym, bool kScale>
+// out[b*ldo + m] = x[b*ldx + m] * w[b*ldw + m]  (ldw == 0: one shared weight row);
+// one correctly rounded multiply per sample, 16-byte accesses.
+__global__ void weigh_kernel(const double* __restrict__ x, int64_t ldx, const double* __restrict__ w,
+                             int64_t ldw, int rows, int M, double* __restrict__ out, int64_t ldo) {
+  const int pairs = (M + 1) / 2;
+  const int64_t total = static_cast<int64_t>(rows) * pairs;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int b = static_cast<int>(i / pairs);
+    const int m = 2 * static_cast<int>(i - static_cast<int64_t>(b) * pairs);
+    const double2 xv = *reinterpret_cast<const double2*>(x + b * ldx + m);
+    const double2 wv = *reinterpret_cast<const double2*>(w + b * ldw + m);
+    double2 o;
+    o.x = mul_rn(xv.x, wv.x);
+    o.y = m + 1 < M ? mul_rn(xv.y, wv.y) : 0.0;
+    *reinterpret_cast<double2*>(out + b * ldo + m) = o;
+  }
+}
+
+template <bool kSym>
 int launch(const GemmParams& p, cudaStream_t stream, const char* what) {
-  const size_t smem = sizeof(double) * STAGES * LDS * (BM + BN + (kScale ? BM : 0));
+  const size_t smem = sizeof(double) * STAGES * LDS * (BM + BN);
   // per-device attribute; cheap enough to set on every launch
-  cudaError_t e = cudaFuncSetAttribute(dgemm_nt_kernel<kSym, kScale>,
+  cudaError_t e = cudaFuncSetAttribute(dgemm_nt_kernel<kSym>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) {
@@ -199,7 +198,17 @@ int launch(const GemmParams& p, cudaStream_t stream, const char* what) {
     return FASE_ERR_CUDA;
   }
   dim3 grid((p.n_rows + BN - 1) / BN, (p.m_rows + BM - 1) / BM);
-  dgemm_nt_kernel<kSym, kScale><<<grid, NTHREADS, smem, stream>>>(p);
+  dgemm_nt_kernel<kSym><<<grid, NTHREADS, smem, stream>>>(p);
+  return check_launch(what);
+}
+
+int launch_weigh(const double* x, int64_t ldx, const double* w, int64_t ldw, int rows, int M,
+                 double* out, int64_t ldo, cudaStream_t stream, const char* what) {
+  const int64_t total = static_cast<int64_t>(rows) * ((M + 1) / 2);
+  const int threads = 256;
+  const int64_t blocks = (total + threads - 1) / threads;
+  weigh_kernel<<<static_cast<unsigned>(blocks < 148 * 16 ? blocks : 148 * 16), threads, 0,
+                 stream>>>(x, ldx, w, ldw, rows, M, out, ldo);
   return check_launch(what);
 }
 
@@ -210,8 +219,16 @@ bool operand_ok(const double* ptr, int64_t ld) { return ptr && aligned16(ptr) &&
 
 using namespace fase;
 
+extern "C" size_t fase_gram_workspace(int K, int M) {
+  return K < 1 || M < 1 ? 0 : sizeof(double) * static_cast<size_t>(K) * ((M + 1) / 2 * 2);
+}
+
+extern "C" size_t fase_init_products_workspace(int M, int B) {
+  return M < 1 || B < 1 ? 0 : sizeof(double) * static_cast<size_t>(B) * ((M + 1) / 2 * 2);
+}
+
 extern "C" int fase_gram(const double* phi, int64_t ldphi, const double* w, int K, int M, double* G,
-                         int64_t ldg, void* stream) {
+                         int64_t ldg, void* ws, size_t ws_bytes, void* stream) {
   if (K < 1 || M < 1) {
     set_error("fase_gram: K and M must be positive (K=%d, M=%d)", K, M);
     return FASE_ERR_SHAPE;
@@ -220,13 +237,22 @@ extern "C" int fase_gram(const double* phi, int64_t ldphi, const double* w, int 
     set_error("fase_gram: bad operand (null, misaligned, odd or short leading dimension)");
     return FASE_ERR_SHAPE;
   }
-  GemmParams p{phi, ldphi, w, 0, phi, ldphi, G, ldg, K, K, M};
-  return launch<true, true>(p, as_stream(stream), "fase_gram");
+  if (!ws || !aligned16(ws) || ws_bytes < fase_gram_workspace(K, M)) {
+    set_error("fase_gram: workspace must hold fase_gram_workspace(K, M) bytes");
+    return FASE_ERR_SHAPE;
+  }
+  double* pw = static_cast<double*>(ws);
+  const int64_t ldw = (M + 1) / 2 * 2;
+  const cudaStream_t s = as_stream(stream);
+  int st = launch_weigh(phi, ldphi, w, 0, K, M, pw, ldw, s, "fase_gram (weigh)");
+  if (st != FASE_OK) return st;
+  GemmParams p{pw, ldw, phi, ldphi, G, ldg, K, K, M};
+  return launch<true>(p, s, "fase_gram");
 }
 
 extern "C" int fase_init_products(const double* phi, int64_t ldphi, const double* f, int64_t ldf,
                                   const double* w, int64_t ldw, int K, int M, int B, double* R0,
-                                  int64_t ldr, void* stream) {
+                                  int64_t ldr, void* ws, size_t ws_bytes, void* stream) {
   if (K < 1 || M < 1 || B < 0) {
     set_error("fase_init_products: bad sizes (K=%d, M=%d, B=%d)", K, M, B);
     return FASE_ERR_SHAPE;
@@ -237,6 +263,30 @@ extern "C" int fase_init_products(const double* phi, int64_t ldphi, const double
     set_error("fase_init_products: bad operand (null, misaligned, odd or short leading dimension)");
     return FASE_ERR_SHAPE;
   }
-  GemmParams p{f, ldf, w, ldw, phi, ldphi, R0, ldr, B, K, M};
-  return launch<false, true>(p, as_stream(stream), "fase_init_products");
+  if (!ws || !aligned16(ws) || ws_bytes < fase_init_products_workspace(M, B)) {
+    set_error("fase_init_products: workspace must hold fase_init_products_workspace(M, B) bytes");
+    return FASE_ERR_SHAPE;
+  }
+  double* fw = static_cast<double*>(ws);
+  const int64_t ldfw = (M + 1) / 2 * 2;
+  const cudaStream_t s = as_stream(stream);
+  int st = launch_weigh(f, ldf, w, ldw, B, M, fw, ldfw, s, "fase_init_products (weigh)");
+  if (st != FASE_OK) return st;
+  GemmParams p{fw, ldfw, phi, ldphi, R0, ldr, B, K, M};
+  return launch<false>(p, s, "fase_init_products");
+}
+
+extern "C" int fase_gemm_nt(const double* A, int64_t lda, const double* B, int64_t ldb, int M,
+                            int N, int Kd, double* C, int64_t ldc, void* stream) {
+  if (M < 0 || N < 0 || Kd < 1) {
+    set_error("fase_gemm_nt: bad sizes (M=%d, N=%d, K=%d)", M, N, Kd);
+    return FASE_ERR_SHAPE;
+  }
+  if (M == 0 || N == 0) return FASE_OK;
+  if (!operand_ok(A, lda) || !operand_ok(B, ldb) || lda < Kd || ldb < Kd || !C || ldc < N) {
+    set_error("fase_gemm_nt: bad operand (null, misaligned, odd or short leading dimension)");
+    return FASE_ERR_SHAPE;
+  }
+  GemmParams p{A, lda, B, ldb, C, ldc, M, N, Kd};
+  return launch<false>(p, as_stream(stream), "fase_gemm_nt");
 }

@@ -516,6 +516,8 @@ class ExtrapolationPlan:
         ldf = M if M % 2 == 0 else dictionary.ld
         self.F = torch.zeros((self.B, ldf), dtype=torch.float64, device=dev)
         self.R0 = torch.empty((self.B, _round_up(K, 2)), dtype=torch.float64, device=dev)
+        self.ws = torch.empty(max(_native.init_products_workspace(M, self.B) // 8, 2),
+                              dtype=torch.float64, device=dev)
         self.selected = torch.empty((self.B, I), dtype=torch.int32, device=dev)
         self.projections = torch.empty((self.B, I), dtype=torch.float64, device=dev)
         self.coefficients = torch.empty((self.B, I), dtype=torch.float64, device=dev)
@@ -533,7 +535,7 @@ class ExtrapolationPlan:
         if signals is not None:
             src = signals.reshape(self.B, -1)
             self.F[:, : self.M].copy_(src, non_blocking=True)
-        _native.init_products(self.phi, self.F, self.W, self.K, self.M, self.R0)
+        _native.init_products(self.phi, self.F, self.W, self.K, self.M, self.R0, ws=self.ws)
         _native.iterate(self.G, self.D, self.R0, self.K, self.I, self.config.gamma, self.selected,
                         self.projections, self.coefficients)
         if self.n_lost:

@@ -42,6 +42,8 @@ def test_every_declared_symbol_is_exported(lib):
 def test_host_queries(lib):
     assert lib.fase_abi_version() == (1 << 16)
     assert lib.fase_max_atoms() >= 8192
+    assert lib.fase_gram_workspace(4608, 2304) == 8 * 4608 * 2304
+    assert lib.fase_init_products_workspace(35, 3) == 8 * 3 * 36
     # rows padded to the kernel variant's capacity, never shorter than K, even
     for k in (1, 35, 2048, 2304, 4608, 8192):
         ld = _native.table_ld(k)
@@ -56,8 +58,9 @@ def test_status_codes_and_messages(lib):
     # argument errors are reported before any CUDA call
     assert lib.fase_iterate(None, None) == -2
     assert b"null argument" in lib.fase_last_error()
-    assert lib.fase_gram(None, 0, None, 0, 0, None, 0, None) == -1
-    assert lib.fase_init_products(None, 0, None, 0, None, 0, 4, 4, -1, None, 0, None) == -1
+    assert lib.fase_gram(None, 0, None, 0, 0, None, 0, None, 0, None) == -1
+    assert lib.fase_init_products(None, 0, None, 0, None, 0, 4, 4, -1, None, 0, None, 0,
+                                  None) == -1
     assert lib.fase_synth_paste(None, 0, None, None, 0, 0, 1, None, None, 0, None, None, 0,
                                 None) == -1
     args = _native.IterateArgs(K=4, B=1, I=1, gamma=2.0)
