@@ -16,7 +16,8 @@
 // Layout: thread t owns the element pairs k = 2*(j*NT + t) + {0,1},
 // j < EPT/2, so one table row is streamed with coalesced 16-byte loads (a
 // warp reads 512 contiguous bytes per j). R and D stay in registers for the
-// whole run; nothing but the table rows comes from memory inside the loop.
+// whole run (or D in shared memory, kDsmem); nothing but the table rows comes
+// from global memory inside the loop.
 // Table rows are padded with zeros to the variant's capacity NT*EPT
 // (fase_table_ld), so row loads carry no bounds predicates.
 //
@@ -49,10 +50,15 @@ namespace {
 
 constexpr unsigned kNone = 0xffffffffu;
 
-// Dead atoms (D == 0, and the padding past K) carry d = -inf in registers:
-// their metric |R| * d is -inf (NaN when R == 0), which never wins a '>'
-// comparison and never reaches a finite threshold.
-template <int NT, int EPT, int MINB, bool kChunked, bool kRecord>
+// Dead atoms (D == 0, and the padding past K) carry d = -inf: their metric
+// |R| * d is -inf (NaN when R == 0), which never wins a '>' comparison and
+// never reaches a finite threshold.
+//
+// kDsmem: D lives in shared memory instead of registers. That frees 2*EPT
+// registers per thread so three 256-thread CTAs fit per SM (more blocks in
+// flight to hide latency) at the cost of one extra 16-byte shared load per
+// element pair and iteration.
+template <int NT, int EPT, int MINB, bool kDsmem, bool kChunked, bool kRecord>
 __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_iterate_args a) {
   constexpr int EP = EPT / 2;
   constexpr int NW = NT / 32;
@@ -62,9 +68,11 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
   __shared__ unsigned s_u[NW];
   __shared__ double s_r[NW];
   __shared__ double s_d[NW];
-  __shared__ __align__(16) double s_dump[NW][2][EPT];  // tie-pass winner's registers
+  __shared__ __align__(16) double s_dump[NW][kDsmem ? 1 : 2][EPT];  // tie-pass winner's registers
   __shared__ __align__(8) uint64_t s_bar;
-  extern __shared__ double2 s_row[];  // staged row: pair p at s_row[p]
+  extern __shared__ double2 s_dyn[];
+  double2* s_row = s_dyn;            // staged row: pair p at s_row[p]
+  double2* s_D = s_dyn + EP * NT;    // kDsmem: normalizer pairs, same indexing
 
   const int b = blockIdx.x;
   const int t = threadIdx.x;
@@ -88,23 +96,42 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
     cids = a.chunk_ids + lo;
   }
 
-  double r[EP][2], d[EP][2];
+  double r[EP][2];
+  double dreg[kDsmem ? 1 : EP][2];
+  // normalizer pair j of this thread (registers or shared memory)
+  auto dpair = [&](int j) -> double2 {
+    if constexpr (kDsmem)
+      return s_D[j * NT + t];
+    else
+      return make_double2(dreg[j][0], dreg[j][1]);
+  };
   double best = kDead;
   unsigned barg = kNone;
 #pragma unroll
   for (int j = 0; j < EP; ++j) {
     const int k = 2 * (j * NT + t);
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const bool in = k + e < K;
-      r[j][e] = in ? R0[k + e] : 0.0;
-      const double dk = in ? D[k + e] : 0.0;
-      d[j][e] = dk != 0.0 ? dk : kDead;
-      const double m = mul_rn(fabs(r[j][e]), d[j][e]);
-      if (m > best) {
-        best = m;
-        barg = static_cast<unsigned>(k + e);
-      }
+    double2 dd;
+    r[j][0] = k < K ? R0[k] : 0.0;
+    r[j][1] = k + 1 < K ? R0[k + 1] : 0.0;
+    dd.x = k < K ? D[k] : 0.0;
+    dd.y = k + 1 < K ? D[k + 1] : 0.0;
+    dd.x = dd.x != 0.0 ? dd.x : kDead;
+    dd.y = dd.y != 0.0 ? dd.y : kDead;
+    if constexpr (kDsmem) {
+      s_D[j * NT + t] = dd;
+    } else {
+      dreg[j][0] = dd.x;
+      dreg[j][1] = dd.y;
+    }
+    const double m0 = mul_rn(fabs(r[j][0]), dd.x);
+    if (m0 > best) {
+      best = m0;
+      barg = static_cast<unsigned>(k);
+    }
+    const double m1 = mul_rn(fabs(r[j][1]), dd.y);
+    if (m1 > best) {
+      best = m1;
+      barg = static_cast<unsigned>(k + 1);
     }
   }
 
@@ -160,27 +187,35 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
     unsigned cand = kNone;
     if (wkey >= 0 && __longlong_as_double(wkey) >= thr) {  // warp-uniform
 #pragma unroll
-      for (int j = EP - 1; j >= 0; --j)
-#pragma unroll
-        for (int e = 1; e >= 0; --e)
-          if (mul_rn(fabs(r[j][e]), d[j][e]) >= thr) cand = 2 * (j * NT + t) + e;
+      for (int j = EP - 1; j >= 0; --j) {
+        const double2 dd = dpair(j);
+        if (mul_rn(fabs(r[j][1]), dd.y) >= thr) cand = 2 * (j * NT + t) + 1;
+        if (mul_rn(fabs(r[j][0]), dd.x) >= thr) cand = 2 * (j * NT + t);
+      }
     }
     const unsigned wmin = __reduce_min_sync(0xffffffffu, cand);
     if (wmin == kNone) {
       if (lane == 0) s_u[warp] = kNone;
     } else if (cand == wmin) {
-      // fetch R and D of the winner through a shared scratch (no dynamic
+      // fetch R (and D) of the winner through a shared scratch (no dynamic
       // register indexing)
 #pragma unroll
       for (int j = 0; j < EP; ++j) {
         *reinterpret_cast<double2*>(&s_dump[warp][0][2 * j]) = make_double2(r[j][0], r[j][1]);
-        *reinterpret_cast<double2*>(&s_dump[warp][1][2 * j]) = make_double2(d[j][0], d[j][1]);
+        if constexpr (!kDsmem)
+          *reinterpret_cast<double2*>(&s_dump[warp][kDsmem ? 0 : 1][2 * j]) = dpair(j);
       }
-      const int jj = (static_cast<int>(cand >> 1) - t) / NT;
+      const int pair = static_cast<int>(cand >> 1);
+      const int jj = (pair - t) / NT;
       const int ee = static_cast<int>(cand & 1u);
       s_u[warp] = cand;
       s_r[warp] = s_dump[warp][0][2 * jj + ee];
-      s_d[warp] = s_dump[warp][1][2 * jj + ee];
+      if constexpr (kDsmem) {
+        const double2 dd = s_D[pair];
+        s_d[warp] = ee ? dd.y : dd.x;
+      } else {
+        s_d[warp] = s_dump[warp][kDsmem ? 0 : 1][2 * jj + ee];
+      }
     }
     __syncthreads();
     unsigned u;
@@ -200,51 +235,57 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
       coef[it] = c;
     }
 
-    double g[EP][2];
-    if (u == guess) {  // block-uniform
-      mbar_wait(&s_bar, it & 1);
+    mbar_wait(&s_bar, it & 1);  // the staged row (also retires it when unused)
+    // ---- rank-1 update fused with the next iteration's running max; the row
+    // source is block-uniform, so each source gets its own unrolled loop
+    auto update = [&](auto row_pair) {
+      best = kDead;
+      barg = kNone;
 #pragma unroll
       for (int j = 0; j < EP; ++j) {
-        const double2 v = s_row[j * NT + t];
-        g[j][0] = v.x;
-        g[j][1] = v.y;
+        const double2 g = row_pair(j);
+        const double2 dd = dpair(j);
+        r[j][0] = sub_rn(r[j][0], mul_rn(c, g.x));
+        r[j][1] = sub_rn(r[j][1], mul_rn(c, g.y));
+        const double m0 = mul_rn(fabs(r[j][0]), dd.x);
+        if (m0 > best) {
+          best = m0;
+          barg = static_cast<unsigned>(2 * (j * NT + t));
+        }
+        const double m1 = mul_rn(fabs(r[j][1]), dd.y);
+        if (m1 > best) {
+          best = m1;
+          barg = static_cast<unsigned>(2 * (j * NT + t) + 1);
+        }
       }
-    } else {  // the tie rule picked a lower twin: fetch its row directly
-      const double* row = a.G0 + static_cast<int64_t>(u) * ldg + 2 * t;
-#pragma unroll
-      for (int j = 0; j < EP; ++j) {
-        const double2 v = ldg2(row + 2 * j * NT);
-        g[j][0] = v.x;
-        g[j][1] = v.y;
+    };
+    if (kChunked && nch > 0) {
+      // row_u of this block = G0[u] - sum of its chunk tables' rows, composed
+      // in the staging buffer (each thread only touches its own pairs)
+      if (u != guess) {
+        const double* urow = a.G0 + static_cast<int64_t>(u) * ldg + 2 * t;
+#pragma unroll 4
+        for (int j = 0; j < EP; ++j) s_row[j * NT + t] = ldg2(urow + 2 * j * NT);
       }
-      mbar_wait(&s_bar, it & 1);  // retire the staged copy before the next one
-    }
-    if (kChunked) {
       for (int ch = 0; ch < nch; ++ch) {
         const double* crow = a.chunk_tables + static_cast<int64_t>(cids[ch]) * a.chunk_stride +
                              static_cast<int64_t>(u) * ldg + 2 * t;
-#pragma unroll
+#pragma unroll 4
         for (int j = 0; j < EP; ++j) {
           const double2 v = ldg2(crow + 2 * j * NT);
-          g[j][0] = sub_rn(g[j][0], v.x);
-          g[j][1] = sub_rn(g[j][1], v.y);
+          double2 g = s_row[j * NT + t];
+          g.x = sub_rn(g.x, v.x);
+          g.y = sub_rn(g.y, v.y);
+          s_row[j * NT + t] = g;
         }
       }
-    }
-    // ---- rank-1 update fused with the next iteration's running max
-    best = kDead;
-    barg = kNone;
-#pragma unroll
-    for (int j = 0; j < EP; ++j) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        r[j][e] = sub_rn(r[j][e], mul_rn(c, g[j][e]));
-        const double m = mul_rn(fabs(r[j][e]), d[j][e]);
-        if (m > best) {
-          best = m;
-          barg = static_cast<unsigned>(2 * (j * NT + t) + e);
-        }
-      }
+      update([&](int j) { return s_row[j * NT + t]; });
+      fence_proxy_async_smem();  // generic writes above precede the next TMA fill
+    } else if (u == guess) {  // block-uniform
+      update([&](int j) { return s_row[j * NT + t]; });
+    } else {
+      const double* urow = a.G0 + static_cast<int64_t>(u) * ldg + 2 * t;
+      update([&](int j) { return ldg2(urow + 2 * j * NT); });
     }
     if (kRecord) {
       double* dst = a.R_log + (static_cast<int64_t>(b) * a.I + it) * a.ldr;
@@ -273,24 +314,29 @@ using KernelFn = void (*)(const fase_iterate_args);
 struct Variant {
   int nt;
   int ept;
+  bool dsmem;        // D in shared memory (else registers)
   KernelFn plain;    // shared geometry
   KernelFn chunked;  // per-block geometry (chunk-corrected rows)
   KernelFn record;   // shared geometry, R logged after every iteration
 };
 
-#define FASE_V(NT, EPT, MINB)                                                \
-  {NT, EPT, fase_iterate_kernel<NT, EPT, MINB, false, false>,                 \
-   fase_iterate_kernel<NT, EPT, MINB, true, false>,                           \
-   fase_iterate_kernel<NT, EPT, MINB, false, true>}
-// Ordered by capacity NT*EPT; the first variant that holds K is used. R and D
-// live in registers (4 registers per owned atom), which caps K at 512 x 24.
+#define FASE_V(NT, EPT, MINB, DS)                                                       \
+  {NT,                                                                                   \
+   EPT,                                                                                  \
+   DS,                                                                                   \
+   fase_iterate_kernel<NT, EPT, MINB, DS, false, false>,                                 \
+   fase_iterate_kernel<NT, EPT, MINB, DS, true, false>,                                  \
+   fase_iterate_kernel<NT, EPT, MINB, DS, false, true>}
+// Ordered by capacity NT*EPT; the first variant that holds K is used.
+// 256-thread variants keep D in shared memory (3-5 CTAs per SM); the
+// 512-thread variants keep R and D in registers (4 registers per atom), which
+// caps K at 512 x 24.
 const Variant kVariants[] = {
-    FASE_V(128, 2, 4),   FASE_V(128, 4, 4),   FASE_V(128, 6, 4),   FASE_V(128, 8, 4),
-    FASE_V(256, 6, 3),   FASE_V(256, 8, 3),   FASE_V(256, 10, 3),  FASE_V(256, 12, 2),
-    FASE_V(256, 14, 2),  FASE_V(256, 16, 2),  FASE_V(256, 18, 2),
-    FASE_V(256, 20, 2),
-    FASE_V(512, 12, 1),  FASE_V(512, 14, 1),  FASE_V(512, 16, 1),  FASE_V(512, 18, 1),
-    FASE_V(512, 20, 1),  FASE_V(512, 24, 1),
+    FASE_V(128, 2, 4, false),  FASE_V(128, 4, 4, false),  FASE_V(128, 8, 4, false),
+    FASE_V(256, 8, 5, true),   FASE_V(256, 10, 4, true),  FASE_V(256, 12, 3, true),
+    FASE_V(256, 14, 3, true),  FASE_V(256, 16, 3, true),  FASE_V(256, 18, 3, true),
+    FASE_V(256, 20, 2, true),  FASE_V(512, 12, 1, false), FASE_V(512, 16, 1, false),
+    FASE_V(512, 20, 1, false), FASE_V(512, 24, 1, false),
 };
 #undef FASE_V
 
@@ -357,14 +403,14 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
     return FASE_ERR_SHAPE;
   }
   KernelFn fn = a.chunk_ptr ? v->chunked : (a.R_log ? v->record : v->plain);
-  const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2);
-  if (smem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(smem));
-    if (e != cudaSuccess) {
-      set_error("fase_iterate: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-      return FASE_ERR_CUDA;
-    }
+  const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2) * (v->dsmem ? 2 : 1);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e == cudaSuccess)  // several CTAs per SM need the full shared-memory carveout
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) {
+    set_error("fase_iterate: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return FASE_ERR_CUDA;
   }
   fn<<<a.B, v->nt, smem, as_stream(stream)>>>(a);
   return check_launch("fase_iterate");

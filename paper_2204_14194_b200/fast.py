@@ -526,7 +526,7 @@ class ExtrapolationPlan:
         self.lost_idx = torch.from_numpy(lost if lost.size else np.zeros(1, np.int32)).to(dev)
         self.lost_pos = torch.arange(max(self.n_lost, 1), dtype=torch.int64, device=dev)
         self.lost = torch.zeros((self.B, max(self.n_lost, 1)), dtype=torch.float64, device=dev)
-        self.launches_per_run = 3 if self.n_lost else 2
+        self.launches_per_run = 4 if self.n_lost else 3  # weigh, gemm, iterate, synth
 
     def run(self, signals=None):
         """Enqueue one batch. ``signals``: None (use ``self.F`` as filled by the
@@ -561,6 +561,67 @@ class ExtrapolationPlan:
         out["coefficients"].copy_(self.coefficients, non_blocking=True)
         out["lost"].copy_(self.lost, non_blocking=True)
         return out
+
+    def run_host_stream(self, host_inputs, host_outputs):
+        """End-to-end over a sequence of batches with copies overlapped.
+
+        ``host_inputs[i]`` (pinned (B, M, N) float64) goes in and
+        ``host_outputs[i]`` (pinned dicts from ``host_buffers``) comes back, for
+        every i. Step i+1's host-to-device copy runs on its own stream while
+        step i computes, and step i's results come back on a third stream.
+        Device input and output buffers are double-buffered, and events order
+        each reuse. Everything is enqueued; the caller synchronizes.
+        """
+        torch = _torch()
+        dev = self.device
+        cs = torch.cuda.current_stream(dev)
+        if not hasattr(self, "_pipe"):
+            self._pipe = {
+                "h2d": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev),
+                "F": [self.F, torch.zeros_like(self.F)],
+                "out": [(self.selected, self.projections, self.coefficients, self.lost),
+                        tuple(torch.empty_like(x) for x in (self.selected, self.projections,
+                                                            self.coefficients, self.lost))],
+            }
+        p = self._pipe
+        h2d, d2h = p["h2d"], p["d2h"]
+        ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_used = [None, None]     # compute finished reading F[slot]
+        ev_out = [None, None]      # results of slot copied back
+        for i, (hin, hout) in enumerate(zip(host_inputs, host_outputs)):
+            s = i % 2
+            F = p["F"][s]
+            sel, proj, coef, lost = p["out"][s]
+            with torch.cuda.stream(h2d):
+                if ev_used[s] is not None:
+                    h2d.wait_event(ev_used[s])
+                F[:, : self.M].copy_(hin.reshape(self.B, -1), non_blocking=True)
+                ev_in[s].record(h2d)
+            cs.wait_event(ev_in[s])
+            if ev_out[s] is not None:
+                cs.wait_event(ev_out[s])
+            _native.init_products(self.phi, F, self.W, self.K, self.M, self.R0, ws=self.ws)
+            ev_used[s] = torch.cuda.Event()
+            ev_used[s].record(cs)
+            _native.iterate(self.G, self.D, self.R0, self.K, self.I, self.config.gamma, sel, proj,
+                            coef)
+            if self.n_lost:
+                _native.synth_paste(self.phi, sel, coef, self.I, self.lost_idx, lost,
+                                    n_shared=self.n_lost, dst=self.lost_pos)
+            done = torch.cuda.Event()
+            done.record(cs)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done)
+                hout["selected"].copy_(sel, non_blocking=True)
+                hout["coefficients"].copy_(coef, non_blocking=True)
+                hout["lost"].copy_(lost, non_blocking=True)
+                ev_out[s] = torch.cuda.Event()
+                ev_out[s].record(d2h)
+        # the caller's stream waits for the last copies
+        for e in ev_out:
+            if e is not None:
+                cs.wait_event(e)
+        return host_outputs
 
     def bytes_h2d(self) -> int:
         return self.B * self.M * 8
