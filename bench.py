@@ -273,11 +273,11 @@ def run_gpu(args):
     # one more table build, kernels only, for the reported Gram time
     G2 = torch.zeros_like(plan.G)
     D2 = torch.empty_like(plan.D)
+    gws = torch.empty(K * plan.phi.shape[1] + 2, dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
     g0 = torch.cuda.Event(enable_timing=True)
     g1 = torch.cuda.Event(enable_timing=True)
     g0.record()
-    gws = torch.empty(K * plan.phi.shape[1] + 2, dtype=torch.float64, device=dev)
     _native.gram(plan.phi, plan.W, K, M, G2, ws=gws)
     _native.gram_finish(G2, K, D2)
     g1.record()

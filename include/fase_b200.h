@@ -85,10 +85,11 @@ FASE_API int fase_gram(const double* phi, int64_t ldphi, const double* w, int K,
 
 /*
  * Plain FP64 contraction C[i*ldc + j] = sum_k A[i*lda + k] * B[j*ldb + k]
- * (the DMMA tile kernel behind fase_gram / fase_init_products).
+ * (the DMMA tile kernel behind fase_gram / fase_init_products; variant 0 is
+ * the library's tile, 1 an alternative tile kept for measurement).
  */
 FASE_API int fase_gemm_nt(const double* A, int64_t lda, const double* B, int64_t ldb, int M,
-                          int N, int Kd, double* C, int64_t ldc, void* stream);
+                          int N, int Kd, double* C, int64_t ldc, int variant, void* stream);
 
 /*
  * Normalizers (replaces _finish_tables, fast.py:97-106):

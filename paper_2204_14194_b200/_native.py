@@ -83,7 +83,7 @@ def load():
     sigs = {
         "fase_basis_outer": [_vp, _i32, _i32, _vp, _i32, _i32, _vp, _i64, _i64, _vp],
         "fase_gram": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp, ctypes.c_size_t, _vp],
-        "fase_gemm_nt": [_vp, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp],
+        "fase_gemm_nt": [_vp, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _i32, _vp],
         "fase_gram_finish": [_vp, _i64, _i32, _vp, _vp, _vp],
         "fase_init_products": [_vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp,
                                ctypes.c_size_t, _vp],
@@ -184,7 +184,7 @@ def init_products_workspace(M: int, B: int) -> int:
     return int(load().fase_init_products_workspace(M, B))
 
 
-def gemm_nt(A, B, C) -> None:
+def gemm_nt(A, B, C, variant: int = 0) -> None:
     """C = A @ B.T in FP64 (all 2-D, contiguous rows)."""
     import torch
 
@@ -192,7 +192,7 @@ def gemm_nt(A, B, C) -> None:
     for t, n in ((A, "A"), (B, "B"), (C, "C")):
         _require(t, n, torch.float64, 2)
     _check(lib.fase_gemm_nt(_ptr(A), _ld(A), _ptr(B), _ld(B), A.shape[0], B.shape[0], A.shape[1],
-                            _ptr(C), _ld(C), _stream(C)))
+                            _ptr(C), _ld(C), variant, _stream(C)))
 
 
 def gram_finish(G, K: int, D, n_alive=None) -> None:

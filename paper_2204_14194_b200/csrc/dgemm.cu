@@ -17,10 +17,12 @@
 // warp-level `mma.sync ... .f64` path, which ptxas lowers to DMMA.8x8x4.
 // Measured DMMA issue peak on the B200: 37 TFLOP/s (tools/probes/dmma_probe.cu).
 //
-// Tiling: 128 x 128 CTA tile, BK = 16, 3-stage cp.async ring, 8 warps as
-// 2 (M) x 4 (N), warp tile 64 x 32 = 8 x 4 DMMA 8x8 accumulators (64 FP64
-// registers). Shared rows are padded to 20 doubles: the 8x4 fragment a
-// half-warp reads then hits 16 distinct 8-byte bank pairs.
+// Tiling: BK = 16, 3-stage cp.async ring; main tile 64 x 128 with 4 warps of
+// 32 x 64 (4 x 8 DMMA 8x8 accumulators, 64 FP64 registers) and two CTAs per
+// SM, so one CTA's k-tile barrier is covered by the other; a 128 x 128 /
+// 8-warp tile is kept as fase_gemm_nt variant 1 for comparison. Shared rows are
+// padded to 20 doubles: the 8x4 fragment a half-warp reads then hits 16
+// distinct 8-byte bank pairs.
 // Symmetric mode (Gram) computes tiles with bm <= bn only and writes each
 // accumulator to (i, j) and (j, i): the table is bit-symmetric.
 
@@ -29,12 +31,9 @@
 namespace fase {
 namespace {
 
-constexpr int BM = 128;
-constexpr int BN = 128;
 constexpr int BK = 16;
 constexpr int LDS = BK + 4;
 constexpr int STAGES = 3;
-constexpr int NTHREADS = 256;
 
 struct GemmParams {
   const double* A;
@@ -54,54 +53,68 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
-template <bool kSym>
-__global__ void __launch_bounds__(NTHREADS, 1) dgemm_nt_kernel(const GemmParams p) {
+// BM x BN CTA tile, warps of WM x WN (a grid of BM/WM x BN/WN warps),
+// MINB resident CTAs per SM.
+template <int BM, int BN, int WM, int WN, int MINB>
+struct Tile {
+  static constexpr int kBM = BM, kBN = BN, kWM = WM, kWN = WN;
+  static constexpr int kWarpsM = BM / WM, kWarpsN = BN / WN;
+  static constexpr int kThreads = 32 * kWarpsM * kWarpsN;
+  static constexpr int kMinBlocks = MINB;
+  static constexpr size_t kSmem = sizeof(double) * STAGES * LDS * (BM + BN);
+};
+using TileBig = Tile<128, 128, 64, 32, 1>;   // 8 warps, 1 CTA / SM
+using TileSmall = Tile<64, 128, 32, 64, 2>;  // 4 warps, 2 CTAs / SM
+
+template <class T, bool kSym>
+__global__ void __launch_bounds__(T::kThreads, T::kMinBlocks) dgemm_nt_kernel(const GemmParams p) {
+  constexpr int BM = T::kBM, BN = T::kBN, NTH = T::kThreads;
+  constexpr int MI = T::kWM / 8, NI = T::kWN / 8;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = As + STAGES * BM * LDS;
 
   const int bm = blockIdx.y;
   const int bn = blockIdx.x;
-  if (kSym && bm > bn) return;
+  if (kSym && bm * BM >= (bn + 1) * BN) return;  // entirely below the diagonal
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int wm = warp >> 2;
-  const int wn = warp & 3;
+  const int wm = warp / T::kWarpsN;
+  const int wn = warp % T::kWarpsN;
   const int row0 = bm * BM;
   const int col0 = bn * BN;
   const int ktiles = (p.kdim + BK - 1) / BK;
 
-  auto load_stage = [&](int stage, int kt) {
-    const int k0 = kt * BK;
+  auto load_rows = [&](double* dst, const double* src, int64_t ld, int rows_total, int row_base,
+                       int nrows, int k0) {
+    constexpr int kChunksPerRow = BK / 2;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int idx = tid + i * NTHREADS;
-      const int r = idx >> 3;
-      const int kc = (idx & 7) * 2;
-      const int k = k0 + kc;
-      int kb = (p.kdim - k) * 8;
-      kb = kb < 0 ? 0 : (kb > 16 ? 16 : kb);
-      {
-        const int gr = row0 + r;
-        const int nb = gr < p.m_rows ? kb : 0;
-        const double* src = nb ? p.A + static_cast<int64_t>(gr) * p.lda + k : p.A;
-        cp_async16(As + (stage * BM + r) * LDS + kc, src, nb);
-      }
-      {
-        const int gr = col0 + r;
-        const int nb = gr < p.n_rows ? kb : 0;
-        const double* src = nb ? p.B + static_cast<int64_t>(gr) * p.ldb + k : p.B;
-        cp_async16(Bs + (stage * BN + r) * LDS + kc, src, nb);
+    for (int i = 0; i < (nrows * kChunksPerRow + NTH - 1) / NTH; ++i) {
+      const int idx = tid + i * NTH;
+      if (idx < nrows * kChunksPerRow) {
+        const int r = idx / kChunksPerRow;
+        const int kc = (idx % kChunksPerRow) * 2;
+        const int k = k0 + kc;
+        int kb = (p.kdim - k) * 8;
+        kb = kb < 0 ? 0 : (kb > 16 ? 16 : kb);
+        const int gr = row_base + r;
+        const int nb = gr < rows_total ? kb : 0;
+        const double* g = nb ? src + static_cast<int64_t>(gr) * ld + k : src;
+        cp_async16(dst + r * LDS + kc, g, nb);
       }
     }
   };
+  auto load_stage = [&](int stage, int kt) {
+    load_rows(As + stage * BM * LDS, p.A, p.lda, p.m_rows, row0, BM, kt * BK);
+    load_rows(Bs + stage * BN * LDS, p.B, p.ldb, p.n_rows, col0, BN, kt * BK);
+  };
 
-  double acc[8][4][2];
+  double acc[MI][NI][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -119,30 +132,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) dgemm_nt_kernel(const GemmParams 
     if (nk < ktiles) load_stage(nk % STAGES, nk);
     cp_async_commit();
 
-    const double* as = As + st * BM * LDS + (wm * 64 + fr) * LDS + fc;
-    const double* bs = Bs + st * BN * LDS + (wn * 32 + fr) * LDS + fc;
+    const double* as = As + st * BM * LDS + (wm * T::kWM + fr) * LDS + fc;
+    const double* bs = Bs + st * BN * LDS + (wn * T::kWN + fr) * LDS + fc;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double a[8], b[4];
+      double a[MI], b[NI];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = as[i * 8 * LDS + kk];
+      for (int i = 0; i < MI; ++i) a[i] = as[i * 8 * LDS + kk];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = bs[j * 8 * LDS + kk];
+      for (int j = 0; j < NI; ++j) b[j] = bs[j * 8 * LDS + kk];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
   cp_async_wait<0>();
 
   const bool vec_ok = ((p.ldc & 1) == 0) && aligned16(p.C);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int r = row0 + wm * 64 + i * 8 + fr;
+  for (int i = 0; i < MI; ++i) {
+    const int r = row0 + wm * T::kWM + i * 8 + fr;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = col0 + wn * 32 + j * 8 + fc * 2;
+    for (int j = 0; j < NI; ++j) {
+      const int c = col0 + wn * T::kWN + j * 8 + fc * 2;
       if (!kSym) {
         if (r < p.m_rows) {
           double* dst = p.C + static_cast<int64_t>(r) * p.ldc + c;
@@ -186,21 +199,26 @@ __global__ void weigh_kernel(const double* __restrict__ x, int64_t ldx, const do
   }
 }
 
-template <bool kSym>
+template <class T, bool kSym>
 int launch(const GemmParams& p, cudaStream_t stream, const char* what) {
-  const size_t smem = sizeof(double) * STAGES * LDS * (BM + BN);
-  // per-device attribute; cheap enough to set on every launch
-  cudaError_t e = cudaFuncSetAttribute(dgemm_nt_kernel<kSym>,
+  // per-device attributes; cheap enough to set on every launch
+  cudaError_t e = cudaFuncSetAttribute(dgemm_nt_kernel<T, kSym>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+                                       static_cast<int>(T::kSmem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(dgemm_nt_kernel<T, kSym>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) {
     set_error("%s: cudaFuncSetAttribute: %s", what, cudaGetErrorString(e));
     return FASE_ERR_CUDA;
   }
-  dim3 grid((p.n_rows + BN - 1) / BN, (p.m_rows + BM - 1) / BM);
-  dgemm_nt_kernel<kSym><<<grid, NTHREADS, smem, stream>>>(p);
+  dim3 grid((p.n_rows + T::kBN - 1) / T::kBN, (p.m_rows + T::kBM - 1) / T::kBM);
+  dgemm_nt_kernel<T, kSym><<<grid, T::kThreads, T::kSmem, stream>>>(p);
   return check_launch(what);
 }
+
+// The tile used by the library entry points (see tools/probes/gemm_probe.py).
+using TileMain = TileSmall;
 
 int launch_weigh(const double* x, int64_t ldx, const double* w, int64_t ldw, int rows, int M,
                  double* out, int64_t ldo, cudaStream_t stream, const char* what) {
@@ -247,7 +265,7 @@ extern "C" int fase_gram(const double* phi, int64_t ldphi, const double* w, int 
   int st = launch_weigh(phi, ldphi, w, 0, K, M, pw, ldw, s, "fase_gram (weigh)");
   if (st != FASE_OK) return st;
   GemmParams p{pw, ldw, phi, ldphi, G, ldg, K, K, M};
-  return launch<true>(p, s, "fase_gram");
+  return launch<TileMain, true>(p, s, "fase_gram");
 }
 
 extern "C" int fase_init_products(const double* phi, int64_t ldphi, const double* f, int64_t ldf,
@@ -273,11 +291,11 @@ extern "C" int fase_init_products(const double* phi, int64_t ldphi, const double
   int st = launch_weigh(f, ldf, w, ldw, B, M, fw, ldfw, s, "fase_init_products (weigh)");
   if (st != FASE_OK) return st;
   GemmParams p{fw, ldfw, phi, ldphi, R0, ldr, B, K, M};
-  return launch<false>(p, s, "fase_init_products");
+  return launch<TileMain, false>(p, s, "fase_init_products");
 }
 
 extern "C" int fase_gemm_nt(const double* A, int64_t lda, const double* B, int64_t ldb, int M,
-                            int N, int Kd, double* C, int64_t ldc, void* stream) {
+                            int N, int Kd, double* C, int64_t ldc, int variant, void* stream) {
   if (M < 0 || N < 0 || Kd < 1) {
     set_error("fase_gemm_nt: bad sizes (M=%d, N=%d, K=%d)", M, N, Kd);
     return FASE_ERR_SHAPE;
@@ -288,5 +306,6 @@ extern "C" int fase_gemm_nt(const double* A, int64_t lda, const double* B, int64
     return FASE_ERR_SHAPE;
   }
   GemmParams p{A, lda, B, ldb, C, ldc, M, N, Kd};
-  return launch<false>(p, as_stream(stream), "fase_gemm_nt");
+  return variant == 1 ? launch<TileBig, false>(p, as_stream(stream), "fase_gemm_nt")
+                      : launch<TileMain, false>(p, as_stream(stream), "fase_gemm_nt");
 }
