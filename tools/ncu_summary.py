@@ -60,6 +60,7 @@ def to_bytes(val: str, unit: str) -> float:
 
 def short(name: str) -> str:
     for key in ("fase_iterate_kernel", "dgemm_nt_kernel", "synth_paste_kernel", "gram_finish_kernel",
+                "weigh_kernel",
                 "block_normalizers_kernel", "basis_outer_kernel", "flush_kernel"):
         if key in name:
             return key
