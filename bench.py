@@ -57,7 +57,7 @@ def parse_args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 4])
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target wall seconds of the bounded CPU-baseline sample")
@@ -72,20 +72,30 @@ _CPU = {}
 
 
 def _cpu_worker(args):
-    """Extrapolate blocks [first, first+n) of the workload with the oracle port."""
+    """Extrapolate blocks [first, first+n) of the workload with the oracle port.
+
+    Shared geometry (configs 0/1/4): tables prebuilt once, as the reference's
+    bench does. Frame configs (2/3): per block weight -> Gram table -> FaSE ->
+    paste, the reference's own frame path (conceal.py:132-141) minus its
+    unbounded table cache.
+    """
     cid, first, n = args
     from threadpoolctl import threadpool_limits
 
     from oracle import fase_oracle as orc
 
     w = wl.WORKLOADS[cid]
-    vals, mask, tables = _CPU["vals"], _CPU["mask"], _CPU["tables"]
-    nb = w.n_blocks
+    vals, tables = _CPU["vals"], _CPU["tables"]
+    nb = _CPU["n_blocks"]
     with threadpool_limits(limits=1):
         t0 = time.perf_counter()
         for i in range(n):
             b = (first + i) % nb
-            sig = wl.block_signals(cid, 1, *w.area, first=b)[0]
+            if tables is not None:
+                sig = wl.block_signals(cid, 1, *w.area, first=b)[0]
+                mask = _CPU["mask"]
+            else:
+                sig, mask = _CPU["signals"][b], _CPU["masks"][b]
             orc.extrapolate_block(sig, mask, vals, w.config.gamma, w.config.iterations,
                                   w.config.rho_hat, tables=tables)
         return n, time.perf_counter() - t0
@@ -97,9 +107,18 @@ def cpu_prepare(cid: int):
     w = wl.WORKLOADS[cid]
     d = w.dictionary()
     vals = d.real_values().astype(np.complex128)
-    mask = wl.central_loss_mask(*w.area, *w.loss)
-    tables = orc.gram(vals.reshape(len(vals), -1), orc.weight_field(mask, w.config.rho_hat))
-    _CPU.update(vals=vals, mask=mask, tables=tables)
+    if w.shared_geometry:
+        mask = wl.central_loss_mask(*w.area, *w.loss)
+        tables = orc.gram(vals.reshape(len(vals), -1), orc.weight_field(mask, w.config.rho_hat))
+        _CPU.update(vals=vals, mask=mask, tables=tables, n_blocks=w.n_blocks)
+    else:
+        case = wl.frame_case(w)
+        signals, masks = wl.frame_areas(case.damaged(), case.lost, case.corners, case.mb,
+                                        case.support)
+        # spread the sample over the frame: every 7th block
+        order = np.arange(len(masks))[::7]
+        _CPU.update(vals=vals, tables=None, signals=signals[order], masks=masks[order],
+                    n_blocks=len(order))
 
 
 def cpu_sample(cid: int, seconds: float, pool, procs: int, per_block_s: float):
@@ -156,13 +175,21 @@ def run_reference(args):
 
 
 def workload_config(w, n_gpus):
-    return {"workload": w.name, "blocks_per_gpu": w.n_blocks, "area": list(w.area),
-            "K": w.n_atoms, "M": w.area[0] * w.area[1],
-            "iterations": w.config.iterations, "gamma": w.config.gamma, "rho": w.config.rho_hat,
-            "dictionary": w.dict_spec, "loss": f"{w.loss[0]}x{w.loss[1]} centred",
-            "tables": "shared Gram prebuilt before the clock (reference bench.py:118-119)",
-            "l2": "flushed between timed steps (256 MiB write)",
-            "parallelism": f"dp{n_gpus} (block sharding, no collective)"}
+    cfg = {"workload": w.name, "area": list(w.area), "K": w.n_atoms,
+           "M": w.area[0] * w.area[1], "iterations": w.config.iterations, "gamma": w.config.gamma,
+           "rho": w.config.rho_hat, "dictionary": w.dict_spec,
+           "l2": "flushed between timed steps (256 MiB write)",
+           "parallelism": f"dp{n_gpus} (block sharding, no collective)"}
+    if w.shared_geometry:
+        cfg.update(blocks_per_gpu=w.n_blocks, loss=f"{w.loss[0]}x{w.loss[1]} centred",
+                   tables="shared Gram prebuilt before the clock (reference bench.py:118-119)")
+    else:
+        cfg.update(frame=list(w.frame), macroblock=w.macroblock, support=w.support,
+                   loss=f"{w.loss_fraction:.0%} of full macroblocks",
+                   tables="frame-independent cell tables prebuilt (G0 + one per area cell); "
+                          "per-frame cell lists, normalizers, products, recursion, paste timed",
+                   parallelism=f"dp{n_gpus} (one frame per GPU, no collective)")
+    return cfg
 
 
 class ClockSampler:
@@ -421,12 +448,155 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
+def run_gpu_frame(args):
+    """Configs 2/3: one step = conceal one damaged frame (all lossy macroblocks)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_14194_b200 import _native
+    from paper_2204_14194_b200.conceal import FrameEngine, lossy_tiles, tile_grid
+
+    rank, world, local = dist_env()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, args.cpu_seconds)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _native.load()
+    w = wl.WORKLOADS[args.config]
+    d = w.dictionary()
+    case = wl.frame_case(w)
+    K, M, I = len(d), w.area[0] * w.area[1], w.config.iterations
+    engine = FrameEngine(d, case.frame.shape, case.mb, case.support, w.config, device=dev)
+    grid_h = tile_grid(case.lost, case.mb)
+    corners_h = lossy_tiles(case.lost, (case.mb, case.mb)).astype(np.int32)
+    L = len(corners_h)
+    frame_u8 = torch.from_numpy(case.frame).pin_memory()
+    lost_h = torch.from_numpy(case.lost)
+    grid = torch.from_numpy(grid_h).to(dev)
+    corners = torch.from_numpy(corners_h).to(dev)
+    damaged = torch.from_numpy(case.damaged()).to(dev)
+    out = damaged.clone()
+    out_host = torch.empty(out.shape, dtype=torch.float64, pin_memory=True)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    lost_dev = lost_h.to(dev)
+    for _ in range(max(args.warmup, 1)):
+        engine.run(damaged, grid, corners, out=out)
+    torch.cuda.synchronize()
+    if engine.dead_blocks():
+        raise RuntimeError("a block had every atom degenerate")
+
+    def e2e_step(frame_dev):
+        # H2D of the uint8 frame, widening + loss zeroing, concealment, D2H
+        frame_dev.copy_(frame_u8, non_blocking=True)
+        f64 = frame_dev.to(torch.float64).masked_fill_(lost_dev, 0.0)
+        engine.run(f64, grid, corners, out=f64)
+        out_host.copy_(f64, non_blocking=True)
+
+    frame_dev = torch.empty(case.frame.shape, dtype=torch.uint8, device=dev)
+    e2e_step(frame_dev)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    gpu_id = str(local)
+    try:
+        gpu_id = f"GPU-{torch.cuda.get_device_properties(dev).uuid}"
+    except AttributeError:
+        pass
+    dev_ms, e2e_ms = [], []
+    with ClockSampler(gpu_id) as clocks:
+        t_wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            _native.l2_flush(flush)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            engine.run(damaged, grid, corners, out=out)
+            e1.record(stream)
+            dev_ms.append((e0, e1))
+        for _ in range(args.steps):
+            _native.l2_flush(flush)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_step(frame_dev)
+            e1.record(stream)
+            e2e_ms.append((e0, e1))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    dev_t = sum(a.elapsed_time(b) for a, b in dev_ms) / 1e3
+    e2e_t = sum(a.elapsed_time(b) for a, b in e2e_ms) / 1e3
+    tot = torch.tensor([dev_t, e2e_t], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    dev_t, e2e_t = tot.tolist()
+    # kernel split of one frame, for the roofline
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    b = engine._buffers(L)
+    ev[0].record(stream)
+    engine.run(damaged, grid, corners, out=out)
+    ev[2].record(stream)
+    torch.cuda.synchronize()
+    counts = b["counts"].float()
+    mean_rows = 1.0 + float(counts.mean())
+    # recursion alone (same inputs as the last run)
+    ev_i0 = torch.cuda.Event(enable_timing=True)
+    ev_i1 = torch.cuda.Event(enable_timing=True)
+    ev_i0.record(stream)
+    _native.iterate(engine.G0, b["D"], b["R0"], K, I, w.config.gamma, b["sel"], b["proj"], b["coef"],
+                    chunk_tables=engine.tables, chunk_stride=engine.stride,
+                    chunk_count=b["counts"], chunk_ids=b["ids"])
+    ev_i1.record(stream)
+    torch.cuda.synchronize()
+    it_s = ev_i0.elapsed_time(ev_i1) / 1e3
+    if rank == 0:
+        hbm, hsrc, fp64, fsrc = measured_peaks()
+        bytes_iter = 8.0 * K * L * I * mean_rows
+        achieved = bytes_iter / it_s / 1e9
+        line = {
+            "metric": "extrapolated blocks/s", "value": world * L * args.steps / dev_t,
+            "unit": "blocks/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dev_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic frame (seeded BASELINE Appendix-A generator)",
+            "config": dict(workload_config(w, world), blocks_per_frame=L,
+                           cells=len(engine.cells), mean_rows_per_iteration=mean_rows),
+            "e2e": {"value": world * L * args.steps / e2e_t, "unit": "blocks/s",
+                    "h2d_bytes_per_step": int(case.frame.nbytes),
+                    "d2h_bytes_per_step": int(out_host.numel() * 8),
+                    "ms_per_step": e2e_t / args.steps * 1e3,
+                    "api": "FrameEngine.run on an uploaded uint8 frame; restored float64 frame read back"},
+            "roofline": {"bound": "hbm", "kernel": "fase_iterate_kernel (chunked rows)",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": None, "algorithmic_bytes_per_launch": bytes_iter,
+                         "ms_per_launch": it_s * 1e3, "peak_source": hsrc,
+                         "note": "8*K bytes per table row, (1 + unavailable cells) rows per "
+                                 "block-iteration"},
+            "table_build_s": engine.table_seconds,
+            "gpu_launches": args.steps * (engine.launches_per_frame + 1) * 2,
+            "clocks": clocks.summary(), "wall_s": t_wall, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         run_reference(args)
-    else:
+    elif wl.WORKLOADS[args.config].shared_geometry:
         run_gpu(args)
+    else:
+        run_gpu_frame(args)
 
 
 if __name__ == "__main__":

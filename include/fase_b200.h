@@ -119,9 +119,9 @@ FASE_API int fase_init_products(const double* phi, int64_t ldphi, const double* 
  * n_alive[b] receives the count of non-degenerate atoms of block b.
  */
 FASE_API int fase_block_normalizers(const double* G0, int64_t ldg, const double* chunk_tables,
-                           int64_t chunk_stride, const int32_t* chunk_ptr,
-                           const int32_t* chunk_ids, int K, int B, double* D, int64_t ldd,
-                           int32_t* n_alive, void* stream);
+                           int64_t chunk_stride, const int32_t* chunk_count,
+                           const int32_t* chunk_ids, int64_t chunk_list_ld, int K, int B,
+                           double* D, int64_t ldd, int32_t* n_alive, void* stream);
 
 /*
  * The FaSE recursion for B independent blocks (replaces the loop of
@@ -129,8 +129,8 @@ FASE_API int fase_block_normalizers(const double* G0, int64_t ldg, const double*
  *   metric_k = |R_k| * D_k  (D_k == 0: never selectable)
  *   q = max(q, 1e-13 * max metric);  u = lowest k with metric_k >= max - q
  *   p = R_u * (D_u * D_u);  c = gamma * p;  R_k <- R_k - c * row_u[k]
- * row_u = G0[u, :] - sum_{j in chunks(b)} C_j[u, :]   (chunk list empty when
- * chunk_ptr == NULL: shared geometry). One persistent CTA per block keeps R and
+ * row_u = G0[u, :] - sum_{j in chunks(b)} C_j[u, :]   (no chunk lists when
+ * chunk_count == NULL: shared geometry). One persistent CTA per block keeps R and
  * D in registers; rows are streamed with 16-byte loads. G0 / C_j rows must be
  * zero-padded to ldg >= fase_table_ld(K).
  *   R0, R_out: B x ldr (R_out may be NULL or alias R0)
@@ -143,8 +143,9 @@ typedef struct {
   int64_t ldg;
   const double* chunk_tables; /* C_j = chunk_tables + j * chunk_stride, row stride ldg */
   int64_t chunk_stride;
-  const int32_t* chunk_ptr;   /* B+1 offsets into chunk_ids, or NULL */
-  const int32_t* chunk_ids;
+  const int32_t* chunk_count; /* B list lengths, or NULL: shared geometry */
+  const int32_t* chunk_ids;   /* B x chunk_list_ld table ids, each list in order */
+  int64_t chunk_list_ld;
   const double* D;
   int64_t ldd;
   const double* R0;
@@ -178,6 +179,35 @@ FASE_API int fase_iterate(const fase_iterate_args* args, void* stream);
 FASE_API int fase_synth_paste(const double* phi, int64_t ldphi, const int32_t* sel, const double* coef,
                      int64_t ldo, int I, int B, const int32_t* idx_ptr, const int32_t* idx,
                      int n_shared, const int64_t* dst, double* out, int64_t ldout, void* stream);
+
+/*
+ * Frame concealment (replaces the per-tile body of conceal_image,
+ * conceal.py:111-148, for every lossy tile of a frame at once). Losses are
+ * whole tiles: grid is the (H/tile) x (W/tile) tile loss map (nonzero = lost);
+ * corners (L x 2, int32) are the top-left pixels of the lossy tiles; areas are
+ * A x A with A = tile + 2*support, out-of-frame samples unavailable.
+ *
+ * fase_frame_areas: X[b, i*A + j] = frame(r0-s+i, c0-s+j) * base_w[i*A + j] on
+ *   support samples, 0 elsewhere -- the weighted operand of the initial products.
+ * fase_frame_cells: counts[b], ids[b, :] = the candidate cells (rectangles of
+ *   the area, one representative sample (i, j) each in cell_rep) unavailable
+ *   for block b -- the chunk lists of fase_iterate / fase_block_normalizers.
+ * fase_frame_paste: the tile's own lost pixels <- sum_t coef * phi[sel, m]
+ *   (conceal.py:144-148).
+ */
+FASE_API int fase_frame_areas(const double* frame, int64_t ldf, const uint8_t* grid,
+                              int64_t ldgrid, int H, int W, int tile, int support,
+                              const int32_t* corners, int L, const double* base_w, double* X,
+                              int64_t ldx, void* stream);
+FASE_API int fase_frame_cells(const uint8_t* grid, int64_t ldgrid, int H, int W, int tile,
+                              int support, const int32_t* corners, int L,
+                              const int32_t* cell_rep, int n_cells, int32_t* counts,
+                              int32_t* ids, int64_t ids_ld, void* stream);
+FASE_API int fase_frame_paste(const double* phi, int64_t ldphi, const int32_t* sel,
+                              const double* coef, int64_t ldo, int I, const uint8_t* grid,
+                              int64_t ldgrid, int H, int W, int tile, int support,
+                              const int32_t* corners, int L, double* out, int64_t ldout,
+                              void* stream);
 
 /* Writes `bytes` of zeros-then-ones into `buf` to evict L2 between timed steps. */
 FASE_API int fase_l2_flush(void* buf, size_t bytes, void* stream);

@@ -32,7 +32,8 @@ EXPORTS = (
     "fase_last_error", "fase_abi_version", "fase_max_atoms", "fase_table_ld", "fase_basis_outer",
     "fase_gram", "fase_gram_workspace", "fase_gemm_nt", "fase_init_products_workspace",
     "fase_gram_finish", "fase_init_products", "fase_block_normalizers", "fase_iterate",
-    "fase_synth_paste", "fase_l2_flush",
+    "fase_synth_paste", "fase_l2_flush", "fase_frame_areas", "fase_frame_cells",
+    "fase_frame_paste",
 )
 
 _vp = ctypes.c_void_p
@@ -46,7 +47,8 @@ class IterateArgs(ctypes.Structure):
 
     _fields_ = [
         ("G0", _vp), ("ldg", _i64), ("chunk_tables", _vp), ("chunk_stride", _i64),
-        ("chunk_ptr", _vp), ("chunk_ids", _vp), ("D", _vp), ("ldd", _i64), ("R0", _vp),
+        ("chunk_count", _vp), ("chunk_ids", _vp), ("chunk_list_ld", _i64), ("D", _vp),
+        ("ldd", _i64), ("R0", _vp),
         ("ldr", _i64), ("R_out", _vp), ("R_log", _vp), ("K", _i32), ("B", _i32), ("I", _i32),
         ("gamma", _f64), ("sel", _vp), ("proj", _vp), ("coef", _vp), ("ldo", _i64),
     ]
@@ -87,12 +89,18 @@ def load():
         "fase_gram_finish": [_vp, _i64, _i32, _vp, _vp, _vp],
         "fase_init_products": [_vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp,
                                ctypes.c_size_t, _vp],
-        "fase_block_normalizers": [_vp, _i64, _vp, _i64, _vp, _vp, _i32, _i32, _vp, _i64, _vp,
-                                   _vp],
+        "fase_block_normalizers": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _i64,
+                                   _vp, _vp],
         "fase_iterate": [ctypes.POINTER(IterateArgs), _vp],
         "fase_synth_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
                              _i64, _vp],
         "fase_l2_flush": [_vp, ctypes.c_size_t, _vp],
+        "fase_frame_areas": [_vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp,
+                             _i64, _vp],
+        "fase_frame_cells": [_vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _vp,
+                             _i64, _vp],
+        "fase_frame_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i32, _i32,
+                             _vp, _i32, _vp, _i64, _vp],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -220,20 +228,22 @@ def init_products(phi, f, w, K: int, M: int, R0, ws=None) -> None:
                                   _ptr(R0), _ld(R0), _ptr(ws), ws.numel() * 8, _stream(R0)))
 
 
-def block_normalizers(G0, chunk_tables, chunk_stride: int, chunk_ptr, chunk_ids, K: int,
+def block_normalizers(G0, chunk_tables, chunk_stride: int, chunk_count, chunk_ids, K: int,
                       D, n_alive) -> None:
+    """D of B per-block geometries; chunk_ids is (B, L) with chunk_count[b] valid entries."""
     import torch
 
     lib = load()
     _require(G0, "G0", torch.float64, 2)
     _require(D, "D", torch.float64, 2)
+    list_ld = _ld(chunk_ids) if chunk_ids is not None else 0
     _check(lib.fase_block_normalizers(_ptr(G0), _ld(G0), _ptr(chunk_tables), chunk_stride,
-                                      _ptr(chunk_ptr), _ptr(chunk_ids), K, D.shape[0], _ptr(D),
-                                      _ld(D), _ptr(n_alive), _stream(D)))
+                                      _ptr(chunk_count), _ptr(chunk_ids), list_ld, K, D.shape[0],
+                                      _ptr(D), _ld(D), _ptr(n_alive), _stream(D)))
 
 
 def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *,
-            chunk_tables=None, chunk_stride: int = 0, chunk_ptr=None, chunk_ids=None,
+            chunk_tables=None, chunk_stride: int = 0, chunk_count=None, chunk_ids=None,
             R_out=None, R_log=None) -> None:
     import torch
 
@@ -246,7 +256,8 @@ def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *
     _require(coef, "coef", torch.float64, 2)
     args = IterateArgs(
         G0=_ptr(G0), ldg=_ld(G0), chunk_tables=_ptr(chunk_tables), chunk_stride=chunk_stride,
-        chunk_ptr=_ptr(chunk_ptr), chunk_ids=_ptr(chunk_ids), D=_ptr(D),
+        chunk_count=_ptr(chunk_count), chunk_ids=_ptr(chunk_ids),
+        chunk_list_ld=_ld(chunk_ids) if chunk_ids is not None else 0, D=_ptr(D),
         ldd=_ld(D) if D.dim() == 2 else 0, R0=_ptr(R0), ldr=_ld(R0), R_out=_ptr(R_out),
         R_log=_ptr(R_log), K=K, B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel),
         proj=_ptr(proj), coef=_ptr(coef), ldo=_ld(sel))
@@ -268,6 +279,49 @@ def synth_paste(phi, sel, coef, iterations: int, idx, out, *, idx_ptr=None, n_sh
     _check(lib.fase_synth_paste(_ptr(phi), _ld(phi), _ptr(sel), _ptr(coef), _ld(sel), iterations,
                                 B, _ptr(idx_ptr), _ptr(idx), n_shared, _ptr(dst), _ptr(out),
                                 ldout, _stream(out)))
+
+
+def frame_areas(frame, grid, tile: int, support: int, corners, base_w, X) -> None:
+    import torch
+
+    lib = load()
+    _require(frame, "frame", torch.float64, 2)
+    _require(grid, "grid", torch.uint8, 2)
+    _require(corners, "corners", torch.int32, 2)
+    _require(base_w, "base_w", torch.float64, 1)
+    _require(X, "X", torch.float64, 2)
+    H, W = frame.shape
+    _check(lib.fase_frame_areas(_ptr(frame), _ld(frame), _ptr(grid), _ld(grid), H, W, tile,
+                                support, _ptr(corners), corners.shape[0], _ptr(base_w), _ptr(X),
+                                _ld(X), _stream(X)))
+
+
+def frame_cells(grid, H: int, W: int, tile: int, support: int, corners, cell_rep, counts,
+                ids) -> None:
+    import torch
+
+    lib = load()
+    _require(grid, "grid", torch.uint8, 2)
+    _require(corners, "corners", torch.int32, 2)
+    _require(cell_rep, "cell_rep", torch.int32, 2)
+    _require(counts, "counts", torch.int32, 1)
+    _require(ids, "ids", torch.int32, 2)
+    _check(lib.fase_frame_cells(_ptr(grid), _ld(grid), H, W, tile, support, _ptr(corners),
+                                corners.shape[0], _ptr(cell_rep), cell_rep.shape[0],
+                                _ptr(counts), _ptr(ids), _ld(ids), _stream(ids)))
+
+
+def frame_paste(phi, sel, coef, iterations: int, grid, tile: int, support: int, corners,
+                out) -> None:
+    import torch
+
+    lib = load()
+    _require(phi, "phi", torch.float64, 2)
+    _require(out, "out", torch.float64, 2)
+    H, W = out.shape
+    _check(lib.fase_frame_paste(_ptr(phi), _ld(phi), _ptr(sel), _ptr(coef), _ld(sel), iterations,
+                                _ptr(grid), _ld(grid), H, W, tile, support, _ptr(corners),
+                                corners.shape[0], _ptr(out), _ld(out), _stream(out)))
 
 
 def l2_flush(buf) -> None:

@@ -3,12 +3,27 @@
 The reference conceals an image tile by tile (``pkg/src/fase/conceal.py:111-245``):
 area = tile +- support, weight from every lost pixel inside the area, FaSE,
 then only the tile's own lost pixels are pasted back (``conceal.py:144-148``).
-Here all lossy tiles of a frame form ONE batch: fixed-size areas (out-of-frame
-samples are masked as unavailable, BASELINE config 2: "lost and unavailable
-samples set to zero"), chunked per-block tables, one recursion launch, and one
-synthesis kernel that pastes straight into the device frame. Interior tiles
-give exactly the reference's per-tile result; border tiles differ from the
-reference's *clipped* areas by design.
+Here all lossy tiles of a frame form ONE batch with fixed-size areas
+(out-of-frame samples are unavailable, BASELINE config 2: "lost and
+unavailable samples set to zero"). Interior tiles give exactly the reference's
+per-tile result; border tiles differ from the reference's *clipped* areas by
+design.
+
+``FrameEngine`` is the device pipeline for the usual case of whole-tile
+(macroblock) losses. Because every area sits at the same offset to the tile
+grid, the area splits into the same *cells* (rectangles cut by tile lines and
+frame edges) for every block, and each cell is entirely available or entirely
+unavailable in any block. So the tables are frame-independent:
+- G0 is the table of the weight without the own tile;
+- C_c is the table of cell c alone.
+A block's table is G0 - sum of its unavailable cells' tables, applied row by row
+inside the recursion kernel. Per frame, only kernels run:
+1. area extraction;
+2. per-block cell lists;
+3. normalizers;
+4. the DMMA GEMM for the initial products;
+5. the recursion;
+6. paste into the frame.
 """
 
 from __future__ import annotations
@@ -21,7 +36,8 @@ from . import _native
 from .dictionary import Dictionary, parse_dict_spec
 from .errors import ParameterError, ShapeError
 from .fast import ChunkedTables, fase_extrapolate_batch, resolve_device
-from .grid import ExtrapConfig, as_mask, psnr_over_region
+from .grid import ExtrapConfig, as_mask, base_weight, psnr_over_region
+from .model import BatchResult
 from .workloads import frame_areas
 
 REPORT_SCHEMA = "fase-b200-conceal-report/1"
@@ -37,8 +53,144 @@ def lossy_tiles(lost: np.ndarray, block: tuple[int, int]) -> np.ndarray:
     return np.stack([r * bh, c * bw], axis=1).astype(np.int64)
 
 
+def tile_grid(lost: np.ndarray, tile: int):
+    """Tile loss grid (Ty, Tx) uint8 if losses are whole full tiles, else None."""
+    h, w = lost.shape
+    ty, tx = h // tile, w // tile
+    full = lost[: ty * tile, : tx * tile].reshape(ty, tile, tx, tile)
+    anyl = full.any(axis=(1, 3))
+    if not np.array_equal(full.all(axis=(1, 3)), anyl):
+        return None
+    if lost[ty * tile:, :].any() or lost[:, tx * tile:].any():
+        return None
+    return anyl.astype(np.uint8)
+
+
+def _cuts(n: int, tile: int, support: int, area: int) -> list[int]:
+    """Area coordinates where the tile grid or a frame edge crosses, for any tile row."""
+    cuts = {0, area}
+    for i in range(1, area):
+        if (i - support) % tile == 0:
+            cuts.add(i)
+    for r0 in range(0, (n // tile) * tile, tile):
+        for edge in (support - r0, n - r0 + support):
+            if 0 < edge < area:
+                cuts.add(edge)
+    return sorted(cuts)
+
+
+class FrameEngine:
+    """Device pipeline concealing the lossy tiles of frames of one geometry."""
+
+    def __init__(self, dictionary: Dictionary, frame_shape: tuple[int, int], tile: int,
+                 support: int, config: ExtrapConfig = ExtrapConfig(), device=None):
+        import torch
+
+        self.device = dev = resolve_device(device)
+        a = tile + 2 * support
+        if dictionary.shape != (a, a):
+            raise ShapeError(f"dictionary area {dictionary.shape} vs extrapolation area {(a, a)}")
+        if not dictionary.is_real:
+            from .errors import UnsupportedDictionaryError
+            raise UnsupportedDictionaryError("complex-valued dictionaries are not supported on the GPU path")
+        self.dictionary, self.config = dictionary, config
+        self.H, self.W = frame_shape
+        self.tile, self.support, self.A = tile, support, a
+        K, M = len(dictionary), a * a
+        self.K, self.M = K, M
+        rows = _cuts(self.H, tile, support, a)
+        cols = _cuts(self.W, tile, support, a)
+        cells = [(i0, i1, j0, j1) for i0, i1 in zip(rows[:-1], rows[1:])
+                 for j0, j1 in zip(cols[:-1], cols[1:])]
+        own = [c for c in cells if c[0] >= support and c[1] <= support + tile
+               and c[2] >= support and c[3] <= support + tile]
+        self.cells = [c for c in cells if c not in own]
+        base = base_weight(a, a, config.rho_hat)
+        w0 = base.copy()
+        w0[support:support + tile, support:support + tile] = 0.0
+        self.phi = phi = dictionary.device_matrix(dev)
+        ld = dictionary.ld
+        from .fast import _device_vector, _gram_on_device
+        t0 = time.perf_counter()
+        self.G0 = _gram_on_device(phi, _device_vector(w0.ravel(), ld, dev), K, M, dev)
+        ldg = self.G0.shape[1]
+        self.tables = torch.zeros((max(len(self.cells), 1), K, ldg), dtype=torch.float64, device=dev)
+        flat_base = base.ravel()
+        for c, (i0, i1, j0, j1) in enumerate(self.cells):
+            ii, jj = np.meshgrid(np.arange(i0, i1), np.arange(j0, j1), indexing="ij")
+            samples = (ii * a + jj).ravel()
+            cols_t = torch.from_numpy(samples.astype(np.int64)).to(dev)
+            width = samples.size + (samples.size & 1)
+            sub = torch.zeros((K, width), dtype=torch.float64, device=dev)
+            sub[:, : samples.size] = phi.index_select(1, cols_t)
+            wj = torch.zeros(width, dtype=torch.float64, device=dev)
+            wj[: samples.size] = torch.from_numpy(flat_base[samples]).to(dev)
+            _native.gram(sub, wj, K, samples.size, self.tables[c])
+        torch.cuda.current_stream(dev).synchronize()
+        self.table_seconds = time.perf_counter() - t0
+        self.stride = self.tables[0].numel()
+        self.cell_rep = torch.tensor([[c[0], c[2]] for c in self.cells] or [[0, 0]],
+                                     dtype=torch.int32, device=dev)
+        self.base_w = torch.from_numpy(flat_base.copy()).to(dev)
+        self._buf = {}
+
+    def _buffers(self, L: int):
+        import torch
+
+        if L not in self._buf:
+            dev, K, I = self.device, self.K, self.config.iterations
+            ldx = self.M + (self.M & 1)
+            self._buf = {L: dict(
+                X=torch.empty((L, ldx), dtype=torch.float64, device=dev),
+                R0=torch.empty((L, K + (K & 1)), dtype=torch.float64, device=dev),
+                D=torch.empty((L, self.G0.shape[1]), dtype=torch.float64, device=dev),
+                alive=torch.empty(L, dtype=torch.int32, device=dev),
+                counts=torch.empty(L, dtype=torch.int32, device=dev),
+                ids=torch.zeros((L, max(len(self.cells), 1)), dtype=torch.int32, device=dev),
+                sel=torch.empty((L, I), dtype=torch.int32, device=dev),
+                proj=torch.empty((L, I), dtype=torch.float64, device=dev),
+                coef=torch.empty((L, I), dtype=torch.float64, device=dev),
+            )}
+        return self._buf[L]
+
+    launches_per_frame = 6  # areas, cells, normalizers, gemm, iterate, paste
+
+    def run(self, frame, grid, corners, out=None) -> BatchResult:
+        """Conceal one frame: ``frame`` (H, W) float64, ``grid`` (H/tile, W/tile)
+        uint8 tile loss map, ``corners`` (L, 2) int32 lossy-tile corners, all on
+        the device. The restored frame is written to ``out`` (default: a copy of
+        ``frame``). Enqueued on the current stream; no host synchronization."""
+        L = int(corners.shape[0])
+        if out is None:
+            out = frame.clone()
+        if L == 0:
+            return BatchResult(selected=None, projections=None, coefficients=None, patched=out)
+        b = self._buffers(L)
+        cfg, K = self.config, self.K
+        _native.frame_areas(frame, grid, self.tile, self.support, corners, self.base_w, b["X"])
+        _native.frame_cells(grid, self.H, self.W, self.tile, self.support, corners, self.cell_rep,
+                            b["counts"], b["ids"])
+        _native.block_normalizers(self.G0, self.tables, self.stride, b["counts"], b["ids"], K,
+                                  b["D"], b["alive"])
+        _native.gemm_nt(b["X"][:, : self.M], self.phi[:, : self.M], b["R0"])
+        _native.iterate(self.G0, b["D"], b["R0"], K, cfg.iterations, cfg.gamma, b["sel"], b["proj"],
+                        b["coef"], chunk_tables=self.tables, chunk_stride=self.stride,
+                        chunk_count=b["counts"], chunk_ids=b["ids"])
+        _native.frame_paste(self.phi, b["sel"], b["coef"], cfg.iterations, grid, self.tile,
+                            self.support, corners, out)
+        return BatchResult(selected=b["sel"], projections=b["proj"], coefficients=b["coef"],
+                           patched=out, dictionary=self.dictionary,
+                           shape=(self.A, self.A))
+
+    def dead_blocks(self) -> int:
+        """Blocks of the last run whose every atom was degenerate (syncs)."""
+        for b in self._buf.values():
+            return int((b["alive"] == 0).sum().item())
+        return 0
+
+
 class FramePlan:
-    """Device-side geometry of one damaged frame: areas, masks, paste targets."""
+    """Host-built geometry for arbitrary (not tile-aligned) loss masks."""
 
     def __init__(self, image, lost, block: int, support: int, device):
         import torch
@@ -61,7 +213,6 @@ class FramePlan:
         self.signals = torch.from_numpy(signals).to(device)
         a = block + 2 * support
         h, w = self.shape
-        # paste targets: each tile's own lost pixels (area index -> frame index)
         idx, dst, ptr = [], [], [0]
         for (r0, c0) in self.corners:
             tile = self.lost[r0:r0 + block, c0:c0 + block]
@@ -81,50 +232,60 @@ class FramePlan:
 
 def conceal_frame(image, lost_mask, *, dictionary: Dictionary | None = None,
                   dict_spec: str = "union:dct+had", config: ExtrapConfig = ExtrapConfig(),
-                  block: int = 16, support: int = 16, reference=None, tables=None,
-                  plan: FramePlan | None = None, device=None):
+                  block: int = 16, support: int = 16, reference=None, engine=None, device=None):
     """Conceal every lossy ``block`` x ``block`` tile of a frame on the GPU.
 
-    Returns (restored float64 frame as a device tensor, report dict). Pass a
-    prebuilt ``plan`` / ``tables`` to reuse geometry across frames with the
-    same loss pattern.
+    Whole-tile losses take the FrameEngine pipeline (pass ``engine`` to reuse
+    its frame-independent tables across frames); other masks take the general
+    per-block path. Returns (restored float64 frame as a device tensor, report).
     """
     import torch
 
     dev = resolve_device(device)
     t0 = time.perf_counter()
-    if plan is None:
-        plan = FramePlan(image, lost_mask, block, support, dev)
-    a = plan.block + 2 * plan.support
+    img = np.asarray(image, dtype=np.float64)
+    lost = as_mask(lost_mask)
+    if img.shape != lost.shape or img.ndim != 2:
+        raise ShapeError(f"image {img.shape} vs mask {lost.shape}")
+    a = block + 2 * support
     if dictionary is None:
         dictionary = parse_dict_spec(dict_spec, a, a)
-    if dictionary.shape != (a, a):
-        raise ShapeError(f"dictionary area {dictionary.shape} vs extrapolation area {(a, a)}")
-    out = plan.frame.clone()
-    if plan.n_blocks:
-        if tables is None:
-            tables = ChunkedTables(dictionary, plan.masks, config.rho_hat, dev)
-        res = fase_extrapolate_batch(plan.signals, plan.masks, dictionary, tables, config,
-                                     patch=False, device=dev)
-        phi = dictionary.device_matrix(dev)
-        _native.synth_paste(phi, res.selected, res.coefficients, config.iterations, plan.idx,
-                            out.view(-1), idx_ptr=plan.ptr, dst=plan.dst)
+    grid = tile_grid(lost, block)
+    damaged = img.copy()
+    damaged[lost] = 0.0
+    if grid is not None:
+        if engine is None:
+            engine = FrameEngine(dictionary, img.shape, block, support, config, dev)
+        corners = lossy_tiles(lost, (block, block)).astype(np.int32)
+        frame = torch.from_numpy(damaged).to(dev)
+        res = engine.run(frame, torch.from_numpy(grid).to(dev), torch.from_numpy(corners).to(dev))
+        out = res.patched
+        n_blocks = len(corners)
     else:
+        plan = FramePlan(img, lost, block, support, dev)
+        out = plan.frame.clone()
+        n_blocks = plan.n_blocks
         res = None
+        if plan.n_blocks:
+            tables = ChunkedTables(dictionary, plan.masks, config.rho_hat, dev)
+            res = fase_extrapolate_batch(plan.signals, plan.masks, dictionary, tables, config,
+                                         patch=False, device=dev)
+            _native.synth_paste(dictionary.device_matrix(dev), res.selected, res.coefficients,
+                                config.iterations, plan.idx, out.view(-1), idx_ptr=plan.ptr,
+                                dst=plan.dst)
     torch.cuda.current_stream(dev).synchronize()
     report = {
         "schema": REPORT_SCHEMA,
-        "image": {"height": plan.shape[0], "width": plan.shape[1]},
-        "settings": {"dict": dict_spec if dictionary is None else dictionary.families[0],
-                     "iterations": config.iterations, "gamma": config.gamma,
-                     "rho": config.rho_hat, "block": [plan.block, plan.block],
-                     "support": plan.support},
-        "lost_pixels": int(plan.lost.sum()),
-        "blocks": int(plan.n_blocks),
+        "image": {"height": img.shape[0], "width": img.shape[1]},
+        "settings": {"dict": dict_spec, "iterations": config.iterations, "gamma": config.gamma,
+                     "rho": config.rho_hat, "block": [block, block], "support": support,
+                     "pipeline": "frame-engine" if grid is not None else "per-block-masks"},
+        "lost_pixels": int(lost.sum()),
+        "blocks": int(n_blocks),
         "seconds": time.perf_counter() - t0,
     }
-    if reference is not None and plan.lost.any():
+    if reference is not None and lost.any():
         report["psnr_db"] = psnr_over_region(np.asarray(reference, dtype=np.float64),
-                                             out.cpu().numpy(), plan.lost)
+                                             out.cpu().numpy(), lost)
     report["result"] = res
     return out, report

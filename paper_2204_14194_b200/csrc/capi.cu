@@ -107,14 +107,13 @@ __device__ __forceinline__ double chunk_diag(const double* G0, int64_t ldg, cons
 
 __global__ void __launch_bounds__(kNormThreads) block_normalizers_kernel(
     const double* __restrict__ G0, int64_t ldg, const double* __restrict__ tabs, int64_t stride,
-    const int32_t* __restrict__ ptr, const int32_t* __restrict__ ids, int K,
+    const int32_t* __restrict__ counts, const int32_t* __restrict__ ids, int64_t list_ld, int K,
     double* __restrict__ D, int64_t ldd, int32_t* n_alive) {
   __shared__ double s_m[kNormThreads / 32];
   __shared__ int s_n[kNormThreads / 32];
   const int b = blockIdx.x;
-  const int lo = ptr ? ptr[b] : 0;
-  const int nch = ptr ? ptr[b + 1] - lo : 0;
-  const int32_t* my = ids ? ids + lo : nullptr;
+  const int nch = counts ? counts[b] : 0;
+  const int32_t* my = ids ? ids + static_cast<int64_t>(b) * list_ld : nullptr;
   double m = 0.0;
   for (int k = threadIdx.x; k < K; k += kNormThreads)
     m = fmax(m, chunk_diag(G0, ldg, tabs, stride, my, nch, k));
@@ -162,8 +161,10 @@ __global__ void __launch_bounds__(kSynthThreads) synth_paste_kernel(
       }
       __syncthreads();
       if (i < n) {
-        for (int t = 0; t < len; ++t)
+        for (int t = 0; t < len; ++t) {
+          if (s_sel[t] < 0) break;  // block stopped: every atom degenerate
           g = add_rn(g, mul_rn(s_coef[t], __ldg(phi + static_cast<int64_t>(s_sel[t]) * ldphi + m)));
+        }
       }
     }
     if (i < n) out[(dst ? dst[lo + i] : static_cast<int64_t>(m)) + static_cast<int64_t>(b) * ldout] = g;
@@ -215,20 +216,22 @@ extern "C" int fase_gram_finish(const double* G, int64_t ldg, int K, double* D, 
 }
 
 extern "C" int fase_block_normalizers(const double* G0, int64_t ldg, const double* chunk_tables,
-                                      int64_t chunk_stride, const int32_t* chunk_ptr,
-                                      const int32_t* chunk_ids, int K, int B, double* D,
-                                      int64_t ldd, int32_t* n_alive, void* stream) {
+                                      int64_t chunk_stride, const int32_t* chunk_count,
+                                      const int32_t* chunk_ids, int64_t chunk_list_ld, int K,
+                                      int B, double* D, int64_t ldd, int32_t* n_alive,
+                                      void* stream) {
   if (K < 1 || B < 0 || ldg < K || ldd < K || !G0 || !D) {
     set_error("fase_block_normalizers: bad operand (K=%d, B=%d)", K, B);
     return FASE_ERR_SHAPE;
   }
-  if (chunk_ptr && (!chunk_ids || !chunk_tables)) {
+  if (chunk_count && (!chunk_ids || !chunk_tables)) {
     set_error("fase_block_normalizers: chunk list without chunk tables");
     return FASE_ERR_SHAPE;
   }
   if (B == 0) return FASE_OK;
   block_normalizers_kernel<<<B, kNormThreads, 0, as_stream(stream)>>>(
-      G0, ldg, chunk_tables, chunk_stride, chunk_ptr, chunk_ids, K, D, ldd, n_alive);
+      G0, ldg, chunk_tables, chunk_stride, chunk_count, chunk_ids, chunk_list_ld, K, D, ldd,
+      n_alive);
   return check_launch("fase_block_normalizers");
 }
 

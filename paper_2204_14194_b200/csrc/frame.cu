@@ -1,0 +1,186 @@
+// Frame concealment kernels: area extraction, per-block cell lists, paste.
+//
+// Reference per-tile path: pkg/src/fase/conceal.py:111-148 -- area = tile +-
+// support, weight from every lost pixel in the area, FaSE, then only the
+// tile's own lost pixels are written back. Here every lossy tile of a frame is
+// one block of a batch; areas have a fixed size A = tile + 2*support and
+// out-of-frame samples count as unavailable (BASELINE configs 2/3).
+//
+// Losses are whole tiles (macroblocks), described by a tile-level loss grid
+// (Ty x Tx bytes); a pixel (y, x) is lost iff it lies in a full tile whose grid
+// entry is set. Pixels past the last full tile row / column (e.g. the 8-row
+// bottom strip of 1080p at 16-pixel tiles) are kept.
+
+#include "common.cuh"
+
+namespace fase {
+namespace {
+
+struct FrameGeom {
+  int H, W, tile, support, A, Ty, Tx;
+};
+
+// 1 = unavailable (outside the frame or lost), 0 = support sample
+__device__ __forceinline__ int unavailable(const FrameGeom& g, const uint8_t* __restrict__ grid,
+                                           int64_t ldgrid, int y, int x) {
+  if (y < 0 || x < 0 || y >= g.H || x >= g.W) return 1;
+  const int ty = y / g.tile, tx = x / g.tile;
+  if (ty >= g.Ty || tx >= g.Tx) return 0;
+  return grid[ty * ldgrid + tx] != 0;
+}
+
+// X[b, i*A + j] = frame(y, x) * base_w[i*A + j] on support samples, 0 elsewhere
+// (the reference's s * w with s = 0 on lost pixels and w = 0 off support),
+// y = r0 - support + i, x = c0 - support + j. One rounded multiply per sample.
+__global__ void frame_areas_kernel(FrameGeom g, const double* __restrict__ frame, int64_t ldf,
+                                   const uint8_t* __restrict__ grid, int64_t ldgrid,
+                                   const int32_t* __restrict__ corners, int L,
+                                   const double* __restrict__ base_w, double* __restrict__ X,
+                                   int64_t ldx) {
+  const int M = g.A * g.A;
+  const int64_t total = static_cast<int64_t>(L) * M;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int b = static_cast<int>(idx / M);
+    const int m = static_cast<int>(idx - static_cast<int64_t>(b) * M);
+    const int i = m / g.A, j = m - (m / g.A) * g.A;
+    const int y = corners[2 * b] - g.support + i;
+    const int x = corners[2 * b + 1] - g.support + j;
+    double v = 0.0;
+    if (!unavailable(g, grid, ldgrid, y, x)) v = mul_rn(frame[y * ldf + x], base_w[m]);
+    X[b * ldx + m] = v;
+  }
+}
+
+// counts[b] / ids[b, :] = the candidate cells (area rectangles, given by one
+// representative sample each) that are unavailable for block b, in cell order.
+__global__ void frame_cells_kernel(FrameGeom g, const uint8_t* __restrict__ grid, int64_t ldgrid,
+                                   const int32_t* __restrict__ corners, int L,
+                                   const int32_t* __restrict__ cell_rep, int n_cells,
+                                   int32_t* __restrict__ counts, int32_t* __restrict__ ids,
+                                   int64_t ids_ld) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < L; b += gridDim.x * blockDim.x) {
+    const int y0 = corners[2 * b] - g.support, x0 = corners[2 * b + 1] - g.support;
+    int n = 0;
+    for (int c = 0; c < n_cells; ++c) {
+      if (unavailable(g, grid, ldgrid, y0 + cell_rep[2 * c], x0 + cell_rep[2 * c + 1]))
+        ids[b * ids_ld + n++] = c;
+    }
+    counts[b] = n;
+  }
+}
+
+// g = sum_t coef_t * phi[sel_t, m] (selection order; SparseModel.materialize,
+// reference.py:120-125) for the tile's own lost pixels, written into the frame
+// (conceal.py:144-148).
+constexpr int kPasteThreads = 256;
+constexpr int kPasteChunk = 1024;
+
+__global__ void __launch_bounds__(kPasteThreads) frame_paste_kernel(
+    FrameGeom g, const double* __restrict__ phi, int64_t ldphi, const int32_t* __restrict__ sel,
+    const double* __restrict__ coef, int64_t ldo, int I, const uint8_t* __restrict__ grid,
+    int64_t ldgrid, const int32_t* __restrict__ corners, double* __restrict__ out, int64_t ldout) {
+  __shared__ int32_t s_sel[kPasteChunk];
+  __shared__ double s_coef[kPasteChunk];
+  const int b = blockIdx.x;
+  const int r0 = corners[2 * b], c0 = corners[2 * b + 1];
+  const int n = g.tile * g.tile;
+  const int32_t* my_sel = sel + static_cast<int64_t>(b) * ldo;
+  const double* my_coef = coef + static_cast<int64_t>(b) * ldo;
+  for (int base = 0; base < n; base += kPasteThreads) {
+    const int p = base + threadIdx.x;
+    const int i = p / g.tile, j = p - (p / g.tile) * g.tile;
+    const bool mine = p < n && r0 + i < g.H && c0 + j < g.W &&
+                      unavailable(g, grid, ldgrid, r0 + i, c0 + j);
+    const int m = (g.support + i) * g.A + g.support + j;
+    double acc = 0.0;
+    for (int t0 = 0; t0 < I; t0 += kPasteChunk) {
+      const int len = min(kPasteChunk, I - t0);
+      __syncthreads();
+      for (int t = threadIdx.x; t < len; t += kPasteThreads) {
+        s_sel[t] = my_sel[t0 + t];
+        s_coef[t] = my_coef[t0 + t];
+      }
+      __syncthreads();
+      if (mine) {
+        for (int t = 0; t < len; ++t) {
+          if (s_sel[t] < 0) break;  // block stopped: every atom degenerate
+          acc = add_rn(acc, mul_rn(s_coef[t], __ldg(phi + static_cast<int64_t>(s_sel[t]) * ldphi + m)));
+        }
+      }
+    }
+    if (mine) out[static_cast<int64_t>(r0 + i) * ldout + c0 + j] = acc;
+  }
+}
+
+bool geom_ok(const FrameGeom& g) {
+  return g.H > 0 && g.W > 0 && g.tile > 0 && g.support >= 0 && g.A == g.tile + 2 * g.support &&
+         g.Ty == g.H / g.tile && g.Tx == g.W / g.tile;
+}
+
+}  // namespace
+}  // namespace fase
+
+using namespace fase;
+
+extern "C" int fase_frame_areas(const double* frame, int64_t ldf, const uint8_t* grid,
+                                int64_t ldgrid, int H, int W, int tile, int support,
+                                const int32_t* corners, int L, const double* base_w, double* X,
+                                int64_t ldx, void* stream) {
+  const FrameGeom g{H, W, tile, support, tile + 2 * support, H / tile, W / tile};
+  if (!geom_ok(g) || L < 0 || ldf < W || ldgrid < g.Tx || ldx < g.A * g.A) {
+    set_error("fase_frame_areas: bad geometry (H=%d W=%d tile=%d support=%d)", H, W, tile, support);
+    return FASE_ERR_SHAPE;
+  }
+  if (L == 0) return FASE_OK;
+  if (!frame || !grid || !corners || !base_w || !X) {
+    set_error("fase_frame_areas: null pointer");
+    return FASE_ERR_SHAPE;
+  }
+  const int64_t total = static_cast<int64_t>(L) * g.A * g.A;
+  const int64_t blocks = (total + 255) / 256;
+  frame_areas_kernel<<<static_cast<unsigned>(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0,
+                       as_stream(stream)>>>(g, frame, ldf, grid, ldgrid, corners, L, base_w, X,
+                                            ldx);
+  return check_launch("fase_frame_areas");
+}
+
+extern "C" int fase_frame_cells(const uint8_t* grid, int64_t ldgrid, int H, int W, int tile,
+                                int support, const int32_t* corners, int L,
+                                const int32_t* cell_rep, int n_cells, int32_t* counts,
+                                int32_t* ids, int64_t ids_ld, void* stream) {
+  const FrameGeom g{H, W, tile, support, tile + 2 * support, H / tile, W / tile};
+  if (!geom_ok(g) || L < 0 || n_cells < 0 || ids_ld < (n_cells > 0 ? n_cells : 1) ||
+      ldgrid < g.Tx) {
+    set_error("fase_frame_cells: bad geometry or list stride");
+    return FASE_ERR_SHAPE;
+  }
+  if (L == 0) return FASE_OK;
+  if (!grid || !corners || !counts || !ids || (n_cells && !cell_rep)) {
+    set_error("fase_frame_cells: null pointer");
+    return FASE_ERR_SHAPE;
+  }
+  frame_cells_kernel<<<(L + 255) / 256, 256, 0, as_stream(stream)>>>(
+      g, grid, ldgrid, corners, L, cell_rep, n_cells, counts, ids, ids_ld);
+  return check_launch("fase_frame_cells");
+}
+
+extern "C" int fase_frame_paste(const double* phi, int64_t ldphi, const int32_t* sel,
+                                const double* coef, int64_t ldo, int I, const uint8_t* grid,
+                                int64_t ldgrid, int H, int W, int tile, int support,
+                                const int32_t* corners, int L, double* out, int64_t ldout,
+                                void* stream) {
+  const FrameGeom g{H, W, tile, support, tile + 2 * support, H / tile, W / tile};
+  if (!geom_ok(g) || L < 0 || I < 1 || ldo < I || ldout < W || ldgrid < g.Tx) {
+    set_error("fase_frame_paste: bad geometry or sizes");
+    return FASE_ERR_SHAPE;
+  }
+  if (L == 0) return FASE_OK;
+  if (!phi || !sel || !coef || !grid || !corners || !out) {
+    set_error("fase_frame_paste: null pointer");
+    return FASE_ERR_SHAPE;
+  }
+  frame_paste_kernel<<<L, kPasteThreads, 0, as_stream(stream)>>>(
+      g, phi, ldphi, sel, coef, ldo, I, grid, ldgrid, corners, out, ldout);
+  return check_launch("fase_frame_paste");
+}

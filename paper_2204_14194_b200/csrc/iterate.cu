@@ -91,9 +91,8 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
   const int32_t* cids = nullptr;
   int nch = 0;
   if (kChunked) {
-    const int lo = a.chunk_ptr[b];
-    nch = a.chunk_ptr[b + 1] - lo;
-    cids = a.chunk_ids + lo;
+    nch = a.chunk_count[b];
+    cids = a.chunk_ids + static_cast<int64_t>(b) * a.chunk_list_ld;
   }
 
   double r[EP][2];
@@ -170,6 +169,14 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
       const unsigned bl = __reduce_max_sync(0xffffffffu, h == bh ? l : 0u);
       guess = __reduce_min_sync(0xffffffffu, (h == bh && l == bl) ? sa : kNone);
       top_key = (static_cast<long long>(bh) << 32) | bl;
+    }
+    if (top_key < 0) {  // every atom degenerate (NoSelectableAtomError): mark and stop
+      for (int k = it + t; k < a.I; k += NT) {
+        sel[k] = -1;
+        proj[k] = 0.0;
+        coef[k] = 0.0;
+      }
+      return;
     }
     // stage the likely selection's row in shared memory (one TMA bulk copy)
     // while the tie pass and the second barrier run
@@ -382,12 +389,12 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
     set_error("fase_iterate: bad operand (null, misaligned, odd or short leading dimension)");
     return FASE_ERR_SHAPE;
   }
-  if (a.chunk_ptr && (!a.chunk_ids || !a.chunk_tables || !aligned16(a.chunk_tables) ||
+  if (a.chunk_count && (!a.chunk_ids || !a.chunk_tables || !aligned16(a.chunk_tables) ||
                       (a.chunk_stride & 1))) {
     set_error("fase_iterate: chunk tables given without ids / aligned storage");
     return FASE_ERR_SHAPE;
   }
-  if (a.chunk_ptr && a.R_log) {
+  if (a.chunk_count && a.R_log) {
     set_error("fase_iterate: R_log recording is not available with chunked tables");
     return FASE_ERR_UNSUPPORTED;
   }
@@ -397,12 +404,12 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
               fase_max_atoms());
     return FASE_ERR_UNSUPPORTED;
   }
-  if (a.ldg < v->nt * v->ept || (a.chunk_ptr && a.chunk_stride < a.ldg * a.K)) {
+  if (a.ldg < v->nt * v->ept || (a.chunk_count && a.chunk_stride < a.ldg * a.K)) {
     set_error("fase_iterate: table rows must be zero-padded to fase_table_ld(K)=%d (ldg=%lld)",
               v->nt * v->ept, static_cast<long long>(a.ldg));
     return FASE_ERR_SHAPE;
   }
-  KernelFn fn = a.chunk_ptr ? v->chunked : (a.R_log ? v->record : v->plain);
+  KernelFn fn = a.chunk_count ? v->chunked : (a.R_log ? v->record : v->plain);
   const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2) * (v->dsmem ? 2 : 1);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));

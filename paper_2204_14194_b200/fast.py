@@ -330,9 +330,12 @@ class ChunkedTables:
             wj = torch.zeros(width, dtype=torch.float64, device=device)
             wj[: len(samples)] = torch.from_numpy(base[samples]).to(device)
             _native.gram(sub, wj, K, len(samples), self.tables[j])
-        self.ptr = torch.from_numpy(self.plan.ptr).to(device)
-        self.ids = torch.from_numpy(self.plan.ids if self.plan.ids.size else
-                                    np.zeros(1, np.int32)).to(device)
+        counts = np.diff(self.plan.ptr).astype(np.int32)
+        lists = np.zeros((len(counts), max(1, int(counts.max(initial=0)))), dtype=np.int32)
+        for b in np.flatnonzero(counts):
+            lists[b, : counts[b]] = self.plan.ids[self.plan.ptr[b]:self.plan.ptr[b + 1]]
+        self.counts = torch.from_numpy(counts).to(device)
+        self.ids = torch.from_numpy(lists).to(device)
         self.masks = masks
         self.key = (dictionary.content_hash(), masks.shape, hashlib.blake2b(
             np.packbits(masks).tobytes(), digest_size=16).hexdigest(), rho_hat)
@@ -426,12 +429,12 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
         D = torch.empty((B, G.shape[1]), dtype=torch.float64, device=dev)
         alive = torch.empty(B, dtype=torch.int32, device=dev)
         stride = tables.tables[0].numel()
-        _native.block_normalizers(G, tables.tables, stride, tables.ptr, tables.ids, K, D, alive)
+        _native.block_normalizers(G, tables.tables, stride, tables.counts, tables.ids, K, D, alive)
         dead = torch.nonzero(alive == 0)
         if dead.numel():
             raise NoSelectableAtomError(f"block {int(dead[0, 0])}: every atom has zero weighted energy")
-        chunk_args = dict(chunk_tables=tables.tables, chunk_stride=stride, chunk_ptr=tables.ptr,
-                          chunk_ids=tables.ids)
+        chunk_args = dict(chunk_tables=tables.tables, chunk_stride=stride,
+                          chunk_count=tables.counts, chunk_ids=tables.ids)
         base = torch.from_numpy(base_weight(*dictionary.shape, config.rho_hat).ravel()).to(dev)
         mdev = torch.from_numpy(mask.reshape(B, -1)).to(dev)
         W = torch.zeros((B, F.shape[1]), dtype=torch.float64, device=dev)

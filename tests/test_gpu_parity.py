@@ -310,3 +310,58 @@ def test_empty_batch_and_odd_area():
         ref = orc.extrapolate_block(sig[b], mask, vals, 0.5, 12, 0.8)
         assert np.array_equal(res.selected[b].cpu().numpy(), ref["selected"])
         assert rel_dev(res.coefficients[b].cpu().numpy(), ref["coefficients"].real) < 1e-12
+
+
+# ----------------------------------------------------------------- frame engine
+
+
+@pytest.mark.parametrize("cid", [3, 2])
+def test_frame_engine_against_reference_blocks(golden_dir, cid):
+    """Whole-frame device pipeline (areas, cell lists, normalizers, GEMM,
+    chunked recursion, paste) against the reference's per-block results."""
+    from paper_2204_14194_b200.conceal import FrameEngine, lossy_tiles, tile_grid
+
+    z = np.load(golden_dir / f"c{cid}_blocks.npz")
+    w8 = wl.WORKLOADS[cid]
+    case = wl.frame_case(w8)
+    d = w8.dictionary()
+    eng = FrameEngine(d, case.frame.shape, case.mb, case.support, w8.config, device=DEV)
+    grid = torch.from_numpy(tile_grid(case.lost, case.mb)).to(DEV)
+    corners_h = lossy_tiles(case.lost, (case.mb, case.mb)).astype(np.int32)
+    assert np.array_equal(corners_h, case.corners)
+    damaged = torch.from_numpy(case.damaged()).to(DEV)
+    res = eng.run(damaged, grid, torch.from_numpy(corners_h).to(DEV))
+    torch.cuda.synchronize()
+    assert eng.dead_blocks() == 0
+    out = res.patched.cpu().numpy()
+    # untouched outside the lost pixels
+    assert np.array_equal(out[~case.lost], case.damaged()[~case.lost])
+    signals, masks = wl.frame_areas(case.damaged(), case.lost, case.corners, case.mb, case.support)
+    vals = d.real_values().reshape(len(d), -1).astype(np.complex128)
+    s, mb = case.support, case.mb
+    exact = 0
+    for b in z["blocks"]:
+        got = res.selected[b].cpu().numpy()
+        want = z[f"b{b}_selected"]
+
+        def metric_at(t, b=b):
+            wb = orc.weight_field(masks[b], w8.config.rho_hat)
+            tab = orc.gram(vals, wb)
+            r0 = orc.initial_products(signals[b], wb, vals)
+            _, _, _, log = orc.fase_run(r0, tab[0], tab[1], w8.config.gamma, t, record=True)
+            return metric_fn(r0, tab[1], log)(t)
+
+        v = compare_selection(got, want, metric_at)
+        assert v.ok, f"block {b}: diverged at {v.stop}, gap {v.gap}"
+        k = v.stop
+        assert rel_dev(res.coefficients[b].cpu().numpy()[:k], z[f"b{b}_coefficients"][:k]) < COEF_REL
+        if v.exact:
+            exact += 1
+            # own-tile lost pixels in the frame vs the reference's reconstruction
+            full = np.zeros(masks[b].shape)
+            full[masks[b]] = z[f"b{b}_patched_lost"]
+            r0_, c0_ = case.corners[b]
+            want_tile = full[s:s + mb, s:s + mb]
+            got_tile = out[r0_:r0_ + mb, c0_:c0_ + mb]
+            assert rel_dev(got_tile, want_tile) < COEF_REL
+    assert exact >= len(z["blocks"]) - 1
