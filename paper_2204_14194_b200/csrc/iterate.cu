@@ -42,6 +42,8 @@
 // chunk-list order, identical to fase_block_normalizers' diagonal.
 
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -335,15 +337,22 @@ struct Variant {
    fase_iterate_kernel<NT, EPT, MINB, DS, true, false>,                                  \
    fase_iterate_kernel<NT, EPT, MINB, DS, false, true>}
 // Ordered by capacity NT*EPT; the first variant that holds K is used.
-// 256-thread variants keep D in shared memory (3-5 CTAs per SM); the
+// 128/256-thread variants keep D in shared memory (3-6 CTAs per SM); the
 // 512-thread variants keep R and D in registers (4 registers per atom), which
 // caps K at 512 x 24.
 const Variant kVariants[] = {
     FASE_V(128, 2, 4, false),  FASE_V(128, 4, 4, false),  FASE_V(128, 8, 4, false),
-    FASE_V(256, 8, 5, true),   FASE_V(256, 10, 4, true),  FASE_V(256, 12, 3, true),
+    FASE_V(128, 16, 6, true),  FASE_V(256, 10, 4, true),  FASE_V(256, 12, 3, true),
     FASE_V(256, 14, 3, true),  FASE_V(256, 16, 3, true),  FASE_V(256, 18, 3, true),
     FASE_V(256, 20, 2, true),  FASE_V(512, 12, 1, false), FASE_V(512, 16, 1, false),
     FASE_V(512, 20, 1, false), FASE_V(512, 24, 1, false),
+};
+
+// Alternative shapes, selectable for measurement with FASE_ITERATE_VARIANT=NTxEPT
+// (must not exceed the default variant's capacity, which sizes the tables).
+const Variant kExtraVariants[] = {
+    FASE_V(256, 8, 5, true),
+    FASE_V(128, 36, 3, true),
 };
 #undef FASE_V
 
@@ -351,6 +360,21 @@ const Variant* pick_variant(int K) {
   for (const Variant& v : kVariants)
     if (v.nt * v.ept >= K) return &v;
   return nullptr;
+}
+
+const Variant* override_variant(int K, const Variant* dflt) {
+  const char* env = getenv("FASE_ITERATE_VARIANT");
+  if (!env || !dflt) return dflt;
+  int nt = 0, ept = 0;
+  if (sscanf(env, "%dx%d", &nt, &ept) != 2) return dflt;
+  auto match = [&](const Variant& v) {
+    return v.nt == nt && v.ept == ept && v.nt * v.ept >= K && v.nt * v.ept <= dflt->nt * dflt->ept;
+  };
+  for (const Variant& v : kVariants)
+    if (match(v)) return &v;
+  for (const Variant& v : kExtraVariants)
+    if (match(v)) return &v;
+  return dflt;
 }
 
 }  // namespace
@@ -398,7 +422,7 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
     set_error("fase_iterate: R_log recording is not available with chunked tables");
     return FASE_ERR_UNSUPPORTED;
   }
-  const Variant* v = pick_variant(a.K);
+  const Variant* v = override_variant(a.K, pick_variant(a.K));
   if (!v) {
     set_error("fase_iterate: K=%d exceeds the largest kernel variant (%d atoms)", a.K,
               fase_max_atoms());
