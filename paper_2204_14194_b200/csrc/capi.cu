@@ -160,12 +160,7 @@ __global__ void __launch_bounds__(kSynthThreads) synth_paste_kernel(
         s_coef[t] = my_coef[t0 + t];
       }
       __syncthreads();
-      if (i < n) {
-        for (int t = 0; t < len; ++t) {
-          if (s_sel[t] < 0) break;  // block stopped: every atom degenerate
-          g = add_rn(g, mul_rn(s_coef[t], __ldg(phi + static_cast<int64_t>(s_sel[t]) * ldphi + m)));
-        }
-      }
+      if (i < n) g = synth_terms(phi, ldphi, s_sel, s_coef, len, m, g);
     }
     if (i < n) out[(dst ? dst[lo + i] : static_cast<int64_t>(m)) + static_cast<int64_t>(b) * ldout] = g;
   }

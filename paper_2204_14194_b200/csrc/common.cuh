@@ -45,6 +45,19 @@ __device__ __forceinline__ long long warp_max_i64(long long v) {
   return (static_cast<long long>(mhi) << 32) | static_cast<long long>(mlo);
 }
 
+// g + sum_t coef[t] * phi[sel[t] * ldphi + m] for t ascending, stopping at the
+// first sel < 0 (a block whose atoms were all degenerate): the reference's
+// sequential summation order (SparseModel.materialize, reference.py:120-125).
+__device__ __forceinline__ double synth_terms(const double* __restrict__ phi, int64_t ldphi,
+                                              const int32_t* s_sel, const double* s_coef,
+                                              int len, int m, double g) {
+  for (int t = 0; t < len; ++t) {
+    if (s_sel[t] < 0) break;
+    g = __dadd_rn(g, __dmul_rn(s_coef[t], __ldg(phi + static_cast<int64_t>(s_sel[t]) * ldphi + m)));
+  }
+  return g;
+}
+
 __device__ __forceinline__ double2 ldg2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }

@@ -180,6 +180,43 @@ __global__ void __launch_bounds__(T::kThreads, T::kMinBlocks) dgemm_nt_kernel(co
   }
 }
 
+// Small batches (B <= kGemvMax, e.g. config 0's single block): one warp per
+// atom row streams phi[k, :] once and dots it with every block's weighted
+// signal (L2/L1-resident), instead of a GEMM tile that would be almost empty.
+constexpr int kGemvMax = 8;
+
+__global__ void gemv_rows_kernel(const double* __restrict__ X, int64_t ldx, int B,
+                                 const double* __restrict__ phi, int64_t ldphi, int K, int M,
+                                 double* __restrict__ R0, int64_t ldr) {
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  for (int k = blockIdx.x * warps + (threadIdx.x >> 5); k < K; k += gridDim.x * warps) {
+    double acc[kGemvMax];
+#pragma unroll
+    for (int b = 0; b < kGemvMax; ++b) acc[b] = 0.0;
+    const double* row = phi + static_cast<int64_t>(k) * ldphi;
+    for (int m = 2 * lane; m < M; m += 64) {
+      const double2 pv = ldg2(row + m);  // even leading dimensions: the pair exists
+      const bool pair = m + 1 < M;       // the odd tail's partner is never used
+#pragma unroll
+      for (int b = 0; b < kGemvMax; ++b) {
+        if (b < B) {
+          const double2 xv = ldg2(X + b * ldx + m);
+          acc[b] = fma(pv.x, xv.x, acc[b]);
+          if (pair) acc[b] = fma(pv.y, xv.y, acc[b]);
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < kGemvMax; ++b) {
+      double v = acc[b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && b < B) R0[b * ldr + k] = v;
+    }
+  }
+}
+
 // out[b*ldo + m] = x[b*ldx + m] * w[b*ldw + m]  (ldw == 0: one shared weight row);
 // one correctly rounded multiply per sample, 16-byte accesses.
 __global__ void weigh_kernel(const double* __restrict__ x, int64_t ldx, const double* __restrict__ w,
@@ -290,6 +327,13 @@ extern "C" int fase_init_products(const double* phi, int64_t ldphi, const double
   const cudaStream_t s = as_stream(stream);
   int st = launch_weigh(f, ldf, w, ldw, B, M, fw, ldfw, s, "fase_init_products (weigh)");
   if (st != FASE_OK) return st;
+  if (B <= kGemvMax) {
+    const int threads = 256;
+    const int blocks = (K + threads / 32 - 1) / (threads / 32);
+    gemv_rows_kernel<<<blocks < 148 * 8 ? blocks : 148 * 8, threads, 0, s>>>(
+        fw, ldfw, B, phi, ldphi, K, M, R0, ldr);
+    return check_launch("fase_init_products (gemv)");
+  }
   GemmParams p{fw, ldfw, phi, ldphi, R0, ldr, B, K, M};
   return launch<TileMain, false>(p, s, "fase_init_products");
 }

@@ -102,12 +102,7 @@ __global__ void __launch_bounds__(kPasteThreads) frame_paste_kernel(
         s_coef[t] = my_coef[t0 + t];
       }
       __syncthreads();
-      if (mine) {
-        for (int t = 0; t < len; ++t) {
-          if (s_sel[t] < 0) break;  // block stopped: every atom degenerate
-          acc = add_rn(acc, mul_rn(s_coef[t], __ldg(phi + static_cast<int64_t>(s_sel[t]) * ldphi + m)));
-        }
-      }
+      if (mine) acc = synth_terms(phi, ldphi, s_sel, s_coef, len, m, acc);
     }
     if (mine) out[static_cast<int64_t>(r0 + i) * ldout + c0 + j] = acc;
   }
