@@ -39,7 +39,9 @@ from .fast import (
     fase_extrapolate,
     fase_extrapolate_batch,
     initial_scalar_products,
+    load_gram_table,
     provenance_hash,
+    save_gram_table,
 )
 from .grid import (
     ExtrapConfig,
@@ -64,6 +66,6 @@ __all__ = [
     "as_mask", "base_weight", "build_gram_tables", "build_weight_field", "build_weight_fields",
     "center_distances", "central_loss_mask", "chunk_plan", "fase_extrapolate",
     "fase_extrapolate_batch", "gaussian_dictionary", "generate_dictionary", "hadamard_matrix",
-    "initial_scalar_products", "load_dictionary", "parse_dict_spec", "provenance_hash",
+    "initial_scalar_products", "load_dictionary", "load_gram_table", "save_gram_table", "parse_dict_spec", "provenance_hash",
     "psnr_over_region", "save_dictionary", "union_dictionaries", "__version__",
 ]

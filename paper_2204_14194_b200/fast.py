@@ -763,3 +763,50 @@ def apply_model(signal, model: SparseModel, mask, *, device=None):
                         n_shared=int(idx.size))
     out[mask] = g.cpu().numpy().ravel()[idx]
     return out, 0.0
+
+
+# ----------------------------------------------------------------- FGRM files
+#
+# Layout of the reference's table files (fast.py:289-328): "FGRM v1\n", u64 LE
+# K, u64 LE provenance, K*K complex entries row-major as (re, im) f64 LE, then
+# K f64 LE entries of D -- exactly 24 + 16*K^2 + 8*K bytes.
+
+_FGRM_MAGIC = b"FGRM v1\n"
+
+
+def save_gram_table(tables: GramTable, path) -> None:
+    """Write a table in the FGRM layout (device tables are downloaded once)."""
+    k = tables.size
+    c = tables.c
+    d = np.asarray(tables.d, dtype="<f8")
+    with open(path, "wb") as fh:
+        fh.write(_FGRM_MAGIC)
+        fh.write(struct.pack("<2Q", k, tables.provenance))
+        step = max(1, (1 << 22) // max(1, k))
+        for lo in range(0, k, step):
+            blk = c[lo:lo + step]
+            pairs = np.empty(blk.shape + (2,), dtype="<f8")
+            pairs[..., 0] = blk.real
+            pairs[..., 1] = blk.imag if np.iscomplexobj(blk) else 0.0
+            fh.write(pairs.tobytes())
+        fh.write(d.tobytes())
+
+
+def load_gram_table(path) -> GramTable:
+    """Read an FGRM file (e.g. written by the reference's ``fase tables``);
+    FormatError on any layout violation. The table is uploaded on first use."""
+    from .errors import FormatError
+
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if len(blob) < 24 or blob[:8] != _FGRM_MAGIC:
+        raise FormatError(f"{path}: not an FGRM v1 file")
+    k, prov = struct.unpack_from("<2Q", blob, 8)
+    if k < 1:
+        raise FormatError(f"{path}: atom count must be positive, got {k}")
+    if len(blob) != 24 + 16 * k * k + 8 * k:
+        raise FormatError(f"{path}: {len(blob)} bytes, layout implies {24 + 16 * k * k + 8 * k}")
+    pairs = np.frombuffer(blob, dtype="<f8", count=2 * k * k, offset=24).reshape(k, k, 2)
+    c = pairs[..., 0] + 1j * pairs[..., 1]
+    d = np.frombuffer(blob, dtype="<f8", count=k, offset=24 + 16 * k * k).copy()
+    return GramTable(c=c, d=d, provenance=int(prov))

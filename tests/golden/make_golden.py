@@ -184,12 +184,22 @@ def frame_config_blocks(cid: int, picks: int):
     return {"config": cid, "blocks": [int(x) for x in chosen], "seconds": time.time() - t0}
 
 
+def fgrm_fixture():
+    """A small table file written by the reference's own save_gram_table."""
+    d = fase.parse_dict_spec("union:dct+wht", 4, 4)
+    w = fase.build_weight_field(wl.central_loss_mask(4, 4, 2, 2), 0.8)
+    t = fase.build_gram_tables(d, w)
+    fase.save_gram_table(t, HERE / "ref_tables.fgrm")
+    return {"spec": "union:dct+wht", "m": 4, "n": 4, "provenance": str(t.provenance)}
+
+
 def main():
     meta = {"generator": "tests/golden/make_golden.py",
             "reference": "/root/reference/pkg (fase 0.1.0, unmodified)",
             "numpy": np.__version__}
     meta.update(weights_and_hashes())
     meta["small_cases"] = small_cases()
+    meta["fgrm"] = fgrm_fixture()
     meta["c0"] = shared_config_blocks(0, [0])
     meta["c1"] = shared_config_blocks(1, [0, 1, 2, 3])
     meta["c4"] = shared_config_blocks(4, [0, 1])

@@ -365,3 +365,19 @@ def test_frame_engine_against_reference_blocks(golden_dir, cid):
             got_tile = out[r0_:r0_ + mb, c0_:c0_ + mb]
             assert rel_dev(got_tile, want_tile) < COEF_REL
     assert exact >= len(z["blocks"]) - 1
+
+
+def test_reference_fgrm_table_drives_the_gpu_path(golden_dir):
+    """A table file written by the reference's save_gram_table runs on the GPU
+    and gives the same selections as a GPU-built table."""
+    from paper_2204_14194_b200 import load_gram_table
+
+    t = load_gram_table(golden_dir / "ref_tables.fgrm")
+    d = parse_dict_spec("union:dct+wht", 4, 4)
+    mask = wl.central_loss_mask(4, 4, 2, 2)
+    sig = np.random.default_rng(7).standard_normal((4, 4))
+    _, a = fase_extrapolate(sig, mask, d, t, ExtrapConfig(8), device=DEV)
+    t2 = build_gram_tables(d, build_weight_field(mask, 0.8), device=DEV)
+    _, b = fase_extrapolate(sig, mask, d, t2, ExtrapConfig(8), device=DEV)
+    assert np.array_equal(a.selected, b.selected)
+    assert rel_dev(a.coefficients.real, b.coefficients.real) < 1e-12

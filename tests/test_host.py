@@ -241,3 +241,39 @@ def test_gpu_entry_points_refuse_without_cuda():
     d = generate_dictionary("dct", 4, 4)
     with pytest.raises(NativeLibraryError):
         fase_extrapolate_batch(np.zeros((1, 4, 4)), np.eye(4, dtype=bool), d)
+
+
+# ----------------------------------------------------------------- FGRM table files
+
+
+def test_fgrm_reads_reference_file_and_round_trips(golden_dir, meta, tmp_path):
+    from paper_2204_14194_b200 import load_gram_table, save_gram_table
+
+    rec = meta["fgrm"]
+    t = load_gram_table(golden_dir / "ref_tables.fgrm")
+    d = parse_dict_spec(rec["spec"], rec["m"], rec["n"])
+    w = build_weight_field(wl.central_loss_mask(4, 4, 2, 2), 0.8)
+    assert t.size == len(d) == 32
+    assert t.provenance == int(rec["provenance"]) == provenance_hash(d, w)
+    out = tmp_path / "t.fgrm"
+    save_gram_table(t, out)
+    assert out.stat().st_size == 24 + 16 * 32 * 32 + 8 * 32
+    back = load_gram_table(out)
+    # values survive (a signed zero in an imaginary part may not: loading
+    # forms re + 1j*im, in the reference as here)
+    assert np.array_equal(back.c, t.c) and np.array_equal(back.d, t.d)
+    assert back.provenance == t.provenance
+    again = tmp_path / "t2.fgrm"
+    save_gram_table(back, again)
+    assert again.read_bytes() == out.read_bytes()
+
+
+def test_fgrm_rejects_bad_files(golden_dir, tmp_path):
+    from paper_2204_14194_b200 import load_gram_table
+
+    blob = (golden_dir / "ref_tables.fgrm").read_bytes()
+    bad = tmp_path / "bad.fgrm"
+    for payload in (b"GARBAGE!" + blob[8:], blob + b"\0", blob[:-8], blob[:20]):
+        bad.write_bytes(payload)
+        with pytest.raises(FormatError):
+            load_gram_table(bad)
