@@ -62,6 +62,9 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target wall seconds of the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--products", default="auto", choices=["auto", "gemm", "separable"],
+                    help="initial products: separable transforms (separable dictionaries) or "
+                         "the dense DMMA GEMM")
     return ap.parse_args()
 
 
@@ -279,6 +282,7 @@ def run_gpu(args):
     import torch.distributed as dist
 
     from paper_2204_14194_b200 import ExtrapolationPlan, _native, build_gram_tables, build_weight_field
+    from paper_2204_14194_b200.fast import initial_products_into
 
     rank, world, local = dist_env()
     cpu = None
@@ -296,7 +300,7 @@ def run_gpu(args):
     mask = wl.central_loss_mask(*w.area, *w.loss)
     d.device_matrix(dev)
     tables = build_gram_tables(d, build_weight_field(mask, w.config.rho_hat), device=dev)
-    plan = ExtrapolationPlan(d, mask, B, w.config, tables, device=dev)
+    plan = ExtrapolationPlan(d, mask, B, w.config, tables, device=dev, products=args.products)
     # one more table build, kernels only, for the reported Gram time
     G2 = torch.zeros_like(plan.G)
     D2 = torch.empty_like(plan.D)
@@ -347,7 +351,7 @@ def run_gpu(args):
             e[0].record(stream)
             if split:
                 plan.F[:, :M].copy_(dev_sig.reshape(B, -1), non_blocking=True)
-                _native.init_products(plan.phi, plan.F, plan.W, K, M, plan.R0, ws=plan.ws)
+                initial_products_into(d, plan.F, plan.W, plan.R0, plan.ws, method=plan.products)
                 e[1].record(stream)
                 _native.iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, plan.selected,
                                 plan.projections, plan.coefficients)
@@ -401,6 +405,11 @@ def run_gpu(args):
         achieved = bytes_iter / it_s / 1e9
         init_s = float(np.mean(init_ms)) / 1e3
         flops_init = 2.0 * K * M * B
+        factors = d.device_factors(dev) if plan.products in ("auto", "separable") else None
+        if factors:  # executed flops of the separable form
+            mr, nc = w.area
+            flops_sep = sum(2.0 * B * (r.shape[0] * mr * nc + r.shape[0] * nc * c.shape[0])
+                            for r, c, _ in factors)
         step_ms = dev_total_s / args.steps * 1e3
         line = {
             "metric": "extrapolated blocks/s",
@@ -429,10 +438,20 @@ def run_gpu(args):
                          "ms_per_launch": it_s * 1e3, "peak_source": hsrc,
                          "note": "8*K bytes per block-iteration (one FP64 table row); hot rows "
                                  "hit L2, so frac can exceed DRAM-bound expectations"},
-            "roofline_init": {"bound": "tensor", "kernel": "dgemm_nt_kernel (DMMA FP64)",
-                              "achieved": flops_init / init_s / 1e12, "peak": fp64,
-                              "unit": "TFLOP/s", "frac": flops_init / init_s / 1e12 / fp64,
-                              "ms_per_launch": init_s * 1e3, "peak_source": fsrc},
+            "roofline_init": ({"bound": "tensor", "kernel": "dgemm_nt_kernel (DMMA FP64)",
+                               "achieved": flops_init / init_s / 1e12, "peak": fp64,
+                               "unit": "TFLOP/s", "frac": flops_init / init_s / 1e12 / fp64,
+                               "ms_per_launch": init_s * 1e3, "peak_source": fsrc}
+                              if not factors else
+                              {"bound": "fp64", "kernel": "weigh_kernel + sep_products_kernel "
+                               "(separable transforms, FP64 FMA)",
+                               "achieved": flops_sep / init_s / 1e12, "peak": fp64,
+                               "unit": "TFLOP/s", "frac": flops_sep / init_s / 1e12 / fp64,
+                               "ms_per_launch": init_s * 1e3, "peak_source": fsrc,
+                               "dense_equivalent_tflops": flops_init / init_s / 1e12,
+                               "note": "executed flops of rows X cols^T per part; the dense "
+                                       "GEMM form (--products gemm) does 24x more work"}),
+            "products": plan.products_method,
             "stage_ms": {"init_products": float(np.mean(init_ms)), "iterate": float(np.mean(iter_ms)),
                          "synth": float(np.mean(synth_ms))},
             "gram_ms": gram_ms,

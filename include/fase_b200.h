@@ -113,6 +113,27 @@ FASE_API int fase_init_products(const double* phi, int64_t ldphi, const double* 
                                 void* stream);
 
 /*
+ * Weighted operand: out[b*ldo + m] = x[b*ldx + m] * w[b*ldw + m] (ldw == 0:
+ * one shared weight row), one correctly rounded multiply per sample -- the
+ * reference's `s * w` (fast.py:154). Even leading dimensions.
+ */
+FASE_API int fase_weigh(const double* x, int64_t ldx, const double* w, int64_t ldw, int rows,
+                        int M, double* out, int64_t ldo, void* stream);
+
+/*
+ * Initial products of one separable dictionary part (atoms
+ * phi[col0 + u*Lc + v](m, n) = rows[u, m] * cols[v, n], dictionary.py:167-178)
+ * for B weighted areas X (B x ldx, Mr*Nc samples each, e.g. the F o W formed
+ * by fase_init_products' first step or by fase_frame_areas):
+ *   R0[b*ldr + col0 + u*Lc + v] = (rows X_b cols^T)[u, v]
+ * -- the separable-transform form of initial_scalar_products (fast.py:145-157),
+ * 2(Lr*Mr*Nc + Lr*Nc*Lc) flops per block instead of 2*Lr*Lc*Mr*Nc.
+ */
+FASE_API int fase_sep_products(const double* rows, int Lr, int Mr, const double* cols, int Lc,
+                               int Nc, const double* X, int64_t ldx, int B, double* R0,
+                               int64_t ldr, int64_t col0, void* stream);
+
+/*
  * Per-block normalizers for per-block geometries whose table rows are
  * G_b = G0 - sum_{j in chunks(b)} C_j (see fase_iterate):
  *   diag_b[k] = G0[k,k] - sum_j C_j[k,k];  D[b*ldd + k] as in fase_gram_finish.

@@ -33,7 +33,7 @@ EXPORTS = (
     "fase_gram", "fase_gram_workspace", "fase_gemm_nt", "fase_init_products_workspace",
     "fase_gram_finish", "fase_init_products", "fase_block_normalizers", "fase_iterate",
     "fase_synth_paste", "fase_l2_flush", "fase_frame_areas", "fase_frame_cells",
-    "fase_frame_paste",
+    "fase_frame_paste", "fase_weigh", "fase_sep_products",
 )
 
 _vp = ctypes.c_void_p
@@ -95,6 +95,9 @@ def load():
         "fase_synth_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
                              _i64, _vp],
         "fase_l2_flush": [_vp, ctypes.c_size_t, _vp],
+        "fase_weigh": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _i64, _vp],
+        "fase_sep_products": [_vp, _i32, _i32, _vp, _i32, _i32, _vp, _i64, _i32, _vp, _i64, _i64,
+                              _vp],
         "fase_frame_areas": [_vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp,
                              _i64, _vp],
         "fase_frame_cells": [_vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _vp,
@@ -322,6 +325,33 @@ def frame_paste(phi, sel, coef, iterations: int, grid, tile: int, support: int, 
     _check(lib.fase_frame_paste(_ptr(phi), _ld(phi), _ptr(sel), _ptr(coef), _ld(sel), iterations,
                                 _ptr(grid), _ld(grid), H, W, tile, support, _ptr(corners),
                                 corners.shape[0], _ptr(out), _ld(out), _stream(out)))
+
+
+def weigh(x, w, M: int, out) -> None:
+    """out[b, :M] = x[b, :M] * w[(b or shared), :M] (one rounding per sample)."""
+    import torch
+
+    lib = load()
+    _require(x, "x", torch.float64, 2)
+    _require(w, "w", torch.float64)
+    _require(out, "out", torch.float64, 2)
+    ldw = _ld(w) if w.dim() == 2 else 0
+    _check(lib.fase_weigh(_ptr(x), _ld(x), _ptr(w), ldw, x.shape[0], M, _ptr(out), _ld(out),
+                          _stream(out)))
+
+
+def sep_products(rows, cols, X, M_rows: int, N_cols: int, R0, col0: int) -> None:
+    """R0[b, col0 + u*Lc + v] = (rows X_b cols^T)[u, v] for one separable part."""
+    import torch
+
+    lib = load()
+    _require(rows, "rows", torch.float64, 2)
+    _require(cols, "cols", torch.float64, 2)
+    _require(X, "X", torch.float64, 2)
+    _require(R0, "R0", torch.float64, 2)
+    _check(lib.fase_sep_products(_ptr(rows), rows.shape[0], M_rows, _ptr(cols), cols.shape[0],
+                                 N_cols, _ptr(X), _ld(X), X.shape[0], _ptr(R0), _ld(R0), col0,
+                                 _stream(R0)))
 
 
 def l2_flush(buf) -> None:

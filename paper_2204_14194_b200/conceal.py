@@ -153,7 +153,12 @@ class FrameEngine:
             )}
         return self._buf[L]
 
-    launches_per_frame = 6  # areas, cells, normalizers, gemm, iterate, paste
+    @property
+    def launches_per_frame(self) -> int:
+        """areas, cells, normalizers, products (one per separable part or one GEMM),
+        iterate, paste"""
+        factors = self.dictionary.device_factors(self.device)
+        return 5 + (len(factors) if factors else 1)
 
     def run(self, frame, grid, corners, out=None) -> BatchResult:
         """Conceal one frame: ``frame`` (H, W) float64, ``grid`` (H/tile, W/tile)
@@ -172,7 +177,12 @@ class FrameEngine:
                             b["counts"], b["ids"])
         _native.block_normalizers(self.G0, self.tables, self.stride, b["counts"], b["ids"], K,
                                   b["D"], b["alive"])
-        _native.gemm_nt(b["X"][:, : self.M], self.phi[:, : self.M], b["R0"])
+        factors = self.dictionary.device_factors(self.device)
+        if factors:  # separable parts: rows X cols^T per part (csrc/separable.cu)
+            for rows, cols, row0 in factors:
+                _native.sep_products(rows, cols, b["X"], self.A, self.A, b["R0"], row0)
+        else:
+            _native.gemm_nt(b["X"][:, : self.M], self.phi[:, : self.M], b["R0"])
         _native.iterate(self.G0, b["D"], b["R0"], K, cfg.iterations, cfg.gamma, b["sel"], b["proj"],
                         b["coef"], chunk_tables=self.tables, chunk_stride=self.stride,
                         chunk_count=b["counts"], chunk_ids=b["ids"])

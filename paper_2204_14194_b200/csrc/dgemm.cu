@@ -353,3 +353,18 @@ extern "C" int fase_gemm_nt(const double* A, int64_t lda, const double* B, int64
   return variant == 1 ? launch<TileBig, false>(p, as_stream(stream), "fase_gemm_nt")
                       : launch<TileMain, false>(p, as_stream(stream), "fase_gemm_nt");
 }
+
+extern "C" int fase_weigh(const double* x, int64_t ldx, const double* w, int64_t ldw, int rows,
+                          int M, double* out, int64_t ldo, void* stream) {
+  if (rows < 0 || M < 1 || ldx < M || ldo < M || (ldw != 0 && ldw < M) || (ldx & 1) ||
+      (ldo & 1) || (ldw & 1)) {
+    set_error("fase_weigh: bad sizes or odd leading dimension (rows=%d, M=%d)", rows, M);
+    return FASE_ERR_SHAPE;
+  }
+  if (rows == 0) return FASE_OK;
+  if (!x || !w || !out || !aligned16(x) || !aligned16(w) || !aligned16(out)) {
+    set_error("fase_weigh: null or misaligned pointer");
+    return FASE_ERR_SHAPE;
+  }
+  return launch_weigh(x, ldx, w, ldw, rows, M, out, ldo, as_stream(stream), "fase_weigh");
+}

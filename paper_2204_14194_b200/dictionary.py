@@ -234,6 +234,24 @@ class Dictionary:
         """Leading dimension of the device Phi (area rounded up to 4 samples)."""
         return _round_up(self.area, 4)
 
+    def device_factors(self, device):
+        """[(rows (Lr, M) , cols (Lc, N), first atom)] on ``device`` for separable
+        sets (cached), or None."""
+        import torch
+
+        if self._parts is None:
+            return None
+        dev = torch.device(device)
+        key = ("factors", dev.type, dev.index)
+        if key not in self._device_cache:
+            out, row = [], 0
+            for p in self._parts:
+                out.append((torch.from_numpy(np.ascontiguousarray(p.rows)).to(dev),
+                            torch.from_numpy(np.ascontiguousarray(p.cols)).to(dev), row))
+                row += p.size
+            self._device_cache[key] = out
+        return self._device_cache[key]
+
     def device_matrix(self, device):
         """(K, ld) float64 Phi in HBM, cached per device.
 

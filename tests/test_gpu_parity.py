@@ -381,3 +381,31 @@ def test_reference_fgrm_table_drives_the_gpu_path(golden_dir):
     _, b = fase_extrapolate(sig, mask, d, t2, ExtrapConfig(8), device=DEV)
     assert np.array_equal(a.selected, b.selected)
     assert rel_dev(a.coefficients.real, b.coefficients.real) < 1e-12
+
+
+@pytest.mark.parametrize("spec,m,n", [("union:dct+had", 48, 48), ("dct", 5, 7), ("wht", 8, 16)])
+def test_separable_products_match_gemm_and_oracle(spec, m, n):
+    from paper_2204_14194_b200.fast import initial_products_into
+
+    d = parse_dict_spec(spec, m, n)
+    K, M = len(d), m * n
+    mask = wl.central_loss_mask(m, n, max(1, m // 3), max(1, n // 3))
+    w = build_weight_field(mask, 0.8)
+    rng = np.random.default_rng(11)
+    sig = rng.uniform(0, 255, (5, m, n))
+    ld = M + (M & 1)
+    F = torch.zeros((5, ld), dtype=torch.float64, device=DEV)
+    F[:, :M] = torch.from_numpy(sig.reshape(5, -1)).to(DEV)
+    W = torch.zeros(ld, dtype=torch.float64, device=DEV)
+    W[:M] = torch.from_numpy(w.ravel()).to(DEV)
+    ws = torch.empty(5 * ld + 2, dtype=torch.float64, device=DEV)
+    outs = {}
+    for method in ("separable", "gemm"):
+        R0 = torch.zeros((5, K + (K & 1)), dtype=torch.float64, device=DEV)
+        assert initial_products_into(d, F, W, R0, ws, method=method) == method
+        outs[method] = R0[:, :K].cpu().numpy()
+    phi = d.real_values().reshape(K, -1).astype(np.complex128)
+    for b in range(5):
+        want = orc.initial_products(sig[b], w, phi).real
+        assert rel_dev(outs["separable"][b], want) < 1e-13
+        assert rel_dev(outs["gemm"][b], want) < 1e-13
