@@ -42,6 +42,7 @@
 // chunk-list order, identical to fase_block_normalizers' diagonal.
 
 #include <climits>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -64,14 +65,17 @@ template <int NT, int EPT, int MINB, bool kDsmem, bool kChunked, bool kRecord>
 __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_iterate_args a) {
   constexpr int EP = EPT / 2;
   constexpr int NW = NT / 32;
-  constexpr unsigned kRowBytes = NT * EPT * sizeof(double);
+
   __shared__ long long s_key[NW];
   __shared__ unsigned s_arg[NW];
   __shared__ unsigned s_u[NW];
   __shared__ double s_r[NW];
   __shared__ double s_d[NW];
   __shared__ __align__(16) double s_dump[NW][kDsmem ? 1 : 2][EPT];  // tie-pass winner's registers
-  __shared__ __align__(8) uint64_t s_bar;
+  // The staged row arrives in kSeg segments, each on its own mbarrier, so the
+  // update can start on the first segment while the rest is still in flight.
+  constexpr int kSeg = EP < 3 ? EP : 3;
+  __shared__ __align__(8) uint64_t s_bar[kSeg];
   extern __shared__ double2 s_dyn[];
   double2* s_row = s_dyn;            // staged row: pair p at s_row[p]
   double2* s_D = s_dyn + EP * NT;    // kDsmem: normalizer pairs, same indexing
@@ -84,7 +88,7 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
   const double kDead = __longlong_as_double(static_cast<long long>(0xfff0000000000000ULL));
 
   if (t == 0) {
-    mbar_init(&s_bar, 1);
+    for (int sg = 0; sg < kSeg; ++sg) mbar_init(&s_bar[sg], 1);
     fence_mbar_init();
   }
 
@@ -184,8 +188,14 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
     // while the tie pass and the second barrier run
     if (t == 0) {
       fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&s_bar, kRowBytes);
-      tma_load_1d(s_row, a.G0 + static_cast<int64_t>(guess) * ldg, kRowBytes, &s_bar);
+      const double* grow = a.G0 + static_cast<int64_t>(guess) * ldg;
+#pragma unroll
+      for (int sg = 0; sg < kSeg; ++sg) {
+        const int j0 = sg * EP / kSeg, j1 = (sg + 1) * EP / kSeg;
+        const unsigned bytes = static_cast<unsigned>((j1 - j0) * NT * sizeof(double2));
+        mbar_arrive_expect_tx(&s_bar[sg], bytes);
+        tma_load_1d(s_row + j0 * NT, grow + 2 * j0 * NT, bytes, &s_bar[sg]);
+      }
     }
     const double top = __longlong_as_double(top_key);
     // tie_quantum: only a finite, strictly positive top moves the ratchet
@@ -244,14 +254,22 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
       coef[it] = c;
     }
 
-    mbar_wait(&s_bar, it & 1);  // the staged row (also retires it when unused)
+    auto wait_all = [&]() {
+#pragma unroll
+      for (int sg = 0; sg < kSeg; ++sg) mbar_wait(&s_bar[sg], it & 1);
+    };
     // ---- rank-1 update fused with the next iteration's running max; the row
     // source is block-uniform, so each source gets its own unrolled loop
-    auto update = [&](auto row_pair) {
+    auto update = [&](auto row_pair, auto staged) {
       best = kDead;
       barg = kNone;
 #pragma unroll
       for (int j = 0; j < EP; ++j) {
+        if constexpr (decltype(staged)::value) {
+#pragma unroll
+          for (int sg = 0; sg < kSeg; ++sg)
+            if (j == sg * EP / kSeg) mbar_wait(&s_bar[sg], it & 1);  // segment arrives
+        }
         const double2 g = row_pair(j);
         const double2 dd = dpair(j);
         r[j][0] = sub_rn(r[j][0], mul_rn(c, g.x));
@@ -268,9 +286,12 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
         }
       }
     };
+    using Staged = std::true_type;
+    using Direct = std::false_type;
     if (kChunked && nch > 0) {
       // row_u of this block = G0[u] - sum of its chunk tables' rows, composed
       // in the staging buffer (each thread only touches its own pairs)
+      wait_all();
       if (u != guess) {
         const double* urow = a.G0 + static_cast<int64_t>(u) * ldg + 2 * t;
 #pragma unroll 4
@@ -288,13 +309,14 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
           s_row[j * NT + t] = g;
         }
       }
-      update([&](int j) { return s_row[j * NT + t]; });
+      update([&](int j) { return s_row[j * NT + t]; }, Direct{});
       fence_proxy_async_smem();  // generic writes above precede the next TMA fill
     } else if (u == guess) {  // block-uniform
-      update([&](int j) { return s_row[j * NT + t]; });
+      update([&](int j) { return s_row[j * NT + t]; }, Staged{});
     } else {
+      wait_all();  // retire the mispredicted copy before the next one
       const double* urow = a.G0 + static_cast<int64_t>(u) * ldg + 2 * t;
-      update([&](int j) { return ldg2(urow + 2 * j * NT); });
+      update([&](int j) { return ldg2(urow + 2 * j * NT); }, Direct{});
     }
     if (kRecord) {
       double* dst = a.R_log + (static_cast<int64_t>(b) * a.I + it) * a.ldr;

@@ -281,7 +281,7 @@ class Dictionary:
                 _native.basis_outer(rows, cols, phi, row)
                 row += p.size
         else:
-            host = torch.from_numpy(np.ascontiguousarray(self._dense.reshape(self._k, -1)))
+            host = torch.from_numpy(np.array(self._dense.reshape(self._k, -1), copy=True))
             phi[:, : m * n].copy_(host.to(dev))
         self._device_cache[key] = phi
         return phi
