@@ -230,6 +230,56 @@ FASE_API int fase_frame_paste(const double* phi, int64_t ldphi, const int32_t* s
                               const int32_t* corners, int L, double* out, int64_t ldout,
                               void* stream);
 
+/*
+ * ---- Complex-valued dictionaries (dft, bdft, their unions; dictionary.py:126-166)
+ *
+ * Device layout of a complex dictionary ("conjugate-split"): 2K rows of ldphi
+ * doubles, row 2k = Re phi_k, row 2k+1 = -Im phi_k. Passed to
+ * fase_init_products as a real dictionary of 2K atoms it yields
+ * conj(Phi) (F o W) interleaved -- R0[b, k] = (re, im) -- which is
+ * initial_scalar_products' conj(phi @ conj(s*w)) (fast.py:154-155).
+ *
+ * Complex tables are rows of interleaved (re, im) doubles; ldt counts complex
+ * elements. The table stores conj(C[u, :]) -- the operand of the update
+ * (fast.py:246) -- exactly Hermitian with a real diagonal:
+ *   T[u*ldt + l] = conj(C[u, l]),  C = conj(Phi) W Phi^T   (fast.py:109-142)
+ * Normalizers of a complex table come from fase_gram_finish(T, 2*ldt + 1, ...)
+ * (the real parts of the diagonal sit at stride 2*ldt + 2 doubles); per-block
+ * chunked normalizers likewise pass ldg = 2*ldt + 1 and a stride in doubles.
+ */
+FASE_API size_t fase_gram_complex_workspace(int K, int64_t ldphi);
+FASE_API int fase_gram_complex(const double* phi2, int64_t ldphi, const double* w, int K, int M,
+                               double* T, int64_t ldt, void* ws, size_t ws_bytes, void* stream);
+
+/* Largest K / table leading dimension (complex elements) of fase_iterate_complex. */
+FASE_API int fase_max_atoms_complex(void);
+FASE_API int fase_table_ld_complex(int K);
+
+/*
+ * The recursion in complex128 (fast.py:224-255): metric |R_k| * D_k with numpy's
+ * complex abs, the same tie rule, p = R_u * (D_u * D_u), c = gamma * p and
+ * R_k <- R_k - c * T[u, k] with numpy's complex product; bit-identical to the
+ * reference given the same R0 / table / D. Same argument block as fase_iterate
+ * with these units: G0 / chunk tables are complex tables (ldg, chunk_stride in
+ * complex elements, ldg >= fase_table_ld_complex(K)); R0 / R_out / R_log
+ * interleaved complex with ldr in complex elements; proj / coef interleaved
+ * complex (B x ldo complex); D, sel as in fase_iterate.
+ */
+FASE_API int fase_iterate_complex(const fase_iterate_args* args, void* stream);
+
+/*
+ * Complex model synthesis and paste (SparseModel.materialize + apply_model):
+ * as fase_synth_paste with phi2 in the conjugate-split layout and coef
+ * interleaved complex; Re g is written to out and, when max_imag != NULL,
+ * max_imag[b] = max |Im g| over block b's samples (apply_model's second result,
+ * fast.py:284).
+ */
+FASE_API int fase_synth_paste_complex(const double* phi2, int64_t ldphi, const int32_t* sel,
+                                      const double* coef, int64_t ldo, int I, int B,
+                                      const int32_t* idx_ptr, const int32_t* idx, int n_shared,
+                                      const int64_t* dst, double* out, int64_t ldout,
+                                      double* max_imag, void* stream);
+
 /* Writes `bytes` of zeros-then-ones into `buf` to evict L2 between timed steps. */
 FASE_API int fase_l2_flush(void* buf, size_t bytes, void* stream);
 

@@ -26,6 +26,38 @@ SELECTION_TIE_RTOL = 1e-13   # reference.py:55
 BINARIZE_SNAP = 1e-12        # dictionary.py:36
 
 
+# ----------------------------------------------------------------- complex128 scalar semantics
+#
+# The reference's complex arithmetic is numpy's. On the build host (numpy 2.x,
+# AVX-512 / FMA3 loops) the contiguous complex128 product and abs evaluate as
+# below; tests/test_oracle_golden.py checks these statements against numpy and
+# against tests/golden/complex_arith.npz, and the CUDA kernels implement the
+# same sequences (csrc/common.cuh: np_cmul, np_cabs).
+
+
+def _fma(a: float, b: float, c: float) -> float:
+    """Correctly rounded a*b + c (exact rational arithmetic, then one rounding)."""
+    from fractions import Fraction
+
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+def cmul_fused(x: complex, y: complex) -> complex:
+    """x*y as numpy's loop computes it: (fma(xr, yr, -(xi*yi)), fma(xr, yi, xi*yr))."""
+    return complex(_fma(x.real, y.real, -(x.imag * y.imag)),
+                   _fma(x.real, y.imag, x.imag * y.real))
+
+
+def cabs_scaled(z: complex) -> float:
+    """|z| as numpy's loop computes it: larger * sqrt(fma(r, r, 1)), r = smaller / larger."""
+    a, b = abs(z.real), abs(z.imag)
+    hi, lo = max(a, b), min(a, b)
+    if hi == 0.0:
+        return 0.0
+    r = lo / hi
+    return math.sqrt(_fma(r, r, 1.0)) * hi
+
+
 # ----------------------------------------------------------------- weighting
 
 

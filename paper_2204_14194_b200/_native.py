@@ -33,7 +33,9 @@ EXPORTS = (
     "fase_gram", "fase_gram_workspace", "fase_gemm_nt", "fase_init_products_workspace",
     "fase_gram_finish", "fase_init_products", "fase_block_normalizers", "fase_iterate",
     "fase_synth_paste", "fase_l2_flush", "fase_frame_areas", "fase_frame_cells",
-    "fase_frame_paste", "fase_weigh", "fase_sep_products",
+    "fase_frame_paste", "fase_weigh", "fase_sep_products", "fase_gram_complex_workspace",
+    "fase_gram_complex", "fase_max_atoms_complex", "fase_table_ld_complex", "fase_iterate_complex",
+    "fase_synth_paste_complex",
 )
 
 _vp = ctypes.c_void_p
@@ -82,6 +84,11 @@ def load():
     lib.fase_gram_workspace.argtypes = [_i32, _i32]
     lib.fase_init_products_workspace.restype = ctypes.c_size_t
     lib.fase_init_products_workspace.argtypes = [_i32, _i32]
+    lib.fase_gram_complex_workspace.restype = ctypes.c_size_t
+    lib.fase_gram_complex_workspace.argtypes = [_i32, _i64]
+    lib.fase_max_atoms_complex.restype = _i32
+    lib.fase_table_ld_complex.restype = _i32
+    lib.fase_table_ld_complex.argtypes = [_i32]
     sigs = {
         "fase_basis_outer": [_vp, _i32, _i32, _vp, _i32, _i32, _vp, _i64, _i64, _vp],
         "fase_gram": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp, ctypes.c_size_t, _vp],
@@ -92,6 +99,10 @@ def load():
         "fase_block_normalizers": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _i64,
                                    _vp, _vp],
         "fase_iterate": [ctypes.POINTER(IterateArgs), _vp],
+        "fase_iterate_complex": [ctypes.POINTER(IterateArgs), _vp],
+        "fase_gram_complex": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp, ctypes.c_size_t, _vp],
+        "fase_synth_paste_complex": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp,
+                                     _vp, _i64, _vp, _vp],
         "fase_synth_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
                              _i64, _vp],
         "fase_l2_flush": [_vp, ctypes.c_size_t, _vp],
@@ -282,6 +293,109 @@ def synth_paste(phi, sel, coef, iterations: int, idx, out, *, idx_ptr=None, n_sh
     _check(lib.fase_synth_paste(_ptr(phi), _ld(phi), _ptr(sel), _ptr(coef), _ld(sel), iterations,
                                 B, _ptr(idx_ptr), _ptr(idx), n_shared, _ptr(dst), _ptr(out),
                                 ldout, _stream(out)))
+
+
+# ---- complex dictionaries: phi2 is the (2K, ld) conjugate-split matrix; tables,
+# products, projections and coefficients are complex128 tensors whose leading
+# dimensions count complex elements.
+
+
+def _require_complex(t, name, ndim=None):
+    import torch
+
+    return _require(t, name, torch.complex128, ndim)
+
+
+def gram_complex(phi2, w, K: int, M: int, T, ws=None) -> None:
+    """T[u, l] = conj(C[u, l]) with C = conj(Phi) W Phi^T (T: complex128 (K, ldt))."""
+    import torch
+
+    lib = load()
+    _require(phi2, "phi2", torch.float64, 2)
+    _require(w, "w", torch.float64, 1)
+    _require_complex(T, "T", 2)
+    need = int(lib.fase_gram_complex_workspace(K, _ld(phi2)))
+    ws = _workspace(need, T.device, ws)
+    _check(lib.fase_gram_complex(_ptr(phi2), _ld(phi2), _ptr(w), K, M, _ptr(T), _ld(T), _ptr(ws),
+                                 ws.numel() * 8, _stream(T)))
+
+
+def gram_finish_complex(T, K: int, D, n_alive=None) -> None:
+    """D from the (real) diagonal of a complex table."""
+    import torch
+
+    lib = load()
+    _require_complex(T, "T", 2)
+    _require(D, "D", torch.float64, 1)
+    _check(lib.fase_gram_finish(_ptr(T), 2 * _ld(T) + 1, K, _ptr(D), _ptr(n_alive), _stream(T)))
+
+
+def block_normalizers_complex(T0, chunk_tables, chunk_stride: int, chunk_count, chunk_ids, K: int,
+                              D, n_alive) -> None:
+    """Per-block D of complex chunked tables (chunk_stride in complex elements)."""
+    import torch
+
+    lib = load()
+    _require_complex(T0, "T0", 2)
+    _require(D, "D", torch.float64, 2)
+    list_ld = _ld(chunk_ids) if chunk_ids is not None else 0
+    _check(lib.fase_block_normalizers(_ptr(T0), 2 * _ld(T0) + 1, _ptr(chunk_tables),
+                                      2 * chunk_stride, _ptr(chunk_count), _ptr(chunk_ids),
+                                      list_ld, K, D.shape[0], _ptr(D), _ld(D), _ptr(n_alive),
+                                      _stream(D)))
+
+
+def iterate_complex(T, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *,
+                    chunk_tables=None, chunk_stride: int = 0, chunk_count=None, chunk_ids=None,
+                    R_out=None, R_log=None) -> None:
+    import torch
+
+    lib = load()
+    _require_complex(T, "T", 2)
+    _require(D, "D", torch.float64)
+    _require_complex(R0, "R0", 2)
+    _require(sel, "sel", torch.int32, 2)
+    _require_complex(proj, "proj", 2)
+    _require_complex(coef, "coef", 2)
+    args = IterateArgs(
+        G0=_ptr(T), ldg=_ld(T), chunk_tables=_ptr(chunk_tables), chunk_stride=chunk_stride,
+        chunk_count=_ptr(chunk_count), chunk_ids=_ptr(chunk_ids),
+        chunk_list_ld=_ld(chunk_ids) if chunk_ids is not None else 0, D=_ptr(D),
+        ldd=_ld(D) if D.dim() == 2 else 0, R0=_ptr(R0), ldr=_ld(R0), R_out=_ptr(R_out),
+        R_log=_ptr(R_log), K=K, B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel),
+        proj=_ptr(proj), coef=_ptr(coef), ldo=_ld(sel))
+    if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
+        raise errors.ShapeError("sel / proj / coef must share one leading dimension")
+    _check(lib.fase_iterate_complex(ctypes.byref(args), _stream(R0)))
+
+
+def synth_paste_complex(phi2, sel, coef, iterations: int, idx, out, *, idx_ptr=None,
+                        n_shared: int = 0, dst=None, max_imag=None) -> None:
+    import torch
+
+    lib = load()
+    _require(phi2, "phi2", torch.float64, 2)
+    _require(idx, "idx", torch.int32, 1)
+    _require(out, "out", torch.float64)
+    _require_complex(coef, "coef", 2)
+    B = sel.shape[0]
+    ldout = _ld(out) if out.dim() == 2 else 0
+    _check(lib.fase_synth_paste_complex(_ptr(phi2), _ld(phi2), _ptr(sel), _ptr(coef), _ld(sel),
+                                        iterations, B, _ptr(idx_ptr), _ptr(idx), n_shared,
+                                        _ptr(dst), _ptr(out), ldout, _ptr(max_imag),
+                                        _stream(out)))
+
+
+def max_atoms_complex() -> int:
+    return int(load().fase_max_atoms_complex())
+
+
+def table_ld_complex(K: int) -> int:
+    ld = int(load().fase_table_ld_complex(K))
+    if ld <= 0:
+        raise errors.UnsupportedDictionaryError(f"K={K} exceeds the complex iteration kernel's "
+                                                f"{max_atoms_complex()} atoms")
+    return ld
 
 
 def frame_areas(frame, grid, tile: int, support: int, corners, base_w, X) -> None:

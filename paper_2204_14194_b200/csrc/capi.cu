@@ -166,6 +166,66 @@ __global__ void __launch_bounds__(kSynthThreads) synth_paste_kernel(
   }
 }
 
+// Complex dictionaries (conjugate-split rows: phi2[2u] = Re phi_u,
+// phi2[2u+1] = -Im phi_u): g = sum_t coef_t * phi_{sel_t} with numpy's fused
+// complex product (np_cmul), accumulated in selection order
+// (reference.py:120-125); Re g is pasted (fast.py:282) and max |Im g| over the
+// block's samples goes to max_imag[b] (apply_model's diagnostic, fast.py:284).
+__global__ void __launch_bounds__(kSynthThreads) synth_paste_complex_kernel(
+    const double* __restrict__ phi2, int64_t ldphi, const int32_t* __restrict__ sel,
+    const double* __restrict__ coef, int64_t ldo, int I, const int32_t* __restrict__ idx_ptr,
+    const int32_t* __restrict__ idx, int n_shared, const int64_t* __restrict__ dst,
+    double* __restrict__ out, int64_t ldout, double* __restrict__ max_imag) {
+  __shared__ int32_t s_sel[kSynthChunk];
+  __shared__ double2 s_coef[kSynthChunk];
+  __shared__ double s_m[kSynthThreads / 32];
+  const int b = blockIdx.x;
+  const int lo = idx_ptr ? idx_ptr[b] : 0;
+  const int n = idx_ptr ? idx_ptr[b + 1] - lo : n_shared;
+  const int32_t* my_idx = idx + lo;
+  const int32_t* my_sel = sel + static_cast<int64_t>(b) * ldo;
+  const double* my_coef = coef + 2 * static_cast<int64_t>(b) * ldo;
+  double imax = 0.0;
+  for (int base = 0; base < n; base += kSynthThreads) {
+    const int i = base + threadIdx.x;
+    const int m = i < n ? my_idx[i] : 0;
+    double gr = 0.0, gi = 0.0;
+    bool done = false;
+    for (int t0 = 0; t0 < I; t0 += kSynthChunk) {
+      const int len = min(kSynthChunk, I - t0);
+      __syncthreads();
+      for (int t = threadIdx.x; t < len; t += kSynthThreads) {
+        s_sel[t] = my_sel[t0 + t];
+        s_coef[t] = make_double2(my_coef[2 * (t0 + t)], my_coef[2 * (t0 + t) + 1]);
+      }
+      __syncthreads();
+      if (i < n && !done) {
+        for (int t = 0; t < len; ++t) {
+          const int u = s_sel[t];
+          if (u < 0) {  // block without selectable atoms: terms end here
+            done = true;
+            break;
+          }
+          const double pr = __ldg(phi2 + (2 * static_cast<int64_t>(u)) * ldphi + m);
+          const double pi = -__ldg(phi2 + (2 * static_cast<int64_t>(u) + 1) * ldphi + m);
+          const double2 c = s_coef[t];
+          const double2 x = np_cmul(c.x, c.y, pr, pi);
+          gr = add_rn(gr, x.x);
+          gi = add_rn(gi, x.y);
+        }
+      }
+    }
+    if (i < n) {
+      out[(dst ? dst[lo + i] : static_cast<int64_t>(m)) + static_cast<int64_t>(b) * ldout] = gr;
+      imax = fmax(imax, fabs(gi));
+    }
+  }
+  if (max_imag) {
+    const double v = block_max<kSynthThreads>(imax, s_m);
+    if (threadIdx.x == 0) max_imag[b] = v;
+  }
+}
+
 __global__ void flush_kernel(uint4* buf, size_t n, unsigned salt) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -246,6 +306,25 @@ extern "C" int fase_synth_paste(const double* phi, int64_t ldphi, const int32_t*
   synth_paste_kernel<<<B, kSynthThreads, 0, as_stream(stream)>>>(
       phi, ldphi, sel, coef, ldo, I, idx_ptr, idx, n_shared, dst, out, ldout);
   return check_launch("fase_synth_paste");
+}
+
+extern "C" int fase_synth_paste_complex(const double* phi2, int64_t ldphi, const int32_t* sel,
+                                        const double* coef, int64_t ldo, int I, int B,
+                                        const int32_t* idx_ptr, const int32_t* idx, int n_shared,
+                                        const int64_t* dst, double* out, int64_t ldout,
+                                        double* max_imag, void* stream) {
+  if (I < 1 || B < 0 || ldo < I || (!idx_ptr && n_shared < 0)) {
+    set_error("fase_synth_paste_complex: bad sizes (I=%d, B=%d)", I, B);
+    return FASE_ERR_SHAPE;
+  }
+  if (B == 0) return FASE_OK;
+  if (!phi2 || !sel || !coef || (!idx && (idx_ptr || n_shared > 0)) || !out) {
+    set_error("fase_synth_paste_complex: null pointer");
+    return FASE_ERR_SHAPE;
+  }
+  synth_paste_complex_kernel<<<B, kSynthThreads, 0, as_stream(stream)>>>(
+      phi2, ldphi, sel, coef, ldo, I, idx_ptr, idx, n_shared, dst, out, ldout, max_imag);
+  return check_launch("fase_synth_paste_complex");
 }
 
 extern "C" int fase_l2_flush(void* buf, size_t bytes, void* stream) {

@@ -58,6 +58,25 @@ __device__ __forceinline__ double synth_terms(const double* __restrict__ phi, in
   return g;
 }
 
+// ---- complex128 arithmetic exactly as numpy evaluates it --------------------
+// (numpy 2.x contiguous complex loops, checked bit-for-bit against np on the
+// build host: tests/golden/complex_arith.npz)
+//
+// product x * y = (fma(xr, yr, -(xi*yi)), fma(xr, yi, xi*yr)): the first
+// operand's real part enters both fused multiply-adds.
+__device__ __forceinline__ double2 np_cmul(double xr, double xi, double yr, double yi) {
+  return make_double2(__fma_rn(xr, yr, -__dmul_rn(xi, yi)), __fma_rn(xr, yi, __dmul_rn(xi, yr)));
+}
+
+// |z| = larger * sqrt(fma(r, r, 1)), r = smaller / larger (0 when both vanish).
+__device__ __forceinline__ double np_cabs(double re, double im) {
+  const double a = fabs(re), b = fabs(im);
+  const double hi = fmax(a, b), lo = fmin(a, b);
+  if (hi == 0.0) return 0.0;
+  const double r = __ddiv_rn(lo, hi);
+  return __dmul_rn(__dsqrt_rn(__fma_rn(r, r, 1.0)), hi);
+}
+
 __device__ __forceinline__ double2 ldg2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }

@@ -269,6 +269,86 @@ int launch_weigh(const double* x, int64_t ldx, const double* w, int64_t ldw, int
 
 bool operand_ok(const double* ptr, int64_t ld) { return ptr && aligned16(ptr) && (ld % 2 == 0); }
 
+// ---- complex tables ---------------------------------------------------------
+//
+// A complex dictionary lives on the device in the conjugate-split layout:
+// row 2k = Re phi_k, row 2k+1 = -Im phi_k (each ldphi doubles). Read as K rows
+// of 2*ldphi doubles, row k is P_k = [A_k | -B_k] (phi = A + iB), so with
+// w2 = [w | w] the Gram table C = conj(Phi) W Phi^T (fast.py:129-131) is
+//   Re C = (P o w2) P^T,   Im C = (P o w2) Q^T,   Q_l = [B_l | A_l],
+// two real DMMA contractions of depth 2*ldphi. Both run in symmetric mode
+// (tiles bm <= bn only); the pack kernel reads the upper triangle and emits
+// the table row by row as conj(C[u, :]) -- the operand of the recursion's
+// update (fast.py:246) -- mirroring the strict lower triangle exactly like
+// the reference's Hermitian fill (fast.py:132-137) and forcing a real
+// diagonal (_finish_tables, fast.py:97-100).
+
+// w2[i] = w[i mod ldphi] for i mod ldphi < M, else 0
+__global__ void dup_weight_kernel(const double* __restrict__ w, int M, int64_t ldphi,
+                                  double* __restrict__ w2) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < 2 * ldphi;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t m = i < ldphi ? i : i - ldphi;
+    w2[i] = m < M ? w[m] : 0.0;
+  }
+}
+
+// Q_k = [-(P_k second half) | P_k first half] = [B_k | A_k]
+__global__ void swap_halves_kernel(const double* __restrict__ P, int K, int64_t ldphi,
+                                   double* __restrict__ Q) {
+  const int64_t total = static_cast<int64_t>(K) * 2 * ldphi;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t k = i / (2 * ldphi);
+    const int64_t c = i - k * 2 * ldphi;
+    const double* row = P + k * 2 * ldphi;
+    Q[i] = c < ldphi ? -row[ldphi + c] : row[c - ldphi];
+  }
+}
+
+// T[u, l] = conj(C[u, l]) for l < ldt (zero past K): u < l (Re[u,l], -Im[u,l]);
+// u > l (Re[l,u], Im[l,u]); u == l (Re[u,u], -0.0). 32 x 32 tiles, the
+// transposed Im tile staged through shared memory.
+__global__ void hermitian_pack_kernel(const double* __restrict__ re, const double* __restrict__ im,
+                                      int64_t ldk, int K, double2* __restrict__ T, int64_t ldt) {
+  __shared__ double s_im_t[32][33];
+  const int u0 = blockIdx.y * 32, l0 = blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  // Im[l0 + i, u0 + tx] for the tile's lower part (u > l): transposed read
+  for (int i = ty; i < 32; i += 8) {
+    const int l = l0 + i, u = u0 + tx;
+    s_im_t[i][tx] = (l < K && u < K && l < u) ? im[static_cast<int64_t>(l) * ldk + u] : 0.0;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int u = u0 + i, l = l0 + tx;
+    if (u >= K || l >= ldt) continue;
+    double2 v;
+    if (l >= K) {
+      v = make_double2(0.0, 0.0);
+    } else if (u < l) {
+      v = make_double2(re[static_cast<int64_t>(u) * ldk + l], -im[static_cast<int64_t>(u) * ldk + l]);
+    } else if (u > l) {
+      v = make_double2(re[static_cast<int64_t>(u) * ldk + l], s_im_t[tx][i]);  // Re bit-symmetric
+    } else {
+      v = make_double2(re[static_cast<int64_t>(u) * ldk + u], -0.0);
+    }
+    T[static_cast<int64_t>(u) * ldt + l] = v;
+  }
+}
+
+size_t complex_gram_parts(int K, int64_t ldphi, size_t* off) {
+  const size_t row = 2 * static_cast<size_t>(ldphi);
+  const size_t ldk = (static_cast<size_t>(K) + 1) / 2 * 2;
+  size_t o = 0;
+  off[0] = o; o += row;                                 // w2
+  off[1] = o; o += static_cast<size_t>(K) * row;        // P o w2
+  off[2] = o; o += static_cast<size_t>(K) * row;        // Q
+  off[3] = o; o += static_cast<size_t>(K) * ldk;        // Re C
+  off[4] = o; o += static_cast<size_t>(K) * ldk;        // Im C
+  return o * sizeof(double);
+}
+
 }  // namespace
 }  // namespace fase
 
@@ -367,4 +447,55 @@ extern "C" int fase_weigh(const double* x, int64_t ldx, const double* w, int64_t
     return FASE_ERR_SHAPE;
   }
   return launch_weigh(x, ldx, w, ldw, rows, M, out, ldo, as_stream(stream), "fase_weigh");
+}
+
+extern "C" size_t fase_gram_complex_workspace(int K, int64_t ldphi) {
+  size_t off[5];
+  return K < 1 || ldphi < 1 ? 0 : complex_gram_parts(K, ldphi, off);
+}
+
+extern "C" int fase_gram_complex(const double* phi2, int64_t ldphi, const double* w, int K, int M,
+                                 double* T, int64_t ldt, void* ws, size_t ws_bytes, void* stream) {
+  if (K < 1 || M < 1) {
+    set_error("fase_gram_complex: K and M must be positive (K=%d, M=%d)", K, M);
+    return FASE_ERR_SHAPE;
+  }
+  if (!operand_ok(phi2, ldphi) || ldphi < M || !w || !T || !aligned16(T) || ldt < K) {
+    set_error("fase_gram_complex: bad operand (null, misaligned, odd or short leading dimension)");
+    return FASE_ERR_SHAPE;
+  }
+  size_t off[5];
+  if (!ws || !aligned16(ws) || ws_bytes < complex_gram_parts(K, ldphi, off)) {
+    set_error("fase_gram_complex: workspace must hold fase_gram_complex_workspace(K, ldphi) bytes");
+    return FASE_ERR_SHAPE;
+  }
+  double* base = static_cast<double*>(ws);
+  double* w2 = base + off[0];
+  double* pw = base + off[1];
+  double* qm = base + off[2];
+  double* cre = base + off[3];
+  double* cim = base + off[4];
+  const int64_t row = 2 * ldphi;
+  const int64_t ldk = (K + 1) / 2 * 2;
+  const cudaStream_t s = as_stream(stream);
+  dup_weight_kernel<<<(static_cast<unsigned>(row) + 255) / 256, 256, 0, s>>>(w, M, ldphi, w2);
+  int st = check_launch("fase_gram_complex (weights)");
+  if (st != FASE_OK) return st;
+  st = launch_weigh(phi2, row, w2, 0, K, static_cast<int>(row), pw, row, s, "fase_gram_complex (weigh)");
+  if (st != FASE_OK) return st;
+  const int64_t total = static_cast<int64_t>(K) * row;
+  swap_halves_kernel<<<static_cast<unsigned>(total / 256 + 1 < 148 * 16 ? total / 256 + 1 : 148 * 16),
+                       256, 0, s>>>(phi2, K, ldphi, qm);
+  st = check_launch("fase_gram_complex (swap)");
+  if (st != FASE_OK) return st;
+  GemmParams pr{pw, row, phi2, row, cre, ldk, K, K, static_cast<int>(row)};
+  st = launch<TileMain, true>(pr, s, "fase_gram_complex (re)");
+  if (st != FASE_OK) return st;
+  GemmParams pi{pw, row, qm, row, cim, ldk, K, K, static_cast<int>(row)};
+  st = launch<TileMain, true>(pi, s, "fase_gram_complex (im)");
+  if (st != FASE_OK) return st;
+  dim3 grid(static_cast<unsigned>((ldt + 31) / 32), static_cast<unsigned>((K + 31) / 32));
+  hermitian_pack_kernel<<<grid, dim3(32, 8), 0, s>>>(cre, cim, ldk, K, reinterpret_cast<double2*>(T),
+                                                     ldt);
+  return check_launch("fase_gram_complex (pack)");
 }

@@ -1,0 +1,490 @@
+// The FaSE recursion for complex-valued dictionaries (dft, bdft, their unions,
+// complex file dictionaries): one persistent CTA per loss block.
+//
+// Reference: the same loop as the real kernel (fast.py:224-255, selection
+// reference.py:55-85) in complex128:
+//
+//   metric_k = |R_k| * D_k                  np.abs: hypot as numpy evaluates it
+//   q        = max(q, 1e-13 * max metric);  u = lowest k with metric_k >= max - q
+//   p        = R_u * (D_u * D_u);  c = gamma * p
+//   R_k     <- R_k - c * conj(C[u, k])       numpy's fused complex multiply
+//
+// The table handed in stores conj(C[u, :]) row by row (fase_gram_complex), so
+// the update streams one 16-byte complex per element. Every operation is the
+// one numpy performs (common.cuh: np_cmul, np_cabs), so given the same R0,
+// table and D the run is bit-identical to the reference.
+//
+// Selection without a hypot per element and iteration: the update pass keeps a
+// cheap proxy P_k = (re^2 + im^2) * D_k^2 and its running max. The exact metric
+// differs from sqrt(P_k) by a few ulp (<= 8 * 2^-53 relative), so only elements
+// with P_k above a conservative bound of the threshold (margins 2^-40) can be
+// the maximum or reach the threshold. Those candidates (normally the predicted
+// atom plus its structural twins, e.g. a conjugate-frequency partner) get the
+// exact metric and land in a short shared list; after the second barrier every
+// warp resolves the list redundantly (exact max, tie quantum, lowest index), so
+// an iteration still has two barriers. An overflowing list, or proxies too
+// small / large to trust, fall back to an exact pass over all elements.
+//
+// Layout: thread t owns complex elements k = j*NT + t, j < EP (R in registers,
+// (D, D^2) in shared memory or registers), so a table row streams with
+// coalesced 16-byte loads; the predicted row is staged by TMA as in the real
+// kernel, and per-block geometries compose rows G0[u] - sum C_j[u] the same way.
+// Leading dimensions (ldg, ldr, ldo, chunk_stride) count complex elements.
+
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace fase {
+namespace {
+
+constexpr unsigned kNone = 0xffffffffu;
+constexpr int kCap = 64;  // candidate list capacity
+
+template <int NT, int EP, int MINB, bool kDsmem, bool kChunked, bool kRecord>
+__global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fase_iterate_args a) {
+  constexpr int NW = NT / 32;
+  constexpr int kSeg = EP < 3 ? EP : 3;
+
+  __shared__ long long s_key[NW];
+  __shared__ unsigned s_arg[NW];
+  __shared__ int s_cnt[2];
+  __shared__ double s_cm[kCap];            // candidate exact metric
+  __shared__ unsigned s_ck[kCap];          // candidate index
+  __shared__ __align__(16) double2 s_cr[kCap];  // candidate R
+  __shared__ double s_cd[kCap];            // candidate D
+  __shared__ __align__(8) uint64_t s_bar[kSeg];
+  extern __shared__ double2 s_dyn[];
+  double2* s_row = s_dyn;          // staged row: element j*NT + t
+  double2* s_D = s_dyn + EP * NT;  // kDsmem: (D, D^2) per element
+
+  const int b = blockIdx.x;
+  const int t = threadIdx.x;
+  const int lane = t & 31;
+  const int warp = t >> 5;
+  const int K = a.K;
+  const double kDead = __longlong_as_double(static_cast<long long>(0xfff0000000000000ULL));
+
+  if (t == 0) {
+    for (int sg = 0; sg < kSeg; ++sg) mbar_init(&s_bar[sg], 1);
+    fence_mbar_init();
+    s_cnt[0] = 0;
+    s_cnt[1] = 0;
+  }
+
+  const double* D = a.D + (a.ldd ? static_cast<int64_t>(b) * a.ldd : 0);
+  const double* R0 = a.R0 + 2 * static_cast<int64_t>(b) * a.ldr;
+  const int32_t* cids = nullptr;
+  int nch = 0;
+  if (kChunked) {
+    nch = a.chunk_count[b];
+    cids = a.chunk_ids + static_cast<int64_t>(b) * a.chunk_list_ld;
+  }
+
+  double r[EP][2];
+  double dreg[kDsmem ? 1 : EP][2];
+  auto dpair = [&](int j) -> double2 {  // (D, D^2); dead: (-inf, -inf)
+    if constexpr (kDsmem)
+      return s_D[j * NT + t];
+    else
+      return make_double2(dreg[j][0], dreg[j][1]);
+  };
+  auto proxy = [](double re, double im, double d2) {
+    return mul_rn(__fma_rn(re, re, mul_rn(im, im)), d2);
+  };
+  double best = kDead;
+  unsigned barg = kNone;
+#pragma unroll
+  for (int j = 0; j < EP; ++j) {
+    const int k = j * NT + t;
+    r[j][0] = k < K ? R0[2 * k] : 0.0;
+    r[j][1] = k < K ? R0[2 * k + 1] : 0.0;
+    const double dk = k < K ? D[k] : 0.0;
+    const double2 dd = dk != 0.0 ? make_double2(dk, mul_rn(dk, dk)) : make_double2(kDead, kDead);
+    if constexpr (kDsmem) {
+      s_D[j * NT + t] = dd;
+    } else {
+      dreg[j][0] = dd.x;
+      dreg[j][1] = dd.y;
+    }
+    const double pk = proxy(r[j][0], r[j][1], dd.y);
+    if (pk > best) {
+      best = pk;
+      barg = static_cast<unsigned>(k);
+    }
+  }
+
+  int32_t* sel = a.sel + static_cast<int64_t>(b) * a.ldo;
+  double* proj = a.proj + 2 * static_cast<int64_t>(b) * a.ldo;
+  double* coef = a.coef + 2 * static_cast<int64_t>(b) * a.ldo;
+  const int64_t ldg2x = 2 * a.ldg;  // row stride in doubles
+  double q = 0.0;
+
+  for (int it = 0; it < a.I; ++it) {
+    // ---- warp max of the proxy and the lowest index attaining it
+    {
+      const long long key = __double_as_longlong(best);
+      const int kh = static_cast<int>(key >> 32);
+      const unsigned kl = static_cast<unsigned>(key);
+      const int wh = __reduce_max_sync(0xffffffffu, kh);
+      const unsigned wl = __reduce_max_sync(0xffffffffu, kh == wh ? kl : 0u);
+      const unsigned wa = __reduce_min_sync(0xffffffffu, (kh == wh && kl == wl) ? barg : kNone);
+      if (lane == 0) {
+        s_key[warp] = (static_cast<long long>(wh) << 32) | wl;
+        s_arg[warp] = wa;
+      }
+    }
+    __syncthreads();
+    if (t == 0) s_cnt[(it + 1) & 1] = 0;  // next iteration's list (last read before this barrier)
+    long long top_key, wkey;
+    unsigned guess;
+    {
+      const long long sk = lane < NW ? s_key[lane] : LLONG_MIN;
+      const unsigned sa = lane < NW ? s_arg[lane] : kNone;
+      wkey = s_key[warp];
+      const int h = static_cast<int>(sk >> 32);
+      const unsigned l = static_cast<unsigned>(sk);
+      const int bh = __reduce_max_sync(0xffffffffu, h);
+      const unsigned bl = __reduce_max_sync(0xffffffffu, h == bh ? l : 0u);
+      guess = __reduce_min_sync(0xffffffffu, (h == bh && l == bl) ? sa : kNone);
+      top_key = (static_cast<long long>(bh) << 32) | bl;
+    }
+    if (top_key < 0) {  // every atom degenerate (NoSelectableAtomError): mark and stop
+      for (int k = it + t; k < a.I; k += NT) {
+        sel[k] = -1;
+        proj[2 * k] = proj[2 * k + 1] = 0.0;
+        coef[2 * k] = coef[2 * k + 1] = 0.0;
+      }
+      return;
+    }
+    if (t == 0) {
+      fence_proxy_async_smem();
+      const double* grow = a.G0 + static_cast<int64_t>(guess) * ldg2x;
+#pragma unroll
+      for (int sg = 0; sg < kSeg; ++sg) {
+        const int j0 = sg * EP / kSeg, j1 = (sg + 1) * EP / kSeg;
+        const unsigned bytes = static_cast<unsigned>((j1 - j0) * NT * sizeof(double2));
+        mbar_arrive_expect_tx(&s_bar[sg], bytes);
+        tma_load_1d(s_row + j0 * NT, grow + 2 * j0 * NT, bytes, &s_bar[sg]);
+      }
+    }
+
+    // ---- candidates: P_k >= a lower bound of thr^2 (conservative margins)
+    const double pmax = __longlong_as_double(top_key);
+    // proxies outside [2^-900, 2^900] lose the relative accuracy the bound needs
+    const bool trusted = pmax >= 0x1p-900 && pmax <= 0x1p+900;
+    double pc = 0.0;
+    if (trusted) {
+      const double s = sqrt(pmax);
+      const double top_lo = s * (1.0 - 0x1p-40), top_hi = s * (1.0 + 0x1p-40);
+      const double thr_lo = top_lo - fmax(q, 1e-13 * top_hi) * (1.0 + 0x1p-40);
+      pc = thr_lo > 0.0 ? thr_lo * thr_lo * (1.0 - 0x1p-40) : 0.0;
+    }
+    if (trusted && pc > 0.0 && wkey >= 0 && __longlong_as_double(wkey) >= pc) {  // warp-uniform
+#pragma unroll
+      for (int j = 0; j < EP; ++j) {
+        const double2 dd = dpair(j);
+        if (proxy(r[j][0], r[j][1], dd.y) >= pc) {  // exact metric after the barrier
+          const int slot = atomicAdd(&s_cnt[it & 1], 1);
+          if (slot < kCap) {
+            s_ck[slot] = static_cast<unsigned>(j * NT + t);
+            s_cr[slot] = make_double2(r[j][0], r[j][1]);
+            s_cd[slot] = dd.x;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int cnt = s_cnt[it & 1];
+
+    unsigned u;
+    double2 ru;
+    double du;
+    if (trusted && pc > 0.0 && cnt >= 1 && cnt <= kCap) {
+      // ---- resolve the list in every warp: exact max, quantum, lowest index
+      // one lane per entry: exact metric (entries past 32 are rare)
+      long long mk = LLONG_MIN;
+      double m0 = -1.0;
+      for (int l = lane; l < cnt; l += 32) {
+        const double2 rv = s_cr[l];
+        const double m = mul_rn(np_cabs(rv.x, rv.y), s_cd[l]);
+        if (l == lane) m0 = m;
+        else s_cm[l] = m;
+        const long long v = __double_as_longlong(m);  // metrics of candidates are >= 0
+        mk = v > mk ? v : mk;
+      }
+      const double top = __longlong_as_double(warp_max_i64(mk));
+      if (top > 0.0 && top < __longlong_as_double(0x7ff0000000000000LL)) q = fmax(q, mul_rn(1e-13, top));
+      const double thr = q > 0.0 ? sub_rn(top, q) : top;
+      unsigned ub = kNone;
+      int ib = 0;
+      for (int l = lane; l < cnt; l += 32) {
+        const unsigned kk = (l == lane ? m0 : s_cm[l]) >= thr ? s_ck[l] : kNone;
+        if (kk < ub) {
+          ub = kk;
+          ib = l;
+        }
+      }
+      u = __reduce_min_sync(0xffffffffu, ub);
+      const int src = __ffs(__ballot_sync(0xffffffffu, ub == u)) - 1;
+      ib = __shfl_sync(0xffffffffu, ib, src);
+      ru = s_cr[ib];
+      du = s_cd[ib];
+    } else {
+      // ---- exact pass over every element (block-uniform branch). One rolled
+      // loop per pass: element jj is picked out of the register array with
+      // selects, so the division / square root appear once in the code.
+      auto element = [&](int jj, double& re, double& im, double& d) {
+        re = 0.0;
+        im = 0.0;
+        d = kDead;
+#pragma unroll
+        for (int j = 0; j < EP; ++j)
+          if (j == jj) {
+            re = r[j][0];
+            im = r[j][1];
+            d = dpair(j).x;
+          }
+      };
+      double mb = kDead;
+#pragma unroll 1
+      for (int jj = 0; jj < EP; ++jj) {
+        double re, im, d;
+        element(jj, re, im, d);
+        const double m = mul_rn(np_cabs(re, im), d);  // dead: -inf or NaN
+        mb = m > mb ? m : mb;
+      }
+      const long long wk = warp_max_i64(__double_as_longlong(mb));
+      if (lane == 0) s_key[warp] = wk;
+      __syncthreads();
+      long long tk = LLONG_MIN;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) tk = s_key[w] > tk ? s_key[w] : tk;
+      const double top = __longlong_as_double(tk);
+      if (tk > 0 && tk < 0x7ff0000000000000LL) q = fmax(q, mul_rn(1e-13, top));
+      const double thr = q > 0.0 ? sub_rn(top, q) : top;
+      unsigned cand = kNone;
+      double2 rv = make_double2(0.0, 0.0);
+      double dv = 0.0;
+#pragma unroll 1
+      for (int jj = 0; jj < EP; ++jj) {
+        double re, im, d;
+        element(jj, re, im, d);
+        if (cand == kNone && mul_rn(np_cabs(re, im), d) >= thr) {
+          cand = static_cast<unsigned>(jj * NT + t);
+          rv = make_double2(re, im);
+          dv = d;
+        }
+      }
+      // exchange through the candidate arrays: s_key / s_arg are rewritten by
+      // fast warps before the next first barrier, the list only after it
+      const unsigned wmin = __reduce_min_sync(0xffffffffu, cand);
+      if (lane == 0) s_ck[warp] = wmin;
+      if (cand != kNone && cand == wmin) {
+        s_cr[warp] = rv;
+        s_cd[warp] = dv;
+      }
+      __syncthreads();
+      const unsigned su = lane < NW ? s_ck[lane] : kNone;
+      u = __reduce_min_sync(0xffffffffu, su);
+      const int uw = __ffs(__ballot_sync(0xffffffffu, su == u)) - 1;
+      ru = s_cr[uw];
+      du = s_cd[uw];
+    }
+
+    const double d2u = mul_rn(du, du);
+    const double pr = mul_rn(ru.x, d2u), pi = mul_rn(ru.y, d2u);
+    const double cr = mul_rn(a.gamma, pr), ci = mul_rn(a.gamma, pi);
+    if (t == 0) {
+      sel[it] = static_cast<int32_t>(u);
+      proj[2 * it] = pr;
+      proj[2 * it + 1] = pi;
+      coef[2 * it] = cr;
+      coef[2 * it + 1] = ci;
+    }
+
+    auto wait_all = [&]() {
+#pragma unroll
+      for (int sg = 0; sg < kSeg; ++sg) mbar_wait(&s_bar[sg], it & 1);
+    };
+    // ---- R <- R - c * conj(C[u, :]) fused with the next running max of the proxy
+    auto update = [&](auto row_elem, auto staged) {
+      best = kDead;
+      barg = kNone;
+#pragma unroll
+      for (int j = 0; j < EP; ++j) {
+        if constexpr (decltype(staged)::value) {
+#pragma unroll
+          for (int sg = 0; sg < kSeg; ++sg)
+            if (j == sg * EP / kSeg) mbar_wait(&s_bar[sg], it & 1);
+        }
+        const double2 g = row_elem(j);
+        const double2 dd = dpair(j);
+        const double2 x = np_cmul(cr, ci, g.x, g.y);
+        r[j][0] = sub_rn(r[j][0], x.x);
+        r[j][1] = sub_rn(r[j][1], x.y);
+        const double pk = proxy(r[j][0], r[j][1], dd.y);
+        if (pk > best) {
+          best = pk;
+          barg = static_cast<unsigned>(j * NT + t);
+        }
+      }
+    };
+    using Staged = std::true_type;
+    using Direct = std::false_type;
+    if (kChunked && nch > 0) {
+      wait_all();
+      if (u != guess) {
+        const double* urow = a.G0 + static_cast<int64_t>(u) * ldg2x + 2 * t;
+#pragma unroll 4
+        for (int j = 0; j < EP; ++j) s_row[j * NT + t] = ldg2(urow + 2 * j * NT);
+      }
+      for (int ch = 0; ch < nch; ++ch) {
+        const double* crow = a.chunk_tables + 2 * static_cast<int64_t>(cids[ch]) * a.chunk_stride +
+                             static_cast<int64_t>(u) * ldg2x + 2 * t;
+#pragma unroll 4
+        for (int j = 0; j < EP; ++j) {
+          const double2 v = ldg2(crow + 2 * j * NT);
+          double2 g = s_row[j * NT + t];
+          g.x = sub_rn(g.x, v.x);
+          g.y = sub_rn(g.y, v.y);
+          s_row[j * NT + t] = g;
+        }
+      }
+      update([&](int j) { return s_row[j * NT + t]; }, Direct{});
+      fence_proxy_async_smem();
+    } else if (u == guess) {
+      update([&](int j) { return s_row[j * NT + t]; }, Staged{});
+    } else {
+      wait_all();
+      const double* urow = a.G0 + static_cast<int64_t>(u) * ldg2x + 2 * t;
+      update([&](int j) { return ldg2(urow + 2 * j * NT); }, Direct{});
+    }
+    if (kRecord) {
+      double* dst = a.R_log + 2 * ((static_cast<int64_t>(b) * a.I + it) * a.ldr);
+#pragma unroll
+      for (int j = 0; j < EP; ++j) {
+        const int k = j * NT + t;
+        if (k < K) *reinterpret_cast<double2*>(dst + 2 * k) = make_double2(r[j][0], r[j][1]);
+      }
+    }
+  }
+
+  if (a.R_out) {
+    double* dst = a.R_out + 2 * static_cast<int64_t>(b) * a.ldr;
+#pragma unroll
+    for (int j = 0; j < EP; ++j) {
+      const int k = j * NT + t;
+      if (k < K) *reinterpret_cast<double2*>(dst + 2 * k) = make_double2(r[j][0], r[j][1]);
+    }
+  }
+}
+
+using KernelFn = void (*)(const fase_iterate_args);
+
+struct Variant {
+  int nt;
+  int ep;  // complex elements per thread
+  bool dsmem;
+  KernelFn plain;
+  KernelFn chunked;
+  KernelFn record;
+};
+
+#define FASE_CV(NT, EP, MINB, DS)                                      \
+  {NT,                                                                  \
+   EP,                                                                  \
+   DS,                                                                  \
+   fase_iterate_complex_kernel<NT, EP, MINB, DS, false, false>,         \
+   fase_iterate_complex_kernel<NT, EP, MINB, DS, true, false>,          \
+   fase_iterate_complex_kernel<NT, EP, MINB, DS, false, true>}
+// Ordered by capacity NT*EP (complex elements); the first that holds K is used.
+// The complex update needs more registers than the real one (4 per element
+// plus the exact-metric paths), so the 256-thread shapes above 6 elements per
+// thread run two CTAs per SM rather than spill at the 80-register cap.
+const Variant kVariants[] = {
+    FASE_CV(128, 1, 4, false), FASE_CV(128, 2, 4, false), FASE_CV(128, 4, 4, false),
+    FASE_CV(128, 8, 4, true),  FASE_CV(256, 5, 3, true),  FASE_CV(256, 6, 3, true),
+    FASE_CV(256, 7, 2, true),  FASE_CV(256, 8, 2, true),  FASE_CV(256, 9, 2, true),
+    FASE_CV(256, 10, 2, true), FASE_CV(512, 6, 1, true),  FASE_CV(512, 8, 1, true),
+    FASE_CV(512, 10, 1, true), FASE_CV(512, 12, 1, true),
+};
+#undef FASE_CV
+
+const Variant* pick_variant(int K) {
+  for (const Variant& v : kVariants)
+    if (v.nt * v.ep >= K) return &v;
+  return nullptr;
+}
+
+}  // namespace
+}  // namespace fase
+
+using namespace fase;
+
+extern "C" int fase_max_atoms_complex(void) {
+  const Variant& last = kVariants[sizeof(kVariants) / sizeof(kVariants[0]) - 1];
+  return last.nt * last.ep;
+}
+
+extern "C" int fase_table_ld_complex(int K) {
+  if (K < 1) return 0;
+  const Variant* v = pick_variant(K);
+  return v ? v->nt * v->ep : 0;
+}
+
+extern "C" int fase_iterate_complex(const fase_iterate_args* args, void* stream) {
+  if (!args) {
+    set_error("fase_iterate_complex: null argument block");
+    return FASE_ERR_PARAMETER;
+  }
+  const fase_iterate_args& a = *args;
+  if (a.K < 1 || a.B < 0 || a.I < 1) {
+    set_error("fase_iterate_complex: bad sizes (K=%d, B=%d, I=%d)", a.K, a.B, a.I);
+    return FASE_ERR_SHAPE;
+  }
+  if (!(a.gamma > 0.0 && a.gamma <= 1.0)) {
+    set_error("fase_iterate_complex: gamma must lie in (0, 1], got %g", a.gamma);
+    return FASE_ERR_PARAMETER;
+  }
+  if (a.B == 0) return FASE_OK;
+  if (!a.G0 || !aligned16(a.G0) || a.ldg < a.K || !a.D || !a.R0 || !aligned16(a.R0) ||
+      a.ldr < a.K || (a.ldd != 0 && a.ldd < a.K) || !a.sel || !a.proj || !a.coef || a.ldo < a.I ||
+      (a.R_out && !aligned16(a.R_out)) || (a.R_log && !aligned16(a.R_log))) {
+    set_error("fase_iterate_complex: bad operand (null, misaligned or short leading dimension)");
+    return FASE_ERR_SHAPE;
+  }
+  if (a.chunk_count && (!a.chunk_ids || !a.chunk_tables || !aligned16(a.chunk_tables))) {
+    set_error("fase_iterate_complex: chunk tables given without ids / aligned storage");
+    return FASE_ERR_SHAPE;
+  }
+  if (a.chunk_count && a.R_log) {
+    set_error("fase_iterate_complex: R_log recording is not available with chunked tables");
+    return FASE_ERR_UNSUPPORTED;
+  }
+  const Variant* v = pick_variant(a.K);
+  if (!v) {
+    set_error("fase_iterate_complex: K=%d exceeds the largest kernel variant (%d atoms)", a.K,
+              fase_max_atoms_complex());
+    return FASE_ERR_UNSUPPORTED;
+  }
+  if (a.ldg < v->nt * v->ep || (a.chunk_count && a.chunk_stride < a.ldg * a.K)) {
+    set_error("fase_iterate_complex: table rows must be zero-padded to fase_table_ld_complex(K)=%d "
+              "(ldg=%lld)", v->nt * v->ep, static_cast<long long>(a.ldg));
+    return FASE_ERR_SHAPE;
+  }
+  KernelFn fn = a.chunk_count ? v->chunked : (a.R_log ? v->record : v->plain);
+  const size_t smem = static_cast<size_t>(v->nt) * v->ep * sizeof(double2) * (v->dsmem ? 2 : 1);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) {
+    set_error("fase_iterate_complex: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return FASE_ERR_CUDA;
+  }
+  fn<<<a.B, v->nt, smem, as_stream(stream)>>>(a);
+  return check_launch("fase_iterate_complex");
+}

@@ -253,25 +253,32 @@ class Dictionary:
         return self._device_cache[key]
 
     def device_matrix(self, device):
-        """(K, ld) float64 Phi in HBM, cached per device.
+        """Phi in HBM, cached per device: (K, ld) float64 for real sets, and
+        for complex sets the (2K, ld) conjugate-split matrix -- row 2k =
+        Re phi_k, row 2k+1 = -Im phi_k (include/fase_b200.h, "Complex-valued
+        dictionaries").
 
         Separable parts are expanded by the native outer-product kernel;
-        dense real atoms are uploaded. Complex sets are rejected here.
+        dense atoms are uploaded.
         """
         import torch
 
         from . import _native
-        from .errors import UnsupportedDictionaryError
 
-        if not self._is_real:
-            raise UnsupportedDictionaryError(
-                "complex-valued dictionaries are not supported by the FP64 GPU path")
         dev = torch.device(device)
         key = (dev.type, dev.index)
         cached = self._device_cache.get(key)
         if cached is not None:
             return cached
         m, n = self._shape
+        if not self._is_real:
+            flat = self._dense.reshape(self._k, -1)
+            split = np.zeros((2 * self._k, self.ld), dtype=np.float64)
+            split[0::2, : m * n] = flat.real
+            split[1::2, : m * n] = -flat.imag
+            phi = torch.from_numpy(split).to(dev)
+            self._device_cache[key] = phi
+            return phi
         phi = torch.zeros((self._k, self.ld), dtype=torch.float64, device=dev)
         if self._parts is not None:
             row = 0

@@ -87,12 +87,14 @@ def provenance_hash(dictionary: Dictionary, weight) -> int:
 
 
 class GramTable:
-    """Weighted cross-energies C = Phi W Phi^T and normalizers D of one weight.
+    """Weighted cross-energies C = conj(Phi) W Phi^T and normalizers D of one weight.
 
     Reference-compatible construction ``GramTable(c, d, provenance)`` from host
     arrays (``fast.py:55-85``), or device-born from ``build_gram_tables``.
-    On the device the table is a (K, ldg) float64 matrix, ldg = K rounded up
-    to even, exactly symmetric.
+    On the device a real table is a (K, ldg) float64 matrix, exactly
+    symmetric; a complex table is a (K, ldt) complex128 matrix holding
+    conj(C) row by row (the recursion's update operand), exactly Hermitian.
+    Rows are zero-padded to the recursion kernel's capacity.
     """
 
     def __init__(self, c=None, d=None, provenance: int = 0, *, G=None, D=None, n_alive=None):
@@ -114,13 +116,20 @@ class GramTable:
             self._host_d = np.asarray(d, dtype=np.float64)
             self._k = c.shape[0]
             self._n_alive = int(np.count_nonzero(self._host_d))
+            self._complex = bool(np.iscomplexobj(c) and np.any(c.imag != 0))
         else:
             self._k = int(G.shape[0])
             self._n_alive = int(n_alive) if n_alive is not None else None
+            self._complex = bool(G.is_complex())
 
     @property
     def size(self) -> int:
         return self._k
+
+    @property
+    def is_complex(self) -> bool:
+        """True when the table carries imaginary parts (complex dictionaries)."""
+        return self._complex
 
     @property
     def n_alive(self) -> int:
@@ -138,35 +147,53 @@ class GramTable:
     def c(self) -> np.ndarray:
         """Host complex128 (K, K) copy (downloads a device table on first use)."""
         if self._host_c is None:
-            self._host_c = self._G[:, : self._k].cpu().numpy().astype(np.complex128)
+            if self._G.is_complex():
+                self._host_c = np.conj(self._G[:, : self._k].cpu().numpy())
+            else:
+                self._host_c = self._G[:, : self._k].cpu().numpy().astype(np.complex128)
         return self._host_c
 
     def degenerate(self) -> np.ndarray:
         return self.d == 0.0
 
-    def device_tables(self, device):
-        """(G, D) on ``device``; host-born tables are uploaded once (real part).
+    def device_tables(self, device, complex_rows: bool = False):
+        """(G, D) on ``device`` in the layout the recursion needs.
 
-        Raises UnsupportedDictionaryError for a table with imaginary content.
+        ``complex_rows=False``: real (K, table_ld(K)) float64 table -- raises
+        UnsupportedDictionaryError when the table has imaginary content.
+        ``complex_rows=True``: (K, table_ld_complex(K)) complex128 rows of
+        conj(C). Host-born or other-layout tables are converted once and cached.
         """
         torch = _torch()
+        k = self._k
         if self._G is not None:
             if self._G.device != device:
                 raise ShapeError(f"table lives on {self._G.device}, run requested on {device}")
-            return self._G, self._D
-        key = (device.type, device.index)
+            if self._G.is_complex() == complex_rows:
+                return self._G, self._D
+        key = (device.type, device.index, complex_rows)
         if key not in self._uploaded:
-            c = self._host_c
-            if np.iscomplexobj(c):
-                if np.any(c.imag != 0):
+            if complex_rows:
+                T = torch.zeros((k, _native.table_ld_complex(k)), dtype=torch.complex128,
+                                device=device)
+                if self._G is not None:  # a real device table: conj(C) = C
+                    T[:, :k].copy_(self._G[:, :k])
+                else:
+                    T[:, :k].copy_(torch.from_numpy(np.conj(np.asarray(self._host_c,
+                                                                       dtype=np.complex128))))
+                self._uploaded[key] = (T, self._D if self._D is not None else
+                                       torch.from_numpy(self._host_d.copy()).to(device))
+            else:
+                if self._complex:
                     raise UnsupportedDictionaryError(
-                        "complex-valued tables are not supported by the FP64 GPU path")
-                c = c.real
-            k = self._k
-            G = torch.zeros((k, _native.table_ld(k)), dtype=torch.float64, device=device)
-            G[:, :k].copy_(torch.from_numpy(np.ascontiguousarray(c, dtype=np.float64)))
-            D = torch.from_numpy(self._host_d.copy()).to(device)
-            self._uploaded[key] = (G, D)
+                        "this table has imaginary parts: run it with a complex dictionary")
+                c = self._host_c if self._G is None else np.conj(
+                    self._G[:, :k].cpu().numpy())
+                c = np.asarray(c.real if np.iscomplexobj(c) else c, dtype=np.float64)
+                G = torch.zeros((k, _native.table_ld(k)), dtype=torch.float64, device=device)
+                G[:, :k].copy_(torch.from_numpy(np.ascontiguousarray(c)))
+                D = self._D if self._D is not None else torch.from_numpy(self._host_d.copy()).to(device)
+                self._uploaded[key] = (G, D)
         return self._uploaded[key]
 
 
@@ -177,11 +204,23 @@ def _device_vector(x: np.ndarray, length: int, device):
     return out
 
 
-def _gram_on_device(phi, w_dev, K: int, M: int, device):
+def _gram_on_device(phi, w_dev, K: int, M: int, device, complex_rows: bool = False):
+    """Real (K, table_ld) table, or complex (K, table_ld_complex) rows of conj(C)
+    from the conjugate-split matrix of a complex dictionary."""
     torch = _torch()
+    if complex_rows:
+        T = torch.zeros((K, _native.table_ld_complex(K)), dtype=torch.complex128, device=device)
+        _native.gram_complex(phi, w_dev, K, M, T)
+        return T
     G = torch.zeros((K, _native.table_ld(K)), dtype=torch.float64, device=device)
     _native.gram(phi, w_dev, K, M, G)
     return G
+
+
+def _real_view(R):
+    """(B, 2*ld) float64 view of a complex128 (B, ld) tensor (same storage)."""
+    torch = _torch()
+    return torch.view_as_real(R).reshape(R.shape[0], -1)
 
 
 def initial_products_into(dictionary: Dictionary, F, W, R0, ws, *, method: str = "auto") -> str:
@@ -195,6 +234,13 @@ def initial_products_into(dictionary: Dictionary, F, W, R0, ws, *, method: str =
     """
     K, M = len(dictionary), dictionary.area
     dev = R0.device
+    if R0.is_complex():
+        # conj(Phi) (F o W) = [Re Phi; -Im Phi] (F o W): the conjugate-split
+        # matrix as 2K real atoms writes (re, im) pairs straight into R0
+        if method == "separable":
+            raise UnsupportedDictionaryError("separable initial products need a real dictionary")
+        _native.init_products(dictionary.device_matrix(dev), F, W, 2 * K, M, _real_view(R0), ws=ws)
+        return "gemm"
     factors = dictionary.device_factors(dev) if method in ("auto", "separable") else None
     if method == "separable" and factors is None:
         raise UnsupportedDictionaryError("separable initial products need a separable dictionary")
@@ -229,10 +275,11 @@ def build_gram_tables(dictionary: Dictionary, weight, *, block: int = 256, count
     dev = resolve_device(device)
     K, M = len(dictionary), dictionary.area
     phi = dictionary.device_matrix(dev)
-    G = _gram_on_device(phi, _device_vector(w, dictionary.ld, dev), K, M, dev)
+    cplx = not dictionary.is_real
+    G = _gram_on_device(phi, _device_vector(w, dictionary.ld, dev), K, M, dev, cplx)
     D = torch.empty(K, dtype=torch.float64, device=dev)
     alive = torch.zeros(1, dtype=torch.int32, device=dev)
-    _native.gram_finish(G, K, D, alive)
+    (_native.gram_finish_complex if cplx else _native.gram_finish)(G, K, D, alive)
     if counter is not None:
         counter.table_pair_products(M, (K * K + K) // 2)
         counter.table_normalizers(K)
@@ -253,8 +300,13 @@ def initial_scalar_products(signal, weight, dictionary: Dictionary, *, counter=N
     K = len(dictionary)
     phi = dictionary.device_matrix(dev)
     f = _device_vector(s, dictionary.ld, dev).reshape(1, -1)
-    R0 = torch.empty((1, _round_up(K, 2)), dtype=torch.float64, device=dev)
-    _native.init_products(phi, f, _device_vector(w, dictionary.ld, dev), K, dictionary.area, R0)
+    wd = _device_vector(w, dictionary.ld, dev)
+    if dictionary.is_real:
+        R0 = torch.empty((1, _round_up(K, 2)), dtype=torch.float64, device=dev)
+        _native.init_products(phi, f, wd, K, dictionary.area, R0)
+    else:
+        R0 = torch.empty((1, K), dtype=torch.complex128, device=dev)
+        _native.init_products(phi, f, wd, 2 * K, dictionary.area, _real_view(R0))
     if counter is not None:
         counter.fase_initial(s.size, K)
     return R0[0, :K].cpu().numpy().astype(np.complex128)
@@ -345,18 +397,21 @@ class ChunkedTables:
         w0 = base.copy()
         w0[self.plan.base_lost] = 0.0
         phi = dictionary.device_matrix(device)
-        self.G0 = _gram_on_device(phi, _device_vector(w0, dictionary.ld, device), K, M, device)
+        self.complex = cplx = not dictionary.is_real
+        self.G0 = _gram_on_device(phi, _device_vector(w0, dictionary.ld, device), K, M, device,
+                                  cplx)
         ldg = self.G0.shape[1]
         nc = self.plan.n_classes
-        self.tables = torch.zeros((max(nc, 1), K, ldg), dtype=torch.float64, device=device)
+        self.tables = torch.zeros((max(nc, 1), K, ldg), dtype=self.G0.dtype, device=device)
         for j, samples in enumerate(self.plan.classes):
             cols = torch.from_numpy(samples.astype(np.int64)).to(device)
             width = _round_up(len(samples), 2)
-            sub = torch.zeros((K, width), dtype=torch.float64, device=device)
+            sub = torch.zeros((phi.shape[0], width), dtype=torch.float64, device=device)
             sub[:, : len(samples)] = phi.index_select(1, cols)
             wj = torch.zeros(width, dtype=torch.float64, device=device)
             wj[: len(samples)] = torch.from_numpy(base[samples]).to(device)
-            _native.gram(sub, wj, K, len(samples), self.tables[j])
+            (_native.gram_complex if cplx else _native.gram)(sub, wj, K, len(samples),
+                                                             self.tables[j])
         counts = np.diff(self.plan.ptr).astype(np.int32)
         lists = np.zeros((len(counts), max(1, int(counts.max(initial=0)))), dtype=np.int32)
         for b in np.flatnonzero(counts):
@@ -371,7 +426,7 @@ class ChunkedTables:
     def table_bytes(dictionary: Dictionary, masks: np.ndarray) -> int:
         plan = chunk_plan(masks)
         k = len(dictionary)
-        return (plan.n_classes + 1) * k * _round_up(k, 2) * 8
+        return (plan.n_classes + 1) * k * _round_up(k, 2) * (8 if dictionary.is_real else 16)
 
 
 def _validate_masks(masks, dictionary: Dictionary, n_blocks: int):
@@ -415,14 +470,14 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
         BatchResult with device tensors.
     """
     torch = _torch()
-    if not dictionary.is_real:
-        raise UnsupportedDictionaryError("complex-valued dictionaries are not supported on the GPU path")
     dev = resolve_device(device)
     F = _signals_on_device(signals, dictionary, dev)
     B = F.shape[0]
     K, M = len(dictionary), dictionary.area
-    if K > _native.max_atoms():
-        raise UnsupportedDictionaryError(f"K={K} exceeds the iteration kernel's {_native.max_atoms()}")
+    cplx = not dictionary.is_real
+    kmax = _native.max_atoms_complex() if cplx else _native.max_atoms()
+    if K > kmax:
+        raise UnsupportedDictionaryError(f"K={K} exceeds the iteration kernel's {kmax}")
     mask, shared = _validate_masks(masks, dictionary, B)
     I = config.iterations
     phi = dictionary.device_matrix(dev)
@@ -441,7 +496,7 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
                                   "dictionary/weight combination")
         if tables.n_alive == 0:
             raise NoSelectableAtomError("every atom has zero weighted energy")
-        G, D = tables.device_tables(dev)
+        G, D = tables.device_tables(dev, complex_rows=cplx)
         W = _device_vector(w, dictionary.ld, dev)
         lost_idx = np.flatnonzero(mask.ravel()).astype(np.int32)
     else:
@@ -456,7 +511,8 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
         D = torch.empty((B, G.shape[1]), dtype=torch.float64, device=dev)
         alive = torch.empty(B, dtype=torch.int32, device=dev)
         stride = tables.tables[0].numel()
-        _native.block_normalizers(G, tables.tables, stride, tables.counts, tables.ids, K, D, alive)
+        (_native.block_normalizers_complex if cplx else _native.block_normalizers)(
+            G, tables.tables, stride, tables.counts, tables.ids, K, D, alive)
         dead = torch.nonzero(alive == 0)
         if dead.numel():
             raise NoSelectableAtomError(f"block {int(dead[0, 0])}: every atom has zero weighted energy")
@@ -469,26 +525,31 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
         lost_idx = None
 
     ldr = _round_up(K, 2)
+    vdt = torch.complex128 if cplx else torch.float64
     if products is None:
-        R0 = torch.empty((B, ldr), dtype=torch.float64, device=dev)
+        R0 = torch.empty((B, ldr), dtype=vdt, device=dev)
         ws = torch.empty(max(_native.init_products_workspace(M, B) // 8, 2), dtype=torch.float64,
                          device=dev)
         initial_products_into(dictionary, F, W, R0, ws)
     else:
-        R0 = _products_on_device(products, B, K, ldr, dev)
+        R0 = _products_on_device(products, B, K, ldr, dev, cplx)
     sel = torch.empty((B, I), dtype=torch.int32, device=dev)
-    proj = torch.empty((B, I), dtype=torch.float64, device=dev)
-    coef = torch.empty((B, I), dtype=torch.float64, device=dev)
-    R_log = torch.empty((B, I, ldr), dtype=torch.float64, device=dev) if record_products else None
-    _native.iterate(G, D, R0, K, I, config.gamma, sel, proj, coef, R_log=R_log, **chunk_args)
+    proj = torch.empty((B, I), dtype=vdt, device=dev)
+    coef = torch.empty((B, I), dtype=vdt, device=dev)
+    R_log = torch.empty((B, I, ldr), dtype=vdt, device=dev) if record_products else None
+    (_native.iterate_complex if cplx else _native.iterate)(
+        G, D, R0, K, I, config.gamma, sel, proj, coef, R_log=R_log, **chunk_args)
 
     patched = None
+    max_imag = torch.zeros(B, dtype=torch.float64, device=dev) if cplx else None
     if patch:
         patched = F[:, :M].clone() if F.shape[1] != M else F.clone()
+        extra = {"max_imag": max_imag} if cplx else {}
+        synth = _native.synth_paste_complex if cplx else _native.synth_paste
         if shared:
             if lost_idx.size:
                 idx = torch.from_numpy(lost_idx).to(dev)
-                _native.synth_paste(phi, sel, coef, I, idx, patched, n_shared=int(lost_idx.size))
+                synth(phi, sel, coef, I, idx, patched, n_shared=int(lost_idx.size), **extra)
         else:
             flat = mask.reshape(B, -1)
             counts = flat.sum(axis=1)
@@ -496,12 +557,13 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
             np.cumsum(counts, out=ptr[1:])
             idx = np.nonzero(flat)[1].astype(np.int32)
             if idx.size:
-                _native.synth_paste(phi, sel, coef, I, torch.from_numpy(idx).to(dev), patched,
-                                    idx_ptr=torch.from_numpy(ptr).to(dev))
+                synth(phi, sel, coef, I, torch.from_numpy(idx).to(dev), patched,
+                      idx_ptr=torch.from_numpy(ptr).to(dev), **extra)
         patched = patched.reshape(B, *dictionary.shape)
     prods = R_log[:, :, :K] if R_log is not None else None
     return BatchResult(selected=sel, projections=proj, coefficients=coef, patched=patched,
-                       products=prods, dictionary=dictionary, shape=dictionary.shape)
+                       products=prods, dictionary=dictionary, shape=dictionary.shape,
+                       max_imag=max_imag)
 
 
 class ExtrapolationPlan:
@@ -520,9 +582,8 @@ class ExtrapolationPlan:
                  config: ExtrapConfig = ExtrapConfig(), tables: GramTable | None = None,
                  device=None, products: str = "auto"):
         torch = _torch()
-        if not dictionary.is_real:
-            raise UnsupportedDictionaryError("complex-valued dictionaries are not supported on the GPU path")
         self.device = dev = resolve_device(device)
+        self.complex = cplx = not dictionary.is_real
         self.dictionary = dictionary
         self.config = config
         mask = as_mask(mask)
@@ -538,30 +599,47 @@ class ExtrapolationPlan:
         if tables.n_alive == 0:
             raise NoSelectableAtomError("every atom has zero weighted energy")
         self.tables = tables
-        self.G, self.D = tables.device_tables(dev)
         K, M, I = len(dictionary), dictionary.area, config.iterations
-        if K > _native.max_atoms():
-            raise UnsupportedDictionaryError(f"K={K} exceeds the iteration kernel's {_native.max_atoms()}")
+        kmax = _native.max_atoms_complex() if cplx else _native.max_atoms()
+        if K > kmax:
+            raise UnsupportedDictionaryError(f"K={K} exceeds the iteration kernel's {kmax}")
+        self.G, self.D = tables.device_tables(dev, complex_rows=cplx)
         self.K, self.M, self.I, self.B = K, M, I, int(n_blocks)
         self.phi = dictionary.device_matrix(dev)
         self.W = _device_vector(w, dictionary.ld, dev)
         ldf = M if M % 2 == 0 else dictionary.ld
         self.F = torch.zeros((self.B, ldf), dtype=torch.float64, device=dev)
-        self.R0 = torch.empty((self.B, _round_up(K, 2)), dtype=torch.float64, device=dev)
+        vdt = torch.complex128 if cplx else torch.float64
+        self.R0 = torch.empty((self.B, _round_up(K, 2)), dtype=vdt, device=dev)
         self.ws = torch.empty(max(_native.init_products_workspace(M, self.B) // 8, 2),
                               dtype=torch.float64, device=dev)
-        self.products = products
+        self.products = "gemm" if cplx else products
         self.selected = torch.empty((self.B, I), dtype=torch.int32, device=dev)
-        self.projections = torch.empty((self.B, I), dtype=torch.float64, device=dev)
-        self.coefficients = torch.empty((self.B, I), dtype=torch.float64, device=dev)
+        self.projections = torch.empty((self.B, I), dtype=vdt, device=dev)
+        self.coefficients = torch.empty((self.B, I), dtype=vdt, device=dev)
+        self.max_imag = torch.zeros(self.B, dtype=torch.float64, device=dev) if cplx else None
         lost = np.flatnonzero(mask.ravel()).astype(np.int32)
         self.n_lost = int(lost.size)
         self.lost_idx = torch.from_numpy(lost if lost.size else np.zeros(1, np.int32)).to(dev)
         self.lost_pos = torch.arange(max(self.n_lost, 1), dtype=torch.int64, device=dev)
         self.lost = torch.zeros((self.B, max(self.n_lost, 1)), dtype=torch.float64, device=dev)
-        factors = dictionary.device_factors(dev) if products in ("auto", "separable") else None
+        factors = dictionary.device_factors(dev) if self.products in ("auto", "separable") else None
         # weigh + (one transform per separable part | one GEMM) + iterate + synth
         self.launches_per_run = 1 + (len(factors) if factors else 1) + 1 + (1 if self.n_lost else 0)
+
+    def _iterate_synth(self, sel, proj, coef, lost):
+        if self.complex:
+            _native.iterate_complex(self.G, self.D, self.R0, self.K, self.I, self.config.gamma,
+                                    sel, proj, coef)
+            if self.n_lost:
+                _native.synth_paste_complex(self.phi, sel, coef, self.I, self.lost_idx, lost,
+                                            n_shared=self.n_lost, dst=self.lost_pos,
+                                            max_imag=self.max_imag)
+            return
+        _native.iterate(self.G, self.D, self.R0, self.K, self.I, self.config.gamma, sel, proj, coef)
+        if self.n_lost:
+            _native.synth_paste(self.phi, sel, coef, self.I, self.lost_idx, lost,
+                                n_shared=self.n_lost, dst=self.lost_pos)
 
     def run(self, signals=None):
         """Enqueue one batch. ``signals``: None (use ``self.F`` as filled by the
@@ -572,11 +650,7 @@ class ExtrapolationPlan:
             self.F[:, : self.M].copy_(src, non_blocking=True)
         self.products_method = initial_products_into(self.dictionary, self.F, self.W, self.R0,
                                                      self.ws, method=self.products)
-        _native.iterate(self.G, self.D, self.R0, self.K, self.I, self.config.gamma, self.selected,
-                        self.projections, self.coefficients)
-        if self.n_lost:
-            _native.synth_paste(self.phi, self.selected, self.coefficients, self.I, self.lost_idx,
-                                self.lost, n_shared=self.n_lost, dst=self.lost_pos)
+        self._iterate_synth(self.selected, self.projections, self.coefficients, self.lost)
         return self
 
     def host_buffers(self):
@@ -584,8 +658,8 @@ class ExtrapolationPlan:
         torch = _torch()
         return {
             "selected": torch.empty(tuple(self.selected.shape), dtype=torch.int32, pin_memory=True),
-            "coefficients": torch.empty(tuple(self.coefficients.shape), dtype=torch.float64,
-                                        pin_memory=True),
+            "coefficients": torch.empty(tuple(self.coefficients.shape),
+                                        dtype=self.coefficients.dtype, pin_memory=True),
             "lost": torch.empty(tuple(self.lost.shape), dtype=torch.float64, pin_memory=True),
         }
 
@@ -640,11 +714,7 @@ class ExtrapolationPlan:
                                   method=self.products)
             ev_used[s] = torch.cuda.Event()
             ev_used[s].record(cs)
-            _native.iterate(self.G, self.D, self.R0, self.K, self.I, self.config.gamma, sel, proj,
-                            coef)
-            if self.n_lost:
-                _native.synth_paste(self.phi, sel, coef, self.I, self.lost_idx, lost,
-                                    n_shared=self.n_lost, dst=self.lost_pos)
+            self._iterate_synth(sel, proj, coef, lost)
             done = torch.cuda.Event()
             done.record(cs)
             with torch.cuda.stream(d2h):
@@ -664,28 +734,32 @@ class ExtrapolationPlan:
         return self.B * self.M * 8
 
     def bytes_d2h(self) -> int:
-        return self.selected.numel() * 4 + self.coefficients.numel() * 8 + self.lost.numel() * 8
+        return (self.selected.numel() * 4 + self.coefficients.numel() * self.coefficients.element_size()
+                + self.lost.numel() * 8)
 
 
-def _products_on_device(products, B: int, K: int, ldr: int, device):
+def _products_on_device(products, B: int, K: int, ldr: int, device, cplx: bool = False):
     torch = _torch()
     if isinstance(products, torch.Tensor):
         p = products.to(device)
-        if p.is_complex():
+        if p.is_complex() and not cplx:
             if torch.any(p.imag != 0):
-                raise UnsupportedDictionaryError("complex products on the real GPU path")
+                raise UnsupportedDictionaryError("complex products for a real dictionary")
             p = p.real
     else:
         arr = np.asarray(products)
-        if np.iscomplexobj(arr):
-            if np.any(arr.imag != 0):
-                raise UnsupportedDictionaryError("complex products on the real GPU path")
-            arr = arr.real
-        p = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device)
+        if cplx:
+            p = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.complex128)).to(device)
+        else:
+            if np.iscomplexobj(arr):
+                if np.any(arr.imag != 0):
+                    raise UnsupportedDictionaryError("complex products for a real dictionary")
+                arr = arr.real
+            p = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device)
     p = p.reshape(-1, K) if p.dim() == 1 else p
     if tuple(p.shape) != (B, K):
         raise ShapeError(f"products shape {tuple(p.shape)}, expected ({B}, {K})")
-    R0 = torch.zeros((B, ldr), dtype=torch.float64, device=device)
+    R0 = torch.zeros((B, ldr), dtype=torch.complex128 if cplx else torch.float64, device=device)
     R0[:, :K].copy_(p)
     return R0
 
@@ -698,9 +772,11 @@ def _run_grouped(F, masks, dictionary, config, dev, patch):
     uniq, inverse = np.unique(flat, axis=0, return_inverse=True)
     inverse = inverse.ravel()
     I = config.iterations
+    vdt = torch.float64 if dictionary.is_real else torch.complex128
     sel = torch.empty((B, I), dtype=torch.int32, device=dev)
-    proj = torch.empty((B, I), dtype=torch.float64, device=dev)
-    coef = torch.empty((B, I), dtype=torch.float64, device=dev)
+    proj = torch.empty((B, I), dtype=vdt, device=dev)
+    coef = torch.empty((B, I), dtype=vdt, device=dev)
+    max_imag = None if dictionary.is_real else torch.zeros(B, dtype=torch.float64, device=dev)
     patched = F[:, : dictionary.area].clone() if patch else None
     for g in range(uniq.shape[0]):
         rows = np.flatnonzero(inverse == g)
@@ -711,12 +787,14 @@ def _run_grouped(F, masks, dictionary, config, dev, patch):
         sel[ridx] = sub.selected
         proj[ridx] = sub.projections
         coef[ridx] = sub.coefficients
+        if max_imag is not None:
+            max_imag[ridx] = sub.max_imag
         if patch:
             patched[ridx] = sub.patched.reshape(len(rows), -1)
     if patch:
         patched = patched.reshape(B, *dictionary.shape)
     return BatchResult(selected=sel, projections=proj, coefficients=coef, patched=patched,
-                       dictionary=dictionary, shape=dictionary.shape)
+                       dictionary=dictionary, shape=dictionary.shape, max_imag=max_imag)
 
 
 # ----------------------------------------------------------------- single block
@@ -766,7 +844,7 @@ def apply_model(signal, model: SparseModel, mask, *, device=None):
     """Replace lost samples by Re(g) (``fast.py:267-286``); g on the GPU.
 
     Returns (patched float64 field, max |Im g| over lost samples) -- the latter
-    is exactly 0.0 for the real dictionaries of the GPU path.
+    is exactly 0.0 for real dictionaries.
     """
     torch = _torch()
     s = np.asarray(signal)
@@ -782,21 +860,28 @@ def apply_model(signal, model: SparseModel, mask, *, device=None):
         out[mask] = 0.0
         return out, 0.0
     dictionary = model.dictionary
-    if not dictionary.is_real:
-        raise UnsupportedDictionaryError("complex-valued models are not supported on the GPU path")
     coefs = np.array([c for _, c in model.terms], dtype=np.complex128)
-    if np.any(coefs.imag != 0):
-        raise UnsupportedDictionaryError("complex coefficients on the real GPU path")
     dev = resolve_device(device)
     phi = dictionary.device_matrix(dev)
     sel = torch.tensor([[int(k) for k, _ in model.terms]], dtype=torch.int32, device=dev)
-    coef = torch.from_numpy(coefs.real.reshape(1, -1).copy()).to(dev)
     idx = np.flatnonzero(mask.ravel()).astype(np.int32)
     g = torch.zeros((1, s.size), dtype=torch.float64, device=dev)
-    _native.synth_paste(phi, sel, coef, len(model.terms), torch.from_numpy(idx).to(dev), g,
-                        n_shared=int(idx.size))
+    if dictionary.is_real:
+        if np.any(coefs.imag != 0):
+            raise UnsupportedDictionaryError("complex coefficients for a real dictionary")
+        coef = torch.from_numpy(coefs.real.reshape(1, -1).copy()).to(dev)
+        _native.synth_paste(phi, sel, coef, len(model.terms), torch.from_numpy(idx).to(dev), g,
+                            n_shared=int(idx.size))
+        max_imag = 0.0
+    else:
+        coef = torch.from_numpy(coefs.reshape(1, -1).copy()).to(dev)
+        mi = torch.zeros(1, dtype=torch.float64, device=dev)
+        _native.synth_paste_complex(phi, sel, coef, len(model.terms),
+                                    torch.from_numpy(idx).to(dev), g, n_shared=int(idx.size),
+                                    max_imag=mi)
+        max_imag = float(mi.item())
     out[mask] = g.cpu().numpy().ravel()[idx]
-    return out, 0.0
+    return out, max_imag
 
 
 # ----------------------------------------------------------------- FGRM files

@@ -60,9 +60,11 @@ class SparseModel:
 class BatchResult:
     """Outcome of one batched run over B blocks (device tensors).
 
-    selected: (B, I) int32; projections, coefficients: (B, I) float64;
-    patched: (B, M, N) float64 areas with lost samples replaced, or None;
-    products: (B, I, K) float64 record of R when requested, else None.
+    selected: (B, I) int32; projections, coefficients: (B, I) float64
+    (complex128 for complex dictionaries); patched: (B, M, N) float64 areas
+    with lost samples replaced (Re g), or None; products: (B, I, K) record of R
+    when requested, else None; max_imag: (B,) max |Im g| over each block's
+    lost samples for complex dictionaries (apply_model's diagnostic), else None.
     """
 
     selected: object
@@ -72,6 +74,7 @@ class BatchResult:
     products: object = None
     dictionary: object = None
     shape: tuple[int, int] | None = None
+    max_imag: object = None
 
     def __len__(self) -> int:
         return int(self.selected.shape[0])

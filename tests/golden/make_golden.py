@@ -95,6 +95,74 @@ def small_cases():
     return cases
 
 
+def complex_cases():
+    """Complex dictionaries (the reference's default ``dft`` and its relatives)."""
+    specs = [("dft", 8, 8, (4, 4)), ("bdft", 8, 8, (4, 4)), ("union:dft+bdft", 6, 6, (2, 2)),
+             ("union:dct+dft", 8, 8, (4, 4)), ("dft", 6, 10, (2, 4)), ("bdft", 12, 12, (4, 4)),
+             ("union:wht+dft", 16, 16, (8, 8))]
+    cases, out = [], {}
+    for i, (spec, m, n, loss) in enumerate(specs):
+        d = fase.parse_dict_spec(spec, m, n)
+        mask = wl.central_loss_mask(m, n, *loss)
+        cfg = fase.ExtrapConfig(iterations=40, gamma=[0.5, 1.0, 0.25][i % 3], rho_hat=0.8)
+        signal = np.random.default_rng([2204, 100 + i]).uniform(0.0, 255.0, (m, n))
+        w = fase.build_weight_field(mask, cfg.rho_hat)
+        tables = fase.build_gram_tables(d, w)
+        r0 = fase.initial_scalar_products(signal, w, d)
+        model, trace = fase.fase_extrapolate(signal, mask, d, tables, cfg, record_products=True)
+        patched, max_imag = fase.apply_model(signal, model, mask)
+        key = f"z{i}"
+        out.update({f"{key}_signal": signal, f"{key}_mask": mask, f"{key}_gram": tables.c,
+                    f"{key}_d": tables.d, f"{key}_r0": r0,
+                    f"{key}_selected": np.asarray(trace.selected, dtype=np.int64),
+                    f"{key}_projections": trace.projections, f"{key}_coefficients": trace.coefficients,
+                    f"{key}_products": np.stack(trace.products),
+                    f"{key}_patched_lost": patched[mask], f"{key}_max_imag": np.float64(max_imag)})
+        cases.append({"key": key, "spec": spec, "m": m, "n": n, "loss": list(loss),
+                      "iterations": cfg.iterations, "gamma": cfg.gamma, "rho_hat": cfg.rho_hat,
+                      "provenance": str(tables.provenance), "content_hash": str(d.content_hash())})
+    np.savez_compressed(HERE / "complex_cases.npz", **out)
+    return cases
+
+
+def complex_blocks(n_blocks: int = 3):
+    """The reference's default dictionary (dft) on the config-1 area and loss."""
+    w1 = wl.WORKLOADS[1]
+    m, n = w1.area
+    d = fase.parse_dict_spec("dft", m, n)
+    mask = wl.central_loss_mask(m, n, *w1.loss)
+    cfg = fase.ExtrapConfig(w1.config.iterations, w1.config.gamma, w1.config.rho_hat)
+    sig = wl.block_signals(1, n_blocks, m, n)
+    w = fase.build_weight_field(mask, cfg.rho_hat)
+    tables = fase.build_gram_tables(d, w)
+    out = {"blocks": np.arange(n_blocks), "d": tables.d.copy(), "provenance": np.uint64(tables.provenance),
+           "gram_diag": tables.c.diagonal().real.copy(), "gram_row0": tables.c[0].copy(),
+           "gram_row777": tables.c[777].copy()}
+    t0 = time.time()
+    for b in range(n_blocks):
+        r0 = fase.initial_scalar_products(sig[b], w, d)
+        model, trace = fase.fase_extrapolate(sig[b], mask, d, tables, cfg)
+        patched, max_imag = fase.apply_model(sig[b], model, mask)
+        out.update({f"b{b}_r0": r0, f"b{b}_selected": np.asarray(trace.selected, dtype=np.int64),
+                    f"b{b}_projections": trace.projections, f"b{b}_coefficients": trace.coefficients,
+                    f"b{b}_patched_lost": patched[mask], f"b{b}_max_imag": np.float64(max_imag)})
+    np.savez_compressed(HERE / "dft48_blocks.npz", **out)
+    return {"spec": "dft", "area": [m, n], "blocks": n_blocks, "seconds": time.time() - t0}
+
+
+def complex_arithmetic():
+    """numpy's complex128 product and abs on this host (the oracle's semantics)."""
+    rng = np.random.default_rng(22041)
+    n = 4099
+    x = (rng.standard_normal(n) + 1j * rng.standard_normal(n)) * 10.0 ** rng.integers(-4, 5, n)
+    y = (rng.standard_normal(n) + 1j * rng.standard_normal(n)) * 10.0 ** rng.integers(-4, 5, n)
+    x[::7] = x[::7].real
+    y[3::11] = 1j * y[3::11].imag
+    c = complex(rng.standard_normal(), rng.standard_normal())
+    np.savez_compressed(HERE / "complex_arith.npz", x=x, y=y, c=np.complex128(c), xy=x * y,
+                        cy=c * np.conj(y), absx=np.abs(x))
+
+
 def weights_and_hashes():
     rec = {"weights": [], "hashes": []}
     arrays = {}
@@ -199,12 +267,15 @@ def main():
             "numpy": np.__version__}
     meta.update(weights_and_hashes())
     meta["small_cases"] = small_cases()
+    meta["complex_cases"] = complex_cases()
+    complex_arithmetic()
     meta["fgrm"] = fgrm_fixture()
     meta["c0"] = shared_config_blocks(0, [0])
     meta["c1"] = shared_config_blocks(1, [0, 1, 2, 3])
     meta["c4"] = shared_config_blocks(4, [0, 1])
     meta["c3"] = frame_config_blocks(3, 6)
     meta["c2"] = frame_config_blocks(2, 4)
+    meta["dft48"] = complex_blocks()
     with open(HERE / "golden.json", "w") as fh:
         json.dump(meta, fh, indent=1)
     print(json.dumps({k: v for k, v in meta.items() if k.startswith("c")}, indent=1))

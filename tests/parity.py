@@ -18,8 +18,12 @@ COEF_REL = 1e-6       # run-scale coefficient / sample tolerance (BASELINE)
 
 
 def rel_dev(a, b) -> float:
-    a = np.asarray(a, dtype=np.float64)
-    b = np.asarray(b, dtype=np.float64)
+    """max |a - b| / max(|a|, |b|) (real or complex)."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    if not (np.iscomplexobj(a) or np.iscomplexobj(b)):
+        a = a.astype(np.float64)
+        b = b.astype(np.float64)
     scale = max(float(np.abs(a).max(initial=0.0)), float(np.abs(b).max(initial=0.0)), 1e-300)
     return float(np.abs(a - b).max(initial=0.0)) / scale
 

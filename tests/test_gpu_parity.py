@@ -291,13 +291,6 @@ def test_stale_tables_detected():
         fase_extrapolate(np.ones((4, 4)), mask, d, rho, device=DEV)
 
 
-def test_complex_dictionary_rejected():
-    d = generate_dictionary("dft", 4, 4)
-    with pytest.raises(UnsupportedDictionaryError):
-        fase_extrapolate_batch(np.ones((1, 4, 4)), wl.central_loss_mask(4, 4, 2, 2), d, None,
-                               device=DEV)
-
-
 def test_empty_batch_and_odd_area():
     d = generate_dictionary("dct", 5, 7)  # K = 35, odd area
     mask = wl.central_loss_mask(5, 7, 1, 3)

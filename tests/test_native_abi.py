@@ -52,6 +52,15 @@ def test_host_queries(lib):
     assert _native.table_ld(2048) == 2048
     with pytest.raises(errors.UnsupportedDictionaryError):
         _native.table_ld(lib.fase_max_atoms() + 1)
+    # complex tables: leading dimensions in complex elements
+    assert lib.fase_max_atoms_complex() >= 4608
+    for k in (1, 64, 2304, 4608):
+        assert _native.table_ld_complex(k) >= k
+    assert _native.table_ld_complex(2304) == 2304
+    with pytest.raises(errors.UnsupportedDictionaryError):
+        _native.table_ld_complex(lib.fase_max_atoms_complex() + 1)
+    # complex Gram workspace: w2, P o w2 and Q (K x 2 ldphi each), Re / Im (K x K)
+    assert lib.fase_gram_complex_workspace(64, 64) == 8 * (128 + 2 * 64 * 128 + 2 * 64 * 64)
 
 
 def test_status_codes_and_messages(lib):
@@ -66,6 +75,11 @@ def test_status_codes_and_messages(lib):
     args = _native.IterateArgs(K=4, B=1, I=1, gamma=2.0)
     assert lib.fase_iterate(ctypes.byref(args), None) == -2
     assert b"gamma" in lib.fase_last_error()
+    assert lib.fase_iterate_complex(ctypes.byref(args), None) == -2
+    assert lib.fase_iterate_complex(None, None) == -2
+    assert lib.fase_gram_complex(None, 0, None, 0, 0, None, 0, None, 0, None) == -1
+    assert lib.fase_synth_paste_complex(None, 0, None, None, 0, 0, 1, None, None, 0, None, None, 0,
+                                        None, None) == -1
     # empty batches are a no-op, not an error
     args = _native.IterateArgs(K=4, B=0, I=1, gamma=0.5)
     assert lib.fase_iterate(ctypes.byref(args), None) == 0

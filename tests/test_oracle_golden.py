@@ -117,3 +117,69 @@ def test_frame_config3_blocks(golden_dir):
         assert np.array_equal(res["selected"], z[f"b{b}_selected"])
         assert np.array_equal(res["coefficients"].real, z[f"b{b}_coefficients"])
         assert np.array_equal(res["patched"][masks[b]], z[f"b{b}_patched_lost"])
+
+
+# ----------------------------------------------------------------- complex dictionaries
+
+
+def test_complex_arithmetic_semantics(golden_dir):
+    """numpy's complex128 product and abs -- the semantics the CUDA kernels
+    restate (csrc/common.cuh) -- are unchanged on this host and equal the
+    oracle's scalar statements of them."""
+    z = np.load(golden_dir / "complex_arith.npz")
+    x, y, c = z["x"], z["y"], complex(z["c"])
+    assert np.array_equal(x * y, z["xy"])
+    assert np.array_equal(c * np.conj(y), z["cy"])
+    assert np.array_equal(np.abs(x), z["absx"])
+    yc = np.conj(y)
+    for i in range(0, len(x), 13):
+        assert orc.cmul_fused(complex(x[i]), complex(y[i])) == z["xy"][i]
+        assert orc.cmul_fused(c, complex(yc[i])) == z["cy"][i]
+        assert orc.cabs_scaled(complex(x[i])) == z["absx"][i]
+
+
+def test_complex_cases(golden_dir, meta):
+    """dft / bdft / mixed unions: the oracle reproduces the reference bit-for-bit."""
+    z = np.load(golden_dir / "complex_cases.npz")
+    for case in meta["complex_cases"]:
+        k = case["key"]
+        vals = oracle_values(case["spec"], case["m"], case["n"])
+        assert orc.content_hash(vals) == int(case["content_hash"]), k
+        phi = vals.reshape(len(vals), -1)
+        sig, mask = z[f"{k}_signal"], z[f"{k}_mask"]
+        w = orc.weight_field(mask, case["rho_hat"])
+        assert orc.provenance(orc.content_hash(vals), w) == int(case["provenance"])
+        c, d = orc.gram(phi, w)
+        assert np.array_equal(c, z[f"{k}_gram"]), k
+        assert np.array_equal(d, z[f"{k}_d"]), k
+        res = orc.extrapolate_block(sig, mask, vals, case["gamma"], case["iterations"],
+                                    case["rho_hat"], tables=(c, d), record=True)
+        assert np.array_equal(res["r0"], z[f"{k}_r0"]), k
+        assert np.array_equal(res["selected"], z[f"{k}_selected"]), k
+        assert np.array_equal(res["projections"], z[f"{k}_projections"]), k
+        assert np.array_equal(res["coefficients"], z[f"{k}_coefficients"]), k
+        assert np.array_equal(np.stack(res["log"]), z[f"{k}_products"]), k
+        assert np.array_equal(res["patched"][mask], z[f"{k}_patched_lost"]), k
+        assert res["max_imag"] == z[f"{k}_max_imag"], k
+
+
+def test_dft48_blocks(golden_dir):
+    """The reference's default dictionary on the config-1 area: oracle == reference."""
+    z = np.load(golden_dir / "dft48_blocks.npz")
+    w1 = wl.WORKLOADS[1]
+    m, n = w1.area
+    vals = orc.family("dft", m, n)
+    mask = orc.central_mask(m, n, *w1.loss)
+    w = orc.weight_field(mask, w1.config.rho_hat)
+    c, d = orc.gram(vals.reshape(len(vals), -1), w)
+    assert np.array_equal(d, z["d"])
+    assert np.array_equal(c[0], z["gram_row0"]) and np.array_equal(c[777], z["gram_row777"])
+    sig = wl.block_signals(1, len(z["blocks"]), m, n)
+    for b in z["blocks"]:
+        res = orc.extrapolate_block(sig[b], mask, vals, w1.config.gamma, w1.config.iterations,
+                                    w1.config.rho_hat, tables=(c, d))
+        assert np.array_equal(res["r0"], z[f"b{b}_r0"])
+        assert np.array_equal(res["selected"], z[f"b{b}_selected"])
+        assert np.array_equal(res["coefficients"], z[f"b{b}_coefficients"])
+        assert np.array_equal(res["patched"][mask], z[f"b{b}_patched_lost"])
+        assert res["max_imag"] == z[f"b{b}_max_imag"]
