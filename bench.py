@@ -65,7 +65,22 @@ def parse_args():
     ap.add_argument("--products", default="auto", choices=["auto", "gemm", "separable"],
                     help="initial products: separable transforms (separable dictionaries) or "
                          "the dense DMMA GEMM")
-    return ap.parse_args()
+    ap.add_argument("--dict", default=None,
+                    help="override the dictionary spec of a shared-geometry config (0, 1, 4), "
+                         "e.g. 'dft' (the reference's default, complex-valued)")
+    args = ap.parse_args()
+    if args.dict and not wl.WORKLOADS[args.config].shared_geometry:
+        ap.error("--dict applies to the shared-geometry configs 0, 1 and 4")
+    return args
+
+
+def bench_dictionary(w, spec):
+    """The workload's dictionary, or ``spec`` over the same area."""
+    if not spec:
+        return w.dictionary()
+    from paper_2204_14194_b200 import parse_dict_spec
+
+    return parse_dict_spec(spec, *w.area)
 
 
 # ----------------------------------------------------------------- CPU reference
@@ -104,12 +119,12 @@ def _cpu_worker(args):
         return n, time.perf_counter() - t0
 
 
-def cpu_prepare(cid: int):
+def cpu_prepare(cid: int, spec=None):
     from oracle import fase_oracle as orc
 
     w = wl.WORKLOADS[cid]
-    d = w.dictionary()
-    vals = d.real_values().astype(np.complex128)
+    d = bench_dictionary(w, spec)
+    vals = d.values
     if w.shared_geometry:
         mask = wl.central_loss_mask(*w.area, *w.loss)
         tables = orc.gram(vals.reshape(len(vals), -1), orc.weight_field(mask, w.config.rho_hat))
@@ -134,10 +149,10 @@ def cpu_sample(cid: int, seconds: float, pool, procs: int, per_block_s: float):
     return blocks / wall, blocks, wall
 
 
-def cpu_baseline(cid: int, seconds: float, steps: int = 1, warmup: int = 0):
+def cpu_baseline(cid: int, seconds: float, steps: int = 1, warmup: int = 0, spec=None):
     import multiprocessing as mp
 
-    cpu_prepare(cid)
+    cpu_prepare(cid, spec)
     procs = os.cpu_count() or 1
     # calibrate one block on one core
     n1, t1 = _cpu_worker((cid, 0, 1))
@@ -161,13 +176,15 @@ def run_reference(args):
     if rank != 0:
         return
     w = wl.WORKLOADS[args.config]
-    base = cpu_baseline(args.config, args.cpu_seconds, steps=args.steps, warmup=args.warmup)
+    base = cpu_baseline(args.config, args.cpu_seconds, steps=args.steps, warmup=args.warmup,
+                        spec=args.dict)
     line = {
         "impl": "reference", "metric": "extrapolated blocks/s", "value": base["value"],
         "unit": "blocks/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded, BASELINE Appendix-A generators)",
-        "config": workload_config(w, args.gpus), "cpu_baseline": base,
+        "dtype": "f64" if bench_dictionary(w, args.dict).is_real else "c128",
+        "data": "synthetic (seeded, BASELINE Appendix-A generators)",
+        "config": workload_config(w, args.gpus, args.dict), "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": "blocks/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -177,10 +194,11 @@ def run_reference(args):
 # ----------------------------------------------------------------- GPU arm
 
 
-def workload_config(w, n_gpus):
-    cfg = {"workload": w.name, "area": list(w.area), "K": w.n_atoms,
+def workload_config(w, n_gpus, spec=None):
+    cfg = {"workload": w.name + (f" with dictionary {spec}" if spec else ""), "area": list(w.area),
+           "K": len(bench_dictionary(w, spec)) if spec else w.n_atoms,
            "M": w.area[0] * w.area[1], "iterations": w.config.iterations, "gamma": w.config.gamma,
-           "rho": w.config.rho_hat, "dictionary": w.dict_spec,
+           "rho": w.config.rho_hat, "dictionary": spec or w.dict_spec,
            "l2": "flushed between timed steps (256 MiB write)",
            "parallelism": f"dp{n_gpus} (block sharding, no collective)"}
     if w.shared_geometry:
@@ -287,7 +305,8 @@ def run_gpu(args):
     rank, world, local = dist_env()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.config, args.cpu_seconds)  # before CUDA init (fork-safe)
+        # before CUDA init (fork-safe)
+        cpu = cpu_baseline(args.config, args.cpu_seconds, spec=args.dict)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -295,22 +314,32 @@ def run_gpu(args):
     _native.load()
 
     w = wl.WORKLOADS[args.config]
-    d = w.dictionary()
+    d = bench_dictionary(w, args.dict)
+    cplx = not d.is_real
     K, M, I, B = len(d), w.area[0] * w.area[1], w.config.iterations, w.n_blocks
     mask = wl.central_loss_mask(*w.area, *w.loss)
     d.device_matrix(dev)
     tables = build_gram_tables(d, build_weight_field(mask, w.config.rho_hat), device=dev)
     plan = ExtrapolationPlan(d, mask, B, w.config, tables, device=dev, products=args.products)
+    iterate = _native.iterate_complex if cplx else _native.iterate
+    synth_extra = {"max_imag": plan.max_imag} if cplx else {}
+    synth = _native.synth_paste_complex if cplx else _native.synth_paste
     # one more table build, kernels only, for the reported Gram time
     G2 = torch.zeros_like(plan.G)
     D2 = torch.empty_like(plan.D)
-    gws = torch.empty(K * plan.phi.shape[1] + 2, dtype=torch.float64, device=dev)
+    gws = torch.empty((int(_native.load().fase_gram_complex_workspace(K, plan.phi.shape[1]))
+                       if cplx else K * plan.phi.shape[1] * 8) // 8 + 2,
+                      dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
     g0 = torch.cuda.Event(enable_timing=True)
     g1 = torch.cuda.Event(enable_timing=True)
     g0.record()
-    _native.gram(plan.phi, plan.W, K, M, G2, ws=gws)
-    _native.gram_finish(G2, K, D2)
+    if cplx:
+        _native.gram_complex(plan.phi, plan.W, K, M, G2, ws=gws)
+        _native.gram_finish_complex(G2, K, D2)
+    else:
+        _native.gram(plan.phi, plan.W, K, M, G2, ws=gws)
+        _native.gram_finish(G2, K, D2)
     g1.record()
     torch.cuda.synchronize()
     gram_ms = g0.elapsed_time(g1)
@@ -353,11 +382,11 @@ def run_gpu(args):
                 plan.F[:, :M].copy_(dev_sig.reshape(B, -1), non_blocking=True)
                 initial_products_into(d, plan.F, plan.W, plan.R0, plan.ws, method=plan.products)
                 e[1].record(stream)
-                _native.iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, plan.selected,
-                                plan.projections, plan.coefficients)
+                iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, plan.selected,
+                        plan.projections, plan.coefficients)
                 e[2].record(stream)
-                _native.synth_paste(plan.phi, plan.selected, plan.coefficients, I, plan.lost_idx,
-                                    plan.lost, n_shared=plan.n_lost, dst=plan.lost_pos)
+                synth(plan.phi, plan.selected, plan.coefficients, I, plan.lost_idx,
+                      plan.lost, n_shared=plan.n_lost, dst=plan.lost_pos, **synth_extra)
                 e[3].record(stream)
             else:
                 fn()
@@ -401,10 +430,10 @@ def run_gpu(args):
     if rank == 0:
         hbm, hsrc, fp64, fsrc = measured_peaks()
         it_s = float(np.mean(iter_ms)) / 1e3
-        bytes_iter = 8.0 * K * B * I
+        bytes_iter = (16.0 if cplx else 8.0) * K * B * I
         achieved = bytes_iter / it_s / 1e9
         init_s = float(np.mean(init_ms)) / 1e3
-        flops_init = 2.0 * K * M * B
+        flops_init = (4.0 if cplx else 2.0) * K * M * B
         factors = d.device_factors(dev) if plan.products in ("auto", "separable") else None
         if factors:  # executed flops of the separable form
             mr, nc = w.area
@@ -422,22 +451,26 @@ def run_gpu(args):
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "f64",
+            "dtype": "c128" if cplx else "f64",
             "data": "synthetic (seeded BASELINE Appendix-A generators; random atoms: none)",
-            "config": workload_config(w, world),
+            "config": workload_config(w, world, args.dict),
             "e2e": {"value": world * B * args.steps / e2e_total_s, "unit": "blocks/s",
                     "h2d_bytes_per_step": plan.bytes_h2d(), "d2h_bytes_per_step": plan.bytes_d2h(),
                     "ms_per_step": e2e_total_s / args.steps * 1e3,
                     "api": "ExtrapolationPlan.run_host_stream: pinned host in/out every step, "
                            "H2D / D2H on side streams overlapped with compute; no L2 flush "
                            "(per-step input comes over PCIe; table 170 MB > L2)"},
-            "roofline": {"bound": "hbm", "kernel": "fase_iterate_kernel",
+            "roofline": {"bound": "hbm",
+                         "kernel": "fase_iterate_complex_kernel" if cplx else "fase_iterate_kernel",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": ncu_traffic("fase_iterate_kernel"),
+                         "frac": achieved / hbm,
+                         "traffic": ncu_traffic("fase_iterate_complex_kernel" if cplx
+                                                else "fase_iterate_kernel"),
                          "algorithmic_bytes_per_launch": bytes_iter,
                          "ms_per_launch": it_s * 1e3, "peak_source": hsrc,
-                         "note": "8*K bytes per block-iteration (one FP64 table row); hot rows "
-                                 "hit L2, so frac can exceed DRAM-bound expectations"},
+                         "note": ("16*K bytes per block-iteration (one complex128 table row)"
+                                  if cplx else "8*K bytes per block-iteration (one FP64 table row)")
+                                 + "; hot rows hit L2, so frac can exceed DRAM-bound expectations"},
             "roofline_init": ({"bound": "tensor", "kernel": "dgemm_nt_kernel (DMMA FP64)",
                                "achieved": flops_init / init_s / 1e12, "peak": fp64,
                                "unit": "TFLOP/s", "frac": flops_init / init_s / 1e12 / fp64,
@@ -455,7 +488,7 @@ def run_gpu(args):
             "stage_ms": {"init_products": float(np.mean(init_ms)), "iterate": float(np.mean(iter_ms)),
                          "synth": float(np.mean(synth_ms))},
             "gram_ms": gram_ms,
-            "gram_tflops": K * (K + 1) * M / (gram_ms * 1e-3) / 1e12,
+            "gram_tflops": (4 if cplx else 1) * K * (K + 1) * M / (gram_ms * 1e-3) / 1e12,
             "gpu_launches": args.steps * (plan.launches_per_run + 1) + args.steps * plan.launches_per_run,
             "clocks": clocks.summary(),
             "wall_s": t_wall,

@@ -22,11 +22,13 @@
 // atom plus its structural twins, e.g. a conjugate-frequency partner) get the
 // exact metric and land in a short shared list; after the second barrier every
 // warp resolves the list redundantly (exact max, tie quantum, lowest index), so
-// an iteration still has two barriers. An overflowing list, or proxies too
+// an iteration still has two barriers. A single candidate is the selection
+// outright; its exact metric is needed only while the tie quantum can move. An overflowing list, or proxies too
 // small / large to trust, fall back to an exact pass over all elements.
 //
 // Layout: thread t owns complex elements k = j*NT + t, j < EP (R in registers,
-// (D, D^2) in shared memory or registers), so a table row streams with
+// D^2 in shared memory or registers; D itself only for exact metrics, from
+// global memory), so a table row streams with
 // coalesced 16-byte loads; the predicted row is staged by TMA as in the real
 // kernel, and per-block geometries compose rows G0[u] - sum C_j[u] the same way.
 // Leading dimensions (ldg, ldr, ldo, chunk_stride) count complex elements.
@@ -59,7 +61,7 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
   __shared__ __align__(8) uint64_t s_bar[kSeg];
   extern __shared__ double2 s_dyn[];
   double2* s_row = s_dyn;          // staged row: element j*NT + t
-  double2* s_D = s_dyn + EP * NT;  // kDsmem: (D, D^2) per element
+  double* s_D2 = reinterpret_cast<double*>(s_dyn + EP * NT);  // kDsmem: D^2 per element
 
   const int b = blockIdx.x;
   const int t = threadIdx.x;
@@ -85,12 +87,19 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
   }
 
   double r[EP][2];
-  double dreg[kDsmem ? 1 : EP][2];
-  auto dpair = [&](int j) -> double2 {  // (D, D^2); dead: (-inf, -inf)
+  double dreg[kDsmem ? 1 : EP];
+  auto d2 = [&](int j) -> double {  // D^2 of element j; dead: -inf
     if constexpr (kDsmem)
-      return s_D[j * NT + t];
+      return s_D2[j * NT + t];
     else
-      return make_double2(dreg[j][0], dreg[j][1]);
+      return dreg[j];
+  };
+  // D itself is only needed for exact metrics (candidates, the exact pass):
+  // read from global memory (L2-resident) there
+  auto dval = [&](int j) -> double {
+    const int k = j * NT + t;
+    const double dk = k < K ? D[k] : 0.0;
+    return dk != 0.0 ? dk : kDead;
   };
   auto proxy = [](double re, double im, double d2) {
     return mul_rn(__fma_rn(re, re, mul_rn(im, im)), d2);
@@ -103,14 +112,12 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
     r[j][0] = k < K ? R0[2 * k] : 0.0;
     r[j][1] = k < K ? R0[2 * k + 1] : 0.0;
     const double dk = k < K ? D[k] : 0.0;
-    const double2 dd = dk != 0.0 ? make_double2(dk, mul_rn(dk, dk)) : make_double2(kDead, kDead);
-    if constexpr (kDsmem) {
-      s_D[j * NT + t] = dd;
-    } else {
-      dreg[j][0] = dd.x;
-      dreg[j][1] = dd.y;
-    }
-    const double pk = proxy(r[j][0], r[j][1], dd.y);
+    const double dsq = dk != 0.0 ? mul_rn(dk, dk) : kDead;
+    if constexpr (kDsmem)
+      s_D2[j * NT + t] = dsq;
+    else
+      dreg[j] = dsq;
+    const double pk = proxy(r[j][0], r[j][1], dsq);
     if (pk > best) {
       best = pk;
       barg = static_cast<unsigned>(k);
@@ -176,23 +183,23 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
     const double pmax = __longlong_as_double(top_key);
     // proxies outside [2^-900, 2^900] lose the relative accuracy the bound needs
     const bool trusted = pmax >= 0x1p-900 && pmax <= 0x1p+900;
-    double pc = 0.0;
+    double pc = 0.0, top_hi = 0.0;
     if (trusted) {
       const double s = sqrt(pmax);
-      const double top_lo = s * (1.0 - 0x1p-40), top_hi = s * (1.0 + 0x1p-40);
+      const double top_lo = s * (1.0 - 0x1p-40);
+      top_hi = s * (1.0 + 0x1p-40);
       const double thr_lo = top_lo - fmax(q, 1e-13 * top_hi) * (1.0 + 0x1p-40);
       pc = thr_lo > 0.0 ? thr_lo * thr_lo * (1.0 - 0x1p-40) : 0.0;
     }
     if (trusted && pc > 0.0 && wkey >= 0 && __longlong_as_double(wkey) >= pc) {  // warp-uniform
 #pragma unroll
       for (int j = 0; j < EP; ++j) {
-        const double2 dd = dpair(j);
-        if (proxy(r[j][0], r[j][1], dd.y) >= pc) {  // exact metric after the barrier
+        if (proxy(r[j][0], r[j][1], d2(j)) >= pc) {  // exact metric after the barrier
           const int slot = atomicAdd(&s_cnt[it & 1], 1);
           if (slot < kCap) {
             s_ck[slot] = static_cast<unsigned>(j * NT + t);
             s_cr[slot] = make_double2(r[j][0], r[j][1]);
-            s_cd[slot] = dd.x;
+            s_cd[slot] = dval(j);
           }
         }
       }
@@ -203,7 +210,19 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
     unsigned u;
     double2 ru;
     double du;
-    if (trusted && pc > 0.0 && cnt >= 1 && cnt <= kCap) {
+    if (trusted && pc > 0.0 && cnt == 1) {
+      // ---- the common case: one candidate, so it is the maximum and the
+      // selection. Its exact metric matters only if the tie quantum can move
+      // (1e-13 * top > q), which the proxy's upper bound rules out after the
+      // first iterations.
+      u = s_ck[0];
+      ru = s_cr[0];
+      du = s_cd[0];
+      if (mul_rn(1e-13, top_hi) > q) {
+        const double top = mul_rn(np_cabs(ru.x, ru.y), du);
+        if (top > 0.0 && top < __longlong_as_double(0x7ff0000000000000LL)) q = fmax(q, mul_rn(1e-13, top));
+      }
+    } else if (trusted && pc > 0.0 && cnt >= 2 && cnt <= kCap) {
       // ---- resolve the list in every warp: exact max, quantum, lowest index
       // one lane per entry: exact metric (entries past 32 are rare)
       long long mk = LLONG_MIN;
@@ -240,14 +259,13 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
       auto element = [&](int jj, double& re, double& im, double& d) {
         re = 0.0;
         im = 0.0;
-        d = kDead;
 #pragma unroll
         for (int j = 0; j < EP; ++j)
           if (j == jj) {
             re = r[j][0];
             im = r[j][1];
-            d = dpair(j).x;
           }
+        d = dval(jj);
       };
       double mb = kDead;
 #pragma unroll 1
@@ -322,11 +340,10 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
             if (j == sg * EP / kSeg) mbar_wait(&s_bar[sg], it & 1);
         }
         const double2 g = row_elem(j);
-        const double2 dd = dpair(j);
         const double2 x = np_cmul(cr, ci, g.x, g.y);
         r[j][0] = sub_rn(r[j][0], x.x);
         r[j][1] = sub_rn(r[j][1], x.y);
-        const double pk = proxy(r[j][0], r[j][1], dd.y);
+        const double pk = proxy(r[j][0], r[j][1], d2(j));
         if (pk > best) {
           best = pk;
           barg = static_cast<unsigned>(j * NT + t);
@@ -410,7 +427,16 @@ const Variant kVariants[] = {
     FASE_CV(128, 8, 4, true),  FASE_CV(256, 5, 3, true),  FASE_CV(256, 6, 3, true),
     FASE_CV(256, 7, 2, true),  FASE_CV(256, 8, 2, true),  FASE_CV(256, 9, 2, true),
     FASE_CV(256, 10, 2, true), FASE_CV(512, 6, 1, true),  FASE_CV(512, 8, 1, true),
-    FASE_CV(512, 10, 1, true), FASE_CV(512, 12, 1, true),
+    FASE_CV(512, 9, 1, true),  FASE_CV(512, 10, 1, true), FASE_CV(512, 12, 1, true),
+};
+// Alternative residency for measurement (FASE_ITERATE_COMPLEX_VARIANT=NTxEPxMINB;
+// same capacity as the default variant for K).
+struct ExtraVariant {
+  int minb;
+  Variant v;
+};
+const ExtraVariant kExtraVariants[] = {
+    {3, FASE_CV(256, 7, 3, true)}, {3, FASE_CV(256, 8, 3, true)}, {3, FASE_CV(256, 9, 3, true)},
 };
 #undef FASE_CV
 
@@ -418,6 +444,18 @@ const Variant* pick_variant(int K) {
   for (const Variant& v : kVariants)
     if (v.nt * v.ep >= K) return &v;
   return nullptr;
+}
+
+const Variant* override_variant(int K, const Variant* dflt) {
+  const char* env = getenv("FASE_ITERATE_COMPLEX_VARIANT");
+  if (!env || !dflt) return dflt;
+  int nt = 0, ep = 0, minb = 0;
+  if (sscanf(env, "%dx%dx%d", &nt, &ep, &minb) != 3) return dflt;
+  for (const ExtraVariant& x : kExtraVariants)
+    if (x.minb == minb && x.v.nt == nt && x.v.ep == ep && nt * ep >= K &&
+        nt * ep <= dflt->nt * dflt->ep)
+      return &x.v;
+  return dflt;
 }
 
 }  // namespace
@@ -465,7 +503,7 @@ extern "C" int fase_iterate_complex(const fase_iterate_args* args, void* stream)
     set_error("fase_iterate_complex: R_log recording is not available with chunked tables");
     return FASE_ERR_UNSUPPORTED;
   }
-  const Variant* v = pick_variant(a.K);
+  const Variant* v = override_variant(a.K, pick_variant(a.K));
   if (!v) {
     set_error("fase_iterate_complex: K=%d exceeds the largest kernel variant (%d atoms)", a.K,
               fase_max_atoms_complex());
@@ -477,7 +515,7 @@ extern "C" int fase_iterate_complex(const fase_iterate_args* args, void* stream)
     return FASE_ERR_SHAPE;
   }
   KernelFn fn = a.chunk_count ? v->chunked : (a.R_log ? v->record : v->plain);
-  const size_t smem = static_cast<size_t>(v->nt) * v->ep * sizeof(double2) * (v->dsmem ? 2 : 1);
+  const size_t smem = static_cast<size_t>(v->nt) * v->ep * (sizeof(double2) + (v->dsmem ? sizeof(double) : 0));
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);

@@ -56,7 +56,7 @@ def test_host_queries(lib):
     assert lib.fase_max_atoms_complex() >= 4608
     for k in (1, 64, 2304, 4608):
         assert _native.table_ld_complex(k) >= k
-    assert _native.table_ld_complex(2304) == 2304
+    assert _native.table_ld_complex(2304) == 2304 and _native.table_ld_complex(4608) == 4608
     with pytest.raises(errors.UnsupportedDictionaryError):
         _native.table_ld_complex(lib.fase_max_atoms_complex() + 1)
     # complex Gram workspace: w2, P o w2 and Q (K x 2 ldphi each), Re / Im (K x K)
