@@ -280,6 +280,33 @@ FASE_API int fase_synth_paste_complex(const double* phi2, int64_t ldphi, const i
                                       const int64_t* dst, double* out, int64_t ldout,
                                       double* max_imag, void* stream);
 
+/*
+ * Transform shortcuts (transform.py:43-110).
+ *
+ * fase_sep_products_complex: initial products of one complex separable part,
+ * atoms phi[col0 + u*Lc + v](m, n) = E[u, m] * F[v, n] (E = rows_re + i rows_im,
+ * F = cols_re + i cols_im; the DFT exponentials of dictionary.py:126-131), for
+ * B real weighted areas X:
+ *   R0[b*ldr + col0 + u*Lc + v] = sum_{m,n} conj(E[u,m]) conj(F[v,n]) X_b[m,n]
+ * (R0 interleaved complex, ldr in complex elements). For the full exponential
+ * grid this is fft2(X_b) -- fft_initial_products' identity -- at
+ * 2 (2 Lc Mr Nc + 4 Lr Lc Mr) flops per block instead of 4 Lr Lc Mr Nc.
+ *
+ * fase_fft_gram: the complex table of a frequency-tagged dictionary from the
+ * spectrum of its weight, spec = fft2(w) (M*N interleaved complex, e.g. from
+ * fase_sep_products_complex with X = w): S = (spec + conj(spec[-a,-b])) / 2,
+ *   T[k*ldt + l] = conj(C(k, l)) = S[(mu_l - mu_k) mod M, (eta_l - eta_k) mod N]
+ * zero-padded past K, exactly Hermitian with a real diagonal (fft_gram_table,
+ * transform.py:84-110). mu / eta: K int32 tags, or both NULL for the canonical
+ * order k = mu*N + eta.
+ */
+FASE_API int fase_sep_products_complex(const double* rows_re, const double* rows_im, int Lr, int Mr,
+                                       const double* cols_re, const double* cols_im, int Lc, int Nc,
+                                       const double* X, int64_t ldx, int B, double* R0, int64_t ldr,
+                                       int64_t col0, void* stream);
+FASE_API int fase_fft_gram(const double* spec, int M, int N, const int32_t* mu, const int32_t* eta,
+                           int K, double* T, int64_t ldt, void* stream);
+
 /* Writes `bytes` of zeros-then-ones into `buf` to evict L2 between timed steps. */
 FASE_API int fase_l2_flush(void* buf, size_t bytes, void* stream);
 

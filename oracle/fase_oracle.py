@@ -221,6 +221,46 @@ def select(metric: np.ndarray, quantum: float) -> int:
     return u
 
 
+# ----------------------------------------------------------------- transform shortcuts
+
+
+def fft_products(signal: np.ndarray, weight: np.ndarray, phi: np.ndarray, tags) -> np.ndarray:
+    """Initial products of tagged atoms from fft2(s*w) at (mu, eta); untagged
+    atoms directly (transform.py:43-69, without the min_tagged fallback)."""
+    s = np.asarray(signal)
+    m, n = s.shape
+    out = np.empty(phi.shape[0], dtype=np.complex128)
+    spec = np.fft.fft2(s * weight)
+    rest = []
+    for k, t in enumerate(tags):
+        if t is None:
+            rest.append(k)
+        else:
+            out[k] = spec[t[0] % m, t[1] % n]
+    if rest:
+        out[rest] = np.conj(phi[rest] @ np.conj((s * weight).ravel()))
+    return out
+
+
+def fft_gram(weight: np.ndarray, tags, m: int, n: int):
+    """Table from the symmetrized spectrum of the weight, gathered at tag
+    differences, then _finish_tables (transform.py:84-110)."""
+    spec = np.fft.fft2(weight)
+    mirror = spec[np.ix_((-np.arange(m)) % m, (-np.arange(n)) % n)]
+    spec = 0.5 * (spec + np.conj(mirror))
+    mu = np.array([t[0] for t in tags]) % m
+    eta = np.array([t[1] for t in tags]) % n
+    c = spec[(mu[:, None] - mu[None, :]) % m, (eta[:, None] - eta[None, :]) % n]
+    diag = c.diagonal().real.copy()
+    np.fill_diagonal(c, diag)
+    top = float(diag.max(initial=0.0))
+    d = np.zeros(diag.shape)
+    if top > 0.0:
+        alive = diag > DEGENERACY_RTOL * top
+        d[alive] = 1.0 / np.sqrt(diag[alive])
+    return c, d
+
+
 # ----------------------------------------------------------------- iteration
 
 

@@ -54,12 +54,13 @@ from .grid import (
     psnr_over_region,
 )
 from .model import BatchResult, IterationTrace, SparseModel
+from .transform import FFT_MIN_TAGGED, fft_gram_table, fft_initial_products
 from .workloads import central_loss_mask
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "Atom", "BatchResult", "ChunkedTables", "ExtrapolationPlan", "DegenerateAtomError", "Dictionary",
+    "Atom", "BatchResult", "FFT_MIN_TAGGED", "fft_gram_table", "fft_initial_products", "ChunkedTables", "ExtrapolationPlan", "DegenerateAtomError", "Dictionary",
     "ExtrapConfig", "FormatError", "GramTable", "IterationTrace", "MaskError",
     "NativeLibraryError", "NoSelectableAtomError", "ParameterError", "ShapeError",
     "SparseModel", "StaleTableError", "UnsupportedDictionaryError", "apply_model", "as_field",

@@ -35,7 +35,7 @@ EXPORTS = (
     "fase_synth_paste", "fase_l2_flush", "fase_frame_areas", "fase_frame_cells",
     "fase_frame_paste", "fase_weigh", "fase_sep_products", "fase_gram_complex_workspace",
     "fase_gram_complex", "fase_max_atoms_complex", "fase_table_ld_complex", "fase_iterate_complex",
-    "fase_synth_paste_complex",
+    "fase_synth_paste_complex", "fase_sep_products_complex", "fase_fft_gram",
 )
 
 _vp = ctypes.c_void_p
@@ -103,6 +103,9 @@ def load():
         "fase_gram_complex": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp, ctypes.c_size_t, _vp],
         "fase_synth_paste_complex": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp,
                                      _vp, _i64, _vp, _vp],
+        "fase_sep_products_complex": [_vp, _vp, _i32, _i32, _vp, _vp, _i32, _i32, _vp, _i64, _i32,
+                                      _vp, _i64, _i64, _vp],
+        "fase_fft_gram": [_vp, _i32, _i32, _vp, _vp, _i32, _vp, _i64, _vp],
         "fase_synth_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
                              _i64, _vp],
         "fase_l2_flush": [_vp, ctypes.c_size_t, _vp],
@@ -384,6 +387,32 @@ def synth_paste_complex(phi2, sel, coef, iterations: int, idx, out, *, idx_ptr=N
                                         iterations, B, _ptr(idx_ptr), _ptr(idx), n_shared,
                                         _ptr(dst), _ptr(out), ldout, _ptr(max_imag),
                                         _stream(out)))
+
+
+def sep_products_complex(rows_re, rows_im, cols_re, cols_im, X, M_rows: int, N_cols: int, R0,
+                         col0: int) -> None:
+    """R0[b, col0 + u*Lc + v] = (conj(E) X_b conj(F)^T)[u, v], E = rows_re + i rows_im,
+    F = cols_re + i cols_im (R0 complex128)."""
+    import torch
+
+    lib = load()
+    for t, n in ((rows_re, "rows_re"), (rows_im, "rows_im"), (cols_re, "cols_re"),
+                 (cols_im, "cols_im"), (X, "X")):
+        _require(t, n, torch.float64, 2)
+    _require_complex(R0, "R0", 2)
+    _check(lib.fase_sep_products_complex(_ptr(rows_re), _ptr(rows_im), rows_re.shape[0], M_rows,
+                                         _ptr(cols_re), _ptr(cols_im), cols_re.shape[0], N_cols,
+                                         _ptr(X), _ld(X), X.shape[0], _ptr(R0), _ld(R0), col0,
+                                         _stream(R0)))
+
+
+def fft_gram(spec, M: int, N: int, mu, eta, K: int, T) -> None:
+    """Complex table rows conj(C) gathered from the spectrum of the weight
+    (spec: complex128 (M*N,) or (1, M*N)); mu/eta int32 tags or None (canonical)."""
+    lib = load()
+    _require_complex(T, "T", 2)
+    _check(lib.fase_fft_gram(_ptr(spec), M, N, _ptr(mu), _ptr(eta), K, _ptr(T), _ld(T),
+                             _stream(T)))
 
 
 def max_atoms_complex() -> int:

@@ -146,6 +146,10 @@ class Dictionary:
         self.freqs = freqs
         self._content_hash: int | None = None if _parts is not None else early_hash
         self._device_cache: dict = {}
+        # complex sets: row ranges that are separable products rows[u,m]*cols[v,n]
+        # with complex factors (DFT exponentials, or real parts of a mixed union):
+        # [(first atom, rows (Lr, M) complex, cols (Lc, N) complex)]
+        self._cfactors: list = []
 
     # -- introspection ------------------------------------------------------
 
@@ -250,6 +254,23 @@ class Dictionary:
                             torch.from_numpy(np.ascontiguousarray(p.cols)).to(dev), row))
                 row += p.size
             self._device_cache[key] = out
+        return self._device_cache[key]
+
+    def device_cfactors(self, device):
+        """[(rows_re, rows_im, cols_re, cols_im, first atom)] on ``device`` for the
+        separable row ranges of a complex set (cached); [] when there are none."""
+        import torch
+
+        if self._is_real or not self._cfactors:
+            return []
+        dev = torch.device(device)
+        key = ("cfactors", dev.type, dev.index)
+        if key not in self._device_cache:
+            def up(a):
+                return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+
+            self._device_cache[key] = [(up(r.real), up(r.imag), up(c.real), up(c.imag), row0)
+                                       for row0, r, c in self._cfactors]
         return self._device_cache[key]
 
     def device_matrix(self, device):
@@ -374,7 +395,7 @@ def _dft_exponentials(m_rows: int, n_cols: int):
     en = np.exp(2j * np.pi * np.outer(np.arange(n_cols), np.arange(n_cols)) / n_cols)
     atoms = np.einsum("um,vn->uvmn", em, en).reshape(m_rows * n_cols, m_rows, n_cols)
     tags = [(mu, eta) for mu in range(m_rows) for eta in range(n_cols)]
-    return atoms, tags
+    return atoms, tags, (em, en)
 
 
 def _sign_snapped(x: np.ndarray) -> np.ndarray:
@@ -391,7 +412,7 @@ def _binarize_complex(values: np.ndarray) -> np.ndarray:
 def real_dft_atoms(m_rows: int, n_cols: int) -> np.ndarray:
     """(M*N, M, N) real DFT set: cos of pair representatives, then sin of the
     non-self-conjugate representatives (see module docstring)."""
-    atoms, _ = _dft_exponentials(m_rows, n_cols)
+    atoms, _, _ = _dft_exponentials(m_rows, n_cols)
     mu = np.arange(m_rows * n_cols) // n_cols
     eta = np.arange(m_rows * n_cols) % n_cols
     partner = ((m_rows - mu) % m_rows) * n_cols + (n_cols - eta) % n_cols
@@ -416,10 +437,12 @@ def generate_dictionary(kind: str, m_rows: int, n_cols: int) -> Dictionary:
     if m_rows < 1 or n_cols < 1:
         raise ParameterError(f"area must be at least 1x1, got {m_rows}x{n_cols}")
     if kind == "dft":
-        atoms, tags = _dft_exponentials(m_rows, n_cols)
-        return Dictionary(atoms, families="dft", freqs=tags)
+        atoms, tags, (em, en) = _dft_exponentials(m_rows, n_cols)
+        d = Dictionary(atoms, families="dft", freqs=tags)
+        d._cfactors = [(0, em, en)]
+        return d
     if kind == "bdft":
-        atoms, _ = _dft_exponentials(m_rows, n_cols)
+        atoms, _, _ = _dft_exponentials(m_rows, n_cols)
         return Dictionary(_binarize_complex(atoms), families="bdft")
     if kind == "dct":
         part = _SeparablePart(dct_rows(m_rows), dct_rows(n_cols))
@@ -467,9 +490,20 @@ def union_dictionaries(parts) -> Dictionary:
         return Dictionary(_parts=sep, _shape=shape, families=families, freqs=freqs)
     if all(p.is_real for p in parts):
         values = np.concatenate([p.real_values() for p in parts], axis=0)
-    else:
-        values = np.concatenate([p.values for p in parts], axis=0)
-    return Dictionary(values, families=families, freqs=freqs)
+        return Dictionary(values, families=families, freqs=freqs)
+    values = np.concatenate([p.values for p in parts], axis=0)
+    out = Dictionary(values, families=families, freqs=freqs)
+    row = 0
+    for p in parts:  # separable row ranges survive the union
+        if p.is_separable:
+            for q in p._parts:
+                out._cfactors.append((row, q.rows.astype(np.complex128),
+                                      q.cols.astype(np.complex128)))
+                row += q.size
+            continue
+        out._cfactors.extend((row + r0, a, b) for r0, a, b in p._cfactors)
+        row += len(p)
+    return out
 
 
 def parse_dict_spec(spec: str, m_rows: int, n_cols: int) -> Dictionary:

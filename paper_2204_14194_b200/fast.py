@@ -236,11 +236,30 @@ def initial_products_into(dictionary: Dictionary, F, W, R0, ws, *, method: str =
     dev = R0.device
     if R0.is_complex():
         # conj(Phi) (F o W) = [Re Phi; -Im Phi] (F o W): the conjugate-split
-        # matrix as 2K real atoms writes (re, im) pairs straight into R0
-        if method == "separable":
-            raise UnsupportedDictionaryError("separable initial products need a real dictionary")
-        _native.init_products(dictionary.device_matrix(dev), F, W, 2 * K, M, _real_view(R0), ws=ws)
-        return "gemm"
+        # matrix as 2K real atoms writes (re, im) pairs straight into R0.
+        # Separable row ranges (DFT exponentials) go through the complex
+        # transform instead (fft_initial_products' identity, transform.py:43-69).
+        parts = dictionary.device_cfactors(dev) if method in ("auto", "separable") else []
+        if method == "separable" and not parts:
+            raise UnsupportedDictionaryError("separable initial products need separable atoms")
+        if not parts:
+            _native.init_products(dictionary.device_matrix(dev), F, W, 2 * K, M, _real_view(R0),
+                                  ws=ws)
+            return "gemm"
+        B = F.shape[0]
+        ldx = M + (M & 1)
+        X = ws[: B * ldx].view(B, ldx)
+        _native.weigh(F, W, M, X)
+        m, n = dictionary.shape
+        covered = np.zeros(K, dtype=bool)
+        for rre, rim, cre, cim, row0 in parts:
+            _native.sep_products_complex(rre, rim, cre, cim, X, m, n, R0, row0)
+            covered[row0: row0 + rre.shape[0] * cre.shape[0]] = True
+        phi2 = dictionary.device_matrix(dev)
+        Rv = _real_view(R0)
+        for lo, hi in _ranges(~covered):  # the remaining rows: one DMMA GEMM each
+            _native.gemm_nt(X, phi2[2 * lo: 2 * hi], Rv[:, 2 * lo:])
+        return "separable" if covered.all() else "separable+gemm"
     factors = dictionary.device_factors(dev) if method in ("auto", "separable") else None
     if method == "separable" and factors is None:
         raise UnsupportedDictionaryError("separable initial products need a separable dictionary")
@@ -255,6 +274,13 @@ def initial_products_into(dictionary: Dictionary, F, W, R0, ws, *, method: str =
     for rows, cols, row0 in factors:
         _native.sep_products(rows, cols, X, m, n, R0, row0)
     return "separable"
+
+
+def _ranges(flags: np.ndarray):
+    """[(lo, hi)] runs of True in a boolean vector."""
+    f = np.concatenate([[False], np.asarray(flags, dtype=bool), [False]])
+    edges = np.flatnonzero(f[1:] != f[:-1])
+    return list(zip(edges[0::2], edges[1::2]))
 
 
 def build_gram_tables(dictionary: Dictionary, weight, *, block: int = 256, counter=None,
@@ -613,7 +639,7 @@ class ExtrapolationPlan:
         self.R0 = torch.empty((self.B, _round_up(K, 2)), dtype=vdt, device=dev)
         self.ws = torch.empty(max(_native.init_products_workspace(M, self.B) // 8, 2),
                               dtype=torch.float64, device=dev)
-        self.products = "gemm" if cplx else products
+        self.products = products
         self.selected = torch.empty((self.B, I), dtype=torch.int32, device=dev)
         self.projections = torch.empty((self.B, I), dtype=vdt, device=dev)
         self.coefficients = torch.empty((self.B, I), dtype=vdt, device=dev)
@@ -623,9 +649,20 @@ class ExtrapolationPlan:
         self.lost_idx = torch.from_numpy(lost if lost.size else np.zeros(1, np.int32)).to(dev)
         self.lost_pos = torch.arange(max(self.n_lost, 1), dtype=torch.int64, device=dev)
         self.lost = torch.zeros((self.B, max(self.n_lost, 1)), dtype=torch.float64, device=dev)
-        factors = dictionary.device_factors(dev) if self.products in ("auto", "separable") else None
-        # weigh + (one transform per separable part | one GEMM) + iterate + synth
-        self.launches_per_run = 1 + (len(factors) if factors else 1) + 1 + (1 if self.n_lost else 0)
+        if cplx:
+            cparts = dictionary.device_cfactors(dev) if products in ("auto", "separable") else []
+            n_prod = 1 + (len(cparts) + len(_ranges(self._uncovered(cparts))) if cparts else 1)
+        else:
+            factors = dictionary.device_factors(dev) if products in ("auto", "separable") else None
+            n_prod = 1 + (len(factors) if factors else 1)
+        # (weigh +) products + iterate + synth
+        self.launches_per_run = n_prod + 1 + (1 if self.n_lost else 0)
+
+    def _uncovered(self, cparts):
+        flags = np.ones(self.K, dtype=bool)
+        for rre, _, cre, _, row0 in cparts:
+            flags[row0: row0 + rre.shape[0] * cre.shape[0]] = False
+        return flags
 
     def _iterate_synth(self, sel, proj, coef, lost):
         if self.complex:

@@ -150,6 +150,27 @@ def complex_blocks(n_blocks: int = 3):
     return {"spec": "dft", "area": [m, n], "blocks": n_blocks, "seconds": time.time() - t0}
 
 
+def transform_cases():
+    """The reference's transform shortcuts (fft_initial_products / fft_gram_table)."""
+    out, rec = {}, []
+    for i, (spec, m, n) in enumerate([("dft", 8, 8), ("dft", 4, 6), ("union:dct+dft", 8, 8),
+                                      ("dft", 12, 12)]):
+        d = fase.parse_dict_spec(spec, m, n)
+        mask = wl.central_loss_mask(m, n, m // 2, n // 2)
+        w = fase.build_weight_field(mask, 0.8)
+        s = np.random.default_rng([2204, 200 + i]).uniform(0.0, 255.0, (m, n))
+        out[f"t{i}_signal"] = s
+        out[f"t{i}_w"] = w
+        out[f"t{i}_products"] = fase.fft_initial_products(s, w, d, min_tagged=1)
+        if len(d.tagged_indices()) == len(d):
+            t = fase.fft_gram_table(w, d)
+            out[f"t{i}_gram"] = t.c
+            out[f"t{i}_d"] = t.d
+        rec.append({"key": f"t{i}", "spec": spec, "m": m, "n": n})
+    np.savez_compressed(HERE / "transform_cases.npz", **out)
+    return rec
+
+
 def complex_arithmetic():
     """numpy's complex128 product and abs on this host (the oracle's semantics)."""
     rng = np.random.default_rng(22041)
@@ -268,6 +289,7 @@ def main():
     meta.update(weights_and_hashes())
     meta["small_cases"] = small_cases()
     meta["complex_cases"] = complex_cases()
+    meta["transform_cases"] = transform_cases()
     complex_arithmetic()
     meta["fgrm"] = fgrm_fixture()
     meta["c0"] = shared_config_blocks(0, [0])

@@ -183,3 +183,18 @@ def test_dft48_blocks(golden_dir):
         assert np.array_equal(res["coefficients"], z[f"b{b}_coefficients"])
         assert np.array_equal(res["patched"][mask], z[f"b{b}_patched_lost"])
         assert res["max_imag"] == z[f"b{b}_max_imag"]
+
+
+def test_transform_cases(golden_dir, meta):
+    """The oracle's restatement of the transform shortcuts equals the reference's."""
+    z = np.load(golden_dir / "transform_cases.npz")
+    for case in meta["transform_cases"]:
+        k, m, n = case["key"], case["m"], case["n"]
+        d = parse_dict_spec(case["spec"], m, n)
+        vals = oracle_values(case["spec"], m, n)
+        got = orc.fft_products(z[f"{k}_signal"], z[f"{k}_w"], vals.reshape(len(vals), -1), d.freqs)
+        assert np.array_equal(got, z[f"{k}_products"]), k
+        if f"{k}_gram" in z:
+            c, dd = orc.fft_gram(z[f"{k}_w"], d.freqs, m, n)
+            assert np.array_equal(c, z[f"{k}_gram"]), k
+            assert np.array_equal(dd, z[f"{k}_d"]), k
