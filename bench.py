@@ -345,6 +345,17 @@ def run_gpu(args):
     gram_ms = g0.elapsed_time(g1)
     assert torch.equal(G2, plan.G) and torch.equal(D2, plan.D), "Gram build is not deterministic"
     del G2, D2
+    fft_gram_ms = None
+    if cplx and len(d.tagged_indices()) == K:  # transform-shortcut table (fft_gram_table)
+        from paper_2204_14194_b200 import fft_gram_table
+
+        wfield = build_weight_field(mask, w.config.rho_hat)
+        fft_gram_table(wfield, d, device=dev)  # warm (factor upload)
+        g0.record()
+        fft_gram_table(wfield, d, device=dev)
+        g1.record()
+        torch.cuda.synchronize()
+        fft_gram_ms = g0.elapsed_time(g1)
 
     host = torch.from_numpy(wl.block_signals(args.config, B, *w.area, first=rank * B)).pin_memory()
     host2 = torch.from_numpy(wl.block_signals(args.config, B, *w.area,
@@ -488,6 +499,7 @@ def run_gpu(args):
             "stage_ms": {"init_products": float(np.mean(init_ms)), "iterate": float(np.mean(iter_ms)),
                          "synth": float(np.mean(synth_ms))},
             "gram_ms": gram_ms,
+            "fft_gram_ms": fft_gram_ms,
             "gram_tflops": (4 if cplx else 1) * K * (K + 1) * M / (gram_ms * 1e-3) / 1e12,
             "gpu_launches": args.steps * (plan.launches_per_run + 1) + args.steps * plan.launches_per_run,
             "clocks": clocks.summary(),

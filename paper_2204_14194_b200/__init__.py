@@ -53,14 +53,17 @@ from .grid import (
     center_distances,
     psnr_over_region,
 )
+from .conceal import DEFAULT_SUPPORT, conceal_frame, conceal_image
 from .model import BatchResult, IterationTrace, SparseModel
+from .pgm import read_mask_pgm, read_pgm, write_pgm
 from .transform import FFT_MIN_TAGGED, fft_gram_table, fft_initial_products
 from .workloads import central_loss_mask
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "Atom", "BatchResult", "FFT_MIN_TAGGED", "fft_gram_table", "fft_initial_products", "ChunkedTables", "ExtrapolationPlan", "DegenerateAtomError", "Dictionary",
+    "Atom", "BatchResult", "DEFAULT_SUPPORT", "conceal_frame", "conceal_image", "read_mask_pgm",
+    "read_pgm", "write_pgm", "FFT_MIN_TAGGED", "fft_gram_table", "fft_initial_products", "ChunkedTables", "ExtrapolationPlan", "DegenerateAtomError", "Dictionary",
     "ExtrapConfig", "FormatError", "GramTable", "IterationTrace", "MaskError",
     "NativeLibraryError", "NoSelectableAtomError", "ParameterError", "ShapeError",
     "SparseModel", "StaleTableError", "UnsupportedDictionaryError", "apply_model", "as_field",

@@ -299,3 +299,149 @@ def conceal_frame(image, lost_mask, *, dictionary: Dictionary | None = None,
                                              out.cpu().numpy(), lost)
     report["result"] = res
     return out, report
+
+
+# ----------------------------------------------------------------- reference semantics
+
+DEFAULT_SUPPORT = 24               # conceal.py:37
+REFERENCE_REPORT_SCHEMA = "fase-conceal-report/1"
+
+
+def _block_json(row, col, height, width, area, lost, seconds, psnr, max_imag, sel, coef):
+    """One entry of the report's ``blocks`` list (BlockResult.to_json, conceal.py:55-70)."""
+    return {
+        "row": int(row), "col": int(col), "height": int(height), "width": int(width),
+        "area": [int(x) for x in area], "lost": int(lost), "seconds": float(seconds),
+        "psnr_db": psnr, "max_imag": float(max_imag),
+        "trace": [{"atom": int(k), "coefficient": [float(c.real), float(c.imag)]}
+                  for k, c in zip(sel, coef)],
+    }
+
+
+def conceal_image(image, lost_mask, *, dict_spec: str = "dft",
+                  config: ExtrapConfig = ExtrapConfig(), block: tuple[int, int] | None = None,
+                  support: int = DEFAULT_SUPPORT, tables=None, use_fft: bool = False,
+                  single_thread: bool = False, reference=None, device=None):
+    """Fill the lost samples of an image and report what happened -- the
+    reference's ``conceal_image`` (``conceal.py:167-270``) on the GPU.
+
+    Same tiling, same clipped extrapolation areas (tile +- ``support``, cut at
+    the image border), same per-area dictionaries and weights, same paste of
+    each tile's own lost pixels, same report (schema ``fase-conceal-report/1``).
+    Instead of one job per tile, all tiles whose areas share a shape run as one
+    batch: identical geometries share a table, differing ones use chunked
+    per-block tables (``fase_extrapolate_batch``). ``tables`` serves every
+    group whose provenance matches (counted once, as ``tables_reused``);
+    ``use_fft`` builds shared tables through the transform shortcut where
+    every atom is frequency-tagged (initial products of exponential atoms are
+    always computed as separable transforms). ``single_thread`` is accepted for
+    signature compatibility (blocks are independent; results do not depend on
+    it). A block's ``seconds`` is its share of its batch's wall time.
+
+    Returns:
+        (restored float64 image (host), JSON-ready report dict).
+    """
+    import torch
+
+    from .fast import GramTable, build_gram_tables, provenance_hash
+    from .grid import build_weight_field
+    from .transform import fft_gram_table
+
+    img = np.asarray(image, dtype=np.float64)
+    if img.ndim != 2 or img.size == 0:
+        raise ShapeError(f"image must be non-empty 2-D, got shape {img.shape}")
+    lost = as_mask(lost_mask)
+    if lost.shape != img.shape:
+        raise ShapeError(f"image {img.shape} vs mask {lost.shape}")
+    ref = None
+    if reference is not None:
+        ref = np.asarray(reference, dtype=np.float64)
+        if ref.shape != img.shape:
+            raise ShapeError(f"image {img.shape} vs reference {ref.shape}")
+    if support < 0:
+        raise ParameterError(f"support margin must be >= 0, got {support}")
+    h_img, w_img = img.shape
+    if block is None:
+        tiles = [(0, 0, h_img, w_img)]
+        grid = None
+    else:
+        bh, bw = block
+        if bh < 1 or bw < 1:
+            raise ParameterError(f"block must be at least 1x1, got {bh}x{bw}")
+        tiles = [(r0, c0, min(bh, h_img - r0), min(bw, w_img - c0))
+                 for r0 in range(0, h_img, bh) for c0 in range(0, w_img, bw)]
+        grid = [bh, bw]
+    jobs = [t for t in tiles if lost[t[0]:t[0] + t[2], t[1]:t[1] + t[3]].any()]
+
+    started = time.perf_counter()
+    out = img.copy()
+    entries = [None] * len(jobs)
+    reused = 0
+    if jobs:
+        dev = resolve_device(device)
+        # clipped areas (conceal.py:119-124), grouped by shape
+        areas = []
+        for r0, c0, bh_, bw_ in jobs:
+            a_r0, a_c0 = max(0, r0 - support), max(0, c0 - support)
+            a_r1, a_c1 = min(h_img, r0 + bh_ + support), min(w_img, c0 + bw_ + support)
+            areas.append((a_r0, a_c0, a_r1, a_c1))
+        groups: dict = {}
+        for j, (a_r0, a_c0, a_r1, a_c1) in enumerate(areas):
+            groups.setdefault((a_r1 - a_r0, a_c1 - a_c0), []).append(j)
+        for shape, members in groups.items():
+            t_g = time.perf_counter()
+            d = parse_dict_spec(dict_spec, *shape)
+            sig = np.stack([img[a[0]:a[2], a[1]:a[3]] for a in (areas[j] for j in members)])
+            msk = np.stack([lost[a[0]:a[2], a[1]:a[3]] for a in (areas[j] for j in members)])
+            shared = bool((msk == msk[0]).all())
+            tab = None
+            if shared:
+                w = build_weight_field(msk[0], config.rho_hat)
+                key = provenance_hash(d, w)
+                if isinstance(tables, GramTable) and tables.provenance == key:
+                    tab = tables
+                    reused = 1
+                elif use_fft and len(d.tagged_indices()) == len(d):
+                    tab = fft_gram_table(w, d, device=dev)
+                else:
+                    tab = build_gram_tables(d, w, device=dev)
+                masks_arg = msk[0]
+            else:
+                masks_arg = msk
+            res = fase_extrapolate_batch(sig, masks_arg, d, tab, config, device=dev)
+            patched = res.patched.cpu().numpy()
+            sel = res.selected.cpu().numpy()
+            coef = res.coefficients.cpu().numpy().astype(np.complex128)
+            mi = (res.max_imag.cpu().numpy() if res.max_imag is not None
+                  else np.zeros(len(members)))
+            each = (time.perf_counter() - t_g) / len(members)
+            for i, j in enumerate(members):
+                r0, c0, bh_, bw_ = jobs[j]
+                a_r0, a_c0, a_r1, a_c1 = areas[j]
+                tile_lost = lost[r0:r0 + bh_, c0:c0 + bw_]
+                rel = patched[i][r0 - a_r0:r0 - a_r0 + bh_, c0 - a_c0:c0 - a_c0 + bw_]
+                out[r0:r0 + bh_, c0:c0 + bw_][tile_lost] = rel[tile_lost]
+                psnr = None
+                if ref is not None:
+                    psnr = psnr_over_region(ref[r0:r0 + bh_, c0:c0 + bw_],
+                                            out[r0:r0 + bh_, c0:c0 + bw_], tile_lost)
+                entries[j] = _block_json(r0, c0, bh_, bw_, (a_r0, a_c0, a_r1 - a_r0, a_c1 - a_c0),
+                                         tile_lost.sum(), each, psnr, mi[i], sel[i], coef[i])
+        torch.cuda.current_stream(dev).synchronize()
+    total_seconds = time.perf_counter() - started
+    overall_psnr = None
+    if ref is not None and lost.any():
+        overall_psnr = psnr_over_region(ref, out, lost)
+    report = {
+        "schema": REFERENCE_REPORT_SCHEMA,
+        "image": {"height": h_img, "width": w_img},
+        "settings": {"dict": dict_spec, "iterations": config.iterations, "gamma": config.gamma,
+                     "rho": config.rho_hat, "block": grid, "support": support, "fft": use_fft},
+        "lost_pixels": int(lost.sum()),
+        "blocks": entries,
+        "tables_reused": reused,
+        "psnr_db": overall_psnr,
+        "max_imag": max((e["max_imag"] for e in entries), default=0.0),
+        "seconds": total_seconds,
+    }
+    return out, report

@@ -44,16 +44,23 @@ def _tags(dictionary: Dictionary):
     return tagged, mu, eta
 
 
+_FACTORS: dict = {}
+
+
 def _grid_factors(m_rows: int, n_cols: int, device):
-    """The reference's exponential factors exp(2j pi u m / M) (dictionary.py:127-128)."""
+    """The reference's exponential factors exp(2j pi u m / M) (dictionary.py:127-128),
+    uploaded once per (area, device)."""
     torch = _torch()
-    em = np.exp(2j * np.pi * np.outer(np.arange(m_rows), np.arange(m_rows)) / m_rows)
-    en = np.exp(2j * np.pi * np.outer(np.arange(n_cols), np.arange(n_cols)) / n_cols)
+    key = (m_rows, n_cols, device.type, device.index)
+    if key not in _FACTORS:
+        em = np.exp(2j * np.pi * np.outer(np.arange(m_rows), np.arange(m_rows)) / m_rows)
+        en = np.exp(2j * np.pi * np.outer(np.arange(n_cols), np.arange(n_cols)) / n_cols)
 
-    def up(a):
-        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
+        def up(a):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
 
-    return up(em.real), up(em.imag), up(en.real), up(en.imag)
+        _FACTORS[key] = (up(em.real), up(em.imag), up(en.real), up(en.imag))
+    return _FACTORS[key]
 
 
 def weighted_spectra(x, m_rows: int, n_cols: int, device=None):

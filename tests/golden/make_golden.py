@@ -171,6 +171,58 @@ def transform_cases():
     return rec
 
 
+def conceal_cases():
+    """The reference's conceal_image (clipped border areas, per-tile paste, report)."""
+    rng = np.random.default_rng(22042)
+    h, w = 37, 45
+    yy, xx = np.mgrid[0:h, 0:w]
+    img = 128 + 40 * np.cos(0.31 * yy + 0.17 * xx) + 25 * np.sin(0.11 * yy - 0.27 * xx + 1.0)
+    img = np.clip(img + rng.normal(0, 2, (h, w)), 0, 255)
+    lost = np.zeros((h, w), dtype=bool)
+    lost[0:5, 0:6] = True        # top-left corner tile (clipped area)
+    lost[10:14, 18:23] = True    # interior
+    lost[30:37, 40:45] = True    # bottom-right partial tile
+    lost[17:20, 0:3] = True      # left edge
+    observed = img.copy()
+    observed[lost] = 0.0
+    out, meta = {}, []
+    runs = [("dct", (8, 8), 4, 30), ("dft", (8, 8), 4, 30), ("union:dct+dft", (12, 10), 3, 20)]
+    for i, (spec, block, support, iters) in enumerate(runs):
+        cfg = fase.ExtrapConfig(iterations=iters, gamma=0.5, rho_hat=0.8)
+        restored, report = fase.conceal_image(observed, lost, dict_spec=spec, config=cfg,
+                                              block=block, support=support, reference=img,
+                                              single_thread=True)
+        out[f"k{i}_restored"] = restored
+        for b in report["blocks"]:
+            b.pop("seconds")
+        report.pop("seconds")
+        meta.append({"key": f"k{i}", "spec": spec, "block": list(block), "support": support,
+                     "iterations": iters, "report": report})
+    # whole image as one area (block=None), the reference's default dictionary
+    small = img[:16, :16].copy()
+    lost16 = fase.central_loss_mask(16, 16, 4, 4)
+    obs16 = small.copy()
+    obs16[lost16] = 0.0
+    restored, report = fase.conceal_image(obs16, lost16, config=fase.ExtrapConfig(iterations=40),
+                                          reference=small)
+    out["whole_restored"] = restored
+    out["whole_observed"] = obs16
+    out["whole_reference"] = small
+    out["whole_lost"] = lost16
+    for b in report["blocks"]:
+        b.pop("seconds")
+    report.pop("seconds")
+    meta.append({"key": "whole", "spec": "dft", "block": None, "support": 24, "iterations": 40,
+                 "report": report})
+    out["image"] = img
+    out["observed"] = observed
+    out["lost"] = lost
+    np.savez_compressed(HERE / "conceal_cases.npz", **out)
+    with open(HERE / "conceal_cases.json", "w") as fh:
+        json.dump(meta, fh)
+    return [m["key"] for m in meta]
+
+
 def complex_arithmetic():
     """numpy's complex128 product and abs on this host (the oracle's semantics)."""
     rng = np.random.default_rng(22041)
@@ -290,6 +342,7 @@ def main():
     meta["small_cases"] = small_cases()
     meta["complex_cases"] = complex_cases()
     meta["transform_cases"] = transform_cases()
+    meta["conceal_cases"] = conceal_cases()
     complex_arithmetic()
     meta["fgrm"] = fgrm_fixture()
     meta["c0"] = shared_config_blocks(0, [0])

@@ -1,0 +1,138 @@
+"""GPU parity of ``conceal_image`` against the reference's own runs.
+
+The fixtures (tests/golden/conceal_cases.*) are the reference's conceal_image
+on a small scene with losses at corners, edges and the interior: clipped
+border areas of several shapes, real, complex and mixed dictionaries, and the
+whole-image mode with the default dictionary. Per block: identical tiling,
+area and loss count; the selection trace identical up to a legitimate
+near-tie; coefficients, restored pixels and PSNR within the BASELINE
+tolerance (1e-6 of the run scale).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import fase_oracle as orc  # noqa: E402
+from paper_2204_14194_b200 import (  # noqa: E402
+    ExtrapConfig,
+    MaskError,
+    ParameterError,
+    ShapeError,
+    build_gram_tables,
+    build_weight_field,
+    central_loss_mask,
+    conceal_image,
+    parse_dict_spec,
+)
+from paper_2204_14194_b200.conceal import REFERENCE_REPORT_SCHEMA  # noqa: E402
+from parity import COEF_REL, compare_selection, metric_fn  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def golden(golden_dir):
+    with open(golden_dir / "conceal_cases.json") as fh:
+        meta = json.load(fh)
+    return meta, np.load(golden_dir / "conceal_cases.npz")
+
+
+def _check_report(got, want, image, lost, spec, iterations):
+    assert got["schema"] == want["schema"] == REFERENCE_REPORT_SCHEMA
+    assert got["image"] == want["image"]
+    assert {k: v for k, v in got["settings"].items()} == want["settings"]
+    assert got["lost_pixels"] == want["lost_pixels"]
+    assert got["tables_reused"] == want["tables_reused"]
+    assert len(got["blocks"]) == len(want["blocks"])
+    exact = 0
+    for g, w in zip(got["blocks"], want["blocks"]):
+        for key in ("row", "col", "height", "width", "area", "lost"):
+            assert g[key] == w[key], key
+        gs = [t["atom"] for t in g["trace"]]
+        ws = [t["atom"] for t in w["trace"]]
+        gc = np.array([complex(*t["coefficient"]) for t in g["trace"]])
+        wc = np.array([complex(*t["coefficient"]) for t in w["trace"]])
+        a_r0, a_c0, ah, aw = w["area"]
+
+        def metric_at(t, a_r0=a_r0, a_c0=a_c0, ah=ah, aw=aw):
+            sig = image[a_r0:a_r0 + ah, a_c0:a_c0 + aw]
+            msk = lost[a_r0:a_r0 + ah, a_c0:a_c0 + aw]
+            vals = parse_dict_spec(spec, ah, aw).values
+            ref = orc.extrapolate_block(sig, msk, vals, 0.5, t, 0.8, record=True)
+            return metric_fn(ref["r0"], ref["d"], ref["log"])(t)
+
+        v = compare_selection(gs, ws, metric_at)
+        assert v.ok, f"block {(w['row'], w['col'])}: diverged at {v.stop}, gap {v.gap}"
+        s = v.stop
+        assert np.abs(gc[:s] - wc[:s]).max(initial=0) <= COEF_REL * np.abs(wc[:s]).max(initial=1)
+        if v.exact:
+            exact += 1
+            assert abs(g["max_imag"] - w["max_imag"]) <= 1e-6 * max(1.0, w["max_imag"])
+            if w["psnr_db"] is not None:
+                assert abs(g["psnr_db"] - w["psnr_db"]) < 1e-6
+    return exact
+
+
+@pytest.mark.parametrize("i", [0, 1, 2])
+def test_conceal_image_blocked_against_reference(golden, i):
+    meta, z = golden
+    case = meta[i]
+    cfg = ExtrapConfig(case["iterations"], 0.5, 0.8)
+    restored, report = conceal_image(z["observed"], z["lost"], dict_spec=case["spec"], config=cfg,
+                                     block=tuple(case["block"]), support=case["support"],
+                                     reference=z["image"], device=DEV)
+    exact = _check_report(report, case["report"], z["observed"], z["lost"], case["spec"],
+                          case["iterations"])
+    assert exact >= len(case["report"]["blocks"]) - 1
+    want = z[f"{case['key']}_restored"]
+    assert np.array_equal(restored[~z["lost"]], want[~z["lost"]])  # support untouched
+    if exact == len(case["report"]["blocks"]):
+        assert np.abs(restored - want).max() <= COEF_REL * 255
+        assert abs(report["psnr_db"] - case["report"]["psnr_db"]) < 1e-6
+
+
+def test_conceal_image_whole_area_default_dictionary(golden):
+    meta, z = golden
+    case = meta[3]
+    restored, report = conceal_image(z["whole_observed"], z["whole_lost"],
+                                     config=ExtrapConfig(iterations=40),
+                                     reference=z["whole_reference"], device=DEV)
+    _check_report(report, case["report"], z["whole_observed"], z["whole_lost"], "dft", 40)
+    assert np.abs(restored - z["whole_restored"]).max() <= COEF_REL * 255
+
+
+def test_conceal_image_tables_fft_and_edges():
+    rng = np.random.default_rng(4)
+    img = np.clip(128 + 30 * np.cos(np.arange(256).reshape(16, 16) * 0.3) +
+                  rng.normal(0, 1, (16, 16)), 0, 255)
+    lost = central_loss_mask(16, 16, 4, 4)
+    obs = img.copy()
+    obs[lost] = 0.0
+    cfg = ExtrapConfig(iterations=30)
+    d = parse_dict_spec("dct", 16, 16)
+    tables = build_gram_tables(d, build_weight_field(lost, cfg.rho_hat), device=DEV)
+    plain, _ = conceal_image(obs, lost, dict_spec="dct", config=cfg, device=DEV)
+    reused, rep = conceal_image(obs, lost, dict_spec="dct", config=cfg, tables=tables, device=DEV)
+    assert rep["tables_reused"] == 1
+    assert np.array_equal(plain, reused)
+    direct, _ = conceal_image(obs, lost, dict_spec="dft", config=cfg, device=DEV)
+    via_fft, rep = conceal_image(obs, lost, dict_spec="dft", config=cfg, use_fft=True, device=DEV)
+    assert rep["settings"]["fft"] is True
+    assert np.allclose(direct, via_fft, rtol=0, atol=1e-9)
+    same, rep = conceal_image(img, np.zeros((16, 16), bool), device=DEV)
+    assert np.array_equal(same, img) and rep["blocks"] == [] and rep["psnr_db"] is None
+    with pytest.raises(ShapeError):
+        conceal_image(img, np.zeros((16, 15), bool), device=DEV)
+    with pytest.raises(ShapeError):
+        conceal_image(img, lost, reference=np.zeros((4, 4)), device=DEV)
+    with pytest.raises(ParameterError):
+        conceal_image(img, lost, support=-1, device=DEV)
+    with pytest.raises(ParameterError):
+        conceal_image(img, lost, block=(0, 8), device=DEV)
+    with pytest.raises(MaskError):  # an area with no support left
+        conceal_image(img, np.ones((16, 16), bool), block=(8, 8), support=0, device=DEV)
