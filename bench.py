@@ -391,7 +391,7 @@ def run_gpu(args):
             e[0].record(stream)
             if split:
                 plan.F[:, :M].copy_(dev_sig.reshape(B, -1), non_blocking=True)
-                initial_products_into(d, plan.F, plan.W, plan.R0, plan.ws, method=plan.products)
+                plan._products(plan.F)
                 e[1].record(stream)
                 iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, plan.selected,
                         plan.projections, plan.coefficients)
@@ -445,6 +445,8 @@ def run_gpu(args):
         achieved = bytes_iter / it_s / 1e9
         init_s = float(np.mean(init_ms)) / 1e3
         flops_init = (4.0 if cplx else 2.0) * K * M * B
+        if plan._support is not None:  # contraction over the support samples only
+            flops_init = (4.0 if cplx else 2.0) * K * int(plan._support[0].shape[0]) * B
         factors = d.device_factors(dev) if plan.products in ("auto", "separable") else None
         if factors:  # executed flops of the separable form
             mr, nc = w.area
@@ -482,7 +484,8 @@ def run_gpu(args):
                          "note": ("16*K bytes per block-iteration (one complex128 table row)"
                                   if cplx else "8*K bytes per block-iteration (one FP64 table row)")
                                  + "; hot rows hit L2, so frac can exceed DRAM-bound expectations"},
-            "roofline_init": ({"bound": "tensor", "kernel": "dgemm_nt_kernel (DMMA FP64)",
+            "roofline_init": ({"bound": "tensor", "kernel": "dgemm_nt_kernel (DMMA FP64)"
+                               + (" over the support samples" if plan._support is not None else ""),
                                "achieved": flops_init / init_s / 1e12, "peak": fp64,
                                "unit": "TFLOP/s", "frac": flops_init / init_s / 1e12 / fp64,
                                "ms_per_launch": init_s * 1e3, "peak_source": fsrc}

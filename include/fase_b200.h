@@ -121,6 +121,16 @@ FASE_API int fase_weigh(const double* x, int64_t ldx, const double* w, int64_t l
                         int M, double* out, int64_t ldo, void* stream);
 
 /*
+ * Weighted operand on the samples with nonzero weight (the support):
+ *   out[b*ldo + i] = x[b*ldx + idx[i]] * w[i]   for i < n, zero-padded to even n
+ * With Phi's columns gathered the same way once, fase_gemm_nt over n instead of
+ * M samples gives the same products: lost samples add exact zeros
+ * (initial_scalar_products, fast.py:154, over the support only).
+ */
+FASE_API int fase_weigh_gather(const double* x, int64_t ldx, const int32_t* idx, const double* w,
+                               int rows, int n, double* out, int64_t ldo, void* stream);
+
+/*
  * Initial products of one separable dictionary part (atoms
  * phi[col0 + u*Lc + v](m, n) = rows[u, m] * cols[v, n], dictionary.py:167-178)
  * for B weighted areas X (B x ldx, Mr*Nc samples each, e.g. the F o W formed

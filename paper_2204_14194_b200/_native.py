@@ -35,7 +35,7 @@ EXPORTS = (
     "fase_synth_paste", "fase_l2_flush", "fase_frame_areas", "fase_frame_cells",
     "fase_frame_paste", "fase_weigh", "fase_sep_products", "fase_gram_complex_workspace",
     "fase_gram_complex", "fase_max_atoms_complex", "fase_table_ld_complex", "fase_iterate_complex",
-    "fase_synth_paste_complex", "fase_sep_products_complex", "fase_fft_gram",
+    "fase_synth_paste_complex", "fase_sep_products_complex", "fase_fft_gram", "fase_weigh_gather",
 )
 
 _vp = ctypes.c_void_p
@@ -106,6 +106,7 @@ def load():
         "fase_sep_products_complex": [_vp, _vp, _i32, _i32, _vp, _vp, _i32, _i32, _vp, _i64, _i32,
                                       _vp, _i64, _i64, _vp],
         "fase_fft_gram": [_vp, _i32, _i32, _vp, _vp, _i32, _vp, _i64, _vp],
+        "fase_weigh_gather": [_vp, _i64, _vp, _vp, _i32, _i32, _vp, _i64, _vp],
         "fase_synth_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
                              _i64, _vp],
         "fase_l2_flush": [_vp, ctypes.c_size_t, _vp],
@@ -481,6 +482,19 @@ def weigh(x, w, M: int, out) -> None:
     ldw = _ld(w) if w.dim() == 2 else 0
     _check(lib.fase_weigh(_ptr(x), _ld(x), _ptr(w), ldw, x.shape[0], M, _ptr(out), _ld(out),
                           _stream(out)))
+
+
+def weigh_gather(x, idx, w, out) -> None:
+    """out[b, i] = x[b, idx[i]] * w[i] (i < len(idx)), zero pad to even width."""
+    import torch
+
+    lib = load()
+    _require(x, "x", torch.float64, 2)
+    _require(idx, "idx", torch.int32, 1)
+    _require(w, "w", torch.float64, 1)
+    _require(out, "out", torch.float64, 2)
+    _check(lib.fase_weigh_gather(_ptr(x), _ld(x), _ptr(idx), _ptr(w), x.shape[0], idx.shape[0],
+                                 _ptr(out), _ld(out), _stream(out)))
 
 
 def sep_products(rows, cols, X, M_rows: int, N_cols: int, R0, col0: int) -> None:

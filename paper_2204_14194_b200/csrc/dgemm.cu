@@ -236,6 +236,22 @@ __global__ void weigh_kernel(const double* __restrict__ x, int64_t ldx, const do
   }
 }
 
+// out[b*ldo + i] = x[b*ldx + idx[i]] * w[i] for i < n (zero pad to even n): the
+// weighted operand restricted to the samples with nonzero weight (lost samples
+// contribute exact zeros to every product, so the contraction skips them).
+__global__ void weigh_gather_kernel(const double* __restrict__ x, int64_t ldx,
+                                    const int32_t* __restrict__ idx, const double* __restrict__ w,
+                                    int rows, int n, double* __restrict__ out, int64_t ldo) {
+  const int np = (n + 1) / 2 * 2;
+  const int64_t total = static_cast<int64_t>(rows) * np;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int b = static_cast<int>(e / np);
+    const int i = static_cast<int>(e - static_cast<int64_t>(b) * np);
+    out[b * ldo + i] = i < n ? mul_rn(__ldg(x + b * ldx + __ldg(idx + i)), __ldg(w + i)) : 0.0;
+  }
+}
+
 template <class T, bool kSym>
 int launch(const GemmParams& p, cudaStream_t stream, const char* what) {
   // per-device attributes; cheap enough to set on every launch
@@ -498,4 +514,23 @@ extern "C" int fase_gram_complex(const double* phi2, int64_t ldphi, const double
   hermitian_pack_kernel<<<grid, dim3(32, 8), 0, s>>>(cre, cim, ldk, K, reinterpret_cast<double2*>(T),
                                                      ldt);
   return check_launch("fase_gram_complex (pack)");
+}
+
+extern "C" int fase_weigh_gather(const double* x, int64_t ldx, const int32_t* idx, const double* w,
+                                 int rows, int n, double* out, int64_t ldo, void* stream) {
+  if (rows < 0 || n < 1 || ldo < (n + 1) / 2 * 2) {
+    set_error("fase_weigh_gather: bad sizes (rows=%d, n=%d, ldo=%lld)", rows, n,
+              static_cast<long long>(ldo));
+    return FASE_ERR_SHAPE;
+  }
+  if (rows == 0) return FASE_OK;
+  if (!x || !idx || !w || !out) {
+    set_error("fase_weigh_gather: null pointer");
+    return FASE_ERR_SHAPE;
+  }
+  const int64_t total = static_cast<int64_t>(rows) * ((n + 1) / 2 * 2);
+  const int64_t blocks = (total + 255) / 256;
+  weigh_gather_kernel<<<static_cast<unsigned>(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0,
+                        as_stream(stream)>>>(x, ldx, idx, w, rows, n, out, ldo);
+  return check_launch("fase_weigh_gather");
 }

@@ -655,8 +655,36 @@ class ExtrapolationPlan:
         else:
             factors = dictionary.device_factors(dev) if products in ("auto", "separable") else None
             n_prod = 1 + (len(factors) if factors else 1)
+        # Dense products over the support only: the lost samples have weight 0
+        # and add exact zeros, so Phi's support columns are gathered once and
+        # each run contracts over them (fase_weigh_gather + one DMMA GEMM).
+        self._support = None
+        dense = (cplx and not cparts) or (not cplx and not factors)
+        support = np.flatnonzero(w.ravel() != 0.0).astype(np.int32)
+        if dense and products in ("auto", "gemm", "support") and support.size < M:
+            n_s = support.size
+            phi_s = torch.zeros((self.phi.shape[0], n_s + (n_s & 1)), dtype=torch.float64,
+                                device=dev)
+            sidx = torch.from_numpy(support).to(dev)
+            phi_s[:, :n_s] = self.phi.index_select(1, sidx.long())
+            w_s = torch.from_numpy(np.ascontiguousarray(w.ravel()[support])).to(dev)
+            self._support = (sidx, w_s, phi_s,
+                             torch.empty((self.B, n_s + (n_s & 1)), dtype=torch.float64,
+                                         device=dev))
+            n_prod = 2
         # (weigh +) products + iterate + synth
         self.launches_per_run = n_prod + 1 + (1 if self.n_lost else 0)
+
+    def _products(self, F):
+        """R0 for signals F (device, (B, ldf)): the support-compacted GEMM when
+        the products are dense, else initial_products_into."""
+        if self._support is None:
+            return initial_products_into(self.dictionary, F, self.W, self.R0, self.ws,
+                                         method=self.products)
+        sidx, w_s, phi_s, X = self._support
+        _native.weigh_gather(F, sidx, w_s, X)
+        _native.gemm_nt(X, phi_s, _real_view(self.R0) if self.complex else self.R0)
+        return "gemm-support"
 
     def _uncovered(self, cparts):
         flags = np.ones(self.K, dtype=bool)
@@ -685,8 +713,7 @@ class ExtrapolationPlan:
         if signals is not None:
             src = signals.reshape(self.B, -1)
             self.F[:, : self.M].copy_(src, non_blocking=True)
-        self.products_method = initial_products_into(self.dictionary, self.F, self.W, self.R0,
-                                                     self.ws, method=self.products)
+        self.products_method = self._products(self.F)
         self._iterate_synth(self.selected, self.projections, self.coefficients, self.lost)
         return self
 
@@ -747,8 +774,7 @@ class ExtrapolationPlan:
             cs.wait_event(ev_in[s])
             if ev_out[s] is not None:
                 cs.wait_event(ev_out[s])
-            initial_products_into(self.dictionary, F, self.W, self.R0, self.ws,
-                                  method=self.products)
+            self._products(F)
             ev_used[s] = torch.cuda.Event()
             ev_used[s].record(cs)
             self._iterate_synth(sel, proj, coef, lost)

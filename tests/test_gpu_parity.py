@@ -402,3 +402,29 @@ def test_separable_products_match_gemm_and_oracle(spec, m, n):
         want = orc.initial_products(sig[b], w, phi).real
         assert rel_dev(outs["separable"][b], want) < 1e-13
         assert rel_dev(outs["gemm"][b], want) < 1e-13
+
+
+@pytest.mark.parametrize("spec", ["gauss:600:7", "union:rdft+brdft", "bdft"])
+def test_plan_support_compacted_products(spec):
+    """Dense products over the support only (lost samples add exact zeros):
+    same R0 as the full GEMM to rounding, same selections as the oracle."""
+    from paper_2204_14194_b200 import ExtrapolationPlan
+
+    d = parse_dict_spec(spec, 16, 16)
+    mask = wl.central_loss_mask(16, 16, 6, 6)
+    cfg = ExtrapConfig(40, 0.5, 0.85)
+    sig = np.random.default_rng(8).uniform(0, 255, (7, 16, 16))
+    plan = ExtrapolationPlan(d, mask, 7, cfg, device=DEV)
+    assert plan._support is not None and plan.launches_per_run == 4
+    plan.run(torch.from_numpy(sig).to(DEV))
+    assert plan.products_method == "gemm-support"
+    R0 = plan.R0[:, : len(d)].cpu().numpy()
+    w = orc.weight_field(mask, 0.85)
+    vals = d.values
+    for b in range(7):
+        ref = orc.extrapolate_block(sig[b], mask, vals, 0.5, 40, 0.85, record=True)
+        assert rel_dev(R0[b], ref["r0"] if not d.is_real else ref["r0"].real) < 1e-13
+        v = compare_selection(plan.selected[b].cpu().numpy(), ref["selected"],
+                              metric_fn(ref["r0"], ref["d"], ref["log"]))
+        assert v.ok
+    del w
