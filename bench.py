@@ -396,7 +396,7 @@ def run_gpu(args):
                 iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, plan.selected,
                         plan.projections, plan.coefficients)
                 e[2].record(stream)
-                synth(plan.phi, plan.selected, plan.coefficients, I, plan.lost_idx,
+                synth(plan.phi_lost, plan.selected, plan.coefficients, I, plan.lost_seq,
                       plan.lost, n_shared=plan.n_lost, dst=plan.lost_pos, **synth_extra)
                 e[3].record(stream)
             else:

@@ -649,6 +649,14 @@ class ExtrapolationPlan:
         self.lost_idx = torch.from_numpy(lost if lost.size else np.zeros(1, np.int32)).to(dev)
         self.lost_pos = torch.arange(max(self.n_lost, 1), dtype=torch.int64, device=dev)
         self.lost = torch.zeros((self.B, max(self.n_lost, 1)), dtype=torch.float64, device=dev)
+        # Phi restricted to the lost samples (synthesis reads only these; the
+        # compact copy stays L2-resident where the full matrix would not)
+        nl = max(self.n_lost, 1)
+        self.phi_lost = torch.zeros((self.phi.shape[0], nl + (nl & 1)), dtype=torch.float64,
+                                    device=dev)
+        if self.n_lost:
+            self.phi_lost[:, : self.n_lost] = self.phi.index_select(1, self.lost_idx.long())
+        self.lost_seq = torch.arange(nl, dtype=torch.int32, device=dev)
         if cplx:
             cparts = dictionary.device_cfactors(dev) if products in ("auto", "separable") else []
             n_prod = 1 + (len(cparts) + len(_ranges(self._uncovered(cparts))) if cparts else 1)
@@ -697,13 +705,13 @@ class ExtrapolationPlan:
             _native.iterate_complex(self.G, self.D, self.R0, self.K, self.I, self.config.gamma,
                                     sel, proj, coef)
             if self.n_lost:
-                _native.synth_paste_complex(self.phi, sel, coef, self.I, self.lost_idx, lost,
+                _native.synth_paste_complex(self.phi_lost, sel, coef, self.I, self.lost_seq, lost,
                                             n_shared=self.n_lost, dst=self.lost_pos,
                                             max_imag=self.max_imag)
             return
         _native.iterate(self.G, self.D, self.R0, self.K, self.I, self.config.gamma, sel, proj, coef)
         if self.n_lost:
-            _native.synth_paste(self.phi, sel, coef, self.I, self.lost_idx, lost,
+            _native.synth_paste(self.phi_lost, sel, coef, self.I, self.lost_seq, lost,
                                 n_shared=self.n_lost, dst=self.lost_pos)
 
     def run(self, signals=None):
