@@ -62,7 +62,7 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target wall seconds of the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--products", default="auto", choices=["auto", "gemm", "separable"],
+    ap.add_argument("--products", default="auto", choices=["auto", "gemm", "separable", "ozaki"],
                     help="initial products: separable transforms (separable dictionaries) or "
                          "the dense DMMA GEMM")
     ap.add_argument("--dict", default=None,
@@ -295,6 +295,30 @@ def ncu_traffic(kernel: str):
         return None
 
 
+def ozaki_roofline(plan, flops_fp64, seconds, fp64_peak, fp64_src):
+    """Initial products on the tcgen05 INT8 tensor cores (Ozaki digit planes):
+    the executed int8 MMA work against the INT8 dense peak (2x the measured
+    BF16 dense peak in MEASURED_PEAKS.json), with the FP64-equivalent rate."""
+    a, b = plan._ozaki
+    s = a.slices
+    pairs = s * (s + 1) // 2
+    ops = 2.0 * pairs * a.rows * b.rows * a.kp
+    i8_peak, src = 2 * 1649.9, "2 x measured BF16 dense burst (MEASURED_PEAKS.json)"
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            i8_peak = 2 * float(json.loads(p.read_text())["bf16_tflops"])
+        except (KeyError, ValueError):
+            pass
+    return {"bound": "tensor", "kernel": "ozaki_gemm_kernel (tcgen05.mma kind::i8, "
+            f"{s} digit planes, {pairs} pairs) over the support samples",
+            "achieved": ops / seconds / 1e12, "peak": i8_peak, "unit": "TOPS (int8)",
+            "frac": ops / seconds / 1e12 / i8_peak, "ms_per_launch": seconds * 1e3,
+            "peak_source": src, "fp64_equivalent_tflops": flops_fp64 / seconds / 1e12,
+            "fp64_peak_tflops": fp64_peak, "fp64_peak_source": fp64_src,
+            "note": "ms includes the weigh-gather and digit-split kernels of the batch"}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -484,7 +508,9 @@ def run_gpu(args):
                          "note": ("16*K bytes per block-iteration (one complex128 table row)"
                                   if cplx else "8*K bytes per block-iteration (one FP64 table row)")
                                  + "; hot rows hit L2, so frac can exceed DRAM-bound expectations"},
-            "roofline_init": ({"bound": "tensor", "kernel": "dgemm_nt_kernel (DMMA FP64)"
+            "roofline_init": (ozaki_roofline(plan, flops_init, init_s, fp64, fsrc)
+                              if plan._ozaki is not None else
+                              {"bound": "tensor", "kernel": "dgemm_nt_kernel (DMMA FP64)"
                                + (" over the support samples" if plan._support is not None else ""),
                                "achieved": flops_init / init_s / 1e12, "peak": fp64,
                                "unit": "TFLOP/s", "frac": flops_init / init_s / 1e12 / fp64,

@@ -317,6 +317,31 @@ FASE_API int fase_sep_products_complex(const double* rows_re, const double* rows
 FASE_API int fase_fft_gram(const double* spec, int M, int N, const int32_t* mu, const int32_t* eta,
                            int K, double* T, int64_t ldt, void* stream);
 
+/*
+ * FP64 contractions on the tcgen05 tensor cores (Ozaki scheme, kind::i8):
+ *
+ * fase_ozaki_split: digit planes of `rows` FP64 rows of length kd:
+ *   e[r] = min e with max_k |x[r,k]| < 2^e;
+ *   x[r,k] = 2^e[r] * sum_{i<slices} digit_i[r,k] * 2^{-7(i+1)} + residual
+ * (signed 7-bit digits, truncated; kd zero-padded to kp, a multiple of 64).
+ * Plane i occupies rows_pad * kp bytes at planes + i * rows_pad * kp, stored
+ * in the UMMA-ready tiled order [k / 64][r / 8][(k / 16) % 4][r % 8][k % 16].
+ *
+ * fase_ozaki_gemm: C[r*ldc + c] = sum_k X[r,k] Y[c,k] from the planes of X
+ * (a_rows_pad a multiple of 128) and Y (b_rows_pad a multiple of 64): int8 x
+ * int8 -> int32 tcgen05 MMAs for every digit pair i + j <= slices - 1
+ * (0-based), one TMEM accumulator per diagonal, combined in FP64 and scaled by
+ * 2^(e_X[r] + e_Y[c]). With 8 planes the result matches an FP64 contraction
+ * to rounding level (initial_scalar_products, fast.py:145-157, on the support).
+ */
+FASE_API int fase_ozaki_split(const double* x, int64_t ldx, int rows, int kd, int slices,
+                              int8_t* planes, int64_t kp, int rows_pad, int32_t* exps,
+                              void* stream);
+FASE_API int fase_ozaki_gemm(const int8_t* a_planes, int a_rows_pad, const int32_t* ea,
+                             int m_rows, const int8_t* b_planes, int b_rows_pad,
+                             const int32_t* eb, int n_rows, int64_t kp, int slices, double* C,
+                             int64_t ldc, void* stream);
+
 /* Writes `bytes` of zeros-then-ones into `buf` to evict L2 between timed steps. */
 FASE_API int fase_l2_flush(void* buf, size_t bytes, void* stream);
 

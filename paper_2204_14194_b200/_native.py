@@ -36,6 +36,7 @@ EXPORTS = (
     "fase_frame_paste", "fase_weigh", "fase_sep_products", "fase_gram_complex_workspace",
     "fase_gram_complex", "fase_max_atoms_complex", "fase_table_ld_complex", "fase_iterate_complex",
     "fase_synth_paste_complex", "fase_sep_products_complex", "fase_fft_gram", "fase_weigh_gather",
+    "fase_ozaki_split", "fase_ozaki_gemm",
 )
 
 _vp = ctypes.c_void_p
@@ -107,6 +108,9 @@ def load():
                                       _vp, _i64, _i64, _vp],
         "fase_fft_gram": [_vp, _i32, _i32, _vp, _vp, _i32, _vp, _i64, _vp],
         "fase_weigh_gather": [_vp, _i64, _vp, _vp, _i32, _i32, _vp, _i64, _vp],
+        "fase_ozaki_split": [_vp, _i64, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp],
+        "fase_ozaki_gemm": [_vp, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i64, _i32, _vp, _i64,
+                            _vp],
         "fase_synth_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
                              _i64, _vp],
         "fase_l2_flush": [_vp, ctypes.c_size_t, _vp],
@@ -495,6 +499,45 @@ def weigh_gather(x, idx, w, out) -> None:
     _require(out, "out", torch.float64, 2)
     _check(lib.fase_weigh_gather(_ptr(x), _ld(x), _ptr(idx), _ptr(w), x.shape[0], idx.shape[0],
                                  _ptr(out), _ld(out), _stream(out)))
+
+
+OZAKI_SLICES = 8
+
+
+class OzakiOperand:
+    """Digit planes of an FP64 operand (rows x kd) for the tcgen05 INT8 path."""
+
+    def __init__(self, rows: int, kd: int, row_align: int, device, slices: int = OZAKI_SLICES):
+        import torch
+
+        self.rows, self.kd, self.slices = rows, kd, slices
+        self.kp = (kd + 63) // 64 * 64
+        self.rows_pad = (max(rows, 1) + row_align - 1) // row_align * row_align
+        self.planes = torch.zeros((slices, self.rows_pad, self.kp), dtype=torch.int8, device=device)
+        self.exps = torch.zeros(self.rows_pad, dtype=torch.int32, device=device)
+
+    def split(self, x) -> "OzakiOperand":
+        import torch
+
+        lib = load()
+        _require(x, "x", torch.float64, 2)
+        _check(lib.fase_ozaki_split(_ptr(x), _ld(x), self.rows, self.kd, self.slices,
+                                    _ptr(self.planes), self.kp, self.rows_pad, _ptr(self.exps),
+                                    _stream(x)))
+        return self
+
+
+def ozaki_gemm(a: OzakiOperand, b: OzakiOperand, C) -> None:
+    """C[:a.rows, :b.rows] = X Y^T from the digit planes (C float64, 2-D)."""
+    import torch
+
+    lib = load()
+    _require(C, "C", torch.float64, 2)
+    if a.kp != b.kp or a.slices != b.slices:
+        raise errors.ShapeError("operands were split with different K padding / plane counts")
+    _check(lib.fase_ozaki_gemm(_ptr(a.planes), a.rows_pad, _ptr(a.exps), a.rows,
+                               _ptr(b.planes), b.rows_pad, _ptr(b.exps), b.rows, a.kp,
+                               a.slices, _ptr(C), _ld(C), _stream(C)))
 
 
 def sep_products(rows, cols, X, M_rows: int, N_cols: int, R0, col0: int) -> None:

@@ -126,6 +126,13 @@ class FrameEngine:
             wj = torch.zeros(width, dtype=torch.float64, device=dev)
             wj[: samples.size] = torch.from_numpy(flat_base[samples]).to(dev)
             _native.gram(sub, wj, K, samples.size, self.tables[c])
+        # dense initial products on the tcgen05 tensor cores (Ozaki digit planes)
+        self._oz_phi = None
+        if not dictionary.device_factors(dev):
+            from .fast import ozaki_worthwhile
+
+            if ozaki_worthwhile(4096, K):
+                self._oz_phi = _native.OzakiOperand(K, M, 64, dev).split(phi[:, :ld])
         torch.cuda.current_stream(dev).synchronize()
         self.table_seconds = time.perf_counter() - t0
         self.stride = self.tables[0].numel()
@@ -151,6 +158,10 @@ class FrameEngine:
                 proj=torch.empty((L, I), dtype=torch.float64, device=dev),
                 coef=torch.empty((L, I), dtype=torch.float64, device=dev),
             )}
+            from .fast import ozaki_worthwhile
+
+            if self._oz_phi is not None and ozaki_worthwhile(L, K):
+                self._buf[L]["oz"] = _native.OzakiOperand(L, self.M, 128, dev)
         return self._buf[L]
 
     @property
@@ -158,7 +169,9 @@ class FrameEngine:
         """areas, cells, normalizers, products (one per separable part or one GEMM),
         iterate, paste"""
         factors = self.dictionary.device_factors(self.device)
-        return 5 + (len(factors) if factors else 1)
+        if factors:
+            return 5 + len(factors)
+        return 5 + (2 if any("oz" in b for b in self._buf.values()) else 1)
 
     def run(self, frame, grid, corners, out=None) -> BatchResult:
         """Conceal one frame: ``frame`` (H, W) float64, ``grid`` (H/tile, W/tile)
@@ -181,6 +194,8 @@ class FrameEngine:
         if factors:  # separable parts: rows X cols^T per part (csrc/separable.cu)
             for rows, cols, row0 in factors:
                 _native.sep_products(rows, cols, b["X"], self.A, self.A, b["R0"], row0)
+        elif self._oz_phi is not None and "oz" in b:
+            _native.ozaki_gemm(b["oz"].split(b["X"]), self._oz_phi, b["R0"])
         else:
             _native.gemm_nt(b["X"][:, : self.M], self.phi[:, : self.M], b["R0"])
         _native.iterate(self.G0, b["D"], b["R0"], K, cfg.iterations, cfg.gamma, b["sel"], b["proj"],

@@ -1,0 +1,304 @@
+// FP64 contractions on the 5th-generation tensor cores: the Ozaki scheme with
+// tcgen05 INT8 MMAs (kind::i8, int32 accumulators in TMEM).
+//
+// FP64 has no tcgen05 kind on sm_100a; DMMA (csrc/dgemm.cu) tops out near
+// 37 TFLOP/s. Splitting every FP64 row into s signed 7-bit digits,
+//   x[r, k] = 2^e_r * sum_{i=1..s} a_i[r, k] 2^{-7i}  (+ |residual| < 2^{e_r - 7s}),
+// turns C = X Y^T into integer products of digit matrices:
+//   C[r, c] ~= 2^{e_r + f_c} * sum_{d=2..s+1} 2^{-7d} * sum_{i+j=d} (A_i B_j^T)[r, c],
+// keeping the pairs i + j <= s + 1 (the dropped pairs lie below 2^{-7(s+2)} of
+// the leading term). Every A_i B_j^T is an exact int8 x int8 -> int32
+// contraction (|sum| <= Kd * 127^2 * s < 2^31 for Kd <= 16384), pairs of one
+// diagonal d share one TMEM accumulator, and the epilogue combines the s
+// diagonals in FP64 from the smallest weight up and applies the row scales.
+//
+// Used for the dense initial products R0 = (F o W) Phi^T over the support
+// (initial_scalar_products, fast.py:145-157): the digit planes of Phi are cut
+// once per plan, those of the weighted signals once per batch.
+//
+// Kernel: one CTA per 128 x 64 output tile, 256 threads. Digit planes are
+// stored in global memory already in the K-major, no-swizzle UMMA layout
+// (8-row x 16-byte core matrices, grouped per 64-byte K block), so a tile's
+// slab of one plane is one contiguous run: a stage (s planes of a 128 x 64-byte
+// A slab and a 64 x 64-byte B slab) arrives by 2s TMA bulk copies issued by one
+// thread, completing on the stage's full mbarrier. Another thread issues the
+// s(s+1)/2 pairs x 2 K-steps of tcgen05.mma per stage and commits to the
+// stage's empty mbarrier. TMEM holds s accumulators of 64 columns; all eight
+// warps run the epilogue.
+
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace fase {
+namespace {
+
+constexpr int OZ_BM = 128, OZ_BN = 64, OZ_BK = 64;  // rows, cols, K bytes per stage
+constexpr int OZ_THREADS = 256;
+constexpr int OZ_STAGES = 2;  // (32-byte stages x 4 measured 5% slower)
+constexpr int OZ_RG = 8 * OZ_BK;  // bytes of one 8-row group of a slab (UMMA SBO)
+constexpr int OZ_MAX_SLICES = 8;
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFF) |
+         (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // version 1
+}
+
+// kind::i8: int32 accumulate (c_format 2), signed A / B (format 1), K-major,
+// N = OZ_BN (bits 17-22, >> 3), M = OZ_BM (bits 24-28, >> 4)
+constexpr uint32_t kOzIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
+                              (static_cast<uint32_t>(OZ_BN >> 3) << 17) |
+                              (static_cast<uint32_t>(OZ_BM >> 4) << 24);
+
+// Byte offset of (row r, K byte k) inside one digit plane, in the UMMA-ready
+// tiled layout: [K block of OZ_BK B][8-row group][16-byte K chunk][row % 8][16 B].
+// A tile's slab (all rows of the tile for one K block) is then one contiguous
+// run of bytes, fetched by a single 1-D TMA bulk copy.
+__device__ __forceinline__ int64_t plane_offset(int r, int64_t k, int64_t rows_pad) {
+  return (k / OZ_BK) * (rows_pad * OZ_BK) + static_cast<int64_t>(r >> 3) * OZ_RG +
+         ((k >> 4) % (OZ_BK / 16)) * 128 + (r & 7) * 16 + (k & 15);
+}
+
+// Digit planes of one FP64 row per warp: e = smallest integer with
+// max|x| < 2^e, then s truncated base-2^7 digits of x * 2^-e (each step exact).
+__global__ void ozaki_split_kernel(const double* __restrict__ x, int64_t ldx, int rows, int kd,
+                                   int s, int8_t* __restrict__ planes, int64_t kp, int64_t rows_pad,
+                                   int64_t plane_stride, int32_t* __restrict__ exps) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += gridDim.x * wpb) {
+    const double* xr = x + static_cast<int64_t>(r) * ldx;
+    double m = 0.0;
+    for (int k = lane; k < kd; k += 32) m = fmax(m, fabs(xr[k]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const int e = m > 0.0 ? ilogb(m) + 1 : 0;
+    if (lane == 0) exps[r] = e;
+    for (int k = lane; k < kp; k += 32) {
+      double y = k < kd ? scalbn(xr[k], -e) : 0.0;  // |y| < 1, exact
+      const int64_t off = plane_offset(r, k, rows_pad);
+      for (int i = 0; i < s; ++i) {
+        y = y * 128.0;                    // exact
+        const double t = trunc(y);       // |t| <= 127
+        y -= t;                           // exact
+        planes[i * plane_stride + off] = static_cast<int8_t>(t);
+      }
+    }
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(
+    const int8_t* __restrict__ A, int64_t a_plane, const int32_t* __restrict__ ea,
+    const int8_t* __restrict__ B, int64_t b_plane, const int32_t* __restrict__ eb, int64_t kp,
+    int m_valid, int n_valid, int rows_a_pad, int rows_b_pad, double* __restrict__ C, int64_t ldc,
+    int group_m) {
+  constexpr int A_SLAB = OZ_BM * OZ_BK, B_SLAB = OZ_BN * OZ_BK;
+  constexpr int STAGE = S * (A_SLAB + B_SLAB);
+  constexpr int TMEM_COLS = 512;
+  static_assert(S * OZ_BN <= TMEM_COLS, "one 64-column accumulator per diagonal");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full_bar[OZ_STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[OZ_STAGES];
+  __shared__ __align__(8) uint64_t done_bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  // grouped raster: CTAs in flight cover group_m M-tiles x a band of N-tiles,
+  // so each A / B slab is read by a bounded number of concurrent CTAs
+  int tm, tn;
+  {
+    const int mt = (m_valid + OZ_BM - 1) / OZ_BM, nt = (n_valid + OZ_BN - 1) / OZ_BN;
+    const int pid = blockIdx.x;
+    const int per_group = group_m * nt;
+    const int first_m = (pid / per_group) * group_m;
+    const int gm = min(mt - first_m, group_m);
+    tm = first_m + (pid % per_group) % gm;
+    tn = (pid % per_group) / gm;
+  }
+  const int m0 = tm * OZ_BM, n0 = tn * OZ_BN;
+  const int nk = static_cast<int>(kp / OZ_BK);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(&tmem_base)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 32) {
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+    fence_mbar_init();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = tmem_base;
+  const uint32_t sbase = smem_u32(smem);
+
+  // warp-specialized pipeline: thread 0 streams slabs with TMA bulk copies
+  // (one per digit plane), thread 32 issues the MMAs; full / empty mbarriers
+  const int64_t a_kblock = static_cast<int64_t>(rows_a_pad) * OZ_BK;  // bytes per K block of a plane
+  const int64_t b_kblock = static_cast<int64_t>(rows_b_pad) * OZ_BK;
+  if (tid == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % OZ_STAGES;
+      mbar_wait(&empty_bar[st], ((kb / OZ_STAGES) & 1) ^ 1);
+      mbar_arrive_expect_tx(&full_bar[st], STAGE);
+      uint8_t* sa = smem + st * STAGE;
+      uint8_t* sb = sa + S * A_SLAB;
+#pragma unroll
+      for (int p = 0; p < S; ++p) {
+        tma_load_1d(sa + p * A_SLAB, A + p * a_plane + kb * a_kblock + static_cast<int64_t>(m0 >> 3) * OZ_RG,
+                    A_SLAB, &full_bar[st]);
+        tma_load_1d(sb + p * B_SLAB, B + p * b_plane + kb * b_kblock + static_cast<int64_t>(n0 >> 3) * OZ_RG,
+                    B_SLAB, &full_bar[st]);
+      }
+    }
+  } else if (tid == 32) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % OZ_STAGES;
+      mbar_wait(&full_bar[st], (kb / OZ_STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      const uint32_t sa = sbase + st * STAGE, sb = sa + S * A_SLAB;
+#pragma unroll
+      for (int ks = 0; ks < OZ_BK / 32; ++ks) {  // K = 32 per MMA
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+#pragma unroll
+          for (int j = 0; j < S - i; ++j) {   // digits i+1, j+1: diagonal index i + j
+            const uint64_t ad = umma_desc(sa + i * A_SLAB + ks * 256, 128, OZ_RG);
+            const uint64_t bd = umma_desc(sb + j * B_SLAB + ks * 256, 128, OZ_RG);
+            const uint32_t acc = (kb > 0 || ks > 0 || i > 0) ? 1u : 0u;  // first pair of a diagonal inits it
+            const uint32_t dst = tmem + static_cast<uint32_t>((i + j) * OZ_BN);
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dst),
+                "l"(ad), "l"(bd), "r"(kOzIdesc), "r"(acc));
+          }
+        }
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+              smem_u32(&empty_bar[st])));
+    }
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_u32(&done_bar)));
+  }
+  __syncwarp();
+  mbar_wait(&done_bar, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+
+  // epilogue: warp w reads lanes 32(w%4).. (tile rows) and columns half (w/4)
+  const int row = m0 + (warp & 3) * 32 + (tid & 31);
+  const int cbase = (warp >> 2) * (OZ_BN / 2);
+  const int er = row < m_valid ? ea[row] : 0;
+  for (int c0 = 0; c0 < OZ_BN / 2; c0 += 8) {
+    double sum[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sum[j] = 0.0;
+#pragma unroll
+    for (int d = S - 1; d >= 0; --d) {  // smallest weight first
+      uint32_t v[8];
+      const uint32_t taddr = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) +
+                             static_cast<uint32_t>(d * OZ_BN + cbase + c0);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+      const double w = scalbn(1.0, -7 * (d + 2));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sum[j] = fma(static_cast<double>(static_cast<int32_t>(v[j])), w, sum[j]);
+    }
+    if (row < m_valid) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int col = n0 + cbase + c0 + j;
+        if (col < n_valid) C[static_cast<int64_t>(row) * ldc + col] = scalbn(sum[j], er + eb[col]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+}
+
+}  // namespace
+}  // namespace fase
+
+using namespace fase;
+
+extern "C" int fase_ozaki_split(const double* x, int64_t ldx, int rows, int kd, int slices,
+                                int8_t* planes, int64_t kp, int rows_pad, int32_t* exps,
+                                void* stream) {
+  if (rows < 0 || kd < 1 || slices < 1 || slices > OZ_MAX_SLICES || kp < kd || kp % OZ_BK ||
+      ldx < kd || rows_pad < rows || rows_pad % 8) {
+    set_error("fase_ozaki_split: bad sizes (rows=%d kd=%d slices=%d kp=%lld rows_pad=%d)", rows,
+              kd, slices, static_cast<long long>(kp), rows_pad);
+    return FASE_ERR_SHAPE;
+  }
+  if (rows == 0) return FASE_OK;
+  if (!x || !planes || !exps) {
+    set_error("fase_ozaki_split: null pointer");
+    return FASE_ERR_SHAPE;
+  }
+  const int blocks = (rows + 7) / 8;
+  ozaki_split_kernel<<<blocks < 148 * 16 ? blocks : 148 * 16, 256, 0, as_stream(stream)>>>(
+      x, ldx, rows, kd, slices, planes, kp, rows_pad, static_cast<int64_t>(rows_pad) * kp, exps);
+  return check_launch("fase_ozaki_split");
+}
+
+extern "C" int fase_ozaki_gemm(const int8_t* a_planes, int a_rows_pad, const int32_t* ea,
+                               int m_rows, const int8_t* b_planes, int b_rows_pad,
+                               const int32_t* eb, int n_rows, int64_t kp, int slices, double* C,
+                               int64_t ldc, void* stream) {
+  if (m_rows < 0 || n_rows < 0 || kp < OZ_BK || kp % OZ_BK || slices < 1 ||
+      slices > OZ_MAX_SLICES || ldc < n_rows || kp > 16384) {
+    set_error("fase_ozaki_gemm: bad sizes (M=%d N=%d kp=%lld slices=%d)", m_rows, n_rows,
+              static_cast<long long>(kp), slices);
+    return FASE_ERR_SHAPE;
+  }
+  if (m_rows == 0 || n_rows == 0) return FASE_OK;
+  const int mt = (m_rows + OZ_BM - 1) / OZ_BM, nt = (n_rows + OZ_BN - 1) / OZ_BN;
+  if (!a_planes || !b_planes || !ea || !eb || !C || a_rows_pad < mt * OZ_BM ||
+      a_rows_pad % OZ_BM || b_rows_pad < nt * OZ_BN || b_rows_pad % OZ_BN ||
+      !aligned16(a_planes) || !aligned16(b_planes)) {
+    set_error("fase_ozaki_gemm: planes must hold rows padded to %d (A) / %d (B), 16-byte aligned",
+              OZ_BM, OZ_BN);
+    return FASE_ERR_SHAPE;
+  }
+  const int64_t a_plane = static_cast<int64_t>(a_rows_pad) * kp;
+  const int64_t b_plane = static_cast<int64_t>(b_rows_pad) * kp;
+  auto launch = [&](auto kern, int s) -> int {
+    const size_t smem = static_cast<size_t>(OZ_STAGES) * s * (OZ_BM + OZ_BN) * OZ_BK;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) {
+      set_error("fase_ozaki_gemm: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+      return FASE_ERR_CUDA;
+    }
+    const char* env = getenv("FASE_OZAKI_GROUP_M");
+    int group_m = env ? atoi(env) : 8;
+    if (group_m < 1) group_m = 1;
+    kern<<<nt * mt, OZ_THREADS, smem, as_stream(stream)>>>(a_planes, a_plane, ea, b_planes, b_plane,
+                                                            eb, kp, m_rows, n_rows, a_rows_pad,
+                                                            b_rows_pad, C, ldc, group_m);
+    return check_launch("fase_ozaki_gemm");
+  };
+  switch (slices) {
+    case 8: return launch(ozaki_gemm_kernel<8>, 8);
+    case 7: return launch(ozaki_gemm_kernel<7>, 7);
+    case 6: return launch(ozaki_gemm_kernel<6>, 6);
+    default:
+      set_error("fase_ozaki_gemm: %d digit planes not instantiated (6-8)", slices);
+      return FASE_ERR_UNSUPPORTED;
+  }
+}

@@ -276,6 +276,13 @@ def initial_products_into(dictionary: Dictionary, F, W, R0, ws, *, method: str =
     return "separable"
 
 
+def ozaki_worthwhile(rows: int, cols: int) -> bool:
+    """Dense FP64 products go to the tcgen05 Ozaki path when the output has
+    enough 128 x 64 tiles to fill the GPU (measured 2x DMMA at config-4 size;
+    small batches stay on DMMA, whose tiles fill the GPU sooner)."""
+    return rows >= 512 and cols >= 512 and ((rows + 127) // 128) * ((cols + 63) // 64) >= 4 * 148
+
+
 def _ranges(flags: np.ndarray):
     """[(lo, hi)] runs of True in a boolean vector."""
     f = np.concatenate([[False], np.asarray(flags, dtype=bool), [False]])
@@ -667,9 +674,10 @@ class ExtrapolationPlan:
         # and add exact zeros, so Phi's support columns are gathered once and
         # each run contracts over them (fase_weigh_gather + one DMMA GEMM).
         self._support = None
+        self._ozaki = None
         dense = (cplx and not cparts) or (not cplx and not factors)
         support = np.flatnonzero(w.ravel() != 0.0).astype(np.int32)
-        if dense and products in ("auto", "gemm", "support") and support.size < M:
+        if dense and products in ("auto", "gemm", "ozaki"):
             n_s = support.size
             phi_s = torch.zeros((self.phi.shape[0], n_s + (n_s & 1)), dtype=torch.float64,
                                 device=dev)
@@ -680,6 +688,13 @@ class ExtrapolationPlan:
                              torch.empty((self.B, n_s + (n_s & 1)), dtype=torch.float64,
                                          device=dev))
             n_prod = 2
+            # FP64 products on the tcgen05 tensor cores (Ozaki digit planes,
+            # csrc/ozaki.cu) for batches that fill the GPU; Phi's planes once here
+            if products == "ozaki" or (products == "auto" and ozaki_worthwhile(self.B, phi_s.shape[0])):
+                rows = phi_s.shape[0]
+                self._ozaki = (_native.OzakiOperand(self.B, n_s, 128, dev),
+                               _native.OzakiOperand(rows, n_s, 64, dev).split(phi_s))
+                n_prod = 3
         # (weigh +) products + iterate + synth
         self.launches_per_run = n_prod + 1 + (1 if self.n_lost else 0)
 
@@ -691,7 +706,12 @@ class ExtrapolationPlan:
                                          method=self.products)
         sidx, w_s, phi_s, X = self._support
         _native.weigh_gather(F, sidx, w_s, X)
-        _native.gemm_nt(X, phi_s, _real_view(self.R0) if self.complex else self.R0)
+        out = _real_view(self.R0) if self.complex else self.R0
+        if self._ozaki is not None:
+            a, b = self._ozaki
+            _native.ozaki_gemm(a.split(X), b, out)
+            return "ozaki-support"
+        _native.gemm_nt(X, phi_s, out)
         return "gemm-support"
 
     def _uncovered(self, cparts):

@@ -170,3 +170,74 @@ def test_plan_uses_separable_complex_products():
     assert plan.products_method == "separable"
     ref = fase_extrapolate_batch(sig, mask, d, plan.tables, cfg, device=DEV)
     assert torch.equal(plan.selected, ref.selected)
+
+
+# ----------------------------------------------------------------- tcgen05 Ozaki products
+
+
+@pytest.mark.parametrize("M,N,Kd,kind", [(300, 200, 131, "uniform"), (1000, 333, 777, "wide"),
+                                         (256, 128, 64, "zeros"), (130, 65, 4000, "signal")])
+def test_ozaki_gemm_matches_fp64(M, N, Kd, kind):
+    """tcgen05 INT8 digit-plane contraction == FP64 contraction to rounding:
+    error within 1e-15 of sum |x y| (the DMMA GEMM measures 1.7e-16 - 2.8e-16
+    on the same data; rows with a wide dynamic range lose low digits of their
+    small entries, so the bound is a few ulp, not one)."""
+    rng = np.random.default_rng(M * 7 + N)
+    if kind == "wide":
+        X = rng.standard_normal((M, Kd)) * 10.0 ** rng.integers(-3, 4, (M, 1))
+        Y = rng.standard_normal((N, Kd)) * 10.0 ** rng.integers(-3, 4, (1, Kd))
+    elif kind == "signal":
+        X = rng.uniform(0, 255, (M, Kd)) * 0.8 ** rng.uniform(0, 30, Kd)
+        Y = rng.standard_normal((N, Kd)) / 64
+    else:
+        X = rng.uniform(-1, 1, (M, Kd))
+        Y = rng.uniform(-1, 1, (N, Kd))
+    if kind == "zeros":
+        X[::3] = 0.0
+        Y[:, ::5] = 0.0
+    ld = Kd + (Kd & 1)
+    Xd = torch.zeros((M, ld), dtype=torch.float64, device=DEV)
+    Xd[:, :Kd] = torch.from_numpy(X)
+    Yd = torch.zeros((N, ld), dtype=torch.float64, device=DEV)
+    Yd[:, :Kd] = torch.from_numpy(Y)
+    a = _native.OzakiOperand(M, Kd, 128, DEV).split(Xd)
+    b = _native.OzakiOperand(N, Kd, 64, DEV).split(Yd)
+    C = torch.full((M, N + 3), 7.0, dtype=torch.float64, device=DEV)
+    _native.ozaki_gemm(a, b, C)
+    c = C.cpu().numpy()
+    assert np.all(c[:, N:] == 7.0)  # nothing written past the valid columns
+    XL, YL = X.astype(np.longdouble), Y.astype(np.longdouble)
+    rows = rng.integers(0, M, 60)
+    cols = rng.integers(0, N, 60)
+    ref = np.array([np.dot(XL[i], YL[j]) for i, j in zip(rows, cols)])
+    scale = np.array([np.dot(np.abs(XL[i]), np.abs(YL[j])) for i, j in zip(rows, cols)])
+    err = np.abs(c[rows, cols] - ref) / np.maximum(scale, 1e-300)
+    assert float(err.max()) < 1e-15
+    if kind == "zeros":
+        assert np.all(c[::3, :N] == 0.0)
+
+
+@pytest.mark.parametrize("spec", ["gauss:700:5", "bdft"])
+def test_plan_ozaki_products(spec):
+    """The plan's tcgen05 path (weigh-gather, digit split, INT8 MMAs) reproduces
+    the reference's initial products to 1e-13 and its selections."""
+    d = parse_dict_spec(spec, 16, 16)
+    mask = wl.central_loss_mask(16, 16, 6, 6)
+    cfg = ExtrapConfig(40, 0.5, 0.85)
+    sig = np.random.default_rng(9).uniform(0, 255, (150, 16, 16))
+    plan = ExtrapolationPlan(d, mask, 150, cfg, device=DEV, products="ozaki")
+    assert plan._ozaki is not None and plan.launches_per_run == 5
+    plan.run(torch.from_numpy(sig).to(DEV))
+    assert plan.products_method == "ozaki-support"
+    R0 = plan.R0[:, : len(d)].cpu().numpy()
+    ref_plan = ExtrapolationPlan(d, mask, 150, cfg, device=DEV, products="gemm")
+    ref_plan.run(torch.from_numpy(sig).to(DEV))
+    assert rel_dev(R0, ref_plan.R0[:, : len(d)].cpu().numpy()) < 1e-13
+    for b in (0, 77, 149):
+        ref = orc.extrapolate_block(sig[b], mask, d.values, 0.5, 40, 0.85, record=True)
+        assert rel_dev(R0[b], ref["r0"] if not d.is_real else ref["r0"].real) < 1e-13
+        from parity import compare_selection, metric_fn
+
+        v = compare_selection(plan.selected[b].cpu().numpy(), ref["selected"],
+                              metric_fn(ref["r0"], ref["d"], ref["log"]))
+        assert v.ok
