@@ -303,20 +303,17 @@ def ozaki_roofline(plan, flops_fp64, seconds, fp64_peak, fp64_src):
     s = a.slices
     pairs = s * (s + 1) // 2
     ops = 2.0 * pairs * a.rows * b.rows * a.kp
-    i8_peak, src = 2 * 1649.9, "2 x measured BF16 dense burst (MEASURED_PEAKS.json)"
-    p = ROOT / "MEASURED_PEAKS.json"
-    if p.exists():
-        try:
-            i8_peak = 2 * float(json.loads(p.read_text())["bf16_tflops"])
-        except (KeyError, ValueError):
-            pass
+    # no measured INT8 figure exists for this pool; the nominal dense INT8 / FP8
+    # rate (B200_PROFILING.md: 4.5 PFLOP/s dense fp8, int8 at the same rate)
+    i8_peak, src = 4500.0, "nominal B200 dense INT8 (= FP8) tensor rate, B200_PROFILING.md"
     return {"bound": "tensor", "kernel": "ozaki_gemm_kernel (tcgen05.mma kind::i8, "
             f"{s} digit planes, {pairs} pairs) over the support samples",
             "achieved": ops / seconds / 1e12, "peak": i8_peak, "unit": "TOPS (int8)",
             "frac": ops / seconds / 1e12 / i8_peak, "ms_per_launch": seconds * 1e3,
             "peak_source": src, "fp64_equivalent_tflops": flops_fp64 / seconds / 1e12,
             "fp64_peak_tflops": fp64_peak, "fp64_peak_source": fp64_src,
-            "note": "ms includes the weigh-gather and digit-split kernels of the batch"}
+            "note": "ms includes the digit-split kernel (support gather and weights fused) "
+                    "of the batch"}
 
 
 def run_gpu(args):
@@ -472,10 +469,19 @@ def run_gpu(args):
         if plan._support is not None:  # contraction over the support samples only
             flops_init = (4.0 if cplx else 2.0) * K * int(plan._support[0].shape[0]) * B
         factors = d.device_factors(dev) if plan.products in ("auto", "separable") else None
+        mr, nc = w.area
         if factors:  # executed flops of the separable form
-            mr, nc = w.area
             flops_sep = sum(2.0 * B * (r.shape[0] * mr * nc + r.shape[0] * nc * c.shape[0])
                             for r, c, _ in factors)
+        elif cplx and plan.products_method.startswith("separable"):
+            # complex transforms: [Cn; Sn] X^T (2 Lc x Mr x Nc), then 2 Lr x Lc x 2 Mr;
+            # rows outside the separable ranges (if any) go through the DMMA GEMM
+            cparts = d.device_cfactors(dev)
+            flops_sep = sum(2.0 * B * (2 * c.shape[0] * mr * nc + 4 * r.shape[0] * c.shape[0] * mr)
+                            for r, _, c, _, _ in cparts)
+            covered = sum(r.shape[0] * c.shape[0] for r, _, c, _, _ in cparts)
+            flops_sep += 4.0 * (K - covered) * M * B
+            factors = cparts
         step_ms = dev_total_s / args.steps * 1e3
         line = {
             "metric": "extrapolated blocks/s",
@@ -516,8 +522,8 @@ def run_gpu(args):
                                "unit": "TFLOP/s", "frac": flops_init / init_s / 1e12 / fp64,
                                "ms_per_launch": init_s * 1e3, "peak_source": fsrc}
                               if not factors else
-                              {"bound": "fp64", "kernel": "weigh_kernel + sep_products_kernel "
-                               "(separable transforms, FP64 FMA)",
+                              {"bound": "fp64", "kernel": "weigh_kernel + sep_products"
+                               + ("_complex" if cplx else "") + "_kernel (separable transforms, FP64 FMA)",
                                "achieved": flops_sep / init_s / 1e12, "peak": fp64,
                                "unit": "TFLOP/s", "frac": flops_sep / init_s / 1e12 / fp64,
                                "ms_per_launch": init_s * 1e3, "peak_source": fsrc,

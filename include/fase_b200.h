@@ -320,10 +320,13 @@ FASE_API int fase_fft_gram(const double* spec, int M, int N, const int32_t* mu, 
 /*
  * FP64 contractions on the tcgen05 tensor cores (Ozaki scheme, kind::i8):
  *
- * fase_ozaki_split: digit planes of `rows` FP64 rows of length kd:
- *   e[r] = min e with max_k |x[r,k]| < 2^e;
- *   x[r,k] = 2^e[r] * sum_{i<slices} digit_i[r,k] * 2^{-7(i+1)} + residual
- * (signed 7-bit digits, truncated; kd zero-padded to kp, a multiple of 64).
+ * fase_ozaki_split: digit planes of `rows` FP64 rows of length kd, with
+ * v[r,k] = x[r*ldx + (idx ? idx[k] : k)] * (w ? w[k] : 1) (one rounding: the
+ * support-restricted weighted operand of fase_weigh_gather, or x itself):
+ *   e[r] = min e with max_k |v[r,k]| < 2^e;
+ *   v[r,k] = 2^e[r] * sum_{i<slices} digit_i[r,k] * 2^{-7(i+1)} + residual
+ * (signed 7-bit digits, truncated; kd zero-padded to kp, a multiple of 64;
+ * slices 6..8).
  * Plane i occupies rows_pad * kp bytes at planes + i * rows_pad * kp, stored
  * in the UMMA-ready tiled order [k / 64][r / 8][(k / 16) % 4][r % 8][k % 16].
  *
@@ -334,9 +337,9 @@ FASE_API int fase_fft_gram(const double* spec, int M, int N, const int32_t* mu, 
  * 2^(e_X[r] + e_Y[c]). With 8 planes the result matches an FP64 contraction
  * to rounding level (initial_scalar_products, fast.py:145-157, on the support).
  */
-FASE_API int fase_ozaki_split(const double* x, int64_t ldx, int rows, int kd, int slices,
-                              int8_t* planes, int64_t kp, int rows_pad, int32_t* exps,
-                              void* stream);
+FASE_API int fase_ozaki_split(const double* x, int64_t ldx, const int32_t* idx, const double* w,
+                              int rows, int kd, int slices, int8_t* planes, int64_t kp,
+                              int rows_pad, int32_t* exps, void* stream);
 FASE_API int fase_ozaki_gemm(const int8_t* a_planes, int a_rows_pad, const int32_t* ea,
                              int m_rows, const int8_t* b_planes, int b_rows_pad,
                              const int32_t* eb, int n_rows, int64_t kp, int slices, double* C,

@@ -108,7 +108,7 @@ def load():
                                       _vp, _i64, _i64, _vp],
         "fase_fft_gram": [_vp, _i32, _i32, _vp, _vp, _i32, _vp, _i64, _vp],
         "fase_weigh_gather": [_vp, _i64, _vp, _vp, _i32, _i32, _vp, _i64, _vp],
-        "fase_ozaki_split": [_vp, _i64, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp],
+        "fase_ozaki_split": [_vp, _i64, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp],
         "fase_ozaki_gemm": [_vp, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i64, _i32, _vp, _i64,
                             _vp],
         "fase_synth_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
@@ -516,14 +516,20 @@ class OzakiOperand:
         self.planes = torch.zeros((slices, self.rows_pad, self.kp), dtype=torch.int8, device=device)
         self.exps = torch.zeros(self.rows_pad, dtype=torch.int32, device=device)
 
-    def split(self, x) -> "OzakiOperand":
+    def split(self, x, idx=None, w=None) -> "OzakiOperand":
+        """Planes of x (rows x kd), or of x[:, idx] * w when a support gather
+        and weights are given (idx int32 (kd,), w float64 (kd,))."""
         import torch
 
         lib = load()
         _require(x, "x", torch.float64, 2)
-        _check(lib.fase_ozaki_split(_ptr(x), _ld(x), self.rows, self.kd, self.slices,
-                                    _ptr(self.planes), self.kp, self.rows_pad, _ptr(self.exps),
-                                    _stream(x)))
+        if idx is not None:
+            _require(idx, "idx", torch.int32, 1)
+        if w is not None:
+            _require(w, "w", torch.float64, 1)
+        _check(lib.fase_ozaki_split(_ptr(x), _ld(x), _ptr(idx), _ptr(w), self.rows, self.kd,
+                                    self.slices, _ptr(self.planes), self.kp, self.rows_pad,
+                                    _ptr(self.exps), _stream(x)))
         return self
 
 

@@ -22,8 +22,11 @@
 // slab of one plane is one contiguous run: a stage (s planes of a 128 x 64-byte
 // A slab and a 64 x 64-byte B slab) arrives by 2s TMA bulk copies issued by one
 // thread, completing on the stage's full mbarrier. Another thread issues the
-// s(s+1)/2 pairs x 2 K-steps of tcgen05.mma per stage and commits to the
-// stage's empty mbarrier. TMEM holds s accumulators of 64 columns; all eight
+// MMAs -- digit i of A against the stacked digits 0..s-1-i of B, up to N = 256
+// per instruction, so each A digit is read from shared memory once or twice per
+// K step instead of s - i times (the smem operand bandwidth, not the tensor
+// pipe, bounded the one-pair-per-MMA form) -- and commits to the stage's empty
+// mbarrier. TMEM holds s accumulators of 64 columns; all eight
 // warps run the epilogue.
 
 #include <cstdlib>
@@ -46,10 +49,9 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint3
 }
 
 // kind::i8: int32 accumulate (c_format 2), signed A / B (format 1), K-major,
-// N = OZ_BN (bits 17-22, >> 3), M = OZ_BM (bits 24-28, >> 4)
-constexpr uint32_t kOzIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
-                              (static_cast<uint32_t>(OZ_BN >> 3) << 17) |
-                              (static_cast<uint32_t>(OZ_BM >> 4) << 24);
+// M = OZ_BM (bits 24-28, >> 4); N (bits 17-22, >> 3) is set per instruction
+constexpr uint32_t kOzIdescBase = (2u << 4) | (1u << 7) | (1u << 10) |
+                                  (static_cast<uint32_t>(OZ_BM >> 4) << 24);
 
 // Byte offset of (row r, K byte k) inside one digit plane, in the UMMA-ready
 // tiled layout: [K block of OZ_BK B][8-row group][16-byte K chunk][row % 8][16 B].
@@ -60,31 +62,69 @@ __device__ __forceinline__ int64_t plane_offset(int r, int64_t k, int64_t rows_p
          ((k >> 4) % (OZ_BK / 16)) * 128 + (r & 7) * 16 + (k & 15);
 }
 
-// Digit planes of one FP64 row per warp: e = smallest integer with
-// max|x| < 2^e, then s truncated base-2^7 digits of x * 2^-e (each step exact).
-__global__ void ozaki_split_kernel(const double* __restrict__ x, int64_t ldx, int rows, int kd,
-                                   int s, int8_t* __restrict__ planes, int64_t kp, int64_t rows_pad,
-                                   int64_t plane_stride, int32_t* __restrict__ exps) {
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
-  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += gridDim.x * wpb) {
+// Digit planes of one FP64 row per CTA: v[k] = x[r, idx[k]] * w[k] (idx / w
+// optional: the weighted operand restricted to the support, rounded once like
+// fase_weigh_gather) is staged in shared memory with coalesced loads; e is the
+// smallest integer with max|v| < 2^e; then each thread cuts 16 consecutive k
+// into s truncated base-2^7 digits of v * 2^-e (each step exact) and stores one
+// 16-byte chunk per plane.
+constexpr int OZ_SPLIT_THREADS = 256;
+
+template <int S>
+__global__ void __launch_bounds__(OZ_SPLIT_THREADS) ozaki_split_kernel(
+    const double* __restrict__ x, int64_t ldx, const int32_t* __restrict__ idx,
+    const double* __restrict__ w, int rows, int kd, int8_t* __restrict__ planes, int64_t kp,
+    int64_t rows_pad, int64_t plane_stride, int32_t* __restrict__ exps) {
+  extern __shared__ double s_v[];  // kp + kp/16 (one pad per 16 against bank conflicts)
+  __shared__ double s_max[OZ_SPLIT_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int chunks = static_cast<int>(kp >> 4);
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     const double* xr = x + static_cast<int64_t>(r) * ldx;
     double m = 0.0;
-    for (int k = lane; k < kd; k += 32) m = fmax(m, fabs(xr[k]));
+    for (int k = tid; k < kp; k += OZ_SPLIT_THREADS) {
+      double v = 0.0;
+      if (k < kd) {
+        v = __ldg(xr + (idx ? __ldg(idx + k) : k));
+        if (w) v = mul_rn(v, __ldg(w + k));
+      }
+      s_v[k + (k >> 4)] = v;
+      m = fmax(m, fabs(v));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_max[warp] = m;
+    __syncthreads();
+    m = s_max[0];
+#pragma unroll
+    for (int i = 1; i < OZ_SPLIT_THREADS / 32; ++i) m = fmax(m, s_max[i]);
     const int e = m > 0.0 ? ilogb(m) + 1 : 0;
-    if (lane == 0) exps[r] = e;
-    for (int k = lane; k < kp; k += 32) {
-      double y = k < kd ? scalbn(xr[k], -e) : 0.0;  // |y| < 1, exact
-      const int64_t off = plane_offset(r, k, rows_pad);
-      for (int i = 0; i < s; ++i) {
-        y = y * 128.0;                    // exact
-        const double t = trunc(y);       // |t| <= 127
-        y -= t;                           // exact
-        planes[i * plane_stride + off] = static_cast<int8_t>(t);
+    if (tid == 0) exps[r] = e;
+    for (int c = tid; c < chunks; c += OZ_SPLIT_THREADS) {
+      uint32_t packed[S][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int i = 0; i < S; ++i) packed[i][q] = 0u;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          double y = scalbn(s_v[17 * c + 4 * q + b], -e);  // |y| < 1, exact
+#pragma unroll
+          for (int i = 0; i < S; ++i) {
+            y = y * 128.0;               // exact
+            const double t = trunc(y);  // |t| <= 127
+            y -= t;                      // exact
+            packed[i][q] |= (static_cast<uint32_t>(static_cast<int>(t)) & 0xffu) << (8 * b);
+          }
+        }
       }
+      const int64_t off = plane_offset(r, 16 * static_cast<int64_t>(c), rows_pad);
+#pragma unroll
+      for (int i = 0; i < S; ++i)
+        *reinterpret_cast<uint4*>(planes + i * plane_stride + off) =
+            make_uint4(packed[i][0], packed[i][1], packed[i][2], packed[i][3]);
     }
+    __syncthreads();  // s_v / s_max reused by the next row
   }
 }
 
@@ -168,16 +208,22 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(
       for (int ks = 0; ks < OZ_BK / 32; ++ks) {  // K = 32 per MMA
 #pragma unroll
         for (int i = 0; i < S; ++i) {
+          // digit i of A against digits j = 0 .. S-1-i of B in one wide MMA per
+          // group of up to 4 planes: the B planes sit back to back in shared
+          // memory (a uniform 64n-row operand) and their diagonals i + j are
+          // consecutive 64-column TMEM blocks, so A is read once per group
 #pragma unroll
-          for (int j = 0; j < S - i; ++j) {   // digits i+1, j+1: diagonal index i + j
+          for (int jb = 0; jb < S - i; jb += 4) {
+            const int nj = (S - i - jb) < 4 ? (S - i - jb) : 4;
             const uint64_t ad = umma_desc(sa + i * A_SLAB + ks * 256, 128, OZ_RG);
-            const uint64_t bd = umma_desc(sb + j * B_SLAB + ks * 256, 128, OZ_RG);
-            const uint32_t acc = (kb > 0 || ks > 0 || i > 0) ? 1u : 0u;  // first pair of a diagonal inits it
-            const uint32_t dst = tmem + static_cast<uint32_t>((i + j) * OZ_BN);
+            const uint64_t bd = umma_desc(sb + jb * B_SLAB + ks * 256, 128, OZ_RG);
+            const uint32_t idesc = kOzIdescBase | (static_cast<uint32_t>((nj * OZ_BN) >> 3) << 17);
+            const uint32_t acc = (kb > 0 || ks > 0 || i > 0) ? 1u : 0u;  // digit 0 of A inits every diagonal
+            const uint32_t dst = tmem + static_cast<uint32_t>((i + jb) * OZ_BN);
             asm volatile(
                 "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                 "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dst),
-                "l"(ad), "l"(bd), "r"(kOzIdesc), "r"(acc));
+                "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
           }
         }
       }
@@ -236,23 +282,37 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(
 
 using namespace fase;
 
-extern "C" int fase_ozaki_split(const double* x, int64_t ldx, int rows, int kd, int slices,
-                                int8_t* planes, int64_t kp, int rows_pad, int32_t* exps,
-                                void* stream) {
-  if (rows < 0 || kd < 1 || slices < 1 || slices > OZ_MAX_SLICES || kp < kd || kp % OZ_BK ||
-      ldx < kd || rows_pad < rows || rows_pad % 8) {
+extern "C" int fase_ozaki_split(const double* x, int64_t ldx, const int32_t* idx, const double* w,
+                                int rows, int kd, int slices, int8_t* planes, int64_t kp,
+                                int rows_pad, int32_t* exps, void* stream) {
+  if (rows < 0 || kd < 1 || slices < 6 || slices > OZ_MAX_SLICES || kp < kd || kp % OZ_BK || kp > 16384 ||
+      (!idx && ldx < kd) || rows_pad < rows || rows_pad % 8) {
     set_error("fase_ozaki_split: bad sizes (rows=%d kd=%d slices=%d kp=%lld rows_pad=%d)", rows,
               kd, slices, static_cast<long long>(kp), rows_pad);
     return FASE_ERR_SHAPE;
   }
   if (rows == 0) return FASE_OK;
-  if (!x || !planes || !exps) {
-    set_error("fase_ozaki_split: null pointer");
+  if (!x || !planes || !exps || !aligned16(planes)) {
+    set_error("fase_ozaki_split: null or misaligned pointer");
     return FASE_ERR_SHAPE;
   }
-  const int blocks = (rows + 7) / 8;
-  ozaki_split_kernel<<<blocks < 148 * 16 ? blocks : 148 * 16, 256, 0, as_stream(stream)>>>(
-      x, ldx, rows, kd, slices, planes, kp, rows_pad, static_cast<int64_t>(rows_pad) * kp, exps);
+  const dim3 grid(rows < 148 * 8 ? rows : 148 * 8);
+  const int64_t stride = static_cast<int64_t>(rows_pad) * kp;
+  const size_t smem = sizeof(double) * static_cast<size_t>(kp + kp / 16);
+  auto run = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<grid, OZ_SPLIT_THREADS, smem, as_stream(stream)>>>(x, ldx, idx, w, rows, kd, planes,
+                                                               kp, rows_pad, stride, exps);
+    return cudaSuccess;
+  };
+  cudaError_t e = slices == 8 ? run(ozaki_split_kernel<8>)
+                              : (slices == 7 ? run(ozaki_split_kernel<7>) : run(ozaki_split_kernel<6>));
+  if (e != cudaSuccess) {
+    set_error("fase_ozaki_split: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return FASE_ERR_CUDA;
+  }
   return check_launch("fase_ozaki_split");
 }
 
@@ -261,7 +321,7 @@ extern "C" int fase_ozaki_gemm(const int8_t* a_planes, int a_rows_pad, const int
                                const int32_t* eb, int n_rows, int64_t kp, int slices, double* C,
                                int64_t ldc, void* stream) {
   if (m_rows < 0 || n_rows < 0 || kp < OZ_BK || kp % OZ_BK || slices < 1 ||
-      slices > OZ_MAX_SLICES || ldc < n_rows || kp > 16384) {
+      slices > OZ_MAX_SLICES || ldc < n_rows || kp > 16384) {  // int32 headroom, split smem
     set_error("fase_ozaki_gemm: bad sizes (M=%d N=%d kp=%lld slices=%d)", m_rows, n_rows,
               static_cast<long long>(kp), slices);
     return FASE_ERR_SHAPE;

@@ -694,7 +694,7 @@ class ExtrapolationPlan:
                 rows = phi_s.shape[0]
                 self._ozaki = (_native.OzakiOperand(self.B, n_s, 128, dev),
                                _native.OzakiOperand(rows, n_s, 64, dev).split(phi_s))
-                n_prod = 3
+                n_prod = 2
         # (weigh +) products + iterate + synth
         self.launches_per_run = n_prod + 1 + (1 if self.n_lost else 0)
 
@@ -705,12 +705,12 @@ class ExtrapolationPlan:
             return initial_products_into(self.dictionary, F, self.W, self.R0, self.ws,
                                          method=self.products)
         sidx, w_s, phi_s, X = self._support
-        _native.weigh_gather(F, sidx, w_s, X)
         out = _real_view(self.R0) if self.complex else self.R0
-        if self._ozaki is not None:
+        if self._ozaki is not None:  # gather, weigh and split in one pass
             a, b = self._ozaki
-            _native.ozaki_gemm(a.split(X), b, out)
+            _native.ozaki_gemm(a.split(F, sidx, w_s), b, out)
             return "ozaki-support"
+        _native.weigh_gather(F, sidx, w_s, X)
         _native.gemm_nt(X, phi_s, out)
         return "gemm-support"
 

@@ -226,7 +226,7 @@ def test_plan_ozaki_products(spec):
     cfg = ExtrapConfig(40, 0.5, 0.85)
     sig = np.random.default_rng(9).uniform(0, 255, (150, 16, 16))
     plan = ExtrapolationPlan(d, mask, 150, cfg, device=DEV, products="ozaki")
-    assert plan._ozaki is not None and plan.launches_per_run == 5
+    assert plan._ozaki is not None and plan.launches_per_run == 4
     plan.run(torch.from_numpy(sig).to(DEV))
     assert plan.products_method == "ozaki-support"
     R0 = plan.R0[:, : len(d)].cpu().numpy()
