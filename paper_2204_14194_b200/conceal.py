@@ -275,7 +275,7 @@ def conceal_frame(image, lost_mask, *, dictionary: Dictionary | None = None,
     a = block + 2 * support
     if dictionary is None:
         dictionary = parse_dict_spec(dict_spec, a, a)
-    grid = tile_grid(lost, block)
+    grid = tile_grid(lost, block) if dictionary.is_real else None  # FrameEngine: real sets
     damaged = img.copy()
     damaged[lost] = 0.0
     if grid is not None:
@@ -295,9 +295,9 @@ def conceal_frame(image, lost_mask, *, dictionary: Dictionary | None = None,
             tables = ChunkedTables(dictionary, plan.masks, config.rho_hat, dev)
             res = fase_extrapolate_batch(plan.signals, plan.masks, dictionary, tables, config,
                                          patch=False, device=dev)
-            _native.synth_paste(dictionary.device_matrix(dev), res.selected, res.coefficients,
-                                config.iterations, plan.idx, out.view(-1), idx_ptr=plan.ptr,
-                                dst=plan.dst)
+            synth = _native.synth_paste if dictionary.is_real else _native.synth_paste_complex
+            synth(dictionary.device_matrix(dev), res.selected, res.coefficients,
+                  config.iterations, plan.idx, out.view(-1), idx_ptr=plan.ptr, dst=plan.dst)
     torch.cuda.current_stream(dev).synchronize()
     report = {
         "schema": REPORT_SCHEMA,

@@ -136,3 +136,32 @@ def test_conceal_image_tables_fft_and_edges():
         conceal_image(img, lost, block=(0, 8), device=DEV)
     with pytest.raises(MaskError):  # an area with no support left
         conceal_image(img, np.ones((16, 16), bool), block=(8, 8), support=0, device=DEV)
+
+
+def test_conceal_frame_complex_dictionary():
+    """conceal_frame (fixed areas) with the default complex dictionary takes the
+    per-block path; every lost pixel matches the oracle's block result."""
+    from paper_2204_14194_b200 import conceal_frame
+    from paper_2204_14194_b200 import workloads as wl
+
+    rng = np.random.default_rng(21)
+    yy, xx = np.mgrid[0:48, 0:56]
+    img = np.clip(120 + 50 * np.sin(0.21 * yy + 0.13 * xx) + rng.normal(0, 3, (48, 56)), 0, 255)
+    lost = np.zeros((48, 56), dtype=bool)
+    for r, c in [(8, 8), (0, 48), (24, 16), (40, 0), (16, 24)]:
+        lost[r:r + 8, c:c + 8] = True
+    cfg = ExtrapConfig(30, 0.5, 0.8)
+    out, rep = conceal_frame(img, lost, dict_spec="dft", config=cfg, block=8, support=4, device=DEV)
+    out = out.cpu().numpy()
+    damaged = img.copy()
+    damaged[lost] = 0.0
+    corners = np.array(sorted({(r // 8 * 8, c // 8 * 8) for r, c in zip(*np.nonzero(lost))}))
+    signals, masks = wl.frame_areas(damaged, lost, corners, 8, 4)
+    vals = parse_dict_spec("dft", 16, 16).values
+    for i, (r0, c0) in enumerate(corners):
+        ref = orc.extrapolate_block(signals[i], masks[i], vals, 0.5, 30, 0.8)
+        tile = ref["patched"][4:12, 4:12]
+        got = out[r0:r0 + 8, c0:c0 + 8]
+        sel_lost = lost[r0:r0 + 8, c0:c0 + 8]
+        assert np.abs(got[sel_lost] - tile[sel_lost]).max() <= COEF_REL * 255
+    assert np.array_equal(out[~lost], img[~lost])
