@@ -242,6 +242,15 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.proc is not None:
+            # a region shorter than the 20 ms sampling period may hold no sample:
+            # then wait (<= 0.2 s) for the first one after it, flagged as such
+            self.region_lines = len(self.path.read_text().splitlines())
+            t0 = time.time()
+            while (self.region_lines <= getattr(self, "skip", 0) and time.time() - t0 < 0.2
+                   and self.proc.poll() is None):
+                time.sleep(0.005)
+                if len(self.path.read_text().splitlines()) > self.region_lines:
+                    break
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -253,7 +262,11 @@ class ClockSampler:
         if self.proc is None or not self.path.exists():
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm, smax, reasons = [], None, set()
-        for line in self.path.read_text().splitlines()[getattr(self, "skip", 0):]:
+        lines = self.path.read_text().splitlines()
+        skip = getattr(self, "skip", 0)
+        end = getattr(self, "region_lines", len(lines))
+        in_region = end > skip
+        for line in (lines[skip:end] if in_region else lines[skip:skip + 1]):
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 3:
                 continue
@@ -266,8 +279,11 @@ class ClockSampler:
             for bit, name in REASONS.items():
                 if mask & bit:
                     reasons.add(name)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if not in_region:
+            out["note"] = "timed region shorter than the 20 ms sampling period: first sample after it"
+        return out
 
 
 def measured_peaks():
@@ -285,12 +301,14 @@ def measured_peaks():
     return hbm, src, fp64, fsrc
 
 
-def ncu_traffic(kernel: str):
+def ncu_traffic(kernel: str, tag: str):
+    """DRAM bytes per launch of ``kernel`` from the committed ncu capture of the
+    same workload (profiles/ncu_summary.json, key "<tag>/<kernel>"), or None."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:
-        return json.loads(p.read_text()).get(kernel, {}).get("dram_bytes_per_launch")
+        return json.loads(p.read_text()).get(f"{tag}/{kernel}", {}).get("dram_bytes_per_launch")
     except ValueError:
         return None
 
@@ -508,7 +526,8 @@ def run_gpu(args):
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm,
                          "traffic": ncu_traffic("fase_iterate_complex_kernel" if cplx
-                                                else "fase_iterate_kernel"),
+                                                else "fase_iterate_kernel",
+                                                "dft" if args.dict == "dft" else f"c{args.config}"),
                          "algorithmic_bytes_per_launch": bytes_iter,
                          "ms_per_launch": it_s * 1e3, "peak_source": hsrc,
                          "note": ("16*K bytes per block-iteration (one complex128 table row)"
@@ -657,8 +676,11 @@ def run_gpu_frame(args):
     it_s = ev_i0.elapsed_time(ev_i1) / 1e3
     if rank == 0:
         hbm, hsrc, fp64, fsrc = measured_peaks()
-        bytes_iter = 8.0 * K * L * I * mean_rows
+        # SURVEY 8(d) unit: one FP64 table row (8 K bytes) per block-iteration;
+        # the chunked tables stream (1 + unavailable cells) rows for it
+        bytes_iter = 8.0 * K * L * I
         achieved = bytes_iter / it_s / 1e9
+        streamed = bytes_iter * mean_rows
         line = {
             "metric": "extrapolated blocks/s", "value": world * L * args.steps / dev_t,
             "unit": "blocks/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -676,8 +698,12 @@ def run_gpu_frame(args):
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": None, "algorithmic_bytes_per_launch": bytes_iter,
                          "ms_per_launch": it_s * 1e3, "peak_source": hsrc,
-                         "note": "8*K bytes per table row, (1 + unavailable cells) rows per "
-                                 "block-iteration"},
+                         "streamed_bytes_per_launch": streamed,
+                         "streamed_gbs": streamed / it_s / 1e9,
+                         "note": "achieved counts 8*K bytes (one table row) per block-iteration, "
+                                 "the SURVEY 8(d) unit; the per-block table G0 - sum C_cell "
+                                 "streams (1 + unavailable cells) rows for it (streamed_*), "
+                                 "served largely from L2"},
             "table_build_s": engine.table_seconds,
             "gpu_launches": args.steps * (engine.launches_per_frame + 1) * 2,
             "clocks": clocks.summary(), "wall_s": t_wall, "cpu_baseline": cpu,

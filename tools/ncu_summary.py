@@ -3,7 +3,9 @@
     python tools/ncu_summary.py OUT_PREFIX REPORT.ncu-rep [REPORT2 ...] [--launches launches.csv]
 
 Writes OUT_PREFIX.md (human summary) and merges per-kernel DRAM traffic into
-profiles/ncu_summary.json (read by bench.py for the roofline "traffic" key).
+profiles/ncu_summary.json under "<tag>/<kernel>", tag = the suffix after
+"_ncu_" in OUT_PREFIX (c1, c4, dft ...); bench.py reads it for the roofline
+"traffic" key of the matching config.
 """
 
 from __future__ import annotations
@@ -26,6 +28,14 @@ METRICS = [
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % peak"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % peak"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active %"),
+    ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+     "tensor pipe active, realtime % of elapsed (tcgen05)"),
+    ("sm__inst_executed_pipe_tensor_subpipe_imma.avg.pct_of_peak_sustained_active",
+     "IMMA subpipe instructions % peak"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+     "tensor memory (smem operand / TMEM) cycles active %"),
+    ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+     "DMMA subpipe instructions % peak"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active %"),
     ("sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active", "shared pipe active %"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
@@ -59,9 +69,12 @@ def to_bytes(val: str, unit: str) -> float:
 
 
 def short(name: str) -> str:
-    for key in ("fase_iterate_kernel", "dgemm_nt_kernel", "synth_paste_kernel", "gram_finish_kernel",
-                "weigh_kernel",
-                "block_normalizers_kernel", "basis_outer_kernel", "flush_kernel"):
+    for key in ("fase_iterate_complex_kernel", "fase_iterate_kernel", "dgemm_nt_kernel",
+                "synth_paste_complex_kernel", "synth_paste_kernel", "gram_finish_kernel",
+                "weigh_gather_kernel", "weigh_kernel", "sep_products_complex_kernel",
+                "sep_products_kernel", "ozaki_gemm_kernel", "ozaki_split_kernel",
+                "block_normalizers_kernel", "basis_outer_kernel", "flush_kernel",
+                "frame_areas_kernel", "frame_cells_kernel", "frame_paste_kernel"):
         if key in name:
             return key
     return name[:60]
@@ -91,7 +104,8 @@ def main():
             lines.append("")
             traffic = to_bytes(row["dram__bytes_read.sum"], unit["dram__bytes_read.sum"]) + \
                 to_bytes(row["dram__bytes_write.sum"], unit["dram__bytes_write.sum"])
-            js[short(name)] = {"dram_bytes_per_launch": traffic, "report": Path(rep).name,
+            tag = Path(out).name.split("_ncu_")[-1]  # e.g. profiles/r01_ncu_c1 -> c1
+            js[f"{tag}/{short(name)}"] = {"dram_bytes_per_launch": traffic, "report": Path(rep).name,
                                "duration_ms": float(row["gpu__time_duration.sum"].replace(",", "")) *
                                (1e-3 if unit["gpu__time_duration.sum"] == "us" else 1.0)}
     if launches:
