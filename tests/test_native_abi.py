@@ -80,9 +80,24 @@ def test_status_codes_and_messages(lib):
     assert lib.fase_gram_complex(None, 0, None, 0, 0, None, 0, None, 0, None) == -1
     assert lib.fase_synth_paste_complex(None, 0, None, None, 0, 0, 1, None, None, 0, None, None, 0,
                                         None, None) == -1
+    # transform shortcuts, support gather, tcgen05 Ozaki products
+    assert lib.fase_sep_products_complex(None, None, 0, 4, None, None, 4, 4, None, 16, 1, None, 16,
+                                         0, None) == -1
+    assert lib.fase_fft_gram(None, 4, 4, None, None, 17, None, 17, None) == -1  # K > M*N
+    assert b"canonical" in lib.fase_last_error()
+    assert lib.fase_weigh_gather(None, 8, None, None, 2, 4, None, 2, None) == -1  # ldo < 4
+    assert lib.fase_ozaki_split(None, 64, None, None, 4, 64, 9, None, 64, 8, None, None) == -1
+    assert b"slices=9" in lib.fase_last_error()
+    assert lib.fase_ozaki_split(None, 64, None, None, 4, 70, 8, None, 64, 8, None, None) == -1
+    assert lib.fase_ozaki_gemm(None, 128, None, 100, None, 64, None, 50, 96, 8, None, 50,
+                               None) == -1  # kp not a multiple of 64
+    assert lib.fase_ozaki_gemm(None, 64, None, 100, None, 64, None, 50, 64, 8, None, 50,
+                               None) == -1  # A rows not padded to 128
+    assert b"padded" in lib.fase_last_error()
     # empty batches are a no-op, not an error
     args = _native.IterateArgs(K=4, B=0, I=1, gamma=0.5)
     assert lib.fase_iterate(ctypes.byref(args), None) == 0
+    assert lib.fase_ozaki_gemm(None, 128, None, 0, None, 64, None, 50, 64, 8, None, 50, None) == 0
 
 
 def test_status_maps_to_reference_exceptions(lib):
