@@ -77,6 +77,70 @@ __device__ __forceinline__ double np_cabs(double re, double im) {
   return __dmul_rn(__dsqrt_rn(__fma_rn(r, r, 1.0)), hi);
 }
 
+// ---- call-free correctly rounded division / square root on a narrow range ---
+// The IEEE __ddiv_rn / __dsqrt_rn carry slow-path subroutine calls for special
+// operands; inlined in a register-resident kernel, every call site forces the
+// caller's live registers around it. These variants cover only normal operands
+// in a fixed binade (the callers scale exactly into it) and are checked
+// bit-for-bit against the IEEE operations (tools/probes/cabs_probe.cu).
+
+// RN(a / b) for 1 <= b < 2 and 2^-61 <= a < 2: hardware reciprocal estimate, two
+// Newton steps, one fused correction of the quotient (Markstein).
+__device__ __forceinline__ double div_rn_unit(double a, double b) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
+  double e = __fma_rn(-b, y, 1.0);
+  y = __fma_rn(y, e, y);
+  e = __fma_rn(-b, y, 1.0);
+  y = __fma_rn(y, e, y);
+  const double q = __dmul_rn(a, y);
+  const double r = __fma_rn(-b, q, a);
+  return __fma_rn(r, y, q);
+}
+
+// RN(sqrt(t)) for 1 <= t <= 2: reciprocal square-root estimate, coupled
+// Newton iterations for sqrt and 1/(2 sqrt), one fused final correction.
+__device__ __forceinline__ double sqrt_rn_unit(double t) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(t));
+  double s = __dmul_rn(t, y);
+  double h = 0.5 * y;
+  double e = __fma_rn(-s, h, 0.5);
+  s = __fma_rn(s, e, s);
+  h = __fma_rn(h, e, h);
+  e = __fma_rn(-s, h, 0.5);
+  s = __fma_rn(s, e, s);
+  h = __fma_rn(h, e, h);
+  const double d = __fma_rn(-s, s, t);
+  return __fma_rn(d, h, s);
+}
+
+// np_cabs without subroutine calls: identical results for finite inputs.
+// lo <= hi * 2^-61 gives r^2 < 2^-122, so fma(r, r, 1) == 1 and |z| == hi.
+// Otherwise both are scaled by the same power of two (exact) into hi in [1, 2).
+__device__ __forceinline__ double np_cabs_fast(double re, double im) {
+  const double a = fabs(re), b = fabs(im);
+  const double hi = fmax(a, b), lo = fmin(a, b);
+  if (hi == 0.0) return 0.0;
+  if (lo <= hi * 0x1p-61) return hi;
+  long long hb = __double_as_longlong(hi);
+  double hs = hi, ls = lo;
+  if ((hb >> 52) == 0) {  // subnormal: lift by 2^64 first (exact)
+    hs *= 0x1p64;
+    ls *= 0x1p64;
+    hb = __double_as_longlong(hs);
+  }
+  const int ex = static_cast<int>(hb >> 52) - 1023;  // hs in [2^ex, 2^(ex+1))
+  // 2^-ex as a double (ex in [-1022 - 64, 1023]; split in two factors to stay normal)
+  const int e1 = -ex / 2, e2 = -ex - e1;
+  const double f1 = __longlong_as_double(static_cast<long long>(e1 + 1023) << 52);
+  const double f2 = __longlong_as_double(static_cast<long long>(e2 + 1023) << 52);
+  hs = (hs * f1) * f2;
+  ls = (ls * f1) * f2;
+  const double r = div_rn_unit(ls, hs);
+  return __dmul_rn(sqrt_rn_unit(__fma_rn(r, r, 1.0)), hi);
+}
+
 __device__ __forceinline__ double2 ldg2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
