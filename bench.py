@@ -541,8 +541,11 @@ def run_gpu(args):
                                "unit": "TFLOP/s", "frac": flops_init / init_s / 1e12 / fp64,
                                "ms_per_launch": init_s * 1e3, "peak_source": fsrc}
                               if not factors else
-                              {"bound": "fp64", "kernel": "weigh_kernel + sep_products"
-                               + ("_complex" if cplx else "") + "_kernel (separable transforms, FP64 FMA)",
+                              {"bound": "tensor" if not cplx else "fp64",
+                               "kernel": ("sep_products_dmma_kernel (separable transforms on DMMA, "
+                                          "weights fused, all parts in one launch)") if not cplx else
+                                         "weigh_kernel + sep_products_complex_kernel (separable "
+                                         "transforms, FP64 FMA)",
                                "achieved": flops_sep / init_s / 1e12, "peak": fp64,
                                "unit": "TFLOP/s", "frac": flops_sep / init_s / 1e12 / fp64,
                                "ms_per_launch": init_s * 1e3, "peak_source": fsrc,

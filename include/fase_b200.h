@@ -144,6 +144,25 @@ FASE_API int fase_sep_products(const double* rows, int Lr, int Mr, const double*
                                int64_t ldr, int64_t col0, void* stream);
 
 /*
+ * All separable parts of a dictionary at once on the FP64 tensor cores
+ * (mma.sync f64), with the weights applied while staging the area:
+ *   X_b = F_b o W (W == NULL: F is already weighted; ldw == 0: one shared W)
+ *   R0[b*ldr + col0_p + u*Lc_p + v] = (rows_p X_b cols_p^T)[u, v]   for every part p
+ * -- fase_weigh + fase_sep_products for up to 8 parts in one launch.
+ */
+typedef struct {
+  const double* rows; /* Lr x Mr */
+  int Lr;
+  const double* cols; /* Lc x Nc */
+  int Lc;
+  int64_t col0;
+} fase_sep_part;
+
+FASE_API int fase_sep_products_batch(const fase_sep_part* parts, int n_parts, int Mr, int Nc,
+                                     const double* F, int64_t ldf, const double* W, int64_t ldw,
+                                     int B, double* R0, int64_t ldr, void* stream);
+
+/*
  * Per-block normalizers for per-block geometries whose table rows are
  * G_b = G0 - sum_{j in chunks(b)} C_j (see fase_iterate):
  *   diag_b[k] = G0[k,k] - sum_j C_j[k,k];  D[b*ldd + k] as in fase_gram_finish.

@@ -36,13 +36,19 @@ EXPORTS = (
     "fase_frame_paste", "fase_weigh", "fase_sep_products", "fase_gram_complex_workspace",
     "fase_gram_complex", "fase_max_atoms_complex", "fase_table_ld_complex", "fase_iterate_complex",
     "fase_synth_paste_complex", "fase_sep_products_complex", "fase_fft_gram", "fase_weigh_gather",
-    "fase_ozaki_split", "fase_ozaki_gemm",
+    "fase_ozaki_split", "fase_ozaki_gemm", "fase_sep_products_batch",
 )
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int
 _i64 = ctypes.c_int64
 _f64 = ctypes.c_double
+
+
+class SepPart(ctypes.Structure):
+    """Mirror of ``fase_sep_part`` (include/fase_b200.h)."""
+
+    _fields_ = [("rows", _vp), ("Lr", _i32), ("cols", _vp), ("Lc", _i32), ("col0", _i64)]
 
 
 class IterateArgs(ctypes.Structure):
@@ -108,6 +114,8 @@ def load():
                                       _vp, _i64, _i64, _vp],
         "fase_fft_gram": [_vp, _i32, _i32, _vp, _vp, _i32, _vp, _i64, _vp],
         "fase_weigh_gather": [_vp, _i64, _vp, _vp, _i32, _i32, _vp, _i64, _vp],
+        "fase_sep_products_batch": [ctypes.POINTER(SepPart), _i32, _i32, _i32, _vp, _i64, _vp,
+                                    _i64, _i32, _vp, _i64, _vp],
         "fase_ozaki_split": [_vp, _i64, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp],
         "fase_ozaki_gemm": [_vp, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i64, _i32, _vp, _i64,
                             _vp],
@@ -544,6 +552,26 @@ def ozaki_gemm(a: OzakiOperand, b: OzakiOperand, C) -> None:
     _check(lib.fase_ozaki_gemm(_ptr(a.planes), a.rows_pad, _ptr(a.exps), a.rows,
                                _ptr(b.planes), b.rows_pad, _ptr(b.exps), b.rows, a.kp,
                                a.slices, _ptr(C), _ld(C), _stream(C)))
+
+
+def sep_products_batch(factors, F, W, M_rows: int, N_cols: int, R0) -> None:
+    """All separable parts [(rows, cols, col0)] of F o W (W None: F already
+    weighted; 1-D W shared) on the FP64 tensor cores, one launch."""
+    import torch
+
+    lib = load()
+    _require(F, "F", torch.float64, 2)
+    _require(R0, "R0", torch.float64, 2)
+    if W is not None:
+        _require(W, "W", torch.float64)
+    parts = (SepPart * len(factors))()
+    for i, (rows, cols, col0) in enumerate(factors):
+        _require(rows, "rows", torch.float64, 2)
+        _require(cols, "cols", torch.float64, 2)
+        parts[i] = SepPart(_ptr(rows), rows.shape[0], _ptr(cols), cols.shape[0], col0)
+    ldw = _ld(W) if (W is not None and W.dim() == 2) else 0
+    _check(lib.fase_sep_products_batch(parts, len(factors), M_rows, N_cols, _ptr(F), _ld(F),
+                                       _ptr(W), ldw, F.shape[0], _ptr(R0), _ld(R0), _stream(R0)))
 
 
 def sep_products(rows, cols, X, M_rows: int, N_cols: int, R0, col0: int) -> None:

@@ -170,7 +170,7 @@ class FrameEngine:
         iterate, paste"""
         factors = self.dictionary.device_factors(self.device)
         if factors:
-            return 5 + len(factors)
+            return 5 + (1 if len(factors) <= 8 else len(factors))
         return 5 + (2 if any("oz" in b for b in self._buf.values()) else 1)
 
     def run(self, frame, grid, corners, out=None) -> BatchResult:
@@ -191,7 +191,9 @@ class FrameEngine:
         _native.block_normalizers(self.G0, self.tables, self.stride, b["counts"], b["ids"], K,
                                   b["D"], b["alive"])
         factors = self.dictionary.device_factors(self.device)
-        if factors:  # separable parts: rows X cols^T per part (csrc/separable.cu)
+        if factors and len(factors) <= 8:  # separable parts on DMMA, one launch
+            _native.sep_products_batch(factors, b["X"], None, self.A, self.A, b["R0"])
+        elif factors:  # rows X cols^T per part (csrc/separable.cu)
             for rows, cols, row0 in factors:
                 _native.sep_products(rows, cols, b["X"], self.A, self.A, b["R0"], row0)
         elif self._oz_phi is not None and "oz" in b:

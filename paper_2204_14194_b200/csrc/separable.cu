@@ -205,6 +205,151 @@ __global__ void __launch_bounds__(256) fft_gram_kernel(const double2* __restrict
   }
 }
 
+// ---- the same transforms on the FP64 tensor cores (DMMA), all parts fused ----
+//
+// One CTA per block: X = F o W (weights applied while staging, one rounding per
+// sample as fase_weigh) stays in shared memory and every separable part runs
+// two small NT contractions on mma.sync.m8n8k4.f64:
+//   T[v][m] = sum_n cols[v][n] X[m][n],   out[u][v] = sum_m rows[u][m] T[v][m].
+// Each warp owns 16 x 16 output macro-tiles (2 x 2 fragments, operands reused
+// across the fragment pair); the factor tables are read through L1 (shared by
+// every block); shared rows are padded to 4 (mod 16) doubles like the GEMM's.
+
+constexpr int kSepMaxParts = 8;
+
+struct SepPartsArg {
+  const double* rows[kSepMaxParts];
+  const double* cols[kSepMaxParts];
+  int lr[kSepMaxParts];
+  int lc[kSepMaxParts];
+  int64_t col0[kSepMaxParts];
+  int n;
+};
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// acc[i][j] (8x8 fragment (i, j) of the macro-tile at rows r0, cols c0) of
+// C[r][c] = sum_k A(r, k) B(c, k), k < kk (a multiple of 4); A / B fetched by
+// the given functors (zero outside their extents).
+template <class FA, class FB>
+__device__ __forceinline__ void macro_nt(FA fa, FB fb, int r0, int c0, int kk, double (&acc)[2][2][2]) {
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // operands of step k + 4 are fetched while step k's four MMAs run
+  double a0 = fa(r0 + fr, fc), a1 = fa(r0 + 8 + fr, fc);
+  double b0 = fb(c0 + fr, fc), b1 = fb(c0 + 8 + fr, fc);
+#pragma unroll 4
+  for (int k = 0; k < kk; k += 4) {
+    const bool more = k + 4 < kk;
+    const double na0 = more ? fa(r0 + fr, k + 4 + fc) : 0.0;
+    const double na1 = more ? fa(r0 + 8 + fr, k + 4 + fc) : 0.0;
+    const double nb0 = more ? fb(c0 + fr, k + 4 + fc) : 0.0;
+    const double nb1 = more ? fb(c0 + 8 + fr, k + 4 + fc) : 0.0;
+    dmma884(acc[0][0][0], acc[0][0][1], a0, b0);
+    dmma884(acc[0][1][0], acc[0][1][1], a0, b1);
+    dmma884(acc[1][0][0], acc[1][0][1], a1, b0);
+    dmma884(acc[1][1][0], acc[1][1][1], a1, b1);
+    a0 = na0;
+    a1 = na1;
+    b0 = nb0;
+    b1 = nb1;
+  }
+}
+
+__global__ void __launch_bounds__(288) sep_products_dmma_kernel(
+    const SepPartsArg parts, int Mr, int Nc, const double* __restrict__ F, int64_t ldf,
+    const double* __restrict__ W, int64_t ldw, double* __restrict__ R0, int64_t ldr) {
+  extern __shared__ __align__(16) double sm[];
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fc = lane & 3;
+  const int Mp = (Mr + 15) & ~15, Nk = (Nc + 3) & ~3, Mk = (Mr + 3) & ~3;
+  const int sx = Nk + ((4 - Nk) & 15), st = Mk + ((4 - Mk) & 15);  // strides = 4 (mod 16)
+  double* sX = sm;                   // Mp x sx: X[m][n], zero padded
+  double* sT = sm + Mp * sx;         // Lcp x st: T[v][m]
+  const double* f = F + static_cast<int64_t>(b) * ldf;
+  const double* w = W ? W + static_cast<int64_t>(b) * ldw : nullptr;
+  // zero the padding, then stage the area with independent loads in flight
+  for (int i = threadIdx.x; i < Mp * sx; i += blockDim.x) {
+    const int m = i / sx, n = i - m * sx;
+    if (m >= Mr || n >= Nc) sX[i] = 0.0;
+  }
+  const int area = Mr * Nc;
+  for (int i0 = 0; i0 < area; i0 += 4 * static_cast<int>(blockDim.x)) {
+    double v[4], wv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + j * blockDim.x + threadIdx.x;
+      v[j] = i < area ? __ldg(f + i) : 0.0;
+      wv[j] = (w && i < area) ? __ldg(w + i) : 1.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + j * blockDim.x + threadIdx.x;
+      if (i < area) {
+        const int m = i / Nc;
+        sX[m * sx + (i - m * Nc)] = w ? __dmul_rn(v[j], wv[j]) : v[j];
+      }
+    }
+  }
+  for (int p = 0; p < parts.n; ++p) {
+    const double* rows = parts.rows[p];
+    const double* cols = parts.cols[p];
+    const int Lr = parts.lr[p], Lc = parts.lc[p];
+    const int Lcp = (Lc + 15) & ~15, Lrp = (Lr + 15) & ~15;
+    __syncthreads();  // sX staged / previous part's sT consumed
+    // T[v][m] = sum_n cols[v][n] X[m][n]
+    {
+      auto fa = [&](int v, int n) { return (v < Lc && n < Nc) ? __ldg(cols + v * Nc + n) : 0.0; };
+      auto fb = [&](int m, int n) { return sX[m * sx + n]; };
+      const int tm = Lcp / 16, tn = Mp / 16;
+      for (int t = warp; t < tm * tn; t += nwarps) {
+        const int r0 = (t / tn) * 16, c0 = (t % tn) * 16;
+        double acc[2][2][2];
+        macro_nt(fa, fb, r0, c0, Nk, acc);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int v = r0 + 8 * i + fr, m = c0 + 8 * j + 2 * fc + e;
+              if (m < st) sT[v * st + m] = (m < Mr) ? acc[i][j][e] : 0.0;
+            }
+      }
+    }
+    __syncthreads();
+    // out[u][v] = sum_m rows[u][m] T[v][m]  ->  R0[b, col0 + u*Lc + v]
+    {
+      auto fa = [&](int u, int m) { return (u < Lr && m < Mr) ? __ldg(rows + u * Mr + m) : 0.0; };
+      auto fb = [&](int v, int m) { return sT[v * st + m]; };
+      const int tm = Lrp / 16, tn = Lcp / 16;
+      double* out = R0 + static_cast<int64_t>(b) * ldr + parts.col0[p];
+      for (int t = warp; t < tm * tn; t += nwarps) {
+        const int r0 = (t / tn) * 16, c0 = (t % tn) * 16;
+        double acc[2][2][2];
+        macro_nt(fa, fb, r0, c0, Mk, acc);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int u = r0 + 8 * i + fr, v = c0 + 8 * j + 2 * fc + e;
+              if (u < Lr && v < Lc) out[u * Lc + v] = acc[i][j][e];
+            }
+      }
+    }
+  }
+}
+
 }  // namespace
 }  // namespace fase
 
@@ -322,4 +467,52 @@ extern "C" int fase_fft_gram(const double* spec, int M, int N, const int32_t* mu
                     as_stream(stream)>>>(reinterpret_cast<const double2*>(spec), M, N, mu, eta, K,
                                          reinterpret_cast<double2*>(T), ldt);
   return check_launch("fase_fft_gram");
+}
+
+extern "C" int fase_sep_products_batch(const fase_sep_part* parts, int n_parts, int Mr, int Nc,
+                                       const double* F, int64_t ldf, const double* W, int64_t ldw,
+                                       int B, double* R0, int64_t ldr, void* stream) {
+  if (n_parts < 1 || n_parts > kSepMaxParts || Mr < 1 || Nc < 1 || B < 0 ||
+      ldf < static_cast<int64_t>(Mr) * Nc || (W && ldw != 0 && ldw < static_cast<int64_t>(Mr) * Nc)) {
+    set_error("fase_sep_products_batch: bad sizes (parts=%d Mr=%d Nc=%d B=%d)", n_parts, Mr, Nc, B);
+    return FASE_ERR_SHAPE;
+  }
+  if (B == 0) return FASE_OK;
+  if (!parts || !F || !R0) {
+    set_error("fase_sep_products_batch: null pointer");
+    return FASE_ERR_SHAPE;
+  }
+  SepPartsArg a{};
+  a.n = n_parts;
+  int lcp_max = 16;
+  for (int p = 0; p < n_parts; ++p) {
+    const fase_sep_part& q = parts[p];
+    if (!q.rows || !q.cols || q.Lr < 1 || q.Lc < 1 || q.col0 < 0 ||
+        ldr < q.col0 + static_cast<int64_t>(q.Lr) * q.Lc) {
+      set_error("fase_sep_products_batch: part %d: bad factors / output range", p);
+      return FASE_ERR_SHAPE;
+    }
+    a.rows[p] = q.rows;
+    a.cols[p] = q.cols;
+    a.lr[p] = q.Lr;
+    a.lc[p] = q.Lc;
+    a.col0[p] = q.col0;
+    lcp_max = (q.Lc + 15) / 16 * 16 > lcp_max ? (q.Lc + 15) / 16 * 16 : lcp_max;
+  }
+  const int Mp = (Mr + 15) / 16 * 16, Nk = (Nc + 3) / 4 * 4, Mk = (Mr + 3) / 4 * 4;
+  const int sx = Nk + ((4 - Nk) & 15), st = Mk + ((4 - Mk) & 15);
+  const size_t smem = sizeof(double) * (static_cast<size_t>(Mp) * sx + static_cast<size_t>(lcp_max) * st);
+  if (smem > 200 * 1024) {
+    set_error("fase_sep_products_batch: area %dx%d too large for shared memory", Mr, Nc);
+    return FASE_ERR_UNSUPPORTED;
+  }
+  cudaError_t e = cudaFuncSetAttribute(sep_products_dmma_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) {
+    set_error("fase_sep_products_batch: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return FASE_ERR_CUDA;
+  }
+  sep_products_dmma_kernel<<<B, 288, smem, as_stream(stream)>>>(a, Mr, Nc, F, ldf, W, ldw, R0, ldr);
+  return check_launch("fase_sep_products_batch");
 }

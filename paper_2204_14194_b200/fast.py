@@ -266,11 +266,14 @@ def initial_products_into(dictionary: Dictionary, F, W, R0, ws, *, method: str =
     if factors is None:
         _native.init_products(dictionary.device_matrix(dev), F, W, K, M, R0, ws=ws)
         return "gemm"
+    m, n = dictionary.shape
+    if len(factors) <= 8:  # weights fused, all parts in one DMMA launch
+        _native.sep_products_batch(factors, F, W, m, n, R0)
+        return "separable"
     B = F.shape[0]
     ldx = M + (M & 1)
     X = ws[: B * ldx].view(B, ldx)
     _native.weigh(F, W, M, X)
-    m, n = dictionary.shape
     for rows, cols, row0 in factors:
         _native.sep_products(rows, cols, X, m, n, R0, row0)
     return "separable"
@@ -669,7 +672,7 @@ class ExtrapolationPlan:
             n_prod = 1 + (len(cparts) + len(_ranges(self._uncovered(cparts))) if cparts else 1)
         else:
             factors = dictionary.device_factors(dev) if products in ("auto", "separable") else None
-            n_prod = 1 + (len(factors) if factors else 1)
+            n_prod = (1 if len(factors) <= 8 else 1 + len(factors)) if factors else 2
         # Dense products over the support only: the lost samples have weight 0
         # and add exact zeros, so Phi's support columns are gathered once and
         # each run contracts over them (fase_weigh_gather + one DMMA GEMM).

@@ -428,3 +428,34 @@ def test_plan_support_compacted_products(spec):
                               metric_fn(ref["r0"], ref["d"], ref["log"]))
         assert v.ok
     del w
+
+
+@pytest.mark.parametrize("spec,m,n", [("union:dct+had", 48, 48), ("dct", 5, 7), ("union:dct+wht", 16, 16)])
+def test_separable_dmma_batch_matches_fma_kernel(spec, m, n):
+    """The fused DMMA transform (weights applied while staging, all parts in one
+    launch) equals the per-part FMA kernel and the oracle to rounding."""
+    d = parse_dict_spec(spec, m, n)
+    K, M = len(d), m * n
+    B = 19
+    sig = np.random.default_rng(31).uniform(0, 255, (B, m, n))
+    mask = wl.central_loss_mask(m, n, max(1, m // 3), max(1, n // 3))
+    w = build_weight_field(mask, 0.8)
+    ld = M + (M & 1)
+    F = torch.zeros((B, ld), dtype=torch.float64, device=DEV)
+    F[:, :M] = torch.from_numpy(sig.reshape(B, -1)).to(DEV)
+    W = torch.zeros(ld, dtype=torch.float64, device=DEV)
+    W[:M] = torch.from_numpy(w.ravel()).to(DEV)
+    factors = d.device_factors(DEV)
+    Rd = torch.zeros((B, K + 3), dtype=torch.float64, device=DEV)
+    _native.sep_products_batch(factors, F, W, m, n, Rd)
+    X = torch.zeros((B, ld), dtype=torch.float64, device=DEV)
+    _native.weigh(F, W, M, X)
+    Rf = torch.zeros((B, K + 3), dtype=torch.float64, device=DEV)
+    for rows, cols, row0 in factors:
+        _native.sep_products(rows, cols, X, m, n, Rf, row0)
+    a, f = Rd.cpu().numpy(), Rf.cpu().numpy()
+    assert np.all(a[:, K:] == 0.0)
+    assert rel_dev(a, f) < 1e-13
+    phi = d.real_values().reshape(K, -1).astype(np.complex128)
+    for b in (0, B - 1):
+        assert rel_dev(a[b, :K], orc.initial_products(sig[b], w, phi).real) < 1e-13
