@@ -48,12 +48,26 @@ __device__ __forceinline__ long long warp_max_i64(long long v) {
 // g + sum_t coef[t] * phi[sel[t] * ldphi + m] for t ascending, stopping at the
 // first sel < 0 (a block whose atoms were all degenerate): the reference's
 // sequential summation order (SparseModel.materialize, reference.py:120-125).
+// Atom values are fetched 8 terms at a time (independent loads in flight), then
+// accumulated strictly in order.
 __device__ __forceinline__ double synth_terms(const double* __restrict__ phi, int64_t ldphi,
                                               const int32_t* s_sel, const double* s_coef,
                                               int len, int m, double g) {
-  for (int t = 0; t < len; ++t) {
-    if (s_sel[t] < 0) break;
-    g = __dadd_rn(g, __dmul_rn(s_coef[t], __ldg(phi + static_cast<int64_t>(s_sel[t]) * ldphi + m)));
+  constexpr int G = 8;
+  for (int t0 = 0; t0 < len; t0 += G) {
+    double v[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int t = t0 + j;
+      const int u = t < len ? s_sel[t] : -1;
+      v[j] = u >= 0 ? __ldg(phi + static_cast<int64_t>(u) * ldphi + m) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int t = t0 + j;
+      if (t >= len || s_sel[t] < 0) return g;
+      g = __dadd_rn(g, __dmul_rn(s_coef[t], v[j]));
+    }
   }
   return g;
 }
