@@ -701,20 +701,41 @@ class ExtrapolationPlan:
         # (weigh +) products + iterate + synth
         self.launches_per_run = n_prod + 1 + (1 if self.n_lost else 0)
 
-    def _products(self, F):
+    def _scratch(self, slot: int = 0) -> dict:
+        """Per-slot work buffers (R0, products scratch, max |Im g|): slot 0 is the
+        plan's own, slot 1 lets a second batch run concurrently (run_host_stream)."""
+        torch = _torch()
+        if slot == 0:
+            return {"R0": self.R0, "ws": self.ws,
+                    "X": self._support[3] if self._support is not None else None,
+                    "oz": self._ozaki[0] if self._ozaki is not None else None,
+                    "max_imag": self.max_imag}
+        if not hasattr(self, "_slot1"):
+            oz = None
+            if self._ozaki is not None:
+                a = self._ozaki[0]
+                oz = _native.OzakiOperand(a.rows, a.kd, 128, self.device, a.slices)
+            self._slot1 = {
+                "R0": torch.empty_like(self.R0), "ws": torch.empty_like(self.ws),
+                "X": torch.empty_like(self._support[3]) if self._support is not None else None,
+                "oz": oz,
+                "max_imag": torch.zeros_like(self.max_imag) if self.max_imag is not None else None}
+        return self._slot1
+
+    def _products(self, F, slot: int = 0):
         """R0 for signals F (device, (B, ldf)): the support-compacted GEMM when
         the products are dense, else initial_products_into."""
+        sc = self._scratch(slot)
         if self._support is None:
-            return initial_products_into(self.dictionary, F, self.W, self.R0, self.ws,
+            return initial_products_into(self.dictionary, F, self.W, sc["R0"], sc["ws"],
                                          method=self.products)
-        sidx, w_s, phi_s, X = self._support
-        out = _real_view(self.R0) if self.complex else self.R0
+        sidx, w_s, phi_s, _ = self._support
+        out = _real_view(sc["R0"]) if self.complex else sc["R0"]
         if self._ozaki is not None:  # gather, weigh and split in one pass
-            a, b = self._ozaki
-            _native.ozaki_gemm(a.split(F, sidx, w_s), b, out)
+            _native.ozaki_gemm(sc["oz"].split(F, sidx, w_s), self._ozaki[1], out)
             return "ozaki-support"
-        _native.weigh_gather(F, sidx, w_s, X)
-        _native.gemm_nt(X, phi_s, out)
+        _native.weigh_gather(F, sidx, w_s, sc["X"])
+        _native.gemm_nt(sc["X"], phi_s, out)
         return "gemm-support"
 
     def _uncovered(self, cparts):
@@ -723,16 +744,18 @@ class ExtrapolationPlan:
             flags[row0: row0 + rre.shape[0] * cre.shape[0]] = False
         return flags
 
-    def _iterate_synth(self, sel, proj, coef, lost):
+    def _iterate_synth(self, sel, proj, coef, lost, slot: int = 0):
+        sc = self._scratch(slot)
         if self.complex:
-            _native.iterate_complex(self.G, self.D, self.R0, self.K, self.I, self.config.gamma,
+            _native.iterate_complex(self.G, self.D, sc["R0"], self.K, self.I, self.config.gamma,
                                     sel, proj, coef)
             if self.n_lost:
                 _native.synth_paste_complex(self.phi_lost, sel, coef, self.I, self.lost_seq, lost,
                                             n_shared=self.n_lost, dst=self.lost_pos,
-                                            max_imag=self.max_imag)
+                                            max_imag=sc["max_imag"])
             return
-        _native.iterate(self.G, self.D, self.R0, self.K, self.I, self.config.gamma, sel, proj, coef)
+        _native.iterate(self.G, self.D, sc["R0"], self.K, self.I, self.config.gamma, sel, proj,
+                        coef)
         if self.n_lost:
             _native.synth_paste(self.phi_lost, sel, coef, self.I, self.lost_seq, lost,
                                 n_shared=self.n_lost, dst=self.lost_pos)
@@ -768,28 +791,35 @@ class ExtrapolationPlan:
         return out
 
     def run_host_stream(self, host_inputs, host_outputs):
-        """End-to-end over a sequence of batches with copies overlapped.
+        """End-to-end over a sequence of batches with copies and batches overlapped.
 
         ``host_inputs[i]`` (pinned (B, M, N) float64) goes in and
         ``host_outputs[i]`` (pinned dicts from ``host_buffers``) comes back, for
-        every i. Step i+1's host-to-device copy runs on its own stream while
-        step i computes, and step i's results come back on a third stream.
-        Device input and output buffers are double-buffered, and events order
-        each reuse. Everything is enqueued; the caller synchronizes.
+        every i. Consecutive batches alternate between two compute streams with
+        their own device buffers, so batch i+1's copy-in, products and first
+        recursion CTAs fill the SMs that batch i's last wave leaves idle;
+        copies run on their own streams; events order every buffer reuse.
+        Everything is enqueued; the caller's stream waits for the last results.
         """
         torch = _torch()
         dev = self.device
         cs = torch.cuda.current_stream(dev)
         if not hasattr(self, "_pipe"):
+            self._scratch(1)
             self._pipe = {
                 "h2d": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev),
+                "comp": [torch.cuda.Stream(dev), torch.cuda.Stream(dev)],
                 "F": [self.F, torch.zeros_like(self.F)],
                 "out": [(self.selected, self.projections, self.coefficients, self.lost),
                         tuple(torch.empty_like(x) for x in (self.selected, self.projections,
                                                             self.coefficients, self.lost))],
             }
         p = self._pipe
-        h2d, d2h = p["h2d"], p["d2h"]
+        h2d, d2h, comp = p["h2d"], p["d2h"], p["comp"]
+        start = torch.cuda.Event()
+        start.record(cs)  # nothing below starts before the caller's prior work
+        for st in (h2d, d2h, comp[0], comp[1]):
+            st.wait_event(start)
         ev_in = [torch.cuda.Event(), torch.cuda.Event()]
         ev_used = [None, None]     # compute finished reading F[slot]
         ev_out = [None, None]      # results of slot copied back
@@ -802,15 +832,17 @@ class ExtrapolationPlan:
                     h2d.wait_event(ev_used[s])
                 F[:, : self.M].copy_(hin.reshape(self.B, -1), non_blocking=True)
                 ev_in[s].record(h2d)
-            cs.wait_event(ev_in[s])
-            if ev_out[s] is not None:
-                cs.wait_event(ev_out[s])
-            self._products(F)
-            ev_used[s] = torch.cuda.Event()
-            ev_used[s].record(cs)
-            self._iterate_synth(sel, proj, coef, lost)
-            done = torch.cuda.Event()
-            done.record(cs)
+            c = comp[s]
+            with torch.cuda.stream(c):
+                c.wait_event(ev_in[s])
+                if ev_out[s] is not None:
+                    c.wait_event(ev_out[s])
+                self._products(F, s)
+                ev_used[s] = torch.cuda.Event()
+                ev_used[s].record(c)
+                self._iterate_synth(sel, proj, coef, lost, s)
+                done = torch.cuda.Event()
+                done.record(c)
             with torch.cuda.stream(d2h):
                 d2h.wait_event(done)
                 hout["selected"].copy_(sel, non_blocking=True)
