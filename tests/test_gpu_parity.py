@@ -459,3 +459,28 @@ def test_separable_dmma_batch_matches_fma_kernel(spec, m, n):
     phi = d.real_values().reshape(K, -1).astype(np.complex128)
     for b in (0, B - 1):
         assert rel_dev(a[b, :K], orc.initial_products(sig[b], w, phi).real) < 1e-13
+
+
+def test_full_config4_properties():
+    """Config 4 at full size (4,096 blocks, K = 8,192, M = 4,096, I = 500):
+    the tcgen05 Ozaki products equal the DMMA products to rounding, the
+    recursion is deterministic, and every output is in range / finite."""
+    from paper_2204_14194_b200 import ExtrapolationPlan
+
+    w4 = wl.WORKLOADS[4]
+    d = w4.dictionary()
+    mask = wl.central_loss_mask(*w4.area, *w4.loss)
+    sig = torch.from_numpy(wl.block_signals(4, w4.n_blocks, *w4.area)).to(DEV)
+    t = build_gram_tables(d, build_weight_field(mask, w4.config.rho_hat), device=DEV)
+    oz = ExtrapolationPlan(d, mask, w4.n_blocks, w4.config, t, device=DEV, products="auto")
+    assert oz._ozaki is not None
+    oz.run(sig)
+    sel_a, coef_a = oz.selected.clone(), oz.coefficients.clone()
+    oz.run(sig)
+    assert torch.equal(oz.selected, sel_a) and torch.equal(oz.coefficients, coef_a)
+    dm = ExtrapolationPlan(d, mask, w4.n_blocks, w4.config, t, device=DEV, products="gemm")
+    dm._products(dm.F.copy_(oz.F))
+    assert rel_dev(oz.R0.cpu().numpy(), dm.R0.cpu().numpy()) < 1e-13
+    s = sel_a.cpu().numpy()
+    assert s.min() >= 0 and s.max() < len(d)
+    assert torch.isfinite(oz.lost).all() and torch.isfinite(oz.coefficients).all()
