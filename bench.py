@@ -339,7 +339,7 @@ def run_gpu(args):
     import torch.distributed as dist
 
     from paper_2204_14194_b200 import ExtrapolationPlan, _native, build_gram_tables, build_weight_field
-    from paper_2204_14194_b200.fast import initial_products_into
+    from paper_2204_14194_b200.fast import gram_into, gram_support
 
     rank, world, local = dist_env()
     cpu = None
@@ -369,6 +369,7 @@ def run_gpu(args):
     gws = torch.empty((int(_native.load().fase_gram_complex_workspace(K, plan.phi.shape[1]))
                        if cplx else K * plan.phi.shape[1] * 8) // 8 + 2,
                       dtype=torch.float64, device=dev)
+    support = None if cplx else gram_support(plan.W, M)
     torch.cuda.synchronize()
     g0 = torch.cuda.Event(enable_timing=True)
     g1 = torch.cuda.Event(enable_timing=True)
@@ -376,8 +377,9 @@ def run_gpu(args):
     if cplx:
         _native.gram_complex(plan.phi, plan.W, K, M, G2, ws=gws)
         _native.gram_finish_complex(G2, K, D2)
+        gram_path = "dmma"
     else:
-        _native.gram(plan.phi, plan.W, K, M, G2, ws=gws)
+        gram_path = gram_into(plan.phi, plan.W, K, M, G2, support)
         _native.gram_finish(G2, K, D2)
     g1.record()
     torch.cuda.synchronize()
@@ -556,6 +558,7 @@ def run_gpu(args):
             "stage_ms": {"init_products": float(np.mean(init_ms)), "iterate": float(np.mean(iter_ms)),
                          "synth": float(np.mean(synth_ms))},
             "gram_ms": gram_ms,
+            "gram_path": gram_path,
             "fft_gram_ms": fft_gram_ms,
             "gram_tflops": (4 if cplx else 1) * K * (K + 1) * M / (gram_ms * 1e-3) / 1e12,
             "gpu_launches": args.steps * (plan.launches_per_run + 1) + args.steps * plan.launches_per_run,

@@ -363,6 +363,13 @@ FASE_API int fase_ozaki_gemm(const int8_t* a_planes, int a_rows_pad, const int32
                              int m_rows, const int8_t* b_planes, int b_rows_pad,
                              const int32_t* eb, int n_rows, int64_t kp, int slices, double* C,
                              int64_t ldc, void* stream);
+/* The weighted Gram table on the same path (build_gram_tables, fast.py:109-142):
+ * planes of Phi o w (A) and Phi (B), K rows each; only tiles holding entries
+ * k <= l are computed, each such entry written to (k, l) and (l, k): G is
+ * bit-symmetric, like fase_gram's. */
+FASE_API int fase_ozaki_gram(const int8_t* a_planes, int a_rows_pad, const int32_t* ea,
+                             const int8_t* b_planes, int b_rows_pad, const int32_t* eb, int K,
+                             int64_t kp, int slices, double* G, int64_t ldg, void* stream);
 
 /* Writes `bytes` of zeros-then-ones into `buf` to evict L2 between timed steps. */
 FASE_API int fase_l2_flush(void* buf, size_t bytes, void* stream);

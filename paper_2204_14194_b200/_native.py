@@ -36,7 +36,7 @@ EXPORTS = (
     "fase_frame_paste", "fase_weigh", "fase_sep_products", "fase_gram_complex_workspace",
     "fase_gram_complex", "fase_max_atoms_complex", "fase_table_ld_complex", "fase_iterate_complex",
     "fase_synth_paste_complex", "fase_sep_products_complex", "fase_fft_gram", "fase_weigh_gather",
-    "fase_ozaki_split", "fase_ozaki_gemm", "fase_sep_products_batch",
+    "fase_ozaki_split", "fase_ozaki_gemm", "fase_ozaki_gram", "fase_sep_products_batch",
 )
 
 _vp = ctypes.c_void_p
@@ -119,6 +119,7 @@ def load():
         "fase_ozaki_split": [_vp, _i64, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp],
         "fase_ozaki_gemm": [_vp, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i64, _i32, _vp, _i64,
                             _vp],
+        "fase_ozaki_gram": [_vp, _i32, _vp, _vp, _i32, _vp, _i32, _i64, _i32, _vp, _i64, _vp],
         "fase_synth_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
                              _i64, _vp],
         "fase_l2_flush": [_vp, ctypes.c_size_t, _vp],
@@ -521,7 +522,9 @@ class OzakiOperand:
         self.rows, self.kd, self.slices = rows, kd, slices
         self.kp = (kd + 63) // 64 * 64
         self.rows_pad = (max(rows, 1) + row_align - 1) // row_align * row_align
-        self.planes = torch.zeros((slices, self.rows_pad, self.kp), dtype=torch.int8, device=device)
+        # every byte of the valid rows is written by split(); the padding rows only
+        # feed output rows that are never stored, so no zero fill is needed
+        self.planes = torch.empty((slices, self.rows_pad, self.kp), dtype=torch.int8, device=device)
         self.exps = torch.zeros(self.rows_pad, dtype=torch.int32, device=device)
 
     def split(self, x, idx=None, w=None) -> "OzakiOperand":
@@ -552,6 +555,19 @@ def ozaki_gemm(a: OzakiOperand, b: OzakiOperand, C) -> None:
     _check(lib.fase_ozaki_gemm(_ptr(a.planes), a.rows_pad, _ptr(a.exps), a.rows,
                                _ptr(b.planes), b.rows_pad, _ptr(b.exps), b.rows, a.kp,
                                a.slices, _ptr(C), _ld(C), _stream(C)))
+
+
+def ozaki_gram(a: "OzakiOperand", b: "OzakiOperand", G) -> None:
+    """Bit-symmetric G = X Y^T (X = Phi o w planes, Y = Phi planes, same K rows)."""
+    import torch
+
+    lib = load()
+    _require(G, "G", torch.float64, 2)
+    if a.kp != b.kp or a.slices != b.slices or a.rows != b.rows:
+        raise errors.ShapeError("Gram operands must share K, the K padding and the plane count")
+    _check(lib.fase_ozaki_gram(_ptr(a.planes), a.rows_pad, _ptr(a.exps), _ptr(b.planes),
+                               b.rows_pad, _ptr(b.exps), a.rows, a.kp, a.slices, _ptr(G), _ld(G),
+                               _stream(G)))
 
 
 def sep_products_batch(factors, F, W, M_rows: int, N_cols: int, R0) -> None:

@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(
     const int8_t* __restrict__ A, int64_t a_plane, const int32_t* __restrict__ ea,
     const int8_t* __restrict__ B, int64_t b_plane, const int32_t* __restrict__ eb, int64_t kp,
     int m_valid, int n_valid, int rows_a_pad, int rows_b_pad, double* __restrict__ C, int64_t ldc,
-    int group_m) {
+    int group_m, int sym) {
   constexpr int A_SLAB = OZ_BM * OZ_BK, B_SLAB = OZ_BN * OZ_BK;
   constexpr int STAGE = S * (A_SLAB + B_SLAB);
   constexpr int TMEM_COLS = 512;
@@ -158,6 +158,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(
   }
   const int m0 = tm * OZ_BM, n0 = tn * OZ_BN;
   const int nk = static_cast<int>(kp / OZ_BK);
+  // symmetric mode (Gram tables): only tiles holding entries r <= c; each such
+  // entry is written to (r, c) and (c, r), so the table is bit-symmetric
+  if (sym && m0 >= n0 + OZ_BN) return;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
@@ -266,7 +269,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int col = n0 + cbase + c0 + j;
-        if (col < n_valid) C[static_cast<int64_t>(row) * ldc + col] = scalbn(sum[j], er + eb[col]);
+        if (col >= n_valid) continue;
+        const double v = scalbn(sum[j], er + eb[col]);
+        if (!sym) {
+          C[static_cast<int64_t>(row) * ldc + col] = v;
+        } else if (row <= col) {
+          C[static_cast<int64_t>(row) * ldc + col] = v;
+          C[static_cast<int64_t>(col) * ldc + row] = v;
+        }
       }
     }
   }
@@ -316,10 +326,28 @@ extern "C" int fase_ozaki_split(const double* x, int64_t ldx, const int32_t* idx
   return check_launch("fase_ozaki_split");
 }
 
+static int ozaki_gemm_impl(const int8_t* a_planes, int a_rows_pad, const int32_t* ea, int m_rows,
+                           const int8_t* b_planes, int b_rows_pad, const int32_t* eb, int n_rows,
+                           int64_t kp, int slices, double* C, int64_t ldc, int sym, void* stream);
+
 extern "C" int fase_ozaki_gemm(const int8_t* a_planes, int a_rows_pad, const int32_t* ea,
                                int m_rows, const int8_t* b_planes, int b_rows_pad,
                                const int32_t* eb, int n_rows, int64_t kp, int slices, double* C,
                                int64_t ldc, void* stream) {
+  return ozaki_gemm_impl(a_planes, a_rows_pad, ea, m_rows, b_planes, b_rows_pad, eb, n_rows, kp,
+                         slices, C, ldc, 0, stream);
+}
+
+extern "C" int fase_ozaki_gram(const int8_t* a_planes, int a_rows_pad, const int32_t* ea,
+                               const int8_t* b_planes, int b_rows_pad, const int32_t* eb, int K,
+                               int64_t kp, int slices, double* G, int64_t ldg, void* stream) {
+  return ozaki_gemm_impl(a_planes, a_rows_pad, ea, K, b_planes, b_rows_pad, eb, K, kp, slices, G,
+                         ldg, 1, stream);
+}
+
+static int ozaki_gemm_impl(const int8_t* a_planes, int a_rows_pad, const int32_t* ea, int m_rows,
+                           const int8_t* b_planes, int b_rows_pad, const int32_t* eb, int n_rows,
+                           int64_t kp, int slices, double* C, int64_t ldc, int sym, void* stream) {
   if (m_rows < 0 || n_rows < 0 || kp < OZ_BK || kp % OZ_BK || slices < 1 ||
       slices > OZ_MAX_SLICES || ldc < n_rows || kp > 16384) {  // int32 headroom, split smem
     set_error("fase_ozaki_gemm: bad sizes (M=%d N=%d kp=%lld slices=%d)", m_rows, n_rows,
@@ -350,7 +378,7 @@ extern "C" int fase_ozaki_gemm(const int8_t* a_planes, int a_rows_pad, const int
     if (group_m < 1) group_m = 1;
     kern<<<nt * mt, OZ_THREADS, smem, as_stream(stream)>>>(a_planes, a_plane, ea, b_planes, b_plane,
                                                             eb, kp, m_rows, n_rows, a_rows_pad,
-                                                            b_rows_pad, C, ldc, group_m);
+                                                            b_rows_pad, C, ldc, group_m, sym);
     return check_launch("fase_ozaki_gemm");
   };
   switch (slices) {

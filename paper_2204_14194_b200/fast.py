@@ -204,6 +204,30 @@ def _device_vector(x: np.ndarray, length: int, device):
     return out
 
 
+def gram_support(w_dev, M: int):
+    """(support indices int32, support weights) of a device weight vector."""
+    torch = _torch()
+    support = torch.nonzero(w_dev[:M] != 0).flatten()
+    return support.to(torch.int32), w_dev.index_select(0, support).contiguous()
+
+
+def gram_into(phi, w_dev, K: int, M: int, G, support=None) -> str:
+    """The real weighted Gram table G = (Phi o w) Phi^T into G (K, ld), exactly
+    symmetric; returns the path used. Large tables go to the tcgen05 Ozaki path
+    over the support samples (digit planes of Phi o w and Phi gathered in one
+    pass each); small ones to the DMMA GEMM. ``support``: gram_support(w_dev, M)
+    when the caller has it (saves a device sync)."""
+    sidx, w_s = support if support is not None else gram_support(w_dev, M)
+    n_s = int(sidx.numel())
+    if K >= 2048 and n_s >= 256:
+        a = _native.OzakiOperand(K, n_s, 128, G.device).split(phi, sidx, w_s)
+        b = _native.OzakiOperand(K, n_s, 64, G.device).split(phi, sidx)
+        _native.ozaki_gram(a, b, G)
+        return "ozaki"
+    _native.gram(phi, w_dev, K, M, G)
+    return "dmma"
+
+
 def _gram_on_device(phi, w_dev, K: int, M: int, device, complex_rows: bool = False):
     """Real (K, table_ld) table, or complex (K, table_ld_complex) rows of conj(C)
     from the conjugate-split matrix of a complex dictionary."""
@@ -213,7 +237,7 @@ def _gram_on_device(phi, w_dev, K: int, M: int, device, complex_rows: bool = Fal
         _native.gram_complex(phi, w_dev, K, M, T)
         return T
     G = torch.zeros((K, _native.table_ld(K)), dtype=torch.float64, device=device)
-    _native.gram(phi, w_dev, K, M, G)
+    gram_into(phi, w_dev, K, M, G)
     return G
 
 
