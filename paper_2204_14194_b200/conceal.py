@@ -141,13 +141,15 @@ class FrameEngine:
         self.base_w = torch.from_numpy(flat_base.copy()).to(dev)
         self._buf = {}
 
-    def _buffers(self, L: int):
+    def _buffers(self, L: int, slot: int = 0):
         import torch
 
-        if L not in self._buf:
+        key = (L, slot)
+        if key not in self._buf:
             dev, K, I = self.device, self.K, self.config.iterations
             ldx = self.M + (self.M & 1)
-            self._buf = {L: dict(
+            self._buf = {k: v for k, v in self._buf.items() if k[0] == L}  # one batch size kept
+            self._buf[key] = dict(
                 X=torch.empty((L, ldx), dtype=torch.float64, device=dev),
                 R0=torch.empty((L, K + (K & 1)), dtype=torch.float64, device=dev),
                 D=torch.empty((L, self.G0.shape[1]), dtype=torch.float64, device=dev),
@@ -157,12 +159,12 @@ class FrameEngine:
                 sel=torch.empty((L, I), dtype=torch.int32, device=dev),
                 proj=torch.empty((L, I), dtype=torch.float64, device=dev),
                 coef=torch.empty((L, I), dtype=torch.float64, device=dev),
-            )}
+            )
             from .fast import ozaki_worthwhile
 
             if self._oz_phi is not None and ozaki_worthwhile(L, K):
-                self._buf[L]["oz"] = _native.OzakiOperand(L, self.M, 128, dev)
-        return self._buf[L]
+                self._buf[key]["oz"] = _native.OzakiOperand(L, self.M, 128, dev)
+        return self._buf[key]
 
     @property
     def launches_per_frame(self) -> int:
@@ -173,17 +175,18 @@ class FrameEngine:
             return 5 + (1 if len(factors) <= 8 else len(factors))
         return 5 + (2 if any("oz" in b for b in self._buf.values()) else 1)
 
-    def run(self, frame, grid, corners, out=None) -> BatchResult:
+    def run(self, frame, grid, corners, out=None, slot: int = 0) -> BatchResult:
         """Conceal one frame: ``frame`` (H, W) float64, ``grid`` (H/tile, W/tile)
         uint8 tile loss map, ``corners`` (L, 2) int32 lossy-tile corners, all on
         the device. The restored frame is written to ``out`` (default: a copy of
-        ``frame``). Enqueued on the current stream; no host synchronization."""
+        ``frame``). Enqueued on the current stream; no host synchronization.
+        ``slot`` picks one of two work-buffer sets (two frames in flight)."""
         L = int(corners.shape[0])
         if out is None:
             out = frame.clone()
         if L == 0:
             return BatchResult(selected=None, projections=None, coefficients=None, patched=out)
-        b = self._buffers(L)
+        b = self._buffers(L, slot)
         cfg, K = self.config, self.K
         _native.frame_areas(frame, grid, self.tile, self.support, corners, self.base_w, b["X"])
         _native.frame_cells(grid, self.H, self.W, self.tile, self.support, corners, self.cell_rep,
@@ -208,6 +211,62 @@ class FrameEngine:
         return BatchResult(selected=b["sel"], projections=b["proj"], coefficients=b["coef"],
                            patched=out, dictionary=self.dictionary,
                            shape=(self.A, self.A))
+
+    def run_host_stream(self, frames_u8, outs, grid, corners, lost):
+        """End to end over a sequence of frames with one loss pattern: pinned
+        uint8 frames in, restored float64 frames (pinned) out. Frames alternate
+        between two compute streams with their own buffers; uploads and
+        read-backs run on their own streams, overlapped with the neighbouring
+        frames' kernels. ``grid`` / ``corners`` / ``lost`` (H x W bool) live on
+        the device. Enqueued; the caller's stream waits for the last read-back."""
+        import torch
+
+        dev = self.device
+        cs = torch.cuda.current_stream(dev)
+        H, W = self.H, self.W
+        if not hasattr(self, "_pipe"):
+            self._pipe = {"h2d": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev),
+                          "comp": [torch.cuda.Stream(dev), torch.cuda.Stream(dev)],
+                          "u8": [torch.empty((H, W), dtype=torch.uint8, device=dev) for _ in range(2)],
+                          "f64": [torch.empty((H, W), dtype=torch.float64, device=dev)
+                                  for _ in range(2)]}
+        p = self._pipe
+        start = torch.cuda.Event()
+        start.record(cs)
+        for st in (p["h2d"], p["d2h"], *p["comp"]):
+            st.wait_event(start)
+        ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_used = [None, None]
+        ev_out = [None, None]
+        for i, (hin, hout) in enumerate(zip(frames_u8, outs)):
+            s = i % 2
+            with torch.cuda.stream(p["h2d"]):
+                if ev_used[s] is not None:
+                    p["h2d"].wait_event(ev_used[s])
+                p["u8"][s].copy_(hin, non_blocking=True)
+                ev_in[s].record(p["h2d"])
+            c = p["comp"][s]
+            with torch.cuda.stream(c):
+                c.wait_event(ev_in[s])
+                if ev_out[s] is not None:
+                    c.wait_event(ev_out[s])
+                f64 = p["f64"][s]
+                f64.copy_(p["u8"][s])
+                f64.masked_fill_(lost, 0.0)
+                ev_used[s] = torch.cuda.Event()
+                ev_used[s].record(c)
+                self.run(f64, grid, corners, out=f64, slot=s)
+                done = torch.cuda.Event()
+                done.record(c)
+            with torch.cuda.stream(p["d2h"]):
+                p["d2h"].wait_event(done)
+                hout.copy_(p["f64"][s], non_blocking=True)
+                ev_out[s] = torch.cuda.Event()
+                ev_out[s].record(p["d2h"])
+        for e in ev_out:
+            if e is not None:
+                cs.wait_event(e)
+        return outs
 
     def dead_blocks(self) -> int:
         """Blocks of the last run whose every atom was degenerate (syncs)."""
