@@ -299,7 +299,14 @@ __global__ void __launch_bounds__(288) sep_products_dmma_kernel(
       }
     }
   }
-  for (int p = 0; p < parts.n; ++p) {
+  // small batches split the work over gridDim.y CTAs per block: part p =
+  // y / splits, and a slice of 16-row groups of u for product 2 (T is formed by
+  // every slice of the part)
+  const int splits = gridDim.y > 1 ? static_cast<int>(gridDim.y) / parts.n : 1;
+  const int p_first = gridDim.y > 1 ? static_cast<int>(blockIdx.y) / splits : 0;
+  const int p_last = gridDim.y > 1 ? p_first + 1 : parts.n;
+  const int slice = gridDim.y > 1 ? static_cast<int>(blockIdx.y) % splits : 0;
+  for (int p = p_first; p < p_last; ++p) {
     const double* rows = parts.rows[p];
     const double* cols = parts.cols[p];
     const int Lr = parts.lr[p], Lc = parts.lc[p];
@@ -330,10 +337,12 @@ __global__ void __launch_bounds__(288) sep_products_dmma_kernel(
     {
       auto fa = [&](int u, int m) { return (u < Lr && m < Mr) ? __ldg(rows + u * Mr + m) : 0.0; };
       auto fb = [&](int v, int m) { return sT[v * st + m]; };
-      const int tm = Lrp / 16, tn = Lcp / 16;
+      const int tm_all = Lrp / 16, tn = Lcp / 16;
+      const int per = (tm_all + splits - 1) / splits;  // 16-row groups of u per slice
+      const int tm_lo = slice * per, tm = max(0, min(tm_all, tm_lo + per) - tm_lo);
       double* out = R0 + static_cast<int64_t>(b) * ldr + parts.col0[p];
       for (int t = warp; t < tm * tn; t += nwarps) {
-        const int r0 = (t / tn) * 16, c0 = (t % tn) * 16;
+        const int r0 = (tm_lo + t / tn) * 16, c0 = (t % tn) * 16;
         double acc[2][2][2];
         macro_nt(fa, fb, r0, c0, Mk, acc);
 #pragma unroll
@@ -513,6 +522,15 @@ extern "C" int fase_sep_products_batch(const fase_sep_part* parts, int n_parts, 
     set_error("fase_sep_products_batch: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return FASE_ERR_CUDA;
   }
-  sep_products_dmma_kernel<<<B, 288, smem, as_stream(stream)>>>(a, Mr, Nc, F, ldf, W, ldw, R0, ldr);
+  // batches smaller than the GPU: one CTA per (block, part, slice of u)
+  int splits = 1;
+  if (B < 148) {
+    const int lr_min_groups = (parts[0].Lr + 15) / 16;
+    splits = lr_min_groups < 4 ? lr_min_groups : 4;
+    if (splits < 1) splits = 1;
+  }
+  const dim3 grid(B, B < 148 ? n_parts * splits : 1);
+  sep_products_dmma_kernel<<<grid, 288, smem, as_stream(stream)>>>(a, Mr, Nc, F, ldf, W, ldw, R0,
+                                                                     ldr);
   return check_launch("fase_sep_products_batch");
 }
