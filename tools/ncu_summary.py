@@ -72,6 +72,7 @@ def short(name: str) -> str:
     for key in ("fase_iterate_complex_kernel", "fase_iterate_kernel", "dgemm_nt_kernel",
                 "synth_paste_complex_kernel", "synth_paste_kernel", "gram_finish_kernel",
                 "weigh_gather_kernel", "weigh_kernel", "sep_products_complex_kernel",
+                "sep_products_dmma_kernel",
                 "sep_products_kernel", "ozaki_gemm_kernel", "ozaki_split_kernel",
                 "block_normalizers_kernel", "basis_outer_kernel", "flush_kernel",
                 "frame_areas_kernel", "frame_cells_kernel", "frame_paste_kernel"):
