@@ -273,3 +273,26 @@ def test_complex_large_k_variant():
 
         _check_block(res.selected[b].cpu().numpy(), res.coefficients[b].cpu().numpy(),
                      ref["selected"], ref["coefficients"], metric_at)
+
+
+@pytest.mark.parametrize("copies", [3, 70])
+def test_many_exact_ties_lowest_index(copies):
+    """Atoms repeated `copies` times tie exactly in every metric: the lowest
+    index must win (reference.py:58-73). 70 copies overflow the complex
+    kernel's 64-entry candidate list and take its exact fallback pass; the
+    real kernel sees the same ties in its tie pass."""
+    rng = np.random.default_rng(copies)
+    for cplx in (True, False):
+        base = parse_dict_spec("dft" if cplx else "dct", 6, 6).values[:12]
+        if not cplx:
+            base = base.real
+        vals = np.concatenate([np.repeat(base[:1], copies, axis=0), base[1:]])
+        d = Dictionary(vals)
+        mask = wl.central_loss_mask(6, 6, 2, 2)
+        sig = rng.uniform(0, 255, (3, 6, 6))
+        res = fase_extrapolate_batch(sig, mask, d, None, ExtrapConfig(15, 0.5, 0.8), device=DEV)
+        for b in range(3):
+            ref = orc.extrapolate_block(sig[b], mask, d.values, 0.5, 15, 0.8)
+            got = res.selected[b].cpu().numpy()
+            assert np.array_equal(got, ref["selected"]), (cplx, b, got, ref["selected"])
+            assert got.min() >= 0 and not np.any((got > 0) & (got < copies))  # only the first copy
