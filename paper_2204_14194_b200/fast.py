@@ -588,9 +588,19 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
     vdt = torch.complex128 if cplx else torch.float64
     if products is None:
         R0 = torch.empty((B, ldr), dtype=vdt, device=dev)
-        ws = torch.empty(max(_native.init_products_workspace(M, B) // 8, 2), dtype=torch.float64,
-                         device=dev)
-        initial_products_into(dictionary, F, W, R0, ws)
+        dense = not (dictionary.device_cfactors(dev) if cplx else dictionary.device_factors(dev))
+        rows = phi.shape[0]
+        if shared and dense and ozaki_worthwhile(B, rows):
+            # large dense batches: support samples only, on the tcgen05 Ozaki path
+            sidx, w_s = gram_support(W, M)
+            n_s = int(sidx.numel())
+            a = _native.OzakiOperand(B, n_s, 128, dev).split(F, sidx, w_s)
+            b = _native.OzakiOperand(rows, n_s, 64, dev).split(phi, sidx)
+            _native.ozaki_gemm(a, b, _real_view(R0) if cplx else R0)
+        else:
+            ws = torch.empty(max(_native.init_products_workspace(M, B) // 8, 2),
+                             dtype=torch.float64, device=dev)
+            initial_products_into(dictionary, F, W, R0, ws)
     else:
         R0 = _products_on_device(products, B, K, ldr, dev, cplx)
     sel = torch.empty((B, I), dtype=torch.int32, device=dev)

@@ -241,3 +241,27 @@ def test_plan_ozaki_products(spec):
         v = compare_selection(plan.selected[b].cpu().numpy(), ref["selected"],
                               metric_fn(ref["r0"], ref["d"], ref["log"]))
         assert v.ok
+
+
+def test_batch_api_uses_ozaki_for_large_dense_batches():
+    """fase_extrapolate_batch on a batch that fills the GPU with a dense
+    dictionary takes the tcgen05 products (support samples only): R0 and the
+    selections still match the oracle."""
+    from paper_2204_14194_b200 import fase_extrapolate_batch
+    from parity import compare_selection, metric_fn
+
+    d = parse_dict_spec("gauss:2560:4", 16, 16)
+    mask = wl.central_loss_mask(16, 16, 6, 6)
+    cfg = ExtrapConfig(20, 0.5, 0.8)
+    sig = np.random.default_rng(12).uniform(0, 255, (2048, 16, 16))
+    from paper_2204_14194_b200.fast import ozaki_worthwhile
+
+    assert ozaki_worthwhile(2048, len(d))
+    res = fase_extrapolate_batch(sig, mask, d, None, cfg, record_products=True, device=DEV)
+    vals = d.values
+    for b in (0, 1000, 2047):
+        ref = orc.extrapolate_block(sig[b], mask, vals, 0.5, 20, 0.8, record=True)
+        v = compare_selection(res.selected[b].cpu().numpy(), ref["selected"],
+                              metric_fn(ref["r0"], ref["d"], ref["log"]))
+        assert v.ok
+        assert rel_dev(res.coefficients[b].cpu().numpy()[: v.stop], ref["coefficients"].real[: v.stop]) < 1e-9
