@@ -61,31 +61,55 @@ constexpr unsigned kNone = 0xffffffffu;
 // registers per thread so three 256-thread CTAs fit per SM (more blocks in
 // flight to hide latency) at the cost of one extra 16-byte shared load per
 // element pair and iteration.
-template <int NT, int EPT, int MINB, bool kDsmem, bool kChunked, bool kRecord>
-__global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_iterate_args a) {
+//
+// NB == 2 (shared D only): one CTA runs two blocks, each on its own NT-thread
+// half with its own staged row, barriers (named, per half) and slots, while
+// the normalizers -- identical for every block of a shared geometry -- are
+// kept once in shared memory for both. For large K this doubles the blocks in
+// flight per SM (two staged rows + one D fit where two CTAs' D + rows do not).
+template <int NT, int EPT, int MINB, bool kDsmem, bool kChunked, bool kRecord, int NB>
+__global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_iterate_args a) {
   constexpr int EP = EPT / 2;
   constexpr int NW = NT / 32;
+  static_assert(NB == 1 || (kDsmem && !kChunked), "paired blocks share one D in shared memory");
 
-  __shared__ long long s_key[NW];
-  __shared__ unsigned s_arg[NW];
-  __shared__ unsigned s_u[NW];
-  __shared__ double s_r[NW];
-  __shared__ double s_d[NW];
-  __shared__ __align__(16) double s_dump[NW][kDsmem ? 1 : 2][EPT];  // tie-pass winner's registers
+  __shared__ long long s_key_all[NB][NW];
+  __shared__ unsigned s_arg_all[NB][NW];
+  __shared__ unsigned s_u_all[NB][NW];
+  __shared__ double s_r_all[NB][NW];
+  __shared__ double s_d_all[NB][NW];
+  __shared__ __align__(16) double s_dump_all[NB][NW][kDsmem ? 1 : 2][EPT];  // tie-pass winner's registers
   // The staged row arrives in kSeg segments, each on its own mbarrier, so the
   // update can start on the first segment while the rest is still in flight.
   constexpr int kSeg = EP < 3 ? EP : 3;
-  __shared__ __align__(8) uint64_t s_bar[kSeg];
+  __shared__ __align__(8) uint64_t s_bar_all[NB][kSeg];
   extern __shared__ double2 s_dyn[];
-  double2* s_row = s_dyn;            // staged row: pair p at s_row[p]
-  double2* s_D = s_dyn + EP * NT;    // kDsmem: normalizer pairs, same indexing
 
-  const int b = blockIdx.x;
-  const int t = threadIdx.x;
+  const int half = NB == 1 ? 0 : static_cast<int>(threadIdx.x) / NT;
+  long long* s_key = s_key_all[half];
+  unsigned* s_arg = s_arg_all[half];
+  unsigned* s_u = s_u_all[half];
+  double* s_r = s_r_all[half];
+  double* s_d = s_d_all[half];
+  auto s_dump = s_dump_all[half];
+  uint64_t* s_bar = s_bar_all[half];
+  double2* s_row = s_dyn + half * EP * NT;  // staged row: pair p at s_row[p]
+  double2* s_D = s_dyn + NB * EP * NT;      // kDsmem: normalizer pairs, same indexing
+
+  const int b = static_cast<int>(blockIdx.x) * NB + half;
+  const int t = static_cast<int>(threadIdx.x) - half * NT;
   const int lane = t & 31;
   const int warp = t >> 5;
   const int K = a.K;
   const double kDead = __longlong_as_double(static_cast<long long>(0xfff0000000000000ULL));
+  const bool active = NB == 1 || b < a.B;
+  // the per-iteration barrier: the whole CTA, or this block's half
+  auto block_sync = [&]() {
+    if constexpr (NB == 1)
+      __syncthreads();
+    else
+      asm volatile("bar.sync %0, %1;\n" ::"r"(1 + half), "r"(NT) : "memory");
+  };
 
   if (t == 0) {
     for (int sg = 0; sg < kSeg; ++sg) mbar_init(&s_bar[sg], 1);
@@ -93,7 +117,7 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
   }
 
   const double* D = a.D + (a.ldd ? static_cast<int64_t>(b) * a.ldd : 0);
-  const double* R0 = a.R0 + static_cast<int64_t>(b) * a.ldr;
+  const double* R0 = a.R0 + static_cast<int64_t>(active ? b : 0) * a.ldr;
   const int32_t* cids = nullptr;
   int nch = 0;
   if (kChunked) {
@@ -123,7 +147,7 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
     dd.x = dd.x != 0.0 ? dd.x : kDead;
     dd.y = dd.y != 0.0 ? dd.y : kDead;
     if constexpr (kDsmem) {
-      s_D[j * NT + t] = dd;
+      if (half == 0) s_D[j * NT + t] = dd;
     } else {
       dreg[j][0] = dd.x;
       dreg[j][1] = dd.y;
@@ -138,6 +162,11 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
       best = m1;
       barg = static_cast<unsigned>(k + 1);
     }
+  }
+
+  if constexpr (NB > 1) {
+    __syncthreads();  // the shared D (written by half 0) is complete
+    if (!active) return;
   }
 
   int32_t* sel = a.sel + static_cast<int64_t>(b) * a.ldo;
@@ -160,7 +189,7 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
         s_arg[warp] = wa;
       }
     }
-    __syncthreads();
+    block_sync();
     // ---- block max: every warp reduces the NW slots in parallel (lane l reads slot l)
     long long top_key;
     unsigned guess;
@@ -236,7 +265,7 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_kernel(const fase_itera
         s_d[warp] = s_dump[warp][kDsmem ? 0 : 1][2 * jj + ee];
       }
     }
-    __syncthreads();
+    block_sync();
     unsigned u;
     int uw;
     {
@@ -349,15 +378,16 @@ struct Variant {
   KernelFn plain;    // shared geometry
   KernelFn chunked;  // per-block geometry (chunk-corrected rows)
   KernelFn record;   // shared geometry, R logged after every iteration
+  int nb = 1;        // blocks per CTA (2: paired blocks sharing one D)
 };
 
 #define FASE_V(NT, EPT, MINB, DS)                                                       \
   {NT,                                                                                   \
    EPT,                                                                                  \
    DS,                                                                                   \
-   fase_iterate_kernel<NT, EPT, MINB, DS, false, false>,                                 \
-   fase_iterate_kernel<NT, EPT, MINB, DS, true, false>,                                  \
-   fase_iterate_kernel<NT, EPT, MINB, DS, false, true>}
+   fase_iterate_kernel<NT, EPT, MINB, DS, false, false, 1>,                              \
+   fase_iterate_kernel<NT, EPT, MINB, DS, true, false, 1>,                               \
+   fase_iterate_kernel<NT, EPT, MINB, DS, false, true, 1>}
 // Ordered by capacity NT*EPT; the first variant that holds K is used.
 // 128/256-thread variants keep D in shared memory (3-6 CTAs per SM); the
 // 512-thread variants keep R and D in registers (4 registers per atom), which
@@ -369,6 +399,17 @@ const Variant kVariants[] = {
     FASE_V(256, 20, 2, true),  FASE_V(512, 12, 1, false), FASE_V(512, 16, 1, false),
     FASE_V(512, 20, 1, false), FASE_V(512, 24, 1, false),
 };
+
+// Paired blocks for large shared-geometry tables (same capacity as the default
+// variant, so the same table layout): one 512-thread CTA runs two blocks that
+// share D in shared memory -- two blocks in flight per SM where one 512-thread
+// CTA with D in registers fits only one.
+#define FASE_VP(NT, EPT)                                                              \
+  {NT, EPT, true, fase_iterate_kernel<NT, EPT, 1, true, false, false, 2>, nullptr, nullptr, 2}
+const Variant kPairVariants[] = {
+    FASE_VP(256, 20), FASE_VP(256, 24), FASE_VP(256, 32),
+};
+#undef FASE_VP
 
 // Alternative shapes, selectable for measurement with FASE_ITERATE_VARIANT=NTxEPT
 // (must not exceed the default variant's capacity, which sizes the tables).
@@ -455,8 +496,15 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
               v->nt * v->ept, static_cast<long long>(a.ldg));
     return FASE_ERR_SHAPE;
   }
+  if (!a.chunk_count && !a.R_log && a.ldd == 0) {
+    const char* env = getenv("FASE_ITERATE_PAIR");
+    if (!env || atoi(env) != 0)
+      for (const Variant& pv : kPairVariants)
+        if (pv.nt * pv.ept == v->nt * v->ept) v = &pv;
+  }
   KernelFn fn = a.chunk_count ? v->chunked : (a.R_log ? v->record : v->plain);
-  const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2) * (v->dsmem ? 2 : 1);
+  const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2) *
+                      (v->nb + (v->dsmem ? 1 : 0));
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e == cudaSuccess)  // several CTAs per SM need the full shared-memory carveout
@@ -465,6 +513,6 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
     set_error("fase_iterate: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return FASE_ERR_CUDA;
   }
-  fn<<<a.B, v->nt, smem, as_stream(stream)>>>(a);
+  fn<<<(a.B + v->nb - 1) / v->nb, v->nt * v->nb, smem, as_stream(stream)>>>(a);
   return check_launch("fase_iterate");
 }

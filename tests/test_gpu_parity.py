@@ -484,3 +484,24 @@ def test_full_config4_properties():
     s = sel_a.cpu().numpy()
     assert s.min() >= 0 and s.max() < len(d)
     assert torch.isfinite(oz.lost).all() and torch.isfinite(oz.coefficients).all()
+
+
+@pytest.mark.parametrize("spec", ["gauss:5000:1", "gauss:8192:2"])
+def test_recursion_bit_exact_paired_blocks(spec):
+    """Large-K shared geometry runs two blocks per CTA sharing D (paired
+    variant; an odd batch leaves the last CTA half idle): given the oracle's
+    tables and initial products the run is bit-identical to the oracle."""
+    d = parse_dict_spec(spec, 16, 16)
+    mask = wl.central_loss_mask(16, 16, 6, 6)
+    cfg = ExtrapConfig(25, 0.5, 0.8)
+    tables, (c, dd) = host_tables(d, mask, cfg.rho_hat)
+    sig = np.random.default_rng(5).uniform(0, 255, (3, 16, 16))
+    w = orc.weight_field(mask, cfg.rho_hat)
+    vals = d.real_values().reshape(len(d), -1).astype(np.complex128)
+    r0 = np.stack([orc.initial_products(sig[b], w, vals) for b in range(3)])
+    res = fase_extrapolate_batch(sig, mask, d, tables, cfg, products=r0.real, device=DEV)
+    for b in range(3):
+        sel, proj, coef, _ = orc.fase_run(r0[b], c, dd, cfg.gamma, cfg.iterations)
+        assert np.array_equal(res.selected[b].cpu().numpy(), sel)
+        assert np.array_equal(res.coefficients[b].cpu().numpy(), coef.real)
+        assert np.array_equal(res.projections[b].cpu().numpy(), proj.real)
