@@ -407,7 +407,7 @@ const Variant kVariants[] = {
 #define FASE_VP(NT, EPT)                                                              \
   {NT, EPT, true, fase_iterate_kernel<NT, EPT, 1, true, false, false, 2>, nullptr, nullptr, 2}
 const Variant kPairVariants[] = {
-    FASE_VP(256, 20), FASE_VP(256, 24), FASE_VP(256, 32),
+    FASE_VP(256, 20), FASE_VP(256, 24), FASE_VP(256, 32), FASE_VP(512, 16),
 };
 #undef FASE_VP
 
@@ -497,10 +497,12 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
     return FASE_ERR_SHAPE;
   }
   if (!a.chunk_count && !a.R_log && a.ldd == 0) {
+    // FASE_ITERATE_PAIR: 0 disables pairing, NT picks the half size (measurement)
     const char* env = getenv("FASE_ITERATE_PAIR");
-    if (!env || atoi(env) != 0)
+    const int want = env ? atoi(env) : 256;
+    if (want != 0)
       for (const Variant& pv : kPairVariants)
-        if (pv.nt * pv.ept == v->nt * v->ept) v = &pv;
+        if (pv.nt * pv.ept == v->nt * v->ept && pv.nt == want) v = &pv;
   }
   KernelFn fn = a.chunk_count ? v->chunked : (a.R_log ? v->record : v->plain);
   const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2) *
