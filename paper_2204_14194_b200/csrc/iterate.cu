@@ -225,6 +225,17 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         mbar_arrive_expect_tx(&s_bar[sg], bytes);
         tma_load_1d(s_row + j0 * NT, grow + 2 * j0 * NT, bytes, &s_bar[sg]);
       }
+      if constexpr (kChunked) {
+        // the guess's chunk-table rows are read right after the second
+        // barrier: pull them into L2 now (one bulk prefetch per row)
+        for (int ch = 0; ch < nch; ++ch) {
+          const double* crow = a.chunk_tables + static_cast<int64_t>(cids[ch]) * a.chunk_stride +
+                               static_cast<int64_t>(guess) * ldg;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(crow),
+                       "r"(static_cast<unsigned>(EP * NT * sizeof(double2)))
+                       : "memory");
+        }
+      }
     }
     const double top = __longlong_as_double(top_key);
     // tie_quantum: only a finite, strictly positive top moves the ratchet
