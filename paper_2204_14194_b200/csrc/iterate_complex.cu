@@ -46,29 +46,50 @@ namespace {
 constexpr unsigned kNone = 0xffffffffu;
 constexpr int kCap = 64;  // candidate list capacity
 
-template <int NT, int EP, int MINB, bool kDsmem, bool kChunked, bool kRecord>
-__global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fase_iterate_args a) {
+// NB == 2 (shared geometry, D^2 in shared memory): one CTA runs two blocks on
+// its two NT-thread halves (own staged row, candidate list, named barriers)
+// that share one copy of D^2, as in the real kernel's paired variants.
+template <int NT, int EP, int MINB, bool kDsmem, bool kChunked, bool kRecord, int NB>
+__global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(const fase_iterate_args a) {
   constexpr int NW = NT / 32;
   constexpr int kSeg = EP < 3 ? EP : 3;
+  static_assert(NB == 1 || (kDsmem && !kChunked), "paired blocks share one D^2 in shared memory");
 
-  __shared__ long long s_key[NW];
-  __shared__ unsigned s_arg[NW];
-  __shared__ int s_cnt[2];
-  __shared__ double s_cm[kCap];            // candidate exact metric
-  __shared__ unsigned s_ck[kCap];          // candidate index
-  __shared__ __align__(16) double2 s_cr[kCap];  // candidate R
-  __shared__ double s_cd[kCap];            // candidate D
-  __shared__ __align__(8) uint64_t s_bar[kSeg];
+  __shared__ long long s_key_all[NB][NW];
+  __shared__ unsigned s_arg_all[NB][NW];
+  __shared__ int s_cnt_all[NB][2];
+  __shared__ double s_cm_all[NB][kCap];            // candidate exact metric
+  __shared__ unsigned s_ck_all[NB][kCap];          // candidate index
+  __shared__ __align__(16) double2 s_cr_all[NB][kCap];  // candidate R
+  __shared__ double s_cd_all[NB][kCap];            // candidate D
+  __shared__ __align__(8) uint64_t s_bar_all[NB][kSeg];
   extern __shared__ double2 s_dyn[];
-  double2* s_row = s_dyn;          // staged row: element j*NT + t
-  double* s_D2 = reinterpret_cast<double*>(s_dyn + EP * NT);  // kDsmem: D^2 per element
 
-  const int b = blockIdx.x;
-  const int t = threadIdx.x;
+  const int half = NB == 1 ? 0 : static_cast<int>(threadIdx.x) / NT;
+  long long* s_key = s_key_all[half];
+  unsigned* s_arg = s_arg_all[half];
+  int* s_cnt = s_cnt_all[half];
+  double* s_cm = s_cm_all[half];
+  unsigned* s_ck = s_ck_all[half];
+  double2* s_cr = s_cr_all[half];
+  double* s_cd = s_cd_all[half];
+  uint64_t* s_bar = s_bar_all[half];
+  double2* s_row = s_dyn + half * EP * NT;  // staged row: element j*NT + t
+  double* s_D2 = reinterpret_cast<double*>(s_dyn + NB * EP * NT);  // kDsmem: D^2 per element
+
+  const int b = static_cast<int>(blockIdx.x) * NB + half;
+  const int t = static_cast<int>(threadIdx.x) - half * NT;
   const int lane = t & 31;
   const int warp = t >> 5;
   const int K = a.K;
   const double kDead = __longlong_as_double(static_cast<long long>(0xfff0000000000000ULL));
+  const bool active = NB == 1 || b < a.B;
+  auto block_sync = [&]() {  // the whole CTA, or this block's half
+    if constexpr (NB == 1)
+      __syncthreads();
+    else
+      asm volatile("bar.sync %0, %1;\n" ::"r"(1 + half), "r"(NT) : "memory");
+  };
 
   if (t == 0) {
     for (int sg = 0; sg < kSeg; ++sg) mbar_init(&s_bar[sg], 1);
@@ -78,7 +99,7 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
   }
 
   const double* D = a.D + (a.ldd ? static_cast<int64_t>(b) * a.ldd : 0);
-  const double* R0 = a.R0 + 2 * static_cast<int64_t>(b) * a.ldr;
+  const double* R0 = a.R0 + 2 * static_cast<int64_t>(active ? b : 0) * a.ldr;
   const int32_t* cids = nullptr;
   int nch = 0;
   if (kChunked) {
@@ -113,15 +134,19 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
     r[j][1] = k < K ? R0[2 * k + 1] : 0.0;
     const double dk = k < K ? D[k] : 0.0;
     const double dsq = dk != 0.0 ? mul_rn(dk, dk) : kDead;
-    if constexpr (kDsmem)
-      s_D2[j * NT + t] = dsq;
-    else
+    if constexpr (kDsmem) {
+      if (half == 0) s_D2[j * NT + t] = dsq;
+    } else
       dreg[j] = dsq;
     const double pk = proxy(r[j][0], r[j][1], dsq);
     if (pk > best) {
       best = pk;
       barg = static_cast<unsigned>(k);
     }
+  }
+  if constexpr (NB > 1) {
+    __syncthreads();  // the shared D^2 (written by half 0) is complete
+    if (!active) return;
   }
 
   int32_t* sel = a.sel + static_cast<int64_t>(b) * a.ldo;
@@ -144,7 +169,7 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
         s_arg[warp] = wa;
       }
     }
-    __syncthreads();
+    block_sync();
     if (t == 0) s_cnt[(it + 1) & 1] = 0;  // next iteration's list (last read before this barrier)
     long long top_key, wkey;
     unsigned guess;
@@ -204,7 +229,7 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
         }
       }
     }
-    __syncthreads();
+    block_sync();
     const int cnt = s_cnt[it & 1];
 
     unsigned u;
@@ -277,7 +302,7 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
       }
       const long long wk = warp_max_i64(__double_as_longlong(mb));
       if (lane == 0) s_key[warp] = wk;
-      __syncthreads();
+      block_sync();
       long long tk = LLONG_MIN;
 #pragma unroll
       for (int w = 0; w < NW; ++w) tk = s_key[w] > tk ? s_key[w] : tk;
@@ -305,7 +330,7 @@ __global__ void __launch_bounds__(NT, MINB) fase_iterate_complex_kernel(const fa
         s_cr[warp] = rv;
         s_cd[warp] = dv;
       }
-      __syncthreads();
+      block_sync();
       const unsigned su = lane < NW ? s_ck[lane] : kNone;
       u = __reduce_min_sync(0xffffffffu, su);
       const int uw = __ffs(__ballot_sync(0xffffffffu, su == u)) - 1;
@@ -409,15 +434,16 @@ struct Variant {
   KernelFn plain;
   KernelFn chunked;
   KernelFn record;
+  int nb = 1;  // blocks per CTA (2: paired blocks sharing D^2)
 };
 
 #define FASE_CV(NT, EP, MINB, DS)                                      \
   {NT,                                                                  \
    EP,                                                                  \
    DS,                                                                  \
-   fase_iterate_complex_kernel<NT, EP, MINB, DS, false, false>,         \
-   fase_iterate_complex_kernel<NT, EP, MINB, DS, true, false>,          \
-   fase_iterate_complex_kernel<NT, EP, MINB, DS, false, true>}
+   fase_iterate_complex_kernel<NT, EP, MINB, DS, false, false, 1>,         \
+   fase_iterate_complex_kernel<NT, EP, MINB, DS, true, false, 1>,          \
+   fase_iterate_complex_kernel<NT, EP, MINB, DS, false, true, 1>}
 // Ordered by capacity NT*EP (complex elements); the first that holds K is used.
 // The exact metric uses call-free division / square root (np_cabs_fast), so
 // the 256-thread shapes fit three CTAs per SM like the real kernel (the IEEE
@@ -430,6 +456,14 @@ const Variant kVariants[] = {
     FASE_CV(256, 10, 2, true), FASE_CV(512, 6, 1, true),  FASE_CV(512, 8, 1, true),
     FASE_CV(512, 9, 1, true),  FASE_CV(512, 10, 1, true), FASE_CV(512, 12, 1, true),
 };
+// Paired blocks for shared geometries, same capacity as the 512-thread default
+// (so the same table layout): two blocks in flight per SM instead of one.
+#define FASE_CVP(NT, EP)                                                                   \
+  {NT, EP, true, fase_iterate_complex_kernel<NT, EP, 1, true, false, false, 2>, nullptr, nullptr, 2}
+const Variant kPairVariants[] = {
+    FASE_CVP(256, 12), FASE_CVP(256, 16), FASE_CVP(256, 18), FASE_CVP(256, 20),
+};
+#undef FASE_CVP
 // Alternative residency for measurement (FASE_ITERATE_COMPLEX_VARIANT=NTxEPxMINB;
 // same capacity as the default variant for K).
 struct ExtraVariant {
@@ -515,8 +549,16 @@ extern "C" int fase_iterate_complex(const fase_iterate_args* args, void* stream)
               "(ldg=%lld)", v->nt * v->ep, static_cast<long long>(a.ldg));
     return FASE_ERR_SHAPE;
   }
+  if (!a.chunk_count && !a.R_log && a.ldd == 0) {
+    // FASE_ITERATE_PAIR: 0 disables pairing (measurement)
+    const char* env = getenv("FASE_ITERATE_PAIR");
+    if (!env || atoi(env) != 0)
+      for (const Variant& pv : kPairVariants)
+        if (pv.nt * pv.ep == v->nt * v->ep) v = &pv;
+  }
   KernelFn fn = a.chunk_count ? v->chunked : (a.R_log ? v->record : v->plain);
-  const size_t smem = static_cast<size_t>(v->nt) * v->ep * (sizeof(double2) + (v->dsmem ? sizeof(double) : 0));
+  const size_t smem = static_cast<size_t>(v->nt) * v->ep *
+                      (v->nb * sizeof(double2) + (v->dsmem ? sizeof(double) : 0));
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -524,6 +566,6 @@ extern "C" int fase_iterate_complex(const fase_iterate_args* args, void* stream)
     set_error("fase_iterate_complex: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return FASE_ERR_CUDA;
   }
-  fn<<<a.B, v->nt, smem, as_stream(stream)>>>(a);
+  fn<<<(a.B + v->nb - 1) / v->nb, v->nt * v->nb, smem, as_stream(stream)>>>(a);
   return check_launch("fase_iterate_complex");
 }

@@ -296,3 +296,33 @@ def test_many_exact_ties_lowest_index(copies):
             got = res.selected[b].cpu().numpy()
             assert np.array_equal(got, ref["selected"]), (cplx, b, got, ref["selected"])
             assert got.min() >= 0 and not np.any((got > 0) & (got < copies))  # only the first copy
+
+
+@pytest.mark.parametrize("k_rand,copies", [(2930, 70), (4500, 3)])
+def test_complex_recursion_bit_exact_paired_blocks(k_rand, copies):
+    """Shared geometries with 2304 < K <= 5120 complex atoms run two blocks per
+    CTA sharing D^2 (paired variant; an odd batch leaves the last half idle).
+    With the oracle's tables and initial products every block is
+    bit-identical to the oracle -- including exact ties among `copies`
+    repeated atoms (70 overflow the candidate list: the exact fallback pass
+    with its extra barriers)."""
+    rng = np.random.default_rng(k_rand)
+    m = n = 12
+    base = rng.normal(size=(k_rand, m, n)) + 1j * rng.normal(size=(k_rand, m, n))
+    vals = np.concatenate([np.repeat(base[:1], copies, axis=0), base[1:]])
+    d = Dictionary(vals)
+    mask = wl.central_loss_mask(m, n, 4, 4)
+    cfg = ExtrapConfig(20, 0.5, 0.8)
+    w = orc.weight_field(mask, cfg.rho_hat)
+    phi = d.values.reshape(len(d), -1)
+    c, dd = orc.gram(phi, w)
+    tables = GramTable(c=c, d=dd, provenance=provenance_hash(d, build_weight_field(mask, cfg.rho_hat)))
+    sig = rng.uniform(0, 255, (3, m, n))
+    r0 = np.stack([orc.initial_products(sig[b], w, phi) for b in range(3)])
+    res = fase_extrapolate_batch(sig, mask, d, tables, cfg, products=r0, device=DEV)
+    for b in range(3):
+        sel, proj, coef, _ = orc.fase_run(r0[b], c, dd, cfg.gamma, cfg.iterations)
+        got = res.selected[b].cpu().numpy()
+        assert np.array_equal(got, sel), b
+        assert np.array_equal(res.coefficients[b].cpu().numpy(), coef), b
+        assert np.array_equal(res.projections[b].cpu().numpy(), proj), b

@@ -9,8 +9,11 @@ for c in 0 4 3 2; do
 done
 python bench.py --config 1 --dict dft --steps 10 --warmup 3 --cpu-seconds 8 > gpurun_out/benches/c1_dft.json 2> gpurun_out/benches/c1_dft.err; echo c1dft=$?
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r01e.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu1.log 2>&1; echo ncu1=$?
-ncu --set full --clock-control none --import-source on -k regex:"fase_iterate|sep_products|weigh|synth_paste" -s 5 -c 5 -o gpurun_out/prof_r01_c1e python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu2.log 2>&1; echo ncu2=$?
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r01f.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu1.log 2>&1; echo ncu1=$?
+ncu --set full --clock-control none --import-source on -k regex:"fase_iterate|sep_products|weigh|synth_paste" -s 5 -c 5 -o gpurun_out/prof_r01_c1f python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu2.log 2>&1; echo ncu2=$?
 python bench.py --config 4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain4.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"ozaki|fase_iterate" -s 2 -c 3 -o gpurun_out/prof_r01_c4c python bench.py --config 4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu4.log 2>&1; echo ncu4=$?
-ncu --set full --clock-control none --import-source on -k regex:"iterate_complex|sep_products_complex" -s 2 -c 2 -o gpurun_out/prof_r01_dftc python bench.py --config 1 --dict dft --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu5.log 2>&1; echo ncu5=$?
+ncu --set full --clock-control none --import-source on -k regex:"ozaki_gemm" -s 2 -c 1 -o gpurun_out/prof_r01_c4f_products python bench.py --config 4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu4.log 2>&1; echo ncu4=$?
+ncu --set full --clock-control none --import-source on -k regex:"fase_iterate" -c 1 -o gpurun_out/prof_r01_c4f_iterate python bench.py --config 4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu4b.log 2>&1; echo ncu4b=$?
+python bench.py --config 2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain2.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"fase_iterate" -c 1 -o gpurun_out/prof_r01_c2f python bench.py --config 2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu2b.log 2>&1; echo ncu2b=$?
+ncu --set full --clock-control none --import-source on -k regex:"iterate_complex|sep_products_complex" -s 2 -c 2 -o gpurun_out/prof_r01_dftf python bench.py --config 1 --dict dft --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu5.log 2>&1; echo ncu5=$?
