@@ -159,6 +159,15 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
+// ld.global.nc as a volatile asm: stays where it is written relative to other
+// volatile asm (e.g. an mbarrier wait), so a batch of loads issued before a
+// wait is not hoisted into one long-lived register block by the compiler.
+__device__ __forceinline__ double2 ldg2_here(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }

@@ -300,16 +300,19 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     };
     // ---- rank-1 update fused with the next iteration's running max; the row
     // source is block-uniform, so each source gets its own unrolled loop
-    auto update = [&](auto row_pair, auto staged) {
+    // `pre(sg)` runs at the start of segment sg, before its arrival is awaited
+    // (chunk-row loads are issued there, so they overlap the TMA wait)
+    auto update = [&](auto row_pair, auto staged, auto pre) {
       best = kDead;
       barg = kNone;
 #pragma unroll
       for (int j = 0; j < EP; ++j) {
-        if constexpr (decltype(staged)::value) {
 #pragma unroll
-          for (int sg = 0; sg < kSeg; ++sg)
-            if (j == sg * EP / kSeg) mbar_wait(&s_bar[sg], it & 1);  // segment arrives
-        }
+        for (int sg = 0; sg < kSeg; ++sg)
+          if (j == sg * EP / kSeg) {
+            pre(sg);
+            if constexpr (decltype(staged)::value) mbar_wait(&s_bar[sg], it & 1);  // segment arrives
+          }
         const double2 g = row_pair(j);
         const double2 dd = dpair(j);
         r[j][0] = sub_rn(r[j][0], mul_rn(c, g.x));
@@ -328,7 +331,43 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     };
     using Staged = std::true_type;
     using Direct = std::false_type;
-    if (kChunked && nch > 0) {
+    auto no_pre = [](int) {};
+    if (kChunked && u == guess && nch == 1) {
+      // row_u of this block = G0[u] - C_0[u] (- C_1[u]), element by element in
+      // chunk order, fused into the update of the staged G0 row: a segment's
+      // chunk values are loaded before its G0 part is awaited
+      const double* c0 = a.chunk_tables + static_cast<int64_t>(cids[0]) * a.chunk_stride +
+                         static_cast<int64_t>(u) * ldg + 2 * t;
+      auto fused = [&](auto two) {
+        constexpr bool kTwo = decltype(two)::value;
+        const double* c1 = kTwo ? a.chunk_tables + static_cast<int64_t>(cids[1]) * a.chunk_stride +
+                                      static_cast<int64_t>(u) * ldg + 2 * t
+                                : c0;
+        double2 v0[EP], v1[EP];
+        auto pre = [&](int sg) {
+          const int j0 = sg * EP / kSeg, j1 = (sg + 1) * EP / kSeg;
+#pragma unroll
+          for (int j = 0; j < EP; ++j)
+            if (j >= j0 && j < j1) {
+              v0[j] = ldg2_here(c0 + 2 * j * NT);
+              if constexpr (kTwo) v1[j] = ldg2_here(c1 + 2 * j * NT);
+            }
+        };
+        update(
+            [&](int j) {
+              double2 g = s_row[j * NT + t];
+              g.x = sub_rn(g.x, v0[j].x);
+              g.y = sub_rn(g.y, v0[j].y);
+              if constexpr (kTwo) {
+                g.x = sub_rn(g.x, v1[j].x);
+                g.y = sub_rn(g.y, v1[j].y);
+              }
+              return g;
+            },
+            Staged{}, pre);
+      };
+      fused(std::false_type{});
+    } else if (kChunked && nch > 0) {
       // row_u of this block = G0[u] - sum of its chunk tables' rows, composed
       // in the staging buffer (each thread only touches its own pairs)
       wait_all();
@@ -349,14 +388,14 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
           s_row[j * NT + t] = g;
         }
       }
-      update([&](int j) { return s_row[j * NT + t]; }, Direct{});
+      update([&](int j) { return s_row[j * NT + t]; }, Direct{}, no_pre);
       fence_proxy_async_smem();  // generic writes above precede the next TMA fill
     } else if (u == guess) {  // block-uniform
-      update([&](int j) { return s_row[j * NT + t]; }, Staged{});
+      update([&](int j) { return s_row[j * NT + t]; }, Staged{}, no_pre);
     } else {
       wait_all();  // retire the mispredicted copy before the next one
       const double* urow = a.G0 + static_cast<int64_t>(u) * ldg + 2 * t;
-      update([&](int j) { return ldg2(urow + 2 * j * NT); }, Direct{});
+      update([&](int j) { return ldg2(urow + 2 * j * NT); }, Direct{}, no_pre);
     }
     if (kRecord) {
       double* dst = a.R_log + (static_cast<int64_t>(b) * a.I + it) * a.ldr;
