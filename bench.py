@@ -65,6 +65,8 @@ def parse_args():
     ap.add_argument("--products", default="auto", choices=["auto", "gemm", "separable", "ozaki"],
                     help="initial products: separable transforms (separable dictionaries) or "
                          "the dense DMMA GEMM")
+    ap.add_argument("--compose", default=None, choices=["none", "singles", "pairs"],
+                    help="frame configs: precomposed base tables (default: the engine's)")
     ap.add_argument("--dict", default=None,
                     help="override the dictionary spec of a shared-geometry config (0, 1, 4), "
                          "e.g. 'dft' (the reference's default, complex-valued)")
@@ -593,7 +595,8 @@ def run_gpu_frame(args):
     d = w.dictionary()
     case = wl.frame_case(w)
     K, M, I = len(d), w.area[0] * w.area[1], w.config.iterations
-    engine = FrameEngine(d, case.frame.shape, case.mb, case.support, w.config, device=dev)
+    engine = FrameEngine(d, case.frame.shape, case.mb, case.support, w.config, device=dev,
+                         **({"compose": args.compose} if args.compose else {}))
     grid_h = tile_grid(case.lost, case.mb)
     corners_h = lossy_tiles(case.lost, (case.mb, case.mb)).astype(np.int32)
     L = len(corners_h)
@@ -675,14 +678,18 @@ def run_gpu_frame(args):
     ev[2].record(stream)
     torch.cuda.synchronize()
     counts = b["counts"].float()
-    mean_rows = 1.0 + float(counts.mean())
+    # rows streamed per block-iteration: the base row plus the chunks left after
+    # the precomposed bases (the first one or two cells of a list)
+    absorbed = {None: 0, "singles": 1, "pairs": 2}[engine.compose_mode]
+    mean_rows = 1.0 + float((counts - counts.clamp(max=absorbed)).mean())
     # recursion alone (same inputs as the last run)
     ev_i0 = torch.cuda.Event(enable_timing=True)
     ev_i1 = torch.cuda.Event(enable_timing=True)
     ev_i0.record(stream)
     _native.iterate(engine.G0, b["D"], b["R0"], K, I, w.config.gamma, b["sel"], b["proj"], b["coef"],
                     chunk_tables=engine.tables, chunk_stride=engine.stride,
-                    chunk_count=b["counts"], chunk_ids=b["ids"])
+                    chunk_count=b["counts"], chunk_ids=b["ids"], compose=engine.compose,
+                    base_stride=engine.G0.numel())
     ev_i1.record(stream)
     torch.cuda.synchronize()
     it_s = ev_i0.elapsed_time(ev_i1) / 1e3
@@ -700,7 +707,8 @@ def run_gpu_frame(args):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic frame (seeded BASELINE Appendix-A generator)",
             "config": dict(workload_config(w, world), blocks_per_frame=L,
-                           cells=len(engine.cells), mean_rows_per_iteration=mean_rows),
+                           cells=len(engine.cells), mean_rows_per_iteration=mean_rows,
+                           composed_bases=engine.compose_mode),
             "e2e": {"value": world * L * args.steps / e2e_t, "unit": "blocks/s",
                     "h2d_bytes_per_step": int(case.frame.nbytes),
                     "d2h_bytes_per_step": int(out_host.numel() * 8),
@@ -716,8 +724,9 @@ def run_gpu_frame(args):
                          "streamed_gbs": streamed / it_s / 1e9,
                          "note": "achieved counts 8*K bytes (one table row) per block-iteration, "
                                  "the SURVEY 8(d) unit; the per-block table G0 - sum C_cell "
-                                 "streams (1 + unavailable cells) rows for it (streamed_*), "
-                                 "served largely from L2"},
+                                 "streams one base row (G0 or a precomposed G0 - C_c1 (- C_c2)) "
+                                 "plus the remaining unavailable cells' rows for it "
+                                 "(streamed_*), served largely from L2"},
             "table_build_s": engine.table_seconds,
             "gpu_launches": args.steps * (engine.launches_per_frame + 1) + args.steps * engine.launches_per_frame,
             "clocks": clocks.summary(), "wall_s": t_wall, "cpu_baseline": cpu,

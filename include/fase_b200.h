@@ -187,6 +187,14 @@ FASE_API int fase_block_normalizers(const double* G0, int64_t ldg, const double*
  *   D: shared vector (ldd == 0) or B x ldd
  *   sel / proj / coef: B x ldo outputs (I entries per block)
  *   R_log: NULL or B x I x ldr record of R after every iteration
+ * Precomposed bases (optional, chunked geometries): when compose != NULL it is an
+ * n_compose x n_compose table; for a block whose list starts c1 (, c2):
+ *   p = compose[c1 * n_compose + c2] > 0  -> row_u = B_p[u, :] - sum over the rest
+ *   else p = compose[c1 * n_compose + c1] > 0 -> row_u = B_p[u, :] - sum over the rest
+ * with B_p = G0 + p * base_stride, which must hold G0 - C_c1 (- C_c2) composed
+ * element by element in list order (so the rows are bit-identical to the
+ * uncomposed ones). Normalizers are unaffected (fase_block_normalizers takes
+ * the full lists).
  */
 typedef struct {
   const double* G0;
@@ -210,6 +218,9 @@ typedef struct {
   double* proj;
   double* coef;
   int64_t ldo;
+  const int32_t* compose; /* NULL, or n_compose x n_compose base indices (see above) */
+  int n_compose;
+  int64_t base_stride;
 } fase_iterate_args;
 
 FASE_API int fase_iterate(const fase_iterate_args* args, void* stream);

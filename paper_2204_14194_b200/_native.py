@@ -60,6 +60,7 @@ class IterateArgs(ctypes.Structure):
         ("ldd", _i64), ("R0", _vp),
         ("ldr", _i64), ("R_out", _vp), ("R_log", _vp), ("K", _i32), ("B", _i32), ("I", _i32),
         ("gamma", _f64), ("sel", _vp), ("proj", _vp), ("coef", _vp), ("ldo", _i64),
+        ("compose", _vp), ("n_compose", _i32), ("base_stride", _i64),
     ]
 
 
@@ -275,7 +276,10 @@ def block_normalizers(G0, chunk_tables, chunk_stride: int, chunk_count, chunk_id
 
 def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *,
             chunk_tables=None, chunk_stride: int = 0, chunk_count=None, chunk_ids=None,
-            R_out=None, R_log=None) -> None:
+            R_out=None, R_log=None, compose=None, base_stride: int = 0) -> None:
+    """The recursion (fase_iterate). ``compose`` (n x n int32, device) with
+    ``base_stride`` selects precomposed base tables at G0 + p * base_stride for
+    the first one or two chunks of each block's list."""
     import torch
 
     lib = load()
@@ -291,7 +295,10 @@ def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *
         chunk_list_ld=_ld(chunk_ids) if chunk_ids is not None else 0, D=_ptr(D),
         ldd=_ld(D) if D.dim() == 2 else 0, R0=_ptr(R0), ldr=_ld(R0), R_out=_ptr(R_out),
         R_log=_ptr(R_log), K=K, B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel),
-        proj=_ptr(proj), coef=_ptr(coef), ldo=_ld(sel))
+        proj=_ptr(proj), coef=_ptr(coef), ldo=_ld(sel), compose=_ptr(compose),
+        n_compose=compose.shape[0] if compose is not None else 0, base_stride=base_stride)
+    if compose is not None:
+        _require(compose, "compose", torch.int32, 2)
     if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
         raise errors.ShapeError("sel / proj / coef must share one leading dimension")
     _check(lib.fase_iterate(ctypes.byref(args), _stream(R0)))
@@ -364,7 +371,7 @@ def block_normalizers_complex(T0, chunk_tables, chunk_stride: int, chunk_count, 
 
 def iterate_complex(T, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *,
                     chunk_tables=None, chunk_stride: int = 0, chunk_count=None, chunk_ids=None,
-                    R_out=None, R_log=None) -> None:
+                    R_out=None, R_log=None, compose=None, base_stride: int = 0) -> None:
     import torch
 
     lib = load()
@@ -380,7 +387,10 @@ def iterate_complex(T, D, R0, K: int, iterations: int, gamma: float, sel, proj, 
         chunk_list_ld=_ld(chunk_ids) if chunk_ids is not None else 0, D=_ptr(D),
         ldd=_ld(D) if D.dim() == 2 else 0, R0=_ptr(R0), ldr=_ld(R0), R_out=_ptr(R_out),
         R_log=_ptr(R_log), K=K, B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel),
-        proj=_ptr(proj), coef=_ptr(coef), ldo=_ld(sel))
+        proj=_ptr(proj), coef=_ptr(coef), ldo=_ld(sel), compose=_ptr(compose),
+        n_compose=compose.shape[0] if compose is not None else 0, base_stride=base_stride)
+    if compose is not None:
+        _require(compose, "compose", torch.int32, 2)
     if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
         raise errors.ShapeError("sel / proj / coef must share one leading dimension")
     _check(lib.fase_iterate_complex(ctypes.byref(args), _stream(R0)))

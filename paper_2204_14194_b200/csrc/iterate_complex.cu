@@ -102,9 +102,23 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
   const double* R0 = a.R0 + 2 * static_cast<int64_t>(active ? b : 0) * a.ldr;
   const int32_t* cids = nullptr;
   int nch = 0;
+  const double* G0 = a.G0;  // this block's base table
   if (kChunked) {
     nch = a.chunk_count[b];
     cids = a.chunk_ids + static_cast<int64_t>(b) * a.chunk_list_ld;
+    if (a.compose && nch > 0) {  // precomposed base for the list's first one or two chunks
+      const int n = a.n_compose, c1 = cids[0];
+      int p = nch > 1 ? a.compose[c1 * n + cids[1]] : 0, used = 2;
+      if (p <= 0) {
+        p = a.compose[c1 * n + c1];
+        used = 1;
+      }
+      if (p > 0) {
+        G0 += 2 * static_cast<int64_t>(p) * a.base_stride;
+        cids += used;
+        nch -= used;
+      }
+    }
   }
 
   double r[EP][2];
@@ -194,7 +208,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
     }
     if (t == 0) {
       fence_proxy_async_smem();
-      const double* grow = a.G0 + static_cast<int64_t>(guess) * ldg2x;
+      const double* grow = G0 + static_cast<int64_t>(guess) * ldg2x;
 #pragma unroll
       for (int sg = 0; sg < kSeg; ++sg) {
         const int j0 = sg * EP / kSeg, j1 = (sg + 1) * EP / kSeg;
@@ -380,7 +394,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
     if (kChunked && nch > 0) {
       wait_all();
       if (u != guess) {
-        const double* urow = a.G0 + static_cast<int64_t>(u) * ldg2x + 2 * t;
+        const double* urow = G0 + static_cast<int64_t>(u) * ldg2x + 2 * t;
 #pragma unroll 4
         for (int j = 0; j < EP; ++j) s_row[j * NT + t] = ldg2(urow + 2 * j * NT);
       }
@@ -402,7 +416,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
       update([&](int j) { return s_row[j * NT + t]; }, Staged{});
     } else {
       wait_all();
-      const double* urow = a.G0 + static_cast<int64_t>(u) * ldg2x + 2 * t;
+      const double* urow = G0 + static_cast<int64_t>(u) * ldg2x + 2 * t;
       update([&](int j) { return ldg2(urow + 2 * j * NT); }, Direct{});
     }
     if (kRecord) {
@@ -532,6 +546,11 @@ extern "C" int fase_iterate_complex(const fase_iterate_args* args, void* stream)
   }
   if (a.chunk_count && (!a.chunk_ids || !a.chunk_tables || !aligned16(a.chunk_tables))) {
     set_error("fase_iterate_complex: chunk tables given without ids / aligned storage");
+    return FASE_ERR_SHAPE;
+  }
+  if (a.compose && (!a.chunk_count || a.n_compose < 1 || a.base_stride < a.ldg * a.K)) {
+    set_error("fase_iterate_complex: compose table needs chunk lists, n_compose >= 1 and "
+              "base_stride >= ldg*K");
     return FASE_ERR_SHAPE;
   }
   if (a.chunk_count && a.R_log) {

@@ -221,6 +221,36 @@ def test_frame_blocks_config3(golden_dir):
     assert exact >= len(z["blocks"]) - 1
 
 
+@pytest.mark.parametrize("cid", [3, 2])
+def test_frame_engine_composed_bases_bit_identical(cid):
+    """Precomposed base tables (G0 - C_c1 (- C_c2), composed in list order)
+    stream fewer rows but must give bit-identical selections, coefficients and
+    restored frames to the uncomposed chunk lists."""
+    from paper_2204_14194_b200.conceal import FrameEngine, lossy_tiles, tile_grid
+
+    w8 = wl.WORKLOADS[cid]
+    case = wl.frame_case(w8)
+    d = w8.dictionary()
+    grid = torch.from_numpy(tile_grid(case.lost, case.mb)).to(DEV)
+    corners = torch.from_numpy(lossy_tiles(case.lost, (case.mb, case.mb)).astype(np.int32)).to(DEV)
+    damaged = torch.from_numpy(case.damaged()).to(DEV)
+    runs = {}
+    for mode in ("none", "singles", "pairs"):
+        eng = FrameEngine(d, case.frame.shape, case.mb, case.support, w8.config, device=DEV,
+                          compose=mode)
+        assert (eng.compose is None) == (mode == "none")
+        res = eng.run(damaged, grid, corners)
+        torch.cuda.synchronize()
+        runs[mode] = (res.selected.clone(), res.coefficients.clone(), res.patched.clone())
+        if mode != "none":  # some blocks do take a composed base
+            counts = eng._buffers(int(corners.shape[0]))["counts"]
+            assert int((counts >= (2 if mode == "pairs" else 1)).sum()) > 0
+        del eng
+    for mode in ("singles", "pairs"):
+        for a, b in zip(runs["none"], runs[mode]):
+            assert torch.equal(a, b), mode
+
+
 # ----------------------------------------------------------------- properties / edges
 
 
@@ -505,3 +535,62 @@ def test_recursion_bit_exact_paired_blocks(spec):
         assert np.array_equal(res.selected[b].cpu().numpy(), sel)
         assert np.array_equal(res.coefficients[b].cpu().numpy(), coef.real)
         assert np.array_equal(res.projections[b].cpu().numpy(), proj.real)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_iterate_compose_map_bit_identical(cplx):
+    """fase_iterate(_complex) with a compose map: base tables G0 - C_c1 (- C_c2)
+    composed in list order replace the first one or two chunks of each list;
+    the run is bit-identical to the plain chunk lists (random tables and lists,
+    some blocks without chunks, singles and pairs both present)."""
+    from paper_2204_14194_b200 import _native
+
+    rng = np.random.default_rng(11 + cplx)
+    K, B, I, n = 300, 9, 30, 4
+    ld = _native.table_ld_complex(K) if cplx else _native.table_ld(K)
+    dt = torch.complex128 if cplx else torch.float64
+
+    def rnd(*shape):
+        x = torch.from_numpy(rng.normal(size=shape))
+        if cplx:
+            x = torch.complex(x, torch.from_numpy(rng.normal(size=shape)))
+        return x.to(DEV)
+
+    G0 = torch.zeros((K, ld), dtype=dt, device=DEV)
+    G0[:, :K] = rnd(K, K)
+    tabs = torch.zeros((n, K, ld), dtype=dt, device=DEV)
+    tabs[:, :, :K] = 0.3 * rnd(n, K, K)
+    counts = torch.tensor([0, 1, 2, 3, 4, 1, 2, 3, 0], dtype=torch.int32, device=DEV)
+    ids = torch.zeros((B, n), dtype=torch.int32)
+    for b, c in enumerate(counts.tolist()):
+        ids[b, :c] = torch.from_numpy(np.sort(rng.choice(n, c, replace=False)))
+    ids = ids.to(DEV)
+    # singles for every cell, pairs only for (0, 1) and (1, 3)
+    pairs = [(0, 1), (1, 3)]
+    bases = torch.empty((1 + n + len(pairs), K, ld), dtype=dt, device=DEV)
+    bases[0] = G0
+    cmap = torch.zeros((n, n), dtype=torch.int32)
+    for c in range(n):
+        torch.sub(G0, tabs[c], out=bases[1 + c])
+        cmap[c, c] = 1 + c
+    for p, (i, j) in enumerate(pairs, start=1 + n):
+        torch.sub(bases[1 + i], tabs[j], out=bases[p])
+        cmap[i, j] = p
+    cmap = cmap.to(DEV)
+    D = torch.from_numpy(rng.uniform(0.5, 1.5, (B, ld))).to(DEV)
+    R0 = torch.zeros((B, ld), dtype=dt, device=DEV)
+    R0[:, :K] = rnd(B, K)
+    fn = _native.iterate_complex if cplx else _native.iterate
+    out = []
+    for composed in (False, True):
+        sel = torch.empty((B, I), dtype=torch.int32, device=DEV)
+        proj = torch.empty((B, I), dtype=dt, device=DEV)
+        coef = torch.empty((B, I), dtype=dt, device=DEV)
+        fn(bases[0], D, R0, K, I, 0.5, sel, proj, coef, chunk_tables=tabs,
+           chunk_stride=tabs[0].numel(), chunk_count=counts, chunk_ids=ids,
+           compose=cmap if composed else None, base_stride=bases[0].numel() if composed else 0)
+        out.append((sel, proj, coef))
+    torch.cuda.synchronize()
+    for a, b in zip(*out):
+        assert torch.equal(a, b)
+    assert (out[0][0] >= 0).all()

@@ -114,7 +114,8 @@ def test_status_maps_to_reference_exceptions(lib):
 def test_iterate_args_layout_matches_header():
     # the ctypes mirror must have the header's field order
     text = HEADER.read_text()
-    body = text[text.index("typedef struct {"):text.index("} fase_iterate_args;")]
+    end = text.index("} fase_iterate_args;")
+    body = text[text.rindex("typedef struct {", 0, end):end]
     fields = re.findall(r"\b(\w+);", body)
     assert fields == [f for f, _ in _native.IterateArgs._fields_]
 
