@@ -65,7 +65,7 @@ def parse_args():
     ap.add_argument("--products", default="auto", choices=["auto", "gemm", "separable", "ozaki"],
                     help="initial products: separable transforms (separable dictionaries) or "
                          "the dense DMMA GEMM")
-    ap.add_argument("--compose", default=None, choices=["none", "singles", "pairs"],
+    ap.add_argument("--compose", default=None, choices=["none", "singles", "pairs", "triples"],
                     help="frame configs: precomposed base tables (default: the engine's)")
     ap.add_argument("--dict", default=None,
                     help="override the dictionary spec of a shared-geometry config (0, 1, 4), "
@@ -680,7 +680,7 @@ def run_gpu_frame(args):
     counts = b["counts"].float()
     # rows streamed per block-iteration: the base row plus the chunks left after
     # the precomposed bases (the first one or two cells of a list)
-    absorbed = {None: 0, "singles": 1, "pairs": 2}[engine.compose_mode]
+    absorbed = {None: 0, "singles": 1, "pairs": 2, "triples": 3}[engine.compose_mode]
     mean_rows = 1.0 + float((counts - counts.clamp(max=absorbed)).mean())
     # recursion alone (same inputs as the last run)
     ev_i0 = torch.cuda.Event(enable_timing=True)

@@ -187,11 +187,13 @@ FASE_API int fase_block_normalizers(const double* G0, int64_t ldg, const double*
  *   D: shared vector (ldd == 0) or B x ldd
  *   sel / proj / coef: B x ldo outputs (I entries per block)
  *   R_log: NULL or B x I x ldr record of R after every iteration
- * Precomposed bases (optional, chunked geometries): when compose != NULL it is an
- * n_compose x n_compose table; for a block whose list starts c1 (, c2):
- *   p = compose[c1 * n_compose + c2] > 0  -> row_u = B_p[u, :] - sum over the rest
- *   else p = compose[c1 * n_compose + c1] > 0 -> row_u = B_p[u, :] - sum over the rest
- * with B_p = G0 + p * base_stride, which must hold G0 - C_c1 (- C_c2) composed
+ * Precomposed bases (optional, chunked geometries): compose != NULL is an
+ * n_compose^compose_depth table (compose_depth 1..3) indexed by a list prefix
+ * padded with its last entry, e.g. depth 3: (c1, c2, c3), (c1, c2, c2), (c1, c1, c1).
+ * For the longest prefix of length k <= compose_depth of a block's (ascending)
+ * list with p = compose[prefix] > 0:
+ *   row_u = B_p[u, :] - sum over the list's remaining chunks,
+ * B_p = G0 + p * base_stride, which must hold G0 - C_c1 - ... - C_ck composed
  * element by element in list order (so the rows are bit-identical to the
  * uncomposed ones). Normalizers are unaffected (fase_block_normalizers takes
  * the full lists).
@@ -218,8 +220,9 @@ typedef struct {
   double* proj;
   double* coef;
   int64_t ldo;
-  const int32_t* compose; /* NULL, or n_compose x n_compose base indices (see above) */
+  const int32_t* compose; /* NULL, or n_compose^compose_depth base indices (see above) */
   int n_compose;
+  int compose_depth;
   int64_t base_stride;
 } fase_iterate_args;
 

@@ -60,7 +60,7 @@ class IterateArgs(ctypes.Structure):
         ("ldd", _i64), ("R0", _vp),
         ("ldr", _i64), ("R_out", _vp), ("R_log", _vp), ("K", _i32), ("B", _i32), ("I", _i32),
         ("gamma", _f64), ("sel", _vp), ("proj", _vp), ("coef", _vp), ("ldo", _i64),
-        ("compose", _vp), ("n_compose", _i32), ("base_stride", _i64),
+        ("compose", _vp), ("n_compose", _i32), ("compose_depth", _i32), ("base_stride", _i64),
     ]
 
 
@@ -277,9 +277,9 @@ def block_normalizers(G0, chunk_tables, chunk_stride: int, chunk_count, chunk_id
 def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *,
             chunk_tables=None, chunk_stride: int = 0, chunk_count=None, chunk_ids=None,
             R_out=None, R_log=None, compose=None, base_stride: int = 0) -> None:
-    """The recursion (fase_iterate). ``compose`` (n x n int32, device) with
-    ``base_stride`` selects precomposed base tables at G0 + p * base_stride for
-    the first one or two chunks of each block's list."""
+    """The recursion (fase_iterate). ``compose`` (int32 device table n^depth,
+    depth 1..3) with ``base_stride`` selects precomposed base tables at
+    G0 + p * base_stride for the longest prefix of each block's chunk list."""
     import torch
 
     lib = load()
@@ -296,9 +296,12 @@ def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *
         ldd=_ld(D) if D.dim() == 2 else 0, R0=_ptr(R0), ldr=_ld(R0), R_out=_ptr(R_out),
         R_log=_ptr(R_log), K=K, B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel),
         proj=_ptr(proj), coef=_ptr(coef), ldo=_ld(sel), compose=_ptr(compose),
-        n_compose=compose.shape[0] if compose is not None else 0, base_stride=base_stride)
+        n_compose=compose.shape[0] if compose is not None else 0,
+        compose_depth=compose.dim() if compose is not None else 0, base_stride=base_stride)
     if compose is not None:
-        _require(compose, "compose", torch.int32, 2)
+        _require(compose, "compose", torch.int32)
+        if compose.dim() > 3 or any(x != compose.shape[0] for x in compose.shape):
+            raise errors.ShapeError("compose must be an n, n x n or n x n x n table")
     if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
         raise errors.ShapeError("sel / proj / coef must share one leading dimension")
     _check(lib.fase_iterate(ctypes.byref(args), _stream(R0)))
@@ -388,9 +391,12 @@ def iterate_complex(T, D, R0, K: int, iterations: int, gamma: float, sel, proj, 
         ldd=_ld(D) if D.dim() == 2 else 0, R0=_ptr(R0), ldr=_ld(R0), R_out=_ptr(R_out),
         R_log=_ptr(R_log), K=K, B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel),
         proj=_ptr(proj), coef=_ptr(coef), ldo=_ld(sel), compose=_ptr(compose),
-        n_compose=compose.shape[0] if compose is not None else 0, base_stride=base_stride)
+        n_compose=compose.shape[0] if compose is not None else 0,
+        compose_depth=compose.dim() if compose is not None else 0, base_stride=base_stride)
     if compose is not None:
-        _require(compose, "compose", torch.int32, 2)
+        _require(compose, "compose", torch.int32)
+        if compose.dim() > 3 or any(x != compose.shape[0] for x in compose.shape):
+            raise errors.ShapeError("compose must be an n, n x n or n x n x n table")
     if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
         raise errors.ShapeError("sel / proj / coef must share one leading dimension")
     _check(lib.fase_iterate_complex(ctypes.byref(args), _stream(R0)))

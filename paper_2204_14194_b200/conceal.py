@@ -28,6 +28,7 @@ inside the recursion kernel. Per frame, only kernels run:
 
 from __future__ import annotations
 
+import math
 import time
 
 import numpy as np
@@ -79,8 +80,9 @@ def _cuts(n: int, tile: int, support: int, area: int) -> list[int]:
     return sorted(cuts)
 
 
-# device bytes the frame engine may spend on precomposed base tables
-COMPOSE_BUDGET = 24 << 30
+# device bytes the frame engine may spend on precomposed base tables (at most
+# half the free memory): config 3 takes 78 GB for all cell triples on a B200
+COMPOSE_BUDGET = 96 << 30
 
 
 class FrameEngine:
@@ -91,11 +93,11 @@ class FrameEngine:
                  compose: str = "auto"):
         """``compose``: precomposed base tables for the first chunks of a block's
         cell list -- "none", "singles" (G0 - C_c for every cell), "pairs" (also
-        G0 - C_c1 - C_c2 for every cell pair) or "auto" (pairs when they fit
-        the memory budget COMPOSE_BUDGET, else singles, else none). Composition
+        G0 - C_c1 - C_c2 for every cell pair), "triples" or "auto" (the deepest
+        that fits the memory budget COMPOSE_BUDGET). Composition
         runs in list order, so every variant streams bit-identical rows; the
         composed ones stream one or two fewer rows per block-iteration
-        (config 2: 2.22 -> 1.27 rows, config 3: 5.95 -> 3.99)."""
+        (triples: config 2 2.22 -> 1.10 rows, config 3 5.95 -> 3.10)."""
         import torch
 
         self.device = dev = resolve_device(device)
@@ -155,34 +157,44 @@ class FrameEngine:
         self._buf = {}
 
     def _compose_bases(self, mode: str):
-        """(bases, compose map): bases[0] is G0, bases[p] = G0 - C_c1 (- C_c2)
-        composed element by element in list order (IEEE subtraction, as the
-        recursion kernel composes rows); compose[c1, c2] / compose[c, c] give p."""
+        """(bases, compose map): bases[0] is G0 and bases[p] = G0 - C_c1 - ... - C_ck
+        for ascending cell prefixes up to the mode's depth (singles 1, pairs 2,
+        triples 3), composed element by element in list order (IEEE
+        subtraction, as the recursion kernel composes rows). The map is indexed
+        by the prefix padded with its last cell (fase_iterate_args.compose)."""
+        import itertools
+
         import torch
 
-        if mode not in ("auto", "none", "singles", "pairs"):
-            raise ParameterError(f"compose must be auto, none, singles or pairs, got {mode!r}")
+        depths = {"none": 0, "singles": 1, "pairs": 2, "triples": 3}
+        if mode != "auto" and mode not in depths:
+            raise ParameterError(f"compose must be auto or one of {sorted(depths)}, got {mode!r}")
         n = len(self.cells)
+
+        def n_bases(depth):
+            return 1 + sum(math.comb(n, k) for k in range(1, depth + 1))
+
         if mode == "auto":
             table = self.G0.numel() * 8
-            free = torch.cuda.mem_get_info(self.device)[0]
-            budget = min(COMPOSE_BUDGET, free // 3)
-            mode = ("pairs" if (1 + n + n * (n - 1) // 2) * table <= budget else
-                    "singles" if (1 + n) * table <= budget else "none")
-        self.compose_mode = None if mode == "none" or n == 0 else mode
-        if self.compose_mode is None:
+            budget = min(COMPOSE_BUDGET, torch.cuda.mem_get_info(self.device)[0] // 2)
+            mode = next((m for m in ("triples", "pairs", "singles")
+                         if n_bases(depths[m]) * table <= budget), "none")
+        depth = depths[mode] if n else 0
+        self.compose_mode = mode if depth else None
+        if not depth:
             return None, None
-        pairs = [(i, j) for i in range(n) for j in range(i + 1, n)] if mode == "pairs" else []
         K, ldg = self.G0.shape
-        bases = torch.empty((1 + n + len(pairs), K, ldg), dtype=torch.float64, device=self.device)
+        bases = torch.empty((n_bases(depth), K, ldg), dtype=torch.float64, device=self.device)
         bases[0].copy_(self.G0)
-        cmap = np.zeros((n, n), dtype=np.int32)
-        for c in range(n):
-            torch.sub(self.G0, self.tables[c], out=bases[1 + c])
-            cmap[c, c] = 1 + c
-        for p, (i, j) in enumerate(pairs, start=1 + n):
-            torch.sub(bases[1 + i], self.tables[j], out=bases[p])
-            cmap[i, j] = p
+        cmap = np.zeros((n,) * depth, dtype=np.int32)
+        index = {(): 0}
+        p = 1
+        for k in range(1, depth + 1):
+            for pre in itertools.combinations(range(n), k):
+                torch.sub(bases[index[pre[:-1]]], self.tables[pre[-1]], out=bases[p])
+                index[pre] = p
+                cmap[pre + (pre[-1],) * (depth - k)] = p
+                p += 1
         self.G0 = bases[0]  # one allocation: base p at G0 + p * stride
         return bases, torch.from_numpy(cmap).to(self.device)
 

@@ -124,17 +124,17 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   if (kChunked) {
     nch = a.chunk_count[b];
     cids = a.chunk_ids + static_cast<int64_t>(b) * a.chunk_list_ld;
-    if (a.compose && nch > 0) {  // precomposed base for the list's first one or two chunks
-      const int n = a.n_compose, c1 = cids[0];
-      int p = nch > 1 ? a.compose[c1 * n + cids[1]] : 0, used = 2;
-      if (p <= 0) {
-        p = a.compose[c1 * n + c1];
-        used = 1;
-      }
-      if (p > 0) {
-        G0 += static_cast<int64_t>(p) * a.base_stride;
-        cids += used;
-        nch -= used;
+    if (a.compose && nch > 0) {  // precomposed base for the longest listed prefix
+      for (int k = min(nch, a.compose_depth); k >= 1; --k) {
+        int64_t idx = 0;
+        for (int d = 0; d < a.compose_depth; ++d) idx = idx * a.n_compose + cids[min(d, k - 1)];
+        const int p = a.compose[idx];
+        if (p > 0) {
+          G0 += static_cast<int64_t>(p) * a.base_stride;
+          cids += k;
+          nch -= k;
+          break;
+        }
       }
     }
   }
@@ -545,10 +545,10 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
     set_error("fase_iterate: chunk tables given without ids / aligned storage");
     return FASE_ERR_SHAPE;
   }
-  if (a.compose &&
-      (!a.chunk_count || a.n_compose < 1 || a.base_stride < a.ldg * a.K || (a.base_stride & 1))) {
-    set_error("fase_iterate: compose table needs chunk lists, n_compose >= 1 and an even "
-              "base_stride >= ldg*K");
+  if (a.compose && (!a.chunk_count || a.n_compose < 1 || a.compose_depth < 1 ||
+                    a.compose_depth > 3 || a.base_stride < a.ldg * a.K || (a.base_stride & 1))) {
+    set_error("fase_iterate: compose table needs chunk lists, n_compose >= 1, depth 1..3 and an "
+              "even base_stride >= ldg*K");
     return FASE_ERR_SHAPE;
   }
   if (a.chunk_count && a.R_log) {

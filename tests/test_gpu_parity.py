@@ -221,32 +221,54 @@ def test_frame_blocks_config3(golden_dir):
     assert exact >= len(z["blocks"]) - 1
 
 
-@pytest.mark.parametrize("cid", [3, 2])
-def test_frame_engine_composed_bases_bit_identical(cid):
-    """Precomposed base tables (G0 - C_c1 (- C_c2), composed in list order)
+def _small_frame_case():
+    """A 72 x 80 frame, 8-pixel tiles, support 4 (16 x 16 areas, 8 cells), 35%
+    of the tiles lost: lists of every length from 0 to 8."""
+    rng = np.random.default_rng(33)
+    h, w, mb = 72, 80, 8
+    yy, xx = np.mgrid[0:h, 0:w]
+    frame = np.clip(128 + 60 * np.sin(0.17 * yy + 0.11 * xx) + rng.normal(0, 6, (h, w)), 0, 255)
+    frame = frame.astype(np.uint8)
+    tiles = [(r, c) for r in range(0, h, mb) for c in range(0, w, mb)]
+    pick = rng.choice(len(tiles), int(0.35 * len(tiles)), replace=False)
+    corners = np.array(sorted(tiles[i] for i in pick), dtype=np.int32)
+    lost = np.zeros((h, w), dtype=bool)
+    for r0, c0 in corners:
+        lost[r0:r0 + mb, c0:c0 + mb] = True
+    case = wl.FrameCase(frame=frame, lost=lost, corners=corners, mb=mb, support=4)
+    return case, parse_dict_spec("dct", 16, 16), ExtrapConfig(40, 0.5, 0.8)
+
+
+@pytest.mark.parametrize("cid,modes", [("small", ("singles", "pairs", "triples")),
+                                       (3, ("singles", "pairs")), (2, ("singles", "pairs"))])
+def test_frame_engine_composed_bases_bit_identical(cid, modes):
+    """Precomposed base tables (G0 - C_c1 - ... - C_ck, composed in list order)
     stream fewer rows but must give bit-identical selections, coefficients and
     restored frames to the uncomposed chunk lists."""
     from paper_2204_14194_b200.conceal import FrameEngine, lossy_tiles, tile_grid
 
-    w8 = wl.WORKLOADS[cid]
-    case = wl.frame_case(w8)
-    d = w8.dictionary()
+    if cid == "small":
+        case, d, cfg = _small_frame_case()
+    else:
+        w8 = wl.WORKLOADS[cid]
+        case, d, cfg = wl.frame_case(w8), w8.dictionary(), w8.config
     grid = torch.from_numpy(tile_grid(case.lost, case.mb)).to(DEV)
     corners = torch.from_numpy(lossy_tiles(case.lost, (case.mb, case.mb)).astype(np.int32)).to(DEV)
     damaged = torch.from_numpy(case.damaged()).to(DEV)
     runs = {}
-    for mode in ("none", "singles", "pairs"):
-        eng = FrameEngine(d, case.frame.shape, case.mb, case.support, w8.config, device=DEV,
+    for mode in ("none",) + modes:
+        eng = FrameEngine(d, case.frame.shape, case.mb, case.support, cfg, device=DEV,
                           compose=mode)
         assert (eng.compose is None) == (mode == "none")
         res = eng.run(damaged, grid, corners)
         torch.cuda.synchronize()
         runs[mode] = (res.selected.clone(), res.coefficients.clone(), res.patched.clone())
-        if mode != "none":  # some blocks do take a composed base
+        if mode != "none":  # some blocks do take a composed base of the full depth
+            depth = eng.compose.dim()
             counts = eng._buffers(int(corners.shape[0]))["counts"]
-            assert int((counts >= (2 if mode == "pairs" else 1)).sum()) > 0
+            assert int((counts >= depth).sum()) > 0
         del eng
-    for mode in ("singles", "pairs"):
+    for mode in modes:
         for a, b in zip(runs["none"], runs[mode]):
             assert torch.equal(a, b), mode
 
@@ -537,8 +559,8 @@ def test_recursion_bit_exact_paired_blocks(spec):
         assert np.array_equal(res.projections[b].cpu().numpy(), proj.real)
 
 
-@pytest.mark.parametrize("cplx", [False, True])
-def test_iterate_compose_map_bit_identical(cplx):
+@pytest.mark.parametrize("cplx,depth", [(False, 2), (True, 2), (False, 3), (True, 1)])
+def test_iterate_compose_map_bit_identical(cplx, depth):
     """fase_iterate(_complex) with a compose map: base tables G0 - C_c1 (- C_c2)
     composed in list order replace the first one or two chunks of each list;
     the run is bit-identical to the plain chunk lists (random tables and lists,
@@ -565,17 +587,17 @@ def test_iterate_compose_map_bit_identical(cplx):
     for b, c in enumerate(counts.tolist()):
         ids[b, :c] = torch.from_numpy(np.sort(rng.choice(n, c, replace=False)))
     ids = ids.to(DEV)
-    # singles for every cell, pairs only for (0, 1) and (1, 3)
-    pairs = [(0, 1), (1, 3)]
-    bases = torch.empty((1 + n + len(pairs), K, ld), dtype=dt, device=DEV)
+    # every single, a few pairs / triples (the rest fall back to shorter prefixes)
+    prefixes = [(c,) for c in range(n)] + [(0, 1), (1, 3), (0, 2), (1, 2), (0, 1, 2), (1, 2, 3)]
+    prefixes = [p for p in prefixes if len(p) <= depth]
+    bases = torch.empty((1 + len(prefixes), K, ld), dtype=dt, device=DEV)
     bases[0] = G0
-    cmap = torch.zeros((n, n), dtype=torch.int32)
-    for c in range(n):
-        torch.sub(G0, tabs[c], out=bases[1 + c])
-        cmap[c, c] = 1 + c
-    for p, (i, j) in enumerate(pairs, start=1 + n):
-        torch.sub(bases[1 + i], tabs[j], out=bases[p])
-        cmap[i, j] = p
+    cmap = torch.zeros((n,) * depth, dtype=torch.int32)
+    index = {(): 0}
+    for p, pre in enumerate(prefixes, start=1):
+        torch.sub(bases[index[pre[:-1]]], tabs[pre[-1]], out=bases[p])
+        index[pre] = p
+        cmap[pre + (pre[-1],) * (depth - len(pre))] = p
     cmap = cmap.to(DEV)
     D = torch.from_numpy(rng.uniform(0.5, 1.5, (B, ld))).to(DEV)
     R0 = torch.zeros((B, ld), dtype=dt, device=DEV)
