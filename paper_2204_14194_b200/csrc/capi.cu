@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kNormThreads) block_normalizers_kernel(
 constexpr int kSynthThreads = 256;
 constexpr int kSynthChunk = 1024;
 
+template <int G>
 __global__ void __launch_bounds__(kSynthThreads) synth_paste_kernel(
     const double* __restrict__ phi, int64_t ldphi, const int32_t* __restrict__ sel,
     const double* __restrict__ coef, int64_t ldo, int I, const int32_t* __restrict__ idx_ptr,
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kSynthThreads) synth_paste_kernel(
         s_coef[t] = my_coef[t0 + t];
       }
       __syncthreads();
-      if (i < n) g = synth_terms(phi, ldphi, s_sel, s_coef, len, m, g);
+      if (i < n) g = synth_terms<G>(phi, ldphi, s_sel, s_coef, len, m, g);
     }
     if (i < n) out[(dst ? dst[lo + i] : static_cast<int64_t>(m)) + static_cast<int64_t>(b) * ldout] = g;
   }
@@ -303,8 +304,10 @@ extern "C" int fase_synth_paste(const double* phi, int64_t ldphi, const int32_t*
     set_error("fase_synth_paste: null pointer");
     return FASE_ERR_SHAPE;
   }
-  synth_paste_kernel<<<B, kSynthThreads, 0, as_stream(stream)>>>(
-      phi, ldphi, sel, coef, ldo, I, idx_ptr, idx, n_shared, dst, out, ldout);
+  // a batch that cannot fill the GPU is latency-bound: keep more atom values in flight
+  auto kernel = B < 148 ? synth_paste_kernel<32> : synth_paste_kernel<8>;
+  kernel<<<B, kSynthThreads, 0, as_stream(stream)>>>(phi, ldphi, sel, coef, ldo, I, idx_ptr, idx,
+                                                      n_shared, dst, out, ldout);
   return check_launch("fase_synth_paste");
 }
 

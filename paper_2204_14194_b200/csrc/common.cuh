@@ -49,11 +49,12 @@ __device__ __forceinline__ long long warp_max_i64(long long v) {
 // first sel < 0 (a block whose atoms were all degenerate): the reference's
 // sequential summation order (SparseModel.materialize, reference.py:120-125).
 // Atom values are fetched 8 terms at a time (independent loads in flight), then
-// accumulated strictly in order.
+// accumulated strictly in order. G: loads in flight (more for small, latency-
+// bound batches).
+template <int G = 8>
 __device__ __forceinline__ double synth_terms(const double* __restrict__ phi, int64_t ldphi,
                                               const int32_t* s_sel, const double* s_coef,
                                               int len, int m, double g) {
-  constexpr int G = 8;
   for (int t0 = 0; t0 < len; t0 += G) {
     double v[G];
 #pragma unroll
