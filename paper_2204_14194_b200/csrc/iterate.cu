@@ -188,6 +188,10 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   double* coef = a.coef + static_cast<int64_t>(b) * a.ldo;
   const int64_t ldg = a.ldg;
   double q = 0.0;
+  // kChunked: the atom whose complete (composed) row the staging buffer holds,
+  // and the number of row copies issued so far (mbarrier phase parity)
+  unsigned held = kNone;
+  unsigned n_copies = 0;
 
   for (int it = 0; it < a.I; ++it) {
     // ---- exact warp max and the lowest index attaining it
@@ -228,8 +232,13 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       return;
     }
     // stage the likely selection's row in shared memory (one TMA bulk copy)
-    // while the tie pass and the second barrier run
-    if (t == 0) {
+    // while the tie pass and the second barrier run -- unless the buffer
+    // already holds that atom's complete row (per-block geometries re-select
+    // the previous atom often: 60% of config-3 iterations)
+    const bool issue = !kChunked || guess != held;  // block-uniform
+    const unsigned par = n_copies & 1u;
+    n_copies += issue ? 1u : 0u;
+    if (t == 0 && issue) {
       fence_proxy_async_smem();
       const double* grow = G0 + static_cast<int64_t>(guess) * ldg;
 #pragma unroll
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
 
     auto wait_all = [&]() {
 #pragma unroll
-      for (int sg = 0; sg < kSeg; ++sg) mbar_wait(&s_bar[sg], it & 1);
+      for (int sg = 0; sg < kSeg; ++sg) mbar_wait(&s_bar[sg], par);
     };
     // ---- rank-1 update fused with the next iteration's running max; the row
     // source is block-uniform, so each source gets its own unrolled loop
@@ -325,7 +334,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         for (int sg = 0; sg < kSeg; ++sg)
           if (j == sg * EP / kSeg) {
             pre(sg);
-            if constexpr (decltype(staged)::value) mbar_wait(&s_bar[sg], it & 1);  // segment arrives
+            if constexpr (decltype(staged)::value) mbar_wait(&s_bar[sg], par);  // segment arrives
           }
         const double2 g = row_pair(j);
         const double2 dd = dpair(j);
@@ -346,64 +355,78 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     using Staged = std::true_type;
     using Direct = std::false_type;
     auto no_pre = [](int) {};
-    if (kChunked && u == guess && nch == 1) {
-      // row_u of this block = G0[u] - C_0[u] (- C_1[u]), element by element in
-      // chunk order, fused into the update of the staged G0 row: a segment's
-      // chunk values are loaded before its G0 part is awaited
-      const double* c0 = a.chunk_tables + static_cast<int64_t>(cids[0]) * a.chunk_stride +
-                         static_cast<int64_t>(u) * ldg + 2 * t;
-      auto fused = [&](auto two) {
-        constexpr bool kTwo = decltype(two)::value;
-        const double* c1 = kTwo ? a.chunk_tables + static_cast<int64_t>(cids[1]) * a.chunk_stride +
-                                      static_cast<int64_t>(u) * ldg + 2 * t
-                                : c0;
-        double2 v0[EP], v1[EP];
+    if constexpr (kChunked) {
+      // row_u of this block = G0[u] - sum of its remaining chunk tables' rows,
+      // element by element in list order; the complete row is left in the
+      // staging buffer (held) for a re-selection of u
+      if (issue && u == guess && nch == 0) {
+        update([&](int j) { return s_row[j * NT + t]; }, Staged{}, no_pre);
+      } else if (issue && u == guess && nch == 1) {
+        // fused: a segment's chunk values are loaded before its staged G0
+        // part is awaited; the composed row is written back
+        const double* c0 = a.chunk_tables + static_cast<int64_t>(cids[0]) * a.chunk_stride +
+                           static_cast<int64_t>(u) * ldg + 2 * t;
+        double2 v0[EP];
         auto pre = [&](int sg) {
           const int j0 = sg * EP / kSeg, j1 = (sg + 1) * EP / kSeg;
 #pragma unroll
           for (int j = 0; j < EP; ++j)
-            if (j >= j0 && j < j1) {
-              v0[j] = ldg2_here(c0 + 2 * j * NT);
-              if constexpr (kTwo) v1[j] = ldg2_here(c1 + 2 * j * NT);
-            }
+            if (j >= j0 && j < j1) v0[j] = ldg2_here(c0 + 2 * j * NT);
         };
         update(
             [&](int j) {
               double2 g = s_row[j * NT + t];
               g.x = sub_rn(g.x, v0[j].x);
               g.y = sub_rn(g.y, v0[j].y);
-              if constexpr (kTwo) {
-                g.x = sub_rn(g.x, v1[j].x);
-                g.y = sub_rn(g.y, v1[j].y);
-              }
+              s_row[j * NT + t] = g;
               return g;
             },
             Staged{}, pre);
-      };
-      fused(std::false_type{});
-    } else if (kChunked && nch > 0) {
-      // row_u of this block = G0[u] - sum of its chunk tables' rows, composed
-      // in the staging buffer (each thread only touches its own pairs)
-      wait_all();
-      if (u != guess) {
-        const double* urow = G0 + static_cast<int64_t>(u) * ldg + 2 * t;
+        fence_proxy_async_smem();  // generic writes precede the next TMA fill
+      } else if (!issue && u == held) {
+        update([&](int j) { return s_row[j * NT + t]; }, Direct{}, no_pre);
+      } else {
+        // compose in the staging buffer (each thread only touches its own pairs)
+        if (issue) wait_all();  // retire the copy before touching the buffer
+        if (!issue || u != guess) {
+          const double* urow = G0 + static_cast<int64_t>(u) * ldg + 2 * t;
 #pragma unroll 4
-        for (int j = 0; j < EP; ++j) s_row[j * NT + t] = ldg2(urow + 2 * j * NT);
-      }
-      for (int ch = 0; ch < nch; ++ch) {
-        const double* crow = a.chunk_tables + static_cast<int64_t>(cids[ch]) * a.chunk_stride +
-                             static_cast<int64_t>(u) * ldg + 2 * t;
-#pragma unroll 4
-        for (int j = 0; j < EP; ++j) {
-          const double2 v = ldg2(crow + 2 * j * NT);
-          double2 g = s_row[j * NT + t];
-          g.x = sub_rn(g.x, v.x);
-          g.y = sub_rn(g.y, v.y);
-          s_row[j * NT + t] = g;
+          for (int j = 0; j < EP; ++j) s_row[j * NT + t] = ldg2(urow + 2 * j * NT);
         }
+        auto crow = [&](int ch) {
+          return a.chunk_tables + static_cast<int64_t>(cids[ch]) * a.chunk_stride +
+                 static_cast<int64_t>(u) * ldg + 2 * t;
+        };
+        int ch = 0;
+        // two chunks per pass (twice the loads in flight) where registers allow
+        for (; EP <= 8 && ch + 1 < nch; ch += 2) {
+          const double* ca = crow(ch);
+          const double* cb = crow(ch + 1);
+#pragma unroll 4
+          for (int j = 0; j < EP; ++j) {
+            const double2 va = ldg2(ca + 2 * j * NT);
+            const double2 vb = ldg2(cb + 2 * j * NT);
+            double2 g = s_row[j * NT + t];
+            g.x = sub_rn(sub_rn(g.x, va.x), vb.x);
+            g.y = sub_rn(sub_rn(g.y, va.y), vb.y);
+            s_row[j * NT + t] = g;
+          }
+        }
+        for (; ch < nch; ++ch) {
+          const double* ca = crow(ch);
+#pragma unroll 4
+          for (int j = 0; j < EP; ++j) {
+            const double2 v = ldg2(ca + 2 * j * NT);
+            double2 g = s_row[j * NT + t];
+            g.x = sub_rn(g.x, v.x);
+            g.y = sub_rn(g.y, v.y);
+            s_row[j * NT + t] = g;
+          }
+        }
+        update([&](int j) { return s_row[j * NT + t]; }, Direct{}, no_pre);
+        fence_proxy_async_smem();  // generic writes above precede the next TMA fill
       }
-      update([&](int j) { return s_row[j * NT + t]; }, Direct{}, no_pre);
-      fence_proxy_async_smem();  // generic writes above precede the next TMA fill
+      held = u;
     } else if (u == guess) {  // block-uniform
       update([&](int j) { return s_row[j * NT + t]; }, Staged{}, no_pre);
     } else {
