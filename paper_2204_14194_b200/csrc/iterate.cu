@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   const double* R0 = a.R0 + static_cast<int64_t>(active ? b : 0) * a.ldr;
   const int32_t* cids = nullptr;
   int nch = 0;
-  const double* G0 = a.G0;  // this block's base table
+  const double* G0b = a.G0;  // kChunked: this block's base table
   if (kChunked) {
     nch = a.chunk_count[b];
     cids = a.chunk_ids + static_cast<int64_t>(b) * a.chunk_list_ld;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         for (int d = 0; d < a.compose_depth; ++d) idx = idx * a.n_compose + cids[min(d, k - 1)];
         const int p = a.compose[idx];
         if (p > 0) {
-          G0 += static_cast<int64_t>(p) * a.base_stride;
+          G0b += static_cast<int64_t>(p) * a.base_stride;
           cids += k;
           nch -= k;
           break;
@@ -235,12 +235,26 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     // while the tie pass and the second barrier run -- unless the buffer
     // already holds that atom's complete row (per-block geometries re-select
     // the previous atom often: 60% of config-3 iterations)
+    // (shared geometries always copy; their base and mbarrier parity come
+    // straight from the parameters and the loop counter at each use)
     const bool issue = !kChunked || guess != held;  // block-uniform
-    const unsigned par = n_copies & 1u;
-    n_copies += issue ? 1u : 0u;
+    const unsigned par_c = n_copies & 1u;
+    if constexpr (kChunked) n_copies += issue ? 1u : 0u;
+    auto parity = [&]() -> unsigned {
+      if constexpr (kChunked)
+        return par_c;
+      else
+        return it & 1;
+    };
+    auto base = [&]() -> const double* {
+      if constexpr (kChunked)
+        return G0b;
+      else
+        return a.G0;
+    };
     if (t == 0 && issue) {
       fence_proxy_async_smem();
-      const double* grow = G0 + static_cast<int64_t>(guess) * ldg;
+      const double* grow = base() + static_cast<int64_t>(guess) * ldg;
 #pragma unroll
       for (int sg = 0; sg < kSeg; ++sg) {
         const int j0 = sg * EP / kSeg, j1 = (sg + 1) * EP / kSeg;
@@ -319,7 +333,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
 
     auto wait_all = [&]() {
 #pragma unroll
-      for (int sg = 0; sg < kSeg; ++sg) mbar_wait(&s_bar[sg], par);
+      for (int sg = 0; sg < kSeg; ++sg) mbar_wait(&s_bar[sg], parity());
     };
     // ---- rank-1 update fused with the next iteration's running max; the row
     // source is block-uniform, so each source gets its own unrolled loop
@@ -334,7 +348,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         for (int sg = 0; sg < kSeg; ++sg)
           if (j == sg * EP / kSeg) {
             pre(sg);
-            if constexpr (decltype(staged)::value) mbar_wait(&s_bar[sg], par);  // segment arrives
+            if constexpr (decltype(staged)::value) mbar_wait(&s_bar[sg], parity());  // segment arrives
           }
         const double2 g = row_pair(j);
         const double2 dd = dpair(j);
@@ -389,7 +403,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         // compose in the staging buffer (each thread only touches its own pairs)
         if (issue) wait_all();  // retire the copy before touching the buffer
         if (!issue || u != guess) {
-          const double* urow = G0 + static_cast<int64_t>(u) * ldg + 2 * t;
+          const double* urow = base() + static_cast<int64_t>(u) * ldg + 2 * t;
 #pragma unroll 4
           for (int j = 0; j < EP; ++j) s_row[j * NT + t] = ldg2(urow + 2 * j * NT);
         }
@@ -431,7 +445,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       update([&](int j) { return s_row[j * NT + t]; }, Staged{}, no_pre);
     } else {
       wait_all();  // retire the mispredicted copy before the next one
-      const double* urow = G0 + static_cast<int64_t>(u) * ldg + 2 * t;
+      const double* urow = base() + static_cast<int64_t>(u) * ldg + 2 * t;
       update([&](int j) { return ldg2(urow + 2 * j * NT); }, Direct{}, no_pre);
     }
     if (kRecord) {
