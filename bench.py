@@ -167,6 +167,7 @@ def cpu_baseline(cid: int, seconds: float, steps: int = 1, warmup: int = 0, spec
     rate = float(np.median([v[0] for v in vals]))
     blocks, wall = vals[-1][1], vals[-1][2]
     return {"value": rate, "unit": "blocks/s", "cores": procs, "kind": "port",
+            "ms_per_sample": float(np.median([v[2] for v in vals])) * 1e3,
             "sample": (f"{blocks} blocks of config {cid} per step ({procs} processes x 1 BLAS "
                        f"thread, ~{wall:.1f} s wall), oracle/fase_oracle.py port of the reference "
                        f"fase_extrapolate+apply_model with tables prebuilt; 1-core "
@@ -178,12 +179,16 @@ def run_reference(args):
     if rank != 0:
         return
     w = wl.WORKLOADS[args.config]
-    base = cpu_baseline(args.config, args.cpu_seconds, steps=args.steps, warmup=args.warmup,
+    # bounded samples: the whole --steps/--warmup run stays within ~2.5 minutes
+    seconds = max(1.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
+    base = cpu_baseline(args.config, seconds, steps=args.steps, warmup=args.warmup,
                         spec=args.dict)
     line = {
         "impl": "reference", "metric": "extrapolated blocks/s", "value": base["value"],
         "unit": "blocks/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        # one step = one bounded sample of the workload on the host cores
+        "ms_per_step": base["ms_per_sample"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None,
         "dtype": "f64" if bench_dictionary(w, args.dict).is_real else "c128",
         "data": "synthetic (seeded, BASELINE Appendix-A generators)",
         "config": workload_config(w, args.gpus, args.dict), "cpu_baseline": base,
