@@ -477,7 +477,7 @@ def conceal_image(image, lost_mask, *, dict_spec: str = "dft",
     """
     import torch
 
-    from .fast import GramTable, build_gram_tables, provenance_hash
+    from .fast import GramTable, build_gram_tables
     from .grid import build_weight_field
     from .transform import fft_gram_table
 
@@ -531,8 +531,7 @@ def conceal_image(image, lost_mask, *, dict_spec: str = "dft",
             tab = None
             if shared:
                 w = build_weight_field(msk[0], config.rho_hat)
-                key = provenance_hash(d, w)
-                if isinstance(tables, GramTable) and tables.provenance == key:
+                if isinstance(tables, GramTable) and tables.matches(d, w):
                     tab = tables
                     reused = 1
                 elif use_fft and len(d.tagged_indices()) == len(d):

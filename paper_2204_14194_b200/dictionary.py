@@ -37,6 +37,7 @@ from __future__ import annotations
 
 import hashlib
 import struct
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -506,10 +507,33 @@ def union_dictionaries(parts) -> Dictionary:
     return out
 
 
+# Generated dictionaries are immutable and deterministic in (spec, M, N): the
+# most recent ones are kept, so repeated calls (one per area shape in every
+# conceal_image call) reuse the atoms, their content hash and device copies.
+_SPEC_CACHE: "OrderedDict[tuple, Dictionary]" = OrderedDict()
+_SPEC_CACHE_SIZE = 8
+
+
 def parse_dict_spec(spec: str, m_rows: int, n_cols: int) -> Dictionary:
     """Resolve ``kind`` | ``union:a+b[+c]`` | ``file:PATH`` | ``gauss:K:SEED``
-    against an M x N area (``dictionary.py:197-219`` plus the gauss form)."""
+    against an M x N area (``dictionary.py:197-219`` plus the gauss form).
+    Generated (non-file) dictionaries are memoized per (spec, M, N)."""
     spec = spec.strip()
+    if spec.startswith("file:"):
+        return _parse_dict_spec(spec, m_rows, n_cols)
+    key = (spec, int(m_rows), int(n_cols))
+    hit = _SPEC_CACHE.get(key)
+    if hit is not None:
+        _SPEC_CACHE.move_to_end(key)
+        return hit
+    d = _parse_dict_spec(spec, m_rows, n_cols)
+    _SPEC_CACHE[key] = d
+    while len(_SPEC_CACHE) > _SPEC_CACHE_SIZE:
+        _SPEC_CACHE.popitem(last=False)
+    return d
+
+
+def _parse_dict_spec(spec: str, m_rows: int, n_cols: int) -> Dictionary:
     if spec.startswith("file:"):
         loaded = load_dictionary(spec[5:])
         if loaded.shape != (m_rows, n_cols):

@@ -22,6 +22,7 @@ so per-block tables are never materialized.
 
 from __future__ import annotations
 
+import functools
 import hashlib
 import struct
 from dataclasses import dataclass
@@ -62,9 +63,14 @@ def _torch():
     return torch
 
 
+@functools.lru_cache(maxsize=1)
+def _cuda_available() -> bool:
+    return bool(_torch().cuda.is_available())
+
+
 def resolve_device(device=None):
     torch = _torch()
-    if not torch.cuda.is_available():
+    if not _cuda_available():
         raise NativeLibraryError("a CUDA device is required: the FaSE hot path has no CPU fallback")
     if device is None:
         return torch.device("cuda", torch.cuda.current_device())
@@ -97,8 +103,14 @@ class GramTable:
     Rows are zero-padded to the recursion kernel's capacity.
     """
 
-    def __init__(self, c=None, d=None, provenance: int = 0, *, G=None, D=None, n_alive=None):
-        self.provenance = int(provenance)
+    def __init__(self, c=None, d=None, provenance: int = 0, *, G=None, D=None, n_alive=None,
+                 source=None):
+        # ``source`` = (dictionary, weight) of a table built here: the
+        # provenance digest (a blake2b pass over every atom) is computed only
+        # when someone asks for it, and ``matches`` recognizes the same pair
+        # without hashing
+        self._provenance = None if source is not None else int(provenance)
+        self._source = source
         self._G = G
         self._D = D
         self._host_c = None
@@ -121,6 +133,21 @@ class GramTable:
             self._k = int(G.shape[0])
             self._n_alive = int(n_alive) if n_alive is not None else None
             self._complex = bool(G.is_complex())
+
+    @property
+    def provenance(self) -> int:
+        if self._provenance is None:
+            self._provenance = provenance_hash(*self._source)
+        return self._provenance
+
+    def matches(self, dictionary: Dictionary, weight) -> bool:
+        """True when this table was built for (dictionary, weight): the
+        reference's provenance comparison (``fast.py:198-208``)."""
+        if self._source is not None and self._source[0] is dictionary:
+            w = np.asarray(weight, dtype=np.float64).ravel()
+            if w.shape == self._source[1].shape and np.array_equal(w, self._source[1]):
+                return True
+        return self.provenance == provenance_hash(dictionary, weight)
 
     @property
     def size(self) -> int:
@@ -343,7 +370,7 @@ def build_gram_tables(dictionary: Dictionary, weight, *, block: int = 256, count
     if counter is not None:
         counter.table_pair_products(M, (K * K + K) // 2)
         counter.table_normalizers(K)
-    return GramTable(G=G, D=D, provenance=provenance_hash(dictionary, w), n_alive=int(alive.item()))
+    return GramTable(G=G, D=D, source=(dictionary, w.copy()), n_alive=int(alive.item()))
 
 
 def initial_scalar_products(signal, weight, dictionary: Dictionary, *, counter=None,
@@ -479,8 +506,14 @@ class ChunkedTables:
         self.counts = torch.from_numpy(counts).to(device)
         self.ids = torch.from_numpy(lists).to(device)
         self.masks = masks
-        self.key = (dictionary.content_hash(), masks.shape, hashlib.blake2b(
-            np.packbits(masks).tobytes(), digest_size=16).hexdigest(), rho_hat)
+        self._dictionary = dictionary
+
+    @property
+    def key(self):
+        """(dictionary content hash, mask shape, mask digest, rho_hat): an
+        identity for caching these tables (hashed on first use)."""
+        return (self._dictionary.content_hash(), self.masks.shape, hashlib.blake2b(
+            np.packbits(self.masks).tobytes(), digest_size=16).hexdigest(), self.rho_hat)
 
     @staticmethod
     def table_bytes(dictionary: Dictionary, masks: np.ndarray) -> int:
@@ -551,7 +584,7 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
             raise StaleTableError("per-block tables given for a shared geometry")
         if tables.size != K:
             raise StaleTableError(f"tables hold {tables.size} atoms, dictionary has {K}")
-        if tables.provenance != provenance_hash(dictionary, w):
+        if not tables.matches(dictionary, w):
             raise StaleTableError("table provenance mismatch: tables were built for a different "
                                   "dictionary/weight combination")
         if tables.n_alive == 0:
@@ -664,7 +697,7 @@ class ExtrapolationPlan:
             tables = build_gram_tables(dictionary, w, device=dev)
         if tables.size != len(dictionary):
             raise StaleTableError(f"tables hold {tables.size} atoms, dictionary has {len(dictionary)}")
-        if tables.provenance != provenance_hash(dictionary, w):
+        if not tables.matches(dictionary, w):
             raise StaleTableError("table provenance mismatch")
         if tables.n_alive == 0:
             raise NoSelectableAtomError("every atom has zero weighted energy")
@@ -978,7 +1011,7 @@ def fase_extrapolate(signal, mask, dictionary: Dictionary, tables: GramTable,
     if tables.size != len(dictionary):
         raise StaleTableError(f"tables hold {tables.size} atoms, dictionary has {len(dictionary)}")
     w = build_weight_field(mask, config.rho_hat)
-    if tables.provenance != provenance_hash(dictionary, w):
+    if not tables.matches(dictionary, w):
         raise StaleTableError("table provenance mismatch: tables were built for a different "
                               "dictionary/weight combination")
     if tables.n_alive == 0:

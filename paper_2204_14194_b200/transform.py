@@ -25,7 +25,7 @@ import numpy as np
 from . import _native
 from .dictionary import Dictionary
 from .errors import ShapeError, UnsupportedDictionaryError
-from .fast import GramTable, initial_scalar_products, provenance_hash, resolve_device
+from .fast import GramTable, initial_scalar_products, resolve_device
 from .grid import as_real_field
 
 FFT_MIN_TAGGED = 64
@@ -137,7 +137,8 @@ def fft_gram_table(weight, dictionary: Dictionary, *, device=None) -> GramTable:
     D = torch.empty(k, dtype=torch.float64, device=dev)
     alive = torch.zeros(1, dtype=torch.int32, device=dev)
     _native.gram_finish_complex(T, k, D, alive)
-    return GramTable(G=T, D=D, provenance=provenance_hash(dictionary, w), n_alive=int(alive.item()))
+    return GramTable(G=T, D=D, source=(dictionary, np.asarray(w, dtype=np.float64).ravel().copy()),
+                     n_alive=int(alive.item()))
 
 
 __all__ = ["FFT_MIN_TAGGED", "fft_gram_table", "fft_initial_products", "weighted_spectra"]
