@@ -517,8 +517,29 @@ const Variant kPairVariants[] = {
 const Variant kExtraVariants[] = {
     FASE_V(256, 8, 5, true),
     FASE_V(128, 36, 3, true),
+    FASE_V(576, 4, 1, true),
+};
+
+// Latency variants: batches of at most one block per SM gain nothing from
+// residency, so each block gets the widest CTA that keeps three pairs per
+// thread (config 0, K = 2304: 384 threads, 113 -> 98 us for 100 iterations).
+const Variant kLatencyVariants[] = {
+    FASE_V(384, 6, 1, true),
+    FASE_V(768, 6, 1, true),
+    FASE_V(1024, 8, 1, true),
 };
 #undef FASE_V
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, count = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return 148;
+    return count;
+  }();
+  return n;
+}
 
 const Variant* pick_variant(int K) {
   for (const Variant& v : kVariants)
@@ -537,6 +558,8 @@ const Variant* override_variant(int K, const Variant* dflt) {
   for (const Variant& v : kVariants)
     if (match(v)) return &v;
   for (const Variant& v : kExtraVariants)
+    if (match(v)) return &v;
+  for (const Variant& v : kLatencyVariants)
     if (match(v)) return &v;
   return dflt;
 }
@@ -592,7 +615,13 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
     set_error("fase_iterate: R_log recording is not available with chunked tables");
     return FASE_ERR_UNSUPPORTED;
   }
-  const Variant* v = override_variant(a.K, pick_variant(a.K));
+  const Variant* dflt = pick_variant(a.K);
+  const Variant* v = override_variant(a.K, dflt);
+  const bool small = a.B <= sm_count();  // at most one block per SM
+  if (v == dflt && dflt && small && !getenv("FASE_ITERATE_VARIANT")) {
+    for (const Variant& lv : kLatencyVariants)
+      if (lv.nt * lv.ept >= a.K && lv.nt * lv.ept <= dflt->nt * dflt->ept && lv.nt > v->nt) v = &lv;
+  }
   if (!v) {
     set_error("fase_iterate: K=%d exceeds the largest kernel variant (%d atoms)", a.K,
               fase_max_atoms());
@@ -603,7 +632,7 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
               v->nt * v->ept, static_cast<long long>(a.ldg));
     return FASE_ERR_SHAPE;
   }
-  if (!a.chunk_count && !a.R_log && a.ldd == 0) {
+  if (!a.chunk_count && !a.R_log && a.ldd == 0 && !small) {
     // FASE_ITERATE_PAIR: 0 disables pairing, NT picks the half size (measurement)
     const char* env = getenv("FASE_ITERATE_PAIR");
     const int want = env ? atoi(env) : 256;

@@ -569,8 +569,15 @@ extern "C" int fase_iterate_complex(const fase_iterate_args* args, void* stream)
               "(ldg=%lld)", v->nt * v->ep, static_cast<long long>(a.ldg));
     return FASE_ERR_SHAPE;
   }
-  if (!a.chunk_count && !a.R_log && a.ldd == 0) {
-    // FASE_ITERATE_PAIR: 0 disables pairing (measurement)
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (!a.chunk_count && !a.R_log && a.ldd == 0 && a.B > sms) {
+    // FASE_ITERATE_PAIR: 0 disables pairing (measurement); batches of at most
+    // one block per SM are not paired (pairs would halve the CTAs)
     const char* env = getenv("FASE_ITERATE_PAIR");
     if (!env || atoi(env) != 0)
       for (const Variant& pv : kPairVariants)

@@ -317,10 +317,11 @@ def test_complex_recursion_bit_exact_paired_blocks(k_rand, copies):
     phi = d.values.reshape(len(d), -1)
     c, dd = orc.gram(phi, w)
     tables = GramTable(c=c, d=dd, provenance=provenance_hash(d, build_weight_field(mask, cfg.rho_hat)))
-    sig = rng.uniform(0, 255, (3, m, n))
-    r0 = np.stack([orc.initial_products(sig[b], w, phi) for b in range(3)])
+    nb = 151  # more blocks than SMs (smaller batches are not paired)
+    sig = rng.uniform(0, 255, (nb, m, n))
+    r0 = np.stack([orc.initial_products(sig[b], w, phi) for b in range(nb)])
     res = fase_extrapolate_batch(sig, mask, d, tables, cfg, products=r0, device=DEV)
-    for b in range(3):
+    for b in (0, 1, 2, nb - 2, nb - 1):
         sel, proj, coef, _ = orc.fase_run(r0[b], c, dd, cfg.gamma, cfg.iterations)
         got = res.selected[b].cpu().numpy()
         assert np.array_equal(got, sel), b

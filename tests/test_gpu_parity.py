@@ -547,12 +547,14 @@ def test_recursion_bit_exact_paired_blocks(spec):
     mask = wl.central_loss_mask(16, 16, 6, 6)
     cfg = ExtrapConfig(25, 0.5, 0.8)
     tables, (c, dd) = host_tables(d, mask, cfg.rho_hat)
-    sig = np.random.default_rng(5).uniform(0, 255, (3, 16, 16))
+    # more blocks than SMs (smaller batches run one wide CTA per block)
+    nb = 151
+    sig = np.random.default_rng(5).uniform(0, 255, (nb, 16, 16))
     w = orc.weight_field(mask, cfg.rho_hat)
     vals = d.real_values().reshape(len(d), -1).astype(np.complex128)
-    r0 = np.stack([orc.initial_products(sig[b], w, vals) for b in range(3)])
+    r0 = np.stack([orc.initial_products(sig[b], w, vals) for b in range(nb)])
     res = fase_extrapolate_batch(sig, mask, d, tables, cfg, products=r0.real, device=DEV)
-    for b in range(3):
+    for b in (0, 1, 2, 77, nb - 2, nb - 1):
         sel, proj, coef, _ = orc.fase_run(r0[b], c, dd, cfg.gamma, cfg.iterations)
         assert np.array_equal(res.selected[b].cpu().numpy(), sel)
         assert np.array_equal(res.coefficients[b].cpu().numpy(), coef.real)
