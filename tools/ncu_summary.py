@@ -1,6 +1,6 @@
 """Summarise ncu reports (read here, captured on the B200 via gpurun).
 
-    python tools/ncu_summary.py OUT_PREFIX REPORT.ncu-rep [REPORT2 ...] [--launches launches.csv]
+    python tools/ncu_summary.py OUT_PREFIX REPORT.ncu-rep|REPORT.raw.csv [...] [--launches launches.csv]
 
 Writes OUT_PREFIX.md (human summary) and merges per-kernel DRAM traffic into
 profiles/ncu_summary.json under "<tag>/<kernel>", tag = the suffix after
@@ -56,8 +56,13 @@ METRICS = [
 
 
 def raw_rows(rep: str):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    """Rows of a report's raw page: from the .ncu-rep (ncu -i), or from a CSV
+    already exported with ``ncu -i REP --page raw --csv`` on the GPU box."""
+    if rep.endswith(".csv"):
+        out = Path(rep).read_text()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     return [(dict(zip(hdr, r)), dict(zip(hdr, units))) for r in rows[2:]]
