@@ -723,7 +723,8 @@ def run_gpu_frame(args):
                            "overlapped on separate streams; no L2 flush (tables >> L2)"},
             "roofline": {"bound": "hbm", "kernel": "fase_iterate_kernel (chunked rows)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": None, "algorithmic_bytes_per_launch": bytes_iter,
+                         "traffic": ncu_traffic("fase_iterate_kernel", f"c{args.config}"),
+                         "algorithmic_bytes_per_launch": bytes_iter,
                          "ms_per_launch": it_s * 1e3, "peak_source": hsrc,
                          "streamed_bytes_per_launch": streamed,
                          "streamed_gbs": streamed / it_s / 1e9,
