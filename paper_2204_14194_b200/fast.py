@@ -46,7 +46,7 @@ from .grid import (
     base_weight,
     build_weight_field,
 )
-from .model import BatchResult, IterationTrace, SparseModel
+from .model import BatchResult, SparseModel
 
 # Chunked per-block tables beyond this many bytes switch to one table per
 # distinct geometry (see _run_grouped).

@@ -22,7 +22,6 @@ from paper_2204_14194_b200 import (  # noqa: E402
     GramTable,
     NoSelectableAtomError,
     StaleTableError,
-    UnsupportedDictionaryError,
     build_gram_tables,
     build_weight_field,
     fase_extrapolate,
