@@ -52,6 +52,9 @@ namespace fase {
 namespace {
 
 constexpr unsigned kNone = 0xffffffffu;
+#ifdef FASE_ITERATE_STATS
+__device__ unsigned long long g_stats[8];  // measurement build: chunked-path counters
+#endif
 
 // Dead atoms (D == 0, and the padding past K) carry d = -inf: their metric
 // |R| * d is -inf (NaN when R == 0), which never wins a '>' comparison and
@@ -83,6 +86,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   // update can start on the first segment while the rest is still in flight.
   constexpr int kSeg = EP < 3 ? EP : 3;
   __shared__ __align__(8) uint64_t s_bar_all[NB][kSeg];
+  __shared__ double s_heldm_all[NB];  // kChunked: metric of the held atom after the update
   extern __shared__ double2 s_dyn[];
 
   const int half = NB == 1 ? 0 : static_cast<int>(threadIdx.x) / NT;
@@ -237,6 +241,19 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     // the previous atom often: 60% of config-3 iterations)
     // (shared geometries always copy; their base and mbarrier parity come
     // straight from the parameters and the loop counter at each use)
+    if constexpr (kChunked) {
+      // predict the tie rule's pick: the held atom, when it reaches this
+      // iteration's threshold and precedes the argmax (the rule takes the
+      // lowest index at or above the threshold; structural near-ties make the
+      // argmax a poor guess: 44% of config-3 copies were mispredicted)
+      if (held != kNone && held < guess) {
+        const double top_ = __longlong_as_double(top_key);
+        double q_ = q;
+        if (top_key > 0 && top_key < 0x7ff0000000000000LL) q_ = fmax(q_, mul_rn(1e-13, top_));
+        const double thr_ = q_ > 0.0 ? sub_rn(top_, q_) : top_;
+        if (s_heldm_all[half] >= thr_) guess = held;
+      }
+    }
     const bool issue = !kChunked || guess != held;  // block-uniform
     const unsigned par_c = n_copies & 1u;
     if constexpr (kChunked) n_copies += issue ? 1u : 0u;
@@ -370,6 +387,17 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     using Direct = std::false_type;
     auto no_pre = [](int) {};
     if constexpr (kChunked) {
+#ifdef FASE_ITERATE_STATS
+      if (t == 0) {  // measurement build only: path counters
+        atomicAdd(&g_stats[0], 1ull);
+        atomicAdd(&g_stats[1], issue ? 1ull : 0ull);
+        atomicAdd(&g_stats[2], (!issue && u == held) ? 1ull : 0ull);
+        atomicAdd(&g_stats[3], (issue && u != guess) ? 1ull : 0ull);
+        atomicAdd(&g_stats[4], static_cast<unsigned long long>(nch));
+        atomicAdd(&g_stats[5], (!issue && u != held) ? 1ull : 0ull);
+        atomicAdd(&g_stats[6], (issue && u == guess) ? static_cast<unsigned long long>(nch) : 0ull);
+      }
+#endif
       // row_u of this block = G0[u] - sum of its remaining chunk tables' rows,
       // element by element in list order; the complete row is left in the
       // staging buffer (held) for a re-selection of u
@@ -441,6 +469,21 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         fence_proxy_async_smem();  // generic writes above precede the next TMA fill
       }
       held = u;
+      {  // publish the held atom's new metric for the next prediction
+        const int pr = static_cast<int>(u >> 1);
+        if (pr % NT == t) {
+          const int jj = pr / NT;
+          double rv = 0.0, dv = 0.0;
+#pragma unroll
+          for (int j = 0; j < EP; ++j)
+            if (j == jj) {  // static register indices
+              const double2 dd = dpair(j);
+              rv = (u & 1u) ? r[j][1] : r[j][0];
+              dv = (u & 1u) ? dd.y : dd.x;
+            }
+          s_heldm_all[half] = mul_rn(fabs(rv), dv);
+        }
+      }
     } else if (u == guess) {  // block-uniform
       update([&](int j) { return s_row[j * NT + t]; }, Staged{}, no_pre);
     } else {
@@ -654,3 +697,16 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
   fn<<<(a.B + v->nb - 1) / v->nb, v->nt * v->nb, smem, as_stream(stream)>>>(a);
   return check_launch("fase_iterate");
 }
+
+#ifdef FASE_ITERATE_STATS
+// measurement build only: chunked-path counters since the last call
+// (iterations, copies issued, held hits, mispredicted copies, remaining chunks,
+// held misses without a copy, remaining chunks on predicted copies)
+extern "C" __attribute__((visibility("default"))) int fase_iterate_stats(unsigned long long* out8) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out8, fase::g_stats, 8 * sizeof(unsigned long long));
+  unsigned long long zero[8] = {0};
+  cudaMemcpyToSymbol(fase::g_stats, zero, sizeof(zero));
+  return check_launch("fase_iterate_stats");
+}
+#endif
