@@ -386,6 +386,14 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     using Staged = std::true_type;
     using Direct = std::false_type;
     auto no_pre = [](int) {};
+#ifdef FASE_ITERATE_STATS
+    if constexpr (!kChunked) {
+      if (t == 0) {
+        atomicAdd(&g_stats[0], 1ull);
+        atomicAdd(&g_stats[3], u != guess ? 1ull : 0ull);
+      }
+    }
+#endif
     if constexpr (kChunked) {
 #ifdef FASE_ITERATE_STATS
       if (t == 0) {  // measurement build only: path counters
