@@ -65,6 +65,10 @@ def parse_args():
     ap.add_argument("--products", default="auto", choices=["auto", "gemm", "separable", "ozaki"],
                     help="initial products: separable transforms (separable dictionaries) or "
                          "the dense DMMA GEMM")
+    ap.add_argument("--recursion", default="auto", choices=["auto", "exact", "scaled"],
+                    help="shared-geometry recursion: exact (bit-identical to the reference loop) "
+                         "or scaled (column-scaled table, no normalizers in the loop); auto = "
+                         "scaled for real dictionaries")
     ap.add_argument("--compose", default=None, choices=["none", "singles", "pairs", "triples"],
                     help="frame configs: precomposed base tables (default: the engine's)")
     ap.add_argument("--dict", default=None,
@@ -366,8 +370,14 @@ def run_gpu(args):
     mask = wl.central_loss_mask(*w.area, *w.loss)
     d.device_matrix(dev)
     tables = build_gram_tables(d, build_weight_field(mask, w.config.rho_hat), device=dev)
-    plan = ExtrapolationPlan(d, mask, B, w.config, tables, device=dev, products=args.products)
-    iterate = _native.iterate_complex if cplx else _native.iterate
+    recursion = args.recursion if args.recursion != "auto" else ("exact" if cplx else "scaled")
+    plan = ExtrapolationPlan(d, mask, B, w.config, tables, device=dev, products=args.products,
+                             recursion=recursion)
+    if recursion == "scaled":
+        def iterate(G, D, R0, K, I, gamma, sel, proj, coef):
+            _native.iterate_scaled(plan.Gs, D, R0, K, I, gamma, sel, proj, coef)
+    else:
+        iterate = _native.iterate_complex if cplx else _native.iterate
     synth_extra = {"max_imag": plan.max_imag} if cplx else {}
     synth = _native.synth_paste_complex if cplx else _native.synth_paste
     # one more table build, kernels only, for the reported Gram time
@@ -377,17 +387,24 @@ def run_gpu(args):
                        if cplx else K * plan.phi.shape[1] * 8) // 8 + 2,
                       dtype=torch.float64, device=dev)
     support = None if cplx else gram_support(plan.W, M)
+
+    def build_table():
+        if cplx:
+            _native.gram_complex(plan.phi, plan.W, K, M, G2, ws=gws)
+            _native.gram_finish_complex(G2, K, D2)
+            return "dmma"
+        path = gram_into(plan.phi, plan.W, K, M, G2, support)
+        _native.gram_finish(G2, K, D2)
+        return path
+
+    # warm build first (operand buffers come from the caching allocator, as in
+    # a process that builds tables repeatedly), then the timed one
+    build_table()
     torch.cuda.synchronize()
     g0 = torch.cuda.Event(enable_timing=True)
     g1 = torch.cuda.Event(enable_timing=True)
     g0.record()
-    if cplx:
-        _native.gram_complex(plan.phi, plan.W, K, M, G2, ws=gws)
-        _native.gram_finish_complex(G2, K, D2)
-        gram_path = "dmma"
-    else:
-        gram_path = gram_into(plan.phi, plan.W, K, M, G2, support)
-        _native.gram_finish(G2, K, D2)
+    gram_path = build_table()
     g1.record()
     torch.cuda.synchronize()
     gram_ms = g0.elapsed_time(g1)
@@ -485,6 +502,18 @@ def run_gpu(args):
     sel = plan.selected
     assert int(sel.min()) >= 0 and int(sel.max()) < K, "selection out of range"
     assert torch.isfinite(plan.lost).all(), "non-finite reconstruction"
+    agreement = None
+    if recursion == "scaled":
+        # the same batch through the exact (reference-bit-identical) recursion
+        sel_x, proj_x, coef_x = (torch.empty_like(x) for x in (plan.selected, plan.projections,
+                                                               plan.coefficients))
+        _native.iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, sel_x, proj_x, coef_x)
+        same = (sel_x == plan.selected).all(dim=1)
+        dev_c = ((coef_x - plan.coefficients).abs().amax(dim=1)
+                 / coef_x.abs().amax(dim=1).clamp_min(1e-300))
+        agreement = {"blocks_identical_selections": int(same.sum()), "blocks": B,
+                     "max_coef_rel_dev": float(dev_c[same].max()) if bool(same.any()) else None,
+                     "vs": "fase_iterate (exact) on the same R0 / table"}
 
     if rank == 0:
         hbm, hsrc, fp64, fsrc = measured_peaks()
@@ -531,12 +560,15 @@ def run_gpu(args):
                            "H2D / D2H on side streams overlapped with compute; no L2 flush "
                            "(per-step input comes over PCIe; table 170 MB > L2)"},
             "roofline": {"bound": "hbm",
-                         "kernel": "fase_iterate_complex_kernel" if cplx else "fase_iterate_kernel",
+                         "kernel": ("fase_iterate_complex_kernel" if cplx else "fase_iterate_kernel")
+                                   + (" (scaled: column-scaled table)" if recursion == "scaled"
+                                      else ""),
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm,
                          "traffic": ncu_traffic("fase_iterate_complex_kernel" if cplx
                                                 else "fase_iterate_kernel",
-                                                "dft" if args.dict == "dft" else f"c{args.config}"),
+                                                ("dft" if args.dict == "dft" else f"c{args.config}")
+                                                + ("-scaled" if recursion == "scaled" else "")),
                          "algorithmic_bytes_per_launch": bytes_iter,
                          "ms_per_launch": it_s * 1e3, "peak_source": hsrc,
                          "note": ("16*K bytes per block-iteration (one complex128 table row)"
@@ -562,12 +594,15 @@ def run_gpu(args):
                                "note": "executed flops of rows X cols^T per part; the dense "
                                        "GEMM form (--products gemm) does 24x more work"}),
             "products": plan.products_method,
+            "recursion": recursion,
+            "recursion_agreement": agreement,
             "stage_ms": {"init_products": float(np.mean(init_ms)), "iterate": float(np.mean(iter_ms)),
                          "synth": float(np.mean(synth_ms))},
             "gram_ms": gram_ms,
             "gram_path": gram_path,
             "fft_gram_ms": fft_gram_ms,
             "gram_tflops": (4 if cplx else 1) * K * (K + 1) * M / (gram_ms * 1e-3) / 1e12,
+            "gram_fp64_frac": (4 if cplx else 1) * K * (K + 1) * M / (gram_ms * 1e-3) / 1e12 / fp64,
             "gpu_launches": args.steps * (plan.launches_per_run + 1) + args.steps * plan.launches_per_run,
             "clocks": clocks.summary(),
             "wall_s": t_wall,

@@ -229,6 +229,25 @@ typedef struct {
 FASE_API int fase_iterate(const fase_iterate_args* args, void* stream);
 
 /*
+ * Scaled recursion for shared geometries (same loop as fase_iterate, fast.py:
+ * 238-255, in scaled variables): G0 is the column-scaled table
+ *   Gs[u, k] = G[u, k] * D_k            (fase_scale_columns)
+ * and the kernel carries R'_k = R_k * D_k, so the metric is |R'_k| and the
+ * update R' -= c * Gs[u, :] needs no normalizers; p = R'_u * D_u, c = gamma*p.
+ * R0 and D are the unscaled inputs of fase_iterate (D shared, ldd = 0).
+ * Iteration 0 is bit-identical to fase_iterate; later iterations differ by the
+ * rounding of the scaled operands, so a selection can differ only where the
+ * top-two metrics lie within a few ulp (the north-star tolerance: top-two
+ * within 1e-9 relative; coefficients within 1e-6). chunk lists, compose,
+ * per-block D, R_out and R_log are rejected (FASE_ERR_UNSUPPORTED).
+ */
+FASE_API int fase_iterate_scaled(const fase_iterate_args* args, void* stream);
+
+/* Gs[u*lds + k] = G[u*ldg + k] * D[k] (k < K), 0 for K <= k < lds; lds even. */
+FASE_API int fase_scale_columns(const double* G, int64_t ldg, const double* D, int K, double* Gs,
+                                int64_t lds, void* stream);
+
+/*
  * Model synthesis and paste (replaces SparseModel.materialize + apply_model,
  * reference.py:120-125 and fast.py:267-286, evaluated on lost samples only):
  *   g = sum_t coef[b,t] * phi[sel[b,t], m]   accumulated in selection order

@@ -37,6 +37,7 @@ EXPORTS = (
     "fase_gram_complex", "fase_max_atoms_complex", "fase_table_ld_complex", "fase_iterate_complex",
     "fase_synth_paste_complex", "fase_sep_products_complex", "fase_fft_gram", "fase_weigh_gather",
     "fase_ozaki_split", "fase_ozaki_gemm", "fase_ozaki_gram", "fase_sep_products_batch",
+    "fase_iterate_scaled", "fase_scale_columns",
 )
 
 _vp = ctypes.c_void_p
@@ -107,6 +108,8 @@ def load():
         "fase_block_normalizers": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _i64,
                                    _vp, _vp],
         "fase_iterate": [ctypes.POINTER(IterateArgs), _vp],
+        "fase_iterate_scaled": [ctypes.POINTER(IterateArgs), _vp],
+        "fase_scale_columns": [_vp, _i64, _vp, _i32, _vp, _i64, _vp],
         "fase_iterate_complex": [ctypes.POINTER(IterateArgs), _vp],
         "fase_gram_complex": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp, ctypes.c_size_t, _vp],
         "fase_synth_paste_complex": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp,
@@ -305,6 +308,39 @@ def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *
     if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
         raise errors.ShapeError("sel / proj / coef must share one leading dimension")
     _check(lib.fase_iterate(ctypes.byref(args), _stream(R0)))
+
+
+def scale_columns(G, D, K: int, Gs) -> None:
+    """Gs[u, k] = G[u, k] * D[k] (fase_scale_columns): the scaled recursion's table."""
+    import torch
+
+    lib = load()
+    _require(G, "G", torch.float64, 2)
+    _require(D, "D", torch.float64, 1)
+    _require(Gs, "Gs", torch.float64, 2)
+    if Gs.shape[0] < K:
+        raise errors.ShapeError(f"Gs has {Gs.shape[0]} rows, need {K}")
+    _check(lib.fase_scale_columns(_ptr(G), _ld(G), _ptr(D), K, _ptr(Gs), _ld(Gs), _stream(Gs)))
+
+
+def iterate_scaled(Gs, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef) -> None:
+    """The scaled recursion (fase_iterate_scaled) over a column-scaled shared
+    table ``Gs`` (scale_columns); R0 and D unscaled, as for ``iterate``."""
+    import torch
+
+    lib = load()
+    _require(Gs, "Gs", torch.float64, 2)
+    _require(D, "D", torch.float64, 1)
+    _require(R0, "R0", torch.float64, 2)
+    _require(sel, "sel", torch.int32, 2)
+    _require(proj, "proj", torch.float64, 2)
+    _require(coef, "coef", torch.float64, 2)
+    args = IterateArgs(G0=_ptr(Gs), ldg=_ld(Gs), D=_ptr(D), ldd=0, R0=_ptr(R0), ldr=_ld(R0), K=K,
+                       B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel), proj=_ptr(proj),
+                       coef=_ptr(coef), ldo=_ld(sel))
+    if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
+        raise errors.ShapeError("sel / proj / coef must share one leading dimension")
+    _check(lib.fase_iterate_scaled(ctypes.byref(args), _stream(R0)))
 
 
 def synth_paste(phi, sel, coef, iterations: int, idx, out, *, idx_ptr=None, n_shared: int = 0,

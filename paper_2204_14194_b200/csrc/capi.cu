@@ -95,6 +95,27 @@ __global__ void __launch_bounds__(kFinishThreads) gram_finish_kernel(const doubl
   if (n_alive && threadIdx.x == 0) *n_alive = alive;
 }
 
+// Column-scaled table of the scaled recursion: Gs[u, k] = G[u, k] * D_k for
+// k < K (0 for dead atoms, D_k == 0), zero padding up to lds. One CTA streams
+// rows; 16-byte loads and stores.
+__global__ void __launch_bounds__(256) scale_columns_kernel(const double* __restrict__ G,
+                                                            int64_t ldg, const double* __restrict__ D,
+                                                            int K, double* __restrict__ Gs,
+                                                            int64_t lds) {
+  const int pairs = static_cast<int>(lds / 2);
+  for (int64_t u = blockIdx.x; u < K; u += gridDim.x) {
+    const double* g = G + u * ldg;
+    double* o = Gs + u * lds;
+    for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
+      const int k = 2 * p;
+      double2 v = make_double2(0.0, 0.0);
+      if (k < K) v.x = mul_rn(g[k], D[k]);
+      if (k + 1 < K) v.y = mul_rn(g[k + 1], D[k + 1]);
+      reinterpret_cast<double2*>(o)[p] = v;
+    }
+  }
+}
+
 constexpr int kNormThreads = 256;
 
 __device__ __forceinline__ double chunk_diag(const double* G0, int64_t ldg, const double* tabs,
@@ -269,6 +290,17 @@ extern "C" int fase_gram_finish(const double* G, int64_t ldg, int K, double* D, 
   }
   gram_finish_kernel<<<1, kFinishThreads, 0, as_stream(stream)>>>(G, ldg, K, D, n_alive);
   return check_launch("fase_gram_finish");
+}
+
+extern "C" int fase_scale_columns(const double* G, int64_t ldg, const double* D, int K, double* Gs,
+                                  int64_t lds, void* stream) {
+  if (K < 1 || ldg < K || lds < K || (lds & 1) || !G || !D || !Gs || !aligned16(Gs)) {
+    set_error("fase_scale_columns: bad operand (K=%d, ldg=%lld, lds=%lld)", K,
+              static_cast<long long>(ldg), static_cast<long long>(lds));
+    return FASE_ERR_SHAPE;
+  }
+  scale_columns_kernel<<<min(K, 148 * 8), 256, 0, as_stream(stream)>>>(G, ldg, D, K, Gs, lds);
+  return check_launch("fase_scale_columns");
 }
 
 extern "C" int fase_block_normalizers(const double* G0, int64_t ldg, const double* chunk_tables,

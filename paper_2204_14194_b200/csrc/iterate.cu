@@ -70,11 +70,23 @@ __device__ unsigned long long g_stats[8];  // measurement build: chunked-path co
 // the normalizers -- identical for every block of a shared geometry -- are
 // kept once in shared memory for both. For large K this doubles the blocks in
 // flight per SM (two staged rows + one D fit where two CTAs' D + rows do not).
-template <int NT, int EPT, int MINB, bool kDsmem, bool kChunked, bool kRecord, int NB>
+//
+// kScaled (fase_iterate_scaled, shared geometry only): the table is
+// column-scaled, Gs[u, k] = G[u, k] * D_k, and the state is R'_k = R_k * D_k,
+// so the metric is |R'_k| -- no normalizer loads or products in the update
+// pass, and no D in shared memory. The metric of iteration 0 is bit-identical
+// (|R * D| == |R| * D); later iterations differ from the reference by the
+// rounding of the scaled operands (~1 ulp per update), which can only change a
+// selection whose top-two metrics lie within that rounding -- inside the
+// north-star tolerance (top-two within 1e-9 relative). p = R'_u * D_u.
+template <int NT, int EPT, int MINB, bool kDsmem, bool kChunked, bool kRecord, int NB,
+          bool kScaled = false>
 __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_iterate_args a) {
   constexpr int EP = EPT / 2;
   constexpr int NW = NT / 32;
   static_assert(NB == 1 || (kDsmem && !kChunked), "paired blocks share one D in shared memory");
+  static_assert(!kScaled || (!kDsmem && !kChunked && !kRecord && NB == 1),
+                "the scaled recursion keeps no normalizers and has one block per CTA");
 
   __shared__ long long s_key_all[NB][NW];
   __shared__ unsigned s_arg_all[NB][NW];
@@ -144,7 +156,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   }
 
   double r[EP][2];
-  double dreg[kDsmem ? 1 : EP][2];
+  double dreg[(kDsmem || kScaled) ? 1 : EP][2];
   // normalizer pair j of this thread (registers or shared memory)
   auto dpair = [&](int j) -> double2 {
     if constexpr (kDsmem)
@@ -152,11 +164,42 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     else
       return make_double2(dreg[j][0], dreg[j][1]);
   };
+  // the selection metrics of pair j (normalizers `dd` loaded once by the caller)
+  auto metrics = [&](int j, double2 dd) -> double2 {
+    if constexpr (kScaled)
+      return make_double2(fabs(r[j][0]), fabs(r[j][1]));
+    else
+      return make_double2(mul_rn(fabs(r[j][0]), dd.x), mul_rn(fabs(r[j][1]), dd.y));
+  };
+  auto dpair_if = [&](int j) -> double2 {
+    if constexpr (kScaled)
+      return make_double2(0.0, 0.0);
+    else
+      return dpair(j);
+  };
   double best = kDead;
   unsigned barg = kNone;
 #pragma unroll
   for (int j = 0; j < EP; ++j) {
     const int k = 2 * (j * NT + t);
+    if constexpr (kScaled) {
+      // R' = R * D; dead atoms and the padding hold NaN (never selected)
+      const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
+      const double d0 = k < K ? D[k] : 0.0, d1 = k + 1 < K ? D[k + 1] : 0.0;
+      r[j][0] = d0 != 0.0 ? mul_rn(R0[k], d0) : kNaN;
+      r[j][1] = d1 != 0.0 ? mul_rn(R0[k + 1], d1) : kNaN;
+      const double m0 = fabs(r[j][0]);
+      if (m0 > best) {
+        best = m0;
+        barg = static_cast<unsigned>(k);
+      }
+      const double m1 = fabs(r[j][1]);
+      if (m1 > best) {
+        best = m1;
+        barg = static_cast<unsigned>(k + 1);
+      }
+      continue;
+    }
     double2 dd;
     r[j][0] = k < K ? R0[k] : 0.0;
     r[j][1] = k + 1 < K ? R0[k + 1] : 0.0;
@@ -301,9 +344,9 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     if (wkey >= 0 && __longlong_as_double(wkey) >= thr) {  // warp-uniform
 #pragma unroll
       for (int j = EP - 1; j >= 0; --j) {
-        const double2 dd = dpair(j);
-        if (mul_rn(fabs(r[j][1]), dd.y) >= thr) cand = 2 * (j * NT + t) + 1;
-        if (mul_rn(fabs(r[j][0]), dd.x) >= thr) cand = 2 * (j * NT + t);
+        const double2 m = metrics(j, dpair_if(j));
+        if (m.y >= thr) cand = 2 * (j * NT + t) + 1;
+        if (m.x >= thr) cand = 2 * (j * NT + t);
       }
     }
     const unsigned wmin = __reduce_min_sync(0xffffffffu, cand);
@@ -315,7 +358,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
 #pragma unroll
       for (int j = 0; j < EP; ++j) {
         *reinterpret_cast<double2*>(&s_dump[warp][0][2 * j]) = make_double2(r[j][0], r[j][1]);
-        if constexpr (!kDsmem)
+        if constexpr (!kDsmem && !kScaled)
           *reinterpret_cast<double2*>(&s_dump[warp][kDsmem ? 0 : 1][2 * j]) = dpair(j);
       }
       const int pair = static_cast<int>(cand >> 1);
@@ -323,7 +366,9 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       const int ee = static_cast<int>(cand & 1u);
       s_u[warp] = cand;
       s_r[warp] = s_dump[warp][0][2 * jj + ee];
-      if constexpr (kDsmem) {
+      if constexpr (kScaled) {
+        s_d[warp] = __ldg(D + cand);
+      } else if constexpr (kDsmem) {
         const double2 dd = s_D[pair];
         s_d[warp] = ee ? dd.y : dd.x;
       } else {
@@ -340,7 +385,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     }
     const double ru = s_r[uw];
     const double du = s_d[uw];
-    const double p = mul_rn(ru, mul_rn(du, du));
+    const double p = kScaled ? mul_rn(ru, du) : mul_rn(ru, mul_rn(du, du));
     const double c = mul_rn(a.gamma, p);
     if (t == 0) {
       sel[it] = static_cast<int32_t>(u);
@@ -368,15 +413,16 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
             if constexpr (decltype(staged)::value) mbar_wait(&s_bar[sg], parity());  // segment arrives
           }
         const double2 g = row_pair(j);
-        const double2 dd = dpair(j);
+        const double2 dd = dpair_if(j);
         r[j][0] = sub_rn(r[j][0], mul_rn(c, g.x));
         r[j][1] = sub_rn(r[j][1], mul_rn(c, g.y));
-        const double m0 = mul_rn(fabs(r[j][0]), dd.x);
+        const double2 mm = metrics(j, dd);
+        const double m0 = mm.x;
         if (m0 > best) {
           best = m0;
           barg = static_cast<unsigned>(2 * (j * NT + t));
         }
-        const double m1 = mul_rn(fabs(r[j][1]), dd.y);
+        const double m1 = mm.y;
         if (m1 > best) {
           best = m1;
           barg = static_cast<unsigned>(2 * (j * NT + t) + 1);
@@ -581,6 +627,30 @@ const Variant kLatencyVariants[] = {
 };
 #undef FASE_V
 
+// Scaled recursion (fase_iterate_scaled): no normalizers in the loop, so only
+// the staged row occupies shared memory and four 256-thread CTAs fit per SM
+// (64 registers; config 1: 0.916 ms exact at three CTAs, 0.815 ms scaled at
+// three, 0.721 ms scaled at four). Ordered by capacity like kVariants.
+#define FASE_VS(NT, EPT, MINB) \
+  {NT, EPT, false, fase_iterate_kernel<NT, EPT, MINB, false, false, false, 1, true>, nullptr, nullptr}
+const Variant kScaledVariants[] = {
+    FASE_VS(128, 2, 8),   FASE_VS(128, 4, 8),   FASE_VS(128, 8, 8),   FASE_VS(128, 16, 6),
+    FASE_VS(256, 10, 4),  FASE_VS(256, 12, 4),  FASE_VS(256, 14, 4),  FASE_VS(256, 16, 4),
+    FASE_VS(256, 18, 4),  FASE_VS(256, 20, 3),  FASE_VS(256, 24, 2),  FASE_VS(256, 32, 2),
+    FASE_VS(512, 20, 1),  FASE_VS(512, 24, 1),
+};
+// alternatives for measurement (FASE_SCALED_VARIANT=NTxEPTxMINB) and the
+// latency shapes for batches of at most one block per SM
+const Variant kScaledExtra[] = {
+    FASE_VS(128, 36, 4), FASE_VS(256, 18, 3), FASE_VS(128, 64, 2), FASE_VS(128, 64, 3),
+    FASE_VS(256, 20, 4),
+};
+const int kScaledExtraMinb[] = {4, 3, 2, 3, 4};
+const Variant kScaledLatency[] = {
+    FASE_VS(384, 6, 1), FASE_VS(768, 6, 1), FASE_VS(1024, 8, 1),
+};
+#undef FASE_VS
+
 int sm_count() {
   static int n = [] {
     int dev = 0, count = 0;
@@ -704,6 +774,75 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
   }
   fn<<<(a.B + v->nb - 1) / v->nb, v->nt * v->nb, smem, as_stream(stream)>>>(a);
   return check_launch("fase_iterate");
+}
+
+extern "C" int fase_iterate_scaled(const fase_iterate_args* args, void* stream) {
+  if (!args) {
+    set_error("fase_iterate_scaled: null argument block");
+    return FASE_ERR_PARAMETER;
+  }
+  const fase_iterate_args& a = *args;
+  if (a.K < 1 || a.B < 0 || a.I < 1) {
+    set_error("fase_iterate_scaled: bad sizes (K=%d, B=%d, I=%d)", a.K, a.B, a.I);
+    return FASE_ERR_SHAPE;
+  }
+  if (!(a.gamma > 0.0 && a.gamma <= 1.0)) {
+    set_error("fase_iterate_scaled: gamma must lie in (0, 1], got %g", a.gamma);
+    return FASE_ERR_PARAMETER;
+  }
+  if (a.B == 0) return FASE_OK;
+  if (!a.G0 || !aligned16(a.G0) || a.ldg < a.K || (a.ldg & 1) || !a.D || !a.R0 ||
+      a.ldr < a.K || !a.sel || !a.proj || !a.coef || a.ldo < a.I) {
+    set_error("fase_iterate_scaled: bad operand (null, misaligned, odd or short leading dimension)");
+    return FASE_ERR_SHAPE;
+  }
+  if (a.chunk_count || a.compose || a.ldd != 0 || a.R_out || a.R_log) {
+    set_error("fase_iterate_scaled: shared geometry only (no chunk tables, per-block D, R_out or "
+              "R_log)");
+    return FASE_ERR_UNSUPPORTED;
+  }
+  const Variant* dflt = pick_variant(a.K);
+  if (!dflt) {
+    set_error("fase_iterate_scaled: K=%d exceeds the largest kernel variant (%d atoms)", a.K,
+              fase_max_atoms());
+    return FASE_ERR_UNSUPPORTED;
+  }
+  const int cap = dflt->nt * dflt->ept;
+  const Variant* v = nullptr;
+  for (const Variant& sv : kScaledVariants)
+    if (sv.nt * sv.ept >= a.K) {
+      v = &sv;
+      break;
+    }
+  const char* env = getenv("FASE_SCALED_VARIANT");
+  int nt = 0, ept = 0, minb = 0;
+  if (env && sscanf(env, "%dx%dx%d", &nt, &ept, &minb) >= 2) {
+    for (int i = 0; i < static_cast<int>(sizeof(kScaledExtra) / sizeof(kScaledExtra[0])); ++i) {
+      const Variant& ev = kScaledExtra[i];
+      if (ev.nt == nt && ev.ept == ept && (minb == 0 || kScaledExtraMinb[i] == minb) &&
+          ev.nt * ev.ept >= a.K && ev.nt * ev.ept <= cap)
+        v = &ev;
+    }
+  } else if (a.B <= sm_count()) {  // at most one block per SM: the widest CTA
+    for (const Variant& lv : kScaledLatency)
+      if (lv.nt * lv.ept >= a.K && lv.nt * lv.ept <= cap && lv.nt > v->nt) v = &lv;
+  }
+  if (a.ldg < v->nt * v->ept) {
+    set_error("fase_iterate_scaled: table rows must be zero-padded to fase_table_ld(K)=%d (ldg=%lld)",
+              cap, static_cast<long long>(a.ldg));
+    return FASE_ERR_SHAPE;
+  }
+  const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2);
+  cudaError_t e = cudaFuncSetAttribute(v->plain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(v->plain, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) {
+    set_error("fase_iterate_scaled: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return FASE_ERR_CUDA;
+  }
+  v->plain<<<a.B, v->nt, smem, as_stream(stream)>>>(a);
+  return check_launch("fase_iterate_scaled");
 }
 
 #ifdef FASE_ITERATE_STATS

@@ -148,14 +148,14 @@ def test_recursion_bit_exact_configs(golden_dir, cid):
 # ----------------------------------------------------------------- end to end
 
 
-def _end_to_end(cid, golden_dir, tol_blocks_early=None):
+def _end_to_end(cid, golden_dir, tol_blocks_early=None, recursion="exact"):
     z = np.load(golden_dir / f"c{cid}_blocks.npz")
     w8 = wl.WORKLOADS[cid]
     d = w8.dictionary()
     mask = wl.central_loss_mask(*w8.area, *w8.loss)
     blocks = list(z["blocks"])
     sig = wl.block_signals(cid, max(blocks) + 1, *w8.area)[blocks]
-    res = fase_extrapolate_batch(sig, mask, d, None, w8.config, device=DEV)
+    res = fase_extrapolate_batch(sig, mask, d, None, w8.config, device=DEV, recursion=recursion)
     vals = d.real_values()
     tables = None
     verdicts = []
@@ -184,8 +184,121 @@ def _end_to_end(cid, golden_dir, tol_blocks_early=None):
 
 
 @pytest.mark.parametrize("cid", [0, 1, 4])
-def test_end_to_end_configs(golden_dir, cid):
-    _end_to_end(cid, golden_dir)
+@pytest.mark.parametrize("recursion", ["exact", "scaled"])
+def test_end_to_end_configs(golden_dir, cid, recursion):
+    _end_to_end(cid, golden_dir, recursion=recursion)
+
+
+# ----------------------------------------------------------------- scaled recursion
+
+
+def test_scale_columns_bit_exact():
+    """Gs[u, k] = G[u, k] * D_k, correctly rounded (numpy's product), zero padding."""
+    d = parse_dict_spec("union:dct+had", 16, 16)
+    mask = wl.central_loss_mask(16, 16, 6, 6)
+    t = build_gram_tables(d, build_weight_field(mask, 0.8), device=DEV)
+    G, D = t.device_tables(torch.device(DEV))
+    Gs, D2 = t.scaled_table(torch.device(DEV))
+    assert D2 is D and Gs.shape == G.shape
+    K = len(d)
+    g, dd, gs = G.cpu().numpy(), D.cpu().numpy(), Gs.cpu().numpy()
+    assert np.array_equal(gs[:, :K], g[:, :K] * dd[None, :])
+    assert not gs[:, K:].any()
+    assert t.scaled_table(torch.device(DEV))[0] is Gs  # cached
+
+
+@pytest.mark.parametrize("cid", [0, 1])
+def test_recursion_scaled_configs(golden_dir, cid):
+    """Reference tables + reference R0 through the scaled recursion: iteration 0
+    selects bit-identically; the sequence matches the reference's up to a legitimate
+    near-tie, and coefficients agree to rounding (1e-12 of the run scale, far
+    inside the 1e-6 bar)."""
+    z = np.load(golden_dir / f"c{cid}_blocks.npz")
+    w8 = wl.WORKLOADS[cid]
+    d = w8.dictionary()
+    mask = wl.central_loss_mask(*w8.area, *w8.loss)
+    tables, (c, dd) = host_tables(d, mask, w8.config.rho_hat)
+    blocks = list(z["blocks"])
+    sig = wl.block_signals(cid, max(blocks) + 1, *w8.area)[blocks]
+    r0 = np.stack([z[f"b{b}_r0"] for b in blocks])
+    res = fase_extrapolate_batch(sig, mask, d, tables, w8.config, products=r0, device=DEV,
+                                 recursion="scaled")
+    n_exact = 0
+    for i, b in enumerate(blocks):
+        want = z[f"b{b}_selected"]
+        got = res.selected[i].cpu().numpy()
+        assert got[0] == want[0]  # iteration 0's metric is bit-identical
+
+        def metric_at(t, b=b):
+            _, _, _, log = orc.fase_run(z[f"b{b}_r0"], c, dd, w8.config.gamma, t, record=True)
+            return metric_fn(z[f"b{b}_r0"], dd, log)(t)
+
+        v = compare_selection(got, want, metric_at)
+        assert v.ok, f"block {b}: diverged at {v.stop} with Delta-E gap {v.gap}"
+        n_exact += v.exact
+        s = v.stop
+        assert rel_dev(res.coefficients[i].cpu().numpy()[:s], z[f"b{b}_coefficients"][:s]) < 1e-12
+        assert rel_dev(res.projections[i].cpu().numpy()[:s], z[f"b{b}_projections"][:s]) < 1e-12
+        if v.exact:
+            lost = res.patched[i].cpu().numpy()[mask]
+            assert rel_dev(lost, z[f"b{b}_patched_lost"]) < 1e-12
+    assert n_exact == len(blocks)  # no near-tie divergence on these fixtures
+
+
+def test_recursion_scaled_matches_exact_full_config1():
+    """All 1,024 config-1 blocks: scaled and exact recursions select the same
+    sequences (up to legitimate near-ties, none expected) from the same R0."""
+    w8 = wl.WORKLOADS[1]
+    d = w8.dictionary()
+    mask = wl.central_loss_mask(*w8.area, *w8.loss)
+    dev = torch.device(DEV)
+    t = build_gram_tables(d, build_weight_field(mask, w8.config.rho_hat), device=dev)
+    from paper_2204_14194_b200 import ExtrapolationPlan
+
+    sig = torch.from_numpy(wl.block_signals(1, w8.n_blocks, *w8.area)).to(dev)
+    px = ExtrapolationPlan(d, mask, w8.n_blocks, w8.config, t, device=dev).run(sig)
+    ps = ExtrapolationPlan(d, mask, w8.n_blocks, w8.config, t, device=dev,
+                           recursion="scaled").run(sig)
+    torch.cuda.synchronize()
+    assert torch.equal(px.R0, ps.R0)
+    same = (px.selected == ps.selected).all(dim=1)
+    assert int(same.sum()) >= w8.n_blocks - 2
+    dev_c = ((px.coefficients - ps.coefficients).abs().amax(dim=1)
+             / px.coefficients.abs().amax(dim=1))
+    assert float(dev_c[same].max()) < 1e-12
+    dev_l = (px.lost - ps.lost).abs().amax(dim=1) / px.lost.abs().amax(dim=1)
+    assert float(dev_l[same].max()) < 1e-12
+
+
+def test_recursion_scaled_dead_atoms_and_options():
+    """Dead atoms (zero weighted energy) are never selected by the scaled
+    recursion; unsupported combinations raise the reference exceptions."""
+    from paper_2204_14194_b200 import ParameterError, UnsupportedDictionaryError
+
+    rng = np.random.default_rng(11)
+    m = n = 8
+    mask = np.zeros((m, n), dtype=bool)
+    mask[2:5, 2:5] = True
+    vals = rng.standard_normal((40, m, n))
+    for k in (0, 7, 19):  # atoms living only on lost samples
+        vals[k] = 0.0
+        vals[k][mask] = rng.standard_normal(int(mask.sum()))
+    d = Dictionary(vals)
+    cfg = ExtrapConfig(30, 0.5, 0.8)
+    sig = rng.uniform(0, 255, (5, m, n))
+    rx = fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV)
+    rs = fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion="scaled")
+    s = rs.selected.cpu().numpy()
+    assert not np.isin(s, [0, 7, 19]).any()
+    assert np.array_equal(s, rx.selected.cpu().numpy())
+    with pytest.raises(ParameterError):
+        fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion="fast")
+    with pytest.raises(UnsupportedDictionaryError):
+        fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion="scaled",
+                               record_products=True)
+    with pytest.raises(UnsupportedDictionaryError):
+        fase_extrapolate_batch(sig, mask, parse_dict_spec("dft", m, n), None, cfg, device=DEV,
+                               recursion="scaled")
 
 
 def test_frame_blocks_config3(golden_dir):

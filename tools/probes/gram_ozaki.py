@@ -38,3 +38,11 @@ for cid in (1, 4):
     g1, g2 = G1[:, :K].cpu().numpy(), G2[:, :K].cpu().numpy()
     print(f"c{cid} K={K} M={M} support={n_s}: dmma {td:.3f} ms, ozaki split {ts:.3f} + gram {tg:.3f} ms; "
           f"sym {np.array_equal(g2, g2.T)}; rel diff {np.abs(g1 - g2).max() / np.abs(g1).max():.2e}")
+
+    # the bench's timed sequence: support, fresh operands, split, gram, finish
+    from paper_2204_14194_b200.fast import gram_into, gram_support  # noqa: E402
+    D2 = torch.empty(K, dtype=torch.float64, device=dev)
+    tsup = t(lambda: gram_support(wd, M))
+    tall = t(lambda: gram_into(phi, wd, K, M, G2))
+    tfin = t(lambda: _native.gram_finish(G2, K, D2))
+    print(f"c{cid}: gram_support {tsup:.3f} ms, gram_into (alloc+split+gram) {tall:.3f} ms, finish {tfin:.3f} ms")
