@@ -458,11 +458,16 @@ def run_gpu(args):
                 plan.F[:, :M].copy_(dev_sig.reshape(B, -1), non_blocking=True)
                 plan._products(plan.F)
                 e[1].record(stream)
-                iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, plan.selected,
-                        plan.projections, plan.coefficients)
-                e[2].record(stream)
-                synth(plan.phi_lost, plan.selected, plan.coefficients, I, plan.lost_seq,
-                      plan.lost, n_shared=plan.n_lost, dst=plan.lost_pos, **synth_extra)
+                if plan.fused_synth:  # recursion with the synthesis inside
+                    plan._iterate_synth(plan.selected, plan.projections, plan.coefficients,
+                                        plan.lost)
+                    e[2].record(stream)
+                else:
+                    iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, plan.selected,
+                            plan.projections, plan.coefficients)
+                    e[2].record(stream)
+                    synth(plan.phi_lost, plan.selected, plan.coefficients, I, plan.lost_seq,
+                          plan.lost, n_shared=plan.n_lost, dst=plan.lost_pos, **synth_extra)
                 e[3].record(stream)
             else:
                 fn()
@@ -595,6 +600,7 @@ def run_gpu(args):
                                        "GEMM form (--products gemm) does 24x more work"}),
             "products": plan.products_method,
             "recursion": recursion,
+            "fused_synth": plan.fused_synth,
             "recursion_agreement": agreement,
             "stage_ms": {"init_products": float(np.mean(init_ms)), "iterate": float(np.mean(iter_ms)),
                          "synth": float(np.mean(synth_ms))},

@@ -241,7 +241,22 @@ FASE_API int fase_iterate(const fase_iterate_args* args, void* stream);
  * within 1e-9 relative; coefficients within 1e-6). chunk lists, compose,
  * per-block D, R_out and R_log are rejected (FASE_ERR_UNSUPPORTED).
  */
-FASE_API int fase_iterate_scaled(const fase_iterate_args* args, void* stream);
+typedef struct {
+  const double* phi; /* K x ldphi: the atoms restricted to the lost samples (16-byte aligned) */
+  int64_t ldphi;     /* even, >= n_lost */
+  int n_lost;
+  double* out;       /* out[b*ldout + i] = g_i of block b (packed lost samples) */
+  int64_t ldout;
+} fase_synth_fused;
+
+/* synth == NULL: recursion only. Otherwise the synthesis of fase_synth_paste
+ * (packed output, dst = 0..n_lost-1) is fused into the recursion: each
+ * iteration adds c * phi[u, i] in selection order, bit-identical to a
+ * separate fase_synth_paste over the same terms. n_lost must not exceed
+ * fase_iterate_scaled_synth_capacity(K, B) (else FASE_ERR_UNSUPPORTED). */
+FASE_API int fase_iterate_scaled(const fase_iterate_args* args, const fase_synth_fused* synth,
+                                 void* stream);
+FASE_API int fase_iterate_scaled_synth_capacity(int K, int B);
 
 /* Gs[u*lds + k] = G[u*ldg + k] * D[k] (k < K), 0 for K <= k < lds; lds even. */
 FASE_API int fase_scale_columns(const double* G, int64_t ldg, const double* D, int K, double* Gs,

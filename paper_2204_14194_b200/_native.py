@@ -37,7 +37,7 @@ EXPORTS = (
     "fase_gram_complex", "fase_max_atoms_complex", "fase_table_ld_complex", "fase_iterate_complex",
     "fase_synth_paste_complex", "fase_sep_products_complex", "fase_fft_gram", "fase_weigh_gather",
     "fase_ozaki_split", "fase_ozaki_gemm", "fase_ozaki_gram", "fase_sep_products_batch",
-    "fase_iterate_scaled", "fase_scale_columns",
+    "fase_iterate_scaled", "fase_scale_columns", "fase_iterate_scaled_synth_capacity",
 )
 
 _vp = ctypes.c_void_p
@@ -50,6 +50,12 @@ class SepPart(ctypes.Structure):
     """Mirror of ``fase_sep_part`` (include/fase_b200.h)."""
 
     _fields_ = [("rows", _vp), ("Lr", _i32), ("cols", _vp), ("Lc", _i32), ("col0", _i64)]
+
+
+class SynthFused(ctypes.Structure):
+    """Mirror of ``fase_synth_fused`` (include/fase_b200.h)."""
+
+    _fields_ = [("phi", _vp), ("ldphi", _i64), ("n_lost", _i32), ("out", _vp), ("ldout", _i64)]
 
 
 class IterateArgs(ctypes.Structure):
@@ -108,7 +114,8 @@ def load():
         "fase_block_normalizers": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _i64,
                                    _vp, _vp],
         "fase_iterate": [ctypes.POINTER(IterateArgs), _vp],
-        "fase_iterate_scaled": [ctypes.POINTER(IterateArgs), _vp],
+        "fase_iterate_scaled": [ctypes.POINTER(IterateArgs), ctypes.POINTER(SynthFused), _vp],
+        "fase_iterate_scaled_synth_capacity": [_i32, _i32],
         "fase_scale_columns": [_vp, _i64, _vp, _i32, _vp, _i64, _vp],
         "fase_iterate_complex": [ctypes.POINTER(IterateArgs), _vp],
         "fase_gram_complex": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp, ctypes.c_size_t, _vp],
@@ -323,9 +330,17 @@ def scale_columns(G, D, K: int, Gs) -> None:
     _check(lib.fase_scale_columns(_ptr(G), _ld(G), _ptr(D), K, _ptr(Gs), _ld(Gs), _stream(Gs)))
 
 
-def iterate_scaled(Gs, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef) -> None:
+def scaled_synth_capacity(K: int, B: int) -> int:
+    """Most lost samples the scaled recursion can synthesize in-kernel for (K, B)."""
+    return int(load().fase_iterate_scaled_synth_capacity(K, B))
+
+
+def iterate_scaled(Gs, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *,
+                   phi_lost=None, n_lost: int = 0, lost=None) -> None:
     """The scaled recursion (fase_iterate_scaled) over a column-scaled shared
-    table ``Gs`` (scale_columns); R0 and D unscaled, as for ``iterate``."""
+    table ``Gs`` (scale_columns); R0 and D unscaled, as for ``iterate``.
+    With ``phi_lost`` (K, ld) and ``lost`` (B, >= n_lost) the synthesis of the
+    n_lost packed lost samples is fused in (bit-identical to synth_paste)."""
     import torch
 
     lib = load()
@@ -340,7 +355,13 @@ def iterate_scaled(Gs, D, R0, K: int, iterations: int, gamma: float, sel, proj, 
                        coef=_ptr(coef), ldo=_ld(sel))
     if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
         raise errors.ShapeError("sel / proj / coef must share one leading dimension")
-    _check(lib.fase_iterate_scaled(ctypes.byref(args), _stream(R0)))
+    syn = None
+    if phi_lost is not None:
+        _require(phi_lost, "phi_lost", torch.float64, 2)
+        _require(lost, "lost", torch.float64, 2)
+        syn = ctypes.byref(SynthFused(phi=_ptr(phi_lost), ldphi=_ld(phi_lost), n_lost=n_lost,
+                                      out=_ptr(lost), ldout=_ld(lost)))
+    _check(lib.fase_iterate_scaled(ctypes.byref(args), syn, _stream(R0)))
 
 
 def synth_paste(phi, sel, coef, iterations: int, idx, out, *, idx_ptr=None, n_shared: int = 0,

@@ -79,14 +79,23 @@ __device__ unsigned long long g_stats[8];  // measurement build: chunked-path co
 // rounding of the scaled operands (~1 ulp per update), which can only change a
 // selection whose top-two metrics lie within that rounding -- inside the
 // north-star tolerance (top-two within 1e-9 relative). p = R'_u * D_u.
+//
+// SYN > 0 (scaled only): synthesis fused into the recursion. Each thread owns
+// up to SYN lost samples (i = t + s*NT) and accumulates g_i += c * phi[u, i]
+// after every update, in selection order with the same mul-then-add as
+// fase_synth_paste (bit-identical output); the phi row of the predicted atom
+// arrives by TMA with the last table segment.
 template <int NT, int EPT, int MINB, bool kDsmem, bool kChunked, bool kRecord, int NB,
-          bool kScaled = false>
-__global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_iterate_args a) {
+          bool kScaled = false, int SYN = 0>
+__global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_iterate_args a,
+                                                                     const fase_synth_fused syn) {
   constexpr int EP = EPT / 2;
   constexpr int NW = NT / 32;
   static_assert(NB == 1 || (kDsmem && !kChunked), "paired blocks share one D in shared memory");
   static_assert(!kScaled || (!kDsmem && !kChunked && !kRecord && NB == 1),
                 "the scaled recursion keeps no normalizers and has one block per CTA");
+  static_assert(SYN == 0 || kScaled, "fused synthesis runs with the scaled recursion");
+  __shared__ __align__(16) double s_phi[SYN > 0 ? SYN * NT : 2];
 
   __shared__ long long s_key_all[NB][NW];
   __shared__ unsigned s_arg_all[NB][NW];
@@ -116,6 +125,18 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   const int t = static_cast<int>(threadIdx.x) - half * NT;
   const int lane = t & 31;
   const int warp = t >> 5;
+  double gacc[SYN > 0 ? SYN : 1];
+#pragma unroll
+  for (int i = 0; i < (SYN > 0 ? SYN : 1); ++i) gacc[i] = 0.0;
+  // fused synthesis output of this block (SYN > 0)
+  auto write_synth = [&](int blk) {
+    if constexpr (SYN > 0) {
+      double* o = syn.out + static_cast<int64_t>(blk) * syn.ldout;
+#pragma unroll
+      for (int i = 0; i < SYN; ++i)
+        if (t + i * NT < syn.n_lost) o[t + i * NT] = gacc[i];
+    }
+  };
   const int K = a.K;
   const double kDead = __longlong_as_double(static_cast<long long>(0xfff0000000000000ULL));
   const bool active = NB == 1 || b < a.B;
@@ -276,6 +297,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         proj[k] = 0.0;
         coef[k] = 0.0;
       }
+      write_synth(b);
       return;
     }
     // stage the likely selection's row in shared memory (one TMA bulk copy)
@@ -315,12 +337,18 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     if (t == 0 && issue) {
       fence_proxy_async_smem();
       const double* grow = base() + static_cast<int64_t>(guess) * ldg;
+      // fused synthesis: the predicted atom's phi row rides on the last segment
+      const unsigned phi_bytes =
+          SYN > 0 ? static_cast<unsigned>((syn.n_lost * sizeof(double) + 15) & ~size_t{15}) : 0u;
 #pragma unroll
       for (int sg = 0; sg < kSeg; ++sg) {
         const int j0 = sg * EP / kSeg, j1 = (sg + 1) * EP / kSeg;
         const unsigned bytes = static_cast<unsigned>((j1 - j0) * NT * sizeof(double2));
-        mbar_arrive_expect_tx(&s_bar[sg], bytes);
+        mbar_arrive_expect_tx(&s_bar[sg], bytes + (sg == kSeg - 1 ? phi_bytes : 0u));
         tma_load_1d(s_row + j0 * NT, grow + 2 * j0 * NT, bytes, &s_bar[sg]);
+        if (SYN > 0 && sg == kSeg - 1)
+          tma_load_1d(s_phi, syn.phi + static_cast<int64_t>(guess) * syn.ldphi, phi_bytes,
+                      &s_bar[sg]);
       }
       if constexpr (kChunked) {
         // the guess's chunk-table rows are read right after the second
@@ -540,10 +568,26 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       }
     } else if (u == guess) {  // block-uniform
       update([&](int j) { return s_row[j * NT + t]; }, Staged{}, no_pre);
+      if constexpr (SYN > 0) {
+#pragma unroll
+        for (int i = 0; i < SYN; ++i)
+          if (t + i * NT < syn.n_lost) gacc[i] = add_rn(gacc[i], mul_rn(c, s_phi[t + i * NT]));
+      }
     } else {
       wait_all();  // retire the mispredicted copy before the next one
       const double* urow = base() + static_cast<int64_t>(u) * ldg + 2 * t;
+      double phv[SYN > 0 ? SYN : 1];
+      if constexpr (SYN > 0) {
+        const double* prow = syn.phi + static_cast<int64_t>(u) * syn.ldphi;
+#pragma unroll
+        for (int i = 0; i < SYN; ++i) phv[i] = t + i * NT < syn.n_lost ? __ldg(prow + t + i * NT) : 0.0;
+      }
       update([&](int j) { return ldg2(urow + 2 * j * NT); }, Direct{}, no_pre);
+      if constexpr (SYN > 0) {
+#pragma unroll
+        for (int i = 0; i < SYN; ++i)
+          if (t + i * NT < syn.n_lost) gacc[i] = add_rn(gacc[i], mul_rn(c, phv[i]));
+      }
     }
     if (kRecord) {
       double* dst = a.R_log + (static_cast<int64_t>(b) * a.I + it) * a.ldr;
@@ -556,6 +600,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     }
   }
 
+  write_synth(b);
   if (a.R_out) {
     double* dst = a.R_out + static_cast<int64_t>(b) * a.ldr;
 #pragma unroll
@@ -567,16 +612,18 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   }
 }
 
-using KernelFn = void (*)(const fase_iterate_args);
+using KernelFn = void (*)(const fase_iterate_args, const fase_synth_fused);
 
 struct Variant {
   int nt;
   int ept;
-  bool dsmem;        // D in shared memory (else registers)
-  KernelFn plain;    // shared geometry
-  KernelFn chunked;  // per-block geometry (chunk-corrected rows)
-  KernelFn record;   // shared geometry, R logged after every iteration
-  int nb = 1;        // blocks per CTA (2: paired blocks sharing one D)
+  bool dsmem;             // D in shared memory (else registers)
+  KernelFn plain;         // shared geometry
+  KernelFn chunked;       // per-block geometry (chunk-corrected rows)
+  KernelFn record;        // shared geometry, R logged after every iteration
+  int nb = 1;             // blocks per CTA (2: paired blocks sharing one D)
+  KernelFn fused = nullptr;  // scaled: synthesis fused (up to syn lost samples per thread)
+  int syn = 0;
 };
 
 #define FASE_V(NT, EPT, MINB, DS)                                                       \
@@ -631,23 +678,27 @@ const Variant kLatencyVariants[] = {
 // the staged row occupies shared memory and four 256-thread CTAs fit per SM
 // (64 registers; config 1: 0.916 ms exact at three CTAs, 0.815 ms scaled at
 // three, 0.721 ms scaled at four). Ordered by capacity like kVariants.
-#define FASE_VS(NT, EPT, MINB) \
-  {NT, EPT, false, fase_iterate_kernel<NT, EPT, MINB, false, false, false, 1, true>, nullptr, nullptr}
+// SYN: lost samples per thread of the fused-synthesis kernel (registers allow
+// only one at the 64-register four-CTA shapes).
+#define FASE_VS(NT, EPT, MINB, SYN)                                                          \
+  {NT,      EPT,     false, fase_iterate_kernel<NT, EPT, MINB, false, false, false, 1, true>, \
+   nullptr, nullptr, 1,     fase_iterate_kernel<NT, EPT, MINB, false, false, false, 1, true, SYN>, SYN}
 const Variant kScaledVariants[] = {
-    FASE_VS(128, 2, 8),   FASE_VS(128, 4, 8),   FASE_VS(128, 8, 8),   FASE_VS(128, 16, 6),
-    FASE_VS(256, 10, 4),  FASE_VS(256, 12, 4),  FASE_VS(256, 14, 4),  FASE_VS(256, 16, 4),
-    FASE_VS(256, 18, 4),  FASE_VS(256, 20, 3),  FASE_VS(256, 24, 2),  FASE_VS(256, 32, 2),
-    FASE_VS(512, 20, 1),  FASE_VS(512, 24, 1),
+    FASE_VS(128, 2, 8, 4),   FASE_VS(128, 4, 8, 4),   FASE_VS(128, 8, 8, 4),
+    FASE_VS(128, 16, 6, 4),  FASE_VS(256, 10, 4, 1),  FASE_VS(256, 12, 4, 1),
+    FASE_VS(256, 14, 4, 1),  FASE_VS(256, 16, 4, 1),  FASE_VS(256, 18, 4, 1),
+    FASE_VS(256, 20, 3, 3),  FASE_VS(256, 24, 2, 3),  FASE_VS(256, 32, 2, 3),
+    FASE_VS(512, 20, 1, 2),  FASE_VS(512, 24, 1, 2),
 };
 // alternatives for measurement (FASE_SCALED_VARIANT=NTxEPTxMINB) and the
 // latency shapes for batches of at most one block per SM
 const Variant kScaledExtra[] = {
-    FASE_VS(128, 36, 4), FASE_VS(256, 18, 3), FASE_VS(128, 64, 2), FASE_VS(128, 64, 3),
-    FASE_VS(256, 20, 4),
+    FASE_VS(128, 36, 4, 2), FASE_VS(256, 18, 3, 2), FASE_VS(128, 64, 2, 4),
+    FASE_VS(128, 64, 3, 4), FASE_VS(256, 20, 4, 1),
 };
 const int kScaledExtraMinb[] = {4, 3, 2, 3, 4};
 const Variant kScaledLatency[] = {
-    FASE_VS(384, 6, 1), FASE_VS(768, 6, 1), FASE_VS(1024, 8, 1),
+    FASE_VS(384, 6, 1, 2), FASE_VS(768, 6, 1, 1), FASE_VS(1024, 8, 1, 1),
 };
 #undef FASE_VS
 
@@ -772,11 +823,51 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
     set_error("fase_iterate: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return FASE_ERR_CUDA;
   }
-  fn<<<(a.B + v->nb - 1) / v->nb, v->nt * v->nb, smem, as_stream(stream)>>>(a);
+  fn<<<(a.B + v->nb - 1) / v->nb, v->nt * v->nb, smem, as_stream(stream)>>>(a, fase_synth_fused{});
   return check_launch("fase_iterate");
 }
 
-extern "C" int fase_iterate_scaled(const fase_iterate_args* args, void* stream) {
+namespace fase {
+namespace {
+// The scaled variant for K atoms and B blocks (nullptr when K is too large):
+// the smallest capacity holding K; FASE_SCALED_VARIANT=NTxEPT[xMINB] picks an
+// alternative shape for measurement; at most one block per SM takes the
+// widest latency shape.
+const Variant* pick_scaled(int K, int B) {
+  const Variant* dflt = pick_variant(K);
+  if (!dflt) return nullptr;
+  const int cap = dflt->nt * dflt->ept;
+  const Variant* v = nullptr;
+  for (const Variant& sv : kScaledVariants)
+    if (sv.nt * sv.ept >= K) {
+      v = &sv;
+      break;
+    }
+  const char* env = getenv("FASE_SCALED_VARIANT");
+  int nt = 0, ept = 0, minb = 0;
+  if (env && sscanf(env, "%dx%dx%d", &nt, &ept, &minb) >= 2) {
+    for (int i = 0; i < static_cast<int>(sizeof(kScaledExtra) / sizeof(kScaledExtra[0])); ++i) {
+      const Variant& ev = kScaledExtra[i];
+      if (ev.nt == nt && ev.ept == ept && (minb == 0 || kScaledExtraMinb[i] == minb) &&
+          ev.nt * ev.ept >= K && ev.nt * ev.ept <= cap)
+        v = &ev;
+    }
+  } else if (B <= sm_count()) {
+    for (const Variant& lv : kScaledLatency)
+      if (lv.nt * lv.ept >= K && lv.nt * lv.ept <= cap && lv.nt > v->nt) v = &lv;
+  }
+  return v;
+}
+}  // namespace
+}  // namespace fase
+
+extern "C" int fase_iterate_scaled_synth_capacity(int K, int B) {
+  const Variant* v = K >= 1 ? pick_scaled(K, B) : nullptr;
+  return v ? v->syn * v->nt : 0;
+}
+
+extern "C" int fase_iterate_scaled(const fase_iterate_args* args, const fase_synth_fused* syn,
+                                   void* stream) {
   if (!args) {
     set_error("fase_iterate_scaled: null argument block");
     return FASE_ERR_PARAMETER;
@@ -801,47 +892,38 @@ extern "C" int fase_iterate_scaled(const fase_iterate_args* args, void* stream) 
               "R_log)");
     return FASE_ERR_UNSUPPORTED;
   }
-  const Variant* dflt = pick_variant(a.K);
-  if (!dflt) {
+  if (syn && (syn->n_lost < 1 || !syn->phi || !aligned16(syn->phi) || (syn->ldphi & 1) ||
+              syn->ldphi < syn->n_lost || !syn->out || syn->ldout < syn->n_lost)) {
+    set_error("fase_iterate_scaled: bad fused-synthesis operand (n_lost=%d)", syn ? syn->n_lost : 0);
+    return FASE_ERR_SHAPE;
+  }
+  const Variant* v = pick_scaled(a.K, a.B);
+  if (!v) {
     set_error("fase_iterate_scaled: K=%d exceeds the largest kernel variant (%d atoms)", a.K,
               fase_max_atoms());
     return FASE_ERR_UNSUPPORTED;
   }
-  const int cap = dflt->nt * dflt->ept;
-  const Variant* v = nullptr;
-  for (const Variant& sv : kScaledVariants)
-    if (sv.nt * sv.ept >= a.K) {
-      v = &sv;
-      break;
-    }
-  const char* env = getenv("FASE_SCALED_VARIANT");
-  int nt = 0, ept = 0, minb = 0;
-  if (env && sscanf(env, "%dx%dx%d", &nt, &ept, &minb) >= 2) {
-    for (int i = 0; i < static_cast<int>(sizeof(kScaledExtra) / sizeof(kScaledExtra[0])); ++i) {
-      const Variant& ev = kScaledExtra[i];
-      if (ev.nt == nt && ev.ept == ept && (minb == 0 || kScaledExtraMinb[i] == minb) &&
-          ev.nt * ev.ept >= a.K && ev.nt * ev.ept <= cap)
-        v = &ev;
-    }
-  } else if (a.B <= sm_count()) {  // at most one block per SM: the widest CTA
-    for (const Variant& lv : kScaledLatency)
-      if (lv.nt * lv.ept >= a.K && lv.nt * lv.ept <= cap && lv.nt > v->nt) v = &lv;
+  if (syn && syn->n_lost > v->syn * v->nt) {
+    set_error("fase_iterate_scaled: %d lost samples exceed the fused synthesis capacity %d "
+              "(fase_iterate_scaled_synth_capacity)", syn->n_lost, v->syn * v->nt);
+    return FASE_ERR_UNSUPPORTED;
   }
   if (a.ldg < v->nt * v->ept) {
-    set_error("fase_iterate_scaled: table rows must be zero-padded to fase_table_ld(K)=%d (ldg=%lld)",
-              cap, static_cast<long long>(a.ldg));
+    set_error("fase_iterate_scaled: table rows must be zero-padded to fase_table_ld(K) (ldg=%lld)",
+              static_cast<long long>(a.ldg));
     return FASE_ERR_SHAPE;
   }
+  KernelFn fn = syn ? v->fused : v->plain;
   const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2);
-  cudaError_t e = cudaFuncSetAttribute(v->plain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(v->plain, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) {
     set_error("fase_iterate_scaled: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return FASE_ERR_CUDA;
   }
-  v->plain<<<a.B, v->nt, smem, as_stream(stream)>>>(a);
+  fn<<<a.B, v->nt, smem, as_stream(stream)>>>(a, syn ? *syn : fase_synth_fused{});
   return check_launch("fase_iterate_scaled");
 }
 

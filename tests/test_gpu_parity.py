@@ -22,6 +22,7 @@ from paper_2204_14194_b200 import (  # noqa: E402
     GramTable,
     NoSelectableAtomError,
     StaleTableError,
+    UnsupportedDictionaryError,
     build_gram_tables,
     build_weight_field,
     fase_extrapolate,
@@ -730,3 +731,38 @@ def test_iterate_compose_map_bit_identical(cplx, depth):
     for a, b in zip(*out):
         assert torch.equal(a, b)
     assert (out[0][0] >= 0).all()
+
+
+@pytest.mark.parametrize("spec,m,loss,nb", [("union:dct+had", 48, 16, 64), ("dct", 48, 16, 1),
+                                            ("gauss:2000:3", 24, 10, 37)])
+def test_fused_synthesis_bit_identical(spec, m, loss, nb):
+    """The scaled recursion with the synthesis fused in writes the same lost
+    samples, bit for bit, as the recursion followed by fase_synth_paste; the
+    plan fuses it for batches of at most one block per SM."""
+    from paper_2204_14194_b200 import ExtrapolationPlan
+
+    d = parse_dict_spec(spec, m, m)
+    mask = wl.central_loss_mask(m, m, loss, loss)
+    cfg = ExtrapConfig(60, 0.5, 0.8)
+    dev = torch.device(DEV)
+    t = build_gram_tables(d, build_weight_field(mask, cfg.rho_hat), device=dev)
+    sig = torch.from_numpy(np.random.default_rng(3).uniform(0, 255, (nb, m, m))).to(dev)
+    p = ExtrapolationPlan(d, mask, nb, cfg, t, device=dev, recursion="scaled")
+    assert p.fused_synth
+    p.run(sig)
+    K, n = len(d), p.n_lost
+    sel, proj, coef = (torch.empty_like(x) for x in (p.selected, p.projections, p.coefficients))
+    lost = torch.zeros_like(p.lost)
+    _native.iterate_scaled(p.Gs, p.D, p.R0, K, cfg.iterations, cfg.gamma, sel, proj, coef)
+    _native.synth_paste(p.phi_lost, sel, coef, cfg.iterations, p.lost_seq, lost, n_shared=n,
+                        dst=p.lost_pos)
+    torch.cuda.synchronize()
+    assert torch.equal(sel, p.selected) and torch.equal(coef, p.coefficients)
+    assert torch.equal(lost[:, :n], p.lost[:, :n])
+    # capacity guard: more lost samples than the fused kernel holds is refused
+    cap = _native.scaled_synth_capacity(K, nb)
+    big = torch.zeros((K, cap + 2), dtype=torch.float64, device=dev)
+    with pytest.raises(UnsupportedDictionaryError):
+        _native.iterate_scaled(p.Gs, p.D, p.R0, K, cfg.iterations, cfg.gamma, sel, proj, coef,
+                               phi_lost=big, n_lost=cap + 1,
+                               lost=torch.zeros((nb, cap + 2), dtype=torch.float64, device=dev))
