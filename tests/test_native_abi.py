@@ -95,23 +95,30 @@ def test_status_codes_and_messages(lib):
                                None) == -1  # A rows not padded to 128
     assert b"padded" in lib.fase_last_error()
     # scaled recursion: same argument checks; shared geometry only
-    assert lib.fase_iterate_scaled(None, None) == -2
+    assert lib.fase_iterate_scaled(None, None, None) == -2
     args = _native.IterateArgs(K=4, B=1, I=1, gamma=2.0)
-    assert lib.fase_iterate_scaled(ctypes.byref(args), None) == -2
+    assert lib.fase_iterate_scaled(ctypes.byref(args), None, None) == -2
     fake = 1 << 20  # aligned, never dereferenced: validation returns first
     args = _native.IterateArgs(G0=fake, ldg=4, D=fake, R0=fake, ldr=4, K=4, B=1, I=1, gamma=0.5,
                                sel=fake, proj=fake, coef=fake, ldo=1, chunk_count=fake)
-    assert lib.fase_iterate_scaled(ctypes.byref(args), None) == -8
+    assert lib.fase_iterate_scaled(ctypes.byref(args), None, None) == -8
     assert b"shared geometry only" in lib.fase_last_error()
     args = _native.IterateArgs(G0=fake, ldg=4, D=fake, R0=fake, ldr=4, K=4, B=1, I=1, gamma=0.5,
                                sel=fake, proj=fake, coef=fake, ldo=1, R_out=fake)
-    assert lib.fase_iterate_scaled(ctypes.byref(args), None) == -8
+    assert lib.fase_iterate_scaled(ctypes.byref(args), None, None) == -8
+    syn = _native.SynthFused(phi=fake, ldphi=3, n_lost=3, out=fake, ldout=3)  # odd ldphi
+    args = _native.IterateArgs(G0=fake, ldg=4, D=fake, R0=fake, ldr=4, K=4, B=1, I=1, gamma=0.5,
+                               sel=fake, proj=fake, coef=fake, ldo=1)
+    assert lib.fase_iterate_scaled(ctypes.byref(args), ctypes.byref(syn), None) == -1
+    assert b"fused-synthesis" in lib.fase_last_error()
+    assert lib.fase_iterate_scaled_synth_capacity(4608, 1024) >= 256
+    assert lib.fase_iterate_scaled_synth_capacity(0, 1) == 0
     assert lib.fase_scale_columns(None, 4, None, 4, None, 4, None) == -1
     assert lib.fase_scale_columns(fake, 4, fake, 4, fake, 5, None) == -1  # odd lds
     # empty batches are a no-op, not an error
     args = _native.IterateArgs(K=4, B=0, I=1, gamma=0.5)
     assert lib.fase_iterate(ctypes.byref(args), None) == 0
-    assert lib.fase_iterate_scaled(ctypes.byref(args), None) == 0
+    assert lib.fase_iterate_scaled(ctypes.byref(args), None, None) == 0
     assert lib.fase_ozaki_gemm(None, 128, None, 0, None, 64, None, 50, 64, 8, None, 50, None) == 0
 
 
