@@ -9,6 +9,9 @@ for c in 4 3 2; do
   python bench.py --config $c --steps 10 --warmup 3 --cpu-seconds 8 > gpurun_out/benches/c$c.json 2> gpurun_out/benches/c$c.err; echo c$c=$?
 done
 python bench.py --config 1 --dict dft --steps 10 --warmup 3 --cpu-seconds 8 > gpurun_out/benches/c1_dft.json 2> gpurun_out/benches/c1_dft.err; echo c1dft=$?
+python bench.py --config 1 --recursion exact --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/benches/c1_exact.json 2> gpurun_out/benches/c1_exact.err; echo c1exact=$?
+python bench.py --config 4 --recursion exact --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/benches/c4_exact.json 2> gpurun_out/benches/c4_exact.err; echo c4exact=$?
+python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/benches/c1_reference.json 2> gpurun_out/benches/c1_reference.err; echo ref=$?
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r01g.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu1.log 2>&1; echo ncu1=$?
 ncu --set full --clock-control none --import-source on -k regex:"fase_iterate|sep_products|weigh|synth_paste" -s 5 -c 5 -o gpurun_out/prof_r01_c1g python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu2.log 2>&1; echo ncu2=$?
