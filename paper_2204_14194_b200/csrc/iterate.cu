@@ -254,6 +254,18 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   int32_t* sel = a.sel + static_cast<int64_t>(b) * a.ldo;
   double* proj = a.proj + static_cast<int64_t>(b) * a.ldo;
   double* coef = a.coef + static_cast<int64_t>(b) * a.ldo;
+  // Chunked shapes re-derive the output rows from the parameter bank at each
+  // (thread-0) use: as loop-carried induction pointers they cost six registers
+  // in every thread and spilled the 80-register chunked variant (local-memory
+  // round trips on the per-iteration path; config 2)
+  auto out_row = [&](auto* base, auto* hoisted) {
+    if constexpr (kChunked) {
+      asm volatile("" : "+l"(base));
+      return base + static_cast<int64_t>(b) * a.ldo;
+    } else {
+      return hoisted;
+    }
+  };
   const int64_t ldg = a.ldg;
   double q = 0.0;
   // kChunked: the atom whose complete (composed) row the staging buffer holds,
@@ -293,9 +305,9 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     }
     if (top_key < 0) {  // every atom degenerate (NoSelectableAtomError): mark and stop
       for (int k = it + t; k < a.I; k += NT) {
-        sel[k] = -1;
-        proj[k] = 0.0;
-        coef[k] = 0.0;
+        out_row(a.sel, sel)[k] = -1;
+        out_row(a.proj, proj)[k] = 0.0;
+        out_row(a.coef, coef)[k] = 0.0;
       }
       write_synth(b);
       return;
@@ -416,9 +428,9 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     const double p = kScaled ? mul_rn(ru, du) : mul_rn(ru, mul_rn(du, du));
     const double c = mul_rn(a.gamma, p);
     if (t == 0) {
-      sel[it] = static_cast<int32_t>(u);
-      proj[it] = p;
-      coef[it] = c;
+      out_row(a.sel, sel)[it] = static_cast<int32_t>(u);
+      out_row(a.proj, proj)[it] = p;
+      out_row(a.coef, coef)[it] = c;
     }
 
     auto wait_all = [&]() {
