@@ -188,6 +188,78 @@ __global__ void __launch_bounds__(kSynthThreads) synth_paste_kernel(
   }
 }
 
+// Throughput shape for batches that fill the GPU: 128 threads per block, two
+// samples per thread (m0 = idx[base + tid], m1 = idx[base + 128 + tid]) sharing
+// each term's row address, coefficient and selection loads, with two
+// independent accumulation chains per thread. The number of valid terms of a
+// chunk (up to the first sel < 0, where the recursion stopped) is found while
+// staging, so the term loop carries no per-term checks. Each sample's sum is
+// still accumulated strictly in selection order (bit-identical output).
+constexpr int kSynthPairThreads = 128;
+
+template <int G>
+__global__ void __launch_bounds__(kSynthPairThreads) synth_paste_pair_kernel(
+    const double* __restrict__ phi, int64_t ldphi, const int32_t* __restrict__ sel,
+    const double* __restrict__ coef, int64_t ldo, int I, const int32_t* __restrict__ idx_ptr,
+    const int32_t* __restrict__ idx, int n_shared, const int64_t* __restrict__ dst,
+    double* __restrict__ out, int64_t ldout) {
+  __shared__ int32_t s_sel[kSynthChunk];
+  __shared__ double s_coef[kSynthChunk];
+  __shared__ int s_len;
+  const int b = blockIdx.x;
+  const int tid = static_cast<int>(threadIdx.x);
+  const int lo = idx_ptr ? idx_ptr[b] : 0;
+  const int n = idx_ptr ? idx_ptr[b + 1] - lo : n_shared;
+  const int32_t* my_idx = idx + lo;
+  const int32_t* my_sel = sel + static_cast<int64_t>(b) * ldo;
+  const double* my_coef = coef + static_cast<int64_t>(b) * ldo;
+  for (int base = 0; base < n; base += 2 * kSynthPairThreads) {
+    const int i0 = base + tid, i1 = base + kSynthPairThreads + tid;
+    const int m0 = i0 < n ? my_idx[i0] : 0;
+    const int m1 = i1 < n ? my_idx[i1] : m0;
+    double g0 = 0.0, g1 = 0.0;
+    for (int t0 = 0; t0 < I; t0 += kSynthChunk) {
+      const int len = min(kSynthChunk, I - t0);
+      __syncthreads();
+      if (tid == 0) s_len = len;
+      __syncthreads();
+      for (int t = tid; t < len; t += kSynthPairThreads) {
+        const int u = my_sel[t0 + t];
+        s_sel[t] = u;
+        s_coef[t] = my_coef[t0 + t];
+        if (u < 0) atomicMin(&s_len, t);
+      }
+      __syncthreads();
+      const int lv = s_len;
+      for (int tb = 0; tb < lv; tb += G) {
+        double v0[G], v1[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          const int t = tb + j;
+          if (t < lv) {
+            const double* row = phi + static_cast<int64_t>(s_sel[t]) * ldphi;
+            v0[j] = __ldg(row + m0);
+            v1[j] = __ldg(row + m1);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          const int t = tb + j;
+          if (t < lv) {
+            const double c = s_coef[t];
+            g0 = __dadd_rn(g0, __dmul_rn(c, v0[j]));
+            g1 = __dadd_rn(g1, __dmul_rn(c, v1[j]));
+          }
+        }
+      }
+      if (lv < len) break;  // the recursion stopped: no later terms
+    }
+    const int64_t ob = static_cast<int64_t>(b) * ldout;
+    if (i0 < n) out[(dst ? dst[lo + i0] : static_cast<int64_t>(m0)) + ob] = g0;
+    if (i1 < n) out[(dst ? dst[lo + i1] : static_cast<int64_t>(m1)) + ob] = g1;
+  }
+}
+
 // Complex dictionaries (conjugate-split rows: phi2[2u] = Re phi_u,
 // phi2[2u+1] = -Im phi_u): g = sum_t coef_t * phi_{sel_t} with numpy's fused
 // complex product (np_cmul), accumulated in selection order
@@ -336,10 +408,15 @@ extern "C" int fase_synth_paste(const double* phi, int64_t ldphi, const int32_t*
     set_error("fase_synth_paste: null pointer");
     return FASE_ERR_SHAPE;
   }
-  // a batch that cannot fill the GPU is latency-bound: keep more atom values in flight
-  auto kernel = B < 148 ? synth_paste_kernel<32> : synth_paste_kernel<8>;
-  kernel<<<B, kSynthThreads, 0, as_stream(stream)>>>(phi, ldphi, sel, coef, ldo, I, idx_ptr, idx,
-                                                      n_shared, dst, out, ldout);
+  // a batch that cannot fill the GPU is latency-bound: keep more atom values in
+  // flight; larger batches take the two-samples-per-thread shape
+  if (B < 148) {
+    synth_paste_kernel<32><<<B, kSynthThreads, 0, as_stream(stream)>>>(
+        phi, ldphi, sel, coef, ldo, I, idx_ptr, idx, n_shared, dst, out, ldout);
+  } else {
+    synth_paste_pair_kernel<8><<<B, kSynthPairThreads, 0, as_stream(stream)>>>(
+        phi, ldphi, sel, coef, ldo, I, idx_ptr, idx, n_shared, dst, out, ldout);
+  }
   return check_launch("fase_synth_paste");
 }
 

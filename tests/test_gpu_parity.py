@@ -766,3 +766,31 @@ def test_fused_synthesis_bit_identical(spec, m, loss, nb):
         _native.iterate_scaled(p.Gs, p.D, p.R0, K, cfg.iterations, cfg.gamma, sel, proj, coef,
                                phi_lost=big, n_lost=cap + 1,
                                lost=torch.zeros((nb, cap + 2), dtype=torch.float64, device=dev))
+
+
+@pytest.mark.parametrize("nb,n_lost,I,stop", [(300, 256, 200, None), (160, 576, 37, 20),
+                                              (151, 100, 1030, 700)])
+def test_synth_paste_throughput_shape_bit_exact(nb, n_lost, I, stop):
+    """fase_synth_paste on batches that fill the GPU (two samples per thread,
+    valid-term count found while staging) against numpy's sequential
+    mul-then-add in selection order (SparseModel.materialize); a recursion that
+    stopped early (sel = -1 from `stop` on) contributes nothing after it."""
+    rng = np.random.default_rng(nb)
+    K, ld = 700, n_lost + (n_lost & 1)
+    phi = rng.standard_normal((K, ld))
+    sel = rng.integers(0, K, (nb, I)).astype(np.int32)
+    coef = rng.standard_normal((nb, I))
+    if stop is not None:
+        sel[::3, stop:] = -1
+    dev = torch.device(DEV)
+    out = torch.zeros((nb, ld), dtype=torch.float64, device=dev)
+    seq = torch.arange(ld, dtype=torch.int32, device=dev)
+    _native.synth_paste(torch.from_numpy(phi).to(dev), torch.from_numpy(sel).to(dev),
+                        torch.from_numpy(coef).to(dev), I, seq, out, n_shared=n_lost,
+                        dst=torch.arange(ld, dtype=torch.int64, device=dev))
+    got = out.cpu().numpy()[:, :n_lost]
+    want = np.zeros((nb, n_lost))
+    for t in range(I):
+        live = sel[:, t] >= 0
+        want[live] = want[live] + coef[live, t, None] * phi[sel[live, t], :n_lost]
+    assert np.array_equal(got, want)
