@@ -426,6 +426,10 @@ def run_gpu(args):
     host2 = torch.from_numpy(wl.block_signals(args.config, B, *w.area,
                                               first=(world + rank) * B)).pin_memory()
     dev_sig = host.to(dev)
+    sig_view = dev_sig.reshape(B, -1)
+    if plan.F.shape[1] != M:  # odd areas: the kernels read the padded layout
+        plan.F[:, :M].copy_(sig_view)
+        sig_view = plan.F
     outs = plan.host_buffers()
     outs2 = plan.host_buffers()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -455,8 +459,7 @@ def run_gpu(args):
             e = [torch.cuda.Event(enable_timing=True) for _ in range(4 if split else 2)]
             e[0].record(stream)
             if split:
-                plan.F[:, :M].copy_(dev_sig.reshape(B, -1), non_blocking=True)
-                plan._products(plan.F)
+                plan._products(sig_view)  # signals resident in HBM, read in place
                 e[1].record(stream)
                 if plan.fused_synth:  # recursion with the synthesis inside
                     plan._iterate_synth(plan.selected, plan.projections, plan.coefficients,

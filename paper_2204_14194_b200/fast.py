@@ -891,10 +891,16 @@ class ExtrapolationPlan:
         """Enqueue one batch. ``signals``: None (use ``self.F`` as filled by the
         caller) or a (B, M, N) / (B, M) float64 tensor on any device (copied
         asynchronously into the device buffer)."""
+        F = self.F
         if signals is not None:
             src = signals.reshape(self.B, -1)
-            self.F[:, : self.M].copy_(src, non_blocking=True)
-        self.products_method = self._products(self.F)
+            torch = _torch()
+            if (src.device == self.device and src.dtype == torch.float64 and src.is_contiguous()
+                    and F.shape[1] == self.M and src.data_ptr() % 16 == 0):
+                F = src  # already in the kernels' layout: read in place, no copy
+            else:
+                F[:, : self.M].copy_(src, non_blocking=True)
+        self.products_method = self._products(F)
         self._iterate_synth(self.selected, self.projections, self.coefficients, self.lost)
         return self
 
