@@ -889,8 +889,11 @@ class ExtrapolationPlan:
 
     def run(self, signals=None):
         """Enqueue one batch. ``signals``: None (use ``self.F`` as filled by the
-        caller) or a (B, M, N) / (B, M) float64 tensor on any device (copied
-        asynchronously into the device buffer)."""
+        caller) or a (B, M, N) / (B, M) float64 tensor on any device. A
+        contiguous float64 tensor on the plan's device whose rows already have
+        the kernels' layout (even area) is read in place and must stay unchanged
+        until the batch completes; anything else is copied asynchronously into
+        ``self.F``."""
         F = self.F
         if signals is not None:
             src = signals.reshape(self.B, -1)
