@@ -312,6 +312,18 @@ def measured_peaks():
     return hbm, src, fp64, fsrc
 
 
+def measured_l2():
+    """(GB/s, source): L2 -> SM read bandwidth measured on this pool's B200 with
+    tools/probes/l2_probe.cu (best over L2-resident buffer sizes), or None."""
+    q = ROOT / "profiles" / "r01_l2_peak.json"
+    try:
+        res = json.loads(q.read_text())["results"]
+        best = max(r["read_gbs"] for r in res if r["mb"] <= 96)
+        return best, "tools/probes/l2_probe.cu: ld.global.cg 16-byte reads of L2-resident buffers"
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def ncu_traffic(kernel: str, tag: str):
     """DRAM bytes per launch of ``kernel`` from the committed ncu capture of the
     same workload (profiles/ncu_summary.json, key "<tag>/<kernel>"), or None."""
@@ -322,6 +334,18 @@ def ncu_traffic(kernel: str, tag: str):
         return json.loads(p.read_text()).get(f"{tag}/{kernel}", {}).get("dram_bytes_per_launch")
     except ValueError:
         return None
+
+
+def l2_roofline(achieved_gbs):
+    """The recursion's row stream against the measured L2 read bandwidth: with
+    most rows L2 hits (ncu), L2 -> SM bandwidth, not HBM, bounds the kernel."""
+    m = measured_l2()
+    if m is None:
+        return None
+    peak, src = m
+    return {"bound": "l2", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+            "frac": achieved_gbs / peak, "peak_source": src,
+            "note": "same algorithmic bytes as roofline (one table row per block-iteration)"}
 
 
 def ozaki_roofline(plan, flops_fp64, seconds, fp64_peak, fp64_src):
@@ -582,6 +606,7 @@ def run_gpu(args):
                          "note": ("16*K bytes per block-iteration (one complex128 table row)"
                                   if cplx else "8*K bytes per block-iteration (one FP64 table row)")
                                  + "; hot rows hit L2, so frac can exceed DRAM-bound expectations"},
+            "roofline_l2": l2_roofline(achieved),
             "roofline_init": (ozaki_roofline(plan, flops_init, init_s, fp64, fsrc)
                               if plan._ozaki is not None else
                               {"bound": "tensor", "kernel": "dgemm_nt_kernel (DMMA FP64)"
