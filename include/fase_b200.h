@@ -258,9 +258,11 @@ FASE_API int fase_iterate_scaled(const fase_iterate_args* args, const fase_synth
                                  void* stream);
 FASE_API int fase_iterate_scaled_synth_capacity(int K, int B);
 
-/* Gs[u*lds + k] = G[u*ldg + k] * D[k] (k < K), 0 for K <= k < lds; lds even. */
-FASE_API int fase_scale_columns(const double* G, int64_t ldg, const double* D, int K, double* Gs,
-                                int64_t lds, void* stream);
+/* Gs[u*lds + k] = G[u*ldg + k] * D[k] (u < rows, k < K), 0 for K <= k < lds;
+ * lds even. A complex table (rows of conj(C)) is scaled as its real view:
+ * rows = K, 2K columns, D repeated per (re, im) pair. */
+FASE_API int fase_scale_columns(const double* G, int64_t ldg, const double* D, int rows, int K,
+                                double* Gs, int64_t lds, void* stream);
 
 /*
  * Model synthesis and paste (replaces SparseModel.materialize + apply_model,
@@ -343,6 +345,11 @@ FASE_API int fase_table_ld_complex(int K);
  * complex (B x ldo complex); D, sel as in fase_iterate.
  */
 FASE_API int fase_iterate_complex(const fase_iterate_args* args, void* stream);
+
+/* The scaled recursion for complex dictionaries (see fase_iterate_scaled):
+ * G0 holds column-scaled rows conj(C)[u, k] * D_k (fase_scale_columns on the
+ * real view), R' = R * D, the metric |R'|; shared geometry only. */
+FASE_API int fase_iterate_complex_scaled(const fase_iterate_args* args, void* stream);
 
 /*
  * Complex model synthesis and paste (SparseModel.materialize + apply_model):

@@ -38,6 +38,7 @@ EXPORTS = (
     "fase_synth_paste_complex", "fase_sep_products_complex", "fase_fft_gram", "fase_weigh_gather",
     "fase_ozaki_split", "fase_ozaki_gemm", "fase_ozaki_gram", "fase_sep_products_batch",
     "fase_iterate_scaled", "fase_scale_columns", "fase_iterate_scaled_synth_capacity",
+    "fase_iterate_complex_scaled",
 )
 
 _vp = ctypes.c_void_p
@@ -116,7 +117,8 @@ def load():
         "fase_iterate": [ctypes.POINTER(IterateArgs), _vp],
         "fase_iterate_scaled": [ctypes.POINTER(IterateArgs), ctypes.POINTER(SynthFused), _vp],
         "fase_iterate_scaled_synth_capacity": [_i32, _i32],
-        "fase_scale_columns": [_vp, _i64, _vp, _i32, _vp, _i64, _vp],
+        "fase_scale_columns": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp],
+        "fase_iterate_complex_scaled": [ctypes.POINTER(IterateArgs), _vp],
         "fase_iterate_complex": [ctypes.POINTER(IterateArgs), _vp],
         "fase_gram_complex": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp, ctypes.c_size_t, _vp],
         "fase_synth_paste_complex": [_vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp,
@@ -318,16 +320,51 @@ def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *
 
 
 def scale_columns(G, D, K: int, Gs) -> None:
-    """Gs[u, k] = G[u, k] * D[k] (fase_scale_columns): the scaled recursion's table."""
+    """Gs[u, k] = G[u, k] * D[k] (fase_scale_columns): the scaled recursion's
+    table. Complex tables (rows of conj(C), complex128) are scaled as their real
+    view with D repeated per (re, im) pair."""
     import torch
 
     lib = load()
+    if G.is_complex():
+        _require(G, "G", torch.complex128, 2)
+        _require(Gs, "Gs", torch.complex128, 2)
+        _require(D, "D", torch.float64, 1)
+        Gr, Gsr = torch.view_as_real(G).reshape(G.shape[0], -1), \
+            torch.view_as_real(Gs).reshape(Gs.shape[0], -1)
+        D2 = D[:K].repeat_interleave(2).contiguous()
+        if Gs.shape[0] < K:
+            raise errors.ShapeError(f"Gs has {Gs.shape[0]} rows, need {K}")
+        _check(lib.fase_scale_columns(_ptr(Gr), Gr.stride(0), _ptr(D2), K, 2 * K, _ptr(Gsr),
+                                      Gsr.stride(0), _stream(Gs)))
+        return
     _require(G, "G", torch.float64, 2)
     _require(D, "D", torch.float64, 1)
     _require(Gs, "Gs", torch.float64, 2)
     if Gs.shape[0] < K:
         raise errors.ShapeError(f"Gs has {Gs.shape[0]} rows, need {K}")
-    _check(lib.fase_scale_columns(_ptr(G), _ld(G), _ptr(D), K, _ptr(Gs), _ld(Gs), _stream(Gs)))
+    _check(lib.fase_scale_columns(_ptr(G), _ld(G), _ptr(D), K, K, _ptr(Gs), _ld(Gs), _stream(Gs)))
+
+
+def iterate_complex_scaled(Gs, D, R0, K: int, iterations: int, gamma: float, sel, proj,
+                           coef) -> None:
+    """The complex scaled recursion (fase_iterate_complex_scaled) over the
+    column-scaled complex table ``Gs``; R0 (B, ldr) complex128, D unscaled."""
+    import torch
+
+    lib = load()
+    _require(Gs, "Gs", torch.complex128, 2)
+    _require(D, "D", torch.float64, 1)
+    _require(R0, "R0", torch.complex128, 2)
+    _require(sel, "sel", torch.int32, 2)
+    _require(proj, "proj", torch.complex128, 2)
+    _require(coef, "coef", torch.complex128, 2)
+    args = IterateArgs(G0=_ptr(Gs), ldg=_ld(Gs), D=_ptr(D), ldd=0, R0=_ptr(R0), ldr=_ld(R0), K=K,
+                       B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel), proj=_ptr(proj),
+                       coef=_ptr(coef), ldo=_ld(sel))
+    if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
+        raise errors.ShapeError("sel / proj / coef must share one leading dimension")
+    _check(lib.fase_iterate_complex_scaled(ctypes.byref(args), _stream(R0)))
 
 
 def scaled_synth_capacity(K: int, B: int) -> int:

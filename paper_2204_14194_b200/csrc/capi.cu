@@ -100,10 +100,10 @@ __global__ void __launch_bounds__(kFinishThreads) gram_finish_kernel(const doubl
 // rows; 16-byte loads and stores.
 __global__ void __launch_bounds__(256) scale_columns_kernel(const double* __restrict__ G,
                                                             int64_t ldg, const double* __restrict__ D,
-                                                            int K, double* __restrict__ Gs,
+                                                            int rows, int K, double* __restrict__ Gs,
                                                             int64_t lds) {
   const int pairs = static_cast<int>(lds / 2);
-  for (int64_t u = blockIdx.x; u < K; u += gridDim.x) {
+  for (int64_t u = blockIdx.x; u < rows; u += gridDim.x) {
     const double* g = G + u * ldg;
     double* o = Gs + u * lds;
     for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
@@ -364,14 +364,15 @@ extern "C" int fase_gram_finish(const double* G, int64_t ldg, int K, double* D, 
   return check_launch("fase_gram_finish");
 }
 
-extern "C" int fase_scale_columns(const double* G, int64_t ldg, const double* D, int K, double* Gs,
-                                  int64_t lds, void* stream) {
-  if (K < 1 || ldg < K || lds < K || (lds & 1) || !G || !D || !Gs || !aligned16(Gs)) {
-    set_error("fase_scale_columns: bad operand (K=%d, ldg=%lld, lds=%lld)", K,
+extern "C" int fase_scale_columns(const double* G, int64_t ldg, const double* D, int rows, int K,
+                                  double* Gs, int64_t lds, void* stream) {
+  if (rows < 1 || K < 1 || ldg < K || lds < K || (lds & 1) || !G || !D || !Gs || !aligned16(Gs)) {
+    set_error("fase_scale_columns: bad operand (rows=%d, K=%d, ldg=%lld, lds=%lld)", rows, K,
               static_cast<long long>(ldg), static_cast<long long>(lds));
     return FASE_ERR_SHAPE;
   }
-  scale_columns_kernel<<<min(K, 148 * 8), 256, 0, as_stream(stream)>>>(G, ldg, D, K, Gs, lds);
+  scale_columns_kernel<<<min(rows, 148 * 8), 256, 0, as_stream(stream)>>>(G, ldg, D, rows, K, Gs,
+                                                                          lds);
   return check_launch("fase_scale_columns");
 }
 

@@ -49,11 +49,21 @@ constexpr int kCap = 64;  // candidate list capacity
 // NB == 2 (shared geometry, D^2 in shared memory): one CTA runs two blocks on
 // its two NT-thread halves (own staged row, candidate list, named barriers)
 // that share one copy of D^2, as in the real kernel's paired variants.
-template <int NT, int EP, int MINB, bool kDsmem, bool kChunked, bool kRecord, int NB>
+//
+// kScaled (fase_iterate_complex_scaled, shared geometry): as the real scaled
+// recursion -- the table rows are column-scaled, conj(C)[u, k] * D_k, and the
+// state is R'_k = R_k * D_k, so the proxy is |R'|^2 and the exact metric
+// |R'| (np.abs of the scaled value) with no normalizers in the loop;
+// p = R'_u * D_u. Dead atoms hold NaN. Selections match the exact kernel up
+// to ties within the rounding of the scaled operands.
+template <int NT, int EP, int MINB, bool kDsmem, bool kChunked, bool kRecord, int NB,
+          bool kScaled = false>
 __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(const fase_iterate_args a) {
   constexpr int NW = NT / 32;
   constexpr int kSeg = EP < 3 ? EP : 3;
   static_assert(NB == 1 || (kDsmem && !kChunked), "paired blocks share one D^2 in shared memory");
+  static_assert(!kScaled || (!kDsmem && !kChunked && !kRecord && NB == 1),
+                "the scaled recursion keeps no normalizers and has one block per CTA");
 
   __shared__ long long s_key_all[NB][NW];
   __shared__ unsigned s_arg_all[NB][NW];
@@ -122,7 +132,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
   }
 
   double r[EP][2];
-  double dreg[kDsmem ? 1 : EP];
+  double dreg[(kDsmem || kScaled) ? 1 : EP];
   auto d2 = [&](int j) -> double {  // D^2 of element j; dead: -inf
     if constexpr (kDsmem)
       return s_D2[j * NT + t];
@@ -137,7 +147,23 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
     return dk != 0.0 ? dk : kDead;
   };
   auto proxy = [](double re, double im, double d2) {
-    return mul_rn(__fma_rn(re, re, mul_rn(im, im)), d2);
+    if constexpr (kScaled)
+      return __fma_rn(re, re, mul_rn(im, im));
+    else
+      return mul_rn(__fma_rn(re, re, mul_rn(im, im)), d2);
+  };
+  auto d2_if = [&](int j) -> double {
+    if constexpr (kScaled)
+      return 1.0;
+    else
+      return d2(j);
+  };
+  // the exact metric |R| * D (scaled: |R'|)
+  auto emetric = [](double re, double im, double d) {
+    if constexpr (kScaled)
+      return np_cabs_fast(re, im);
+    else
+      return mul_rn(np_cabs_fast(re, im), d);
   };
   double best = kDead;
   unsigned barg = kNone;
@@ -148,7 +174,11 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
     r[j][1] = k < K ? R0[2 * k + 1] : 0.0;
     const double dk = k < K ? D[k] : 0.0;
     const double dsq = dk != 0.0 ? mul_rn(dk, dk) : kDead;
-    if constexpr (kDsmem) {
+    if constexpr (kScaled) {
+      const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
+      r[j][0] = dk != 0.0 ? mul_rn(r[j][0], dk) : kNaN;
+      r[j][1] = dk != 0.0 ? mul_rn(r[j][1], dk) : kNaN;
+    } else if constexpr (kDsmem) {
       if (half == 0) s_D2[j * NT + t] = dsq;
     } else
       dreg[j] = dsq;
@@ -233,7 +263,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
     if (trusted && pc > 0.0 && wkey >= 0 && __longlong_as_double(wkey) >= pc) {  // warp-uniform
 #pragma unroll
       for (int j = 0; j < EP; ++j) {
-        if (proxy(r[j][0], r[j][1], d2(j)) >= pc) {  // exact metric after the barrier
+        if (proxy(r[j][0], r[j][1], d2_if(j)) >= pc) {  // exact metric after the barrier
           const int slot = atomicAdd(&s_cnt[it & 1], 1);
           if (slot < kCap) {
             s_ck[slot] = static_cast<unsigned>(j * NT + t);
@@ -258,7 +288,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
       ru = s_cr[0];
       du = s_cd[0];
       if (mul_rn(1e-13, top_hi) > q) {
-        const double top = mul_rn(np_cabs_fast(ru.x, ru.y), du);
+        const double top = emetric(ru.x, ru.y, du);
         if (top > 0.0 && top < __longlong_as_double(0x7ff0000000000000LL)) q = fmax(q, mul_rn(1e-13, top));
       }
     } else if (trusted && pc > 0.0 && cnt >= 2 && cnt <= kCap) {
@@ -268,7 +298,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
       double m0 = -1.0;
       for (int l = lane; l < cnt; l += 32) {
         const double2 rv = s_cr[l];
-        const double m = mul_rn(np_cabs_fast(rv.x, rv.y), s_cd[l]);
+        const double m = emetric(rv.x, rv.y, s_cd[l]);
         if (l == lane) m0 = m;
         else s_cm[l] = m;
         const long long v = __double_as_longlong(m);  // metrics of candidates are >= 0
@@ -311,7 +341,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
       for (int jj = 0; jj < EP; ++jj) {
         double re, im, d;
         element(jj, re, im, d);
-        const double m = mul_rn(np_cabs_fast(re, im), d);  // dead: -inf or NaN
+        const double m = emetric(re, im, d);  // dead: -inf or NaN
         mb = m > mb ? m : mb;
       }
       const long long wk = warp_max_i64(__double_as_longlong(mb));
@@ -330,7 +360,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
       for (int jj = 0; jj < EP; ++jj) {
         double re, im, d;
         element(jj, re, im, d);
-        if (cand == kNone && mul_rn(np_cabs_fast(re, im), d) >= thr) {
+        if (cand == kNone && emetric(re, im, d) >= thr) {
           cand = static_cast<unsigned>(jj * NT + t);
           rv = make_double2(re, im);
           dv = d;
@@ -352,7 +382,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
       du = s_cd[uw];
     }
 
-    const double d2u = mul_rn(du, du);
+    const double d2u = kScaled ? du : mul_rn(du, du);  // scaled: p = R'_u * D_u
     const double pr = mul_rn(ru.x, d2u), pi = mul_rn(ru.y, d2u);
     const double cr = mul_rn(a.gamma, pr), ci = mul_rn(a.gamma, pi);
     if (t == 0) {
@@ -382,7 +412,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
         const double2 x = np_cmul(cr, ci, g.x, g.y);
         r[j][0] = sub_rn(r[j][0], x.x);
         r[j][1] = sub_rn(r[j][1], x.y);
-        const double pk = proxy(r[j][0], r[j][1], d2(j));
+        const double pk = proxy(r[j][0], r[j][1], d2_if(j));
         if (pk > best) {
           best = pk;
           barg = static_cast<unsigned>(j * NT + t);
@@ -488,6 +518,19 @@ const ExtraVariant kExtraVariants[] = {
     {2, FASE_CV(256, 7, 2, true)}, {2, FASE_CV(256, 8, 2, true)}, {2, FASE_CV(256, 9, 2, true)},
 };
 #undef FASE_CV
+
+// Scaled recursion: no D^2 in shared memory; ordered by capacity like
+// kVariants (same table layout), 256-thread shapes up to 5120 atoms (two
+// blocks per SM where the exact kernel needs paired 512-thread CTAs).
+#define FASE_CS(NT, EP, MINB) \
+  {NT, EP, false, fase_iterate_complex_kernel<NT, EP, MINB, false, false, false, 1, true>, nullptr, nullptr}
+const Variant kScaledVariants[] = {
+    FASE_CS(128, 1, 4),  FASE_CS(128, 2, 4),  FASE_CS(128, 4, 4),  FASE_CS(128, 8, 4),
+    FASE_CS(256, 5, 3),  FASE_CS(256, 6, 3),  FASE_CS(256, 7, 3),  FASE_CS(256, 8, 3),
+    FASE_CS(256, 9, 3),  FASE_CS(256, 10, 2), FASE_CS(256, 12, 2), FASE_CS(256, 16, 2),
+    FASE_CS(256, 18, 2), FASE_CS(256, 20, 2), FASE_CS(512, 12, 1),
+};
+#undef FASE_CS
 
 const Variant* pick_variant(int K) {
   for (const Variant& v : kVariants)
@@ -595,4 +638,61 @@ extern "C" int fase_iterate_complex(const fase_iterate_args* args, void* stream)
   }
   fn<<<(a.B + v->nb - 1) / v->nb, v->nt * v->nb, smem, as_stream(stream)>>>(a);
   return check_launch("fase_iterate_complex");
+}
+
+extern "C" int fase_iterate_complex_scaled(const fase_iterate_args* args, void* stream) {
+  if (!args) {
+    set_error("fase_iterate_complex_scaled: null argument block");
+    return FASE_ERR_PARAMETER;
+  }
+  const fase_iterate_args& a = *args;
+  if (a.K < 1 || a.B < 0 || a.I < 1) {
+    set_error("fase_iterate_complex_scaled: bad sizes (K=%d, B=%d, I=%d)", a.K, a.B, a.I);
+    return FASE_ERR_SHAPE;
+  }
+  if (!(a.gamma > 0.0 && a.gamma <= 1.0)) {
+    set_error("fase_iterate_complex_scaled: gamma must lie in (0, 1], got %g", a.gamma);
+    return FASE_ERR_PARAMETER;
+  }
+  if (a.B == 0) return FASE_OK;
+  if (!a.G0 || !aligned16(a.G0) || a.ldg < a.K || !a.D || !a.R0 || !aligned16(a.R0) ||
+      a.ldr < a.K || !a.sel || !a.proj || !a.coef || a.ldo < a.I) {
+    set_error("fase_iterate_complex_scaled: bad operand (null, misaligned or short leading "
+              "dimension)");
+    return FASE_ERR_SHAPE;
+  }
+  if (a.chunk_count || a.compose || a.ldd != 0 || a.R_out || a.R_log) {
+    set_error("fase_iterate_complex_scaled: shared geometry only (no chunk tables, per-block D, "
+              "R_out or R_log)");
+    return FASE_ERR_UNSUPPORTED;
+  }
+  const Variant* dflt = pick_variant(a.K);
+  const Variant* v = nullptr;
+  for (const Variant& sv : kScaledVariants)
+    if (sv.nt * sv.ep >= a.K) {
+      v = &sv;
+      break;
+    }
+  if (!dflt || !v) {
+    set_error("fase_iterate_complex_scaled: K=%d exceeds the largest kernel variant (%d atoms)",
+              a.K, fase_max_atoms_complex());
+    return FASE_ERR_UNSUPPORTED;
+  }
+  if (a.ldg < v->nt * v->ep) {
+    set_error("fase_iterate_complex_scaled: table rows must be zero-padded to "
+              "fase_table_ld_complex(K)=%d (ldg=%lld)", dflt->nt * dflt->ep,
+              static_cast<long long>(a.ldg));
+    return FASE_ERR_SHAPE;
+  }
+  const size_t smem = static_cast<size_t>(v->nt) * v->ep * sizeof(double2);
+  cudaError_t e = cudaFuncSetAttribute(v->plain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(v->plain, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) {
+    set_error("fase_iterate_complex_scaled: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return FASE_ERR_CUDA;
+  }
+  v->plain<<<a.B, v->nt, smem, as_stream(stream)>>>(a);
+  return check_launch("fase_iterate_complex_scaled");
 }

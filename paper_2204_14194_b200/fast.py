@@ -224,14 +224,15 @@ class GramTable:
                 self._uploaded[key] = (G, D)
         return self._uploaded[key]
 
-    def scaled_table(self, device):
-        """(Gs, D): the column-scaled real table Gs[u, k] = G[u, k] * D_k of the
-        scaled recursion (``fase_iterate_scaled``), built on the device once and
-        cached (one more K x table_ld(K) float64 matrix)."""
+    def scaled_table(self, device, complex_rows: bool = False):
+        """(Gs, D): the column-scaled table Gs[u, k] = G[u, k] * D_k of the
+        scaled recursion (``fase_iterate_scaled``; complex rows of conj(C) for
+        ``fase_iterate_complex_scaled``), built on the device once and cached
+        (one more table of the layout ``device_tables`` gives)."""
         torch = _torch()
-        key = (device.type, device.index, "scaled")
+        key = (device.type, device.index, "scaled", complex_rows)
         if key not in self._uploaded:
-            G, D = self.device_tables(device)
+            G, D = self.device_tables(device, complex_rows=complex_rows)
             Gs = torch.empty_like(G)
             _native.scale_columns(G, D, self._k, Gs)
             self._uploaded[key] = (Gs, D)
@@ -244,17 +245,17 @@ RECURSIONS = ("exact", "scaled")
 def _check_recursion(recursion: str, cplx: bool, shared: bool = True, record: bool = False):
     """Validate the ``recursion`` option of the batch entry points.
 
-    ``exact``: fase_iterate, bit-identical to the reference given the same
-    tables and initial products. ``scaled``: fase_iterate_scaled over the
-    column-scaled table (real shared geometries; ~1.25x faster at config 1):
-    selections identical except within a few ulp of a tie, coefficients to
-    rounding -- the north-star parity bar, not bit-identity.
+    ``exact``: fase_iterate(_complex), bit-identical to the reference given
+    the same tables and initial products. ``scaled``: fase_iterate(_complex)
+    _scaled over the column-scaled table (shared geometries; ~1.25x faster at
+    config 1): selections identical except within a few ulp of a tie,
+    coefficients to rounding -- the north-star parity bar, not bit-identity.
     """
     if recursion not in RECURSIONS:
         raise ParameterError(f"recursion must be one of {RECURSIONS}, got {recursion!r}")
-    if recursion == "scaled" and (cplx or not shared or record):
+    if recursion == "scaled" and (not shared or record):
         raise UnsupportedDictionaryError(
-            "the scaled recursion runs real shared-geometry batches without product logs")
+            "the scaled recursion runs shared-geometry batches without product logs")
 
 
 def _device_vector(x: np.ndarray, length: int, device):
@@ -677,8 +678,9 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
     coef = torch.empty((B, I), dtype=vdt, device=dev)
     R_log = torch.empty((B, I, ldr), dtype=vdt, device=dev) if record_products else None
     if recursion == "scaled":
-        Gs, _ = tables.scaled_table(dev)
-        _native.iterate_scaled(Gs, D, R0, K, I, config.gamma, sel, proj, coef)
+        Gs, _ = tables.scaled_table(dev, complex_rows=cplx)
+        (_native.iterate_complex_scaled if cplx else _native.iterate_scaled)(
+            Gs, D, R0, K, I, config.gamma, sel, proj, coef)
     else:
         (_native.iterate_complex if cplx else _native.iterate)(
             G, D, R0, K, I, config.gamma, sel, proj, coef, R_log=R_log, **chunk_args)
@@ -750,7 +752,7 @@ class ExtrapolationPlan:
             raise UnsupportedDictionaryError(f"K={K} exceeds the iteration kernel's {kmax}")
         self.G, self.D = tables.device_tables(dev, complex_rows=cplx)
         # the scaled recursion reads the column-scaled table instead of G
-        self.Gs = tables.scaled_table(dev)[0] if recursion == "scaled" else None
+        self.Gs = tables.scaled_table(dev, complex_rows=cplx)[0] if recursion == "scaled" else None
         self.K, self.M, self.I, self.B = K, M, I, int(n_blocks)
         self.phi = dictionary.device_matrix(dev)
         self.W = _device_vector(w, dictionary.ld, dev)
@@ -782,7 +784,7 @@ class ExtrapolationPlan:
         # the synthesis runs inside the recursion (config 0: 0.112 -> 0.099 ms);
         # at full occupancy the separate kernel is faster (fused: c1 -6%, c4 -4%)
         self.fused_synth = bool(
-            self.Gs is not None and self.n_lost
+            self.Gs is not None and not cplx and self.n_lost
             and self.B <= torch.cuda.get_device_properties(dev).multi_processor_count
             and self.n_lost <= _native.scaled_synth_capacity(K, self.B))
         if cplx:
@@ -865,8 +867,12 @@ class ExtrapolationPlan:
     def _iterate_synth(self, sel, proj, coef, lost, slot: int = 0):
         sc = self._scratch(slot)
         if self.complex:
-            _native.iterate_complex(self.G, self.D, sc["R0"], self.K, self.I, self.config.gamma,
-                                    sel, proj, coef)
+            if self.Gs is not None:
+                _native.iterate_complex_scaled(self.Gs, self.D, sc["R0"], self.K, self.I,
+                                               self.config.gamma, sel, proj, coef)
+            else:
+                _native.iterate_complex(self.G, self.D, sc["R0"], self.K, self.I,
+                                        self.config.gamma, sel, proj, coef)
             if self.n_lost:
                 _native.synth_paste_complex(self.phi_lost, sel, coef, self.I, self.lost_seq, lost,
                                             n_shared=self.n_lost, dst=self.lost_pos,

@@ -143,7 +143,8 @@ def _check_block(got_sel, got_coef, want_sel, want_coef, metric_at):
     return v
 
 
-def test_dft48_end_to_end(golden_dir):
+@pytest.mark.parametrize("recursion", ["exact", "scaled"])
+def test_dft48_end_to_end(golden_dir, recursion):
     """The reference's default dictionary on the config-1 geometry, GPU-built
     tables and products, against the reference's own results."""
     z = np.load(golden_dir / "dft48_blocks.npz")
@@ -153,7 +154,7 @@ def test_dft48_end_to_end(golden_dir):
     mask = wl.central_loss_mask(m, n, *w1.loss)
     blocks = list(z["blocks"])
     sig = wl.block_signals(1, len(blocks), m, n)
-    res = fase_extrapolate_batch(sig, mask, d, None, w1.config, device=DEV)
+    res = fase_extrapolate_batch(sig, mask, d, None, w1.config, device=DEV, recursion=recursion)
     tabs = None
     for b in blocks:
         def metric_at(t, b=b):
@@ -173,12 +174,13 @@ def test_dft48_end_to_end(golden_dir):
 
 @pytest.mark.parametrize("spec,m,n", [("union:dft+bdft", 16, 16), ("union:wht+dft", 16, 16),
                                       ("bdft", 9, 7)])
-def test_complex_batch_against_oracle(spec, m, n):
+@pytest.mark.parametrize("recursion", ["exact", "scaled"])
+def test_complex_batch_against_oracle(spec, m, n, recursion):
     d = parse_dict_spec(spec, m, n)
     mask = wl.central_loss_mask(m, n, m // 3, n // 3)
     sig = np.random.default_rng(11).uniform(0, 255, (5, m, n))
     cfg = ExtrapConfig(60, 0.5, 0.8)
-    res = fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV)
+    res = fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion=recursion)
     vals = d.values
     for b in range(5):
         ref = orc.extrapolate_block(sig[b], mask, vals, 0.5, 60, 0.8, record=True)
@@ -327,3 +329,33 @@ def test_complex_recursion_bit_exact_paired_blocks(k_rand, copies):
         assert np.array_equal(got, sel), b
         assert np.array_equal(res.coefficients[b].cpu().numpy(), coef), b
         assert np.array_equal(res.projections[b].cpu().numpy(), proj), b
+
+
+def test_complex_scaled_matches_exact_and_dead_atoms():
+    """The scaled complex recursion: the same selections as the exact kernel on
+    the config-1 geometry with the default dictionary (coefficients to
+    rounding); a zero signal selects the lowest live atom with coefficient 0;
+    dead atoms are never selected."""
+    w1 = wl.WORKLOADS[1]
+    m, n = w1.area
+    d = parse_dict_spec("dft", m, n)
+    mask = wl.central_loss_mask(m, n, *w1.loss)
+    sig = wl.block_signals(1, 200, m, n)
+    rx = fase_extrapolate_batch(sig, mask, d, None, w1.config, device=DEV)
+    rs = fase_extrapolate_batch(sig, mask, d, None, w1.config, device=DEV, recursion="scaled")
+    same = (rx.selected == rs.selected).all(dim=1)
+    assert int(same.sum()) >= 198
+    cx, cs = rx.coefficients[same], rs.coefficients[same]
+    assert float(((cx - cs).abs().amax(dim=1) / cx.abs().amax(dim=1)).max()) < 1e-12
+    d8 = parse_dict_spec("dft", 8, 8)
+    m8 = wl.central_loss_mask(8, 8, 4, 4)
+    r0 = fase_extrapolate_batch(np.zeros((2, 8, 8)), m8, d8, None, ExtrapConfig(5), device=DEV,
+                                recursion="scaled")
+    assert (r0.selected.cpu().numpy() == 0).all() and (r0.coefficients.cpu().numpy() == 0).all()
+    inside = np.zeros((4, 4), dtype=np.complex128)
+    inside[1:3, 1:3] = 1.0 + 1.0j
+    dd = Dictionary(np.concatenate([inside[None], parse_dict_spec("dft", 4, 4).values]))
+    m4 = wl.central_loss_mask(4, 4, 2, 2)
+    r = fase_extrapolate_batch(np.random.default_rng(2).standard_normal((3, 4, 4)), m4, dd, None,
+                               ExtrapConfig(10), device=DEV, recursion="scaled")
+    assert (r.selected.cpu().numpy() != 0).all()

@@ -297,8 +297,8 @@ def test_recursion_scaled_dead_atoms_and_options():
     with pytest.raises(UnsupportedDictionaryError):
         fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion="scaled",
                                record_products=True)
-    with pytest.raises(UnsupportedDictionaryError):
-        fase_extrapolate_batch(sig, mask, parse_dict_spec("dft", m, n), None, cfg, device=DEV,
+    with pytest.raises(UnsupportedDictionaryError):  # per-block geometries: exact only
+        fase_extrapolate_batch(sig, np.stack([mask] * 4 + [~mask]), d, None, cfg, device=DEV,
                                recursion="scaled")
 
 

@@ -113,12 +113,14 @@ def test_status_codes_and_messages(lib):
     assert b"fused-synthesis" in lib.fase_last_error()
     assert lib.fase_iterate_scaled_synth_capacity(4608, 1024) >= 256
     assert lib.fase_iterate_scaled_synth_capacity(0, 1) == 0
-    assert lib.fase_scale_columns(None, 4, None, 4, None, 4, None) == -1
-    assert lib.fase_scale_columns(fake, 4, fake, 4, fake, 5, None) == -1  # odd lds
+    assert lib.fase_scale_columns(None, 4, None, 4, 4, None, 4, None) == -1
+    assert lib.fase_scale_columns(fake, 4, fake, 4, 4, fake, 5, None) == -1  # odd lds
     # empty batches are a no-op, not an error
     args = _native.IterateArgs(K=4, B=0, I=1, gamma=0.5)
     assert lib.fase_iterate(ctypes.byref(args), None) == 0
     assert lib.fase_iterate_scaled(ctypes.byref(args), None, None) == 0
+    assert lib.fase_iterate_complex_scaled(ctypes.byref(args), None) == 0
+    assert lib.fase_iterate_complex_scaled(None, None) == -2
     assert lib.fase_ozaki_gemm(None, 128, None, 0, None, 64, None, 50, 64, 8, None, 50, None) == 0
 
 
