@@ -9,6 +9,7 @@ for c in 4 3 2; do
   python bench.py --config $c --steps 10 --warmup 3 --cpu-seconds 8 > gpurun_out/benches/c$c.json 2> gpurun_out/benches/c$c.err; echo c$c=$?
 done
 python bench.py --config 1 --dict dft --steps 10 --warmup 3 --cpu-seconds 8 > gpurun_out/benches/c1_dft.json 2> gpurun_out/benches/c1_dft.err; echo c1dft=$?
+python bench.py --config 1 --dict union:dft+bdft --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/benches/c1_dftbdft.json 2> gpurun_out/benches/c1_dftbdft.err; echo c1dftbdft=$?
 python bench.py --config 1 --recursion exact --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/benches/c1_exact.json 2> gpurun_out/benches/c1_exact.err; echo c1exact=$?
 python bench.py --config 4 --recursion exact --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/benches/c4_exact.json 2> gpurun_out/benches/c4_exact.err; echo c4exact=$?
 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/benches/c1_reference.json 2> gpurun_out/benches/c1_reference.err; echo ref=$?
