@@ -75,7 +75,8 @@ def to_bytes(val: str, unit: str) -> float:
 
 def short(name: str) -> str:
     for key in ("fase_iterate_complex_kernel", "fase_iterate_kernel", "dgemm_nt_kernel",
-                "synth_paste_complex_kernel", "synth_paste_kernel", "gram_finish_kernel",
+                "synth_paste_complex_kernel", "synth_paste_pair_kernel", "synth_paste_kernel",
+                "scale_columns_kernel", "gram_finish_kernel",
                 "weigh_gather_kernel", "weigh_kernel", "sep_products_complex_kernel",
                 "sep_products_dmma_kernel",
                 "sep_products_kernel", "ozaki_gemm_kernel", "ozaki_split_kernel",
