@@ -167,6 +167,8 @@ FASE_API int fase_sep_products_batch(const fase_sep_part* parts, int n_parts, in
  * G_b = G0 - sum_{j in chunks(b)} C_j (see fase_iterate):
  *   diag_b[k] = G0[k,k] - sum_j C_j[k,k];  D[b*ldd + k] as in fase_gram_finish.
  * n_alive[b] receives the count of non-degenerate atoms of block b.
+ * ldg == 0: G0 and the chunk tables are passed as their diagonals instead
+ * (G0[k] and chunk_tables[j*chunk_stride + k]); same values, same order.
  */
 FASE_API int fase_block_normalizers(const double* G0, int64_t ldg, const double* chunk_tables,
                            int64_t chunk_stride, const int32_t* chunk_count,

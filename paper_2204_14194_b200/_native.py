@@ -274,11 +274,13 @@ def init_products(phi, f, w, K: int, M: int, R0, ws=None) -> None:
 
 def block_normalizers(G0, chunk_tables, chunk_stride: int, chunk_count, chunk_ids, K: int,
                       D, n_alive) -> None:
-    """D of B per-block geometries; chunk_ids is (B, L) with chunk_count[b] valid entries."""
+    """D of B per-block geometries; chunk_ids is (B, L) with chunk_count[b] valid entries.
+    ``G0`` 1-D: the tables are given as their diagonals (G0 (K,), chunk_tables
+    (n, chunk_stride) rows of diagonals), read contiguously."""
     import torch
 
     lib = load()
-    _require(G0, "G0", torch.float64, 2)
+    _require(G0, "G0", torch.float64)
     _require(D, "D", torch.float64, 2)
     list_ld = _ld(chunk_ids) if chunk_ids is not None else 0
     _check(lib.fase_block_normalizers(_ptr(G0), _ld(G0), _ptr(chunk_tables), chunk_stride,

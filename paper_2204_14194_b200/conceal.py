@@ -151,6 +151,10 @@ class FrameEngine:
         torch.cuda.current_stream(dev).synchronize()
         self.table_seconds = time.perf_counter() - t0
         self.stride = self.tables[0].numel()
+        # diagonals of G0 and of every cell table for the per-frame normalizers:
+        # contiguous, L2-resident reads instead of one sector per diagonal element
+        self._diag_G0 = self.G0.diagonal()[:K].contiguous()
+        self._diag_tabs = self.tables.diagonal(dim1=1, dim2=2)[:, :K].contiguous()
         self.cell_rep = torch.tensor([[c[0], c[2]] for c in self.cells] or [[0, 0]],
                                      dtype=torch.int32, device=dev)
         self.base_w = torch.from_numpy(flat_base.copy()).to(dev)
@@ -248,7 +252,7 @@ class FrameEngine:
         _native.frame_areas(frame, grid, self.tile, self.support, corners, self.base_w, b["X"])
         _native.frame_cells(grid, self.H, self.W, self.tile, self.support, corners, self.cell_rep,
                             b["counts"], b["ids"])
-        _native.block_normalizers(self.G0, self.tables, self.stride, b["counts"], b["ids"], K,
+        _native.block_normalizers(self._diag_G0, self._diag_tabs, K, b["counts"], b["ids"], K,
                                   b["D"], b["alive"])
         factors = self.dictionary.device_factors(self.device)
         if factors and len(factors) <= 8:  # separable parts on DMMA, one launch

@@ -381,7 +381,10 @@ extern "C" int fase_block_normalizers(const double* G0, int64_t ldg, const doubl
                                       const int32_t* chunk_ids, int64_t chunk_list_ld, int K,
                                       int B, double* D, int64_t ldd, int32_t* n_alive,
                                       void* stream) {
-  if (K < 1 || B < 0 || ldg < K || ldd < K || !G0 || !D) {
+  // ldg == 0: G0 and the chunk tables are given as their diagonals
+  // (G0[k], chunk_tables[id * chunk_stride + k]), e.g. extracted once per table
+  // set -- contiguous reads instead of one sector per diagonal element
+  if (K < 1 || B < 0 || (ldg != 0 && ldg < K) || ldd < K || !G0 || !D) {
     set_error("fase_block_normalizers: bad operand (K=%d, B=%d)", K, B);
     return FASE_ERR_SHAPE;
   }
