@@ -71,6 +71,9 @@ def central_loss_mask(m_rows: int, n_cols: int, loss_rows: int, loss_cols: int) 
     if not (1 <= loss_rows <= m_rows and 1 <= loss_cols <= n_cols):
         from .errors import ParameterError
         raise ParameterError(f"loss block {loss_rows}x{loss_cols} does not fit {m_rows}x{n_cols}")
+    if loss_rows == m_rows and loss_cols == n_cols:
+        from .errors import ParameterError
+        raise ParameterError("loss block covers the whole area; no support left")
     mask = np.zeros((m_rows, n_cols), dtype=bool)
     r0 = (m_rows - loss_rows) // 2
     c0 = (n_cols - loss_cols) // 2

@@ -277,3 +277,27 @@ def test_fgrm_rejects_bad_files(golden_dir, tmp_path):
         bad.write_bytes(payload)
         with pytest.raises(FormatError):
             load_gram_table(bad)
+
+
+def test_central_loss_mask_errors():
+    """Same ParameterError conditions as the reference (verify.py:37-49)."""
+    assert wl.central_loss_mask(48, 48, 16, 16)[16:32, 16:32].all()
+    assert wl.central_loss_mask(4, 4, 4, 3).sum() == 12
+    for bad in ((4, 4, 4, 4), (4, 4, 0, 2), (4, 4, 5, 1), (3, 5, 1, 6)):
+        with pytest.raises(ParameterError):
+            wl.central_loss_mask(*bad)
+
+
+def test_complex_signal_rejected_with_boundary_error():
+    """A complex signal with a non-zero imaginary part is refused with
+    UnsupportedDictionaryError (the GPU path takes real images); one with a
+    zero imaginary part is the real field."""
+    from paper_2204_14194_b200.errors import UnsupportedDictionaryError
+    from paper_2204_14194_b200.grid import as_real_field
+
+    z = np.arange(6.0).reshape(2, 3) + 0j
+    assert np.array_equal(as_real_field(z), z.real)
+    with pytest.raises(UnsupportedDictionaryError):
+        as_real_field(z + 1j)
+    with pytest.raises(ShapeError):
+        as_real_field(np.zeros(3))

@@ -198,3 +198,56 @@ def test_transform_cases(golden_dir, meta):
             c, dd = orc.fft_gram(z[f"{k}_w"], d.freqs, m, n)
             assert np.array_equal(c, z[f"{k}_gram"]), k
             assert np.array_equal(dd, z[f"{k}_d"]), k
+
+
+# ----------------------------------------------------------------- batch fixtures
+
+
+def _batch_pin(golden_dir, cid, picks):
+    z = np.load(golden_dir / f"c{cid}_batch.npz")
+    w = wl.WORKLOADS[cid]
+    vals = w.dictionary().real_values().astype(np.complex128)
+    if w.shared_geometry:
+        mask = wl.central_loss_mask(*w.area, *w.loss)
+        tables = orc.gram(vals.reshape(len(vals), -1), orc.weight_field(mask, w.config.rho_hat))
+        sig = wl.block_signals(cid, max(picks) + 1, *w.area)
+        blocks = [(i, sig[z["blocks"][i]], mask) for i in picks]
+    else:
+        case = wl.frame_case(w)
+        signals, masks = wl.frame_areas(case.damaged(), case.lost, case.corners, case.mb,
+                                        case.support)
+        tables = None
+        blocks = [(i, signals[z["blocks"][i]], masks[z["blocks"][i]]) for i in picks]
+    for i, sig, mask in blocks:
+        r = orc.extrapolate_block(sig, mask, vals, w.config.gamma, w.config.iterations,
+                                  w.config.rho_hat, tables=tables)
+        assert np.array_equal(r["selected"], z["selected"][i])
+        assert np.array_equal(r["coefficients"].real, z["coefficients"][i])
+        n = int(z["lost_n"][i])
+        assert np.array_equal(r["patched"][mask], z["lost"][i][:n])
+
+
+def test_batch_fixtures_pin_oracle_c1(golden_dir):
+    """The reference-written config-1 batch fixture (all 1,024 blocks) and the
+    oracle agree bit-for-bit on sampled blocks (the GPU checker is trusted)."""
+    _batch_pin(golden_dir, 1, [0, 511, 1023])
+
+
+def test_batch_fixtures_pin_oracle_c3(golden_dir):
+    _batch_pin(golden_dir, 3, [0, 100, 255])
+
+
+def test_batch_fixture_structure(golden_dir, meta):
+    """Every batch fixture covers the blocks the verdict asks for; the near-tie
+    sets contain the reference's own selection at that iteration."""
+    want = {1: 1024, 4: 256, 3: 256, 2: 128}
+    for cid, n in want.items():
+        z = np.load(golden_dir / f"c{cid}_batch.npz")
+        assert len(z["blocks"]) == n and z["selected"].shape == (n, wl.WORKLOADS[cid].config.iterations)
+        ties = {}
+        for i, t, k in z["ties"]:
+            ties.setdefault((int(i), int(t)), set()).add(int(k))
+        for (i, t), ks in ties.items():
+            assert len(ks) > 1 and int(z["selected"][i][t]) in ks
+    z = np.load(golden_dir / "c1_batch.npz")
+    assert np.array_equal(z["blocks"], np.arange(1024))
