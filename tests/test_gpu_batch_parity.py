@@ -32,7 +32,7 @@ import pytest
 
 from paper_2204_14194_b200 import workloads as wl
 
-from .parity import COEF_REL
+from parity import COEF_REL  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
