@@ -3,23 +3,28 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
 
-A *step* is one pass of the hot path over one batch: BASELINE config 1 by
-default -- 1,024 independent 48x48 areas per GPU with a centred 16x16 loss,
-DCT u Hadamard-48 (K = 4608), 200 iterations, FP64. Per step: batched initial
-products (DMMA GEMM), the FaSE recursion, synthesis of the lost samples. The
+A *step* is one pass of the hot path over one batch: BASELINE config 4 by
+default (the largest single-GPU config, the one the "blocks/s at 1/2/4/8 B200"
+metric is quoted on) -- 4,096 independent 64x64 areas with a centred 24x24
+loss, 8,192 unit-norm Gaussian atoms, 500 iterations, rho 0.85, FP64. Per
+step: batched initial products (tcgen05 Ozaki digit planes over the support),
+the FaSE recursion, synthesis of the lost samples, and the result gather. The
 shared Gram table is built once before the clock, exactly as the reference's
 own benchmark does (pkg/src/fase/bench.py:6-9,118-119); its build time is
-reported as ``gram_ms``.
+reported as ``gram_ms``. ``--config 0..3`` selects the other BASELINE configs.
 
 ``value``: device-resident throughput (signals already in HBM), CUDA events
 per step on the launching stream, L2 flushed (256 MiB write) between steps.
-``e2e``: the same batch through ExtrapolationPlan.run_host -- pinned host
-signals -> device, kernels, selections / coefficients / lost samples -> pinned
-host -- all inside the timed region.
+``e2e``: the same batch through ShardedBatch.run_host_stream -- pinned host
+signals -> device, kernels, gather, selections / coefficients / lost samples
+-> pinned host -- all inside the timed region. After the clock the timed
+outputs are classified against the reference-written batch fixture
+(``parity_vs_reference``).
 
-Multi-GPU (torchrun): one process per GPU, each rank extrapolates its own 1,024
-blocks (weak scaling; blocks are independent, so no collective in the data
-path); time = max over ranks.
+Multi-GPU (torchrun): one process per GPU; the ONE batch (or the frame's lossy
+tiles) is sharded by contiguous block ranges (shard.block_range) and the
+per-rank results are gathered to rank 0 with one NCCL gather per step, inside
+the timed region (strong scaling); time = max over ranks.
 
 --impl reference: the reference algorithm's CPU path (the oracle port of the
 pure-Python reference, oracle/fase_oracle.py) on all host cores, one process
@@ -57,7 +62,7 @@ def parse_args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)  # ~0.17 s timed: several clock samples
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=4, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target wall seconds of the bounded CPU-baseline sample")
@@ -115,8 +120,8 @@ def _cpu_worker(args):
         t0 = time.perf_counter()
         for i in range(n):
             b = (first + i) % nb
-            if tables is not None:
-                sig = wl.block_signals(cid, 1, *w.area, first=b)[0]
+            if tables is not None:  # signals generated before the clock
+                sig = _CPU["signals"][b % len(_CPU["signals"])]
                 mask = _CPU["mask"]
             else:
                 sig, mask = _CPU["signals"][b], _CPU["masks"][b]
@@ -134,7 +139,9 @@ def cpu_prepare(cid: int, spec=None):
     if w.shared_geometry:
         mask = wl.central_loss_mask(*w.area, *w.loss)
         tables = orc.gram(vals.reshape(len(vals), -1), orc.weight_field(mask, w.config.rho_hat))
-        _CPU.update(vals=vals, mask=mask, tables=tables, n_blocks=w.n_blocks)
+        # a pool of the workload's own blocks, generated outside the timed loop
+        _CPU.update(vals=vals, mask=mask, tables=tables, n_blocks=w.n_blocks,
+                    signals=wl.block_signals(cid, min(w.n_blocks, 256), *w.area))
     else:
         case = wl.frame_case(w)
         signals, masks = wl.frame_areas(case.damaged(), case.lost, case.corners, case.mb,
@@ -191,7 +198,7 @@ def run_reference(args):
         "impl": "reference", "metric": "extrapolated blocks/s", "value": base["value"],
         "unit": "blocks/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         # one step = one bounded sample of the workload on the host cores
-        "ms_per_step": base["ms_per_sample"], "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": base["ms_per_sample"], "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64" if bench_dictionary(w, args.dict).is_real else "c128",
         "data": "synthetic (seeded, BASELINE Appendix-A generators)",
@@ -211,16 +218,20 @@ def workload_config(w, n_gpus, spec=None):
            "M": w.area[0] * w.area[1], "iterations": w.config.iterations, "gamma": w.config.gamma,
            "rho": w.config.rho_hat, "dictionary": spec or w.dict_spec,
            "l2": "flushed between timed steps (256 MiB write)",
-           "parallelism": f"dp{n_gpus} (block sharding, no collective)"}
+           "parallelism": f"dp{n_gpus}: one batch sharded by block ranges, results gathered "
+                          f"to rank 0 (NCCL gather, inside the timed region)"
+                          if n_gpus > 1 else "dp1"}
     if w.shared_geometry:
-        cfg.update(blocks_per_gpu=w.n_blocks, loss=f"{w.loss[0]}x{w.loss[1]} centred",
+        cfg.update(blocks=w.n_blocks, loss=f"{w.loss[0]}x{w.loss[1]} centred",
                    tables="shared Gram prebuilt before the clock (reference bench.py:118-119)")
     else:
         cfg.update(frame=list(w.frame), macroblock=w.macroblock, support=w.support,
                    loss=f"{w.loss_fraction:.0%} of full macroblocks",
                    tables="frame-independent cell tables prebuilt (G0 + one per area cell); "
                           "per-frame cell lists, normalizers, products, recursion, paste timed",
-                   parallelism=f"dp{n_gpus} (one frame per GPU, no collective)")
+                   parallelism=f"dp{n_gpus}: the frame's lossy tiles sharded by ranges, results "
+                               f"gathered to rank 0 which pastes them (NCCL gather, timed)"
+                               if n_gpus > 1 else "dp1")
     return cfg
 
 
@@ -336,6 +347,20 @@ def ncu_traffic(kernel: str, tag: str):
         return None
 
 
+def ncu_profile(kernel: str, tag: str):
+    """The committed ncu counters of ``kernel`` for workload ``tag`` beyond DRAM
+    bytes (L2 throughput, issue activity, instructions per warp-iteration)."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        rec = json.loads(p.read_text()).get(f"{tag}/{kernel}", {})
+    except ValueError:
+        return None
+    keep = {k: v for k, v in rec.items() if k != "dram_bytes_per_launch"}
+    return keep or None
+
+
 def l2_roofline(achieved_gbs):
     """The recursion's row stream against the measured L2 read bandwidth: with
     most rows L2 hits (ncu), L2 -> SM bandwidth, not HBM, bounds the kernel."""
@@ -369,11 +394,54 @@ def ozaki_roofline(plan, flops_fp64, seconds, fp64_peak, fp64_src):
                     "of the batch"}
 
 
+def parity_vs_reference(cid, sel, coef, lost, n_lost):
+    """Classify the timed outputs against the reference-written batch fixture
+    (tests/golden/c{cid}_batch.npz, make_batch_golden.py) after the clock:
+    identical sequences, legitimate near-tie stops (the GPU's atom is one the
+    reference's tie rule could pick under a 1e-9 relative Delta-E change),
+    failures; coefficient / lost-sample deviation on the run scale."""
+    p = ROOT / "tests" / "golden" / f"c{cid}_batch.npz"
+    if not p.exists():
+        return None
+    z = np.load(p)
+    blocks = z["blocks"]
+    ties = {}
+    for i, t, k in z["ties"]:
+        ties.setdefault((int(i), int(t)), set()).add(int(k))
+    out = {"fixture": p.name, "blocks_checked": int(len(blocks)), "identical": 0, "near_tie": 0,
+           "failure": 0}
+    worst_c = worst_l = 0.0
+    for i, b in enumerate(blocks):
+        g = sel[int(b)].astype(np.int64)
+        want = z["selected"][i].astype(np.int64)
+        diff = np.flatnonzero(g != want)
+        stop = int(diff[0]) if diff.size else len(g)
+        if diff.size == 0:
+            out["identical"] += 1
+        elif int(g[stop]) in ties.get((i, stop), ()):
+            out["near_tie"] += 1
+        else:
+            out["failure"] += 1
+            continue
+        sc = max(float(np.abs(z["coefficients"][i]).max()), 1e-300)
+        worst_c = max(worst_c, float(np.abs(coef[int(b)][:stop] - z["coefficients"][i][:stop])
+                                     .max(initial=0.0)) / sc)
+        if diff.size == 0 and lost is not None:
+            n = int(z["lost_n"][i])
+            want_l = z["lost"][i][:n]
+            worst_l = max(worst_l, float(np.abs(lost[int(b)][:n] - want_l).max(initial=0.0))
+                          / max(float(np.abs(want_l).max()), 1e-300))
+    out.update(max_coef_rel_dev=worst_c, max_lost_rel_dev=worst_l,
+               rule="selection bit-exact except legitimate near-ties (1e-9 rel. Delta-E); "
+                    "coefficients / samples within 1e-6 of the run scale")
+    return out
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2204_14194_b200 import ExtrapolationPlan, _native, build_gram_tables, build_weight_field
+    from paper_2204_14194_b200 import ShardedBatch, _native, build_gram_tables, build_weight_field
     from paper_2204_14194_b200.fast import gram_into, gram_support
 
     rank, world, local = dist_env()
@@ -390,17 +458,25 @@ def run_gpu(args):
     w = wl.WORKLOADS[args.config]
     d = bench_dictionary(w, args.dict)
     cplx = not d.is_real
-    K, M, I, B = len(d), w.area[0] * w.area[1], w.config.iterations, w.n_blocks
+    K, M, I, B_total = len(d), w.area[0] * w.area[1], w.config.iterations, w.n_blocks
     mask = wl.central_loss_mask(*w.area, *w.loss)
     d.device_matrix(dev)
+    # every rank builds the shared table itself: recomputing it (c4: 3.9 ms on
+    # the tensor cores) is cheaper than moving 537 MB, and it is outside the
+    # timed region (reference bench.py:118-119)
     tables = build_gram_tables(d, build_weight_field(mask, w.config.rho_hat), device=dev)
     # auto: scaled for real dictionaries; for complex ones where the exact kernel
     # needs 512-thread / paired shapes (K > 2560: union:dft+bdft 2.31 -> 1.84 ms;
     # at K = 2304 the two are within 3%)
     recursion = args.recursion if args.recursion != "auto" else (
         "scaled" if not cplx or K > 2560 else "exact")
-    plan = ExtrapolationPlan(d, mask, B, w.config, tables, device=dev, products=args.products,
-                             recursion=recursion)
+    if cplx and world > 1:
+        raise SystemExit("complex dictionaries: single GPU only in the bench")
+    # ONE batch of B_total blocks, rank r taking block_range(B_total, r, N)
+    sb = ShardedBatch(d, mask, B_total, w.config, tables, dev, products=args.products,
+                      recursion=recursion)
+    plan = sb.plan
+    B, lo = sb.hi - sb.lo, sb.lo
     if recursion == "scaled":
         scaled_fn = _native.iterate_complex_scaled if cplx else _native.iterate_scaled
 
@@ -439,7 +515,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     gram_ms = g0.elapsed_time(g1)
     assert torch.equal(G2, plan.G) and torch.equal(D2, plan.D), "Gram build is not deterministic"
-    del G2, D2
+    del G2, D2, gws
     fft_gram_ms = None
     if cplx and len(d.tagged_indices()) == K:  # transform-shortcut table (fft_gram_table)
         from paper_2204_14194_b200 import fft_gram_table
@@ -452,59 +528,59 @@ def run_gpu(args):
         torch.cuda.synchronize()
         fft_gram_ms = g0.elapsed_time(g1)
 
-    host = torch.from_numpy(wl.block_signals(args.config, B, *w.area, first=rank * B)).pin_memory()
+    # this rank's shard of batch 0 (timed device-resident and e2e) and of a
+    # second batch (blocks B_total + ...) the e2e stream alternates with
+    host = torch.from_numpy(wl.block_signals(args.config, B, *w.area, first=lo)).pin_memory()
     host2 = torch.from_numpy(wl.block_signals(args.config, B, *w.area,
-                                              first=(world + rank) * B)).pin_memory()
+                                              first=B_total + lo)).pin_memory()
     dev_sig = host.to(dev)
     sig_view = dev_sig.reshape(B, -1)
     if plan.F.shape[1] != M:  # odd areas: the kernels read the padded layout
         plan.F[:, :M].copy_(sig_view)
         sig_view = plan.F
-    outs = plan.host_buffers()
-    outs2 = plan.host_buffers()
+    harena = [sb.host_arena(), sb.host_arena()] if sb.is_root else [None, None]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     for _ in range(max(args.warmup, 0)):
-        plan.run(dev_sig)
-    plan.run_host_stream([host, host2] * max(args.warmup, 1), [outs, outs2] * max(args.warmup, 1))
+        sb.run(dev_sig)
+    sb.run_host_stream([host, host2] * max(args.warmup, 1), harena * max(args.warmup, 1))
     torch.cuda.synchronize()
 
     def timed_e2e():
-        """All K steps through run_host_stream (copies overlapped with compute);
-        one event pair around the whole sequence."""
+        """All K steps through ShardedBatch.run_host_stream (copies overlapped
+        with compute): shard H2D, extrapolate, gather to the root, root D2H of
+        the gathered results; one event pair around the whole sequence."""
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         ins = [host if i % 2 == 0 else host2 for i in range(args.steps)]
-        out = [outs if i % 2 == 0 else outs2 for i in range(args.steps)]
+        out = [harena[i % 2] for i in range(args.steps)]
         e0.record(stream)
-        plan.run_host_stream(ins, out)
+        sb.run_host_stream(ins, out)
         e1.record(stream)
         return [[e0, e1]]
 
-    def timed(fn, split=False):
+    def timed():
         evs = []
         for _ in range(args.steps):
             _native.l2_flush(flush)
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(4 if split else 2)]
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
             e[0].record(stream)
-            if split:
-                plan._products(sig_view)  # signals resident in HBM, read in place
-                e[1].record(stream)
-                if plan.fused_synth:  # recursion with the synthesis inside
-                    plan._iterate_synth(plan.selected, plan.projections, plan.coefficients,
-                                        plan.lost)
-                    e[2].record(stream)
-                else:
-                    iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, plan.selected,
-                            plan.projections, plan.coefficients)
-                    e[2].record(stream)
-                    synth(plan.phi_lost, plan.selected, plan.coefficients, I, plan.lost_seq,
-                          plan.lost, n_shared=plan.n_lost, dst=plan.lost_pos, **synth_extra)
-                e[3].record(stream)
+            plan._products(sig_view)  # signals resident in HBM, read in place
+            e[1].record(stream)
+            if plan.fused_synth:  # recursion with the synthesis inside
+                plan._iterate_synth(plan.selected, plan.projections, plan.coefficients,
+                                    plan.lost)
+                e[2].record(stream)
             else:
-                fn()
-                e[1].record(stream)
+                iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, plan.selected,
+                        plan.projections, plan.coefficients)
+                e[2].record(stream)
+                synth(plan.phi_lost, plan.selected, plan.coefficients, I, plan.lost_seq,
+                      plan.lost, n_shared=plan.n_lost, dst=plan.lost_pos, **synth_extra)
+            e[3].record(stream)
+            sb.arena.gather(0)  # results of every rank to the root (NCCL; no-op at N=1)
+            e[4].record(stream)
             evs.append(e)
         return evs
 
@@ -519,30 +595,41 @@ def run_gpu(args):
     torch.cuda.synchronize()
     with ClockSampler(gpu_id) as clocks:
         t_wall0 = time.perf_counter()
-        ev_dev = timed(None, split=True)
+        ev_dev = timed()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         ev_e2e = timed_e2e()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
-    dev_ms = [e[0].elapsed_time(e[3]) for e in ev_dev]
+    dev_ms = [e[0].elapsed_time(e[4]) for e in ev_dev]
     init_ms = [e[0].elapsed_time(e[1]) for e in ev_dev]
     iter_ms = [e[1].elapsed_time(e[2]) for e in ev_dev]
     synth_ms = [e[2].elapsed_time(e[3]) for e in ev_dev]
+    gather_ms = [e[3].elapsed_time(e[4]) for e in ev_dev]
     e2e_ms = [e[0].elapsed_time(e[1]) for e in ev_e2e]
     tot = torch.tensor([sum(dev_ms), sum(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     dev_total_s, e2e_total_s = tot[0].item() / 1e3, tot[1].item() / 1e3
 
-    # correctness guard on the timed outputs (cheap; not timed)
+    # correctness guard on the timed outputs (not timed): range / finiteness on
+    # every rank; on the root, the gathered batch against the reference fixture
     sel = plan.selected
     assert int(sel.min()) >= 0 and int(sel.max()) < K, "selection out of range"
     assert torch.isfinite(plan.lost).all(), "non-finite reconstruction"
+    parity = None
+    if sb.is_root and not args.dict:
+        g_sel, g_coef, g_lost = (x.cpu().numpy() for x in sb.arena.assemble(0))
+        parity = parity_vs_reference(args.config, g_sel, g_coef, g_lost, plan.n_lost)
+        if parity is not None and parity["failure"]:
+            raise RuntimeError(f"timed outputs diverge from the reference: {parity}")
     agreement = None
     if recursion == "scaled":
-        # the same batch through the exact (reference-bit-identical) recursion
+        # the same shard through the exact (reference-bit-identical) recursion
         sel_x, proj_x, coef_x = (torch.empty_like(x) for x in (plan.selected, plan.projections,
                                                                plan.coefficients))
         (_native.iterate_complex if cplx else _native.iterate)(
@@ -553,6 +640,9 @@ def run_gpu(args):
         agreement = {"blocks_identical_selections": int(same.sum()), "blocks": B,
                      "max_coef_rel_dev": float(dev_c[same].max()) if bool(same.any()) else None,
                      "vs": "fase_iterate (exact) on the same R0 / table"}
+    dropin = None
+    if rank == 0 and world == 1 and not cplx:
+        dropin = time_dropin(w, d, mask, tables, dev)
 
     if rank == 0:
         hbm, hsrc, fp64, fsrc = measured_peaks()
@@ -578,41 +668,34 @@ def run_gpu(args):
             flops_sep += 4.0 * (K - covered) * M * B
             factors = cparts
         step_ms = dev_total_s / args.steps * 1e3
+        tag = ("dft" if args.dict == "dft" else f"c{args.config}") + (
+            "-scaled" if recursion == "scaled" else "")
+        kname = "fase_iterate_complex_kernel" if cplx else "fase_iterate_kernel"
         line = {
             "metric": "extrapolated blocks/s",
-            "value": world * B * args.steps / dev_total_s,
+            "value": B_total * args.steps / dev_total_s,
             "unit": "blocks/s",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": step_ms,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": "c128" if cplx else "f64",
             "data": "synthetic (seeded BASELINE Appendix-A generators; random atoms: none)",
             "config": workload_config(w, world, args.dict),
-            "e2e": {"value": world * B * args.steps / e2e_total_s, "unit": "blocks/s",
-                    "h2d_bytes_per_step": plan.bytes_h2d(), "d2h_bytes_per_step": plan.bytes_d2h(),
+            "e2e": {"value": B_total * args.steps / e2e_total_s, "unit": "blocks/s",
+                    "h2d_bytes_per_step": int(host.numel() * 8) * world,
+                    "d2h_bytes_per_step": sb.arena.nbytes * world,
                     "ms_per_step": e2e_total_s / args.steps * 1e3,
-                    "api": "ExtrapolationPlan.run_host_stream: pinned host in/out every step, "
-                           "H2D / D2H on side streams overlapped with compute; no L2 flush "
-                           "(per-step input comes over PCIe; table 170 MB > L2)"},
-            "roofline": {"bound": "hbm",
-                         "kernel": ("fase_iterate_complex_kernel" if cplx else "fase_iterate_kernel")
-                                   + (" (scaled: column-scaled table)" if recursion == "scaled"
-                                      else ""),
-                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm,
-                         "traffic": ncu_traffic("fase_iterate_complex_kernel" if cplx
-                                                else "fase_iterate_kernel",
-                                                ("dft" if args.dict == "dft" else f"c{args.config}")
-                                                + ("-scaled" if recursion == "scaled" else "")),
-                         "algorithmic_bytes_per_launch": bytes_iter,
-                         "ms_per_launch": it_s * 1e3, "peak_source": hsrc,
-                         "note": ("16*K bytes per block-iteration (one complex128 table row)"
-                                  if cplx else "8*K bytes per block-iteration (one FP64 table row)")
-                                 + "; hot rows hit L2, so frac can exceed DRAM-bound expectations"},
+                    "api": "ShardedBatch.run_host_stream (ExtrapolationPlan per rank): pinned host "
+                           "shard in, extrapolation, result gather to rank 0, rank-0 D2H of the "
+                           "gathered selections / coefficients / lost samples, every step; copies "
+                           "on side streams overlapped with compute; no L2 flush (per-step input "
+                           "comes over PCIe)"},
+            "roofline": roofline_recursion(achieved, hbm, hsrc, kname, tag, recursion, bytes_iter,
+                                           it_s, cplx, B, I),
             "roofline_l2": l2_roofline(achieved),
             "roofline_init": (ozaki_roofline(plan, flops_init, init_s, fp64, fsrc)
                               if plan._ozaki is not None else
@@ -636,15 +719,22 @@ def run_gpu(args):
             "products": plan.products_method,
             "recursion": recursion,
             "fused_synth": plan.fused_synth,
+            "parity_vs_reference": parity,
             "recursion_agreement": agreement,
             "stage_ms": {"init_products": float(np.mean(init_ms)), "iterate": float(np.mean(iter_ms)),
-                         "synth": float(np.mean(synth_ms))},
+                         "synth": float(np.mean(synth_ms)), "gather": float(np.mean(gather_ms))},
+            "shard": {"blocks_total": B_total, "blocks_rank0": B, "ranks": world,
+                      "gather_bytes_per_rank": sb.arena.nbytes,
+                      "collective": "torch.distributed.gather (NCCL) of one result arena per "
+                                    "rank, inside the timed region" if world > 1 else
+                                    "none (one rank)"},
             "gram_ms": gram_ms,
             "gram_path": gram_path,
             "fft_gram_ms": fft_gram_ms,
             "gram_tflops": (4 if cplx else 1) * K * (K + 1) * M / (gram_ms * 1e-3) / 1e12,
             "gram_fp64_frac": (4 if cplx else 1) * K * (K + 1) * M / (gram_ms * 1e-3) / 1e12 / fp64,
             "gpu_launches": args.steps * (plan.launches_per_run + 1) + args.steps * plan.launches_per_run,
+            "e2e_dropin": dropin,
             "clocks": clocks.summary(),
             "wall_s": t_wall,
             "cpu_baseline": cpu,
@@ -655,12 +745,63 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
+def time_dropin(w, d, mask, tables, dev):
+    """One batch through the drop-in ``fase_extrapolate_batch`` (host numpy in,
+    host results out, per-call validation / provenance check / uploads /
+    allocations): the host overhead of the reference-facing call next to the
+    prepared-plan figure. Warm once, then time one call (wall clock around a
+    synchronizing call)."""
+    import torch
+
+    from paper_2204_14194_b200 import fase_extrapolate_batch
+
+    sig = wl.block_signals(w.cid, w.n_blocks, *w.area)
+    fase_extrapolate_batch(sig, mask, d, tables, w.config, device=dev, recursion="scaled")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = fase_extrapolate_batch(sig, mask, d, tables, w.config, device=dev, recursion="scaled")
+    sel = res.selected.cpu().numpy()
+    coef = res.coefficients.cpu().numpy()
+    patched = res.patched.cpu().numpy()
+    t = time.perf_counter() - t0
+    return {"value": w.n_blocks / t, "unit": "blocks/s", "ms_per_call": t * 1e3,
+            "api": "fase_extrapolate_batch(host signals, mask, dictionary, tables, config): "
+                   "host in, device results read back (selected, coefficients, patched areas)",
+            "h2d_bytes": int(sig.nbytes), "d2h_bytes": int(sel.nbytes + coef.nbytes + patched.nbytes)}
+
+
+def roofline_recursion(achieved, hbm, hsrc, kname, tag, recursion, bytes_iter, it_s, cplx, B, I):
+    """The recursion against HBM: ``achieved`` counts the algorithmic bytes (one
+    table row per block-iteration); most rows are L2 hits, so the
+    DRAM bytes ncu measured for the same kernel (``traffic``) are reported with
+    their own rate and fraction (``dram_*``) -- the honest HBM figure."""
+    traffic = ncu_traffic(kname, tag)
+    prof = ncu_profile(kname, tag)
+    out = {"bound": "hbm", "kernel": kname + (" (scaled: column-scaled table)"
+                                              if recursion == "scaled" else ""),
+           "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+           "traffic": traffic, "algorithmic_bytes_per_launch": bytes_iter,
+           "ms_per_launch": it_s * 1e3, "peak_source": hsrc,
+           "note": ("16*K" if cplx else "8*K") + " bytes per block-iteration (one table row); "
+                   "rows mostly hit L2, so achieved/frac exceed what DRAM serves: dram_gbs / "
+                   "dram_frac are the ncu DRAM bytes of the same kernel over the live time"}
+    if traffic:
+        out["dram_gbs"] = traffic / it_s / 1e9
+        out["dram_frac"] = traffic / it_s / 1e9 / hbm
+    if prof:
+        out["ncu"] = prof
+    return out
+
+
 def run_gpu_frame(args):
-    """Configs 2/3: one step = conceal one damaged frame (all lossy macroblocks)."""
+    """Configs 2/3: one step = conceal one damaged frame (all lossy macroblocks),
+    the lossy tiles sharded over the ranks (ShardedFrame: every rank conceals
+    block_range(L, r, N) of the tiles, results gathered to rank 0, which pastes
+    the other ranks' tiles)."""
     import torch
     import torch.distributed as dist
 
-    from paper_2204_14194_b200 import _native
+    from paper_2204_14194_b200 import ShardedFrame, _native
     from paper_2204_14194_b200.conceal import FrameEngine, lossy_tiles, tile_grid
 
     rank, world, local = dist_env()
@@ -680,36 +821,28 @@ def run_gpu_frame(args):
                          **({"compose": args.compose} if args.compose else {}))
     grid_h = tile_grid(case.lost, case.mb)
     corners_h = lossy_tiles(case.lost, (case.mb, case.mb)).astype(np.int32)
-    L = len(corners_h)
+    L_total = len(corners_h)
     frame_u8 = torch.from_numpy(case.frame).pin_memory()
     lost_h = torch.from_numpy(case.lost)
     grid = torch.from_numpy(grid_h).to(dev)
     corners = torch.from_numpy(corners_h).to(dev)
+    sf = ShardedFrame(engine, grid, corners)
+    L = sf.hi - sf.lo
     damaged = torch.from_numpy(case.damaged()).to(dev)
     out = damaged.clone()
     out_host = torch.empty(out.shape, dtype=torch.float64, pin_memory=True)
+    out_host2 = torch.empty(out.shape, dtype=torch.float64, pin_memory=True)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     lost_dev = lost_h.to(dev)
     for _ in range(max(args.warmup, 1)):
-        engine.run(damaged, grid, corners, out=out)
+        sf.run(damaged, out=out)
     torch.cuda.synchronize()
     if engine.dead_blocks():
         raise RuntimeError("a block had every atom degenerate")
-
-    def e2e_step(frame_dev):
-        # H2D of the uint8 frame, widening + loss zeroing, concealment, D2H
-        frame_dev.copy_(frame_u8, non_blocking=True)
-        f64 = frame_dev.to(torch.float64).masked_fill_(lost_dev, 0.0)
-        engine.run(f64, grid, corners, out=f64)
-        out_host.copy_(f64, non_blocking=True)
-
-    frame_dev = torch.empty(case.frame.shape, dtype=torch.uint8, device=dev)
-    e2e_step(frame_dev)
-    out_host2 = torch.empty(out.shape, dtype=torch.float64, pin_memory=True)
-    engine.run_host_stream([frame_u8] * 2, [out_host, out_host2], grid, corners, lost_dev)
+    sf.run_host_stream([frame_u8] * 2, [out_host, out_host2], lost_dev)
     torch.cuda.synchronize()
-    if not torch.equal(out_host, out_host2) or not torch.equal(out_host, out.cpu()):
+    if sf.is_root and (not torch.equal(out_host, out_host2) or not torch.equal(out_host, out.cpu())):
         raise RuntimeError("pipelined frames differ from the single-frame run")
     if world > 1:
         dist.barrier()
@@ -727,17 +860,19 @@ def run_gpu_frame(args):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            engine.run(damaged, grid, corners, out=out)
+            sf.run(damaged, out=out)  # this rank's tiles + gather (+ root paste)
             e1.record(stream)
             dev_ms.append((e0, e1))
-        # end to end: K frames through FrameEngine.run_host_stream (uploads,
-        # kernels and read-backs of neighbouring frames overlapped); one event
-        # pair around the whole sequence
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        # end to end: K frames through ShardedFrame.run_host_stream (uploads,
+        # kernels, gather and root read-backs of neighbouring frames
+        # overlapped); one event pair around the whole sequence
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        engine.run_host_stream([frame_u8] * args.steps, [out_host, out_host2] * args.steps,
-                               grid, corners, lost_dev)
+        sf.run_host_stream([frame_u8] * args.steps, [out_host, out_host2] * args.steps, lost_dev)
         e1.record(stream)
         e2e_ms.append((e0, e1))
         torch.cuda.synchronize()
@@ -751,12 +886,15 @@ def run_gpu_frame(args):
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     dev_t, e2e_t = tot.tolist()
-    # kernel split of one frame, for the roofline
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    parity = None
+    if sf.is_root:
+        g_sel, g_coef, _ = (x.cpu().numpy() for x in sf.arena.assemble(0))
+        parity = parity_vs_reference(args.config, g_sel, g_coef, None, 0)
+        if parity is not None and parity["failure"]:
+            raise RuntimeError(f"timed outputs diverge from the reference: {parity}")
+    # kernel split of this rank's tiles, for the roofline
     b = engine._buffers(L)
-    ev[0].record(stream)
-    engine.run(damaged, grid, corners, out=out)
-    ev[2].record(stream)
+    engine.run(damaged, grid, sf.local_corners, out=out)
     torch.cuda.synchronize()
     counts = b["counts"].float()
     # rows streamed per block-iteration: the base row plus the chunks left after
@@ -781,34 +919,42 @@ def run_gpu_frame(args):
         bytes_iter = 8.0 * K * L * I
         achieved = bytes_iter / it_s / 1e9
         streamed = bytes_iter * mean_rows
+        traffic = ncu_traffic("fase_iterate_kernel", f"c{args.config}")
         line = {
-            "metric": "extrapolated blocks/s", "value": world * L * args.steps / dev_t,
+            "metric": "extrapolated blocks/s", "value": L_total * args.steps / dev_t,
             "unit": "blocks/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dev_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": dev_t / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic frame (seeded BASELINE Appendix-A generator)",
-            "config": dict(workload_config(w, world), blocks_per_frame=L,
+            "config": dict(workload_config(w, world), blocks_per_frame=L_total,
                            cells=len(engine.cells), mean_rows_per_iteration=mean_rows,
                            composed_bases=engine.compose_mode),
-            "e2e": {"value": world * L * args.steps / e2e_t, "unit": "blocks/s",
-                    "h2d_bytes_per_step": int(case.frame.nbytes),
+            "e2e": {"value": L_total * args.steps / e2e_t, "unit": "blocks/s",
+                    "h2d_bytes_per_step": int(case.frame.nbytes) * world,
                     "d2h_bytes_per_step": int(out_host.numel() * 8),
                     "ms_per_step": e2e_t / args.steps * 1e3,
-                    "api": "FrameEngine.run_host_stream: pinned uint8 frame in, restored float64 "
-                           "frame (pinned) out every step; neighbouring frames' copies and kernels "
-                           "overlapped on separate streams; no L2 flush (tables >> L2)"},
+                    "api": "ShardedFrame.run_host_stream (FrameEngine per rank): pinned uint8 frame "
+                           "in on every rank, its tiles concealed, results gathered to rank 0 "
+                           "(pastes the rest), restored float64 frame (pinned) out every step; "
+                           "neighbouring frames' copies and kernels overlapped; no L2 flush"},
             "roofline": {"bound": "hbm", "kernel": "fase_iterate_kernel (chunked rows)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": ncu_traffic("fase_iterate_kernel", f"c{args.config}"),
+                         "traffic": traffic,
+                         "dram_gbs": traffic / it_s / 1e9 if traffic else None,
+                         "dram_frac": traffic / it_s / 1e9 / hbm if traffic else None,
                          "algorithmic_bytes_per_launch": bytes_iter,
                          "ms_per_launch": it_s * 1e3, "peak_source": hsrc,
                          "streamed_bytes_per_launch": streamed,
                          "streamed_gbs": streamed / it_s / 1e9,
+                         "ncu": ncu_profile("fase_iterate_kernel", f"c{args.config}"),
                          "note": "achieved counts 8*K bytes (one table row) per block-iteration, "
                                  "the SURVEY 8(d) unit; the per-block table G0 - sum C_cell "
                                  "streams one base row (G0 or a precomposed G0 - C_c1 (- C_c2)) "
                                  "plus the remaining unavailable cells' rows for it "
                                  "(streamed_*), served largely from L2"},
+            "parity_vs_reference": parity,
+            "shard": {"blocks_total": L_total, "blocks_rank0": L, "ranks": world,
+                      "gather_bytes_per_rank": sf.arena.nbytes},
             "table_build_s": engine.table_seconds,
             "gpu_launches": args.steps * (engine.launches_per_frame + 1) + args.steps * engine.launches_per_frame,
             "clocks": clocks.summary(), "wall_s": t_wall, "cpu_baseline": cpu,

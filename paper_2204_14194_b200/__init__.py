@@ -57,6 +57,7 @@ from .conceal import DEFAULT_SUPPORT, conceal_frame, conceal_image
 from .model import BatchResult, IterationTrace, SparseModel
 from .pgm import read_mask_pgm, read_pgm, write_pgm
 from .transform import FFT_MIN_TAGGED, fft_gram_table, fft_initial_products
+from .shard import ResultArena, ShardedBatch, ShardedFrame, block_range
 from .workloads import central_loss_mask
 
 __version__ = "0.1.0"
@@ -72,4 +73,5 @@ __all__ = [
     "fase_extrapolate_batch", "gaussian_dictionary", "generate_dictionary", "hadamard_matrix",
     "initial_scalar_products", "load_dictionary", "load_gram_table", "save_gram_table", "parse_dict_spec", "provenance_hash",
     "psnr_over_region", "save_dictionary", "union_dictionaries", "__version__",
+    "ResultArena", "ShardedBatch", "ShardedFrame", "block_range",
 ]

@@ -236,18 +236,30 @@ class FrameEngine:
             return 5 + (1 if len(factors) <= 8 else len(factors))
         return 5 + (2 if any("oz" in b for b in self._buf.values()) else 1)
 
-    def run(self, frame, grid, corners, out=None, slot: int = 0) -> BatchResult:
+    def run(self, frame, grid, corners, out=None, slot: int = 0, outputs=None) -> BatchResult:
         """Conceal one frame: ``frame`` (H, W) float64, ``grid`` (H/tile, W/tile)
         uint8 tile loss map, ``corners`` (L, 2) int32 lossy-tile corners, all on
         the device. The restored frame is written to ``out`` (default: a copy of
         ``frame``). Enqueued on the current stream; no host synchronization.
-        ``slot`` picks one of two work-buffer sets (two frames in flight)."""
+        ``slot`` picks one of two work-buffer sets (two frames in flight).
+        ``outputs``: optional caller-owned (selected (L, I) int32, coefficients
+        (L, I) float64) device buffers to write instead of the engine's (views
+        of a result arena a collective gathers, ``shard.ShardedFrame``)."""
         L = int(corners.shape[0])
         if out is None:
             out = frame.clone()
         if L == 0:
             return BatchResult(selected=None, projections=None, coefficients=None, patched=out)
         b = self._buffers(L, slot)
+        if outputs is not None:
+            import torch
+
+            sel, coef = outputs
+            I = self.config.iterations
+            if (tuple(sel.shape) != (L, I) or sel.dtype != torch.int32 or tuple(coef.shape) != (L, I)
+                    or coef.dtype != torch.float64 or not (sel.is_contiguous() and coef.is_contiguous())):
+                raise ShapeError("outputs must be contiguous (L, I) int32 / float64 buffers")
+            b = dict(b, sel=sel, coef=coef)
         cfg, K = self.config, self.K
         _native.frame_areas(frame, grid, self.tile, self.support, corners, self.base_w, b["X"])
         _native.frame_cells(grid, self.H, self.W, self.tile, self.support, corners, self.cell_rep,
@@ -274,13 +286,18 @@ class FrameEngine:
                            patched=out, dictionary=self.dictionary,
                            shape=(self.A, self.A))
 
-    def run_host_stream(self, frames_u8, outs, grid, corners, lost):
+    def run_host_stream(self, frames_u8, outs, grid, corners, lost, *, slot_outputs=None,
+                        finish=None):
         """End to end over a sequence of frames with one loss pattern: pinned
         uint8 frames in, restored float64 frames (pinned) out. Frames alternate
         between two compute streams with their own buffers; uploads and
         read-backs run on their own streams, overlapped with the neighbouring
         frames' kernels. ``grid`` / ``corners`` / ``lost`` (H x W bool) live on
-        the device. Enqueued; the caller's stream waits for the last read-back."""
+        the device. Enqueued; the caller's stream waits for the last read-back.
+        ``slot_outputs`` optionally gives per-slot (selected, coefficients)
+        buffers for ``run``; ``finish(slot, frame, hout)``, called on the
+        slot's compute stream after ``run``, returns the (host, device) copies
+        to make instead of the default frame read-back (``shard.ShardedFrame``)."""
         import torch
 
         dev = self.device
@@ -317,12 +334,15 @@ class FrameEngine:
                 f64.masked_fill_(lost, 0.0)
                 ev_used[s] = torch.cuda.Event()
                 ev_used[s].record(c)
-                self.run(f64, grid, corners, out=f64, slot=s)
+                self.run(f64, grid, corners, out=f64, slot=s,
+                         outputs=None if slot_outputs is None else slot_outputs[s])
+                copies = [(hout, f64)] if finish is None else finish(s, f64, hout)
                 done = torch.cuda.Event()
                 done.record(c)
             with torch.cuda.stream(p["d2h"]):
                 p["d2h"].wait_event(done)
-                hout.copy_(p["f64"][s], non_blocking=True)
+                for dst, src in copies:
+                    dst.copy_(src, non_blocking=True)
                 ev_out[s] = torch.cuda.Event()
                 ev_out[s].record(p["d2h"])
         for e in ev_out:

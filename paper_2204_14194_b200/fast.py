@@ -711,6 +711,17 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
                        max_imag=max_imag)
 
 
+def _bound_output(outputs: dict, key: str, shape, dtype, dev):
+    """A caller-owned output buffer, checked against what the kernels write."""
+    t = outputs[key]
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype or t.device != dev:
+        raise ShapeError(f"output {key}: {tuple(t.shape)} {t.dtype} on {t.device}, expected "
+                         f"{tuple(shape)} {dtype} on {dev}")
+    if not t.is_contiguous():
+        raise ShapeError(f"output {key} must be contiguous")
+    return t
+
+
 class ExtrapolationPlan:
     """A prepared shared-geometry batch: validate, hash and build tables once,
     then ``run`` only enqueues the three kernels (initial products, recursion,
@@ -725,7 +736,12 @@ class ExtrapolationPlan:
 
     def __init__(self, dictionary: Dictionary, mask, n_blocks: int,
                  config: ExtrapConfig = ExtrapConfig(), tables: GramTable | None = None,
-                 device=None, products: str = "auto", recursion: str = "exact"):
+                 device=None, products: str = "auto", recursion: str = "exact",
+                 outputs: dict | None = None):
+        """``outputs``: optional caller-owned device buffers ``selected`` (B, I)
+        int32, ``coefficients`` (B, I) and ``lost`` (B, max(L, 1)) float64 the
+        kernels write instead of plan-owned ones (e.g. views of one contiguous
+        result arena that a collective gathers, ``shard.ShardedBatch``)."""
         torch = _torch()
         self.device = dev = resolve_device(device)
         self.complex = cplx = not dictionary.is_real
@@ -766,12 +782,18 @@ class ExtrapolationPlan:
         self.selected = torch.empty((self.B, I), dtype=torch.int32, device=dev)
         self.projections = torch.empty((self.B, I), dtype=vdt, device=dev)
         self.coefficients = torch.empty((self.B, I), dtype=vdt, device=dev)
+        if outputs is not None:
+            self.selected = _bound_output(outputs, "selected", (self.B, I), torch.int32, dev)
+            self.coefficients = _bound_output(outputs, "coefficients", (self.B, I), vdt, dev)
         self.max_imag = torch.zeros(self.B, dtype=torch.float64, device=dev) if cplx else None
         lost = np.flatnonzero(mask.ravel()).astype(np.int32)
         self.n_lost = int(lost.size)
         self.lost_idx = torch.from_numpy(lost if lost.size else np.zeros(1, np.int32)).to(dev)
         self.lost_pos = torch.arange(max(self.n_lost, 1), dtype=torch.int64, device=dev)
         self.lost = torch.zeros((self.B, max(self.n_lost, 1)), dtype=torch.float64, device=dev)
+        if outputs is not None:
+            self.lost = _bound_output(outputs, "lost", (self.B, max(self.n_lost, 1)),
+                                      torch.float64, dev)
         # Phi restricted to the lost samples (synthesis reads only these; the
         # compact copy stays L2-resident where the full matrix would not)
         nl = max(self.n_lost, 1)
@@ -932,7 +954,7 @@ class ExtrapolationPlan:
         out["lost"].copy_(self.lost, non_blocking=True)
         return out
 
-    def run_host_stream(self, host_inputs, host_outputs):
+    def run_host_stream(self, host_inputs, host_outputs, *, slot_outputs=None, finish=None):
         """End-to-end over a sequence of batches with copies and batches overlapped.
 
         ``host_inputs[i]`` (pinned (B, M, N) float64) goes in and
@@ -942,6 +964,13 @@ class ExtrapolationPlan:
         recursion CTAs fill the SMs that batch i's last wave leaves idle;
         copies run on their own streams; events order every buffer reuse.
         Everything is enqueued; the caller's stream waits for the last results.
+
+        ``slot_outputs`` optionally gives the second slot's device outputs
+        (selected, projections, coefficients, lost); ``finish(slot, hout)``,
+        called on the slot's compute stream after its kernels, replaces the
+        default read-back: it returns the (host destination, device source)
+        pairs to copy (``shard.ShardedBatch`` gathers the ranks' results there
+        and reads back the gathered arena on the root rank only).
         """
         torch = _torch()
         dev = self.device
@@ -953,6 +982,7 @@ class ExtrapolationPlan:
                 "comp": [torch.cuda.Stream(dev), torch.cuda.Stream(dev)],
                 "F": [self.F, torch.zeros_like(self.F)],
                 "out": [(self.selected, self.projections, self.coefficients, self.lost),
+                        tuple(slot_outputs) if slot_outputs is not None else
                         tuple(torch.empty_like(x) for x in (self.selected, self.projections,
                                                             self.coefficients, self.lost))],
             }
@@ -983,13 +1013,17 @@ class ExtrapolationPlan:
                 ev_used[s] = torch.cuda.Event()
                 ev_used[s].record(c)
                 self._iterate_synth(sel, proj, coef, lost, s)
+                if finish is not None:
+                    copies = finish(s, hout)
+                else:
+                    copies = [(hout["selected"], sel), (hout["coefficients"], coef),
+                              (hout["lost"], lost)]
                 done = torch.cuda.Event()
                 done.record(c)
             with torch.cuda.stream(d2h):
                 d2h.wait_event(done)
-                hout["selected"].copy_(sel, non_blocking=True)
-                hout["coefficients"].copy_(coef, non_blocking=True)
-                hout["lost"].copy_(lost, non_blocking=True)
+                for dst, src in copies:
+                    dst.copy_(src, non_blocking=True)
                 ev_out[s] = torch.cuda.Event()
                 ev_out[s].record(d2h)
         # the caller's stream waits for the last copies

@@ -16,6 +16,7 @@ import torch.multiprocessing as mp
 
 from paper_2204_14194_b200.shard import block_range, gather_blocks
 from paper_2204_14194_b200 import workloads as wl
+from oracle import fase_oracle as orc
 
 
 def _free_port():
@@ -57,3 +58,163 @@ def test_gloo_world2_shards_and_gather(n_blocks):
     assert np.array_equal(sig, want)
     assert np.array_equal(sel[:, 0], np.arange(n_blocks))
     assert tmax == 2.0
+
+
+# ----------------------------------------------------------------- result arenas
+
+
+def _arena_worker(rank, world, port, n_blocks, iters, n_lost, out_q):
+    """Every rank fills its shard of a result arena with values derived from
+    the global block index; the root gathers and reassembles the batch."""
+    from paper_2204_14194_b200.shard import ResultArena
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    arena = ResultArena(n_blocks, iters, n_lost, torch.device("cpu"), world, rank)
+    sel, coef, lost = arena.local(0)
+    idx = torch.arange(arena.lo, arena.hi, dtype=torch.int64)
+    sel.copy_((idx[:, None] * 7 + torch.arange(iters)[None, :]) % 8192)
+    coef.copy_(idx[:, None].double() + torch.arange(iters)[None, :].double() / iters)
+    lost.copy_(-idx[:, None].double() - torch.arange(n_lost)[None, :].double() / n_lost)
+    arena.gather(0)
+    if rank == 0:
+        s, c, l_ = arena.assemble(0)
+        out_q.put((s.numpy(), c.numpy(), l_.numpy(), [(lo, hi) for lo, hi in arena.ranges]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_blocks", [4096, 4095])
+def test_gloo_world2_result_arena_config4_shapes(n_blocks):
+    """Config-4 result shapes (I = 500, 576 lost samples), even and uneven
+    shards: one gather per batch reassembles every block's selections,
+    coefficients and lost samples in block order on the root."""
+    iters, n_lost = 500, 576
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_arena_worker, args=(r, 2, port, n_blocks, iters, n_lost, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    sel, coef, lost, ranges = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ranges == [block_range(n_blocks, r, 2) for r in range(2)]
+    idx = np.arange(n_blocks)
+    assert np.array_equal(sel, (idx[:, None] * 7 + np.arange(iters)[None, :]) % 8192)
+    assert np.array_equal(coef, idx[:, None] + np.arange(iters)[None, :] / iters)
+    assert np.array_equal(lost, -idx[:, None] - np.arange(n_lost)[None, :] / n_lost)
+
+
+# ----------------------------------------------------------------- sharded frames
+
+
+FRAME = dict(h=40, w=48, mb=4, support=2, iters=12, rho=0.8, gamma=0.5, seed=7)
+
+
+def _frame_case():
+    """A small damaged frame with whole-tile losses, including border tiles."""
+    rng = np.random.default_rng(FRAME["seed"])
+    h, w, mb = FRAME["h"], FRAME["w"], FRAME["mb"]
+    img = rng.uniform(0, 255, (h, w))
+    lost = np.zeros((h, w), dtype=bool)
+    tiles = [(0, 0), (0, 5), (3, 3), (3, 4), (9, 11), (5, 0), (7, 8), (2, 11), (9, 2)]
+    for ty, tx in tiles:
+        lost[ty * mb:(ty + 1) * mb, tx * mb:(tx + 1) * mb] = True
+    img[lost] = 0.0
+    return img, lost
+
+
+class _HostEngine:
+    """A CPU stand-in for FrameEngine with the same run() contract: conceals
+    the given tiles of the frame with the oracle (fixed areas, out-of-frame
+    samples unavailable) and pastes each tile's own pixels into ``out``."""
+
+    def __init__(self):
+        from paper_2204_14194_b200.grid import ExtrapConfig
+
+        self.tile, self.support = FRAME["mb"], FRAME["support"]
+        a = self.tile + 2 * self.support
+        self.values = orc.family("dct", a, a)
+        self.phi = torch.from_numpy(self.values.real.reshape(len(self.values), -1).copy())
+        self.config = ExtrapConfig(FRAME["iters"], FRAME["gamma"], FRAME["rho"])
+        self.device = torch.device("cpu")
+
+    def run(self, frame, grid, corners, out=None, slot=0, outputs=None):
+        from paper_2204_14194_b200.model import BatchResult
+
+        img = frame.numpy()
+        lost = np.kron(grid.numpy().astype(bool), np.ones((self.tile, self.tile), dtype=bool))
+        cs = corners.numpy().astype(np.int64)
+        sigs, masks = wl.frame_areas(img, lost, cs, self.tile, self.support)
+        sel, coef = outputs
+        for i in range(len(cs)):
+            r = orc.extrapolate_block(sigs[i], masks[i], self.values, self.config.gamma,
+                                      self.config.iterations, self.config.rho_hat)
+            sel[i] = torch.from_numpy(r["selected"].astype(np.int32))
+            coef[i] = torch.from_numpy(r["coefficients"].real.copy())
+        host_paste(self.phi, sel, coef, self.config.iterations, grid, self.tile, self.support,
+                   corners, out)
+        return BatchResult(selected=sel, projections=None, coefficients=coef, patched=out)
+
+
+def host_paste(phi, sel, coef, iterations, grid, tile, support, corners, out):
+    """The frame_paste contract on the host (oracle synthesis, own tile only)."""
+    a = tile + 2 * support
+    vals = phi.numpy().reshape(-1, a, a)
+    for i, (r0, c0) in enumerate(corners.numpy()):
+        g = orc.materialize(vals, sel[i].numpy(), coef[i].numpy())
+        out[r0:r0 + tile, c0:c0 + tile] = torch.from_numpy(
+            np.ascontiguousarray(g.real[support:support + tile, support:support + tile]))
+
+
+def _frame_worker(rank, world, port, out_q):
+    from paper_2204_14194_b200 import _native
+    from paper_2204_14194_b200.conceal import lossy_tiles, tile_grid
+    from paper_2204_14194_b200.shard import ShardedFrame
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    _native.frame_paste = host_paste  # the root's paste of other ranks' tiles
+    img, lost = _frame_case()
+    grid = torch.from_numpy(tile_grid(lost, FRAME["mb"]))
+    corners = torch.from_numpy(lossy_tiles(lost, (FRAME["mb"],) * 2).astype(np.int32))
+    sf = ShardedFrame(_HostEngine(), grid, corners)
+    out = torch.from_numpy(img.copy())
+    sf.run(torch.from_numpy(img), out=out)
+    if rank == 0:
+        s, c, _ = sf.arena.assemble(0)
+        out_q.put((out.numpy(), s.numpy(), c.numpy(), (sf.lo, sf.hi)))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_frame_reassembles():
+    """Frame tiles split over two ranks (uneven: 9 tiles), results gathered to
+    the root, which pastes the other rank's tiles: the restored frame and the
+    per-tile results equal the single-process run bit-for-bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_frame_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out2, sel2, coef2, rng2 = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    q1 = ctx.Queue()
+    p1 = ctx.Process(target=_frame_worker, args=(0, 1, _free_port(), q1))
+    p1.start()
+    out1, sel1, coef1, rng1 = q1.get(timeout=300)
+    p1.join(timeout=120)
+    assert rng2 == (0, 5) and rng1 == (0, 9)
+    assert np.array_equal(sel1, sel2) and np.array_equal(coef1, coef2)
+    assert np.array_equal(out1, out2)
+    img, lost = _frame_case()
+    assert not np.array_equal(out1[lost], img[lost])  # every tile was pasted
+    assert np.array_equal(out1[~lost], img[~lost])
