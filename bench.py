@@ -381,9 +381,19 @@ def ozaki_roofline(plan, flops_fp64, seconds, fp64_peak, fp64_src):
     s = a.slices
     pairs = s * (s + 1) // 2
     ops = 2.0 * pairs * a.rows * b.rows * a.kp
-    # no measured INT8 figure exists for this pool; the nominal dense INT8 / FP8
-    # rate (B200_PROFILING.md: 4.5 PFLOP/s dense fp8, int8 at the same rate)
+    # measured on this pool's B200 with an issue-only tcgen05.mma kind::i8 probe
+    # (tools/probes/i8_peak_probe.cu, profiles/r02_int8_peak.json); fallback:
+    # the nominal dense INT8 (= FP8) rate of B200_PROFILING.md
     i8_peak, src = 4500.0, "nominal B200 dense INT8 (= FP8) tensor rate, B200_PROFILING.md"
+    q = ROOT / "profiles" / "r02_int8_peak.json"
+    if q.exists():
+        try:
+            rec = json.loads(q.read_text())
+            i8_peak = max(float(rec["tops_n128"]), float(rec["tops_n256"]))
+            src = ("measured: issue-only tcgen05.mma kind::i8 M=128 N=128/256 on every SM "
+                   "(tools/probes/i8_peak_probe.cu, profiles/r02_int8_peak.json)")
+        except (KeyError, ValueError):
+            pass
     return {"bound": "tensor", "kernel": "ozaki_gemm_kernel (tcgen05.mma kind::i8, "
             f"{s} digit planes, {pairs} pairs) over the support samples",
             "achieved": ops / seconds / 1e12, "peak": i8_peak, "unit": "TOPS (int8)",
