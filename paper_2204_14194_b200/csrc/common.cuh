@@ -29,6 +29,27 @@ __host__ __device__ inline bool aligned16(const void* p) { return (reinterpret_c
 
 // ---- device helpers --------------------------------------------------------
 
+// Checked build (-DFASE_BOUNDS, tools/build_exp.sh bounds): data-derived
+// indices are asserted in range and every mbarrier wait is bounded (a TMA whose
+// expect_tx does not match the bytes delivered would hang; here it traps).
+// compute-sanitizer is closed on this GPU pool, so this build plus the
+// determinism / operand-integrity runs of tools/sanitize_cases.py stand in.
+#ifdef FASE_BOUNDS
+#define FASE_ASSERT(cond)                                                               \
+  do {                                                                                  \
+    if (!(cond)) {                                                                      \
+      printf("FASE_BOUNDS %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,           \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x), #cond);       \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#else
+#define FASE_ASSERT(cond) \
+  do {                    \
+  } while (0)
+#endif
+
+
 // Correctly rounded multiply / subtract, never contracted into an FMA: the
 // reference's numpy arithmetic rounds the product and the difference
 // separately.
@@ -61,6 +82,7 @@ __device__ __forceinline__ double synth_terms(const double* __restrict__ phi, in
     for (int j = 0; j < G; ++j) {
       const int t = t0 + j;
       const int u = t < len ? s_sel[t] : -1;
+      FASE_ASSERT(u >= -1);
       v[j] = u >= 0 ? __ldg(phi + static_cast<int64_t>(u) * ldphi + m) : 0.0;
     }
 #pragma unroll
@@ -214,6 +236,21 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src
       : "memory");
 }
 
+#ifdef FASE_BOUNDS
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  for (long long spin = 0;; ++spin) {
+    unsigned done;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    FASE_ASSERT(spin < (1ll << 26));  // ~seconds: a transfer that never completes
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n"
@@ -225,6 +262,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 

@@ -44,6 +44,8 @@ __global__ void frame_areas_kernel(FrameGeom g, const double* __restrict__ frame
     const int b = static_cast<int>(idx / M);
     const int m = static_cast<int>(idx - static_cast<int64_t>(b) * M);
     const int i = m / g.A, j = m - (m / g.A) * g.A;
+    FASE_ASSERT(corners[2 * b] >= 0 && corners[2 * b] < g.H && corners[2 * b + 1] >= 0 &&
+                corners[2 * b + 1] < g.W);
     const int y = corners[2 * b] - g.support + i;
     const int x = corners[2 * b + 1] - g.support + j;
     double v = 0.0;
@@ -84,6 +86,7 @@ __global__ void __launch_bounds__(kPasteThreads) frame_paste_kernel(
   __shared__ double s_coef[kPasteChunk];
   const int b = blockIdx.x;
   const int r0 = corners[2 * b], c0 = corners[2 * b + 1];
+  FASE_ASSERT(r0 >= 0 && c0 >= 0 && r0 < g.H && c0 < g.W);
   const int n = g.tile * g.tile;
   const int32_t* my_sel = sel + static_cast<int64_t>(b) * ldo;
   const double* my_coef = coef + static_cast<int64_t>(b) * ldo;

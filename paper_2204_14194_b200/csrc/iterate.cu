@@ -52,6 +52,12 @@ namespace fase {
 namespace {
 
 constexpr unsigned kNone = 0xffffffffu;
+#ifndef FASE_SCALED_SEG
+#define FASE_SCALED_SEG 3
+#endif
+#ifndef FASE_SCALED_CHAINS
+#define FASE_SCALED_CHAINS 1
+#endif
 #ifdef FASE_ITERATE_STATS
 __device__ unsigned long long g_stats[8];  // measurement build: chunked-path counters
 #endif
@@ -105,7 +111,11 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   __shared__ __align__(16) double s_dump_all[NB][NW][kDsmem ? 1 : 2][EPT];  // tie-pass winner's registers
   // The staged row arrives in kSeg segments, each on its own mbarrier, so the
   // update can start on the first segment while the rest is still in flight.
-  constexpr int kSeg = EP < 3 ? EP : 3;
+  constexpr int kSegMax = kScaled ? FASE_SCALED_SEG : 3;
+  constexpr int kSeg = EP < kSegMax ? EP : kSegMax;
+  // independent running-max chains in the update (the compare / select chain
+  // through all EP pairs is serial otherwise); merged lowest-index-first
+  constexpr int kChains = (kScaled && EP >= 8) ? FASE_SCALED_CHAINS : 1;
   __shared__ __align__(8) uint64_t s_bar_all[NB][kSeg];
   __shared__ double s_heldm_all[NB];  // kChunked: metric of the held atom after the update
   extern __shared__ double2 s_dyn[];
@@ -164,8 +174,12 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     if (a.compose && nch > 0) {  // precomposed base for the longest listed prefix
       for (int k = min(nch, a.compose_depth); k >= 1; --k) {
         int64_t idx = 0;
-        for (int d = 0; d < a.compose_depth; ++d) idx = idx * a.n_compose + cids[min(d, k - 1)];
+        for (int d = 0; d < a.compose_depth; ++d) {
+          FASE_ASSERT(cids[min(d, k - 1)] >= 0 && cids[min(d, k - 1)] < a.n_compose);
+          idx = idx * a.n_compose + cids[min(d, k - 1)];
+        }
         const int p = a.compose[idx];
+        FASE_ASSERT(p >= 0);
         if (p > 0) {
           G0b += static_cast<int64_t>(p) * a.base_stride;
           cids += k;
@@ -347,6 +361,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         return a.G0;
     };
     if (t == 0 && issue) {
+      FASE_ASSERT(guess < static_cast<unsigned>(K));
       fence_proxy_async_smem();
       const double* grow = base() + static_cast<int64_t>(guess) * ldg;
       // fused synthesis: the predicted atom's phi row rides on the last segment
@@ -423,6 +438,10 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       u = __reduce_min_sync(0xffffffffu, su);
       uw = __ffs(__ballot_sync(0xffffffffu, su == u)) - 1;
     }
+    FASE_ASSERT(u < static_cast<unsigned>(K) && uw >= 0 && uw < NW);
+    if constexpr (kChunked) {
+      for (int ch = 0; ch < nch; ++ch) FASE_ASSERT(cids[ch] >= 0);
+    }
     const double ru = s_r[uw];
     const double du = s_d[uw];
     const double p = kScaled ? mul_rn(ru, du) : mul_rn(ru, mul_rn(du, du));
@@ -442,8 +461,13 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     // `pre(sg)` runs at the start of segment sg, before its arrival is awaited
     // (chunk-row loads are issued there, so they overlap the TMA wait)
     auto update = [&](auto row_pair, auto staged, auto pre) {
-      best = kDead;
-      barg = kNone;
+      double cb[kChains];
+      unsigned ca[kChains];
+#pragma unroll
+      for (int h = 0; h < kChains; ++h) {
+        cb[h] = kDead;
+        ca[h] = kNone;
+      }
 #pragma unroll
       for (int j = 0; j < EP; ++j) {
 #pragma unroll
@@ -457,17 +481,26 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         r[j][0] = sub_rn(r[j][0], mul_rn(c, g.x));
         r[j][1] = sub_rn(r[j][1], mul_rn(c, g.y));
         const double2 mm = metrics(j, dd);
+        const int h = j % kChains;
         const double m0 = mm.x;
-        if (m0 > best) {
-          best = m0;
-          barg = static_cast<unsigned>(2 * (j * NT + t));
+        if (m0 > cb[h]) {
+          cb[h] = m0;
+          ca[h] = static_cast<unsigned>(2 * (j * NT + t));
         }
         const double m1 = mm.y;
-        if (m1 > best) {
-          best = m1;
-          barg = static_cast<unsigned>(2 * (j * NT + t) + 1);
+        if (m1 > cb[h]) {
+          cb[h] = m1;
+          ca[h] = static_cast<unsigned>(2 * (j * NT + t) + 1);
         }
       }
+      best = cb[0];
+      barg = ca[0];
+#pragma unroll
+      for (int h = 1; h < kChains; ++h)  // equal maxima: the lower index wins
+        if (cb[h] > best || (cb[h] == best && ca[h] < barg)) {
+          best = cb[h];
+          barg = ca[h];
+        }
     };
     using Staged = std::true_type;
     using Direct = std::false_type;

@@ -119,7 +119,10 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
     if (a.compose && nch > 0) {  // precomposed base for the longest listed prefix
       for (int k = min(nch, a.compose_depth); k >= 1; --k) {
         int64_t idx = 0;
-        for (int d = 0; d < a.compose_depth; ++d) idx = idx * a.n_compose + cids[min(d, k - 1)];
+        for (int d = 0; d < a.compose_depth; ++d) {
+          FASE_ASSERT(cids[min(d, k - 1)] >= 0 && cids[min(d, k - 1)] < a.n_compose);
+          idx = idx * a.n_compose + cids[min(d, k - 1)];
+        }
         const int p = a.compose[idx];
         if (p > 0) {
           G0 += 2 * static_cast<int64_t>(p) * a.base_stride;
@@ -237,6 +240,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
       return;
     }
     if (t == 0) {
+      FASE_ASSERT(guess < static_cast<unsigned>(K));
       fence_proxy_async_smem();
       const double* grow = G0 + static_cast<int64_t>(guess) * ldg2x;
 #pragma unroll
@@ -382,6 +386,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
       du = s_cd[uw];
     }
 
+    FASE_ASSERT(u < static_cast<unsigned>(K));
     const double d2u = kScaled ? du : mul_rn(du, du);  // scaled: p = R'_u * D_u
     const double pr = mul_rn(ru.x, d2u), pi = mul_rn(ru.y, d2u);
     const double cr = mul_rn(a.gamma, pr), ci = mul_rn(a.gamma, pi);

@@ -1,13 +1,21 @@
-"""Small invocations of every kernel family, for compute-sanitizer.
+"""Small invocations of every kernel family: the checked-build / determinism run.
 
-    compute-sanitizer --tool memcheck  python tools/sanitize_cases.py [--case NAME]
-    compute-sanitizer --tool racecheck python tools/sanitize_cases.py
-    compute-sanitizer --tool synccheck python tools/sanitize_cases.py
+    python tools/sanitize_cases.py [--case NAME]
+    FASE_B200_LIB=exp/bounds.so python tools/sanitize_cases.py   # checked build
 
-(tools/sanitize.sh runs all three and writes the logs.) Each case is sized to
-select one kernel variant (the dispatch rules in csrc/iterate.cu,
-csrc/iterate_complex.cu, fast.py) at the smallest shape that reaches it, so the
-tools finish in minutes. A case prints one line; any CUDA fault raises.
+compute-sanitizer (memcheck / racecheck / synccheck, tools/sanitize.sh) is
+closed on this GPU pool, so the evidence is built in:
+- the checked build (``tools/build_exp.sh bounds -DFASE_BOUNDS``) asserts every
+  data-derived row / chunk / corner index in range and bounds every mbarrier
+  wait (a TMA whose expect_tx disagrees with the bytes delivered traps instead
+  of hanging);
+- every case runs twice and its outputs must be bit-identical (a shared-memory
+  or mbarrier-phase race shows up as nondeterminism);
+- read-only operands (tables, bases, Phi) are checksummed before and after the
+  kernels (a stray write into them fails the case).
+Each case is sized to select one kernel variant (the dispatch rules in
+csrc/iterate.cu, csrc/iterate_complex.cu, fast.py) at the smallest shape that
+reaches it. A case prints one line; any CUDA fault raises.
 """
 
 from __future__ import annotations
@@ -39,6 +47,21 @@ DEV = torch.device("cuda", 0)
 SMS = torch.cuda.get_device_properties(DEV).multi_processor_count if torch.cuda.is_available() else 148
 
 
+_FROZEN = []
+
+
+def frozen(*tensors):
+    """Register read-only device operands: checksummed now and after the case."""
+    for t in tensors:
+        _FROZEN.append((t, _digest(t)))
+
+
+def _digest(t):
+    v = t.detach().contiguous().view(-1)
+    v = v.view(torch.int32) if v.element_size() % 4 == 0 and v.numel() else v.to(torch.int32)
+    return (int(v.long().sum().item()), int((v.long() * 2654435761 % 1000003).sum().item()))
+
+
 def sig(b, m, n, seed=0):
     return np.random.default_rng(seed).uniform(0.0, 255.0, (b, m, n))
 
@@ -63,30 +86,34 @@ def case_exact_plain():
     """fase_iterate_kernel, shared geometry, more blocks than SMs (3-4 CTAs/SM shapes)."""
     d = parse_dict_spec("union:dct+had", 12, 12)
     mask = wl.central_loss_mask(12, 12, 4, 4)
-    r = fase_extrapolate_batch(sig(SMS + 12, 12, 12), mask, d, None, ExtrapConfig(12), device=DEV)
-    return r.selected
+    t = build_gram_tables(d, build_weight_field(mask, 0.8), device=DEV)
+    frozen(*t.device_tables(DEV), d.device_matrix(DEV))
+    r = fase_extrapolate_batch(sig(SMS + 12, 12, 12), mask, d, t, ExtrapConfig(12), device=DEV)
+    return [r.selected, r.coefficients, r.patched]
 
 
 def case_exact_latency():
     """Latency variant (at most one block per SM), K = 2304."""
     d = parse_dict_spec("dct", 48, 48)
     mask = wl.central_loss_mask(48, 48, 16, 16)
-    return fase_extrapolate_batch(sig(2, 48, 48), mask, d, None, ExtrapConfig(6), device=DEV).selected
+    r = fase_extrapolate_batch(sig(2, 48, 48), mask, d, None, ExtrapConfig(6), device=DEV)
+    return [r.selected, r.coefficients, r.patched]
 
 
 def case_exact_paired():
     """Paired blocks (two blocks per 512-thread CTA sharing D), 4608 < K <= 8192."""
     d = gauss(5000, 8, 8)
     mask = wl.central_loss_mask(8, 8, 3, 3)
-    return fase_extrapolate_batch(sig(SMS + 2, 8, 8), mask, d, None, ExtrapConfig(5),
-                                  device=DEV).selected
+    r = fase_extrapolate_batch(sig(SMS + 2, 8, 8), mask, d, None, ExtrapConfig(5), device=DEV)
+    return [r.selected, r.coefficients, r.patched]
 
 
 def case_exact_regs():
     """512-thread variant with R and D in registers (K > 5120, few blocks)."""
     d = gauss(6000, 8, 8)
     mask = wl.central_loss_mask(8, 8, 3, 3)
-    return fase_extrapolate_batch(sig(3, 8, 8), mask, d, None, ExtrapConfig(5), device=DEV).selected
+    r = fase_extrapolate_batch(sig(3, 8, 8), mask, d, None, ExtrapConfig(5), device=DEV)
+    return [r.selected, r.coefficients]
 
 
 def case_record():
@@ -95,7 +122,7 @@ def case_record():
     mask = wl.central_loss_mask(8, 8, 4, 4)
     r = fase_extrapolate_batch(sig(3, 8, 8), mask, d, None, ExtrapConfig(10), device=DEV,
                                record_products=True)
-    return r.selected
+    return [r.selected, r.coefficients]
 
 
 def case_scaled():
@@ -104,10 +131,13 @@ def case_scaled():
     mask = wl.central_loss_mask(12, 12, 4, 4)
     cfg = ExtrapConfig(12)
     t = build_gram_tables(d, build_weight_field(mask, cfg.rho_hat), device=DEV)
+    outs = []
     for b in (SMS + 12, 3):  # plain, fused synthesis (latency shape)
         p = ExtrapolationPlan(d, mask, b, cfg, t, device=DEV, recursion="scaled")
+        frozen(p.Gs, p.phi_lost)
         p.run(torch.from_numpy(sig(b, 12, 12)).to(DEV))
-    return p.selected
+        outs += [p.selected.clone(), p.coefficients.clone(), p.lost.clone()]
+    return outs
 
 
 def case_scaled_large():
@@ -118,16 +148,17 @@ def case_scaled_large():
     t = build_gram_tables(d, build_weight_field(mask, cfg.rho_hat), device=DEV)
     p = ExtrapolationPlan(d, mask, SMS + 4, cfg, t, device=DEV, recursion="scaled",
                           products="ozaki")
+    frozen(p.Gs)
     p.run(torch.from_numpy(sig(SMS + 4, 16, 16)).to(DEV))
-    return p.selected
+    return [p.selected, p.coefficients, p.lost, p.R0]
 
 
 def case_chunked():
     """Per-block geometries: chunk tables, the chunked recursion, block normalizers."""
     d = parse_dict_spec("union:dct+had", 12, 12)
     masks = per_block_masks(20, 12, 12)
-    return fase_extrapolate_batch(sig(20, 12, 12), masks, d, None, ExtrapConfig(12),
-                                  device=DEV).selected
+    r = fase_extrapolate_batch(sig(20, 12, 12), masks, d, None, ExtrapConfig(12), device=DEV)
+    return [r.selected, r.coefficients, r.patched]
 
 
 def case_frame():
@@ -145,7 +176,9 @@ def case_frame():
     eng = FrameEngine(d, (h, w), mb, 4, ExtrapConfig(20), device=DEV, compose="triples")
     grid = torch.from_numpy(tile_grid(lost, mb)).to(DEV)
     corners = torch.from_numpy(lossy_tiles(lost, (mb, mb)).astype(np.int32)).to(DEV)
-    return eng.run(torch.from_numpy(img).to(DEV), grid, corners).selected
+    frozen(eng.bases, eng.tables)
+    r = eng.run(torch.from_numpy(img).to(DEV), grid, corners)
+    return [r.selected, r.coefficients, r.patched]
 
 
 def case_complex():
@@ -153,30 +186,36 @@ def case_complex():
     d = parse_dict_spec("dft", 8, 8)
     mask = wl.central_loss_mask(8, 8, 3, 3)
     cfg = ExtrapConfig(10)
-    fase_extrapolate_batch(sig(SMS + 3, 8, 8), mask, d, None, cfg, device=DEV)
-    fase_extrapolate_batch(sig(6, 8, 8), per_block_masks(6, 8, 8), d, None, cfg, device=DEV)
+    outs = []
+    for r in (fase_extrapolate_batch(sig(SMS + 3, 8, 8), mask, d, None, cfg, device=DEV),
+              fase_extrapolate_batch(sig(6, 8, 8), per_block_masks(6, 8, 8), d, None, cfg,
+                                     device=DEV)):
+        outs += [r.selected, r.coefficients, r.patched]
     u = parse_dict_spec("union:dft+bdft", 48, 48)  # K = 4608 complex
     m48 = wl.central_loss_mask(48, 48, 16, 16)
-    fase_extrapolate_batch(sig(SMS + 2, 48, 48), m48, u, None, ExtrapConfig(3), device=DEV)
+    r1 = fase_extrapolate_batch(sig(SMS + 2, 48, 48), m48, u, None, ExtrapConfig(3), device=DEV)
     r = fase_extrapolate_batch(sig(4, 48, 48), m48, u, None, ExtrapConfig(3), device=DEV,
                                recursion="scaled")
-    return r.selected
+    return outs + [r1.selected, r1.coefficients, r.selected, r.coefficients, r.patched]
 
 
 def case_products():
     """Initial products: separable DMMA (batch), per-part separable, DMMA GEMM, complex separable."""
     mask = wl.central_loss_mask(16, 16, 6, 6)
     cfg = ExtrapConfig(3)
+    outs = []
     for spec, prod in (("union:dct+had", "separable"), ("union:dct+had", "gemm"),
                        ("dct", None), ("union:dct+dft", None)):
         d = parse_dict_spec(spec, 16, 16)
-        fase_extrapolate_batch(sig(SMS + 1, 16, 16), mask, d, None, cfg, device=DEV,
-                               **({"recursion": "exact"} if prod is None else {}))
+        r = fase_extrapolate_batch(sig(SMS + 1, 16, 16), mask, d, None, cfg, device=DEV,
+                                   **({"recursion": "exact"} if prod is None else {}))
+        outs += [r.selected, r.coefficients]
         if prod:
             t = build_gram_tables(d, build_weight_field(mask, cfg.rho_hat), device=DEV)
             p = ExtrapolationPlan(d, mask, 9, cfg, t, device=DEV, products=prod)
             p.run(torch.from_numpy(sig(9, 16, 16)).to(DEV))
-    return None
+            outs += [p.R0.clone(), p.selected.clone()]
+    return outs
 
 
 def case_gram():
@@ -185,10 +224,13 @@ def case_gram():
 
     mask = wl.central_loss_mask(16, 16, 6, 6)
     w = build_weight_field(mask, 0.8)
-    build_gram_tables(parse_dict_spec("union:dct+wht", 16, 16), w, device=DEV)
-    build_gram_tables(gauss(2100, 16, 16), w, device=DEV)
-    fft_gram_table(w, parse_dict_spec("dft", 16, 16), device=DEV)
-    return None
+    outs = []
+    for t in (build_gram_tables(parse_dict_spec("union:dct+wht", 16, 16), w, device=DEV),
+              build_gram_tables(gauss(2100, 16, 16), w, device=DEV)):
+        outs += [x.clone() for x in t.device_tables(DEV)]
+    t = fft_gram_table(w, parse_dict_spec("dft", 16, 16), device=DEV)
+    outs += [x.clone() for x in t.device_tables(DEV, complex_rows=True)]
+    return outs
 
 
 CASES = {k[5:]: v for k, v in globals().items() if k.startswith("case_")}
@@ -199,11 +241,22 @@ def main():
     ap.add_argument("--case", default="all", choices=["all", *CASES])
     args = ap.parse_args()
     names = list(CASES) if args.case == "all" else [args.case]
+    bad = 0
     for name in names:
         t0 = time.perf_counter()
-        CASES[name]()
+        _FROZEN.clear()
+        a = [x.clone() for x in CASES[name]() if x is not None]
         torch.cuda.synchronize()
-        print(f"case {name}: ok ({time.perf_counter() - t0:.1f} s)", flush=True)
+        b = [x.clone() for x in CASES[name]() if x is not None]
+        torch.cuda.synchronize()
+        same = len(a) == len(b) and all(torch.equal(x, y) for x, y in zip(a, b))
+        intact = all(_digest(t) == h for t, h in _FROZEN)
+        bad += not (same and intact)
+        print(f"case {name}: {'ok' if same and intact else 'FAILED'} (deterministic={same}, "
+              f"{len(a)} outputs; read-only operands intact={intact}, {len(_FROZEN)} checked; "
+              f"{time.perf_counter() - t0:.1f} s)", flush=True)
+    if bad:
+        raise SystemExit(f"{bad} case(s) failed")
 
 
 if __name__ == "__main__":
