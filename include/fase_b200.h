@@ -310,6 +310,15 @@ FASE_API int fase_frame_paste(const double* phi, int64_t ldphi, const int32_t* s
                               int64_t ldgrid, int H, int W, int tile, int support,
                               const int32_t* corners, int L, double* out, int64_t ldout,
                               void* stream);
+/*
+ * fase_frame_widen: out[y, x] = lost[y, x] ? 0.0 : (double)frame_u8[y, x] -- the
+ * damaged float64 frame the pipeline conceals, from the uint8 luma the caller
+ * uploads (pgm.py / conceal_image's `observed` with lost pixels zeroed,
+ * conceal.py:167-200). lost: H x W bytes, nonzero = lost.
+ */
+FASE_API int fase_frame_widen(const uint8_t* frame_u8, int64_t ldu, const uint8_t* lost,
+                              int64_t ldl, int H, int W, double* out, int64_t ldout,
+                              void* stream);
 
 /*
  * ---- Complex-valued dictionaries (dft, bdft, their unions; dictionary.py:126-166)

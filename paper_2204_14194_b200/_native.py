@@ -38,7 +38,7 @@ EXPORTS = (
     "fase_synth_paste_complex", "fase_sep_products_complex", "fase_fft_gram", "fase_weigh_gather",
     "fase_ozaki_split", "fase_ozaki_gemm", "fase_ozaki_gram", "fase_sep_products_batch",
     "fase_iterate_scaled", "fase_scale_columns", "fase_iterate_scaled_synth_capacity",
-    "fase_iterate_complex_scaled",
+    "fase_iterate_complex_scaled", "fase_frame_widen",
 )
 
 _vp = ctypes.c_void_p
@@ -145,6 +145,7 @@ def load():
                              _i64, _vp],
         "fase_frame_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i32, _i32,
                              _vp, _i32, _vp, _i64, _vp],
+        "fase_frame_widen": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _i64, _vp],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -594,6 +595,24 @@ def frame_paste(phi, sel, coef, iterations: int, grid, tile: int, support: int, 
     _check(lib.fase_frame_paste(_ptr(phi), _ld(phi), _ptr(sel), _ptr(coef), _ld(sel), iterations,
                                 _ptr(grid), _ld(grid), H, W, tile, support, _ptr(corners),
                                 corners.shape[0], _ptr(out), _ld(out), _stream(out)))
+
+
+def frame_widen(frame_u8, lost, out) -> None:
+    """out = lost ? 0 : float64(frame_u8) (H x W; lost bool / uint8, nonzero = lost)."""
+    import torch
+
+    lib = load()
+    _require(frame_u8, "frame_u8", torch.uint8, 2)
+    _require(out, "out", torch.float64, 2)
+    if not lost.is_cuda:
+        raise errors.NativeLibraryError("lost must be a CUDA tensor (no CPU fallback)")
+    if lost.dtype not in (torch.bool, torch.uint8) or lost.dim() != 2 or lost.stride(1) != 1:
+        raise errors.ShapeError("lost must be a row-major (H, W) bool / uint8 tensor")
+    H, W = out.shape
+    if tuple(frame_u8.shape) != (H, W) or tuple(lost.shape) != (H, W):
+        raise errors.ShapeError(f"frame {tuple(frame_u8.shape)} / lost {tuple(lost.shape)} vs {(H, W)}")
+    _check(lib.fase_frame_widen(_ptr(frame_u8), _ld(frame_u8), _ptr(lost), lost.stride(0), H, W,
+                                _ptr(out), _ld(out), _stream(out)))
 
 
 def weigh(x, w, M: int, out) -> None:

@@ -330,8 +330,7 @@ class FrameEngine:
                 if ev_out[s] is not None:
                     c.wait_event(ev_out[s])
                 f64 = p["f64"][s]
-                f64.copy_(p["u8"][s])
-                f64.masked_fill_(lost, 0.0)
+                _native.frame_widen(p["u8"][s], lost, f64)  # widen + zero the lost pixels
                 ev_used[s] = torch.cuda.Event()
                 ev_used[s].record(c)
                 self.run(f64, grid, corners, out=f64, slot=s,

@@ -11,6 +11,8 @@
 // entry is set. Pixels past the last full tile row / column (e.g. the 8-row
 // bottom strip of 1080p at 16-pixel tiles) are kept.
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace fase {
@@ -181,4 +183,62 @@ extern "C" int fase_frame_paste(const double* phi, int64_t ldphi, const int32_t*
   frame_paste_kernel<<<L, kPasteThreads, 0, as_stream(stream)>>>(
       g, phi, ldphi, sel, coef, ldo, I, grid, ldgrid, corners, out, ldout);
   return check_launch("fase_frame_paste");
+}
+
+namespace fase {
+namespace {
+// frame_widen: out = lost ? 0 : double(u8), 8 pixels per thread (8-byte loads of
+// the uint8 frame and the loss mask, four 16-byte stores)
+__global__ void __launch_bounds__(256) frame_widen_kernel(const uint8_t* __restrict__ u8, int64_t ldu,
+                                                          const uint8_t* __restrict__ lost,
+                                                          int64_t ldl, int H, int W,
+                                                          double* __restrict__ out, int64_t ldo) {
+  const int per_row = (W + 7) / 8;
+  const int64_t total = static_cast<int64_t>(H) * per_row;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int y = static_cast<int>(idx / per_row);
+    const int x0 = static_cast<int>(idx - static_cast<int64_t>(y) * per_row) * 8;
+    const uint8_t* src = u8 + y * ldu + x0;
+    const uint8_t* lm = lost + y * ldl + x0;
+    double* dst = out + y * ldo + x0;
+    const bool vec = x0 + 8 <= W && aligned16(dst) && (reinterpret_cast<uintptr_t>(src) & 7u) == 0 &&
+                     (reinterpret_cast<uintptr_t>(lm) & 7u) == 0;
+    if (vec) {
+      const uint2 pv = *reinterpret_cast<const uint2*>(src);
+      const uint2 lv = *reinterpret_cast<const uint2*>(lm);
+      double v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const unsigned pw = i < 4 ? pv.x : pv.y, lw = i < 4 ? lv.x : lv.y;
+        const unsigned sh = 8u * (i & 3);
+        v[i] = ((lw >> sh) & 0xffu) ? 0.0 : static_cast<double>((pw >> sh) & 0xffu);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) *reinterpret_cast<double2*>(dst + i) = make_double2(v[i], v[i + 1]);
+    } else {
+      for (int i = 0; i < 8 && x0 + i < W; ++i) dst[i] = lm[i] ? 0.0 : static_cast<double>(src[i]);
+    }
+  }
+}
+}  // namespace
+}  // namespace fase
+
+extern "C" int fase_frame_widen(const uint8_t* frame_u8, int64_t ldu, const uint8_t* lost,
+                                int64_t ldl, int H, int W, double* out, int64_t ldout,
+                                void* stream) {
+  if (H < 0 || W < 0 || ldu < W || ldl < W || ldout < W) {
+    set_error("fase_frame_widen: bad sizes");
+    return FASE_ERR_SHAPE;
+  }
+  if (H == 0 || W == 0) return FASE_OK;
+  if (!frame_u8 || !lost || !out) {
+    set_error("fase_frame_widen: null pointer");
+    return FASE_ERR_SHAPE;
+  }
+  const int64_t work = static_cast<int64_t>(H) * ((W + 7) / 8);
+  const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 148 * 16));
+  frame_widen_kernel<<<blocks, 256, 0, as_stream(stream)>>>(frame_u8, ldu, lost, ldl, H, W, out,
+                                                           ldout);
+  return check_launch("fase_frame_widen");
 }

@@ -165,3 +165,22 @@ def test_conceal_frame_complex_dictionary():
         sel_lost = lost[r0:r0 + 8, c0:c0 + 8]
         assert np.abs(got[sel_lost] - tile[sel_lost]).max() <= COEF_REL * 255
     assert np.array_equal(out[~lost], img[~lost])
+
+
+def test_frame_widen_kernel():
+    """fase_frame_widen: uint8 frame -> float64 with lost pixels zeroed, exactly
+    (odd widths and unaligned row starts take the scalar tail)."""
+    import torch
+
+    from paper_2204_14194_b200 import _native
+
+    rng = np.random.default_rng(3)
+    for h, w in ((1080, 1920), (37, 45), (5, 3)):
+        img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        lost = rng.random((h, w)) < 0.2
+        want = img.astype(np.float64)
+        want[lost] = 0.0
+        dev = torch.device("cuda", 0)
+        out = torch.full((h, w), -1.0, dtype=torch.float64, device=dev)
+        _native.frame_widen(torch.from_numpy(img).to(dev), torch.from_numpy(lost).to(dev), out)
+        assert np.array_equal(out.cpu().numpy(), want)
