@@ -310,6 +310,15 @@ FASE_API int fase_frame_paste(const double* phi, int64_t ldphi, const int32_t* s
                               int64_t ldgrid, int H, int W, int tile, int support,
                               const int32_t* corners, int L, double* out, int64_t ldout,
                               void* stream);
+/* fase_frame_paste for complex dictionaries: phi2 in the conjugate-split
+ * layout (rows 2u = Re phi_u, 2u+1 = -Im phi_u), coef interleaved complex (ldo
+ * in complex elements); Re g is pasted and, when max_imag != NULL,
+ * max_imag[b] = max |Im g| over tile b's pixels (apply_model, fast.py:267-286). */
+FASE_API int fase_frame_paste_complex(const double* phi2, int64_t ldphi, const int32_t* sel,
+                                      const double* coef, int64_t ldo, int I, const uint8_t* grid,
+                                      int64_t ldgrid, int H, int W, int tile, int support,
+                                      const int32_t* corners, int L, double* out, int64_t ldout,
+                                      double* max_imag, void* stream);
 /*
  * fase_frame_widen: out[y, x] = lost[y, x] ? 0.0 : (double)frame_u8[y, x] -- the
  * damaged float64 frame the pipeline conceals, from the uint8 luma the caller

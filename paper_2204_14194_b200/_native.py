@@ -38,7 +38,7 @@ EXPORTS = (
     "fase_synth_paste_complex", "fase_sep_products_complex", "fase_fft_gram", "fase_weigh_gather",
     "fase_ozaki_split", "fase_ozaki_gemm", "fase_ozaki_gram", "fase_sep_products_batch",
     "fase_iterate_scaled", "fase_scale_columns", "fase_iterate_scaled_synth_capacity",
-    "fase_iterate_complex_scaled", "fase_frame_widen",
+    "fase_iterate_complex_scaled", "fase_frame_widen", "fase_frame_paste_complex",
 )
 
 _vp = ctypes.c_void_p
@@ -146,6 +146,8 @@ def load():
         "fase_frame_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i32, _i32,
                              _vp, _i32, _vp, _i64, _vp],
         "fase_frame_widen": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _i64, _vp],
+        "fase_frame_paste_complex": [_vp, _i64, _vp, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i32,
+                                     _i32, _vp, _i32, _vp, _i64, _vp, _vp],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -595,6 +597,21 @@ def frame_paste(phi, sel, coef, iterations: int, grid, tile: int, support: int, 
     _check(lib.fase_frame_paste(_ptr(phi), _ld(phi), _ptr(sel), _ptr(coef), _ld(sel), iterations,
                                 _ptr(grid), _ld(grid), H, W, tile, support, _ptr(corners),
                                 corners.shape[0], _ptr(out), _ld(out), _stream(out)))
+
+
+def frame_paste_complex(phi2, sel, coef, iterations: int, grid, tile: int, support: int,
+                        corners, out, max_imag=None) -> None:
+    import torch
+
+    lib = load()
+    _require(phi2, "phi2", torch.float64, 2)
+    _require(out, "out", torch.float64, 2)
+    _require_complex(coef, "coef", 2)
+    H, W = out.shape
+    _check(lib.fase_frame_paste_complex(_ptr(phi2), _ld(phi2), _ptr(sel), _ptr(coef), _ld(sel),
+                                        iterations, _ptr(grid), _ld(grid), H, W, tile, support,
+                                        _ptr(corners), corners.shape[0], _ptr(out), _ld(out),
+                                        _ptr(max_imag), _stream(out)))
 
 
 def frame_widen(frame_u8, lost, out) -> None:

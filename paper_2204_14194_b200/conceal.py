@@ -104,9 +104,10 @@ class FrameEngine:
         a = tile + 2 * support
         if dictionary.shape != (a, a):
             raise ShapeError(f"dictionary area {dictionary.shape} vs extrapolation area {(a, a)}")
-        if not dictionary.is_real:
-            from .errors import UnsupportedDictionaryError
-            raise UnsupportedDictionaryError("complex-valued dictionaries are not supported on the GPU path")
+        # complex dictionaries (the reference's default `dft`, conceal.py:169):
+        # conjugate-split Phi, tables of rows of conj(C), the complex recursion
+        # and paste (iterate_complex.cu, fase_frame_paste_complex)
+        self.complex = cplx = not dictionary.is_real
         self.dictionary, self.config = dictionary, config
         self.H, self.W = frame_shape
         self.tile, self.support, self.A = tile, support, a
@@ -126,35 +127,42 @@ class FrameEngine:
         ld = dictionary.ld
         from .fast import _device_vector, _gram_on_device
         t0 = time.perf_counter()
-        self.G0 = _gram_on_device(phi, _device_vector(w0.ravel(), ld, dev), K, M, dev)
+        self.G0 = _gram_on_device(phi, _device_vector(w0.ravel(), ld, dev), K, M, dev,
+                                  complex_rows=cplx)
         ldg = self.G0.shape[1]
-        self.tables = torch.zeros((max(len(self.cells), 1), K, ldg), dtype=torch.float64, device=dev)
+        self.tables = torch.zeros((max(len(self.cells), 1), K, ldg), dtype=self.G0.dtype,
+                                  device=dev)
         flat_base = base.ravel()
         for c, (i0, i1, j0, j1) in enumerate(self.cells):
             ii, jj = np.meshgrid(np.arange(i0, i1), np.arange(j0, j1), indexing="ij")
             samples = (ii * a + jj).ravel()
             cols_t = torch.from_numpy(samples.astype(np.int64)).to(dev)
             width = samples.size + (samples.size & 1)
-            sub = torch.zeros((K, width), dtype=torch.float64, device=dev)
+            sub = torch.zeros((phi.shape[0], width), dtype=torch.float64, device=dev)
             sub[:, : samples.size] = phi.index_select(1, cols_t)
             wj = torch.zeros(width, dtype=torch.float64, device=dev)
             wj[: samples.size] = torch.from_numpy(flat_base[samples]).to(dev)
-            _native.gram(sub, wj, K, samples.size, self.tables[c])
+            (_native.gram_complex if cplx else _native.gram)(sub, wj, K, samples.size,
+                                                             self.tables[c])
         self.bases, self.compose = self._compose_bases(compose)
-        # dense initial products on the tcgen05 tensor cores (Ozaki digit planes)
+        # dense initial products on the tcgen05 tensor cores (Ozaki digit planes);
+        # complex sets: separable DFT row ranges through the complex transform
         self._oz_phi = None
-        if not dictionary.device_factors(dev):
+        self._cparts = dictionary.device_cfactors(dev) if cplx else []
+        if not (self._cparts if cplx else dictionary.device_factors(dev)):
             from .fast import ozaki_worthwhile
 
-            if ozaki_worthwhile(4096, K):
-                self._oz_phi = _native.OzakiOperand(K, M, 64, dev).split(phi[:, :ld])
+            if ozaki_worthwhile(4096, phi.shape[0]):
+                self._oz_phi = _native.OzakiOperand(phi.shape[0], M, 64, dev).split(phi[:, :ld])
         torch.cuda.current_stream(dev).synchronize()
         self.table_seconds = time.perf_counter() - t0
         self.stride = self.tables[0].numel()
         # diagonals of G0 and of every cell table for the per-frame normalizers:
         # contiguous, L2-resident reads instead of one sector per diagonal element
-        self._diag_G0 = self.G0.diagonal()[:K].contiguous()
-        self._diag_tabs = self.tables.diagonal(dim1=1, dim2=2)[:, :K].contiguous()
+        # (complex tables: the real diagonal, exactly what fase_block_normalizers
+        # reads from a complex table with its complex stride)
+        self._diag_G0 = self.G0.diagonal()[:K].real.contiguous()
+        self._diag_tabs = self.tables.diagonal(dim1=1, dim2=2)[:, :K].real.contiguous()
         self.cell_rep = torch.tensor([[c[0], c[2]] for c in self.cells] or [[0, 0]],
                                      dtype=torch.int32, device=dev)
         self.base_w = torch.from_numpy(flat_base.copy()).to(dev)
@@ -179,7 +187,7 @@ class FrameEngine:
             return 1 + sum(math.comb(n, k) for k in range(1, depth + 1))
 
         if mode == "auto":
-            table = self.G0.numel() * 8
+            table = self.G0.numel() * self.G0.element_size()
             budget = min(COMPOSE_BUDGET, torch.cuda.mem_get_info(self.device)[0] // 2)
             mode = next((m for m in ("triples", "pairs", "singles")
                          if n_bases(depths[m]) * table <= budget), "none")
@@ -188,7 +196,7 @@ class FrameEngine:
         if not depth:
             return None, None
         K, ldg = self.G0.shape
-        bases = torch.empty((n_bases(depth), K, ldg), dtype=torch.float64, device=self.device)
+        bases = torch.empty((n_bases(depth), K, ldg), dtype=self.G0.dtype, device=self.device)
         bases[0].copy_(self.G0)
         cmap = np.zeros((n,) * depth, dtype=np.int32)
         index = {(): 0}
@@ -209,21 +217,23 @@ class FrameEngine:
         if key not in self._buf:
             dev, K, I = self.device, self.K, self.config.iterations
             ldx = self.M + (self.M & 1)
+            vdt = torch.complex128 if self.complex else torch.float64
             self._buf = {k: v for k, v in self._buf.items() if k[0] == L}  # one batch size kept
             self._buf[key] = dict(
                 X=torch.empty((L, ldx), dtype=torch.float64, device=dev),
-                R0=torch.empty((L, K + (K & 1)), dtype=torch.float64, device=dev),
+                R0=torch.empty((L, K + (K & 1)), dtype=vdt, device=dev),
                 D=torch.empty((L, self.G0.shape[1]), dtype=torch.float64, device=dev),
                 alive=torch.empty(L, dtype=torch.int32, device=dev),
                 counts=torch.empty(L, dtype=torch.int32, device=dev),
                 ids=torch.zeros((L, max(len(self.cells), 1)), dtype=torch.int32, device=dev),
                 sel=torch.empty((L, I), dtype=torch.int32, device=dev),
-                proj=torch.empty((L, I), dtype=torch.float64, device=dev),
-                coef=torch.empty((L, I), dtype=torch.float64, device=dev),
+                proj=torch.empty((L, I), dtype=vdt, device=dev),
+                coef=torch.empty((L, I), dtype=vdt, device=dev),
+                max_imag=torch.zeros(L, dtype=torch.float64, device=dev) if self.complex else None,
             )
             from .fast import ozaki_worthwhile
 
-            if self._oz_phi is not None and ozaki_worthwhile(L, K):
+            if self._oz_phi is not None and ozaki_worthwhile(L, self.phi.shape[0]):
                 self._buf[key]["oz"] = _native.OzakiOperand(L, self.M, 128, dev)
         return self._buf[key]
 
@@ -231,10 +241,48 @@ class FrameEngine:
     def launches_per_frame(self) -> int:
         """areas, cells, normalizers, products (one per separable part or one GEMM),
         iterate, paste"""
-        factors = self.dictionary.device_factors(self.device)
+        if self.complex and self._cparts:
+            from .fast import _ranges
+
+            return 5 + len(self._cparts) + len(_ranges(self._uncovered()))
+        factors = None if self.complex else self.dictionary.device_factors(self.device)
         if factors:
             return 5 + (1 if len(factors) <= 8 else len(factors))
         return 5 + (2 if any("oz" in b for b in self._buf.values()) else 1)
+
+    def _uncovered(self):
+        flags = np.ones(self.K, dtype=bool)
+        for rre, _, cre, _, row0 in self._cparts:
+            flags[row0: row0 + rre.shape[0] * cre.shape[0]] = False
+        return flags
+
+    def _products(self, b):
+        """R0 of the frame's areas from the weighted areas X (frame_areas)."""
+        from .fast import _ranges, _real_view
+
+        X, R0 = b["X"], b["R0"]
+        if self.complex:
+            if self._cparts:  # conj(E) X conj(F)^T per separable part; the rest by GEMM
+                for rre, rim, cre, cim, row0 in self._cparts:
+                    _native.sep_products_complex(rre, rim, cre, cim, X, self.A, self.A, R0, row0)
+                Rv = _real_view(R0)
+                for lo, hi in _ranges(self._uncovered()):
+                    _native.gemm_nt(X[:, : self.M], self.phi[2 * lo: 2 * hi, : self.M], Rv[:, 2 * lo:])
+            elif self._oz_phi is not None and "oz" in b:
+                _native.ozaki_gemm(b["oz"].split(X), self._oz_phi, _real_view(R0))
+            else:
+                _native.gemm_nt(X[:, : self.M], self.phi[:, : self.M], _real_view(R0))
+            return
+        factors = self.dictionary.device_factors(self.device)
+        if factors and len(factors) <= 8:  # separable parts on DMMA, one launch
+            _native.sep_products_batch(factors, X, None, self.A, self.A, R0)
+        elif factors:  # rows X cols^T per part (csrc/separable.cu)
+            for rows, cols, row0 in factors:
+                _native.sep_products(rows, cols, X, self.A, self.A, R0, row0)
+        elif self._oz_phi is not None and "oz" in b:
+            _native.ozaki_gemm(b["oz"].split(X), self._oz_phi, R0)
+        else:
+            _native.gemm_nt(X[:, : self.M], self.phi[:, : self.M], R0)
 
     def run(self, frame, grid, corners, out=None, slot: int = 0, outputs=None) -> BatchResult:
         """Conceal one frame: ``frame`` (H, W) float64, ``grid`` (H/tile, W/tile)
@@ -256,9 +304,10 @@ class FrameEngine:
 
             sel, coef = outputs
             I = self.config.iterations
+            cdt = torch.complex128 if self.complex else torch.float64
             if (tuple(sel.shape) != (L, I) or sel.dtype != torch.int32 or tuple(coef.shape) != (L, I)
-                    or coef.dtype != torch.float64 or not (sel.is_contiguous() and coef.is_contiguous())):
-                raise ShapeError("outputs must be contiguous (L, I) int32 / float64 buffers")
+                    or coef.dtype != cdt or not (sel.is_contiguous() and coef.is_contiguous())):
+                raise ShapeError(f"outputs must be contiguous (L, I) int32 / {cdt} buffers")
             b = dict(b, sel=sel, coef=coef)
         cfg, K = self.config, self.K
         _native.frame_areas(frame, grid, self.tile, self.support, corners, self.base_w, b["X"])
@@ -266,25 +315,20 @@ class FrameEngine:
                             b["counts"], b["ids"])
         _native.block_normalizers(self._diag_G0, self._diag_tabs, K, b["counts"], b["ids"], K,
                                   b["D"], b["alive"])
-        factors = self.dictionary.device_factors(self.device)
-        if factors and len(factors) <= 8:  # separable parts on DMMA, one launch
-            _native.sep_products_batch(factors, b["X"], None, self.A, self.A, b["R0"])
-        elif factors:  # rows X cols^T per part (csrc/separable.cu)
-            for rows, cols, row0 in factors:
-                _native.sep_products(rows, cols, b["X"], self.A, self.A, b["R0"], row0)
-        elif self._oz_phi is not None and "oz" in b:
-            _native.ozaki_gemm(b["oz"].split(b["X"]), self._oz_phi, b["R0"])
+        self._products(b)
+        (_native.iterate_complex if self.complex else _native.iterate)(
+            self.G0, b["D"], b["R0"], K, cfg.iterations, cfg.gamma, b["sel"], b["proj"], b["coef"],
+            chunk_tables=self.tables, chunk_stride=self.stride, chunk_count=b["counts"],
+            chunk_ids=b["ids"], compose=self.compose, base_stride=self.G0.numel())
+        if self.complex:
+            _native.frame_paste_complex(self.phi, b["sel"], b["coef"], cfg.iterations, grid,
+                                        self.tile, self.support, corners, out, b["max_imag"])
         else:
-            _native.gemm_nt(b["X"][:, : self.M], self.phi[:, : self.M], b["R0"])
-        _native.iterate(self.G0, b["D"], b["R0"], K, cfg.iterations, cfg.gamma, b["sel"], b["proj"],
-                        b["coef"], chunk_tables=self.tables, chunk_stride=self.stride,
-                        chunk_count=b["counts"], chunk_ids=b["ids"], compose=self.compose,
-                        base_stride=self.G0.numel())
-        _native.frame_paste(self.phi, b["sel"], b["coef"], cfg.iterations, grid, self.tile,
-                            self.support, corners, out)
+            _native.frame_paste(self.phi, b["sel"], b["coef"], cfg.iterations, grid, self.tile,
+                                self.support, corners, out)
         return BatchResult(selected=b["sel"], projections=b["proj"], coefficients=b["coef"],
                            patched=out, dictionary=self.dictionary,
-                           shape=(self.A, self.A))
+                           shape=(self.A, self.A), max_imag=b["max_imag"])
 
     def run_host_stream(self, frames_u8, outs, grid, corners, lost, *, slot_outputs=None,
                         finish=None):
@@ -417,7 +461,7 @@ def conceal_frame(image, lost_mask, *, dictionary: Dictionary | None = None,
     a = block + 2 * support
     if dictionary is None:
         dictionary = parse_dict_spec(dict_spec, a, a)
-    grid = tile_grid(lost, block) if dictionary.is_real else None  # FrameEngine: real sets
+    grid = tile_grid(lost, block)  # whole-tile losses: the FrameEngine (real and complex sets)
     damaged = img.copy()
     damaged[lost] = 0.0
     if grid is not None:

@@ -113,6 +113,75 @@ __global__ void __launch_bounds__(kPasteThreads) frame_paste_kernel(
   }
 }
 
+// Complex dictionaries (conjugate-split rows phi2[2u] = Re phi_u, phi2[2u+1] =
+// -Im phi_u; coef interleaved complex): g = sum_t coef_t * phi_{sel_t} with
+// numpy's complex product, accumulated in selection order (reference.py:120-125,
+// as synth_paste_complex); Re g is pasted (fast.py:282) and max |Im g| over the
+// tile goes to max_imag[b] when given (apply_model's diagnostic).
+__global__ void __launch_bounds__(kPasteThreads) frame_paste_complex_kernel(
+    FrameGeom g, const double* __restrict__ phi2, int64_t ldphi, const int32_t* __restrict__ sel,
+    const double* __restrict__ coef, int64_t ldo, int I, const uint8_t* __restrict__ grid,
+    int64_t ldgrid, const int32_t* __restrict__ corners, double* __restrict__ out, int64_t ldout,
+    double* __restrict__ max_imag) {
+  __shared__ int32_t s_sel[kPasteChunk];
+  __shared__ double2 s_coef[kPasteChunk];
+  __shared__ double s_m[kPasteThreads / 32];
+  const int b = blockIdx.x;
+  const int r0 = corners[2 * b], c0 = corners[2 * b + 1];
+  FASE_ASSERT(r0 >= 0 && c0 >= 0 && r0 < g.H && c0 < g.W);
+  const int n = g.tile * g.tile;
+  const int32_t* my_sel = sel + static_cast<int64_t>(b) * ldo;
+  const double* my_coef = coef + 2 * static_cast<int64_t>(b) * ldo;
+  double imax = 0.0;
+  for (int base = 0; base < n; base += kPasteThreads) {
+    const int p = base + threadIdx.x;
+    const int i = p / g.tile, j = p - (p / g.tile) * g.tile;
+    const bool mine = p < n && r0 + i < g.H && c0 + j < g.W &&
+                      unavailable(g, grid, ldgrid, r0 + i, c0 + j);
+    const int m = (g.support + i) * g.A + g.support + j;
+    double gr = 0.0, gi = 0.0;
+    bool done = false;
+    for (int t0 = 0; t0 < I; t0 += kPasteChunk) {
+      const int len = min(kPasteChunk, I - t0);
+      __syncthreads();
+      for (int t = threadIdx.x; t < len; t += kPasteThreads) {
+        s_sel[t] = my_sel[t0 + t];
+        s_coef[t] = make_double2(my_coef[2 * (t0 + t)], my_coef[2 * (t0 + t) + 1]);
+      }
+      __syncthreads();
+      if (mine && !done) {
+        for (int t = 0; t < len; ++t) {
+          const int u = s_sel[t];
+          if (u < 0) {  // block without selectable atoms: terms end here
+            done = true;
+            break;
+          }
+          const double pr = __ldg(phi2 + (2 * static_cast<int64_t>(u)) * ldphi + m);
+          const double pi = -__ldg(phi2 + (2 * static_cast<int64_t>(u) + 1) * ldphi + m);
+          const double2 c = s_coef[t];
+          const double2 x = np_cmul(c.x, c.y, pr, pi);
+          gr = add_rn(gr, x.x);
+          gi = add_rn(gi, x.y);
+        }
+      }
+    }
+    if (mine) {
+      out[static_cast<int64_t>(r0 + i) * ldout + c0 + j] = gr;
+      imax = fmax(imax, fabs(gi));
+    }
+  }
+  if (max_imag) {
+    for (int o = 16; o > 0; o >>= 1) imax = fmax(imax, __shfl_xor_sync(0xffffffffu, imax, o));
+    if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = imax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v = 0.0;
+      for (int w = 0; w < kPasteThreads / 32; ++w) v = fmax(v, s_m[w]);
+      max_imag[b] = v;
+    }
+  }
+}
+
 bool geom_ok(const FrameGeom& g) {
   return g.H > 0 && g.W > 0 && g.tile > 0 && g.support >= 0 && g.A == g.tile + 2 * g.support &&
          g.Ty == g.H / g.tile && g.Tx == g.W / g.tile;
@@ -223,6 +292,27 @@ __global__ void __launch_bounds__(256) frame_widen_kernel(const uint8_t* __restr
 }
 }  // namespace
 }  // namespace fase
+
+extern "C" int fase_frame_paste_complex(const double* phi2, int64_t ldphi, const int32_t* sel,
+                                        const double* coef, int64_t ldo, int I,
+                                        const uint8_t* grid, int64_t ldgrid, int H, int W,
+                                        int tile, int support, const int32_t* corners, int L,
+                                        double* out, int64_t ldout, double* max_imag,
+                                        void* stream) {
+  const FrameGeom g{H, W, tile, support, tile + 2 * support, H / tile, W / tile};
+  if (!geom_ok(g) || L < 0 || I < 1 || ldo < I || ldout < W || ldgrid < g.Tx) {
+    set_error("fase_frame_paste_complex: bad geometry or sizes");
+    return FASE_ERR_SHAPE;
+  }
+  if (L == 0) return FASE_OK;
+  if (!phi2 || !sel || !coef || !grid || !corners || !out) {
+    set_error("fase_frame_paste_complex: null pointer");
+    return FASE_ERR_SHAPE;
+  }
+  frame_paste_complex_kernel<<<L, kPasteThreads, 0, as_stream(stream)>>>(
+      g, phi2, ldphi, sel, coef, ldo, I, grid, ldgrid, corners, out, ldout, max_imag);
+  return check_launch("fase_frame_paste_complex");
+}
 
 extern "C" int fase_frame_widen(const uint8_t* frame_u8, int64_t ldu, const uint8_t* lost,
                                 int64_t ldl, int H, int W, double* out, int64_t ldout,

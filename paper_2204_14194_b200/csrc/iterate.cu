@@ -782,6 +782,12 @@ const Variant* override_variant(int K, const Variant* dflt) {
 }
 
 }  // namespace
+
+int sm_count_cluster() { return sm_count(); }
+// csrc/iterate_cluster.cu: one block over a CTA cluster (latency-bound batches)
+int launch_iterate_cluster(const fase_iterate_args& a, const fase_synth_fused* syn, bool scaled,
+                           cudaStream_t stream);
+int cluster_synth_capacity(int K, int64_t ldg, int B);
 }  // namespace fase
 
 using namespace fase;
@@ -835,6 +841,10 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
   const Variant* dflt = pick_variant(a.K);
   const Variant* v = override_variant(a.K, dflt);
   const bool small = a.B <= sm_count();  // at most one block per SM
+  if (small && !getenv("FASE_ITERATE_VARIANT")) {  // a block over a CTA cluster
+    const int rc = launch_iterate_cluster(a, nullptr, false, as_stream(stream));
+    if (rc != 1) return rc;
+  }
   if (v == dflt && dflt && small && !getenv("FASE_ITERATE_VARIANT")) {
     for (const Variant& lv : kLatencyVariants)
       if (lv.nt * lv.ept >= a.K && lv.nt * lv.ept <= dflt->nt * dflt->ept && lv.nt > v->nt) v = &lv;
@@ -907,8 +917,13 @@ const Variant* pick_scaled(int K, int B) {
 }  // namespace fase
 
 extern "C" int fase_iterate_scaled_synth_capacity(int K, int B) {
+  // the larger of the cluster path's (taken when the lost samples fit it) and
+  // the one-CTA variant's capacity
+  int c = 0;
+  if (K >= 1 && B >= 1 && B <= sm_count() && !getenv("FASE_SCALED_VARIANT"))
+    c = cluster_synth_capacity(K, fase_table_ld(K), B);
   const Variant* v = K >= 1 ? pick_scaled(K, B) : nullptr;
-  return v ? v->syn * v->nt : 0;
+  return v ? max(c, v->syn * v->nt) : c;
 }
 
 extern "C" int fase_iterate_scaled(const fase_iterate_args* args, const fase_synth_fused* syn,
@@ -941,6 +956,10 @@ extern "C" int fase_iterate_scaled(const fase_iterate_args* args, const fase_syn
               syn->ldphi < syn->n_lost || !syn->out || syn->ldout < syn->n_lost)) {
     set_error("fase_iterate_scaled: bad fused-synthesis operand (n_lost=%d)", syn ? syn->n_lost : 0);
     return FASE_ERR_SHAPE;
+  }
+  if (a.B <= sm_count() && !getenv("FASE_SCALED_VARIANT")) {  // a block over a CTA cluster
+    const int rc = launch_iterate_cluster(a, syn, true, as_stream(stream));
+    if (rc != 1) return rc;
   }
   const Variant* v = pick_scaled(a.K, a.B);
   if (!v) {

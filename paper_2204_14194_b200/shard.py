@@ -78,17 +78,18 @@ class ResultArena:
     """
 
     def __init__(self, n_blocks: int, iterations: int, n_lost: int, device, world: int,
-                 rank: int, root: int = 0, slots: int = 1):
+                 rank: int, root: int = 0, slots: int = 1, complex_coef: bool = False):
         import torch
 
+        self.cw = 2 if complex_coef else 1  # float64 words per coefficient
         self.n_blocks, self.I, self.L = n_blocks, iterations, n_lost
         self.world, self.rank, self.root = world, rank, root
         self.ranges = [block_range(n_blocks, r, world) for r in range(world)]
         self.lo, self.hi = self.ranges[rank]
         self.width = max(h - l for l, h in self.ranges)
-        w, I, L = self.width, iterations, n_lost
-        self.offsets = (0, 8 * w * I, 8 * w * (I + L))
-        self.nbytes = 8 * w * (I + L) + 4 * w * I
+        w, I, L, cw = self.width, iterations, n_lost, self.cw
+        self.offsets = (0, 8 * w * I * cw, 8 * w * (I * cw + L))
+        self.nbytes = 8 * w * (I * cw + L) + 4 * w * I
         self.nbytes += (-self.nbytes) % 8
         self.device = device
         self.bufs = [torch.zeros(self.nbytes, dtype=torch.uint8, device=device)
@@ -107,7 +108,9 @@ class ResultArena:
         n = self.width if n is None else n
         w, I, L = self.width, self.I, self.L
         o_c, o_l, o_s = self.offsets
-        coef = buf[o_c:o_l].view(torch.float64).view(w, I)[:n]
+        coef = buf[o_c:o_l].view(torch.float64).view(w, I * self.cw)[:n]
+        if self.cw == 2:
+            coef = torch.view_as_complex(coef.view(n, I, 2))
         lost = buf[o_l:o_s].view(torch.float64).view(w, max(L, 0))[:n]
         sel = buf[o_s:o_s + 4 * w * I].view(torch.int32).view(w, I)[:n]
         return sel, coef, lost
@@ -158,7 +161,7 @@ class ShardedBatch:
         probe = np.asarray(mask, dtype=bool)
         n_lost = int(probe.sum())
         self.arena = ResultArena(n_blocks, config.iterations, max(n_lost, 1), device, self.world,
-                                 self.rank, root, slots=2)
+                                 self.rank, root, slots=2, complex_coef=not dictionary.is_real)
         self.lo, self.hi = self.arena.lo, self.arena.hi
         sel, coef, lost = self.arena.local(0)
         self.plan = ExtrapolationPlan(dictionary, mask, self.hi - self.lo, config, tables,
@@ -225,7 +228,8 @@ class ShardedFrame:
         self.group, self.root = group, root
         L = int(corners.shape[0])
         self.arena = ResultArena(L, engine.config.iterations, 0, engine.device, self.world,
-                                 self.rank, root, slots=2)
+                                 self.rank, root, slots=2,
+                                 complex_coef=getattr(engine, "complex", False))
         self.lo, self.hi = self.arena.lo, self.arena.hi
         self.corners = corners
         self.local_corners = corners[self.lo:self.hi].contiguous()
@@ -243,11 +247,12 @@ class ShardedFrame:
         if not self.is_root or self.world == 1:
             return
         eng = self.engine
+        paste = _native.frame_paste_complex if getattr(eng, "complex", False) else _native.frame_paste
         for r, (lo, hi, sel, coef, _) in enumerate(self.arena.shards(slot)):
             if r == self.rank or hi == lo:
                 continue
-            _native.frame_paste(eng.phi, sel, coef, eng.config.iterations, self.grid, eng.tile,
-                                eng.support, self.rank_corners[r], out)
+            paste(eng.phi, sel, coef, eng.config.iterations, self.grid, eng.tile, eng.support,
+                  self.rank_corners[r], out)
 
     def run(self, frame, out=None, slot: int = 0):
         """Conceal this rank's tiles of ``frame`` (device float64) into ``out``,

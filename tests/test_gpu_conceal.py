@@ -140,7 +140,9 @@ def test_conceal_image_tables_fft_and_edges():
 
 def test_conceal_frame_complex_dictionary():
     """conceal_frame (fixed areas) with the default complex dictionary takes the
-    per-block path; every lost pixel matches the oracle's block result."""
+    FrameEngine pipeline (complex cell tables, precomposed bases, the complex
+    chunked recursion and paste); every block's selections / coefficients and
+    every lost pixel match the oracle's block result."""
     from paper_2204_14194_b200 import conceal_frame
     from paper_2204_14194_b200 import workloads as wl
 
@@ -158,13 +160,66 @@ def test_conceal_frame_complex_dictionary():
     corners = np.array(sorted({(r // 8 * 8, c // 8 * 8) for r, c in zip(*np.nonzero(lost))}))
     signals, masks = wl.frame_areas(damaged, lost, corners, 8, 4)
     vals = parse_dict_spec("dft", 16, 16).values
+    assert rep["settings"]["pipeline"] == "frame-engine"
+    res = rep["result"]
     for i, (r0, c0) in enumerate(corners):
-        ref = orc.extrapolate_block(signals[i], masks[i], vals, 0.5, 30, 0.8)
+        ref = orc.extrapolate_block(signals[i], masks[i], vals, 0.5, 30, 0.8, record=True)
+        v = compare_selection(res.selected[i].cpu().numpy(), ref["selected"],
+                              metric_fn(ref["r0"], ref["d"], ref["log"]))
+        assert v.ok, f"block {i}: diverged at {v.stop}, gap {v.gap}"
+        c = res.coefficients[i].cpu().numpy()[: v.stop]
+        assert np.abs(c - ref["coefficients"][: v.stop]).max() <= COEF_REL * np.abs(
+            ref["coefficients"]).max()
         tile = ref["patched"][4:12, 4:12]
         got = out[r0:r0 + 8, c0:c0 + 8]
         sel_lost = lost[r0:r0 + 8, c0:c0 + 8]
         assert np.abs(got[sel_lost] - tile[sel_lost]).max() <= COEF_REL * 255
+        # apply_model's diagnostic over the tile's pasted pixels
+        want_imag = float(np.abs(ref["g"].imag[4:12, 4:12][sel_lost]).max())
+        assert abs(float(res.max_imag[i]) - want_imag) <= COEF_REL * max(want_imag, 1.0)
     assert np.array_equal(out[~lost], img[~lost])
+
+
+@pytest.mark.parametrize("spec", ["dft", "union:dct+dft", "bdft"])
+def test_frame_engine_complex_compose_bit_identical(spec):
+    """Complex FrameEngine: precomposed bases (pairs, triples) stream rows
+    bit-identical to the uncomposed cell lists, so every composition mode gives
+    the same selections, coefficients and frame; mixed unions take the complex
+    separable transform plus the DMMA GEMM for the real rows."""
+    import torch
+
+    from paper_2204_14194_b200.conceal import FrameEngine, lossy_tiles, tile_grid
+
+    rng = np.random.default_rng(8)
+    h, w, mb, sup = 40, 48, 8, 4
+    img = rng.uniform(0, 255, (h, w))
+    lost = np.zeros((h, w), dtype=bool)
+    for ty, tx in [(0, 0), (0, 1), (1, 1), (2, 3), (4, 5), (3, 0), (4, 4)]:
+        lost[ty * mb:(ty + 1) * mb, tx * mb:(tx + 1) * mb] = True
+    img[lost] = 0.0
+    d = parse_dict_spec(spec, mb + 2 * sup, mb + 2 * sup)
+    cfg = ExtrapConfig(25, 0.5, 0.8)
+    dev = torch.device(DEV)
+    grid = torch.from_numpy(tile_grid(lost, mb)).to(dev)
+    corners = torch.from_numpy(lossy_tiles(lost, (mb, mb)).astype(np.int32)).to(dev)
+    outs = {}
+    for mode in ("none", "pairs", "triples"):
+        eng = FrameEngine(d, (h, w), mb, sup, cfg, device=dev, compose=mode)
+        r = eng.run(torch.from_numpy(img).to(dev), grid, corners)
+        outs[mode] = (r.selected.clone(), r.coefficients.clone(), r.patched.clone())
+    for mode in ("pairs", "triples"):
+        for a, b in zip(outs["none"], outs[mode]):
+            assert torch.equal(a, b)
+    # against the general per-block path (ChunkedTables) on the same areas
+    from paper_2204_14194_b200 import fase_extrapolate_batch
+    from paper_2204_14194_b200 import workloads as wl
+
+    signals, masks = wl.frame_areas(img, lost, corners.cpu().numpy(), mb, sup)
+    res = fase_extrapolate_batch(signals, masks, d, None, cfg, device=dev)
+    same = (res.selected == outs["none"][0]).all(dim=1)
+    assert int(same.sum()) >= len(same) - 1
+    dc = (res.coefficients - outs["none"][1]).abs().amax(dim=1) / res.coefficients.abs().amax(dim=1)
+    assert float(dc[same].max()) < 1e-12
 
 
 def test_frame_widen_kernel():
