@@ -324,13 +324,24 @@ def measured_peaks():
 
 
 def measured_l2():
-    """(GB/s, source): L2 -> SM read bandwidth measured on this pool's B200 with
-    tools/probes/l2_probe.cu (best over L2-resident buffer sizes), or None."""
+    """(GB/s, lts__throughput % at that rate, source): the L2 -> SM read
+    bandwidth measured on this pool's B200 with tools/probes/l2_probe.cu, taken
+    under ncu in round 2 (profiles/r02_l2_peak_ncu.json: the probe's best
+    L2-resident stream registers ~54.4% lts__throughput, the reachable ceiling),
+    else the round-1 plain run; None if neither exists."""
+    q = ROOT / "profiles" / "r02_l2_peak_ncu.json"
+    try:
+        s = json.loads(q.read_text())["summary"]
+        return (s["l2_read_peak_gbs"], s["at_lts_throughput_pct"],
+                "tools/probes/l2_probe.cu under ncu (profiles/r02_l2_peak_ncu.json): lts__t_sectors_op_read "
+                "bytes / time of the best L2-resident read stream")
+    except (OSError, ValueError, KeyError):
+        pass
     q = ROOT / "profiles" / "r01_l2_peak.json"
     try:
         res = json.loads(q.read_text())["results"]
         best = max(r["read_gbs"] for r in res if r["mb"] <= 96)
-        return best, "tools/probes/l2_probe.cu: ld.global.cg 16-byte reads of L2-resident buffers"
+        return best, None, "tools/probes/l2_probe.cu: ld.global.cg 16-byte reads of L2-resident buffers"
     except (OSError, ValueError, KeyError):
         return None
 
@@ -361,16 +372,31 @@ def ncu_profile(kernel: str, tag: str):
     return keep or None
 
 
-def l2_roofline(achieved_gbs):
+def l2_roofline(achieved_gbs, prof=None, warps_per_block=None, blocks=None, iters=None):
     """The recursion's row stream against the measured L2 read bandwidth: with
-    most rows L2 hits (ncu), L2 -> SM bandwidth, not HBM, bounds the kernel."""
+    most rows L2 hits, L2 -> SM bandwidth, not HBM, bounds the kernel. ``prof``
+    (the committed ncu counters of the same kernel) adds the ncu-side
+    fractions: its lts__throughput over the probe's, and its L2 -> SM crossbar
+    bytes (= the algorithmic row bytes) at ncu's own duration."""
     m = measured_l2()
     if m is None:
         return None
-    peak, src = m
-    return {"bound": "l2", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
-            "frac": achieved_gbs / peak, "peak_source": src,
-            "note": "same algorithmic bytes as roofline (one table row per block-iteration)"}
+    peak, probe_lts, src = m
+    out = {"bound": "l2", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+           "frac": achieved_gbs / peak, "peak_source": src,
+           "note": "same algorithmic bytes as roofline (one table row per block-iteration)"}
+    if prof:
+        if prof.get("lts_throughput_pct") and probe_lts:
+            out["ncu_lts_throughput_pct"] = prof["lts_throughput_pct"]
+            out["probe_lts_throughput_pct"] = probe_lts
+            out["ncu_frac_of_probe"] = prof["lts_throughput_pct"] / probe_lts
+        if prof.get("xbar_read_bytes_per_launch") and prof.get("duration_ms"):
+            out["ncu_xbar_read_gbs"] = prof["xbar_read_bytes_per_launch"] / (prof["duration_ms"] * 1e-3) / 1e9
+            out["ncu_xbar_frac"] = out["ncu_xbar_read_gbs"] / peak
+        if prof.get("warp_instructions") and warps_per_block and blocks and iters:
+            out["warp_instructions_per_warp_iteration"] = (
+                prof["warp_instructions"] / (warps_per_block * blocks * iters))
+    return out
 
 
 def ozaki_roofline(plan, flops_fp64, seconds, fp64_peak, fp64_src):
@@ -706,7 +732,7 @@ def run_gpu(args):
                            "comes over PCIe)"},
             "roofline": roofline_recursion(achieved, hbm, hsrc, kname, tag, recursion, bytes_iter,
                                            it_s, cplx, B, I),
-            "roofline_l2": l2_roofline(achieved),
+            "roofline_l2": l2_roofline(achieved, ncu_profile(kname, tag), 8, B, I),
             "roofline_init": (ozaki_roofline(plan, flops_init, init_s, fp64, fsrc)
                               if plan._ozaki is not None else
                               {"bound": "tensor", "kernel": "dgemm_nt_kernel (DMMA FP64)"

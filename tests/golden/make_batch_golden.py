@@ -11,7 +11,9 @@ The unmodified reference (``/root/reference/pkg/src``) runs ``fase_extrapolate``
 - c4: blocks 0..255 of the config-4 batch (shared table);
 - c3: 256 of the 25,920 frame blocks, every edge / corner / neighbour-loss class
   first, then an even stride over the frame (per-block tables);
-- c2: 128 of the 804 frame blocks, chosen the same way.
+- c2: 128 of the 804 frame blocks, chosen the same way;
+- dft1: blocks 0..255 of the config-1 batch with the reference's default
+  (complex) dictionary ``dft`` (K = 2304; complex coefficients).
 
 Per block it stores the selected sequence (int16), the coefficients, the
 reconstructed lost samples (mask order) and the reference's NEAR-TIE SETS: for
@@ -107,8 +109,8 @@ def _block(args):
         model, trace = fase.fase_extrapolate(signal, mask, d, tables, cfg, record_products=True)
         patched, _ = fase.apply_model(signal, model, mask)
         ties = near_ties(r0, trace.products, tables.d, trace.selected)
-    return (i, np.asarray(trace.selected, dtype=np.int16), trace.coefficients.real.copy(),
-            patched[mask].copy(), ties)
+    coef = trace.coefficients if _G.get("complex") else trace.coefficients.real.copy()
+    return (i, np.asarray(trace.selected, dtype=np.int16), coef, patched[mask].real.copy(), ties)
 
 
 def _run(jobs, procs):
@@ -140,21 +142,21 @@ def _pack(name, blocks, results, extra):
             "iterations": int(sel.size), "file": f"{name}_batch.npz"}
 
 
-def shared_batch(cid: int, n_blocks: int, procs: int):
+def shared_batch(cid: int, n_blocks: int, procs: int, spec: str | None = None, name=None):
     w = wl.WORKLOADS[cid]
     m, n = w.area
-    d = ref_dictionary(w.dict_spec, m, n)
+    d = ref_dictionary(spec or w.dict_spec, m, n)
     mask = wl.central_loss_mask(m, n, *w.loss)
     cfg = fase.ExtrapConfig(w.config.iterations, w.config.gamma, w.config.rho_hat)
     t0 = time.time()
     tables = fase.build_gram_tables(d, fase.build_weight_field(mask, cfg.rho_hat))
     t_tab = time.time() - t0
-    _G.update(d=d, cfg=cfg, tables=tables)
+    _G.update(d=d, cfg=cfg, tables=tables, complex=bool(spec) and not np.isrealobj(d.values))
     sig = wl.block_signals(cid, n_blocks, m, n)
     blocks = list(range(n_blocks))
     t0 = time.time()
     res = _run([(i, sig[b], mask) for i, b in enumerate(blocks)], procs)
-    rec = _pack(f"c{cid}", blocks, res, {"provenance": np.uint64(tables.provenance)})
+    rec = _pack(name or f"c{cid}", blocks, res, {"provenance": np.uint64(tables.provenance)})
     rec.update(table_seconds=t_tab, seconds=time.time() - t0)
     _G.clear()
     return rec
@@ -213,7 +215,7 @@ def frame_batch(cid: int, picks: int, procs: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--procs", type=int, default=mp.cpu_count())
-    ap.add_argument("--only", default="c1,c4,c3,c2")
+    ap.add_argument("--only", default="c1,c4,c3,c2,dft1")
     args = ap.parse_args()
     todo = args.only.split(",")
     meta_path = HERE / "batch_golden.json"
@@ -233,6 +235,9 @@ def main():
     if "c2" in todo:
         meta["c2"] = frame_batch(2, 128, args.procs)
         print("c2", meta["c2"], flush=True)
+    if "dft1" in todo:  # the reference's default dictionary on the config-1 batch
+        meta["dft1"] = shared_batch(1, 256, args.procs, spec="dft", name="dft1")
+        print("dft1", meta["dft1"], flush=True)
     meta_path.write_text(json.dumps(meta, indent=1))
 
 

@@ -171,3 +171,33 @@ def test_frame_batch_against_reference(cid):
     counts["classes_covered"] = int(len({tuple(c) for c in z["classes"]}))
     _report(f"c{cid}-frame", counts)
     _check(counts)
+
+
+@pytest.mark.parametrize("recursion", ["exact", "scaled"])
+def test_dft_batch_against_reference(recursion):
+    """The reference's default (complex) dictionary ``dft`` on the config-1
+    batch (bench.py --dict dft): 1,024 blocks through ExtrapolationPlan, the
+    first 256 pinned by the reference (complex coefficients)."""
+    import torch
+
+    from paper_2204_14194_b200 import (ExtrapolationPlan, build_gram_tables, build_weight_field,
+                                       parse_dict_spec)
+
+    z = np.load(GOLD / "dft1_batch.npz")
+    w = wl.WORKLOADS[1]
+    dev = torch.device("cuda", 0)
+    d = parse_dict_spec("dft", *w.area)
+    mask = wl.central_loss_mask(*w.area, *w.loss)
+    tables = build_gram_tables(d, build_weight_field(mask, w.config.rho_hat), device=dev)
+    assert int(tables.provenance) == int(z["provenance"])
+    plan = ExtrapolationPlan(d, mask, w.n_blocks, w.config, tables, device=dev,
+                             recursion=recursion)
+    sig = torch.from_numpy(wl.block_signals(1, w.n_blocks, *w.area)).to(dev)
+    plan.run(sig)
+    torch.cuda.synchronize()
+    lost = plan.lost.cpu().numpy()
+    counts = classify(plan.selected.cpu().numpy(), plan.coefficients.cpu().numpy(), z,
+                      got_lost=lambda i, r: lost[r, : plan.n_lost])
+    counts["recursion"] = recursion
+    _report(f"dft1-{recursion}", counts)
+    _check(counts)

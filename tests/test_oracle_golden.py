@@ -240,9 +240,9 @@ def test_batch_fixtures_pin_oracle_c3(golden_dir):
 def test_batch_fixture_structure(golden_dir, meta):
     """Every batch fixture covers the blocks the verdict asks for; the near-tie
     sets contain the reference's own selection at that iteration."""
-    want = {1: 1024, 4: 256, 3: 256, 2: 128}
-    for cid, n in want.items():
-        z = np.load(golden_dir / f"c{cid}_batch.npz")
+    want = {"c1": (1024, 1), "c4": (256, 4), "c3": (256, 3), "c2": (128, 2), "dft1": (256, 1)}
+    for name, (n, cid) in want.items():
+        z = np.load(golden_dir / f"{name}_batch.npz")
         assert len(z["blocks"]) == n and z["selected"].shape == (n, wl.WORKLOADS[cid].config.iterations)
         ties = {}
         for i, t, k in z["ties"]:

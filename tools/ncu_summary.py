@@ -25,6 +25,8 @@ METRICS = [
     ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
     ("l1tex__t_sector_hit_rate.pct", "L1 hit rate"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput % peak"),
+    ("lts__t_bytes.sum", "L2 slice traffic (`lts__t_bytes`)"),
+    ("l1tex__m_xbar2l1tex_read_bytes.sum", "L2 -> SM read bytes over the crossbar"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % peak"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % peak"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active %"),
@@ -112,9 +114,20 @@ def main():
             traffic = to_bytes(row["dram__bytes_read.sum"], unit["dram__bytes_read.sum"]) + \
                 to_bytes(row["dram__bytes_write.sum"], unit["dram__bytes_write.sum"])
             tag = Path(out).name.split("_ncu_")[-1]  # e.g. profiles/r01_ncu_c1 -> c1
-            js[f"{tag}/{short(name)}"] = {"dram_bytes_per_launch": traffic, "report": Path(rep).name,
-                               "duration_ms": float(row["gpu__time_duration.sum"].replace(",", "")) *
-                               (1e-3 if unit["gpu__time_duration.sum"] == "us" else 1.0)}
+            rec = {"dram_bytes_per_launch": traffic, "report": Path(rep).name,
+                   "duration_ms": float(row["gpu__time_duration.sum"].replace(",", "")) *
+                   (1e-3 if unit["gpu__time_duration.sum"] == "us" else 1.0)}
+            for key, field in (("l1tex__m_xbar2l1tex_read_bytes.sum", "xbar_read_bytes_per_launch"),
+                               ("lts__t_bytes.sum", "lts_bytes_per_launch")):
+                if row.get(key):
+                    rec[field] = to_bytes(row[key], unit[key])
+            for key, field in (("lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts_throughput_pct"),
+                               ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_active_pct"),
+                               ("smsp__inst_executed.sum", "warp_instructions"),
+                               ("lts__t_sector_hit_rate.pct", "l2_hit_pct")):
+                if row.get(key):
+                    rec[field] = float(row[key].replace(",", ""))
+            js[f"{tag}/{short(name)}"] = rec
     if launches:
         lines.append("## launch list (cold-cache, serialised: compare shares, not absolutes)")
         lines.append("")
