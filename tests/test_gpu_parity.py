@@ -263,7 +263,10 @@ def test_recursion_scaled_matches_exact_full_config1():
     torch.cuda.synchronize()
     assert torch.equal(px.R0, ps.R0)
     same = (px.selected == ps.selected).all(dim=1)
-    assert int(same.sum()) >= w8.n_blocks - 2
+    # every block identical (measured); a divergence must be a legitimate
+    # near-tie against the reference, which tests/test_gpu_batch_parity.py
+    # checks block by block on this same batch
+    assert int(same.sum()) == w8.n_blocks
     dev_c = ((px.coefficients - ps.coefficients).abs().amax(dim=1)
              / px.coefficients.abs().amax(dim=1))
     assert float(dev_c[same].max()) < 1e-12
