@@ -76,6 +76,10 @@ def parse_args():
                          "scaled for real dictionaries")
     ap.add_argument("--compose", default=None, choices=["none", "singles", "pairs", "triples"],
                     help="frame configs: precomposed base tables (default: the engine's)")
+    ap.add_argument("--l2-hint", default="off", choices=["on", "off"],
+                    help="shared-geometry recursion: L2 residency hint for the most frequently "
+                         "selected rows, tuned on a separate (never timed) batch (measured: "
+                         "L2 hits 67 -> 74%%, DRAM reads -17%%, no speed-up; off by default)")
     ap.add_argument("--dict", default=None,
                     help="override the dictionary spec of a shared-geometry config (0, 1, 4), "
                          "e.g. 'dft' (the reference's default, complex-valued)")
@@ -430,13 +434,13 @@ def ozaki_roofline(plan, flops_fp64, seconds, fp64_peak, fp64_src):
                     "of the batch"}
 
 
-def parity_vs_reference(cid, sel, coef, lost, n_lost):
+def parity_vs_reference(cid, sel, coef, lost, n_lost, name=None):
     """Classify the timed outputs against the reference-written batch fixture
-    (tests/golden/c{cid}_batch.npz, make_batch_golden.py) after the clock:
+    (tests/golden/<name or c{cid}>_batch.npz, make_batch_golden.py) after the clock:
     identical sequences, legitimate near-tie stops (the GPU's atom is one the
     reference's tie rule could pick under a 1e-9 relative Delta-E change),
     failures; coefficient / lost-sample deviation on the run scale."""
-    p = ROOT / "tests" / "golden" / f"c{cid}_batch.npz"
+    p = ROOT / "tests" / "golden" / f"{name or f'c{cid}'}_batch.npz"
     if not p.exists():
         return None
     z = np.load(p)
@@ -578,6 +582,21 @@ def run_gpu(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    # L2 residency hint: the rows a separate batch (blocks 2*B_total + ..., never
+    # timed) selects most often are copied evict_last, the others evict_first
+    l2_hint = None
+    if args.l2_hint == "on" and not cplx:
+        tune = torch.from_numpy(wl.block_signals(args.config, B, *w.area,
+                                                 first=2 * B_total + lo)).to(dev)
+        plan.run(tune)
+        torch.cuda.synchronize()
+        n_hot = plan.tune_l2(plan.selected)
+        G_ = plan.Gs if plan.Gs is not None else plan.G
+        l2_hint = {"hot_rows": n_hot, "hot_bytes": n_hot * G_.shape[1] * 8,
+                   "hot_share_of_tuning_selections": plan.l2_hot_share,
+                   "tuned_on": f"blocks {2 * B_total + lo}..{2 * B_total + lo + B - 1} (never timed)",
+                   "policy": "staged-row TMA copies: hot rows L2::evict_last, others L2::evict_first"}
+        del tune
     for _ in range(max(args.warmup, 0)):
         sb.run(dev_sig)
     sb.run_host_stream([host, host2] * max(args.warmup, 1), harena * max(args.warmup, 1))
@@ -658,9 +677,10 @@ def run_gpu(args):
     assert int(sel.min()) >= 0 and int(sel.max()) < K, "selection out of range"
     assert torch.isfinite(plan.lost).all(), "non-finite reconstruction"
     parity = None
-    if sb.is_root and not args.dict:
+    fixture = None if not args.dict else ("dft1" if args.dict == "dft" and args.config == 1 else "")
+    if sb.is_root and fixture != "":
         g_sel, g_coef, g_lost = (x.cpu().numpy() for x in sb.arena.assemble(0))
-        parity = parity_vs_reference(args.config, g_sel, g_coef, g_lost, plan.n_lost)
+        parity = parity_vs_reference(args.config, g_sel, g_coef, g_lost, plan.n_lost, fixture)
         if parity is not None and parity["failure"]:
             raise RuntimeError(f"timed outputs diverge from the reference: {parity}")
     agreement = None
@@ -755,6 +775,7 @@ def run_gpu(args):
             "products": plan.products_method,
             "recursion": recursion,
             "fused_synth": plan.fused_synth,
+            "l2_hint": l2_hint,
             "parity_vs_reference": parity,
             "recursion_agreement": agreement,
             "stage_ms": {"init_products": float(np.mean(init_ms)), "iterate": float(np.mean(iter_ms)),

@@ -226,6 +226,11 @@ typedef struct {
   int n_compose;
   int compose_depth;
   int64_t base_stride;
+  /* optional L2 residency hint (shared geometries): bit u of l2_hot[u / 32] set
+   * = row u is "hot" (frequently selected): its staged-row copies carry an
+   * L2 evict_last policy, every other row evict_first, so the hot rows stay
+   * L2-resident. NULL: default policy. Does not change any result. */
+  const uint32_t* l2_hot;
 } fase_iterate_args;
 
 FASE_API int fase_iterate(const fase_iterate_args* args, void* stream);

@@ -69,6 +69,7 @@ class IterateArgs(ctypes.Structure):
         ("ldr", _i64), ("R_out", _vp), ("R_log", _vp), ("K", _i32), ("B", _i32), ("I", _i32),
         ("gamma", _f64), ("sel", _vp), ("proj", _vp), ("coef", _vp), ("ldo", _i64),
         ("compose", _vp), ("n_compose", _i32), ("compose_depth", _i32), ("base_stride", _i64),
+        ("l2_hot", _vp),
     ]
 
 
@@ -291,9 +292,21 @@ def block_normalizers(G0, chunk_tables, chunk_stride: int, chunk_count, chunk_id
                                       _ptr(D), _ld(D), _ptr(n_alive), _stream(D)))
 
 
+def _hot_ptr(l2_hot, K: int):
+    """Device pointer of an L2 hot-row mask (int32 words, bit u of word u // 32), or None."""
+    import torch
+
+    if l2_hot is None:
+        return None
+    _require(l2_hot, "l2_hot", torch.int32, 1)
+    if l2_hot.numel() * 32 < K:
+        raise errors.ShapeError(f"l2_hot holds {l2_hot.numel() * 32} bits, K = {K}")
+    return _ptr(l2_hot)
+
+
 def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *,
             chunk_tables=None, chunk_stride: int = 0, chunk_count=None, chunk_ids=None,
-            R_out=None, R_log=None, compose=None, base_stride: int = 0) -> None:
+            R_out=None, R_log=None, compose=None, base_stride: int = 0, l2_hot=None) -> None:
     """The recursion (fase_iterate). ``compose`` (int32 device table n^depth,
     depth 1..3) with ``base_stride`` selects precomposed base tables at
     G0 + p * base_stride for the longest prefix of each block's chunk list."""
@@ -314,7 +327,8 @@ def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *
         R_log=_ptr(R_log), K=K, B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel),
         proj=_ptr(proj), coef=_ptr(coef), ldo=_ld(sel), compose=_ptr(compose),
         n_compose=compose.shape[0] if compose is not None else 0,
-        compose_depth=compose.dim() if compose is not None else 0, base_stride=base_stride)
+        compose_depth=compose.dim() if compose is not None else 0, base_stride=base_stride,
+        l2_hot=_hot_ptr(l2_hot, K))
     if compose is not None:
         _require(compose, "compose", torch.int32)
         if compose.dim() > 3 or any(x != compose.shape[0] for x in compose.shape):
@@ -366,7 +380,7 @@ def iterate_complex_scaled(Gs, D, R0, K: int, iterations: int, gamma: float, sel
     _require(coef, "coef", torch.complex128, 2)
     args = IterateArgs(G0=_ptr(Gs), ldg=_ld(Gs), D=_ptr(D), ldd=0, R0=_ptr(R0), ldr=_ld(R0), K=K,
                        B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel), proj=_ptr(proj),
-                       coef=_ptr(coef), ldo=_ld(sel))
+                       coef=_ptr(coef), ldo=_ld(sel), l2_hot=_hot_ptr(l2_hot, K))
     if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
         raise errors.ShapeError("sel / proj / coef must share one leading dimension")
     _check(lib.fase_iterate_complex_scaled(ctypes.byref(args), _stream(R0)))
@@ -378,7 +392,7 @@ def scaled_synth_capacity(K: int, B: int) -> int:
 
 
 def iterate_scaled(Gs, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *,
-                   phi_lost=None, n_lost: int = 0, lost=None) -> None:
+                   phi_lost=None, n_lost: int = 0, lost=None, l2_hot=None) -> None:
     """The scaled recursion (fase_iterate_scaled) over a column-scaled shared
     table ``Gs`` (scale_columns); R0 and D unscaled, as for ``iterate``.
     With ``phi_lost`` (K, ld) and ``lost`` (B, >= n_lost) the synthesis of the
@@ -394,7 +408,7 @@ def iterate_scaled(Gs, D, R0, K: int, iterations: int, gamma: float, sel, proj, 
     _require(coef, "coef", torch.float64, 2)
     args = IterateArgs(G0=_ptr(Gs), ldg=_ld(Gs), D=_ptr(D), ldd=0, R0=_ptr(R0), ldr=_ld(R0), K=K,
                        B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel), proj=_ptr(proj),
-                       coef=_ptr(coef), ldo=_ld(sel))
+                       coef=_ptr(coef), ldo=_ld(sel), l2_hot=_hot_ptr(l2_hot, K))
     if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
         raise errors.ShapeError("sel / proj / coef must share one leading dimension")
     syn = None

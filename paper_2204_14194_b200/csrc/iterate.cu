@@ -367,12 +367,18 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       // fused synthesis: the predicted atom's phi row rides on the last segment
       const unsigned phi_bytes =
           SYN > 0 ? static_cast<unsigned>((syn.n_lost * sizeof(double) + 15) & ~size_t{15}) : 0u;
+      // L2 residency hint: hot rows evict_last, the rest evict_first
+      const bool hint = !kChunked && a.l2_hot != nullptr;
+      const uint64_t pol = hint ? l2_policy((__ldg(a.l2_hot + (guess >> 5)) >> (guess & 31)) & 1u) : 0ull;
 #pragma unroll
       for (int sg = 0; sg < kSeg; ++sg) {
         const int j0 = sg * EP / kSeg, j1 = (sg + 1) * EP / kSeg;
         const unsigned bytes = static_cast<unsigned>((j1 - j0) * NT * sizeof(double2));
         mbar_arrive_expect_tx(&s_bar[sg], bytes + (sg == kSeg - 1 ? phi_bytes : 0u));
-        tma_load_1d(s_row + j0 * NT, grow + 2 * j0 * NT, bytes, &s_bar[sg]);
+        if (hint)
+          tma_load_1d_hint(s_row + j0 * NT, grow + 2 * j0 * NT, bytes, &s_bar[sg], pol);
+        else
+          tma_load_1d(s_row + j0 * NT, grow + 2 * j0 * NT, bytes, &s_bar[sg]);
         if (SYN > 0 && sg == kSeg - 1)
           tma_load_1d(s_phi, syn.phi + static_cast<int64_t>(guess) * syn.ldphi, phi_bytes,
                       &s_bar[sg]);
@@ -803,12 +809,22 @@ extern "C" int fase_table_ld(int K) {
   return v ? v->nt * v->ept : 0;
 }
 
+namespace {
+// FASE_L2_HINT=0 drops the L2 residency hint (measurement)
+fase_iterate_args hint_policy(const fase_iterate_args& in) {
+  fase_iterate_args a = in;
+  const char* env = getenv("FASE_L2_HINT");
+  if (env && env[0] == '0') a.l2_hot = nullptr;
+  return a;
+}
+}  // namespace
+
 extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
   if (!args) {
     set_error("fase_iterate: null argument block");
     return FASE_ERR_PARAMETER;
   }
-  const fase_iterate_args& a = *args;
+  const fase_iterate_args a = hint_policy(*args);
   if (a.K < 1 || a.B < 0 || a.I < 1) {
     set_error("fase_iterate: bad sizes (K=%d, B=%d, I=%d)", a.K, a.B, a.I);
     return FASE_ERR_SHAPE;
@@ -932,7 +948,7 @@ extern "C" int fase_iterate_scaled(const fase_iterate_args* args, const fase_syn
     set_error("fase_iterate_scaled: null argument block");
     return FASE_ERR_PARAMETER;
   }
-  const fase_iterate_args& a = *args;
+  const fase_iterate_args a = hint_policy(*args);
   if (a.K < 1 || a.B < 0 || a.I < 1) {
     set_error("fase_iterate_scaled: bad sizes (K=%d, B=%d, I=%d)", a.K, a.B, a.I);
     return FASE_ERR_SHAPE;

@@ -886,6 +886,33 @@ class ExtrapolationPlan:
             flags[row0: row0 + rre.shape[0] * cre.shape[0]] = False
         return flags
 
+    def tune_l2(self, selected, fraction: float = 0.5):
+        """L2 residency hint from a previous batch's selections (host work, once):
+        the most frequently selected atoms whose table rows fill ``fraction`` of
+        the L2 are marked hot; the recursion copies their rows with an L2
+        evict_last policy and every other row evict_first
+        (``fase_iterate_args.l2_hot``). Results are unchanged (a cache hint).
+        ``selected``: (B', I) int32 selections (host or device); None clears."""
+        torch = _torch()
+        if selected is None:
+            self.l2_hot = None
+            self.l2_hot_rows = 0
+            return 0
+        sel = np.asarray(selected.cpu() if hasattr(selected, "cpu") else selected).ravel()
+        sel = sel[(sel >= 0) & (sel < self.K)]
+        counts = np.bincount(sel, minlength=self.K)
+        G = self.Gs if self.Gs is not None else self.G
+        row_bytes = G.shape[1] * G.element_size()
+        l2 = torch.cuda.get_device_properties(self.device).L2_cache_size
+        n_hot = min(int(fraction * l2 // row_bytes), int((counts > 0).sum()))
+        hot = np.argsort(-counts, kind="stable")[:n_hot]
+        words = np.zeros((self.K + 31) // 32, dtype=np.uint32)
+        np.bitwise_or.at(words, hot // 32, (np.uint32(1) << (hot % 32).astype(np.uint32)))
+        self.l2_hot = torch.from_numpy(words.view(np.int32)).to(self.device)
+        self.l2_hot_rows = int(n_hot)
+        self.l2_hot_share = float(counts[hot].sum() / max(counts.sum(), 1))
+        return n_hot
+
     def _iterate_synth(self, sel, proj, coef, lost, slot: int = 0):
         sc = self._scratch(slot)
         if self.complex:
@@ -900,17 +927,18 @@ class ExtrapolationPlan:
                                             n_shared=self.n_lost, dst=self.lost_pos,
                                             max_imag=sc["max_imag"])
             return
+        hot = getattr(self, "l2_hot", None)
         if self.fused_synth:
             _native.iterate_scaled(self.Gs, self.D, sc["R0"], self.K, self.I, self.config.gamma,
                                    sel, proj, coef, phi_lost=self.phi_lost, n_lost=self.n_lost,
-                                   lost=lost)
+                                   lost=lost, l2_hot=hot)
             return
         if self.Gs is not None:
             _native.iterate_scaled(self.Gs, self.D, sc["R0"], self.K, self.I, self.config.gamma,
-                                   sel, proj, coef)
+                                   sel, proj, coef, l2_hot=hot)
         else:
             _native.iterate(self.G, self.D, sc["R0"], self.K, self.I, self.config.gamma, sel,
-                            proj, coef)
+                            proj, coef, l2_hot=hot)
         if self.n_lost:
             _native.synth_paste(self.phi_lost, sel, coef, self.I, self.lost_seq, lost,
                                 n_shared=self.n_lost, dst=self.lost_pos)
