@@ -58,6 +58,12 @@ constexpr unsigned kNone = 0xffffffffu;
 #ifndef FASE_SCALED_CHAINS
 #define FASE_SCALED_CHAINS 1
 #endif
+// chunked recursion: runner-up rows prefetched into L2 (measurement knob; 0 by
+// default -- config 2 recursion 1.856 ms without, 1.896 / 2.034 / 2.232 ms with
+// 1 / 2 / 3 runners: the extra DRAM traffic evicts more than it saves)
+#ifndef FASE_RUNNER_PREFETCH
+#define FASE_RUNNER_PREFETCH 0
+#endif
 #ifdef FASE_ITERATE_STATS
 __device__ unsigned long long g_stats[8];  // measurement build: chunked-path counters
 #endif
@@ -316,6 +322,32 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       const unsigned bl = __reduce_max_sync(0xffffffffu, h == bh ? l : 0u);
       guess = __reduce_min_sync(0xffffffffu, (h == bh && l == bl) ? sa : kNone);
       top_key = (static_cast<long long>(bh) << 32) | bl;
+      if constexpr (kChunked && FASE_RUNNER_PREFETCH > 0) {
+        // Per-block geometries read their (composed) base rows mostly from
+        // DRAM. The next selection is often one of this iteration's runners-up
+        // (config 2: the runner-up 46%, one of the top two 62%): pull the rows
+        // of the best two other warps' maxima into L2 now, a whole iteration
+        // ahead (bulk prefetches: no registers or shared memory held).
+        if (warp == 0) {
+          unsigned prev = guess;
+#pragma unroll
+          for (int rr = 0; rr < FASE_RUNNER_PREFETCH; ++rr) {
+            const long long k2 = (sa == guess || sa == prev) ? LLONG_MIN : sk;
+            const int h2 = static_cast<int>(k2 >> 32);
+            const unsigned l2 = static_cast<unsigned>(k2);
+            const int b2 = __reduce_max_sync(0xffffffffu, h2);
+            const unsigned c2 = __reduce_max_sync(0xffffffffu, h2 == b2 ? l2 : 0u);
+            const unsigned r2 = __reduce_min_sync(0xffffffffu, (h2 == b2 && l2 == c2) ? sa : kNone);
+            if (b2 < 0 || r2 >= static_cast<unsigned>(K)) break;
+            if (lane == 0)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(
+                               G0b + static_cast<int64_t>(r2) * ldg),
+                           "r"(static_cast<unsigned>(EP * NT * sizeof(double2)))
+                           : "memory");
+            prev = r2;
+          }
+        }
+      }
     }
     if (top_key < 0) {  // every atom degenerate (NoSelectableAtomError): mark and stop
       for (int k = it + t; k < a.I; k += NT) {
