@@ -64,6 +64,9 @@ constexpr unsigned kNone = 0xffffffffu;
 #ifndef FASE_RUNNER_PREFETCH
 #define FASE_RUNNER_PREFETCH 0
 #endif
+#ifndef FASE_BASE_EVICT_FIRST  // chunked recursion: composed-base rows copied evict_first
+#define FASE_BASE_EVICT_FIRST 1
+#endif
 #ifdef FASE_ITERATE_STATS
 __device__ unsigned long long g_stats[8];  // measurement build: chunked-path counters
 #endif
@@ -399,9 +402,16 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       // fused synthesis: the predicted atom's phi row rides on the last segment
       const unsigned phi_bytes =
           SYN > 0 ? static_cast<unsigned>((syn.n_lost * sizeof(double) + 15) & ~size_t{15}) : 0u;
-      // L2 residency hint: hot rows evict_last, the rest evict_first
-      const bool hint = !kChunked && a.l2_hot != nullptr;
-      const uint64_t pol = hint ? l2_policy((__ldg(a.l2_hot + (guess >> 5)) >> (guess & 31)) & 1u) : 0ull;
+      // L2 residency hint: hot rows evict_last, the rest evict_first. Per-block
+      // geometries: rows of a precomposed base (used by this block, or a few)
+      // stream through L2 evict_first so they do not displace the shared G0 rows
+      // (FASE_BASE_EVICT_FIRST 2: G0's own rows evict_last besides)
+      const bool composed = kChunked && FASE_BASE_EVICT_FIRST && G0b != a.G0;
+      const bool shared_g0 = kChunked && FASE_BASE_EVICT_FIRST == 2 && G0b == a.G0;
+      const bool hint = (!kChunked && a.l2_hot != nullptr) || composed || shared_g0;
+      const uint64_t pol =
+          kChunked ? l2_policy(shared_g0)
+                   : (hint ? l2_policy((__ldg(a.l2_hot + (guess >> 5)) >> (guess & 31)) & 1u) : 0ull);
 #pragma unroll
       for (int sg = 0; sg < kSeg; ++sg) {
         const int j0 = sg * EP / kSeg, j1 = (sg + 1) * EP / kSeg;

@@ -56,6 +56,9 @@ class SparseModel:
         return g
 
 
+_PINNED = {}  # (shape, dtype) -> pinned host staging buffer of BatchResult.to_host
+
+
 @dataclass
 class BatchResult:
     """Outcome of one batched run over B blocks (device tensors).
@@ -78,6 +81,33 @@ class BatchResult:
 
     def __len__(self) -> int:
         return int(self.selected.shape[0])
+
+    def to_host(self, fields=("selected", "coefficients", "patched")) -> dict:
+        """Host numpy copies of the named fields through reusable pinned staging
+        buffers (one per shape / dtype, kept across calls): a read-back at
+        PCIe rate instead of a pageable copy into fresh, page-faulting memory
+        (config 4's 134 MB of patched areas: 61 ms pageable). The arrays are
+        views of the staging buffers, valid until the next ``to_host`` with
+        the same shape and dtype; copy them to keep them longer."""
+        import torch
+
+        out, pending = {}, []
+        for name in fields:
+            t = getattr(self, name)
+            if t is None:
+                out[name] = None
+                continue
+            key = (tuple(t.shape), t.dtype)
+            buf = _PINNED.get(key)
+            if buf is None:
+                buf = _PINNED[key] = torch.empty(key[0], dtype=key[1], pin_memory=True)
+            buf.copy_(t, non_blocking=True)
+            pending.append((name, buf))
+        if pending:
+            torch.cuda.current_stream(self.selected.device).synchronize()
+        for name, buf in pending:
+            out[name] = buf.numpy()
+        return out
 
     def block(self, b: int) -> tuple[SparseModel, IterationTrace]:
         """Per-block reference-style (model, trace) pair (host copies)."""

@@ -13,7 +13,11 @@ The unmodified reference (``/root/reference/pkg/src``) runs ``fase_extrapolate``
   first, then an even stride over the frame (per-block tables);
 - c2: 128 of the 804 frame blocks, chosen the same way;
 - dft1: blocks 0..255 of the config-1 batch with the reference's default
-  (complex) dictionary ``dft`` (K = 2304; complex coefficients).
+  (complex) dictionary ``dft`` (K = 2304; complex coefficients);
+- c4all / c2all / c3all: EVERY block of the config-4 batch / config-2 frame /
+  config-3 frame, selected sequences and near-tie sets only (coefficients and
+  samples are pinned on the samples above). Not in the default --only list
+  for c3all (about 25 minutes on 8 cores).
 
 Per block it stores the selected sequence (int16), the coefficients, the
 reconstructed lost samples (mask order) and the reference's NEAR-TIE SETS: for
@@ -121,9 +125,17 @@ def _run(jobs, procs):
     return out
 
 
-def _pack(name, blocks, results, extra):
+def _pack(name, blocks, results, extra, selections_only=False):
     n = len(blocks)
     sel = np.stack([r[1] for r in results])
+    if selections_only:  # whole batches: the selected sequences and near-tie sets only
+        ties = np.array([(i, t, k) for i, r in enumerate(results) for t, k in r[4]],
+                        dtype=np.int32).reshape(-1, 3)
+        np.savez_compressed(HERE / f"{name}_batch.npz", blocks=np.asarray(blocks, dtype=np.int32),
+                            selected=sel, ties=ties, **extra)
+        return {"blocks": n, "iterations": int(sel.size), "selections_only": True,
+                "tie_iterations": len({(int(a), int(b)) for a, b, _ in ties}) if len(ties) else 0,
+                "file": f"{name}_batch.npz"}
     coef = np.stack([r[2] for r in results])
     lost = [r[3] for r in results]
     nl = max(len(x) for x in lost)
@@ -142,7 +154,8 @@ def _pack(name, blocks, results, extra):
             "iterations": int(sel.size), "file": f"{name}_batch.npz"}
 
 
-def shared_batch(cid: int, n_blocks: int, procs: int, spec: str | None = None, name=None):
+def shared_batch(cid: int, n_blocks: int, procs: int, spec: str | None = None, name=None,
+                 selections_only=False):
     w = wl.WORKLOADS[cid]
     m, n = w.area
     d = ref_dictionary(spec or w.dict_spec, m, n)
@@ -156,7 +169,8 @@ def shared_batch(cid: int, n_blocks: int, procs: int, spec: str | None = None, n
     blocks = list(range(n_blocks))
     t0 = time.time()
     res = _run([(i, sig[b], mask) for i, b in enumerate(blocks)], procs)
-    rec = _pack(name or f"c{cid}", blocks, res, {"provenance": np.uint64(tables.provenance)})
+    rec = _pack(name or f"c{cid}", blocks, res, {"provenance": np.uint64(tables.provenance)},
+                selections_only)
     rec.update(table_seconds=t_tab, seconds=time.time() - t0)
     _G.clear()
     return rec
@@ -179,7 +193,7 @@ def block_classes(case, masks):
     return keys
 
 
-def frame_batch(cid: int, picks: int, procs: int):
+def frame_batch(cid: int, picks: int, procs: int, name=None, selections_only=False):
     w = wl.WORKLOADS[cid]
     case = wl.frame_case(w)
     signals, masks = wl.frame_areas(case.damaged(), case.lost, case.corners, case.mb, case.support)
@@ -190,7 +204,7 @@ def frame_batch(cid: int, picks: int, procs: int):
     chosen = []
     for rnd in range(3):  # one block of every class, then a second, then a third
         chosen += [v[rnd] for v in by_class.values() if len(v) > rnd]
-    chosen = chosen[:picks]
+    chosen = chosen[:picks] if picks < len(keys) else list(range(len(keys)))
     taken = set(chosen)
     rest = [i for i in range(len(keys)) if i not in taken]
     need = picks - len(chosen)
@@ -203,9 +217,10 @@ def frame_batch(cid: int, picks: int, procs: int):
     _G.update(d=d, cfg=cfg, tables=None)
     t0 = time.time()
     res = _run([(i, signals[b], masks[b]) for i, b in enumerate(blocks)], procs)
-    rec = _pack(f"c{cid}", blocks, res, {"n_blocks": np.int64(len(masks)),
-                                         "classes": np.asarray([keys[b] for b in blocks],
-                                                               dtype=np.int32)})
+    rec = _pack(name or f"c{cid}", blocks, res, {"n_blocks": np.int64(len(masks)),
+                                                 "classes": np.asarray([keys[b] for b in blocks],
+                                                                       dtype=np.int32)},
+                selections_only)
     rec.update(seconds=time.time() - t0, classes=len(set(keys)),
                classes_covered=len({keys[b] for b in blocks}))
     _G.clear()
@@ -215,7 +230,7 @@ def frame_batch(cid: int, picks: int, procs: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--procs", type=int, default=mp.cpu_count())
-    ap.add_argument("--only", default="c1,c4,c3,c2,dft1")
+    ap.add_argument("--only", default="c1,c4,c3,c2,dft1,c4all,c2all")
     args = ap.parse_args()
     todo = args.only.split(",")
     meta_path = HERE / "batch_golden.json"
@@ -235,6 +250,14 @@ def main():
     if "c2" in todo:
         meta["c2"] = frame_batch(2, 128, args.procs)
         print("c2", meta["c2"], flush=True)
+    if "c4all" in todo:  # every block of the config-4 batch: selections + near-tie sets
+        meta["c4all"] = shared_batch(4, wl.WORKLOADS[4].n_blocks, args.procs, name="c4all",
+                                     selections_only=True)
+        print("c4all", meta["c4all"], flush=True)
+    for cid, key in ((2, "c2all"), (3, "c3all")):  # every frame block: selections + ties
+        if key in todo:
+            meta[key] = frame_batch(cid, 10 ** 9, args.procs, name=key, selections_only=True)
+            print(key, meta[key], flush=True)
     if "dft1" in todo:  # the reference's default dictionary on the config-1 batch
         meta["dft1"] = shared_batch(1, 256, args.procs, spec="dft", name="dft1")
         print("dft1", meta["dft1"], flush=True)

@@ -239,3 +239,22 @@ def test_frame_widen_kernel():
         out = torch.full((h, w), -1.0, dtype=torch.float64, device=dev)
         _native.frame_widen(torch.from_numpy(img).to(dev), torch.from_numpy(lost).to(dev), out)
         assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_batch_result_to_host_pinned():
+    """BatchResult.to_host: host copies through reusable pinned buffers equal
+    the plain read-back."""
+    import torch
+
+    from paper_2204_14194_b200 import fase_extrapolate_batch
+
+    d = parse_dict_spec("union:dct+wht", 8, 8)
+    mask = central_loss_mask(8, 8, 4, 4)
+    sig = np.random.default_rng(5).uniform(0, 255, (7, 8, 8))
+    res = fase_extrapolate_batch(sig, mask, d, None, ExtrapConfig(12), device=DEV)
+    for _ in range(2):  # second call reuses the staging buffers
+        h = res.to_host()
+        assert np.array_equal(h["selected"], res.selected.cpu().numpy())
+        assert np.array_equal(h["coefficients"], res.coefficients.cpu().numpy())
+        assert np.array_equal(h["patched"], res.patched.cpu().numpy())
+        assert torch.from_numpy(h["patched"]).is_pinned()
