@@ -380,7 +380,7 @@ def iterate_complex_scaled(Gs, D, R0, K: int, iterations: int, gamma: float, sel
     _require(coef, "coef", torch.complex128, 2)
     args = IterateArgs(G0=_ptr(Gs), ldg=_ld(Gs), D=_ptr(D), ldd=0, R0=_ptr(R0), ldr=_ld(R0), K=K,
                        B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel), proj=_ptr(proj),
-                       coef=_ptr(coef), ldo=_ld(sel), l2_hot=_hot_ptr(l2_hot, K))
+                       coef=_ptr(coef), ldo=_ld(sel))
     if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
         raise errors.ShapeError("sel / proj / coef must share one leading dimension")
     _check(lib.fase_iterate_complex_scaled(ctypes.byref(args), _stream(R0)))

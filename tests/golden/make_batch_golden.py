@@ -207,7 +207,7 @@ def frame_batch(cid: int, picks: int, procs: int, name=None, selections_only=Fal
     chosen = chosen[:picks] if picks < len(keys) else list(range(len(keys)))
     taken = set(chosen)
     rest = [i for i in range(len(keys)) if i not in taken]
-    need = picks - len(chosen)
+    need = min(picks, len(keys)) - len(chosen)
     if need > 0:
         chosen += [rest[j] for j in np.linspace(0, len(rest) - 1, need).astype(int)]
     blocks = sorted(set(chosen))
