@@ -961,6 +961,12 @@ def run_gpu_frame(args):
         parity = parity_vs_reference(args.config, g_sel, g_coef, None, 0)
         if parity is not None and parity["failure"]:
             raise RuntimeError(f"timed outputs diverge from the reference: {parity}")
+        every = parity_vs_reference(args.config, g_sel, g_coef, None, 0, f"c{args.config}all")
+        if every is not None:  # every block of the frame: selected sequences
+            if every["failure"]:
+                raise RuntimeError(f"timed selections diverge from the reference: {every}")
+            parity["all_blocks_selections"] = {k: every[k] for k in (
+                "fixture", "blocks_checked", "identical", "near_tie", "failure")}
     # kernel split of this rank's tiles, for the roofline
     b = engine._buffers(L)
     engine.run(damaged, grid, sf.local_corners, out=out)

@@ -180,6 +180,12 @@ def test_frame_batch_against_reference(cid):
     counts["classes_covered"] = int(len({tuple(c) for c in z["classes"]}))
     _report(f"c{cid}-frame", counts)
     _check(counts)
+    # every block of the frame: selected sequences vs the reference
+    za = np.load(GOLD / f"c{cid}all_batch.npz")
+    assert np.array_equal(za["blocks"], np.arange(len(corners_h)))
+    counts = classify(res.selected.cpu().numpy(), res.coefficients.cpu().numpy(), za)
+    _report(f"c{cid}all-frame", counts)
+    assert counts["failure"] == 0, f"non-tie divergences: {counts['failures']}"
 
 
 @pytest.mark.parametrize("recursion", ["exact", "scaled"])

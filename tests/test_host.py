@@ -301,3 +301,34 @@ def test_complex_signal_rejected_with_boundary_error():
         as_real_field(z + 1j)
     with pytest.raises(ShapeError):
         as_real_field(np.zeros(3))
+
+
+def test_bench_parity_classifier(golden_dir):
+    """bench.parity_vs_reference (the post-clock check of the timed outputs):
+    the reference's own outputs classify as identical; a swap at an iteration
+    with a near-tie set is a near-tie stop; any other swap is a failure."""
+    import bench
+
+    z = np.load(golden_dir / "c3_batch.npz")
+    n = int(z["n_blocks"])
+    I = z["selected"].shape[1]
+    sel = np.zeros((n, I), dtype=np.int32)
+    coef = np.zeros((n, I))
+    sel[z["blocks"]] = z["selected"]
+    coef[z["blocks"]] = z["coefficients"]
+    out = bench.parity_vs_reference(3, sel, coef, None, 0)
+    assert out["identical"] == len(z["blocks"]) and out["failure"] == 0
+    assert out["max_coef_rel_dev"] == 0.0
+    i, t, k = (int(x) for x in z["ties"][0])
+    want = int(z["selected"][i][t])
+    alt = next(int(kk) for ii, tt, kk in z["ties"] if ii == i and tt == t and kk != want)
+    s2 = sel.copy()
+    s2[z["blocks"][i], t] = alt
+    out = bench.parity_vs_reference(3, s2, coef, None, 0)
+    assert out["near_tie"] == 1 and out["failure"] == 0
+    tied = {(int(a), int(b)) for a, b, _ in z["ties"]}
+    j, tj = next((j, tt) for j in range(len(z["blocks"])) for tt in range(I) if (j, tt) not in tied)
+    s3 = sel.copy()
+    s3[z["blocks"][j], tj] = (int(z["selected"][j][tj]) + 1) % 2048
+    out = bench.parity_vs_reference(3, s3, coef, None, 0)
+    assert out["failure"] == 1
