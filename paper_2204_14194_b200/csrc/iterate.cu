@@ -67,6 +67,14 @@ constexpr unsigned kNone = 0xffffffffu;
 #ifndef FASE_BASE_EVICT_FIRST  // chunked recursion: composed-base rows copied evict_first
 #define FASE_BASE_EVICT_FIRST 1
 #endif
+// latency shapes: spare buffers for the runners-up's rows (measurement knob; 0
+// by default -- config 0 recursion 100.5 us without, 164 us with 3 spare
+// buffers: the speculative copies compete with the selected row for the one
+// SM's L2 -> shared-memory bandwidth, and warp 0's extra reductions sit on the
+// path to the second barrier)
+#ifndef FASE_SPEC
+#define FASE_SPEC 0
+#endif
 #ifdef FASE_ITERATE_STATS
 __device__ unsigned long long g_stats[8];  // measurement build: chunked-path counters
 #endif
@@ -100,12 +108,29 @@ __device__ unsigned long long g_stats[8];  // measurement build: chunked-path co
 // after every update, in selection order with the same mul-then-add as
 // fase_synth_paste (bit-identical output); the phi row of the predicted atom
 // arrives by TMA with the last table segment.
+//
+// SPEC > 0 (latency shapes: at most one block per SM): speculative row staging.
+// The next selection is usually one of this iteration's runners-up (the best
+// maxima of the other warps), so besides the selected row, SPEC spare buffers
+// receive the runners' rows a whole iteration ahead (one TMA each). When the
+// next iteration's predicted atom is already in a spare buffer, no copy is
+// issued and the update reads that buffer: the row's L2 round trip leaves the
+// critical path of a latency-bound block. Arithmetic is unchanged.
 template <int NT, int EPT, int MINB, bool kDsmem, bool kChunked, bool kRecord, int NB,
-          bool kScaled = false, int SYN = 0>
+          bool kScaled = false, int SYN = 0, int SPEC = 0>
 __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_iterate_args a,
                                                                      const fase_synth_fused syn) {
   constexpr int EP = EPT / 2;
   constexpr int NW = NT / 32;
+  static_assert(SPEC == 0 || (NB == 1 && !kChunked && !kRecord), "speculative staging: one "
+                "shared-geometry block per CTA");
+  constexpr int kSp = SPEC > 0 ? SPEC : 1;
+  __shared__ __align__(8) uint64_t s_sbar[kSp];   // SPEC: one mbarrier per spare buffer
+  __shared__ unsigned s_stag[kSp];                 // SPEC: atom held by each spare buffer
+  __shared__ unsigned s_sfill[kSp];                // SPEC: fills issued per spare buffer
+  __shared__ int s_use;                            // SPEC: spare buffer holding the guess, or -1
+  __shared__ unsigned s_upar;                      // SPEC: its mbarrier parity
+  __shared__ __align__(16) double s_sphi[SPEC > 0 && SYN > 0 ? SPEC : 1][SYN > 0 ? SYN * NT : 2];
   static_assert(NB == 1 || (kDsmem && !kChunked), "paired blocks share one D in shared memory");
   static_assert(!kScaled || (!kDsmem && !kChunked && !kRecord && NB == 1),
                 "the scaled recursion keeps no normalizers and has one block per CTA");
@@ -139,6 +164,8 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   uint64_t* s_bar = s_bar_all[half];
   double2* s_row = s_dyn + half * EP * NT;  // staged row: pair p at s_row[p]
   double2* s_D = s_dyn + NB * EP * NT;      // kDsmem: normalizer pairs, same indexing
+  // SPEC: spare row buffers k at s_spare + k * EP * NT
+  double2* s_spare = s_dyn + NB * EP * NT + (kDsmem ? EP * NT : 0);
 
   const int b = static_cast<int>(blockIdx.x) * NB + half;
   const int t = static_cast<int>(threadIdx.x) - half * NT;
@@ -169,6 +196,13 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
 
   if (t == 0) {
     for (int sg = 0; sg < kSeg; ++sg) mbar_init(&s_bar[sg], 1);
+    if constexpr (SPEC > 0) {
+      for (int k = 0; k < SPEC; ++k) {
+        mbar_init(&s_sbar[k], 1);
+        s_stag[k] = kNone;
+        s_sfill[k] = 0;
+      }
+    }
     fence_mbar_init();
   }
 
@@ -295,6 +329,10 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   // and the number of row copies issued so far (mbarrier phase parity)
   unsigned held = kNone;
   unsigned n_copies = 0;
+  unsigned par_m = 0;     // SPEC: mbarrier parity of this iteration's main-buffer copy
+  unsigned runner[kSp];  // SPEC: this iteration's runners-up (warp 0)
+#pragma unroll
+  for (int rr = 0; rr < kSp; ++rr) runner[rr] = kNone;
 
   for (int it = 0; it < a.I; ++it) {
     // ---- exact warp max and the lowest index attaining it
@@ -325,6 +363,24 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       const unsigned bl = __reduce_max_sync(0xffffffffu, h == bh ? l : 0u);
       guess = __reduce_min_sync(0xffffffffu, (h == bh && l == bl) ? sa : kNone);
       top_key = (static_cast<long long>(bh) << 32) | bl;
+      if constexpr (SPEC > 0) {
+        // the best maxima of the other warps (warp 0; thread 0 stages their rows)
+        if (warp == 0) {
+#pragma unroll
+          for (int rr = 0; rr < SPEC; ++rr) {
+            bool taken = sa == guess;
+#pragma unroll
+            for (int q2 = 0; q2 < rr; ++q2) taken = taken || sa == runner[q2];
+            const long long k2 = taken ? LLONG_MIN : sk;
+            const int h2 = static_cast<int>(k2 >> 32);
+            const unsigned l2 = static_cast<unsigned>(k2);
+            const int b2 = __reduce_max_sync(0xffffffffu, h2);
+            const unsigned c2 = __reduce_max_sync(0xffffffffu, h2 == b2 ? l2 : 0u);
+            const unsigned r2 = __reduce_min_sync(0xffffffffu, (h2 == b2 && l2 == c2) ? sa : kNone);
+            runner[rr] = (b2 < 0 || r2 >= static_cast<unsigned>(K)) ? kNone : r2;
+          }
+        }
+      }
       if constexpr (kChunked && FASE_RUNNER_PREFETCH > 0) {
         // Per-block geometries read their (composed) base rows mostly from
         // DRAM. The next selection is often one of this iteration's runners-up
@@ -386,6 +442,8 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     auto parity = [&]() -> unsigned {
       if constexpr (kChunked)
         return par_c;
+      else if constexpr (SPEC > 0)
+        return par_m;
       else
         return it & 1;
     };
@@ -398,6 +456,14 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     if (t == 0 && issue) {
       FASE_ASSERT(guess < static_cast<unsigned>(K));
       fence_proxy_async_smem();
+      int use = -1;  // SPEC: a spare buffer already holding the guess's row
+      if constexpr (SPEC > 0) {
+        for (int k = 0; k < SPEC; ++k)
+          if (s_stag[k] == guess) use = k;
+        s_use = use;
+        s_upar = use >= 0 ? ((s_sfill[use] - 1u) & 1u) : 0u;
+      }
+      if (use < 0) {
       const double* grow = base() + static_cast<int64_t>(guess) * ldg;
       // fused synthesis: the predicted atom's phi row rides on the last segment
       const unsigned phi_bytes =
@@ -424,6 +490,40 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         if (SYN > 0 && sg == kSeg - 1)
           tma_load_1d(s_phi, syn.phi + static_cast<int64_t>(guess) * syn.ldphi, phi_bytes,
                       &s_bar[sg]);
+      }
+      }  // use < 0
+      if constexpr (SPEC > 0) {
+        // stage the runners' rows (and phi rows) for the next iteration in
+        // spare buffers other than the one read now, round robin; a buffer's
+        // previous fill (issued at least one iteration ago) is retired first
+        const unsigned row_bytes = static_cast<unsigned>(EP * NT * sizeof(double2));
+        const unsigned pb =
+            SYN > 0 ? static_cast<unsigned>((syn.n_lost * sizeof(double) + 15) & ~size_t{15}) : 0u;
+        int victim = (use + 1) % SPEC;
+        for (int rr = 0; rr < SPEC; ++rr) {
+          const unsigned r2 = runner[rr];
+          if (r2 == kNone) break;
+          bool have = false;
+          for (int k = 0; k < SPEC; ++k) have = have || s_stag[k] == r2;
+          if (have) continue;
+          int k = -1;
+          for (int step = 0; step < SPEC && k < 0; ++step) {
+            const int c2 = (victim + step) % SPEC;
+            bool keep = c2 == use;
+            for (int q2 = 0; q2 < SPEC; ++q2) keep = keep || (runner[q2] != kNone && s_stag[c2] == runner[q2]);
+            if (!keep) k = c2;
+          }
+          if (k < 0) break;
+          victim = (k + 1) % SPEC;
+          if (s_sfill[k] > 0) mbar_wait(&s_sbar[k], (s_sfill[k] - 1u) & 1u);
+          mbar_arrive_expect_tx(&s_sbar[k], row_bytes + pb);
+          tma_load_1d(s_spare + k * EP * NT, base() + static_cast<int64_t>(r2) * ldg, row_bytes,
+                      &s_sbar[k]);
+          if constexpr (SYN > 0)
+            tma_load_1d(s_sphi[k], syn.phi + static_cast<int64_t>(r2) * syn.ldphi, pb, &s_sbar[k]);
+          s_stag[k] = r2;
+          s_sfill[k] += 1u;
+        }
       }
       if constexpr (kChunked) {
         // the guess's chunk-table rows are read right after the second
@@ -489,6 +589,16 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     FASE_ASSERT(u < static_cast<unsigned>(K) && uw >= 0 && uw < NW);
     if constexpr (kChunked) {
       for (int ch = 0; ch < nch; ++ch) FASE_ASSERT(cids[ch] >= 0);
+    }
+    int use_b = -1;  // SPEC: the spare buffer holding the guess's row (no main copy issued)
+    unsigned use_par = 0;
+    if constexpr (SPEC > 0) {
+      use_b = s_use;
+      use_par = s_upar;
+      if (use_b < 0) {
+        par_m = n_copies & 1u;
+        n_copies += 1u;
+      }
     }
     const double ru = s_r[uw];
     const double du = s_d[uw];
@@ -659,6 +769,16 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
           s_heldm_all[half] = mul_rn(fabs(rv), dv);
         }
       }
+    } else if (SPEC > 0 && u == guess && use_b >= 0) {  // row staged one iteration ahead
+      mbar_wait(&s_sbar[use_b], use_par);
+      const double2* sb = s_spare + use_b * EP * NT;
+      update([&](int j) { return sb[j * NT + t]; }, Direct{}, no_pre);
+      if constexpr (SYN > 0) {
+#pragma unroll
+        for (int i = 0; i < SYN; ++i)
+          if (t + i * NT < syn.n_lost)
+            gacc[i] = add_rn(gacc[i], mul_rn(c, s_sphi[SPEC > 0 ? use_b : 0][t + i * NT]));
+      }
     } else if (u == guess) {  // block-uniform
       update([&](int j) { return s_row[j * NT + t]; }, Staged{}, no_pre);
       if constexpr (SYN > 0) {
@@ -667,7 +787,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
           if (t + i * NT < syn.n_lost) gacc[i] = add_rn(gacc[i], mul_rn(c, s_phi[t + i * NT]));
       }
     } else {
-      wait_all();  // retire the mispredicted copy before the next one
+      if (use_b < 0) wait_all();  // retire the mispredicted copy before the next one
       const double* urow = base() + static_cast<int64_t>(u) * ldg + 2 * t;
       double phv[SYN > 0 ? SYN : 1];
       if constexpr (SYN > 0) {
@@ -717,6 +837,7 @@ struct Variant {
   int nb = 1;             // blocks per CTA (2: paired blocks sharing one D)
   KernelFn fused = nullptr;  // scaled: synthesis fused (up to syn lost samples per thread)
   int syn = 0;
+  int spec = 0;              // spare row buffers (speculative staging, latency shapes)
 };
 
 #define FASE_V(NT, EPT, MINB, DS)                                                       \
@@ -760,11 +881,20 @@ const Variant kExtraVariants[] = {
 // Latency variants: batches of at most one block per SM gain nothing from
 // residency, so each block gets the widest CTA that keeps three pairs per
 // thread (config 0, K = 2304: 384 threads, 113 -> 98 us for 100 iterations).
+#define FASE_VL(NT, EPT, SPEC)                                                           \
+  {NT,                                                                                  \
+   EPT,                                                                                 \
+   true,                                                                                \
+   fase_iterate_kernel<NT, EPT, 1, true, false, false, 1, false, 0, SPEC>,             \
+   fase_iterate_kernel<NT, EPT, 1, true, true, false, 1>,                               \
+   fase_iterate_kernel<NT, EPT, 1, true, false, true, 1>,                               \
+   1, nullptr, 0, SPEC}
 const Variant kLatencyVariants[] = {
-    FASE_V(384, 6, 1, true),
-    FASE_V(768, 6, 1, true),
-    FASE_V(1024, 8, 1, true),
+    FASE_VL(384, 6, FASE_SPEC),
+    FASE_VL(768, 6, FASE_SPEC),
+    FASE_VL(1024, 8, 0),
 };
+#undef FASE_VL
 #undef FASE_V
 
 // Scaled recursion (fase_iterate_scaled): no normalizers in the loop, so only
@@ -790,9 +920,14 @@ const Variant kScaledExtra[] = {
     FASE_VS(128, 64, 3, 4), FASE_VS(256, 20, 4, 1),
 };
 const int kScaledExtraMinb[] = {4, 3, 2, 3, 4};
+#define FASE_VSL(NT, EPT, SYN, SPEC)                                                            \
+  {NT,      EPT,     false, fase_iterate_kernel<NT, EPT, 1, false, false, false, 1, true, 0, SPEC>, \
+   nullptr, nullptr, 1,     fase_iterate_kernel<NT, EPT, 1, false, false, false, 1, true, SYN, SPEC>, \
+   SYN,     SPEC}
 const Variant kScaledLatency[] = {
-    FASE_VS(384, 6, 1, 2), FASE_VS(768, 6, 1, 1), FASE_VS(1024, 8, 1, 1),
+    FASE_VSL(384, 6, 2, FASE_SPEC), FASE_VSL(768, 6, 1, FASE_SPEC), FASE_VSL(1024, 8, 1, 0),
 };
+#undef FASE_VSL
 #undef FASE_VS
 
 int sm_count() {
@@ -927,7 +1062,7 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
   }
   KernelFn fn = a.chunk_count ? v->chunked : (a.R_log ? v->record : v->plain);
   const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2) *
-                      (v->nb + (v->dsmem ? 1 : 0));
+                      (v->nb + (v->dsmem ? 1 : 0) + (fn == v->plain ? v->spec : 0));
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e == cudaSuccess)  // several CTAs per SM need the full shared-memory carveout
@@ -1036,7 +1171,7 @@ extern "C" int fase_iterate_scaled(const fase_iterate_args* args, const fase_syn
     return FASE_ERR_SHAPE;
   }
   KernelFn fn = syn ? v->fused : v->plain;
-  const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2);
+  const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2) * (1 + v->spec);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e == cudaSuccess)
