@@ -452,9 +452,14 @@ def parity_vs_reference(cid, sel, coef, lost, n_lost, name=None):
            "failure": 0}
     worst_c = worst_l = 0.0
     has_coef = "coefficients" in z.files  # selections-only fixtures (c4all)
+    # (NpzFile members decompress on every access: load each array once)
+    z_sel = z["selected"]
+    z_coef = z["coefficients"] if has_coef else None
+    z_lost = z["lost"] if has_coef else None
+    z_lost_n = z["lost_n"] if has_coef else None
     for i, b in enumerate(blocks):
         g = sel[int(b)].astype(np.int64)
-        want = z["selected"][i].astype(np.int64)
+        want = z_sel[i].astype(np.int64)
         diff = np.flatnonzero(g != want)
         stop = int(diff[0]) if diff.size else len(g)
         if diff.size == 0:
@@ -466,12 +471,12 @@ def parity_vs_reference(cid, sel, coef, lost, n_lost, name=None):
             continue
         if not has_coef:
             continue
-        sc = max(float(np.abs(z["coefficients"][i]).max()), 1e-300)
-        worst_c = max(worst_c, float(np.abs(coef[int(b)][:stop] - z["coefficients"][i][:stop])
+        sc = max(float(np.abs(z_coef[i]).max()), 1e-300)
+        worst_c = max(worst_c, float(np.abs(coef[int(b)][:stop] - z_coef[i][:stop])
                                      .max(initial=0.0)) / sc)
         if diff.size == 0 and lost is not None:
-            n = int(z["lost_n"][i])
-            want_l = z["lost"][i][:n]
+            n = int(z_lost_n[i])
+            want_l = z_lost[i][:n]
             worst_l = max(worst_l, float(np.abs(lost[int(b)][:n] - want_l).max(initial=0.0))
                           / max(float(np.abs(want_l).max()), 1e-300))
     out.update(max_coef_rel_dev=worst_c, max_lost_rel_dev=worst_l,

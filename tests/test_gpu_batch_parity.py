@@ -46,6 +46,10 @@ def classify(got_sel, got_coef, z, rows=None, got_lost=None):
     fixture block i in the GPU outputs (default: i)."""
     want_sel = z["selected"].astype(np.int64)
     want_coef = z["coefficients"] if "coefficients" in z.files else None  # selections-only fixtures
+    # (NpzFile members decompress on every access: load each array once)
+    z_lost = z["lost"] if want_coef is not None else None
+    z_lost_n = z["lost_n"] if want_coef is not None else None
+    z_blocks = z["blocks"]
     ties = {}
     for i, t, k in z["ties"]:
         ties.setdefault((int(i), int(t)), set()).add(int(k))
@@ -63,7 +67,7 @@ def classify(got_sel, got_coef, z, rows=None, got_lost=None):
             stops.append(stop)
         else:
             counts["failure"] += 1
-            failures.append((int(z["blocks"][i]), stop, int(g[stop]), int(want_sel[i][stop])))
+            failures.append((int(z_blocks[i]), stop, int(g[stop]), int(want_sel[i][stop])))
             continue
         if want_coef is None:
             continue
@@ -72,8 +76,8 @@ def classify(got_sel, got_coef, z, rows=None, got_lost=None):
         dev = float(np.abs(c - want_coef[i][:stop]).max(initial=0.0)) / scale
         worst_coef = max(worst_coef, dev)
         if diff.size == 0 and got_lost is not None:
-            n = int(z["lost_n"][i])
-            want = z["lost"][i][:n]
+            n = int(z_lost_n[i])
+            want = z_lost[i][:n]
             got = np.asarray(got_lost(i, r))
             worst_lost = max(worst_lost, float(np.abs(got - want).max(initial=0.0))
                              / max(np.abs(want).max(initial=0.0), 1e-300))
@@ -164,6 +168,7 @@ def test_frame_batch_against_reference(cid):
     own = np.zeros((a, a), dtype=bool)
     own[s:s + mb, s:s + mb] = True
     blocks = z["blocks"]
+    z_lost, z_lost_n = z["lost"], z["lost_n"]
 
     def got_lost(i, r):
         # the fixture's lost samples are in area-mask order; the frame holds
@@ -171,7 +176,7 @@ def test_frame_batch_against_reference(cid):
         b = int(blocks[i])
         sel = own[masks[b]]
         r0, c0 = case.corners[b]
-        full = z["lost"][i][: int(z["lost_n"][i])].copy()
+        full = z_lost[i][: int(z_lost_n[i])].copy()
         full[sel] = out[r0:r0 + mb, c0:c0 + mb].ravel()  # row-major = mask order
         return full
 

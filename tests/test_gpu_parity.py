@@ -28,6 +28,7 @@ from paper_2204_14194_b200 import (  # noqa: E402
     fase_extrapolate,
     fase_extrapolate_batch,
     generate_dictionary,
+    initial_scalar_products,
     parse_dict_spec,
     provenance_hash,
 )
@@ -797,3 +798,32 @@ def test_synth_paste_throughput_shape_bit_exact(nb, n_lost, I, stop):
         live = sel[:, t] >= 0
         want[live] = want[live] + coef[live, t, None] * phi[sel[live, t], :n_lost]
     assert np.array_equal(got, want)
+
+
+def test_maximum_atom_count():
+    """K at the largest recursion variant (fase_max_atoms, 512 x 24 = 12,288):
+    the exact recursion stays bit-exact against the oracle's loop on the same
+    (device-built) table / normalizers / initial products; K + 1 atoms raise
+    UnsupportedDictionaryError, the reference-facing error class."""
+    kmax = _native.max_atoms()
+    rng = np.random.default_rng(12)
+    m = n = 16
+    mask = wl.central_loss_mask(m, n, 6, 6)
+    vals = rng.standard_normal((kmax, m, n))
+    d = Dictionary(vals)
+    cfg = ExtrapConfig(20, 0.5, 0.8)
+    sig = rng.uniform(0, 255, (3, m, n))
+    w = build_weight_field(mask, cfg.rho_hat)
+    t = build_gram_tables(d, w, device=DEV)
+    r0 = np.stack([initial_scalar_products(sig[b], w, d, device=DEV).real for b in range(3)])
+    res = fase_extrapolate_batch(sig, mask, d, t, cfg, device=DEV, patch=False, products=r0)
+    G, D = t.device_tables(torch.device(DEV))
+    g = G[:, :kmax].cpu().numpy()
+    dd = D.cpu().numpy()
+    for b in range(3):
+        sel, _, coef, _ = orc.fase_run(r0[b], g, dd, cfg.gamma, cfg.iterations)
+        assert np.array_equal(res.selected[b].cpu().numpy(), sel)
+        assert np.array_equal(res.coefficients[b].cpu().numpy(), coef.real)
+    with pytest.raises(UnsupportedDictionaryError):
+        fase_extrapolate_batch(sig, mask, Dictionary(rng.standard_normal((kmax + 1, m, n))),
+                               None, cfg, device=DEV)
