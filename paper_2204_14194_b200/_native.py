@@ -41,6 +41,7 @@ EXPORTS = (
     "fase_iterate_complex_scaled", "fase_frame_widen", "fase_frame_paste_complex",
 )
 
+ABI_MAJOR = 2  # fase_abi_version() >> 16 of the library this binding matches
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int
 _i64 = ctypes.c_int64
@@ -94,6 +95,10 @@ def load():
     lib.fase_last_error.restype = ctypes.c_char_p
     lib.fase_last_error.argtypes = []
     lib.fase_abi_version.restype = _i32
+    if lib.fase_abi_version() >> 16 != ABI_MAJOR:  # IterateArgs must match the library's struct
+        raise errors.NativeLibraryError(
+            f"{path}: ABI {lib.fase_abi_version() >> 16}.{lib.fase_abi_version() & 0xffff}, this "
+            f"package needs {ABI_MAJOR}.x: rebuild with `python -m paper_2204_14194_b200._build`")
     lib.fase_max_atoms.restype = _i32
     lib.fase_table_ld.restype = _i32
     lib.fase_table_ld.argtypes = [_i32]
