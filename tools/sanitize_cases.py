@@ -233,6 +233,53 @@ def case_gram():
     return outs
 
 
+def case_cluster():
+    """One block over a CTA cluster (csrc/iterate_cluster.cu): 8 CTAs at K > 4608
+    (default), 4 CTAs forced at K <= 4608; exact, scaled, fused synthesis."""
+    import os
+
+    outs = []
+    for k, cs in ((6000, None), (1500, "4")):
+        if cs:
+            os.environ["FASE_CLUSTER"] = cs
+        try:
+            d = gauss(k, 16, 16)
+            mask = wl.central_loss_mask(16, 16, 6, 6)
+            cfg = ExtrapConfig(8)
+            t = build_gram_tables(d, build_weight_field(mask, cfg.rho_hat), device=DEV)
+            frozen(*t.device_tables(DEV))
+            for rec in ("exact", "scaled"):
+                p = ExtrapolationPlan(d, mask, 3, cfg, t, device=DEV, recursion=rec)
+                p.run(torch.from_numpy(sig(3, 16, 16)).to(DEV))
+                outs += [p.selected.clone(), p.coefficients.clone(), p.lost.clone()]
+        finally:
+            os.environ.pop("FASE_CLUSTER", None)
+    return outs
+
+
+def case_frame_complex():
+    """Complex FrameEngine (complex cell tables, bases, chunked recursion, paste)
+    and the uint8 frame widening kernel."""
+    from paper_2204_14194_b200 import _native
+    from paper_2204_14194_b200.conceal import FrameEngine, lossy_tiles, tile_grid
+
+    d = parse_dict_spec("dft", 16, 16)
+    rng = np.random.default_rng(9)
+    h, w, mb = 40, 48, 8
+    img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+    lost = np.zeros((h, w), dtype=bool)
+    for ty, tx in [(0, 0), (0, 1), (2, 3), (4, 5), (3, 0)]:
+        lost[ty * mb:(ty + 1) * mb, tx * mb:(tx + 1) * mb] = True
+    f64 = torch.empty((h, w), dtype=torch.float64, device=DEV)
+    _native.frame_widen(torch.from_numpy(img).to(DEV), torch.from_numpy(lost).to(DEV), f64)
+    eng = FrameEngine(d, (h, w), mb, 4, ExtrapConfig(15), device=DEV, compose="triples")
+    grid = torch.from_numpy(tile_grid(lost, mb)).to(DEV)
+    corners = torch.from_numpy(lossy_tiles(lost, (mb, mb)).astype(np.int32)).to(DEV)
+    frozen(eng.bases, eng.tables)
+    r = eng.run(f64, grid, corners)
+    return [f64.clone(), r.selected, r.coefficients, r.patched, r.max_imag]
+
+
 CASES = {k[5:]: v for k, v in globals().items() if k.startswith("case_")}
 
 
