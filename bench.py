@@ -513,11 +513,9 @@ def run_gpu(args):
     # the tensor cores) is cheaper than moving 537 MB, and it is outside the
     # timed region (reference bench.py:118-119)
     tables = build_gram_tables(d, build_weight_field(mask, w.config.rho_hat), device=dev)
-    # auto: scaled for real dictionaries; for complex ones where the exact kernel
-    # needs 512-thread / paired shapes (K > 2560: union:dft+bdft 2.31 -> 1.84 ms;
-    # at K = 2304 the two are within 3%)
-    recursion = args.recursion if args.recursion != "auto" else (
-        "scaled" if not cplx or K > 2560 else "exact")
+    # auto: the scaled recursion (complex: union:dft+bdft 2.31 -> 1.84 ms; dft
+    # 48^2 0.994 -> 0.830 ms at four CTAs per SM)
+    recursion = args.recursion if args.recursion != "auto" else "scaled"
     if cplx and world > 1:
         raise SystemExit("complex dictionaries: single GPU only in the bench")
     # ONE batch of B_total blocks, rank r taking block_range(B_total, r, N)

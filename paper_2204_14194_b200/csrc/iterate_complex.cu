@@ -521,6 +521,7 @@ struct ExtraVariant {
 };
 const ExtraVariant kExtraVariants[] = {
     {2, FASE_CV(256, 7, 2, true)}, {2, FASE_CV(256, 8, 2, true)}, {2, FASE_CV(256, 9, 2, true)},
+    {4, FASE_CV(256, 9, 4, true)},
 };
 #undef FASE_CV
 
@@ -529,11 +530,20 @@ const ExtraVariant kExtraVariants[] = {
 // blocks per SM where the exact kernel needs paired 512-thread CTAs).
 #define FASE_CS(NT, EP, MINB) \
   {NT, EP, false, fase_iterate_complex_kernel<NT, EP, MINB, false, false, false, 1, true>, nullptr, nullptr}
+// The 256-thread shapes up to 2304 atoms run four CTAs per SM (64 registers,
+// a few spilled): 1,024 blocks then take two waves of 592 slots instead of
+// three of 444 (`dft` 48^2, config-1 batch: 1.018 -> 0.830 ms per recursion,
+// tools/ab_complex.sh; the exact kernel, with D^2 in shared memory, was slower
+// at four CTAs: 0.994 -> 1.198 ms).
 const Variant kScaledVariants[] = {
     FASE_CS(128, 1, 4),  FASE_CS(128, 2, 4),  FASE_CS(128, 4, 4),  FASE_CS(128, 8, 4),
-    FASE_CS(256, 5, 3),  FASE_CS(256, 6, 3),  FASE_CS(256, 7, 3),  FASE_CS(256, 8, 3),
-    FASE_CS(256, 9, 3),  FASE_CS(256, 10, 2), FASE_CS(256, 12, 2), FASE_CS(256, 16, 2),
+    FASE_CS(256, 5, 4),  FASE_CS(256, 6, 4),  FASE_CS(256, 7, 4),  FASE_CS(256, 8, 4),
+    FASE_CS(256, 9, 4),  FASE_CS(256, 10, 2), FASE_CS(256, 12, 2), FASE_CS(256, 16, 2),
     FASE_CS(256, 18, 2), FASE_CS(256, 20, 2), FASE_CS(512, 12, 1),
+};
+// alternative residency of the scaled shapes (FASE_COMPLEX_SCALED_VARIANT=NTxEPxMINB)
+const ExtraVariant kScaledExtra[] = {
+    {3, FASE_CS(256, 9, 3)}, {3, FASE_CS(256, 8, 3)}, {3, FASE_CS(256, 10, 3)},
 };
 #undef FASE_CS
 
@@ -678,6 +688,14 @@ extern "C" int fase_iterate_complex_scaled(const fase_iterate_args* args, void* 
       v = &sv;
       break;
     }
+  if (const char* env = getenv("FASE_COMPLEX_SCALED_VARIANT")) {
+    int nt = 0, ep = 0, minb = 0;
+    if (v && dflt && sscanf(env, "%dx%dx%d", &nt, &ep, &minb) == 3)
+      for (const ExtraVariant& x : kScaledExtra)
+        if (x.minb == minb && x.v.nt == nt && x.v.ep == ep && nt * ep >= a.K &&
+            nt * ep <= dflt->nt * dflt->ep)
+          v = &x.v;
+  }
   if (!dflt || !v) {
     set_error("fase_iterate_complex_scaled: K=%d exceeds the largest kernel variant (%d atoms)",
               a.K, fase_max_atoms_complex());
