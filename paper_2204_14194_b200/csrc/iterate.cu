@@ -879,7 +879,7 @@ const Variant kExtraVariants[] = {
 };
 
 // Latency variants: batches of at most one block per SM gain nothing from
-// residency, so each block gets the widest CTA that keeps three pairs per
+// residency, so each block gets the widest CTA (576 x 4 / 768 x 6 / 1024 x 8) that keeps two or three pairs per
 // thread (config 0, K = 2304: 384 threads, 113 -> 98 us for 100 iterations).
 #define FASE_VL(NT, EPT, SPEC)                                                           \
   {NT,                                                                                  \
@@ -889,8 +889,11 @@ const Variant kExtraVariants[] = {
    fase_iterate_kernel<NT, EPT, 1, true, true, false, 1>,                               \
    fase_iterate_kernel<NT, EPT, 1, true, false, true, 1>,                               \
    1, nullptr, 0, SPEC}
+// (576 x 4 for K <= 2304: two pairs per thread, config-0 exact recursion
+// 115.2 -> 106.6 us against 384 x 6)
 const Variant kLatencyVariants[] = {
     FASE_VL(384, 6, FASE_SPEC),
+    FASE_VL(576, 4, 0),
     FASE_VL(768, 6, FASE_SPEC),
     FASE_VL(1024, 8, 0),
 };
@@ -924,6 +927,7 @@ const int kScaledExtraMinb[] = {4, 3, 2, 3, 4};
   {NT,      EPT,     false, fase_iterate_kernel<NT, EPT, 1, false, false, false, 1, true, 0, SPEC>, \
    nullptr, nullptr, 1,     fase_iterate_kernel<NT, EPT, 1, false, false, false, 1, true, SYN, SPEC>, \
    SYN,     SPEC}
+// (576 x 4 measured slower for the scaled recursion: config 0 106.6 vs ~97 us)
 const Variant kScaledLatency[] = {
     FASE_VSL(384, 6, 2, FASE_SPEC), FASE_VSL(768, 6, 1, FASE_SPEC), FASE_VSL(1024, 8, 1, 0),
 };
