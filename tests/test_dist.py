@@ -218,3 +218,25 @@ def test_gloo_world2_sharded_frame_reassembles():
     img, lost = _frame_case()
     assert not np.array_equal(out1[lost], img[lost])  # every tile was pasted
     assert np.array_equal(out1[~lost], img[~lost])
+
+
+def test_result_arena_layout_single_process():
+    """ResultArena on one process: the arena IS the gathered buffer (no copy);
+    selections / coefficients / lost samples are disjoint, 8-byte aligned
+    views; complex coefficients (complex dictionaries) take two words each."""
+    from paper_2204_14194_b200.shard import ResultArena
+
+    for cplx in (False, True):
+        a = ResultArena(5, 7, 3, torch.device("cpu"), 1, 0, slots=2, complex_coef=cplx)
+        assert a.gathered[0].data_ptr() == a.bufs[0].data_ptr()
+        sel, coef, lost = a.local(1)
+        assert sel.shape == (5, 7) and coef.shape == (5, 7) and lost.shape == (5, 3)
+        assert coef.dtype == (torch.complex128 if cplx else torch.float64)
+        for t in (sel, coef, lost):
+            assert t.data_ptr() % 8 == 0
+        sel.fill_(-3)
+        coef.fill_(2.5)
+        lost.fill_(7.0)
+        s2, c2, l2 = a.assemble(1)
+        assert (s2 == -3).all() and (c2 == 2.5).all() and (l2 == 7.0).all()
+        assert (a.assemble(0)[0] == 0).all()  # slot 0 untouched
