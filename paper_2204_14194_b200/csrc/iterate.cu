@@ -67,13 +67,16 @@ constexpr unsigned kNone = 0xffffffffu;
 #ifndef FASE_BASE_EVICT_FIRST  // chunked recursion: composed-base rows copied evict_first
 #define FASE_BASE_EVICT_FIRST 1
 #endif
-// latency shapes: spare buffers for the runners-up's rows (measurement knob; 0
-// by default -- config 0 recursion 100.5 us without, 164 us with 3 spare
-// buffers: the speculative copies compete with the selected row for the one
-// SM's L2 -> shared-memory bandwidth, and warp 0's extra reductions sit on the
-// path to the second barrier)
+// Row staging of the latency shapes (at most one block per SM), the kernel's
+// SPEC argument: -1 (default) every thread loads its pairs of the predicted
+// row straight into registers after the block max (config 0 scaled recursion
+// 101.6 -> 96.3 us against 0); 0 one TMA copy into shared memory, as at full
+// occupancy; N > 0 that copy plus N speculative spare buffers for the
+// runners-up's rows (measured: 100.5 -> 164 us with 3 -- the speculative
+// copies compete with the selected row for the one SM's L2 -> shared-memory
+// bandwidth, and warp 0's extra reductions sit before the second barrier)
 #ifndef FASE_SPEC
-#define FASE_SPEC 0
+#define FASE_SPEC -1
 #endif
 #ifdef FASE_ITERATE_STATS
 __device__ unsigned long long g_stats[8];  // measurement build: chunked-path counters
@@ -125,6 +128,11 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   static_assert(SPEC == 0 || (NB == 1 && !kChunked && !kRecord), "speculative staging: one "
                 "shared-geometry block per CTA");
   constexpr int kSp = SPEC > 0 ? SPEC : 1;
+  // SPEC < 0 (latency shapes, measurement): the predicted row is loaded straight
+  // into registers by every thread right after the block max (no TMA, no
+  // mbarrier), overlapping the tie pass and the second barrier like the copy
+  constexpr bool kRegRow = SPEC < 0;
+  static_assert(!kRegRow || (NB == 1 && !kChunked), "register-staged rows: shared geometry");
   __shared__ __align__(8) uint64_t s_sbar[kSp];   // SPEC: one mbarrier per spare buffer
   __shared__ unsigned s_stag[kSp];                 // SPEC: atom held by each spare buffer
   __shared__ unsigned s_sfill[kSp];                // SPEC: fills issued per spare buffer
@@ -436,7 +444,19 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         if (s_heldm_all[half] >= thr_) guess = held;
       }
     }
-    const bool issue = !kChunked || guess != held;  // block-uniform
+    const bool issue = (!kChunked || guess != held) && !kRegRow;  // block-uniform
+    double2 rrow[kRegRow ? EP : 1];  // kRegRow: this thread's pairs of the predicted row
+    double rphi[kRegRow && SYN > 0 ? SYN : 1];
+    if constexpr (kRegRow) {
+      const double* grow = a.G0 + static_cast<int64_t>(guess < static_cast<unsigned>(K) ? guess : 0u) * ldg + 2 * t;
+#pragma unroll
+      for (int j = 0; j < EP; ++j) rrow[j] = ldg2_here(grow + 2 * j * NT);
+      if constexpr (SYN > 0) {
+        const double* prow = syn.phi + static_cast<int64_t>(guess < static_cast<unsigned>(K) ? guess : 0u) * syn.ldphi;
+#pragma unroll
+        for (int i = 0; i < SYN; ++i) rphi[i] = t + i * NT < syn.n_lost ? __ldg(prow + t + i * NT) : 0.0;
+      }
+    }
     const unsigned par_c = n_copies & 1u;
     if constexpr (kChunked) n_copies += issue ? 1u : 0u;
     auto parity = [&]() -> unsigned {
@@ -779,6 +799,13 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
           if (t + i * NT < syn.n_lost)
             gacc[i] = add_rn(gacc[i], mul_rn(c, s_sphi[SPEC > 0 ? use_b : 0][t + i * NT]));
       }
+    } else if (kRegRow && u == guess) {  // the row is already in registers
+      update([&](int j) { return rrow[kRegRow ? j : 0]; }, Direct{}, no_pre);
+      if constexpr (SYN > 0 && kRegRow) {
+#pragma unroll
+        for (int i = 0; i < SYN; ++i)
+          if (t + i * NT < syn.n_lost) gacc[i] = add_rn(gacc[i], mul_rn(c, rphi[i]));
+      }
     } else if (u == guess) {  // block-uniform
       update([&](int j) { return s_row[j * NT + t]; }, Staged{}, no_pre);
       if constexpr (SYN > 0) {
@@ -787,7 +814,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
           if (t + i * NT < syn.n_lost) gacc[i] = add_rn(gacc[i], mul_rn(c, s_phi[t + i * NT]));
       }
     } else {
-      if (use_b < 0) wait_all();  // retire the mispredicted copy before the next one
+      if (use_b < 0 && !kRegRow) wait_all();  // retire the mispredicted copy before the next one
       const double* urow = base() + static_cast<int64_t>(u) * ldg + 2 * t;
       double phv[SYN > 0 ? SYN : 1];
       if constexpr (SYN > 0) {
@@ -890,12 +917,12 @@ const Variant kExtraVariants[] = {
    fase_iterate_kernel<NT, EPT, 1, true, false, true, 1>,                               \
    1, nullptr, 0, SPEC}
 // (576 x 4 for K <= 2304: two pairs per thread, config-0 exact recursion
-// 115.2 -> 106.6 us against 384 x 6)
+// 115.2 -> 106.6 us against 384 x 6; 87.7 us with register rows)
 const Variant kLatencyVariants[] = {
     FASE_VL(384, 6, FASE_SPEC),
-    FASE_VL(576, 4, 0),
+    FASE_VL(576, 4, FASE_SPEC),
     FASE_VL(768, 6, FASE_SPEC),
-    FASE_VL(1024, 8, 0),
+    FASE_VL(1024, 8, 0),  // (register rows measured slower at 4 pairs per thread)
 };
 #undef FASE_VL
 #undef FASE_V
@@ -927,7 +954,8 @@ const int kScaledExtraMinb[] = {4, 3, 2, 3, 4};
   {NT,      EPT,     false, fase_iterate_kernel<NT, EPT, 1, false, false, false, 1, true, 0, SPEC>, \
    nullptr, nullptr, 1,     fase_iterate_kernel<NT, EPT, 1, false, false, false, 1, true, SYN, SPEC>, \
    SYN,     SPEC}
-// (576 x 4 measured slower for the scaled recursion: config 0 106.6 vs ~97 us)
+// (576 x 4 measured slower for the scaled recursion: config 0 106.6 vs ~97 us
+// with staged rows, 102.4 vs 96.3 us with register rows)
 const Variant kScaledLatency[] = {
     FASE_VSL(384, 6, 2, FASE_SPEC), FASE_VSL(768, 6, 1, FASE_SPEC), FASE_VSL(1024, 8, 1, 0),
 };
@@ -1066,7 +1094,7 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
   }
   KernelFn fn = a.chunk_count ? v->chunked : (a.R_log ? v->record : v->plain);
   const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2) *
-                      (v->nb + (v->dsmem ? 1 : 0) + (fn == v->plain ? v->spec : 0));
+                      (v->nb + (v->dsmem ? 1 : 0) + (fn == v->plain && v->spec > 0 ? v->spec : 0));
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e == cudaSuccess)  // several CTAs per SM need the full shared-memory carveout
@@ -1175,7 +1203,8 @@ extern "C" int fase_iterate_scaled(const fase_iterate_args* args, const fase_syn
     return FASE_ERR_SHAPE;
   }
   KernelFn fn = syn ? v->fused : v->plain;
-  const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2) * (1 + v->spec);
+  const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2) *
+                      (1 + (v->spec > 0 ? v->spec : 0));
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e == cudaSuccess)
