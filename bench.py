@@ -514,8 +514,15 @@ def run_gpu(args):
     # timed region (reference bench.py:118-119)
     tables = build_gram_tables(d, build_weight_field(mask, w.config.rho_hat), device=dev)
     # auto: the scaled recursion (complex: union:dft+bdft 2.31 -> 1.84 ms; dft
-    # 48^2 0.994 -> 0.830 ms at four CTAs per SM)
-    recursion = args.recursion if args.recursion != "auto" else "scaled"
+    # 48^2 0.994 -> 0.830 ms at four CTAs per SM), except for batches of at most
+    # one block per SM, where the bit-exact recursion with the synthesis fused
+    # in is the faster one (config 0: 113.9 vs 118.1 us per step)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    n_lost = int(mask.sum())
+    latency_exact = (not cplx and B_total <= n_sm and world == 1
+                     and 0 < n_lost <= _native.synth_capacity(K, B_total))
+    recursion = args.recursion if args.recursion != "auto" else (
+        "exact" if latency_exact else "scaled")
     if cplx and world > 1:
         raise SystemExit("complex dictionaries: single GPU only in the bench")
     # ONE batch of B_total blocks, rank r taking block_range(B_total, r, N)

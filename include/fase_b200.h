@@ -265,6 +265,15 @@ FASE_API int fase_iterate_scaled(const fase_iterate_args* args, const fase_synth
                                  void* stream);
 FASE_API int fase_iterate_scaled_synth_capacity(int K, int B);
 
+/* The exact recursion (fase_iterate, bit-identical selections / coefficients)
+ * with the synthesis fused in, for shared geometries and batches of at most one
+ * block per SM (latency-bound: config 0): bit-identical to fase_iterate
+ * followed by fase_synth_paste over the packed lost samples. n_lost must not
+ * exceed fase_iterate_synth_capacity(K, B) (0: not available for this batch). */
+FASE_API int fase_iterate_synth(const fase_iterate_args* args, const fase_synth_fused* synth,
+                                void* stream);
+FASE_API int fase_iterate_synth_capacity(int K, int B);
+
 /* Gs[u*lds + k] = G[u*ldg + k] * D[k] (u < rows, k < K), 0 for K <= k < lds;
  * lds even. A complex table (rows of conj(C)) is scaled as its real view:
  * rows = K, 2K columns, D repeated per (re, im) pair. */

@@ -39,6 +39,7 @@ EXPORTS = (
     "fase_ozaki_split", "fase_ozaki_gemm", "fase_ozaki_gram", "fase_sep_products_batch",
     "fase_iterate_scaled", "fase_scale_columns", "fase_iterate_scaled_synth_capacity",
     "fase_iterate_complex_scaled", "fase_frame_widen", "fase_frame_paste_complex",
+    "fase_iterate_synth", "fase_iterate_synth_capacity",
 )
 
 ABI_MAJOR = 2  # fase_abi_version() >> 16 of the library this binding matches
@@ -123,6 +124,8 @@ def load():
         "fase_iterate": [ctypes.POINTER(IterateArgs), _vp],
         "fase_iterate_scaled": [ctypes.POINTER(IterateArgs), ctypes.POINTER(SynthFused), _vp],
         "fase_iterate_scaled_synth_capacity": [_i32, _i32],
+        "fase_iterate_synth": [ctypes.POINTER(IterateArgs), ctypes.POINTER(SynthFused), _vp],
+        "fase_iterate_synth_capacity": [_i32, _i32],
         "fase_scale_columns": [_vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp],
         "fase_iterate_complex_scaled": [ctypes.POINTER(IterateArgs), _vp],
         "fase_iterate_complex": [ctypes.POINTER(IterateArgs), _vp],
@@ -309,9 +312,15 @@ def _hot_ptr(l2_hot, K: int):
     return _ptr(l2_hot)
 
 
+def synth_capacity(K: int, B: int) -> int:
+    """Lost samples the exact recursion with fused synthesis can carry (0: n/a)."""
+    return int(load().fase_iterate_synth_capacity(K, B))
+
+
 def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *,
             chunk_tables=None, chunk_stride: int = 0, chunk_count=None, chunk_ids=None,
-            R_out=None, R_log=None, compose=None, base_stride: int = 0, l2_hot=None) -> None:
+            R_out=None, R_log=None, compose=None, base_stride: int = 0, l2_hot=None,
+            phi_lost=None, n_lost: int = 0, lost=None) -> None:
     """The recursion (fase_iterate). ``compose`` (int32 device table n^depth,
     depth 1..3) with ``base_stride`` selects precomposed base tables at
     G0 + p * base_stride for the longest prefix of each block's chunk list."""
@@ -340,6 +349,13 @@ def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *
             raise errors.ShapeError("compose must be an n, n x n or n x n x n table")
     if proj.stride(0) != args.ldo or coef.stride(0) != args.ldo:
         raise errors.ShapeError("sel / proj / coef must share one leading dimension")
+    if phi_lost is not None:  # the synthesis fused in (fase_iterate_synth)
+        _require(phi_lost, "phi_lost", torch.float64, 2)
+        _require(lost, "lost", torch.float64, 2)
+        syn = SynthFused(phi=_ptr(phi_lost), ldphi=_ld(phi_lost), n_lost=n_lost, out=_ptr(lost),
+                         ldout=_ld(lost))
+        _check(lib.fase_iterate_synth(ctypes.byref(args), ctypes.byref(syn), _stream(R0)))
+        return
     _check(lib.fase_iterate(ctypes.byref(args), _stream(R0)))
 
 

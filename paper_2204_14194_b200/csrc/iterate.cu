@@ -142,7 +142,8 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   static_assert(NB == 1 || (kDsmem && !kChunked), "paired blocks share one D in shared memory");
   static_assert(!kScaled || (!kDsmem && !kChunked && !kRecord && NB == 1),
                 "the scaled recursion keeps no normalizers and has one block per CTA");
-  static_assert(SYN == 0 || kScaled, "fused synthesis runs with the scaled recursion");
+  static_assert(SYN == 0 || (!kChunked && !kRecord && NB == 1),
+                "fused synthesis: one shared-geometry block per CTA");
   __shared__ __align__(16) double s_phi[SYN > 0 ? SYN * NT : 2];
 
   __shared__ long long s_key_all[NB][NW];
@@ -908,21 +909,22 @@ const Variant kExtraVariants[] = {
 // Latency variants: batches of at most one block per SM gain nothing from
 // residency, so each block gets the widest CTA (576 x 4 / 768 x 6 / 1024 x 8) that keeps two or three pairs per
 // thread (config 0, K = 2304: 384 threads, 113 -> 98 us for 100 iterations).
-#define FASE_VL(NT, EPT, SPEC)                                                           \
+// (fused: the exact recursion with the synthesis fused in, fase_iterate_synth)
+#define FASE_VL(NT, EPT, SPEC, SYN)                                                      \
   {NT,                                                                                  \
    EPT,                                                                                 \
    true,                                                                                \
    fase_iterate_kernel<NT, EPT, 1, true, false, false, 1, false, 0, SPEC>,             \
    fase_iterate_kernel<NT, EPT, 1, true, true, false, 1>,                               \
    fase_iterate_kernel<NT, EPT, 1, true, false, true, 1>,                               \
-   1, nullptr, 0, SPEC}
+   1, fase_iterate_kernel<NT, EPT, 1, true, false, false, 1, false, SYN, SPEC>, SYN, SPEC}
 // (576 x 4 for K <= 2304: two pairs per thread, config-0 exact recursion
 // 115.2 -> 106.6 us against 384 x 6; 87.7 us with register rows)
 const Variant kLatencyVariants[] = {
-    FASE_VL(384, 6, FASE_SPEC),
-    FASE_VL(576, 4, FASE_SPEC),
-    FASE_VL(768, 6, FASE_SPEC),
-    FASE_VL(1024, 8, 0),  // (register rows measured slower at 4 pairs per thread)
+    FASE_VL(384, 6, FASE_SPEC, 2),
+    FASE_VL(576, 4, FASE_SPEC, 1),
+    FASE_VL(768, 6, FASE_SPEC, 1),
+    FASE_VL(1024, 8, 0, 1),  // (register rows measured slower at 4 pairs per thread)
 };
 #undef FASE_VL
 #undef FASE_V
@@ -1140,6 +1142,82 @@ const Variant* pick_scaled(int K, int B) {
 }
 }  // namespace
 }  // namespace fase
+
+namespace fase {
+namespace {
+// The exact latency variant for K (the widest one-block-per-SM shape whose
+// capacity fits the default variant's table layout), or nullptr.
+const Variant* pick_latency_exact(int K) {
+  const Variant* dflt = pick_variant(K);
+  if (!dflt) return nullptr;
+  const Variant* v = nullptr;
+  for (const Variant& lv : kLatencyVariants)
+    if (lv.nt * lv.ept >= K && lv.nt * lv.ept <= dflt->nt * dflt->ept && (!v || lv.nt > v->nt))
+      v = &lv;
+  return v;
+}
+}  // namespace
+}  // namespace fase
+
+extern "C" int fase_iterate_synth_capacity(int K, int B) {
+  if (K < 1 || B < 1 || B > sm_count()) return 0;
+  const Variant* v = pick_latency_exact(K);
+  return v ? v->syn * v->nt : 0;
+}
+
+extern "C" int fase_iterate_synth(const fase_iterate_args* args, const fase_synth_fused* syn,
+                                  void* stream) {
+  if (!args || !syn) {
+    set_error("fase_iterate_synth: null argument block");
+    return FASE_ERR_PARAMETER;
+  }
+  const fase_iterate_args a = hint_policy(*args);
+  if (a.K < 1 || a.B < 0 || a.I < 1) {
+    set_error("fase_iterate_synth: bad sizes (K=%d, B=%d, I=%d)", a.K, a.B, a.I);
+    return FASE_ERR_SHAPE;
+  }
+  if (!(a.gamma > 0.0 && a.gamma <= 1.0)) {
+    set_error("fase_iterate_synth: gamma must lie in (0, 1], got %g", a.gamma);
+    return FASE_ERR_PARAMETER;
+  }
+  if (a.B == 0) return FASE_OK;
+  if (!a.G0 || !aligned16(a.G0) || a.ldg < a.K || (a.ldg & 1) || !a.D || !a.R0 ||
+      a.ldr < a.K || !a.sel || !a.proj || !a.coef || a.ldo < a.I) {
+    set_error("fase_iterate_synth: bad operand (null, misaligned, odd or short leading dimension)");
+    return FASE_ERR_SHAPE;
+  }
+  if (a.chunk_count || a.compose || a.ldd != 0 || a.R_out || a.R_log) {
+    set_error("fase_iterate_synth: shared geometry only (no chunk tables, per-block D, R_out or "
+              "R_log)");
+    return FASE_ERR_UNSUPPORTED;
+  }
+  if (syn->n_lost < 1 || !syn->phi || !aligned16(syn->phi) || (syn->ldphi & 1) ||
+      syn->ldphi < syn->n_lost || !syn->out || syn->ldout < syn->n_lost) {
+    set_error("fase_iterate_synth: bad fused-synthesis operand (n_lost=%d)", syn->n_lost);
+    return FASE_ERR_SHAPE;
+  }
+  const Variant* v = a.B <= sm_count() ? pick_latency_exact(a.K) : nullptr;
+  if (!v || !v->fused || syn->n_lost > v->syn * v->nt) {
+    set_error("fase_iterate_synth: needs at most one block per SM and n_lost <= "
+              "fase_iterate_synth_capacity(K, B) (K=%d, B=%d, n_lost=%d)", a.K, a.B, syn->n_lost);
+    return FASE_ERR_UNSUPPORTED;
+  }
+  if (a.ldg < pick_variant(a.K)->nt * pick_variant(a.K)->ept) {
+    set_error("fase_iterate_synth: table rows must be zero-padded to fase_table_ld(K) (ldg=%lld)",
+              static_cast<long long>(a.ldg));
+    return FASE_ERR_SHAPE;
+  }
+  const size_t smem = static_cast<size_t>(v->nt) * (v->ept / 2) * sizeof(double2) *
+                      (1 + 1 + (v->spec > 0 ? v->spec : 0));  // row, D (+ spare rows)
+  cudaError_t e = cudaFuncSetAttribute(v->fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) {
+    set_error("fase_iterate_synth: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return FASE_ERR_CUDA;
+  }
+  v->fused<<<a.B, v->nt, smem, as_stream(stream)>>>(a, *syn);
+  return check_launch("fase_iterate_synth");
+}
 
 extern "C" int fase_iterate_scaled_synth_capacity(int K, int B) {
   // the larger of the cluster path's (taken when the lost samples fit it) and

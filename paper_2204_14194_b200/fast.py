@@ -805,10 +805,13 @@ class ExtrapolationPlan:
         # scaled recursion, batches of at most one block per SM (latency bound):
         # the synthesis runs inside the recursion (config 0: 0.112 -> 0.099 ms);
         # at full occupancy the separate kernel is faster (fused: c1 -6%, c4 -4%)
+        # (the exact recursion fuses it too: fase_iterate_synth; config 0 exact
+        # recursion + separate synthesis 87.7 + 16.9 us)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self.fused_synth = bool(
-            self.Gs is not None and not cplx and self.n_lost
-            and self.B <= torch.cuda.get_device_properties(dev).multi_processor_count
-            and self.n_lost <= _native.scaled_synth_capacity(K, self.B))
+            not cplx and self.n_lost and self.B <= sms
+            and self.n_lost <= (_native.scaled_synth_capacity(K, self.B) if self.Gs is not None
+                                else _native.synth_capacity(K, self.B)))
         if cplx:
             cparts = dictionary.device_cfactors(dev) if products in ("auto", "separable") else []
             n_prod = 1 + (len(cparts) + len(_ranges(self._uncovered(cparts))) if cparts else 1)
@@ -928,10 +931,14 @@ class ExtrapolationPlan:
                                             max_imag=sc["max_imag"])
             return
         hot = getattr(self, "l2_hot", None)
-        if self.fused_synth:
+        if self.fused_synth and self.Gs is not None:
             _native.iterate_scaled(self.Gs, self.D, sc["R0"], self.K, self.I, self.config.gamma,
                                    sel, proj, coef, phi_lost=self.phi_lost, n_lost=self.n_lost,
                                    lost=lost, l2_hot=hot)
+            return
+        if self.fused_synth:
+            _native.iterate(self.G, self.D, sc["R0"], self.K, self.I, self.config.gamma, sel, proj,
+                            coef, l2_hot=hot, phi_lost=self.phi_lost, n_lost=self.n_lost, lost=lost)
             return
         if self.Gs is not None:
             _native.iterate_scaled(self.Gs, self.D, sc["R0"], self.K, self.I, self.config.gamma,

@@ -740,7 +740,8 @@ def test_iterate_compose_map_bit_identical(cplx, depth):
 @pytest.mark.parametrize("spec,m,loss,nb", [("union:dct+had", 48, 16, 64), ("dct", 48, 16, 1),
                                             ("gauss:2000:3", 24, 10, 37)])
 def test_fused_synthesis_bit_identical(spec, m, loss, nb):
-    """The scaled recursion with the synthesis fused in writes the same lost
+    """The recursion with the synthesis fused in (scaled: fase_iterate_scaled
+    with a synth block; exact: fase_iterate_synth) writes the same lost
     samples, bit for bit, as the recursion followed by fase_synth_paste; the
     plan fuses it for batches of at most one block per SM."""
     from paper_2204_14194_b200 import ExtrapolationPlan
@@ -751,25 +752,35 @@ def test_fused_synthesis_bit_identical(spec, m, loss, nb):
     dev = torch.device(DEV)
     t = build_gram_tables(d, build_weight_field(mask, cfg.rho_hat), device=dev)
     sig = torch.from_numpy(np.random.default_rng(3).uniform(0, 255, (nb, m, m))).to(dev)
-    p = ExtrapolationPlan(d, mask, nb, cfg, t, device=dev, recursion="scaled")
-    assert p.fused_synth
-    p.run(sig)
-    K, n = len(d), p.n_lost
-    sel, proj, coef = (torch.empty_like(x) for x in (p.selected, p.projections, p.coefficients))
-    lost = torch.zeros_like(p.lost)
-    _native.iterate_scaled(p.Gs, p.D, p.R0, K, cfg.iterations, cfg.gamma, sel, proj, coef)
-    _native.synth_paste(p.phi_lost, sel, coef, cfg.iterations, p.lost_seq, lost, n_shared=n,
-                        dst=p.lost_pos)
-    torch.cuda.synchronize()
-    assert torch.equal(sel, p.selected) and torch.equal(coef, p.coefficients)
-    assert torch.equal(lost[:, :n], p.lost[:, :n])
-    # capacity guard: more lost samples than the fused kernel holds is refused
-    cap = _native.scaled_synth_capacity(K, nb)
-    big = torch.zeros((K, cap + 2), dtype=torch.float64, device=dev)
-    with pytest.raises(UnsupportedDictionaryError):
-        _native.iterate_scaled(p.Gs, p.D, p.R0, K, cfg.iterations, cfg.gamma, sel, proj, coef,
-                               phi_lost=big, n_lost=cap + 1,
-                               lost=torch.zeros((nb, cap + 2), dtype=torch.float64, device=dev))
+    for rec in ("scaled", "exact"):
+        p = ExtrapolationPlan(d, mask, nb, cfg, t, device=dev, recursion=rec)
+        K, n = len(d), p.n_lost
+        if rec == "exact" and _native.synth_capacity(K, nb) < n:  # no latency shape for this K
+            assert not p.fused_synth
+            continue
+        assert p.fused_synth
+        p.run(sig)
+        sel, proj, coef = (torch.empty_like(x) for x in (p.selected, p.projections,
+                                                         p.coefficients))
+        lost = torch.zeros_like(p.lost)
+        if rec == "scaled":
+            _native.iterate_scaled(p.Gs, p.D, p.R0, K, cfg.iterations, cfg.gamma, sel, proj, coef)
+        else:
+            _native.iterate(p.G, p.D, p.R0, K, cfg.iterations, cfg.gamma, sel, proj, coef)
+        _native.synth_paste(p.phi_lost, sel, coef, cfg.iterations, p.lost_seq, lost, n_shared=n,
+                            dst=p.lost_pos)
+        torch.cuda.synchronize()
+        assert torch.equal(sel, p.selected) and torch.equal(coef, p.coefficients)
+        assert torch.equal(lost[:, :n], p.lost[:, :n])
+        # capacity guard: more lost samples than the fused kernel holds is refused
+        cap = (_native.scaled_synth_capacity(K, nb) if rec == "scaled"
+               else _native.synth_capacity(K, nb))
+        big = torch.zeros((K, cap + 2), dtype=torch.float64, device=dev)
+        fn = _native.iterate_scaled if rec == "scaled" else _native.iterate
+        with pytest.raises(UnsupportedDictionaryError):
+            fn(p.Gs if rec == "scaled" else p.G, p.D, p.R0, K, cfg.iterations, cfg.gamma, sel,
+               proj, coef, phi_lost=big, n_lost=cap + 1,
+               lost=torch.zeros((nb, cap + 2), dtype=torch.float64, device=dev))
 
 
 @pytest.mark.parametrize("nb,n_lost,I,stop", [(300, 256, 200, None), (160, 576, 37, 20),
