@@ -93,11 +93,21 @@ def case_exact_plain():
 
 
 def case_exact_latency():
-    """Latency variant (at most one block per SM), K = 2304."""
+    """Latency variants (at most one block per SM), K = 2304: register-staged
+    rows, exact and scaled, with the synthesis fused in (fase_iterate_synth /
+    fase_iterate_scaled) and separate."""
     d = parse_dict_spec("dct", 48, 48)
     mask = wl.central_loss_mask(48, 48, 16, 16)
     r = fase_extrapolate_batch(sig(2, 48, 48), mask, d, None, ExtrapConfig(6), device=DEV)
-    return [r.selected, r.coefficients, r.patched]
+    outs = [r.selected, r.coefficients, r.patched]
+    cfg = ExtrapConfig(10)
+    t = build_gram_tables(d, build_weight_field(mask, cfg.rho_hat), device=DEV)
+    for rec in ("exact", "scaled"):
+        p = ExtrapolationPlan(d, mask, 2, cfg, t, device=DEV, recursion=rec)
+        assert p.fused_synth
+        p.run(torch.from_numpy(sig(2, 48, 48)).to(DEV))
+        outs += [p.selected.clone(), p.coefficients.clone(), p.lost.clone()]
+    return outs
 
 
 def case_exact_paired():
