@@ -407,10 +407,33 @@ def build_gram_tables(dictionary: Dictionary, weight, *, block: int = 256, count
     return GramTable(G=G, D=D, source=(dictionary, w.copy()), n_alive=int(alive.item()))
 
 
+def _complex_field(signal):
+    """The signal as a 2-D complex128 field when it carries a non-zero imaginary
+    part (``grid.as_field``'s coercion, ``grid.py:26-33``), else None."""
+    arr = np.asarray(signal)
+    if not np.iscomplexobj(arr) or not np.any(arr.imag != 0):
+        return None
+    if arr.ndim != 2:
+        raise ShapeError(f"field must be 2-D, got shape {arr.shape}")
+    if arr.size == 0:
+        raise ShapeError("field must be non-empty")
+    return np.ascontiguousarray(arr, dtype=np.complex128)
+
+
 def initial_scalar_products(signal, weight, dictionary: Dictionary, *, counter=None,
                             device=None) -> np.ndarray:
-    """R0_k = sum s * w * phi_k over the area (``fast.py:145-157``), on the GPU."""
+    """R0_k = sum s * w * phi_k over the area (``fast.py:145-157``), on the GPU.
+
+    A complex signal s = a + ib (the reference coerces with ``as_field``) gives
+    R0(a) + i R0(b): the real path twice, combined in complex arithmetic."""
     torch = _torch()
+    cs = _complex_field(signal)
+    if cs is not None:
+        ra = initial_scalar_products(cs.real, weight, dictionary, device=device)
+        rb = initial_scalar_products(cs.imag, weight, dictionary, device=device)
+        if counter is not None:
+            counter.fase_initial(cs.size, len(dictionary))
+        return ra + 1j * rb
     s = as_real_field(signal)
     w = np.asarray(weight, dtype=np.float64)
     if w.shape != s.shape:
@@ -578,7 +601,8 @@ def _validate_masks(masks, dictionary: Dictionary, n_blocks: int):
 def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
                            config: ExtrapConfig = ExtrapConfig(), *, products=None,
                            record_products: bool = False, patch: bool = True,
-                           device=None, recursion: str = "exact") -> BatchResult:
+                           device=None, recursion: str = "exact",
+                           _complex_state: bool = False) -> BatchResult:
     """Run FaSE on B independent blocks; equals B calls of ``fase_extrapolate``.
 
     Args:
@@ -603,7 +627,11 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
     F = _signals_on_device(signals, dictionary, dev)
     B = F.shape[0]
     K, M = len(dictionary), dictionary.area
-    cplx = not dictionary.is_real
+    # (_complex_state: complex initial products with a real dictionary -- a
+    # complex signal -- run the complex recursion over the real table; no synthesis)
+    cplx = not dictionary.is_real or _complex_state
+    if _complex_state and (patch or products is None):
+        raise ParameterError("_complex_state needs given products and patch=False")
     kmax = _native.max_atoms_complex() if cplx else _native.max_atoms()
     if K > kmax:
         raise UnsupportedDictionaryError(f"K={K} exceeds the iteration kernel's {kmax}")
@@ -1146,7 +1174,8 @@ def fase_extrapolate(signal, mask, dictionary: Dictionary, tables: GramTable,
     provenance (StaleTableError), all-degenerate (NoSelectableAtomError).
     Returns (SparseModel, IterationTrace) with host arrays.
     """
-    s = as_real_field(signal)
+    cs = _complex_field(signal)  # complex signals: products R0(re) + i R0(im)
+    s = as_real_field(signal) if cs is None else np.ascontiguousarray(cs.real)
     mask = as_mask(mask)
     if mask.shape != s.shape:
         raise ShapeError(f"signal {s.shape} vs mask {mask.shape}")
@@ -1165,8 +1194,13 @@ def fase_extrapolate(signal, mask, dictionary: Dictionary, tables: GramTable,
         if p.shape != (len(dictionary),):
             raise ShapeError(f"products shape {p.shape}, expected ({len(dictionary)},)")
         products = p.reshape(1, -1)
+    elif cs is not None:
+        products = initial_scalar_products(cs, w, dictionary, device=device).reshape(1, -1)
+    cstate = (dictionary.is_real and products is not None and np.iscomplexobj(products)
+              and bool(np.any(np.asarray(products).imag != 0)))
     res = fase_extrapolate_batch(s[None], mask, dictionary, tables, config, products=products,
-                                 record_products=record_products, patch=False, device=device)
+                                 record_products=record_products, patch=False, device=device,
+                                 _complex_state=cstate)
     model, trace = res.block(0)
     if counter is not None:
         if products is None:
@@ -1204,12 +1238,19 @@ def apply_model(signal, model: SparseModel, mask, *, device=None):
     idx = np.flatnonzero(mask.ravel()).astype(np.int32)
     g = torch.zeros((1, s.size), dtype=torch.float64, device=dev)
     if dictionary.is_real:
-        if np.any(coefs.imag != 0):
-            raise UnsupportedDictionaryError("complex coefficients for a real dictionary")
+        # g = sum c * phi with real atoms: Re g and Im g are the real synthesis
+        # of Re c and Im c (numpy's complex product with a zero imaginary part
+        # rounds each component once, as here); complex coefficients come from
+        # complex signals
         coef = torch.from_numpy(coefs.real.reshape(1, -1).copy()).to(dev)
-        _native.synth_paste(phi, sel, coef, len(model.terms), torch.from_numpy(idx).to(dev), g,
-                            n_shared=int(idx.size))
+        idx_d = torch.from_numpy(idx).to(dev)
+        _native.synth_paste(phi, sel, coef, len(model.terms), idx_d, g, n_shared=int(idx.size))
         max_imag = 0.0
+        if np.any(coefs.imag != 0):
+            gi = torch.zeros_like(g)
+            ci = torch.from_numpy(coefs.imag.reshape(1, -1).copy()).to(dev)
+            _native.synth_paste(phi, sel, ci, len(model.terms), idx_d, gi, n_shared=int(idx.size))
+            max_imag = float(gi.abs().max().item())
     else:
         coef = torch.from_numpy(coefs.reshape(1, -1).copy()).to(dev)
         mi = torch.zeros(1, dtype=torch.float64, device=dev)

@@ -838,3 +838,38 @@ def test_maximum_atom_count():
     with pytest.raises(UnsupportedDictionaryError):
         fase_extrapolate_batch(sig, mask, Dictionary(rng.standard_normal((kmax + 1, m, n))),
                                None, cfg, device=DEV)
+
+
+@pytest.mark.parametrize("spec", ["dft", "dct", "union:dct+dft"])
+def test_complex_signals(spec):
+    """Complex signals (the reference's as_field coercion; its own
+    test_initial_products_match_bruteforce uses one): initial products equal the
+    oracle's conj(Phi) (s o w) to 1e-13; fase_extrapolate selects exactly the
+    oracle loop's atoms on the same products and table, for real dictionaries
+    (complex state over the real table) and complex ones; apply_model returns
+    Re g with max |Im g|."""
+    from paper_2204_14194_b200 import apply_model, initial_scalar_products
+
+    rng = np.random.default_rng(4)
+    m = n = 8
+    d = parse_dict_spec(spec, m, n)
+    mask = wl.central_loss_mask(m, n, 3, 3)
+    w = build_weight_field(mask, 0.8)
+    s = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    vals = d.values.reshape(len(d), -1).astype(np.complex128)
+    r0 = initial_scalar_products(s, w, d, device=DEV)
+    want = orc.initial_products(s, w, vals)
+    assert np.abs(r0 - want).max() <= 1e-13 * np.abs(want).max()
+    cfg = ExtrapConfig(25, 0.5, 0.8)
+    t = build_gram_tables(d, w, device=DEV)
+    model, trace = fase_extrapolate(s, mask, d, t, cfg, device=DEV)
+    c, dd = orc.gram(vals, w)
+    sel, _, coef, _ = orc.fase_run(r0, c, dd, cfg.gamma, cfg.iterations)
+    assert np.array_equal(trace.selected, sel)
+    assert np.abs(trace.coefficients - coef).max() <= 1e-12 * np.abs(coef).max()
+    out, max_imag = apply_model(s, model, mask, device=DEV)
+    g = orc.materialize(d.values, trace.selected, trace.coefficients)
+    assert out.dtype == np.complex128
+    assert np.abs(out[mask] - g.real[mask]).max() <= 1e-12 * np.abs(g).max()
+    assert np.array_equal(out[~mask], s[~mask])
+    assert abs(max_imag - np.abs(g.imag[mask]).max()) <= 1e-12 * np.abs(g).max()
