@@ -359,3 +359,36 @@ def test_complex_scaled_matches_exact_and_dead_atoms():
     r = fase_extrapolate_batch(np.random.default_rng(2).standard_normal((3, 4, 4)), m4, dd, None,
                                ExtrapConfig(10), device=DEV, recursion="scaled")
     assert (r.selected.cpu().numpy() != 0).all()
+
+
+def test_maximum_atom_count_complex():
+    """K at the largest complex recursion variant: the exact complex recursion
+    is bit-exact against the oracle's loop on the same device-built table,
+    normalizers and initial products; one atom more raises
+    UnsupportedDictionaryError."""
+    from paper_2204_14194_b200 import (ExtrapConfig, UnsupportedDictionaryError, _native,
+                                       build_gram_tables, build_weight_field,
+                                       fase_extrapolate_batch, initial_scalar_products)
+
+    kmax = _native.max_atoms_complex()
+    rng = np.random.default_rng(21)
+    m = n = 16
+    mask = wl.central_loss_mask(m, n, 6, 6)
+    vals = rng.standard_normal((kmax, m, n)) + 1j * rng.standard_normal((kmax, m, n))
+    d = Dictionary(vals)
+    cfg = ExtrapConfig(15, 0.5, 0.8)
+    sig = rng.uniform(0, 255, (2, m, n))
+    w = build_weight_field(mask, cfg.rho_hat)
+    t = build_gram_tables(d, w, device=DEV)
+    r0 = np.stack([initial_scalar_products(sig[b], w, d, device=DEV) for b in range(2)])
+    res = fase_extrapolate_batch(sig, mask, d, t, cfg, device=DEV, patch=False, products=r0)
+    G, D = t.device_tables(torch.device(DEV), complex_rows=True)
+    c = np.conj(G[:, :kmax].cpu().numpy())
+    dd = D.cpu().numpy()
+    for b in range(2):
+        sel, _, coef, _ = orc.fase_run(r0[b], c, dd, cfg.gamma, cfg.iterations)
+        assert np.array_equal(res.selected[b].cpu().numpy(), sel)
+        assert np.array_equal(res.coefficients[b].cpu().numpy(), coef)
+    with pytest.raises(UnsupportedDictionaryError):
+        fase_extrapolate_batch(sig, mask, Dictionary(vals[:1].repeat(kmax + 1, axis=0)), None,
+                               cfg, device=DEV)
