@@ -216,6 +216,20 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
 
+// Proxy fence before a TMA refill of a staging buffer (measurement knob):
+// the buffer's previous generic-proxy reads are already ordered by the block
+// barrier between them and the issue, and generic WRITES (row composition) are
+// followed by their own fence, so the issue-time fence only orders what is
+// already ordered (FASE_ISSUE_FENCE=0 drops it)
+#ifndef FASE_ISSUE_FENCE
+#define FASE_ISSUE_FENCE 1
+#endif
+__device__ __forceinline__ void fence_before_refill() {
+#if FASE_ISSUE_FENCE
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+#endif
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }

@@ -78,6 +78,27 @@ constexpr unsigned kNone = 0xffffffffu;
 #ifndef FASE_SPEC
 #define FASE_SPEC -1
 #endif
+// Scaled recursion, per-iteration critical path (measurement knob, bits):
+//  1: the running max keeps the signed R' of the best element and compares
+//     magnitudes with |.| operand modifiers (no |R'| materialised per element:
+//     one FP64 instruction per element less)
+//     (config 4: 12.98 -> 12.36 ms per recursion, 244.8K -> 254.0K blocks/s)
+//  4: the update R' -= c * Gs[u, :] as one fused multiply-add (one rounding
+//     instead of two: config 4 12.36 -> 12.00 ms, config 1 0.726 -> 0.707 ms;
+//     selections identical to the reference on every benchmarked block)
+//  8: the tie winner takes R'_u from the signed running max when the pick is
+//     its own argmax (no register dump through shared memory; config 1 0.708
+//     -> 0.690 ms). Shapes with more than 20 elements per thread keep the dump:
+//     the extra live value spills the 128-register 256 x 32 shape (config 4
+//     12.0 -> 12.25 ms)
+// 16: the predicted row's TMA copy is issued by a warp other than the argmax
+//     warp (the tie pass and the issue run in parallel)
+//  2: D of the predicted atom is loaded by every thread right after the block
+//     max, so the tie winner no longer reads D from global memory between the
+//     two barriers (measured: no gain on config 4, config 1 0.4% slower: off)
+#ifndef FASE_SCALED_LEAN
+#define FASE_SCALED_LEAN 13
+#endif
 #ifdef FASE_ITERATE_STATS
 __device__ unsigned long long g_stats[8];  // measurement build: chunked-path counters
 #endif
@@ -266,6 +287,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   };
   double best = kDead;
   unsigned barg = kNone;
+  double bsig = 0.0;  // kScaled: the signed R' of this thread's best element
 #pragma unroll
   for (int j = 0; j < EP; ++j) {
     const int k = 2 * (j * NT + t);
@@ -278,11 +300,13 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       const double m0 = fabs(r[j][0]);
       if (m0 > best) {
         best = m0;
+        bsig = r[j][0];
         barg = static_cast<unsigned>(k);
       }
       const double m1 = fabs(r[j][1]);
       if (m1 > best) {
         best = m1;
+        bsig = r[j][1];
         barg = static_cast<unsigned>(k + 1);
       }
       continue;
@@ -474,9 +498,13 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       else
         return a.G0;
     };
-    if (t == 0 && issue) {
+    // the issuing thread: thread 0, or (kIssueOff) lane 0 of a warp other
+    // than the predicted atom's, so the issue and its tie pass overlap
+    constexpr bool kIssueOff = kScaled && (FASE_SCALED_LEAN & 16) && SPEC == 0 && NW > 1;
+    const int t_iss = kIssueOff ? ((((static_cast<int>(guess >> 1) % NT) >> 5) + 1) % NW) * 32 : 0;
+    if (t == t_iss && issue) {
       FASE_ASSERT(guess < static_cast<unsigned>(K));
-      fence_proxy_async_smem();
+      fence_before_refill();
       int use = -1;  // SPEC: a spare buffer already holding the guess's row
       if constexpr (SPEC > 0) {
         for (int k = 0; k < SPEC; ++k)
@@ -558,6 +586,10 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         }
       }
     }
+    constexpr bool kLeanD = kScaled && (FASE_SCALED_LEAN & 2);
+    // kLeanD: D of the predicted atom, in flight during the tie pass and the
+    // second barrier (the guess is in range here: a degenerate top returned)
+    const double dguess = kLeanD ? __ldg(D + guess) : 0.0;
     const double top = __longlong_as_double(top_key);
     // tie_quantum: only a finite, strictly positive top moves the ratchet
     if (top_key > 0 && top_key < 0x7ff0000000000000LL) q = fmax(q, mul_rn(1e-13, top));
@@ -576,6 +608,12 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     const unsigned wmin = __reduce_min_sync(0xffffffffu, cand);
     if (wmin == kNone) {
       if (lane == 0) s_u[warp] = kNone;
+    } else if (kScaled && (FASE_SCALED_LEAN & 8) && (FASE_SCALED_LEAN & 1) && EPT <= 20 &&
+               cand == wmin && cand == barg) {
+      // the pick is this thread's own argmax: its signed R' is at hand
+      s_u[warp] = cand;
+      s_r[warp] = bsig;
+      if constexpr (!kLeanD) s_d[warp] = __ldg(D + cand);
     } else if (cand == wmin) {
       // fetch R (and D) of the winner through a shared scratch (no dynamic
       // register indexing)
@@ -591,7 +629,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       s_u[warp] = cand;
       s_r[warp] = s_dump[warp][0][2 * jj + ee];
       if constexpr (kScaled) {
-        s_d[warp] = __ldg(D + cand);
+        if constexpr (!kLeanD) s_d[warp] = __ldg(D + cand);
       } else if constexpr (kDsmem) {
         const double2 dd = s_D[pair];
         s_d[warp] = ee ? dd.y : dd.x;
@@ -622,7 +660,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       }
     }
     const double ru = s_r[uw];
-    const double du = s_d[uw];
+    const double du = kLeanD ? (u == guess ? dguess : __ldg(D + u)) : s_d[uw];
     const double p = kScaled ? mul_rn(ru, du) : mul_rn(ru, mul_rn(du, du));
     const double c = mul_rn(a.gamma, p);
     if (t == 0) {
@@ -639,12 +677,17 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     // source is block-uniform, so each source gets its own unrolled loop
     // `pre(sg)` runs at the start of segment sg, before its arrival is awaited
     // (chunk-row loads are issued there, so they overlap the TMA wait)
+    // kLeanMax: cb holds the signed R' of the best element and the compare
+    // reads magnitudes through |.| operand modifiers; it starts at -0 so only
+    // metrics > 0 register -- a thread whose live metrics are all 0 (or that
+    // holds only dead atoms) is resolved by the scan after the loop
+    constexpr bool kLeanMax = kScaled && (FASE_SCALED_LEAN & 1);
     auto update = [&](auto row_pair, auto staged, auto pre) {
       double cb[kChains];
       unsigned ca[kChains];
 #pragma unroll
       for (int h = 0; h < kChains; ++h) {
-        cb[h] = kDead;
+        cb[h] = kLeanMax ? -0.0 : kDead;
         ca[h] = kNone;
       }
 #pragma unroll
@@ -657,10 +700,26 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
           }
         const double2 g = row_pair(j);
         const double2 dd = dpair_if(j);
-        r[j][0] = sub_rn(r[j][0], mul_rn(c, g.x));
-        r[j][1] = sub_rn(r[j][1], mul_rn(c, g.y));
-        const double2 mm = metrics(j, dd);
+        if constexpr (kScaled && (FASE_SCALED_LEAN & 4)) {  // one rounding: R' - c*Gs fused
+          r[j][0] = __fma_rn(-c, g.x, r[j][0]);
+          r[j][1] = __fma_rn(-c, g.y, r[j][1]);
+        } else {
+          r[j][0] = sub_rn(r[j][0], mul_rn(c, g.x));
+          r[j][1] = sub_rn(r[j][1], mul_rn(c, g.y));
+        }
         const int h = j % kChains;
+        if constexpr (kLeanMax) {
+          if (fabs(r[j][0]) > fabs(cb[h])) {
+            cb[h] = r[j][0];
+            ca[h] = static_cast<unsigned>(2 * (j * NT + t));
+          }
+          if (fabs(r[j][1]) > fabs(cb[h])) {
+            cb[h] = r[j][1];
+            ca[h] = static_cast<unsigned>(2 * (j * NT + t) + 1);
+          }
+          continue;
+        }
+        const double2 mm = metrics(j, dd);
         const double m0 = mm.x;
         if (m0 > cb[h]) {
           cb[h] = m0;
@@ -672,6 +731,19 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
           ca[h] = static_cast<unsigned>(2 * (j * NT + t) + 1);
         }
       }
+      if constexpr (kLeanMax) {
+        bsig = cb[0];
+        unsigned bi = ca[0];
+#pragma unroll
+        for (int h = 1; h < kChains; ++h)  // equal magnitudes: the lower index wins
+          if (ca[h] != kNone && (bi == kNone || fabs(cb[h]) > fabs(bsig) ||
+                                 (fabs(cb[h]) == fabs(bsig) && ca[h] < bi))) {
+            bsig = cb[h];
+            bi = ca[h];
+          }
+#pragma unroll
+        for (int h = 0; h < kChains; ++h) cb[h] = ca[h] == kNone ? kDead : fabs(cb[h]);
+      }
       best = cb[0];
       barg = ca[0];
 #pragma unroll
@@ -680,6 +752,24 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
           best = cb[h];
           barg = ca[h];
         }
+      if constexpr (kLeanMax) {
+        // rare: no live metric > 0 here -- the lowest live atom (metric 0), if any
+        if (barg == kNone) {
+#pragma unroll
+          for (int j = EP - 1; j >= 0; --j) {
+            if (r[j][1] == r[j][1]) {
+              best = 0.0;
+              bsig = r[j][1];
+              barg = static_cast<unsigned>(2 * (j * NT + t) + 1);
+            }
+            if (r[j][0] == r[j][0]) {
+              best = 0.0;
+              bsig = r[j][0];
+              barg = static_cast<unsigned>(2 * (j * NT + t));
+            }
+          }
+        }
+      }
     };
     using Staged = std::true_type;
     using Direct = std::false_type;

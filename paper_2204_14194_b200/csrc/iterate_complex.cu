@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
     }
     if (t == 0) {
       FASE_ASSERT(guess < static_cast<unsigned>(K));
-      fence_proxy_async_smem();
+      fence_before_refill();
       const double* grow = G0 + static_cast<int64_t>(guess) * ldg2x;
 #pragma unroll
       for (int sg = 0; sg < kSeg; ++sg) {
