@@ -78,6 +78,12 @@ constexpr unsigned kNone = 0xffffffffu;
 #ifndef FASE_SPEC
 #define FASE_SPEC -1
 #endif
+// chunked recursion: start stagger of up to N ns per block (measurement knob;
+// measured no effect on configs 2 / 3 at 2 and 8 us: the DRAM-resident row
+// fetches are latency-, not burst-bound)
+#ifndef FASE_STAGGER_NS
+#define FASE_STAGGER_NS 0
+#endif
 // Scaled recursion, per-iteration critical path (measurement knob, bits):
 //  1: the running max keeps the signed R' of the best element and compares
 //     magnitudes with |.| operand modifiers (no |R'| materialised per element:
@@ -340,6 +346,11 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     __syncthreads();  // the shared D (written by half 0) is complete
     if (!active) return;
   }
+#if FASE_STAGGER_NS > 0
+  // measurement: desynchronise the blocks' row requests (per-block geometries
+  // read their rows mostly from DRAM, in bursts when every block iterates in step)
+  if constexpr (kChunked) __nanosleep(static_cast<unsigned>((blockIdx.x * 5u) % 8u) * (FASE_STAGGER_NS / 8));
+#endif
 
   int32_t* sel = a.sel + static_cast<int64_t>(b) * a.ldo;
   double* proj = a.proj + static_cast<int64_t>(b) * a.ldo;

@@ -45,6 +45,10 @@ namespace {
 
 constexpr unsigned kNone = 0xffffffffu;
 constexpr int kCap = 64;  // candidate list capacity
+// scaled recursion: the update as fused multiply-adds (measurement knob)
+#ifndef FASE_CSCALED_FMA
+#define FASE_CSCALED_FMA 1
+#endif
 
 // NB == 2 (shared geometry, D^2 in shared memory): one CTA runs two blocks on
 // its two NT-thread halves (own staged row, candidate list, named barriers)
@@ -414,9 +418,16 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
             if (j == sg * EP / kSeg) mbar_wait(&s_bar[sg], it & 1);
         }
         const double2 g = row_elem(j);
-        const double2 x = np_cmul(cr, ci, g.x, g.y);
-        r[j][0] = sub_rn(r[j][0], x.x);
-        r[j][1] = sub_rn(r[j][1], x.y);
+        if constexpr (kScaled && FASE_CSCALED_FMA) {
+          // scaled recursion: R' - c * row fused (two roundings per component
+          // instead of numpy's three)
+          r[j][0] = __fma_rn(ci, g.y, __fma_rn(-cr, g.x, r[j][0]));
+          r[j][1] = __fma_rn(-ci, g.x, __fma_rn(-cr, g.y, r[j][1]));
+        } else {
+          const double2 x = np_cmul(cr, ci, g.x, g.y);
+          r[j][0] = sub_rn(r[j][0], x.x);
+          r[j][1] = sub_rn(r[j][1], x.y);
+        }
         const double pk = proxy(r[j][0], r[j][1], d2_if(j));
         if (pk > best) {
           best = pk;
