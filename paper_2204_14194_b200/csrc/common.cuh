@@ -221,6 +221,12 @@ __device__ __forceinline__ void fence_mbar_init() {
 // barrier between them and the issue, and generic WRITES (row composition) are
 // followed by their own fence, so the issue-time fence only orders what is
 // already ordered (FASE_ISSUE_FENCE=0 drops it)
+// Scaled recursion variants (bits; see iterate.cu): 1 signed running max,
+// 2 D prefetch, 4 fused update (iterate.cu and iterate_cluster.cu), 8 tie-dump
+// shortcut, 16 issue-warp offset
+#ifndef FASE_SCALED_LEAN
+#define FASE_SCALED_LEAN 13
+#endif
 #ifndef FASE_ISSUE_FENCE
 #define FASE_ISSUE_FENCE 1
 #endif

@@ -102,9 +102,7 @@ constexpr unsigned kNone = 0xffffffffu;
 //  2: D of the predicted atom is loaded by every thread right after the block
 //     max, so the tie winner no longer reads D from global memory between the
 //     two barriers (measured: no gain on config 4, config 1 0.4% slower: off)
-#ifndef FASE_SCALED_LEAN
-#define FASE_SCALED_LEAN 13
-#endif
+// (FASE_SCALED_LEAN is defined in common.cuh: the cluster recursion follows bit 4 too)
 #ifdef FASE_ITERATE_STATS
 __device__ unsigned long long g_stats[8];  // measurement build: chunked-path counters
 #endif

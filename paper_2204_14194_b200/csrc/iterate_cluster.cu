@@ -328,8 +328,13 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(NT, 1)
     best = kDead;
     barg = kNoneC;
     auto step = [&](int j, double2 g) {
-      r[j][0] = sub_rn(r[j][0], mul_rn(c, g.x));
-      r[j][1] = sub_rn(r[j][1], mul_rn(c, g.y));
+      if constexpr (kScaled && (FASE_SCALED_LEAN & 4)) {  // as the one-CTA scaled kernel
+        r[j][0] = __fma_rn(-c, g.x, r[j][0]);
+        r[j][1] = __fma_rn(-c, g.y, r[j][1]);
+      } else {
+        r[j][0] = sub_rn(r[j][0], mul_rn(c, g.x));
+        r[j][1] = sub_rn(r[j][1], mul_rn(c, g.y));
+      }
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const double m = kScaled ? fabs(r[j][e]) : mul_rn(fabs(r[j][e]), dreg[j][kScaled ? 0 : e]);
