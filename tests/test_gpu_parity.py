@@ -448,6 +448,39 @@ def test_degenerate_atoms_never_selected_and_all_dead_raises():
         fase_extrapolate(np.ones((4, 4)), mask, dead, td, device=DEV)
 
 
+@pytest.mark.parametrize("blocks", [3, 200])
+def test_scaled_recursion_zero_metrics_and_dead_atoms(blocks):
+    """The scaled recursion's running max keeps the signed R' and starts at
+    -0, so all-zero metrics take the lowest live atom through its fallback
+    scan: zero signals select atom 0 (pkg/tests/test_reference.py:186-191), and
+    with atom 0 dead (zero weighted energy) atom 1, exactly like the bit-exact
+    kernel; one-CTA shapes (200 blocks) and latency / cluster shapes (3)."""
+    mask = wl.central_loss_mask(4, 4, 2, 2)
+    inside = np.zeros((4, 4))
+    inside[1:3, 1:3] = 1.0
+    base = generate_dictionary("dct", 4, 4).real_values()
+    cfg = ExtrapConfig(6)
+    for vals, first in ((base, 0), (np.concatenate([inside[None], base]), 1)):
+        d = Dictionary(vals)
+        zero = np.zeros((blocks, 4, 4))
+        out = {}
+        for rec in ("exact", "scaled"):
+            r = fase_extrapolate_batch(zero, mask, d, None, cfg, device=DEV, recursion=rec)
+            out[rec] = r
+            assert (r.selected.cpu().numpy() == first).all(), rec
+            assert (r.coefficients.cpu().numpy() == 0.0).all(), rec
+        # a live signal in one block: the others stay at the first live atom
+        sig = zero.copy()
+        sig[blocks // 2] = np.random.default_rng(5).standard_normal((4, 4))
+        a = fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion="exact")
+        b = fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion="scaled")
+        assert torch.equal(a.selected, b.selected)
+        sel = b.selected.cpu().numpy()
+        assert (np.delete(sel, blocks // 2, axis=0) == first).all()
+        if first == 1:
+            assert (sel != 0).all()
+
+
 def test_stale_tables_detected():
     d = generate_dictionary("dct", 4, 4)
     mask = wl.central_loss_mask(4, 4, 2, 2)
