@@ -226,6 +226,7 @@ struct SepPartsArg {
   int lc[kSepMaxParts];
   int64_t col0[kSepMaxParts];
   int n;
+  int stage;  // small batches: factor tables staged in shared memory (fits)
 };
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
@@ -268,12 +269,16 @@ __device__ __forceinline__ void macro_nt(FA fa, FB fb, int r0, int c0, int kk, d
 // MINB 4 for batches that fill the GPU: four CTAs per SM (56 registers, no
 // spills; three at 70 registers), config-1 products 0.080 -> 0.074 ms. Small
 // batches keep the unconstrained allocation (latency: config 0 0.021 ms
-// against 0.031 ms at 56 registers).
+// against 0.031 ms at 56 registers), and (kStage) copy their part's factor
+// tables into shared memory with async copies issued alongside the area's
+// loads: one round of memory latency, where the operand stream's one-step
+// prefetch waited on a cold line every few k-steps.
 template <int MINB>
 __global__ void __launch_bounds__(288, MINB) sep_products_dmma_kernel(
     const SepPartsArg parts, int Mr, int Nc, const double* __restrict__ F, int64_t ldf,
     const double* __restrict__ W, int64_t ldw, double* __restrict__ R0, int64_t ldr) {
   extern __shared__ __align__(16) double sm[];
+  constexpr bool kStage = MINB == 1;
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31, fr = lane >> 2, fc = lane & 3;
@@ -281,8 +286,43 @@ __global__ void __launch_bounds__(288, MINB) sep_products_dmma_kernel(
   const int sx = Nk + ((4 - Nk) & 15), st = Mk + ((4 - Mk) & 15);  // strides = 4 (mod 16)
   double* sX = sm;                   // Mp x sx: X[m][n], zero padded
   double* sT = sm + Mp * sx;         // Lcp x st: T[v][m]
+  int lcp_max = 16;
+  for (int p = 0; p < parts.n; ++p) lcp_max = max(lcp_max, (parts.lc[p] + 15) & ~15);
+  double* sC = sT + lcp_max * st;    // kStage: cols of this CTA's part, Lcp x sx
+  double* sR = sC + lcp_max * sx;    // kStage: its slice of rows, 16*per x st
   const double* f = F + static_cast<int64_t>(b) * ldf;
   const double* w = W ? W + static_cast<int64_t>(b) * ldw : nullptr;
+  // small batches split the work over gridDim.y CTAs per block: part p =
+  // y / splits, and a slice of 16-row groups of u for product 2 (T is formed by
+  // every slice of the part)
+  const int splits = gridDim.y > 1 ? static_cast<int>(gridDim.y) / parts.n : 1;
+  const int p_first = gridDim.y > 1 ? static_cast<int>(blockIdx.y) / splits : 0;
+  const int p_last = gridDim.y > 1 ? p_first + 1 : parts.n;
+  const int slice = gridDim.y > 1 ? static_cast<int>(blockIdx.y) % splits : 0;
+  // kStage (one part per CTA): the part's cols and the rows of its u slice,
+  // zero padded, as async copies in flight with the area's loads below
+  const bool stage = kStage && parts.stage && p_last == p_first + 1;
+  int u_lo = 0;
+  if (stage) {
+    const int p = p_first, Lr = parts.lr[p], Lc = parts.lc[p];
+    const int tm_all = ((Lr + 15) & ~15) / 16, per = (tm_all + splits - 1) / splits;
+    u_lo = slice * per * 16;
+    const int u_n = max(0, min(tm_all * 16, u_lo + per * 16) - u_lo);
+    const double* cols = parts.cols[p];
+    const double* rows = parts.rows[p];
+    const int nc = ((Lc + 15) & ~15) * sx, nr = u_n * st;
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      const int v = i / sx, n = i - v * sx;
+      const bool in = v < Lc && n < Nc;
+      cp_async8(sC + i, in ? cols + v * Nc + n : cols, in ? 8 : 0);
+    }
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+      const int uu = i / st, m = i - uu * st, u = u_lo + uu;
+      const bool in = u < Lr && m < Mr;
+      cp_async8(sR + i, in ? rows + u * Mr + m : rows, in ? 8 : 0);
+    }
+    cp_async_commit();
+  }
   // zero the padding, then stage the area with independent loads in flight
   for (int i = threadIdx.x; i < Mp * sx; i += blockDim.x) {
     const int m = i / sx, n = i - m * sx;
@@ -306,13 +346,7 @@ __global__ void __launch_bounds__(288, MINB) sep_products_dmma_kernel(
       }
     }
   }
-  // small batches split the work over gridDim.y CTAs per block: part p =
-  // y / splits, and a slice of 16-row groups of u for product 2 (T is formed by
-  // every slice of the part)
-  const int splits = gridDim.y > 1 ? static_cast<int>(gridDim.y) / parts.n : 1;
-  const int p_first = gridDim.y > 1 ? static_cast<int>(blockIdx.y) / splits : 0;
-  const int p_last = gridDim.y > 1 ? p_first + 1 : parts.n;
-  const int slice = gridDim.y > 1 ? static_cast<int>(blockIdx.y) % splits : 0;
+  if (stage) cp_async_wait<0>();
   for (int p = p_first; p < p_last; ++p) {
     const double* rows = parts.rows[p];
     const double* cols = parts.cols[p];
@@ -321,7 +355,10 @@ __global__ void __launch_bounds__(288, MINB) sep_products_dmma_kernel(
     __syncthreads();  // sX staged / previous part's sT consumed
     // T[v][m] = sum_n cols[v][n] X[m][n]
     {
-      auto fa = [&](int v, int n) { return (v < Lc && n < Nc) ? __ldg(cols + v * Nc + n) : 0.0; };
+      auto fa = [&](int v, int n) {
+        if (stage) return sC[v * sx + n];
+        return (v < Lc && n < Nc) ? __ldg(cols + v * Nc + n) : 0.0;
+      };
       auto fb = [&](int m, int n) { return sX[m * sx + n]; };
       const int tm = Lcp / 16, tn = Mp / 16;
       for (int t = warp; t < tm * tn; t += nwarps) {
@@ -342,7 +379,10 @@ __global__ void __launch_bounds__(288, MINB) sep_products_dmma_kernel(
     __syncthreads();
     // out[u][v] = sum_m rows[u][m] T[v][m]  ->  R0[b, col0 + u*Lc + v]
     {
-      auto fa = [&](int u, int m) { return (u < Lr && m < Mr) ? __ldg(rows + u * Mr + m) : 0.0; };
+      auto fa = [&](int u, int m) {
+        if (stage) return sR[(u - u_lo) * st + m];
+        return (u < Lr && m < Mr) ? __ldg(rows + u * Mr + m) : 0.0;
+      };
       auto fb = [&](int v, int m) { return sT[v * st + m]; };
       const int tm_all = Lrp / 16, tn = Lcp / 16;
       const int per = (tm_all + splits - 1) / splits;  // 16-row groups of u per slice
@@ -517,24 +557,36 @@ extern "C" int fase_sep_products_batch(const fase_sep_part* parts, int n_parts, 
   }
   const int Mp = (Mr + 15) / 16 * 16, Nk = (Nc + 3) / 4 * 4, Mk = (Mr + 3) / 4 * 4;
   const int sx = Nk + ((4 - Nk) & 15), st = Mk + ((4 - Mk) & 15);
-  const size_t smem = sizeof(double) * (static_cast<size_t>(Mp) * sx + static_cast<size_t>(lcp_max) * st);
+  size_t smem = sizeof(double) * (static_cast<size_t>(Mp) * sx + static_cast<size_t>(lcp_max) * st);
   if (smem > 200 * 1024) {
     set_error("fase_sep_products_batch: area %dx%d too large for shared memory", Mr, Nc);
     return FASE_ERR_UNSUPPORTED;
   }
   auto kernel = B < 148 ? sep_products_dmma_kernel<1> : sep_products_dmma_kernel<4>;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) {
-    set_error("fase_sep_products_batch: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    return FASE_ERR_CUDA;
-  }
   // batches smaller than the GPU: one CTA per (block, part, slice of u)
   int splits = 1;
   if (B < 148) {
     const int lr_min_groups = (parts[0].Lr + 15) / 16;
     splits = lr_min_groups < 4 ? lr_min_groups : 4;
     if (splits < 1) splits = 1;
+    // staged factor tables: cols Lcp x sx, the rows of a u slice 16*per x st
+    int per_max = 1;
+    for (int p = 0; p < n_parts; ++p) {
+      const int tm_all = (parts[p].Lr + 15) / 16, per = (tm_all + splits - 1) / splits;
+      per_max = per > per_max ? per : per_max;
+    }
+    const size_t staged = smem + sizeof(double) * (static_cast<size_t>(lcp_max) * sx +
+                                                   static_cast<size_t>(16 * per_max) * st);
+    if (staged <= 200 * 1024) {  // else the factors stream from global memory
+      smem = staged;
+      a.stage = 1;
+    }
+  }
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) {
+    set_error("fase_sep_products_batch: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return FASE_ERR_CUDA;
   }
   const dim3 grid(B, B < 148 ? n_parts * splits : 1);
   kernel<<<grid, 288, smem, as_stream(stream)>>>(a, Mr, Nc, F, ldf, W, ldw, R0, ldr);
