@@ -231,6 +231,12 @@ typedef struct {
    * L2 evict_last policy, every other row evict_first, so the hot rows stay
    * L2-resident. NULL: default policy. Does not change any result. */
   const uint32_t* l2_hot;
+  /* optional dispatch order (ABI 3.0): NULL, or a permutation of 0..B-1, and
+   * the i-th CTA (slot) runs block order[i]. Blocks are independent, so only the
+   * schedule changes, never a result: per-block geometries put their costliest
+   * blocks first (fase_block_order) so the last wave holds the cheap ones. The
+   * one-block-over-a-cluster path ignores it. */
+  const int32_t* order;
 } fase_iterate_args;
 
 FASE_API int fase_iterate(const fase_iterate_args* args, void* stream);
@@ -319,6 +325,13 @@ FASE_API int fase_frame_cells(const uint8_t* grid, int64_t ldgrid, int H, int W,
                               int support, const int32_t* corners, int L,
                               const int32_t* cell_rep, int n_cells, int32_t* counts,
                               int32_t* ids, int64_t ids_ld, void* stream);
+/* fase_block_order: order = the blocks 0..B-1 by descending cost class
+ * min(7, max(0, counts[b] - depth)) -- the chunk-table rows a block streams per
+ * iteration beyond its (precomposed) base when compose_depth = depth -- stable
+ * (ascending block index within a class); the fase_iterate_args.order of the
+ * frame's recursion (longest-processing-time-first dispatch). */
+FASE_API int fase_block_order(const int32_t* counts, int B, int depth, int32_t* order,
+                              void* stream);
 FASE_API int fase_frame_paste(const double* phi, int64_t ldphi, const int32_t* sel,
                               const double* coef, int64_t ldo, int I, const uint8_t* grid,
                               int64_t ldgrid, int H, int W, int tile, int support,

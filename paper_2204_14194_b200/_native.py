@@ -39,10 +39,10 @@ EXPORTS = (
     "fase_ozaki_split", "fase_ozaki_gemm", "fase_ozaki_gram", "fase_sep_products_batch",
     "fase_iterate_scaled", "fase_scale_columns", "fase_iterate_scaled_synth_capacity",
     "fase_iterate_complex_scaled", "fase_frame_widen", "fase_frame_paste_complex",
-    "fase_iterate_synth", "fase_iterate_synth_capacity",
+    "fase_iterate_synth", "fase_iterate_synth_capacity", "fase_block_order",
 )
 
-ABI_MAJOR = 2  # fase_abi_version() >> 16 of the library this binding matches
+ABI_MAJOR = 3  # fase_abi_version() >> 16 of the library this binding matches
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int
 _i64 = ctypes.c_int64
@@ -71,7 +71,7 @@ class IterateArgs(ctypes.Structure):
         ("ldr", _i64), ("R_out", _vp), ("R_log", _vp), ("K", _i32), ("B", _i32), ("I", _i32),
         ("gamma", _f64), ("sel", _vp), ("proj", _vp), ("coef", _vp), ("ldo", _i64),
         ("compose", _vp), ("n_compose", _i32), ("compose_depth", _i32), ("base_stride", _i64),
-        ("l2_hot", _vp),
+        ("l2_hot", _vp), ("order", _vp),
     ]
 
 
@@ -155,6 +155,7 @@ def load():
         "fase_frame_paste": [_vp, _i64, _vp, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i32, _i32,
                              _vp, _i32, _vp, _i64, _vp],
         "fase_frame_widen": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _i64, _vp],
+        "fase_block_order": [_vp, _i32, _i32, _vp, _vp],
         "fase_frame_paste_complex": [_vp, _i64, _vp, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i32,
                                      _i32, _vp, _i32, _vp, _i64, _vp, _vp],
     }
@@ -317,13 +318,40 @@ def synth_capacity(K: int, B: int) -> int:
     return int(load().fase_iterate_synth_capacity(K, B))
 
 
+def _order_ptr(order, B: int):
+    import torch
+
+    if order is None:
+        return None
+    _require(order, "order", torch.int32, 1)
+    if order.shape[0] != B:
+        raise errors.ShapeError(f"order must hold one entry per block ({B}), got {order.shape[0]}")
+    return _ptr(order)
+
+
+def block_order(counts, depth: int, order) -> None:
+    """order <- blocks by descending cost class min(7, max(0, counts - depth)),
+    stable (fase_block_order): the dispatch order of a chunked recursion."""
+    import torch
+
+    lib = load()
+    _require(counts, "counts", torch.int32, 1)
+    _require(order, "order", torch.int32, 1)
+    if order.shape[0] != counts.shape[0]:
+        raise errors.ShapeError("order and counts must have one entry per block")
+    _check(lib.fase_block_order(_ptr(counts), counts.shape[0], depth, _ptr(order),
+                                _stream(counts)))
+
+
 def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *,
             chunk_tables=None, chunk_stride: int = 0, chunk_count=None, chunk_ids=None,
             R_out=None, R_log=None, compose=None, base_stride: int = 0, l2_hot=None,
-            phi_lost=None, n_lost: int = 0, lost=None) -> None:
+            phi_lost=None, n_lost: int = 0, lost=None, order=None) -> None:
     """The recursion (fase_iterate). ``compose`` (int32 device table n^depth,
     depth 1..3) with ``base_stride`` selects precomposed base tables at
-    G0 + p * base_stride for the longest prefix of each block's chunk list."""
+    G0 + p * base_stride for the longest prefix of each block's chunk list.
+    ``order`` (int32 (B,) device permutation, optional): CTA i runs block
+    order[i] (a schedule only; ``block_order``)."""
     import torch
 
     lib = load()
@@ -342,7 +370,7 @@ def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *
         proj=_ptr(proj), coef=_ptr(coef), ldo=_ld(sel), compose=_ptr(compose),
         n_compose=compose.shape[0] if compose is not None else 0,
         compose_depth=compose.dim() if compose is not None else 0, base_stride=base_stride,
-        l2_hot=_hot_ptr(l2_hot, K))
+        l2_hot=_hot_ptr(l2_hot, K), order=_order_ptr(order, R0.shape[0]))
     if compose is not None:
         _require(compose, "compose", torch.int32)
         if compose.dim() > 3 or any(x != compose.shape[0] for x in compose.shape):
@@ -508,7 +536,8 @@ def block_normalizers_complex(T0, chunk_tables, chunk_stride: int, chunk_count, 
 
 def iterate_complex(T, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *,
                     chunk_tables=None, chunk_stride: int = 0, chunk_count=None, chunk_ids=None,
-                    R_out=None, R_log=None, compose=None, base_stride: int = 0) -> None:
+                    R_out=None, R_log=None, compose=None, base_stride: int = 0,
+                    order=None) -> None:
     import torch
 
     lib = load()
@@ -526,7 +555,8 @@ def iterate_complex(T, D, R0, K: int, iterations: int, gamma: float, sel, proj, 
         R_log=_ptr(R_log), K=K, B=R0.shape[0], I=iterations, gamma=gamma, sel=_ptr(sel),
         proj=_ptr(proj), coef=_ptr(coef), ldo=_ld(sel), compose=_ptr(compose),
         n_compose=compose.shape[0] if compose is not None else 0,
-        compose_depth=compose.dim() if compose is not None else 0, base_stride=base_stride)
+        compose_depth=compose.dim() if compose is not None else 0, base_stride=base_stride,
+        order=_order_ptr(order, R0.shape[0]))
     if compose is not None:
         _require(compose, "compose", torch.int32)
         if compose.dim() > 3 or any(x != compose.shape[0] for x in compose.shape):

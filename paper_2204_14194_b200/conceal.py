@@ -29,6 +29,7 @@ inside the recursion kernel. Per frame, only kernels run:
 from __future__ import annotations
 
 import math
+import os
 import time
 
 import numpy as np
@@ -83,6 +84,9 @@ def _cuts(n: int, tile: int, support: int, area: int) -> list[int]:
 # device bytes the frame engine may spend on precomposed base tables (at most
 # half the free memory): config 3 takes 78 GB for all cell triples on a B200
 COMPOSE_BUDGET = 96 << 30
+# longest-processing-time-first dispatch of the frame recursion (fase_block_order);
+# FASE_BLOCK_ORDER=0 keeps the row-major tile order (measurement)
+BLOCK_ORDER = os.environ.get("FASE_BLOCK_ORDER", "1") != "0"
 
 
 class FrameEngine:
@@ -225,6 +229,7 @@ class FrameEngine:
                 D=torch.empty((L, self.G0.shape[1]), dtype=torch.float64, device=dev),
                 alive=torch.empty(L, dtype=torch.int32, device=dev),
                 counts=torch.empty(L, dtype=torch.int32, device=dev),
+                order=torch.empty(L, dtype=torch.int32, device=dev),
                 ids=torch.zeros((L, max(len(self.cells), 1)), dtype=torch.int32, device=dev),
                 sel=torch.empty((L, I), dtype=torch.int32, device=dev),
                 proj=torch.empty((L, I), dtype=vdt, device=dev),
@@ -316,10 +321,17 @@ class FrameEngine:
         _native.block_normalizers(self._diag_G0, self._diag_tabs, K, b["counts"], b["ids"], K,
                                   b["D"], b["alive"])
         self._products(b)
+        # costliest blocks first (chunk rows beyond the precomposed base), so the
+        # last wave of CTAs holds the cheap ones; a schedule only, results unchanged
+        order = None
+        if BLOCK_ORDER:
+            depth = self.compose.dim() if self.compose is not None else 0
+            _native.block_order(b["counts"], depth, b["order"])
+            order = b["order"]
         (_native.iterate_complex if self.complex else _native.iterate)(
             self.G0, b["D"], b["R0"], K, cfg.iterations, cfg.gamma, b["sel"], b["proj"], b["coef"],
             chunk_tables=self.tables, chunk_stride=self.stride, chunk_count=b["counts"],
-            chunk_ids=b["ids"], compose=self.compose, base_stride=self.G0.numel())
+            chunk_ids=b["ids"], compose=self.compose, base_stride=self.G0.numel(), order=order)
         if self.complex:
             _native.frame_paste_complex(self.phi, b["sel"], b["coef"], cfg.iterations, grid,
                                         self.tile, self.support, corners, out, b["max_imag"])

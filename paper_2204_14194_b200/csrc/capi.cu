@@ -335,7 +335,8 @@ extern "C" const char* fase_last_error(void) { return g_last_error; }
 
 // 2.0: fase_iterate_args gained l2_hot (round 2) -- callers built against 1.x
 // pass a shorter argument block
-extern "C" int fase_abi_version(void) { return (2 << 16) | 0; }
+// 3.0: fase_iterate_args.order (dispatch order) appended
+extern "C" int fase_abi_version(void) { return (3 << 16) | 0; }
 
 extern "C" int fase_basis_outer(const double* rows, int Lr, int Mr, const double* cols, int Lc,
                                 int Nc, double* phi, int64_t ldphi, int64_t row0, void* stream) {

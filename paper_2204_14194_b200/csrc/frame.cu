@@ -314,6 +314,91 @@ extern "C" int fase_frame_paste_complex(const double* phi2, int64_t ldphi, const
   return check_launch("fase_frame_paste_complex");
 }
 
+namespace fase {
+namespace {
+// Dispatch order of a chunked recursion (longest processing time first): the
+// blocks by descending cost class, stable. One CTA: each thread counts the
+// classes of a contiguous range of blocks, a scan per class (descending) over
+// the threads gives every (class, thread) its first output slot, and each
+// thread writes its range again in index order.
+constexpr int kOrderThreads = 1024, kOrderClasses = 8;
+__global__ void __launch_bounds__(kOrderThreads) block_order_kernel(const int32_t* __restrict__ counts,
+                                                                    int B, int depth,
+                                                                    int32_t* __restrict__ order) {
+  __shared__ int s_hist[kOrderClasses][kOrderThreads];
+  __shared__ int s_tot[kOrderClasses];
+  __shared__ int s_warp[kOrderThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int per = (B + kOrderThreads - 1) / kOrderThreads;
+  const int lo = min(B, t * per), hi = min(B, lo + per);
+  auto cls = [&](int b) {
+    const int r = counts[b] - depth;
+    return r <= 0 ? 0 : (r >= kOrderClasses - 1 ? kOrderClasses - 1 : r);
+  };
+  int h[kOrderClasses];
+#pragma unroll
+  for (int c = 0; c < kOrderClasses; ++c) h[c] = 0;
+  for (int b = lo; b < hi; ++b) {
+    const int c = cls(b);
+#pragma unroll
+    for (int k = 0; k < kOrderClasses; ++k) h[k] += (k == c);
+  }
+  // exclusive scan over threads, one class at a time (descending classes first)
+  int base = 0;
+  for (int c = kOrderClasses - 1; c >= 0; --c) {
+    int v = h[c];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += n;
+    }
+    if (lane == 31) s_warp[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      int w = s_warp[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += n;
+      }
+      s_warp[lane] = w;  // inclusive over warps
+      if (lane == 31) s_tot[c] = w;
+    }
+    __syncthreads();
+    const int before = (warp > 0 ? s_warp[warp - 1] : 0) + v - h[c];
+    s_hist[c][t] = base + before;
+    base += s_tot[c];
+    __syncthreads();
+  }
+  int pos[kOrderClasses];
+#pragma unroll
+  for (int c = 0; c < kOrderClasses; ++c) pos[c] = s_hist[c][t];
+  for (int b = lo; b < hi; ++b) {
+    const int c = cls(b);
+#pragma unroll
+    for (int k = 0; k < kOrderClasses; ++k)
+      if (k == c) order[pos[k]++] = b;
+  }
+}
+}  // namespace
+}  // namespace fase
+
+extern "C" int fase_block_order(const int32_t* counts, int B, int depth, int32_t* order,
+                                void* stream) {
+  if (B < 0 || depth < 0) {
+    set_error("fase_block_order: bad sizes (B=%d, depth=%d)", B, depth);
+    return FASE_ERR_SHAPE;
+  }
+  if (B == 0) return FASE_OK;
+  if (!counts || !order) {
+    set_error("fase_block_order: null pointer");
+    return FASE_ERR_SHAPE;
+  }
+  fase::block_order_kernel<<<1, fase::kOrderThreads, 0, as_stream(stream)>>>(counts, B, depth,
+                                                                             order);
+  return check_launch("fase_block_order");
+}
+
 extern "C" int fase_frame_widen(const uint8_t* frame_u8, int64_t ldu, const uint8_t* lost,
                                 int64_t ldl, int H, int W, double* out, int64_t ldout,
                                 void* stream) {

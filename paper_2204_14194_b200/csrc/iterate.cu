@@ -201,7 +201,9 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   // SPEC: spare row buffers k at s_spare + k * EP * NT
   double2* s_spare = s_dyn + NB * EP * NT + (kDsmem ? EP * NT : 0);
 
-  const int b = static_cast<int>(blockIdx.x) * NB + half;
+  // the block of this CTA slot: slot order, or the caller's dispatch order
+  const int slot = static_cast<int>(blockIdx.x) * NB + half;
+  const int b = (a.order && slot < a.B) ? __ldg(a.order + slot) : slot;
   const int t = static_cast<int>(threadIdx.x) - half * NT;
   const int lane = t & 31;
   const int warp = t >> 5;
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   };
   const int K = a.K;
   const double kDead = __longlong_as_double(static_cast<long long>(0xfff0000000000000ULL));
-  const bool active = NB == 1 || b < a.B;
+  const bool active = NB == 1 || slot < a.B;
   // the per-iteration barrier: the whole CTA, or this block's half
   auto block_sync = [&]() {
     if constexpr (NB == 1)

@@ -91,13 +91,15 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
   double2* s_row = s_dyn + half * EP * NT;  // staged row: element j*NT + t
   double* s_D2 = reinterpret_cast<double*>(s_dyn + NB * EP * NT);  // kDsmem: D^2 per element
 
-  const int b = static_cast<int>(blockIdx.x) * NB + half;
+  // the block of this CTA slot: slot order, or the caller's dispatch order
+  const int slot = static_cast<int>(blockIdx.x) * NB + half;
+  const int b = (a.order && slot < a.B) ? __ldg(a.order + slot) : slot;
   const int t = static_cast<int>(threadIdx.x) - half * NT;
   const int lane = t & 31;
   const int warp = t >> 5;
   const int K = a.K;
   const double kDead = __longlong_as_double(static_cast<long long>(0xfff0000000000000ULL));
-  const bool active = NB == 1 || b < a.B;
+  const bool active = NB == 1 || slot < a.B;
   auto block_sync = [&]() {  // the whole CTA, or this block's half
     if constexpr (NB == 1)
       __syncthreads();

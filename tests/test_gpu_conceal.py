@@ -222,6 +222,58 @@ def test_frame_engine_complex_compose_bit_identical(spec):
     assert float(dc[same].max()) < 1e-12
 
 
+@pytest.mark.parametrize("B", [1, 7, 1000, 25920])
+def test_block_order_stable_by_cost_class(B):
+    """fase_block_order: a permutation of the blocks by descending cost class
+    min(7, max(0, count - depth)), ascending block index within a class."""
+    from paper_2204_14194_b200 import _native
+
+    rng = np.random.default_rng(B)
+    counts = rng.integers(0, 14, B).astype(np.int32)
+    dev = torch.device(DEV)
+    for depth in (0, 3):
+        order = torch.empty(B, dtype=torch.int32, device=dev)
+        _native.block_order(torch.from_numpy(counts).to(dev), depth, order)
+        got = order.cpu().numpy()
+        cls = np.clip(counts - depth, 0, 7)
+        want = np.lexsort((np.arange(B), -cls))  # class descending, then index
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("spec", ["dct", "dft"])
+def test_frame_engine_dispatch_order_is_a_schedule_only(spec, monkeypatch):
+    """Costliest-first dispatch (fase_iterate_args.order) changes which CTA runs
+    which block, never a result: the frame, selections and coefficients are
+    bit-identical to row-major dispatch."""
+    from paper_2204_14194_b200 import conceal
+    from paper_2204_14194_b200.conceal import FrameEngine, lossy_tiles, tile_grid
+
+    rng = np.random.default_rng(9)
+    h, w, mb, sup = 48, 56, 8, 4
+    img = rng.uniform(0, 255, (h, w))
+    lost = np.zeros((h, w), dtype=bool)
+    for ty, tx in [(0, 0), (0, 1), (1, 1), (2, 3), (4, 5), (3, 0), (4, 4), (5, 6), (2, 2), (1, 3)]:
+        lost[ty * mb:(ty + 1) * mb, tx * mb:(tx + 1) * mb] = True
+    img[lost] = 0.0
+    d = parse_dict_spec(spec, mb + 2 * sup, mb + 2 * sup)
+    cfg = ExtrapConfig(20, 0.5, 0.8)
+    dev = torch.device(DEV)
+    grid = torch.from_numpy(tile_grid(lost, mb)).to(dev)
+    corners = torch.from_numpy(lossy_tiles(lost, (mb, mb)).astype(np.int32)).to(dev)
+    outs = []
+    for on in (False, True):
+        monkeypatch.setattr(conceal, "BLOCK_ORDER", on)
+        eng = FrameEngine(d, (h, w), mb, sup, cfg, device=dev, compose="pairs")
+        r = eng.run(torch.from_numpy(img).to(dev), grid, corners)
+        outs.append((r.selected.clone(), r.coefficients.clone(), r.patched.clone()))
+        if on:  # the order really permutes (cells lost around some tiles, not others)
+            order = eng._buffers(int(corners.shape[0]))["order"].cpu().numpy()
+            assert sorted(order.tolist()) == list(range(int(corners.shape[0])))
+            assert not np.array_equal(order, np.arange(len(order)))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
 def test_frame_widen_kernel():
     """fase_frame_widen: uint8 frame -> float64 with lost pixels zeroed, exactly
     (odd widths and unaligned row starts take the scalar tail)."""

@@ -40,7 +40,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_host_queries(lib):
-    assert lib.fase_abi_version() == (2 << 16)  # 2.0: fase_iterate_args.l2_hot
+    assert lib.fase_abi_version() == (3 << 16)  # 3.0: fase_iterate_args.order
     assert lib.fase_max_atoms() >= 8192
     assert lib.fase_gram_workspace(4608, 2304) == 8 * 4608 * 2304
     assert lib.fase_init_products_workspace(35, 3) == 8 * 3 * 36
