@@ -83,9 +83,14 @@ def parse_args():
     ap.add_argument("--dict", default=None,
                     help="override the dictionary spec of a shared-geometry config (0, 1, 4), "
                          "e.g. 'dft' (the reference's default, complex-valued)")
+    ap.add_argument("--blocks", type=int, default=None,
+                    help="override the batch size of a shared-geometry config (the first B "
+                         "blocks), e.g. one rank's shard of a multi-GPU run measured on one GPU")
     args = ap.parse_args()
     if args.dict and not wl.WORKLOADS[args.config].shared_geometry:
         ap.error("--dict applies to the shared-geometry configs 0, 1 and 4")
+    if args.blocks is not None and (args.blocks < 1 or not wl.WORKLOADS[args.config].shared_geometry):
+        ap.error("--blocks takes a positive batch size for the shared-geometry configs 0, 1 and 4")
     return args
 
 
@@ -458,6 +463,9 @@ def parity_vs_reference(cid, sel, coef, lost, n_lost, name=None):
     z_lost = z["lost"] if has_coef else None
     z_lost_n = z["lost_n"] if has_coef else None
     for i, b in enumerate(blocks):
+        if int(b) >= len(sel):  # a smaller batch (--blocks): the fixture blocks it holds
+            out["blocks_checked"] -= 1
+            continue
         g = sel[int(b)].astype(np.int64)
         want = z_sel[i].astype(np.int64)
         diff = np.flatnonzero(g != want)
@@ -506,7 +514,7 @@ def run_gpu(args):
     w = wl.WORKLOADS[args.config]
     d = bench_dictionary(w, args.dict)
     cplx = not d.is_real
-    K, M, I, B_total = len(d), w.area[0] * w.area[1], w.config.iterations, w.n_blocks
+    K, M, I, B_total = len(d), w.area[0] * w.area[1], w.config.iterations, args.blocks or w.n_blocks
     mask = wl.central_loss_mask(*w.area, *w.loss)
     d.device_matrix(dev)
     # every rank builds the shared table itself: recomputing it (c4: 3.9 ms on
@@ -760,7 +768,9 @@ def run_gpu(args):
             "vs_baseline": None,
             "dtype": "c128" if cplx else "f64",
             "data": "synthetic (seeded BASELINE Appendix-A generators; random atoms: none)",
-            "config": workload_config(w, world, args.dict),
+            "config": dict(workload_config(w, world, args.dict),
+                           **({"blocks": B_total, "blocks_note": "--blocks: the first B blocks of "
+                               "the workload's batch"} if args.blocks else {})),
             "e2e": {"value": B_total * args.steps / e2e_total_s, "unit": "blocks/s",
                     "h2d_bytes_per_step": int(host.numel() * 8) * world,
                     "d2h_bytes_per_step": sb.arena.nbytes * world,
