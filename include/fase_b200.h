@@ -56,8 +56,13 @@ FASE_API const char* fase_last_error(void);
 /* ABI version: (major << 16) | minor. */
 FASE_API int fase_abi_version(void);
 
-/* Largest dictionary size K the iteration kernel accepts. */
+/* Largest dictionary size K fase_iterate accepts (real tables). Up to
+ * fase_iterate_register_atoms() the recursion keeps R in registers; beyond it a
+ * streaming recursion (csrc/iterate_generic.cu, bit-identical arithmetic) keeps
+ * R in the caller's R_out, which is then required (it may alias R0; no R_log),
+ * and the scaled / fused-synthesis entry points are not available. */
 FASE_API int fase_max_atoms(void);
+FASE_API int fase_iterate_register_atoms(void);
 
 /* Leading dimension (>= K, even) that table rows handed to fase_iterate must
  * have, zero-padded past K; 0 if K is unsupported. */

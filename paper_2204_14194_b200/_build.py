@@ -18,7 +18,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libfase_b200.so"
-SOURCES = ["capi.cu", "dgemm.cu", "iterate.cu", "iterate_cluster.cu", "iterate_complex.cu", "frame.cu", "separable.cu", "ozaki.cu"]
+SOURCES = ["capi.cu", "dgemm.cu", "iterate.cu", "iterate_cluster.cu", "iterate_complex.cu",
+           "iterate_generic.cu", "frame.cu", "separable.cu", "ozaki.cu"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 

@@ -40,6 +40,7 @@ EXPORTS = (
     "fase_iterate_scaled", "fase_scale_columns", "fase_iterate_scaled_synth_capacity",
     "fase_iterate_complex_scaled", "fase_frame_widen", "fase_frame_paste_complex",
     "fase_iterate_synth", "fase_iterate_synth_capacity", "fase_block_order",
+    "fase_iterate_register_atoms",
 )
 
 ABI_MAJOR = 3  # fase_abi_version() >> 16 of the library this binding matches
@@ -101,6 +102,7 @@ def load():
             f"{path}: ABI {lib.fase_abi_version() >> 16}.{lib.fase_abi_version() & 0xffff}, this "
             f"package needs {ABI_MAJOR}.x: rebuild with `python -m paper_2204_14194_b200._build`")
     lib.fase_max_atoms.restype = _i32
+    lib.fase_iterate_register_atoms.restype = _i32
     lib.fase_table_ld.restype = _i32
     lib.fase_table_ld.argtypes = [_i32]
     lib.fase_gram_workspace.restype = ctypes.c_size_t
@@ -361,6 +363,9 @@ def iterate(G0, D, R0, K: int, iterations: int, gamma: float, sel, proj, coef, *
     _require(sel, "sel", torch.int32, 2)
     _require(proj, "proj", torch.float64, 2)
     _require(coef, "coef", torch.float64, 2)
+    if R_out is None and phi_lost is None and K > register_atoms():
+        # beyond the registers the streaming recursion works in R_out
+        R_out = torch.empty_like(R0)
     args = IterateArgs(
         G0=_ptr(G0), ldg=_ld(G0), chunk_tables=_ptr(chunk_tables), chunk_stride=chunk_stride,
         chunk_count=_ptr(chunk_count), chunk_ids=_ptr(chunk_ids),
@@ -824,6 +829,12 @@ def l2_flush(buf) -> None:
 
 def max_atoms() -> int:
     return int(load().fase_max_atoms())
+
+
+def register_atoms() -> int:
+    """Largest K whose recursion keeps R in registers (the tuned kernels); larger
+    real dictionaries run the streaming recursion (exact only)."""
+    return int(load().fase_iterate_register_atoms())
 
 
 def table_ld(K: int) -> int:

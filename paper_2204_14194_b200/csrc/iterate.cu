@@ -1102,6 +1102,14 @@ const Variant* override_variant(int K, const Variant* dflt) {
 }  // namespace
 
 int sm_count_cluster() { return sm_count(); }
+int iterate_register_atoms() {
+  const Variant& last = kVariants[sizeof(kVariants) / sizeof(kVariants[0]) - 1];
+  return last.nt * last.ept;
+}
+// csrc/iterate_generic.cu: R streamed through global memory (K beyond the registers)
+int launch_iterate_generic(const fase_iterate_args& a, cudaStream_t stream);
+// the streaming recursion's atom limit (tables of K x K doubles beyond it)
+constexpr int kGenericMaxAtoms = 1 << 20;
 // csrc/iterate_cluster.cu: one block over a CTA cluster (latency-bound batches)
 int launch_iterate_cluster(const fase_iterate_args& a, const fase_synth_fused* syn, bool scaled,
                            cudaStream_t stream);
@@ -1110,15 +1118,14 @@ int cluster_synth_capacity(int K, int64_t ldg, int B);
 
 using namespace fase;
 
-extern "C" int fase_max_atoms(void) {
-  const Variant& last = kVariants[sizeof(kVariants) / sizeof(kVariants[0]) - 1];
-  return last.nt * last.ept;
-}
+extern "C" int fase_max_atoms(void) { return kGenericMaxAtoms; }
+
+extern "C" int fase_iterate_register_atoms(void) { return iterate_register_atoms(); }
 
 extern "C" int fase_table_ld(int K) {
-  if (K < 1) return 0;
+  if (K < 1 || K > kGenericMaxAtoms) return 0;
   const Variant* v = pick_variant(K);
-  return v ? v->nt * v->ept : 0;
+  return v ? v->nt * v->ept : K + (K & 1);  // beyond the registers: even, unpadded
 }
 
 namespace {
@@ -1167,6 +1174,13 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
     return FASE_ERR_UNSUPPORTED;
   }
   const Variant* dflt = pick_variant(a.K);
+  if (!dflt && a.K <= kGenericMaxAtoms) {  // beyond the registers: the streaming recursion
+    if (a.ldg < a.K || (a.chunk_count && a.chunk_stride < a.ldg * a.K)) {
+      set_error("fase_iterate: table rows shorter than K (ldg=%lld)", static_cast<long long>(a.ldg));
+      return FASE_ERR_SHAPE;
+    }
+    return launch_iterate_generic(a, as_stream(stream));
+  }
   const Variant* v = override_variant(a.K, dflt);
   const bool small = a.B <= sm_count();  // at most one block per SM
   if (small && !getenv("FASE_ITERATE_VARIANT")) {  // a block over a CTA cluster

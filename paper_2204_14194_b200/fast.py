@@ -258,6 +258,15 @@ def _check_recursion(recursion: str, cplx: bool, shared: bool = True, record: bo
             "the scaled recursion runs shared-geometry batches without product logs")
 
 
+def _check_large_k(recursion: str, K: int, cplx: bool):
+    """Real dictionaries beyond the register kernels run the streaming exact
+    recursion (csrc/iterate_generic.cu); the scaled one needs R in registers."""
+    if recursion == "scaled" and not cplx and K > _native.register_atoms():
+        raise UnsupportedDictionaryError(
+            f"the scaled recursion holds at most {_native.register_atoms()} atoms (K={K}); "
+            "use recursion='exact'")
+
+
 def _device_vector(x: np.ndarray, length: int, device):
     torch = _torch()
     out = torch.zeros(length, dtype=torch.float64, device=device)
@@ -636,6 +645,7 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
     kmax = _native.max_atoms_complex() if cplx else _native.max_atoms()
     if K > kmax:
         raise UnsupportedDictionaryError(f"K={K} exceeds the iteration kernel's {kmax}")
+    _check_large_k(recursion, K, cplx)
     mask, shared = _validate_masks(masks, dictionary, B)
     _check_recursion(recursion, cplx, shared, record_products)
     I = config.iterations
@@ -795,6 +805,7 @@ class ExtrapolationPlan:
         kmax = _native.max_atoms_complex() if cplx else _native.max_atoms()
         if K > kmax:
             raise UnsupportedDictionaryError(f"K={K} exceeds the iteration kernel's {kmax}")
+        _check_large_k(recursion, K, cplx)
         self.G, self.D = tables.device_tables(dev, complex_rows=cplx)
         # the scaled recursion reads the column-scaled table instead of G
         self.Gs = tables.scaled_table(dev, complex_rows=cplx)[0] if recursion == "scaled" else None

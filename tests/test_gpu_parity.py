@@ -845,32 +845,84 @@ def test_synth_paste_throughput_shape_bit_exact(nb, n_lost, I, stop):
 
 
 def test_maximum_atom_count():
-    """K at the largest recursion variant (fase_max_atoms, 512 x 24 = 12,288):
-    the exact recursion stays bit-exact against the oracle's loop on the same
-    (device-built) table / normalizers / initial products; K + 1 atoms raise
+    """K at the largest register-resident variant (512 x 24 = 12,288) and one
+    atom beyond it (odd K: the streaming recursion, csrc/iterate_generic.cu):
+    both stay bit-exact against the oracle's loop on the same (device-built)
+    table / normalizers / initial products. The scaled recursion refuses K
+    beyond the registers; K beyond fase_max_atoms raises
     UnsupportedDictionaryError, the reference-facing error class."""
-    kmax = _native.max_atoms()
+    kreg = _native.register_atoms()
+    assert kreg == 12288 and _native.max_atoms() > kreg
     rng = np.random.default_rng(12)
     m = n = 16
     mask = wl.central_loss_mask(m, n, 6, 6)
-    vals = rng.standard_normal((kmax, m, n))
-    d = Dictionary(vals)
     cfg = ExtrapConfig(20, 0.5, 0.8)
     sig = rng.uniform(0, 255, (3, m, n))
     w = build_weight_field(mask, cfg.rho_hat)
-    t = build_gram_tables(d, w, device=DEV)
-    r0 = np.stack([initial_scalar_products(sig[b], w, d, device=DEV).real for b in range(3)])
-    res = fase_extrapolate_batch(sig, mask, d, t, cfg, device=DEV, patch=False, products=r0)
-    G, D = t.device_tables(torch.device(DEV))
-    g = G[:, :kmax].cpu().numpy()
-    dd = D.cpu().numpy()
-    for b in range(3):
-        sel, _, coef, _ = orc.fase_run(r0[b], g, dd, cfg.gamma, cfg.iterations)
-        assert np.array_equal(res.selected[b].cpu().numpy(), sel)
-        assert np.array_equal(res.coefficients[b].cpu().numpy(), coef.real)
+    for K in (kreg, kreg + 1):
+        d = Dictionary(rng.standard_normal((K, m, n)))
+        t = build_gram_tables(d, w, device=DEV)
+        r0 = np.stack([initial_scalar_products(sig[b], w, d, device=DEV).real for b in range(3)])
+        res = fase_extrapolate_batch(sig, mask, d, t, cfg, device=DEV, patch=False, products=r0)
+        G, D = t.device_tables(torch.device(DEV))
+        g = G[:, :K].cpu().numpy()
+        dd = D.cpu().numpy()
+        for b in range(3):
+            sel, _, coef, _ = orc.fase_run(r0[b], g, dd, cfg.gamma, cfg.iterations)
+            assert np.array_equal(res.selected[b].cpu().numpy(), sel), K
+            assert np.array_equal(res.coefficients[b].cpu().numpy(), coef.real), K
+        del G, g, t
     with pytest.raises(UnsupportedDictionaryError):
-        fase_extrapolate_batch(sig, mask, Dictionary(rng.standard_normal((kmax + 1, m, n))),
-                               None, cfg, device=DEV)
+        fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion="scaled")
+    with pytest.raises(UnsupportedDictionaryError):
+        _native.table_ld(_native.max_atoms() + 1)
+
+
+def test_streaming_recursion_chunk_lists_and_dead_atoms():
+    """The streaming recursion (K beyond the registers) with per-block chunk
+    lists, per-block normalizers with dead atoms and a dispatch order:
+    bit-exact against the oracle's loop on rows composed in list order."""
+    from paper_2204_14194_b200 import _native
+
+    rng = np.random.default_rng(21)
+    K, B, I, n = _native.register_atoms() + 3, 4, 15, 2
+    ld = _native.table_ld(K)
+    assert ld >= K and ld % 2 == 0
+    G0 = torch.zeros((K, ld), dtype=torch.float64, device=DEV)
+    G0[:, :K] = torch.from_numpy(rng.normal(size=(K, K))).to(DEV)
+    tabs = torch.zeros((n, K, ld), dtype=torch.float64, device=DEV)
+    tabs[:, :, :K] = 0.3 * torch.from_numpy(rng.normal(size=(n, K, K))).to(DEV)
+    counts = torch.tensor([0, 1, 2, 1], dtype=torch.int32, device=DEV)
+    ids = torch.tensor([[0, 0], [1, 0], [0, 1], [0, 0]], dtype=torch.int32, device=DEV)
+    Dh = rng.uniform(0.5, 1.5, (B, ld))
+    Dh[:, [3, 77, K - 1]] = 0.0  # dead atoms: never selected
+    D = torch.from_numpy(Dh).to(DEV)
+    R0 = torch.zeros((B, ld), dtype=torch.float64, device=DEV)
+    R0[:, :K] = torch.from_numpy(rng.normal(size=(B, K))).to(DEV)
+    sel = torch.empty((B, I), dtype=torch.int32, device=DEV)
+    proj = torch.empty((B, I), dtype=torch.float64, device=DEV)
+    coef = torch.empty((B, I), dtype=torch.float64, device=DEV)
+    order = torch.tensor([2, 0, 3, 1], dtype=torch.int32, device=DEV)
+    _native.iterate(G0, D, R0, K, I, 0.5, sel, proj, coef, chunk_tables=tabs,
+                    chunk_stride=tabs[0].numel(), chunk_count=counts, chunk_ids=ids, order=order)
+    torch.cuda.synchronize()
+
+    class Rows:  # row u of block b's table: G0[u] - C_j1[u] - ... in list order
+        def __init__(self, b):
+            self.lst = ids[b, : int(counts[b])].tolist()
+
+        def __getitem__(self, u):
+            r = G0[u, :K].clone()
+            for j in self.lst:
+                r = r - tabs[j, u, :K]
+            return r.cpu().numpy()
+
+    for b in range(B):
+        s_ref, p_ref, c_ref, _ = orc.fase_run(R0[b, :K].cpu().numpy(), Rows(b), Dh[b, :K], 0.5, I)
+        assert np.array_equal(sel[b].cpu().numpy(), s_ref), b
+        assert np.array_equal(proj[b].cpu().numpy(), p_ref.real), b
+        assert np.array_equal(coef[b].cpu().numpy(), c_ref.real), b
+        assert not np.isin(s_ref, [3, 77, K - 1]).any()
 
 
 @pytest.mark.parametrize("spec", ["dft", "dct", "union:dct+dft"])
