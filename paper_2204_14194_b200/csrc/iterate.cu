@@ -1193,7 +1193,7 @@ extern "C" int fase_iterate(const fase_iterate_args* args, void* stream) {
   }
   if (!v) {
     set_error("fase_iterate: K=%d exceeds the largest kernel variant (%d atoms)", a.K,
-              fase_max_atoms());
+              iterate_register_atoms());
     return FASE_ERR_UNSUPPORTED;
   }
   if (a.ldg < v->nt * v->ept || (a.chunk_count && a.chunk_stride < a.ldg * a.K)) {
@@ -1382,7 +1382,7 @@ extern "C" int fase_iterate_scaled(const fase_iterate_args* args, const fase_syn
   const Variant* v = pick_scaled(a.K, a.B);
   if (!v) {
     set_error("fase_iterate_scaled: K=%d exceeds the largest kernel variant (%d atoms)", a.K,
-              fase_max_atoms());
+              iterate_register_atoms());
     return FASE_ERR_UNSUPPORTED;
   }
   if (syn && syn->n_lost > v->syn * v->nt) {
