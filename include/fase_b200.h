@@ -385,6 +385,10 @@ FASE_API int fase_gram_complex(const double* phi2, int64_t ldphi, const double* 
 /* Largest K / table leading dimension (complex elements) of fase_iterate_complex. */
 FASE_API int fase_max_atoms_complex(void);
 FASE_API int fase_table_ld_complex(int K);
+/* Largest complex K whose recursion keeps R in registers; beyond it (up to
+ * fase_max_atoms_complex()) fase_iterate_complex runs the streaming recursion
+ * (csrc/iterate_generic.cu, same arithmetic), which needs R_out (may alias R0). */
+FASE_API int fase_iterate_complex_register_atoms(void);
 
 /*
  * The recursion in complex128 (fast.py:224-255): metric |R_k| * D_k with numpy's

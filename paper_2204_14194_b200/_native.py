@@ -40,7 +40,7 @@ EXPORTS = (
     "fase_iterate_scaled", "fase_scale_columns", "fase_iterate_scaled_synth_capacity",
     "fase_iterate_complex_scaled", "fase_frame_widen", "fase_frame_paste_complex",
     "fase_iterate_synth", "fase_iterate_synth_capacity", "fase_block_order",
-    "fase_iterate_register_atoms",
+    "fase_iterate_register_atoms", "fase_iterate_complex_register_atoms",
 )
 
 ABI_MAJOR = 3  # fase_abi_version() >> 16 of the library this binding matches
@@ -103,6 +103,7 @@ def load():
             f"package needs {ABI_MAJOR}.x: rebuild with `python -m paper_2204_14194_b200._build`")
     lib.fase_max_atoms.restype = _i32
     lib.fase_iterate_register_atoms.restype = _i32
+    lib.fase_iterate_complex_register_atoms.restype = _i32
     lib.fase_table_ld.restype = _i32
     lib.fase_table_ld.argtypes = [_i32]
     lib.fase_gram_workspace.restype = ctypes.c_size_t
@@ -552,6 +553,9 @@ def iterate_complex(T, D, R0, K: int, iterations: int, gamma: float, sel, proj, 
     _require(sel, "sel", torch.int32, 2)
     _require_complex(proj, "proj", 2)
     _require_complex(coef, "coef", 2)
+    if R_out is None and K > register_atoms_complex():
+        # beyond the registers the streaming recursion works in R_out
+        R_out = torch.empty_like(R0)
     args = IterateArgs(
         G0=_ptr(T), ldg=_ld(T), chunk_tables=_ptr(chunk_tables), chunk_stride=chunk_stride,
         chunk_count=_ptr(chunk_count), chunk_ids=_ptr(chunk_ids),
@@ -616,6 +620,11 @@ def fft_gram(spec, M: int, N: int, mu, eta, K: int, T) -> None:
 
 def max_atoms_complex() -> int:
     return int(load().fase_max_atoms_complex())
+
+
+def register_atoms_complex() -> int:
+    """Largest complex K whose recursion keeps R in registers."""
+    return int(load().fase_iterate_complex_register_atoms())
 
 
 def table_ld_complex(K: int) -> int:

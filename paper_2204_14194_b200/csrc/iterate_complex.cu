@@ -583,15 +583,26 @@ const Variant* override_variant(int K, const Variant* dflt) {
 
 using namespace fase;
 
-extern "C" int fase_max_atoms_complex(void) {
+namespace fase {
+// csrc/iterate_generic.cu: R streamed through global memory (K beyond the registers)
+int launch_iterate_generic_complex(const fase_iterate_args& a, int reg_atoms, cudaStream_t stream);
+}
+namespace {
+constexpr int kGenericMaxAtomsComplex = 1 << 20;
+int complex_register_atoms() {
   const Variant& last = kVariants[sizeof(kVariants) / sizeof(kVariants[0]) - 1];
   return last.nt * last.ep;
 }
+}  // namespace
+
+extern "C" int fase_max_atoms_complex(void) { return kGenericMaxAtomsComplex; }
+
+extern "C" int fase_iterate_complex_register_atoms(void) { return complex_register_atoms(); }
 
 extern "C" int fase_table_ld_complex(int K) {
-  if (K < 1) return 0;
+  if (K < 1 || K > kGenericMaxAtomsComplex) return 0;
   const Variant* v = pick_variant(K);
-  return v ? v->nt * v->ep : 0;
+  return v ? v->nt * v->ep : K;  // beyond the registers: unpadded (16-byte elements)
 }
 
 extern "C" int fase_iterate_complex(const fase_iterate_args* args, void* stream) {
@@ -629,10 +640,18 @@ extern "C" int fase_iterate_complex(const fase_iterate_args* args, void* stream)
     set_error("fase_iterate_complex: R_log recording is not available with chunked tables");
     return FASE_ERR_UNSUPPORTED;
   }
+  if (!pick_variant(a.K) && a.K <= kGenericMaxAtomsComplex) {  // the streaming recursion
+    if (a.ldg < a.K || (a.chunk_count && a.chunk_stride < a.ldg * a.K)) {
+      set_error("fase_iterate_complex: table rows shorter than K (ldg=%lld)",
+                static_cast<long long>(a.ldg));
+      return FASE_ERR_SHAPE;
+    }
+    return launch_iterate_generic_complex(a, complex_register_atoms(), as_stream(stream));
+  }
   const Variant* v = override_variant(a.K, pick_variant(a.K));
   if (!v) {
     set_error("fase_iterate_complex: K=%d exceeds the largest kernel variant (%d atoms)", a.K,
-              fase_max_atoms_complex());
+              complex_register_atoms());
     return FASE_ERR_UNSUPPORTED;
   }
   if (a.ldg < v->nt * v->ep || (a.chunk_count && a.chunk_stride < a.ldg * a.K)) {
@@ -711,7 +730,7 @@ extern "C" int fase_iterate_complex_scaled(const fase_iterate_args* args, void* 
   }
   if (!dflt || !v) {
     set_error("fase_iterate_complex_scaled: K=%d exceeds the largest kernel variant (%d atoms)",
-              a.K, fase_max_atoms_complex());
+              a.K, complex_register_atoms());
     return FASE_ERR_UNSUPPORTED;
   }
   if (a.ldg < v->nt * v->ep) {

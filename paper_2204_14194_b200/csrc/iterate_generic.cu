@@ -170,10 +170,159 @@ __global__ void __launch_bounds__(kGenThreads, 1) fase_iterate_generic_kernel(co
   }
 }
 
+// Complex tables (rows of conj(C), csrc/iterate_complex.cu's arithmetic: numpy's
+// complex product and hypot, one rounding at a time): the same streaming loop
+// with R complex (interleaved) in R_out and the exact metric |R| * D per element.
+__global__ void __launch_bounds__(kGenThreads, 1) fase_iterate_generic_complex_kernel(const fase_iterate_args a) {
+  __shared__ long long s_key[kGenWarps];
+  __shared__ unsigned s_arg[kGenWarps];
+  __shared__ unsigned s_u[kGenWarps];
+  const int slot = static_cast<int>(blockIdx.x);
+  const int b = a.order ? __ldg(a.order + slot) : slot;
+  const int t = static_cast<int>(threadIdx.x), lane = t & 31, warp = t >> 5;
+  const int K = a.K;
+  const double kDead = __longlong_as_double(static_cast<long long>(0xfff0000000000000ULL));
+  const double* D = a.D + (a.ldd ? static_cast<int64_t>(b) * a.ldd : 0);
+  const double2* R0 = reinterpret_cast<const double2*>(a.R0) + static_cast<int64_t>(b) * a.ldr;
+  double2* R = reinterpret_cast<double2*>(a.R_out) + static_cast<int64_t>(b) * a.ldr;
+  int32_t* sel = a.sel + static_cast<int64_t>(b) * a.ldo;
+  double* proj = a.proj + 2 * static_cast<int64_t>(b) * a.ldo;
+  double* coef = a.coef + 2 * static_cast<int64_t>(b) * a.ldo;
+  const int64_t ldg = a.ldg;  // complex elements
+  const double2* C = reinterpret_cast<const double2*>(a.chunk_tables);
+
+  const int32_t* cids = nullptr;
+  int nch = 0;
+  const double2* G0b = reinterpret_cast<const double2*>(a.G0);
+  if (a.chunk_count) {
+    nch = a.chunk_count[b];
+    cids = a.chunk_ids + static_cast<int64_t>(b) * a.chunk_list_ld;
+    if (a.compose && nch > 0) {
+      for (int k = min(nch, a.compose_depth); k >= 1; --k) {
+        int64_t idx = 0;
+        for (int d = 0; d < a.compose_depth; ++d) {
+          FASE_ASSERT(cids[min(d, k - 1)] >= 0 && cids[min(d, k - 1)] < a.n_compose);
+          idx = idx * a.n_compose + cids[min(d, k - 1)];
+        }
+        const int p = a.compose[idx];
+        if (p > 0) {
+          G0b += static_cast<int64_t>(p) * a.base_stride;
+          cids += k;
+          nch -= k;
+          break;
+        }
+      }
+    }
+  }
+  auto metric = [&](double2 r, int k) {
+    const double d = __ldg(D + k);
+    return mul_rn(np_cabs_fast(r.x, r.y), d != 0.0 ? d : kDead);
+  };
+  auto block_max = [&](double best, unsigned barg, long long& top_key) {
+    const long long key = __double_as_longlong(best);
+    const int kh = static_cast<int>(key >> 32);
+    const unsigned kl = static_cast<unsigned>(key);
+    const int wh = __reduce_max_sync(0xffffffffu, kh);
+    const unsigned wl = __reduce_max_sync(0xffffffffu, kh == wh ? kl : 0u);
+    if (lane == 0) s_key[warp] = (static_cast<long long>(wh) << 32) | wl;
+    __syncthreads();
+    const long long sk = s_key[lane];
+    const int h = static_cast<int>(sk >> 32);
+    const unsigned l = static_cast<unsigned>(sk);
+    const int bh = __reduce_max_sync(0xffffffffu, h);
+    const unsigned bl = __reduce_max_sync(0xffffffffu, h == bh ? l : 0u);
+    top_key = (static_cast<long long>(bh) << 32) | bl;
+  };
+
+  double best = kDead;
+  unsigned barg = kGenNone;
+  for (int k = t; k < K; k += kGenThreads) {
+    const double2 r = R0[k];
+    R[k] = r;
+    const double m = metric(r, k);
+    if (m > best) {
+      best = m;
+      barg = static_cast<unsigned>(k);
+    }
+  }
+  double q = 0.0;
+  for (int it = 0; it < a.I; ++it) {
+    long long top_key;
+    block_max(best, barg, top_key);
+    if (top_key < 0) {  // every atom degenerate: mark and stop
+      for (int k = it + t; k < a.I; k += kGenThreads) {
+        sel[k] = -1;
+        proj[2 * k] = proj[2 * k + 1] = 0.0;
+        coef[2 * k] = coef[2 * k + 1] = 0.0;
+      }
+      return;
+    }
+    const double top = __longlong_as_double(top_key);
+    if (top_key > 0 && top_key < 0x7ff0000000000000LL) q = fmax(q, mul_rn(1e-13, top));
+    const double thr = q > 0.0 ? sub_rn(top, q) : top;
+    unsigned cand = kGenNone;
+    if (best >= thr) {
+      for (int k = t; k < K && cand == kGenNone; k += kGenThreads)
+        if (metric(R[k], k) >= thr) cand = static_cast<unsigned>(k);
+    }
+    const unsigned wmin = __reduce_min_sync(0xffffffffu, cand);
+    if (lane == 0) s_u[warp] = wmin;
+    __syncthreads();
+    const unsigned u = __reduce_min_sync(0xffffffffu, s_u[lane]);
+    FASE_ASSERT(u < static_cast<unsigned>(K));
+    const double2 ru = R[u];
+    const double du = __ldg(D + u);
+    const double d2u = mul_rn(du, du);
+    const double pr = mul_rn(ru.x, d2u), pi = mul_rn(ru.y, d2u);
+    const double cr = mul_rn(a.gamma, pr), ci = mul_rn(a.gamma, pi);
+    if (t == 0) {
+      sel[it] = static_cast<int32_t>(u);
+      proj[2 * it] = pr;
+      proj[2 * it + 1] = pi;
+      coef[2 * it] = cr;
+      coef[2 * it + 1] = ci;
+    }
+    __syncthreads();
+    const double2* grow = G0b + static_cast<int64_t>(u) * ldg;
+    best = kDead;
+    barg = kGenNone;
+    for (int k = t; k < K; k += kGenThreads) {
+      double2 g = grow[k];
+      for (int ch = 0; ch < nch; ++ch) {
+        const double2 v = C[static_cast<int64_t>(cids[ch]) * a.chunk_stride +
+                            static_cast<int64_t>(u) * ldg + k];
+        g.x = sub_rn(g.x, v.x);
+        g.y = sub_rn(g.y, v.y);
+      }
+      const double2 x = np_cmul(cr, ci, g.x, g.y);
+      double2 r = R[k];
+      r.x = sub_rn(r.x, x.x);
+      r.y = sub_rn(r.y, x.y);
+      R[k] = r;
+      const double m = metric(r, k);
+      if (m > best) {
+        best = m;
+        barg = static_cast<unsigned>(k);
+      }
+    }
+  }
+}
+
 }  // namespace
 
 // the register-resident kernels' capacity (csrc/iterate.cu)
 int iterate_register_atoms();
+
+int launch_iterate_generic_complex(const fase_iterate_args& a, int reg_atoms, cudaStream_t stream) {
+  if (!a.R_out || a.R_log) {
+    set_error("fase_iterate_complex: K=%d exceeds the register kernels' %d atoms: the streaming "
+              "recursion needs R_out (B x ldr, may alias R0) as its working vector and takes "
+              "no R_log", a.K, reg_atoms);
+    return a.R_log ? FASE_ERR_UNSUPPORTED : FASE_ERR_SHAPE;
+  }
+  fase_iterate_generic_complex_kernel<<<a.B, kGenThreads, 0, stream>>>(a);
+  return check_launch("fase_iterate_complex (streaming, large K)");
+}
 
 int launch_iterate_generic(const fase_iterate_args& a, cudaStream_t stream) {
   if (!a.R_out || a.R_log) {

@@ -261,10 +261,10 @@ def _check_recursion(recursion: str, cplx: bool, shared: bool = True, record: bo
 def _check_large_k(recursion: str, K: int, cplx: bool):
     """Real dictionaries beyond the register kernels run the streaming exact
     recursion (csrc/iterate_generic.cu); the scaled one needs R in registers."""
-    if recursion == "scaled" and not cplx and K > _native.register_atoms():
+    reg = _native.register_atoms_complex() if cplx else _native.register_atoms()
+    if recursion == "scaled" and K > reg:
         raise UnsupportedDictionaryError(
-            f"the scaled recursion holds at most {_native.register_atoms()} atoms (K={K}); "
-            "use recursion='exact'")
+            f"the scaled recursion holds at most {reg} atoms (K={K}); use recursion='exact'")
 
 
 def _device_vector(x: np.ndarray, length: int, device):

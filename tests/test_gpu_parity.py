@@ -925,6 +925,62 @@ def test_streaming_recursion_chunk_lists_and_dead_atoms():
         assert not np.isin(s_ref, [3, 77, K - 1]).any()
 
 
+def test_streaming_recursion_complex():
+    """The complex streaming recursion (K beyond the complex register kernels):
+    rows of conj(C) composed in list order, per-block normalizers with dead
+    atoms; bit-exact against the oracle's complex loop (numpy's product and
+    abs); the complex scaled recursion refuses such K."""
+    from paper_2204_14194_b200 import _native
+
+    rng = np.random.default_rng(22)
+    K, B, I, n = _native.register_atoms_complex() + 1, 3, 12, 2
+    ld = _native.table_ld_complex(K)
+
+    def crnd(*shape):
+        return torch.complex(torch.from_numpy(rng.normal(size=shape)),
+                             torch.from_numpy(rng.normal(size=shape))).to(DEV)
+
+    T0 = torch.zeros((K, ld), dtype=torch.complex128, device=DEV)
+    T0[:, :K] = crnd(K, K)
+    tabs = torch.zeros((n, K, ld), dtype=torch.complex128, device=DEV)
+    tabs[:, :, :K] = 0.3 * crnd(n, K, K)
+    counts = torch.tensor([0, 2, 1], dtype=torch.int32, device=DEV)
+    ids = torch.tensor([[0, 0], [0, 1], [1, 0]], dtype=torch.int32, device=DEV)
+    Dh = rng.uniform(0.5, 1.5, (B, ld))
+    Dh[:, [5, K - 2]] = 0.0
+    D = torch.from_numpy(Dh).to(DEV)
+    R0 = torch.zeros((B, ld), dtype=torch.complex128, device=DEV)
+    R0[:, :K] = crnd(B, K)
+    sel = torch.empty((B, I), dtype=torch.int32, device=DEV)
+    proj = torch.empty((B, I), dtype=torch.complex128, device=DEV)
+    coef = torch.empty((B, I), dtype=torch.complex128, device=DEV)
+    _native.iterate_complex(T0, D, R0, K, I, 0.5, sel, proj, coef, chunk_tables=tabs,
+                            chunk_stride=tabs[0].numel(), chunk_count=counts, chunk_ids=ids)
+    torch.cuda.synchronize()
+
+    class ConjRows:  # the oracle conjugates row u: hand it conj(composed row of conj(C))
+        def __init__(self, b):
+            self.lst = ids[b, : int(counts[b])].tolist()
+
+        def __getitem__(self, u):
+            r = T0[u, :K].clone()
+            for j in self.lst:
+                r = r - tabs[j, u, :K]
+            return np.conj(r.cpu().numpy())
+
+    for b in range(B):
+        s_ref, p_ref, c_ref, _ = orc.fase_run(R0[b, :K].cpu().numpy(), ConjRows(b), Dh[b, :K], 0.5, I)
+        assert np.array_equal(sel[b].cpu().numpy(), s_ref), b
+        assert np.array_equal(proj[b].cpu().numpy(), p_ref), b
+        assert np.array_equal(coef[b].cpu().numpy(), c_ref), b
+        assert not np.isin(s_ref, [5, K - 2]).any()
+    d = parse_dict_spec("dft", 79, 79)  # 6,241 complex atoms
+    assert len(d) > _native.register_atoms_complex()
+    with pytest.raises(UnsupportedDictionaryError):
+        fase_extrapolate_batch(np.zeros((1, 79, 79)), wl.central_loss_mask(79, 79, 9, 9), d, None,
+                               ExtrapConfig(3), device=DEV, recursion="scaled")
+
+
 @pytest.mark.parametrize("spec", ["dft", "dct", "union:dct+dft"])
 def test_complex_signals(spec):
     """Complex signals (the reference's as_field coercion; its own
