@@ -602,9 +602,20 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     // second barrier (the guess is in range here: a degenerate top returned)
     const double dguess = kLeanD ? __ldg(D + guess) : 0.0;
     const double top = __longlong_as_double(top_key);
-    // tie_quantum: only a finite, strictly positive top moves the ratchet
-    if (top_key > 0 && top_key < 0x7ff0000000000000LL) q = fmax(q, mul_rn(1e-13, top));
-    const double thr = q > 0.0 ? sub_rn(top, q) : top;
+    // tie_quantum (reference.py:55-85): only a finite, strictly positive top moves the ratchet
+    double thr;
+    if constexpr (kChunked) {
+      // (the branch-free form below perturbs the chunked shapes' register
+      // allocation into spills: config 3 12.6 -> 13.7 ms)
+      if (top_key > 0 && top_key < 0x7ff0000000000000LL) q = fmax(q, mul_rn(1e-13, top));
+      thr = q > 0.0 ? sub_rn(top, q) : top;
+    } else {
+      // a +0 top leaves the ratchet (1e-13 * 0), a +inf one must not move it;
+      // q == 0 gives exactly top (c1 0.780 -> 0.772 ms)
+      const double qn = mul_rn(1e-13, top);
+      q = qn < __longlong_as_double(0x7ff0000000000000LL) ? fmax(q, qn) : q;
+      thr = sub_rn(top, q);
+    }
 
     // ---- lowest index reaching the threshold (only warps whose max reaches it)
     unsigned cand = kNone;

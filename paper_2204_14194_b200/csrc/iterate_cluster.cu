@@ -255,8 +255,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(NT, 1)
       }
     }
     const double top = __longlong_as_double(top_key);
-    if (top_key > 0 && top_key < 0x7ff0000000000000LL) q = fmax(q, mul_rn(1e-13, top));
-    const double thr = q > 0.0 ? sub_rn(top, q) : top;
+    {  // the ratchet; a +0 top leaves it (1e-13 * 0), a +inf one must not move it
+      const double qn = mul_rn(1e-13, top);
+      q = qn < __longlong_as_double(0x7ff0000000000000LL) ? fmax(q, qn) : q;
+    }
+    const double thr = sub_rn(top, q);  // (q == 0: exactly top)
 
     // ---- B: this CTA's lowest index reaching the threshold, with R (and D)
     unsigned cand = kNoneC;

@@ -127,8 +127,11 @@ __global__ void __launch_bounds__(kGenThreads, 1) fase_iterate_generic_kernel(co
       return;
     }
     const double top = __longlong_as_double(top_key);
-    if (top_key > 0 && top_key < 0x7ff0000000000000LL) q = fmax(q, mul_rn(1e-13, top));
-    const double thr = q > 0.0 ? sub_rn(top, q) : top;
+    {  // the ratchet; a +0 top leaves it (1e-13 * 0), a +inf one must not move it
+      const double qn = mul_rn(1e-13, top);
+      q = qn < __longlong_as_double(0x7ff0000000000000LL) ? fmax(q, qn) : q;
+    }
+    const double thr = sub_rn(top, q);  // (q == 0: exactly top)
     // lowest index reaching the threshold: only threads whose max reaches it
     unsigned cand = kGenNone;
     if (best >= thr) {
@@ -258,8 +261,11 @@ __global__ void __launch_bounds__(kGenThreads, 1) fase_iterate_generic_complex_k
       return;
     }
     const double top = __longlong_as_double(top_key);
-    if (top_key > 0 && top_key < 0x7ff0000000000000LL) q = fmax(q, mul_rn(1e-13, top));
-    const double thr = q > 0.0 ? sub_rn(top, q) : top;
+    {  // the ratchet; a +0 top leaves it (1e-13 * 0), a +inf one must not move it
+      const double qn = mul_rn(1e-13, top);
+      q = qn < __longlong_as_double(0x7ff0000000000000LL) ? fmax(q, qn) : q;
+    }
+    const double thr = sub_rn(top, q);  // (q == 0: exactly top)
     unsigned cand = kGenNone;
     if (best >= thr) {
       for (int k = t; k < K && cand == kGenNone; k += kGenThreads)

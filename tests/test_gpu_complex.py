@@ -362,15 +362,16 @@ def test_complex_scaled_matches_exact_and_dead_atoms():
 
 
 def test_maximum_atom_count_complex():
-    """K at the largest complex recursion variant: the exact complex recursion
-    is bit-exact against the oracle's loop on the same device-built table,
-    normalizers and initial products; one atom more raises
-    UnsupportedDictionaryError."""
+    """K at the largest register-resident complex variant: the exact complex
+    recursion is bit-exact against the oracle's loop on the same device-built
+    table, normalizers and initial products (one atom more runs the streaming
+    recursion: test_gpu_parity.py::test_streaming_recursion_complex); K beyond
+    fase_max_atoms_complex raises UnsupportedDictionaryError."""
     from paper_2204_14194_b200 import (ExtrapConfig, UnsupportedDictionaryError, _native,
                                        build_gram_tables, build_weight_field,
                                        fase_extrapolate_batch, initial_scalar_products)
 
-    kmax = _native.max_atoms_complex()
+    kmax = _native.register_atoms_complex()
     rng = np.random.default_rng(21)
     m = n = 16
     mask = wl.central_loss_mask(m, n, 6, 6)
@@ -390,5 +391,4 @@ def test_maximum_atom_count_complex():
         assert np.array_equal(res.selected[b].cpu().numpy(), sel)
         assert np.array_equal(res.coefficients[b].cpu().numpy(), coef)
     with pytest.raises(UnsupportedDictionaryError):
-        fase_extrapolate_batch(sig, mask, Dictionary(vals[:1].repeat(kmax + 1, axis=0)), None,
-                               cfg, device=DEV)
+        _native.table_ld_complex(_native.max_atoms_complex() + 1)
