@@ -1045,10 +1045,11 @@ const Variant kLatencyVariants[] = {
 // the staged row occupies shared memory and four 256-thread CTAs fit per SM
 // (64 registers; config 1: 0.916 ms exact at three CTAs, 0.815 ms scaled at
 // three, 0.721 ms scaled at four). Ordered by capacity like kVariants.
-// Capacity 8192 runs 128 x 64 (4 warps, 255 registers, two CTAs per SM): half
-// the per-warp iteration overhead of 256 x 32 at the same residency, so the
-// power-capped config 4 holds a higher clock (1837 vs 1747 MHz; 251.0K ->
-// 254.0K blocks/s on one box, tools/ab_variant128.sh).
+// (Capacity 8192 as 128 x 64 -- 4 warps, 255 registers, two CTAs per SM --
+// halves the per-warp iteration overhead: on a power-capped box config 4 holds
+// 1837 instead of 1747 MHz and gains 1.3%, but without the cap it is 8% slower
+// (11.89 vs 11.0 ms under ncu, fewer warps to hide the row latency); the
+// default stays 256 x 32, tools/ab_variant128*.sh, profiles/r02b/ab_variant128.txt)
 // SYN: lost samples per thread of the fused-synthesis kernel (registers allow
 // only one at the 64-register four-CTA shapes).
 #define FASE_VS(NT, EPT, MINB, SYN)                                                          \
@@ -1058,13 +1059,13 @@ const Variant kScaledVariants[] = {
     FASE_VS(128, 2, 8, 4),   FASE_VS(128, 4, 8, 4),   FASE_VS(128, 8, 8, 4),
     FASE_VS(128, 16, 6, 4),  FASE_VS(256, 10, 4, 1),  FASE_VS(256, 12, 4, 1),
     FASE_VS(256, 14, 4, 1),  FASE_VS(256, 16, 4, 1),  FASE_VS(256, 18, 4, 1),
-    FASE_VS(256, 20, 3, 3),  FASE_VS(256, 24, 2, 3),  FASE_VS(128, 64, 2, 4),
+    FASE_VS(256, 20, 3, 3),  FASE_VS(256, 24, 2, 3),  FASE_VS(256, 32, 2, 3),
     FASE_VS(512, 20, 1, 2),  FASE_VS(512, 24, 1, 2),
 };
 // alternatives for measurement (FASE_SCALED_VARIANT=NTxEPTxMINB) and the
 // latency shapes for batches of at most one block per SM
 const Variant kScaledExtra[] = {
-    FASE_VS(128, 36, 4, 2), FASE_VS(256, 18, 3, 2), FASE_VS(256, 32, 2, 3),
+    FASE_VS(128, 36, 4, 2), FASE_VS(256, 18, 3, 2), FASE_VS(128, 64, 2, 4),
     FASE_VS(128, 64, 3, 4), FASE_VS(256, 20, 4, 1),
 };
 const int kScaledExtraMinb[] = {4, 3, 2, 3, 4};
