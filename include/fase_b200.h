@@ -239,8 +239,9 @@ typedef struct {
   /* optional dispatch order (ABI 3.0): NULL, or a permutation of 0..B-1, and
    * the i-th CTA (slot) runs block order[i]. Blocks are independent, so only the
    * schedule changes, never a result: per-block geometries put their costliest
-   * blocks first (fase_block_order) so the last wave holds the cheap ones. The
-   * one-block-over-a-cluster path ignores it. */
+   * blocks first (fase_block_order) so the last wave holds the cheap ones. Only
+   * the chunk-list recursions (and the streaming one) honour it: shared
+   * geometries, whose blocks cost the same, run slot order. */
   const int32_t* order;
 } fase_iterate_args;
 

@@ -201,10 +201,18 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   // SPEC: spare row buffers k at s_spare + k * EP * NT
   double2* s_spare = s_dyn + NB * EP * NT + (kDsmem ? EP * NT : 0);
 
-  // the block of this CTA slot: slot order, or the caller's dispatch order
+  // the block of this CTA slot: slot order, or (per-block geometries) the
+  // caller's dispatch order. Shared geometries ignore the order: their blocks
+  // cost the same, and a block index that is a load instead of a function of
+  // blockIdx.x is one more live register -- at 64 / 128 registers the config-1
+  // / config-4 shapes spilled (16 -> 120 bytes, 0 -> 28)
   const int slot = static_cast<int>(blockIdx.x) * NB + half;
-  const int b = (a.order && slot < a.B) ? __ldg(a.order + slot) : slot;
+  const int b = (kChunked && a.order && slot < a.B) ? __ldg(a.order + slot) : slot;
+  // kChunked: the block index parked in shared memory for the loop's (thread-0)
+  // output rows instead of held in a register across it
+  __shared__ int s_blk[NB];
   const int t = static_cast<int>(threadIdx.x) - half * NT;
+  if (kChunked && t == 0) s_blk[half] = b;  // (read after the loop's first barrier)
   const int lane = t & 31;
   const int warp = t >> 5;
   double gacc[SYN > 0 ? SYN : 1];
@@ -362,7 +370,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   auto out_row = [&](auto* base, auto* hoisted) {
     if constexpr (kChunked) {
       asm volatile("" : "+l"(base));
-      return base + static_cast<int64_t>(b) * a.ldo;
+      return base + static_cast<int64_t>(s_blk[half]) * a.ldo;
     } else {
       return hoisted;
     }

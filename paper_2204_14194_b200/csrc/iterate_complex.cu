@@ -91,9 +91,11 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_complex_kernel(con
   double2* s_row = s_dyn + half * EP * NT;  // staged row: element j*NT + t
   double* s_D2 = reinterpret_cast<double*>(s_dyn + NB * EP * NT);  // kDsmem: D^2 per element
 
-  // the block of this CTA slot: slot order, or the caller's dispatch order
+  // the block of this CTA slot: slot order, or (per-block geometries) the
+  // caller's dispatch order (shared geometries ignore it: equal-cost blocks, and
+  // a loaded block index costs a register, csrc/iterate.cu)
   const int slot = static_cast<int>(blockIdx.x) * NB + half;
-  const int b = (a.order && slot < a.B) ? __ldg(a.order + slot) : slot;
+  const int b = (kChunked && a.order && slot < a.B) ? __ldg(a.order + slot) : slot;
   const int t = static_cast<int>(threadIdx.x) - half * NT;
   const int lane = t & 31;
   const int warp = t >> 5;
