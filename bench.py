@@ -498,6 +498,7 @@ def run_gpu(args):
     import torch.distributed as dist
 
     from paper_2204_14194_b200 import ShardedBatch, _native, build_gram_tables, build_weight_field
+    from paper_2204_14194_b200.shard import build_gram_tables_sharded
     from paper_2204_14194_b200.fast import gram_into, gram_support
 
     rank, world, local = dist_env()
@@ -517,10 +518,11 @@ def run_gpu(args):
     K, M, I, B_total = len(d), w.area[0] * w.area[1], w.config.iterations, args.blocks or w.n_blocks
     mask = wl.central_loss_mask(*w.area, *w.loss)
     d.device_matrix(dev)
-    # every rank builds the shared table itself: recomputing it (c4: 3.9 ms on
-    # the tensor cores) is cheaper than moving 537 MB, and it is outside the
-    # timed region (reference bench.py:118-119)
-    tables = build_gram_tables(d, build_weight_field(mask, w.config.rho_hat), device=dev)
+    # the shared table, outside the timed region (reference bench.py:118-119):
+    # under torchrun every rank builds 1/N of its rows on the tensor cores and
+    # the row panels are broadcast (bit-identical to one GPU's
+    # table); one GPU builds it whole
+    tables = build_gram_tables_sharded(d, build_weight_field(mask, w.config.rho_hat), device=dev)
     # auto: the scaled recursion (complex: union:dft+bdft 2.31 -> 1.84 ms; dft
     # 48^2 0.994 -> 0.830 ms at four CTAs per SM), except for batches of at most
     # one block per SM, where the bit-exact recursion with the synthesis fused

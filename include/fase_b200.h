@@ -484,6 +484,11 @@ FASE_API int fase_ozaki_gram(const int8_t* a_planes, int a_rows_pad, const int32
                              int64_t kp, int slices, double* G, int64_t ldg, void* stream);
 
 /* Writes `bytes` of zeros-then-ones into `buf` to evict L2 between timed steps. */
+/* G[i*ldg + j] <- G[j*ldg + i] for K > i > j: a table assembled from row
+ * panels (multi-GPU build, each rank's rows of the non-symmetric product)
+ * becomes the exact mirror of its upper triangle, bit-identical to the
+ * single-GPU symmetric build (fase_gram / fase_ozaki_gram write that mirror). */
+FASE_API int fase_mirror_upper(double* G, int64_t ldg, int K, void* stream);
 FASE_API int fase_l2_flush(void* buf, size_t bytes, void* stream);
 
 #ifdef __cplusplus

@@ -40,7 +40,7 @@ EXPORTS = (
     "fase_iterate_scaled", "fase_scale_columns", "fase_iterate_scaled_synth_capacity",
     "fase_iterate_complex_scaled", "fase_frame_widen", "fase_frame_paste_complex",
     "fase_iterate_synth", "fase_iterate_synth_capacity", "fase_block_order",
-    "fase_iterate_register_atoms", "fase_iterate_complex_register_atoms",
+    "fase_iterate_register_atoms", "fase_iterate_complex_register_atoms", "fase_mirror_upper",
 )
 
 ABI_MAJOR = 3  # fase_abi_version() >> 16 of the library this binding matches
@@ -159,6 +159,7 @@ def load():
                              _vp, _i32, _vp, _i64, _vp],
         "fase_frame_widen": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _i64, _vp],
         "fase_block_order": [_vp, _i32, _i32, _vp, _vp],
+        "fase_mirror_upper": [_vp, _i64, _i32, _vp],
         "fase_frame_paste_complex": [_vp, _i64, _vp, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i32,
                                      _i32, _vp, _i32, _vp, _i64, _vp, _vp],
     }
@@ -330,6 +331,15 @@ def _order_ptr(order, B: int):
     if order.shape[0] != B:
         raise errors.ShapeError(f"order must hold one entry per block ({B}), got {order.shape[0]}")
     return _ptr(order)
+
+
+def mirror_upper(G, K: int) -> None:
+    """G[i, j] <- G[j, i] for i > j (fase_mirror_upper), in place."""
+    import torch
+
+    lib = load()
+    _require(G, "G", torch.float64, 2)
+    _check(lib.fase_mirror_upper(_ptr(G), _ld(G), K, _stream(G)))
 
 
 def block_order(counts, depth: int, order) -> None:

@@ -326,6 +326,30 @@ __global__ void flush_kernel(uint4* buf, size_t n, unsigned salt) {
     buf[i] = make_uint4(salt, salt ^ 1u, salt ^ 2u, static_cast<unsigned>(i));
 }
 
+// G[i, j] <- G[j, i] for i > j (32 x 32 tiles through shared memory): the
+// lower triangle of a table whose rows were built as independent panels
+// (multi-GPU table build) becomes the exact mirror of the upper one, as the
+// single-GPU symmetric build writes it
+__global__ void __launch_bounds__(256) mirror_upper_kernel(double* __restrict__ G, int64_t ldg,
+                                                           int K) {
+  __shared__ double tile[32][33];
+  const int tiles = (K + 31) / 32;
+  for (int64_t tt = blockIdx.x; tt < static_cast<int64_t>(tiles) * tiles; tt += gridDim.x) {
+    const int bi = static_cast<int>(tt / tiles), bj = static_cast<int>(tt % tiles);
+    if (bi < bj) continue;  // destination tiles on or below the diagonal
+    __syncthreads();
+    // read the source tile (rows bj*32.., cols bi*32..) of the upper triangle
+    for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+      const int r = bj * 32 + (e >> 5), c = bi * 32 + (e & 31);
+      tile[e >> 5][e & 31] = (r < K && c < K) ? G[static_cast<int64_t>(r) * ldg + c] : 0.0;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+      const int r = bi * 32 + (e >> 5), c = bj * 32 + (e & 31);
+      if (r < K && c < K && r > c) G[static_cast<int64_t>(r) * ldg + c] = tile[e & 31][e >> 5];
+    }
+  }
+}
 }  // namespace
 }  // namespace fase
 
@@ -444,6 +468,22 @@ extern "C" int fase_synth_paste_complex(const double* phi2, int64_t ldphi, const
   synth_paste_complex_kernel<<<B, kSynthThreads, 0, as_stream(stream)>>>(
       phi2, ldphi, sel, coef, ldo, I, idx_ptr, idx, n_shared, dst, out, ldout, max_imag);
   return check_launch("fase_synth_paste_complex");
+}
+
+extern "C" int fase_mirror_upper(double* G, int64_t ldg, int K, void* stream) {
+  if (K < 0 || ldg < K) {
+    set_error("fase_mirror_upper: bad sizes (K=%d, ldg=%lld)", K, static_cast<long long>(ldg));
+    return FASE_ERR_SHAPE;
+  }
+  if (K < 2) return FASE_OK;
+  if (!G) {
+    set_error("fase_mirror_upper: null table");
+    return FASE_ERR_SHAPE;
+  }
+  const int64_t tiles = static_cast<int64_t>((K + 31) / 32) * ((K + 31) / 32);
+  const int grid = static_cast<int>(tiles < 148 * 8 ? tiles : 148 * 8);
+  mirror_upper_kernel<<<grid, 256, 0, as_stream(stream)>>>(G, ldg, K);
+  return check_launch("fase_mirror_upper");
 }
 
 extern "C" int fase_l2_flush(void* buf, size_t bytes, void* stream) {

@@ -298,6 +298,33 @@ def gram_into(phi, w_dev, K: int, M: int, G, support=None) -> str:
     return "dmma"
 
 
+def gram_panel_worthwhile(K: int, n_support: int) -> bool:
+    """Row panels reproduce the single-GPU table bit for bit on the Ozaki path
+    (exact integer accumulation, the same per-element epilogue whatever the
+    tile), which is the one large tables take (``gram_into``)."""
+    return K >= 2048 and n_support >= 256
+
+
+def gram_panel_into(phi, w_dev, K: int, M: int, G, r0: int, r1: int, support=None) -> None:
+    """Rows r0..r1 of the non-symmetric product (Phi o w) Phi^T into G[r0:r1]
+    on the tcgen05 Ozaki path: every entry (i, j) with i <= j is bit-identical
+    to the single-GPU symmetric build (``gram_into``), so assembling all panels
+    and mirroring the upper triangle (``_native.mirror_upper``) gives that
+    table exactly (multi-GPU table build, ``shard.build_gram_tables_sharded``)."""
+    sidx, w_s = support if support is not None else gram_support(w_dev, M)
+    n_s = int(sidx.numel())
+    if not gram_panel_worthwhile(K, n_s):
+        raise ParameterError("row panels need the Ozaki table path (K >= 2048, >= 256 support "
+                             "samples)")
+    if not (0 <= r0 <= r1 <= K):
+        raise ShapeError(f"panel rows {r0}..{r1} outside 0..{K}")
+    if r1 == r0:
+        return
+    a = _native.OzakiOperand(r1 - r0, n_s, 128, G.device).split(phi[r0:r1], sidx, w_s)
+    b = _native.OzakiOperand(K, n_s, 64, G.device).split(phi, sidx)
+    _native.ozaki_gemm(a, b, G[r0:r1])
+
+
 def _gram_on_device(phi, w_dev, K: int, M: int, device, complex_rows: bool = False):
     """Real (K, table_ld) table, or complex (K, table_ld_complex) rows of conj(C)
     from the conjugate-split matrix of a complex dictionary."""

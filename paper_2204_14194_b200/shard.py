@@ -68,6 +68,64 @@ def gather_blocks(tensor, lo: int, hi: int, n_blocks: int, group=None):
     return torch.cat([p[: h - l] for p, (l, h) in zip(parts, sizes)], dim=0)
 
 
+def assemble_row_panels(G, n_rows: int, build_panel, finish=None, group=None):
+    """Cooperative build of an (n_rows, ld) table: rank r fills its row panel
+    ``block_range(n_rows, r, N)`` with ``build_panel(G, lo, hi)``, one broadcast
+    per rank (panel sizes differ by at most one row) hands every panel to every
+    rank, and ``finish(G)`` completes the table locally (the Gram build mirrors
+    the upper triangle). SURVEY 8(e): each GPU computes 1/N of the row panels
+    instead of the whole table."""
+    import torch.distributed as dist
+
+    rank, world = _world(group)
+    lo, hi = block_range(n_rows, rank, world)
+    build_panel(G, lo, hi)
+    if world > 1:
+        for r in range(world):
+            l, h = block_range(n_rows, r, world)
+            if h > l:
+                dist.broadcast(G[l:h], src=r if group is None else dist.get_global_rank(group, r),
+                               group=group)
+    if finish is not None:
+        finish(G)
+    return G
+
+
+def build_gram_tables_sharded(dictionary, weight, device=None, group=None):
+    """``build_gram_tables`` with the table rows split over the ranks: each rank
+    builds its row panel of the non-symmetric product on the tensor cores
+    (``fast.gram_panel_into``), the panels are broadcast (NCCL over NVLink),
+    and every rank mirrors the upper triangle and derives D. The result is
+    bit-identical to the single-GPU table (entries i <= j are computed the
+    same way, the mirror copies them). Dictionaries off the Ozaki table path
+    (complex, small K) build the whole table on every rank."""
+    import torch
+
+    from . import _native
+    from .fast import (GramTable, _device_vector, build_gram_tables, gram_panel_into,
+                       gram_panel_worthwhile, gram_support, resolve_device)
+
+    dev = resolve_device(device)
+    w = np.asarray(weight, dtype=np.float64).ravel()
+    K, M = len(dictionary), dictionary.area
+    _, world = _world(group)
+    if world == 1 or not dictionary.is_real or w.size != M:
+        return build_gram_tables(dictionary, weight, device=dev)
+    w_dev = _device_vector(w, dictionary.ld, dev)
+    support = gram_support(w_dev, M)
+    if not gram_panel_worthwhile(K, int(support[0].numel())):
+        return build_gram_tables(dictionary, weight, device=dev)
+    phi = dictionary.device_matrix(dev)
+    G = torch.zeros((K, _native.table_ld(K)), dtype=torch.float64, device=dev)
+    assemble_row_panels(
+        G, K, lambda g, lo, hi: gram_panel_into(phi, w_dev, K, M, g, lo, hi, support),
+        finish=lambda g: _native.mirror_upper(g, K), group=group)
+    D = torch.empty(K, dtype=torch.float64, device=dev)
+    alive = torch.zeros(1, dtype=torch.int32, device=dev)
+    _native.gram_finish(G, K, D, alive)
+    return GramTable(G=G, D=D, source=(dictionary, w.copy()), n_alive=int(alive.item()))
+
+
 class ResultArena:
     """Per-rank result rows of a sharded batch in one contiguous byte buffer.
 

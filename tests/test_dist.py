@@ -240,3 +240,58 @@ def test_result_arena_layout_single_process():
         s2, c2, l2 = a.assemble(1)
         assert (s2 == -3).all() and (c2 == 2.5).all() and (l2 == 7.0).all()
         assert (a.assemble(0)[0] == 0).all()  # slot 0 untouched
+
+
+def _panel_worker(rank, world, port, n_rows, ld, out_q):
+    """Row-panel table build (shard.assemble_row_panels): each rank fills its
+    rows of a non-symmetric stand-in product, one broadcast per rank, and the
+    local finish mirrors the upper triangle -- the host logic of the multi-GPU
+    Gram build (fast.gram_panel_into + fase_mirror_upper on the GPU)."""
+    from paper_2204_14194_b200.shard import assemble_row_panels
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(3)  # small integers: every product exact in any order
+    A = torch.from_numpy(rng.integers(-9, 10, size=(n_rows, 5)).astype(np.float64))
+    B = torch.from_numpy(rng.integers(-9, 10, size=(n_rows, 5)).astype(np.float64))
+    G = torch.full((n_rows, ld), float("nan"), dtype=torch.float64)  # unbuilt rows stay NaN
+    G[:, n_rows:] = 0.0
+    built = []
+
+    def panel(g, lo, hi):
+        built.append((lo, hi))
+        g[lo:hi, :n_rows] = A[lo:hi] @ B.T  # (A_i . B_j): not symmetric
+
+    def finish(g):
+        up = torch.triu(g[:, :n_rows])
+        g[:, :n_rows] = up + torch.triu(up, diagonal=1).T
+
+    assemble_row_panels(G, n_rows, panel, finish=finish)
+    out_q.put((rank, built, G.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_rows", [7, 12])
+def test_gloo_world2_row_panel_table_build(n_rows):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ld = n_rows + 3
+    procs = [ctx.Process(target=_panel_worker, args=(r, 2, port, n_rows, ld, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(3)
+    A = rng.integers(-9, 10, size=(n_rows, 5)).astype(np.float64)
+    B = rng.integers(-9, 10, size=(n_rows, 5)).astype(np.float64)
+    P = A @ B.T
+    want = np.triu(P) + np.triu(P, 1).T  # the upper triangle, mirrored
+    for rank, built, G in got:
+        assert built == [block_range(n_rows, rank, 2)]  # each rank built only its panel
+        assert np.array_equal(G[:, :n_rows], want)
+        assert np.array_equal(G[:, :n_rows], G[:, :n_rows].T)
+        assert (G[:, n_rows:] == 0).all()

@@ -265,3 +265,34 @@ def test_batch_api_uses_ozaki_for_large_dense_batches():
                               metric_fn(ref["r0"], ref["d"], ref["log"]))
         assert v.ok
         assert rel_dev(res.coefficients[b].cpu().numpy()[: v.stop], ref["coefficients"].real[: v.stop]) < 1e-9
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_gram_row_panels_bit_identical(world):
+    """The multi-GPU table build (shard.build_gram_tables_sharded): each rank's
+    row panel of the non-symmetric Ozaki product, assembled and mirrored
+    (fase_mirror_upper), equals the single-GPU symmetric table bit for bit --
+    here the N ranks' panels are built one after another on one GPU."""
+    from paper_2204_14194_b200 import _native
+    from paper_2204_14194_b200.fast import _device_vector, gram_into, gram_panel_into, gram_support
+    from paper_2204_14194_b200.shard import block_range
+
+    d = parse_dict_spec("gauss:2304:7", 24, 24)
+    mask = wl.central_loss_mask(24, 24, 8, 8)
+    w = build_weight_field(mask, 0.85)
+    K, M = len(d), d.area
+    dev = torch.device(DEV)
+    phi = d.device_matrix(dev)
+    w_dev = _device_vector(w.ravel(), d.ld, dev)
+    support = gram_support(w_dev, M)
+    ld = _native.table_ld(K)
+    G1 = torch.zeros((K, ld), dtype=torch.float64, device=dev)
+    assert gram_into(phi, w_dev, K, M, G1, support) == "ozaki"
+    G2 = torch.full((K, ld), float("nan"), dtype=torch.float64, device=dev)
+    G2[:, K:] = 0.0
+    for r in range(world):
+        lo, hi = block_range(K, r, world)
+        gram_panel_into(phi, w_dev, K, M, G2, lo, hi, support)
+    _native.mirror_upper(G2, K)
+    torch.cuda.synchronize()
+    assert torch.equal(G1, G2)
