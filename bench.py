@@ -638,25 +638,35 @@ def run_gpu(args):
         e1.record(stream)
         return [[e0, e1]]
 
-    def timed():
+    def timed(steps, split=False):
+        """``steps`` device-resident steps, each between two events (L2 flushed
+        before each). ``split``: also events between the stages -- a separate,
+        untimed diagnostic pass, since an event between two kernels serializes
+        them (the latency shapes' programmatic dependent launch) and adds its
+        own gap to a ~100 us step."""
         evs = []
-        for _ in range(args.steps):
+        for _ in range(steps):
             _native.l2_flush(flush)
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            e = [torch.cuda.Event(enable_timing=True) if split or i in (0, 4) else None
+                 for i in range(5)]
             e[0].record(stream)
             plan._products(sig_view)  # signals resident in HBM, read in place
-            e[1].record(stream)
+            if split:
+                e[1].record(stream)
             if plan.fused_synth:  # recursion with the synthesis inside
                 plan._iterate_synth(plan.selected, plan.projections, plan.coefficients,
                                     plan.lost)
-                e[2].record(stream)
+                if split:
+                    e[2].record(stream)
             else:
                 iterate(plan.G, plan.D, plan.R0, K, I, w.config.gamma, plan.selected,
                         plan.projections, plan.coefficients)
-                e[2].record(stream)
+                if split:
+                    e[2].record(stream)
                 synth(plan.phi_lost, plan.selected, plan.coefficients, I, plan.lost_seq,
                       plan.lost, n_shared=plan.n_lost, dst=plan.lost_pos, **synth_extra)
-            e[3].record(stream)
+            if split:
+                e[3].record(stream)
             sb.arena.gather(0)  # results of every rank to the root (NCCL; no-op at N=1)
             e[4].record(stream)
             evs.append(e)
@@ -673,7 +683,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     with ClockSampler(gpu_id) as clocks:
         t_wall0 = time.perf_counter()
-        ev_dev = timed()
+        ev_dev = timed(args.steps)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -684,10 +694,16 @@ def run_gpu(args):
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
     dev_ms = [e[0].elapsed_time(e[4]) for e in ev_dev]
-    init_ms = [e[0].elapsed_time(e[1]) for e in ev_dev]
-    iter_ms = [e[1].elapsed_time(e[2]) for e in ev_dev]
-    synth_ms = [e[2].elapsed_time(e[3]) for e in ev_dev]
-    gather_ms = [e[3].elapsed_time(e[4]) for e in ev_dev]
+    # the stage split: a separate pass after the clock (stage events inside the
+    # timed steps would serialize the kernels they sit between)
+    ev_split = timed(min(args.steps, 20), split=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    init_ms = [e[0].elapsed_time(e[1]) for e in ev_split]
+    iter_ms = [e[1].elapsed_time(e[2]) for e in ev_split]
+    synth_ms = [e[2].elapsed_time(e[3]) for e in ev_split]
+    gather_ms = [e[3].elapsed_time(e[4]) for e in ev_split]
     e2e_ms = [e[0].elapsed_time(e[1]) for e in ev_e2e]
     tot = torch.tensor([sum(dev_ms), sum(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -812,6 +828,8 @@ def run_gpu(args):
             "recursion_agreement": agreement,
             "stage_ms": {"init_products": float(np.mean(init_ms)), "iterate": float(np.mean(iter_ms)),
                          "synth": float(np.mean(synth_ms)), "gather": float(np.mean(gather_ms))},
+            "stage_ms_pass": f"{len(ev_split)} untimed steps after the clock with events between "
+                             "the stages (the timed steps carry events at their ends only)",
             "shard": {"blocks_total": B_total, "blocks_rank0": B, "ranks": world,
                       "gather_bytes_per_rank": sb.arena.nbytes,
                       "collective": "torch.distributed.gather (NCCL) of one result arena per "

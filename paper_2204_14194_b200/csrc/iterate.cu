@@ -84,6 +84,10 @@ constexpr unsigned kNone = 0xffffffffu;
 #ifndef FASE_STAGGER_NS
 #define FASE_STAGGER_NS 0
 #endif
+// programmatic dependent launch of the latency shapes (measurement knob: 0 off)
+#ifndef FASE_PDL
+#define FASE_PDL 1
+#endif
 // Scaled recursion, per-iteration critical path (measurement knob, bits):
 //  1: the running max keeps the signed R' of the best element and compares
 //     magnitudes with |.| operand modifiers (no |R'| materialised per element:
@@ -148,6 +152,10 @@ template <int NT, int EPT, int MINB, bool kDsmem, bool kChunked, bool kRecord, i
           bool kScaled = false, int SYN = 0, int SPEC = 0>
 __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_iterate_args a,
                                                                      const fase_synth_fused syn) {
+  // programmatic dependent launch (latency shapes): the grid may be scheduled
+  // while the kernel that writes R0 finishes; wait for its results here (a
+  // no-op for ordinary launches)
+  if constexpr (SPEC != 0 || SYN > 0) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   constexpr int EP = EPT / 2;
   constexpr int NW = NT / 32;
   static_assert(SPEC == 0 || (NB == 1 && !kChunked && !kRecord), "speculative staging: one "
@@ -1354,7 +1362,24 @@ extern "C" int fase_iterate_synth(const fase_iterate_args* args, const fase_synt
     set_error("fase_iterate_synth: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return FASE_ERR_CUDA;
   }
-  v->fused<<<a.B, v->nt, smem, as_stream(stream)>>>(a, *syn);
+  // one block per SM at most: launched as a programmatic dependent of the
+  // products kernel before it (which releases it at its start), so this grid is
+  // resident when the products finish instead of launching after them
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.B);
+  cfg.blockDim = dim3(v->nt);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = FASE_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, v->fused, a, *syn);
+  if (e != cudaSuccess) {
+    set_error("fase_iterate_synth: launch: %s", cudaGetErrorString(e));
+    return FASE_ERR_CUDA;
+  }
   return check_launch("fase_iterate_synth");
 }
 

@@ -279,6 +279,9 @@ __global__ void __launch_bounds__(288, MINB) sep_products_dmma_kernel(
     const double* __restrict__ W, int64_t ldw, double* __restrict__ R0, int64_t ldr) {
   extern __shared__ __align__(16) double sm[];
   constexpr bool kStage = MINB == 1;
+  // small batches: release a programmatic dependent (the latency recursion)
+  // now, so it is scheduled while these products run (it waits for them)
+  if constexpr (MINB == 1) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31, fr = lane >> 2, fc = lane & 3;
