@@ -36,7 +36,7 @@ import numpy as np
 
 from . import _native
 from .dictionary import Dictionary, parse_dict_spec
-from .errors import ParameterError, ShapeError
+from .errors import ParameterError, ShapeError, UnsupportedDictionaryError
 from .fast import ChunkedTables, fase_extrapolate_batch, resolve_device
 from .grid import ExtrapConfig, as_mask, base_weight, psnr_over_region
 from .model import BatchResult
@@ -268,10 +268,15 @@ class FrameEngine:
         X, R0 = b["X"], b["R0"]
         if self.complex:
             if self._cparts:  # conj(E) X conj(F)^T per separable part; the rest by GEMM
-                for rre, rim, cre, cim, row0 in self._cparts:
-                    _native.sep_products_complex(rre, rim, cre, cim, X, self.A, self.A, R0, row0)
+                try:
+                    for rre, rim, cre, cim, row0 in self._cparts:
+                        _native.sep_products_complex(rre, rim, cre, cim, X, self.A, self.A, R0,
+                                                     row0)
+                    uncovered = self._uncovered()
+                except UnsupportedDictionaryError:  # area too large for the transform
+                    uncovered = np.ones(self.K, dtype=bool)
                 Rv = _real_view(R0)
-                for lo, hi in _ranges(self._uncovered()):
+                for lo, hi in _ranges(uncovered):
                     _native.gemm_nt(X[:, : self.M], self.phi[2 * lo: 2 * hi, : self.M], Rv[:, 2 * lo:])
             elif self._oz_phi is not None and "oz" in b:
                 _native.ozaki_gemm(b["oz"].split(X), self._oz_phi, _real_view(R0))
@@ -279,12 +284,17 @@ class FrameEngine:
                 _native.gemm_nt(X[:, : self.M], self.phi[:, : self.M], _real_view(R0))
             return
         factors = self.dictionary.device_factors(self.device)
-        if factors and len(factors) <= 8:  # separable parts on DMMA, one launch
-            _native.sep_products_batch(factors, X, None, self.A, self.A, R0)
-        elif factors:  # rows X cols^T per part (csrc/separable.cu)
-            for rows, cols, row0 in factors:
-                _native.sep_products(rows, cols, X, self.A, self.A, R0, row0)
-        elif self._oz_phi is not None and "oz" in b:
+        if factors:
+            try:
+                if len(factors) <= 8:  # separable parts on DMMA, one launch
+                    _native.sep_products_batch(factors, X, None, self.A, self.A, R0)
+                else:  # rows X cols^T per part (csrc/separable.cu)
+                    for rows, cols, row0 in factors:
+                        _native.sep_products(rows, cols, X, self.A, self.A, R0, row0)
+                return
+            except UnsupportedDictionaryError:  # area too large for the transform
+                pass
+        if self._oz_phi is not None and "oz" in b:
             _native.ozaki_gemm(b["oz"].split(X), self._oz_phi, R0)
         else:
             _native.gemm_nt(X[:, : self.M], self.phi[:, : self.M], R0)

@@ -373,9 +373,16 @@ def initial_products_into(dictionary: Dictionary, F, W, R0, ws, *, method: str =
         _native.weigh(F, W, M, X)
         m, n = dictionary.shape
         covered = np.zeros(K, dtype=bool)
-        for rre, rim, cre, cim, row0 in parts:
-            _native.sep_products_complex(rre, rim, cre, cim, X, m, n, R0, row0)
-            covered[row0: row0 + rre.shape[0] * cre.shape[0]] = True
+        try:
+            for rre, rim, cre, cim, row0 in parts:
+                _native.sep_products_complex(rre, rim, cre, cim, X, m, n, R0, row0)
+                covered[row0: row0 + rre.shape[0] * cre.shape[0]] = True
+        except UnsupportedDictionaryError:
+            # areas whose factor tables exceed shared memory (about 71 x 71 and
+            # up; the library refuses before launching): every row by GEMM
+            if method == "separable":
+                raise
+            covered[:] = False
         phi2 = dictionary.device_matrix(dev)
         Rv = _real_view(R0)
         for lo, hi in _ranges(~covered):  # the remaining rows: one DMMA GEMM each
@@ -388,16 +395,24 @@ def initial_products_into(dictionary: Dictionary, F, W, R0, ws, *, method: str =
         _native.init_products(dictionary.device_matrix(dev), F, W, K, M, R0, ws=ws)
         return "gemm"
     m, n = dictionary.shape
-    if len(factors) <= 8:  # weights fused, all parts in one DMMA launch
-        _native.sep_products_batch(factors, F, W, m, n, R0)
+    try:
+        if len(factors) <= 8:  # weights fused, all parts in one DMMA launch
+            _native.sep_products_batch(factors, F, W, m, n, R0)
+            return "separable"
+        B = F.shape[0]
+        ldx = M + (M & 1)
+        X = ws[: B * ldx].view(B, ldx)
+        _native.weigh(F, W, M, X)
+        for rows, cols, row0 in factors:
+            _native.sep_products(rows, cols, X, m, n, R0, row0)
         return "separable"
-    B = F.shape[0]
-    ldx = M + (M & 1)
-    X = ws[: B * ldx].view(B, ldx)
-    _native.weigh(F, W, M, X)
-    for rows, cols, row0 in factors:
-        _native.sep_products(rows, cols, X, m, n, R0, row0)
-    return "separable"
+    except UnsupportedDictionaryError:
+        # areas too large for the shared-memory transform (refused before
+        # launching): the dense products cover every row
+        if method == "separable":
+            raise
+        _native.init_products(dictionary.device_matrix(dev), F, W, K, M, R0, ws=ws)
+        return "gemm"
 
 
 def ozaki_worthwhile(rows: int, cols: int) -> bool:

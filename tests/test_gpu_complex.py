@@ -392,3 +392,38 @@ def test_maximum_atom_count_complex():
         assert np.array_equal(res.coefficients[b].cpu().numpy(), coef)
     with pytest.raises(UnsupportedDictionaryError):
         _native.table_ld_complex(_native.max_atoms_complex() + 1)
+
+
+def test_large_area_products_fall_back_to_gemm():
+    """dft over a 72 x 72 area (5,184 atoms): the complex separable transform's
+    factor tables exceed shared memory, so the products take the dense GEMM for
+    every row (the library refuses the transform before launching); R0 matches
+    the oracle, and the batch entry point runs end to end."""
+    from paper_2204_14194_b200.fast import initial_products_into  # noqa: F401
+
+    d = parse_dict_spec("dft", 72, 72)
+    mask = wl.central_loss_mask(72, 72, 8, 8)
+    w = build_weight_field(mask, 0.8)
+    sig = np.random.default_rng(31).uniform(0, 255, (72, 72))
+    got = initial_scalar_products(sig, w, d, device=DEV)
+    want = orc.initial_products(sig, w, d.values.reshape(len(d), -1))
+    assert rel_dev(got.real, want.real) < 1e-13 and rel_dev(got.imag, want.imag) < 1e-13
+    r = fase_extrapolate_batch(np.stack([sig, sig[::-1]]), mask, d, None, ExtrapConfig(5),
+                               device=DEV)
+    assert r.selected.shape == (2, 5) and (r.selected >= 0).all()
+
+
+def test_large_area_real_products_fall_back_to_gemm():
+    """dct over a 112 x 112 area (12,544 atoms: also past the register kernels):
+    the real separable transform does not fit shared memory either, the dense
+    products take over; R0 matches the oracle and a short batch runs end to end
+    through the streaming recursion."""
+    d = parse_dict_spec("dct", 112, 112)
+    mask = wl.central_loss_mask(112, 112, 16, 16)
+    w = build_weight_field(mask, 0.8)
+    sig = np.random.default_rng(32).uniform(0, 255, (112, 112))
+    got = initial_scalar_products(sig, w, d, device=DEV)
+    want = orc.initial_products(sig, w, d.values.reshape(len(d), -1))
+    assert rel_dev(got.real, want.real) < 1e-13
+    r = fase_extrapolate_batch(sig[None], mask, d, None, ExtrapConfig(3), device=DEV)
+    assert (r.selected >= 0).all()

@@ -290,6 +290,55 @@ def case_frame_complex():
     return [f64.clone(), r.selected, r.coefficients, r.patched, r.max_imag]
 
 
+def case_streaming():
+    """Beyond the register kernels (csrc/iterate_generic.cu): a shared-geometry
+    batch and per-block geometries (chunk lists) with K = 12,289 real atoms."""
+    from paper_2204_14194_b200 import _native
+
+    K = _native.register_atoms() + 1
+    d = gauss(K, 12, 12)
+    mask = wl.central_loss_mask(12, 12, 4, 4)
+    cfg = ExtrapConfig(6)
+    r1 = fase_extrapolate_batch(sig(3, 12, 12), mask, d, None, cfg, device=DEV)
+    r2 = fase_extrapolate_batch(sig(4, 12, 12), per_block_masks(4, 12, 12), d, None, cfg,
+                                device=DEV)
+    return [r1.selected, r1.coefficients, r1.patched, r2.selected, r2.coefficients, r2.patched]
+
+
+def case_streaming_complex():
+    """The complex streaming recursion: dft on 79 x 79 (6,241 complex atoms)."""
+    d = parse_dict_spec("dft", 79, 79)
+    mask = wl.central_loss_mask(79, 79, 9, 9)
+    r = fase_extrapolate_batch(sig(2, 79, 79), mask, d, None, ExtrapConfig(4), device=DEV)
+    return [r.selected, r.coefficients, r.patched]
+
+
+def case_gram_panels():
+    """Row-panel table build (multi-GPU path) on one GPU: three ranks' Ozaki
+    panels, the mirror kernel, against the symmetric build."""
+    from paper_2204_14194_b200 import _native
+    from paper_2204_14194_b200.fast import _device_vector, gram_into, gram_panel_into, gram_support
+    from paper_2204_14194_b200.shard import block_range
+
+    d = gauss(2304, 24, 24)
+    w = build_weight_field(wl.central_loss_mask(24, 24, 8, 8), 0.85)
+    K, M = len(d), d.area
+    phi = d.device_matrix(DEV)
+    frozen(phi)
+    w_dev = _device_vector(w.ravel(), d.ld, DEV)
+    support = gram_support(w_dev, M)
+    G1 = torch.zeros((K, _native.table_ld(K)), dtype=torch.float64, device=DEV)
+    gram_into(phi, w_dev, K, M, G1, support)
+    G2 = torch.zeros_like(G1)
+    for r in range(3):
+        lo, hi = block_range(K, r, 3)
+        gram_panel_into(phi, w_dev, K, M, G2, lo, hi, support)
+    _native.mirror_upper(G2, K)
+    torch.cuda.synchronize()
+    assert torch.equal(G1, G2), "row panels differ from the symmetric build"
+    return [G1, G2]
+
+
 CASES = {k[5:]: v for k, v in globals().items() if k.startswith("case_")}
 
 
