@@ -1014,3 +1014,52 @@ def test_complex_signals(spec):
     assert np.abs(out[mask] - g.real[mask]).max() <= 1e-12 * np.abs(g).max()
     assert np.array_equal(out[~mask], s[~mask])
     assert abs(max_imag - np.abs(g.imag[mask]).max()) <= 1e-12 * np.abs(g).max()
+
+
+@pytest.mark.parametrize("case", ["no_loss", "one_sample_area", "iterations_beyond_k",
+                                  "gamma_rho_one", "single_block_per_block_mask"])
+def test_drop_in_edge_shapes(case):
+    """Edge shapes of the drop-in batch call against the oracle's per-block
+    pipeline (weights -> tables -> R0 -> recursion -> synthesis -> paste):
+    nothing lost, a 1 x 2 area, more iterations than atoms, gamma = rho = 1,
+    a one-block batch with its own mask (chunked path)."""
+    rng = np.random.default_rng(41)
+    if case == "no_loss":
+        d, m, n = generate_dictionary("dct", 6, 6), 6, 6
+        masks = np.zeros((6, 6), dtype=bool)
+        cfg, B = ExtrapConfig(8), 3
+    elif case == "one_sample_area":
+        d, m, n = Dictionary(rng.standard_normal((3, 1, 2))), 1, 2
+        masks = np.array([[False, True]])
+        cfg, B = ExtrapConfig(4), 2
+    elif case == "iterations_beyond_k":
+        d, m, n = generate_dictionary("wht", 4, 4), 4, 4
+        masks = wl.central_loss_mask(4, 4, 2, 2)
+        cfg, B = ExtrapConfig(60), 2
+    elif case == "gamma_rho_one":
+        d, m, n = generate_dictionary("dct", 8, 8), 8, 8
+        masks = wl.central_loss_mask(8, 8, 2, 4)
+        cfg, B = ExtrapConfig(12, 1.0, 1.0), 2
+    else:
+        d, m, n = parse_dict_spec("union:dct+had", 12, 12), 12, 12
+        masks = wl.central_loss_mask(12, 12, 4, 4)[None].copy()
+        masks[0, 0:2, 0:2] = True
+        cfg, B = ExtrapConfig(10), 1
+    sig = rng.uniform(0, 255, (B, m, n))
+    res = fase_extrapolate_batch(sig, masks, d, None, cfg, device=DEV)
+    vals = d.real_values().astype(np.complex128)
+    for b in range(B):
+        mb = masks if masks.ndim == 2 else masks[b]
+        ref = orc.extrapolate_block(sig[b], mb, vals, cfg.gamma, cfg.iterations, cfg.rho_hat,
+                                    record=True)
+        v = compare_selection(res.selected[b].cpu().numpy(), ref["selected"],
+                              metric_fn(ref["r0"], ref["d"], ref["log"]))
+        assert v.ok, (case, b, v)
+        s = v.stop
+        scale = max(np.abs(ref["coefficients"][:s]).max(initial=0.0), 1e-300)
+        assert np.abs(res.coefficients[b].cpu().numpy()[:s] - ref["coefficients"].real[:s]).max(
+            initial=0.0) <= COEF_REL * scale
+        got = res.patched[b].cpu().numpy()
+        assert np.array_equal(got[~mb], sig[b][~mb])  # support untouched
+        if v.exact and mb.any():
+            assert rel_dev(got[mb], ref["patched"][mb]) < COEF_REL
