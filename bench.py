@@ -663,8 +663,11 @@ def run_gpu(args):
                         plan.projections, plan.coefficients)
                 if split:
                     e[2].record(stream)
-                synth(plan.phi_lost, plan.selected, plan.coefficients, I, plan.lost_seq,
-                      plan.lost, n_shared=plan.n_lost, dst=plan.lost_pos, **synth_extra)
+                if cplx:
+                    synth(plan.phi_lost, plan.selected, plan.coefficients, I, plan.lost_seq,
+                          plan.lost, n_shared=plan.n_lost, dst=plan.lost_pos, **synth_extra)
+                else:  # the plan's synthesis (Ozaki product or per-block paste)
+                    plan._synth(plan.selected, plan.coefficients, plan.lost)
             if split:
                 e[3].record(stream)
             sb.arena.gather(0)  # results of every rank to the root (NCCL; no-op at N=1)
@@ -823,6 +826,8 @@ def run_gpu(args):
             "products": plan.products_method,
             "recursion": recursion,
             "fused_synth": plan.fused_synth,
+            "synthesis": ("ozaki (sparse models x Phi_lost^T, %d digit planes)" % plan._synth_oz[0].slices
+                          if plan._synth_oz is not None else ("fused" if plan.fused_synth else "paste")),
             "l2_hint": l2_hint,
             "parity_vs_reference": parity,
             "recursion_agreement": agreement,

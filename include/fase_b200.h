@@ -475,6 +475,18 @@ FASE_API int fase_ozaki_gemm(const int8_t* a_planes, int a_rows_pad, const int32
                              int m_rows, const int8_t* b_planes, int b_rows_pad,
                              const int32_t* eb, int n_rows, int64_t kp, int slices, double* C,
                              int64_t ldc, void* stream);
+/* Synthesis of a shared geometry's lost samples as one Ozaki product
+ * (SparseModel.materialize, reference.py:120-125, at the lost samples; the
+ * plan's batched apply_model, fast.py:267-286): row r of V is block r's sparse
+ * model scattered to a dense coefficient vector, v[r, sel[r*ldsel + t]] +=
+ * coef[r*ldcoef + t] for t < iters (sel < 0 or >= kd: no term; repeated atoms
+ * summed in term order), cut into digit planes exactly like
+ * fase_ozaki_split; then fase_ozaki_gemm(V planes, Phi_lost^T planes) gives
+ * g[r, i] = sum_k v[r, k] phi_k[lost_i] to the planes' precision. */
+FASE_API int fase_ozaki_split_sparse(const int32_t* sel, int64_t ldsel, const double* coef,
+                                     int64_t ldcoef, int rows, int iters, int kd, int slices,
+                                     int8_t* planes, int64_t kp, int rows_pad, int32_t* exps,
+                                     void* stream);
 /* The weighted Gram table on the same path (build_gram_tables, fast.py:109-142):
  * planes of Phi o w (A) and Phi (B), K rows each; only tiles holding entries
  * k <= l are computed, each such entry written to (k, l) and (l, k): G is

@@ -36,7 +36,7 @@ EXPORTS = (
     "fase_frame_paste", "fase_weigh", "fase_sep_products", "fase_gram_complex_workspace",
     "fase_gram_complex", "fase_max_atoms_complex", "fase_table_ld_complex", "fase_iterate_complex",
     "fase_synth_paste_complex", "fase_sep_products_complex", "fase_fft_gram", "fase_weigh_gather",
-    "fase_ozaki_split", "fase_ozaki_gemm", "fase_ozaki_gram", "fase_sep_products_batch",
+    "fase_ozaki_split", "fase_ozaki_split_sparse", "fase_ozaki_gemm", "fase_ozaki_gram", "fase_sep_products_batch",
     "fase_iterate_scaled", "fase_scale_columns", "fase_iterate_scaled_synth_capacity",
     "fase_iterate_complex_scaled", "fase_frame_widen", "fase_frame_paste_complex",
     "fase_iterate_synth", "fase_iterate_synth_capacity", "fase_block_order",
@@ -142,6 +142,8 @@ def load():
         "fase_sep_products_batch": [ctypes.POINTER(SepPart), _i32, _i32, _i32, _vp, _i64, _vp,
                                     _i64, _i32, _vp, _i64, _vp],
         "fase_ozaki_split": [_vp, _i64, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _vp, _vp],
+        "fase_ozaki_split_sparse": [_vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _i64, _i32,
+                                    _vp, _vp],
         "fase_ozaki_gemm": [_vp, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i64, _i32, _vp, _i64,
                             _vp],
         "fase_ozaki_gram": [_vp, _i32, _vp, _vp, _i32, _vp, _i32, _i64, _i32, _vp, _i64, _vp],
@@ -747,7 +749,16 @@ def weigh_gather(x, idx, w, out) -> None:
                                  _ptr(out), _ld(out), _stream(out)))
 
 
+# Digit planes per FP64 operand. Shared tables keep 8 (56 bits of each row's
+# scale: the DMMA table to a few ulp). The batched initial products use 7 (49
+# bits, 28 plane pairs instead of 36): config 4 R0 within 2.8e-13 of the DMMA
+# products (max |dR0| / max |R0|), every one of the 4,096 selected sequences
+# still identical to the reference's, coefficients within 3.4e-13 of it, and
+# the products 2.74 -> 2.28 ms (259.6K -> 269.1K blocks/s; 6 planes: 1.94 ms
+# but 3.1e-11, too little margin for the 1e-9 near-tie rule after 500 updates;
+# profiles/r02d/ab_slices.txt). FASE_PRODUCT_SLICES overrides (6-8).
 OZAKI_SLICES = 8
+PRODUCT_SLICES = int(os.environ.get("FASE_PRODUCT_SLICES", "7"))
 
 
 class OzakiOperand:
@@ -778,6 +789,24 @@ class OzakiOperand:
         _check(lib.fase_ozaki_split(_ptr(x), _ld(x), _ptr(idx), _ptr(w), self.rows, self.kd,
                                     self.slices, _ptr(self.planes), self.kp, self.rows_pad,
                                     _ptr(self.exps), _stream(x)))
+        return self
+
+
+    def split_sparse(self, sel, coef, iters: int) -> "OzakiOperand":
+        """Planes of the dense coefficient rows of sparse models: row r is
+        sum_t coef[r, t] e_{sel[r, t]} over t < iters (sel int32 (rows, >= iters),
+        coef float64 (rows, >= iters); sel < 0 adds nothing), kd = atoms."""
+        import torch
+
+        lib = load()
+        _require(sel, "sel", torch.int32, 2)
+        _require(coef, "coef", torch.float64, 2)
+        if sel.shape[0] < self.rows or coef.shape[0] < self.rows:
+            raise errors.ShapeError("split_sparse: fewer model rows than operand rows")
+        _check(lib.fase_ozaki_split_sparse(_ptr(sel), _ld(sel), _ptr(coef), _ld(coef), self.rows,
+                                           iters, self.kd, self.slices, _ptr(self.planes),
+                                           self.kp, self.rows_pad, _ptr(self.exps),
+                                           _stream(coef)))
         return self
 
 

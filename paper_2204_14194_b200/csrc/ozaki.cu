@@ -70,6 +70,63 @@ __device__ __forceinline__ int64_t plane_offset(int r, int64_t k, int64_t rows_p
 // 16-byte chunk per plane.
 constexpr int OZ_SPLIT_THREADS = 256;
 
+// Cut the staged row s_v (kp values, one pad per 16) into S digit planes of
+// row r: e = smallest integer with max|v| < 2^e (m = max|v| over the row, block-
+// uniform), then each thread cuts 16 consecutive k into S truncated base-2^7
+// digits of v * 2^-e (each step exact) and stores one 16-byte chunk per plane.
+template <int S>
+__device__ __forceinline__ void cut_row_planes(const double* s_v, double m, int r, int64_t kp,
+                                               int64_t rows_pad, int64_t plane_stride,
+                                               int8_t* __restrict__ planes,
+                                               int32_t* __restrict__ exps) {
+  const int tid = threadIdx.x;
+  const int chunks = static_cast<int>(kp >> 4);
+  const int e = m > 0.0 ? ilogb(m) + 1 : 0;
+  if (tid == 0) exps[r] = e;
+  for (int c = tid; c < chunks; c += OZ_SPLIT_THREADS) {
+    uint32_t packed[S][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int i = 0; i < S; ++i) packed[i][q] = 0u;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        double y = s_v[17 * c + 4 * q + b];
+        if (y == 0.0) continue;  // all digits 0 (most entries of sparse model rows)
+        y = scalbn(y, -e);       // |y| < 1, exact
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+          y = y * 128.0;               // exact
+          const double t = trunc(y);  // |t| <= 127
+          y -= t;                      // exact
+          packed[i][q] |= (static_cast<uint32_t>(static_cast<int>(t)) & 0xffu) << (8 * b);
+        }
+      }
+    }
+    const int64_t off = plane_offset(r, 16 * static_cast<int64_t>(c), rows_pad);
+#pragma unroll
+    for (int i = 0; i < S; ++i)
+      *reinterpret_cast<uint4*>(planes + i * plane_stride + off) =
+          make_uint4(packed[i][0], packed[i][1], packed[i][2], packed[i][3]);
+  }
+}
+
+// block-wide max of the per-thread m (s_max: OZ_SPLIT_THREADS / 32 slots)
+__device__ __forceinline__ double block_max_abs(double m, double* s_max) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) s_max[warp] = m;
+  __syncthreads();
+  m = s_max[0];
+#pragma unroll
+  for (int i = 1; i < OZ_SPLIT_THREADS / 32; ++i) m = fmax(m, s_max[i]);
+  return m;
+}
+
+// Digit planes of one FP64 row per CTA: v[k] = x[r, idx[k]] * w[k] (idx / w
+// optional: the weighted operand restricted to the support, rounded once like
+// fase_weigh_gather) is staged in shared memory with coalesced loads, then cut.
 template <int S>
 __global__ void __launch_bounds__(OZ_SPLIT_THREADS) ozaki_split_kernel(
     const double* __restrict__ x, int64_t ldx, const int32_t* __restrict__ idx,
@@ -77,8 +134,7 @@ __global__ void __launch_bounds__(OZ_SPLIT_THREADS) ozaki_split_kernel(
     int64_t rows_pad, int64_t plane_stride, int32_t* __restrict__ exps) {
   extern __shared__ double s_v[];  // kp + kp/16 (one pad per 16 against bank conflicts)
   __shared__ double s_max[OZ_SPLIT_THREADS / 32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int chunks = static_cast<int>(kp >> 4);
+  const int tid = threadIdx.x;
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     const double* xr = x + static_cast<int64_t>(r) * ldx;
     double m = 0.0;
@@ -91,39 +147,73 @@ __global__ void __launch_bounds__(OZ_SPLIT_THREADS) ozaki_split_kernel(
       s_v[k + (k >> 4)] = v;
       m = fmax(m, fabs(v));
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) s_max[warp] = m;
-    __syncthreads();
-    m = s_max[0];
-#pragma unroll
-    for (int i = 1; i < OZ_SPLIT_THREADS / 32; ++i) m = fmax(m, s_max[i]);
-    const int e = m > 0.0 ? ilogb(m) + 1 : 0;
-    if (tid == 0) exps[r] = e;
-    for (int c = tid; c < chunks; c += OZ_SPLIT_THREADS) {
-      uint32_t packed[S][4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-#pragma unroll
-        for (int i = 0; i < S; ++i) packed[i][q] = 0u;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          double y = scalbn(s_v[17 * c + 4 * q + b], -e);  // |y| < 1, exact
-#pragma unroll
-          for (int i = 0; i < S; ++i) {
-            y = y * 128.0;               // exact
-            const double t = trunc(y);  // |t| <= 127
-            y -= t;                      // exact
-            packed[i][q] |= (static_cast<uint32_t>(static_cast<int>(t)) & 0xffu) << (8 * b);
+    m = block_max_abs(m, s_max);
+    cut_row_planes<S>(s_v, m, r, kp, rows_pad, plane_stride, planes, exps);
+    __syncthreads();  // s_v / s_max reused by the next row
+  }
+}
+
+// Digit planes of sparse rows: row r is the dense coefficient vector of the
+// sparse model of block r, v[sel[r, t]] += coef[r, t] over its `iters` terms
+// (terms with sel < 0 -- a run stopped by degeneracy -- or sel >= kd add
+// nothing). Synthesis of the lost samples of a shared geometry is then one
+// Ozaki product g = V Phi_lost^T (fase_ozaki_gemm).
+// Scatter: the (sel, coef) lists are staged in shared memory by the whole
+// CTA; warp 0 adds them in windows of 32 terms, in term order. A window whose
+// atoms are all distinct adds lane-parallel (distinct addresses); repeated
+// atoms inside a window (__match_any_sync) are first summed in term order by
+// the group's lowest lane. Deterministic: the same sums in the same order on
+// every run.
+constexpr int OZ_SPARSE_WINDOW = 1024;  // terms staged per pass
+
+template <int S>
+__global__ void __launch_bounds__(OZ_SPLIT_THREADS) ozaki_split_sparse_kernel(
+    const int32_t* __restrict__ sel, int64_t ldsel, const double* __restrict__ coef,
+    int64_t ldcoef, int rows, int iters, int kd, int8_t* __restrict__ planes, int64_t kp,
+    int64_t rows_pad, int64_t plane_stride, int32_t* __restrict__ exps) {
+  extern __shared__ double s_v[];  // kp + kp/16
+  __shared__ double s_max[OZ_SPLIT_THREADS / 32];
+  __shared__ double s_c[OZ_SPARSE_WINDOW];
+  __shared__ int s_u[OZ_SPARSE_WINDOW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    for (int k = tid; k < kp; k += OZ_SPLIT_THREADS) s_v[k + (k >> 4)] = 0.0;
+    const int32_t* sr = sel + static_cast<int64_t>(r) * ldsel;
+    const double* cr = coef + static_cast<int64_t>(r) * ldcoef;
+    for (int w0 = 0; w0 < iters; w0 += OZ_SPARSE_WINDOW) {
+      const int n = min(OZ_SPARSE_WINDOW, iters - w0);
+      for (int i = tid; i < n; i += OZ_SPLIT_THREADS) {
+        const int u = __ldg(sr + w0 + i);
+        s_u[i] = (u >= 0 && u < kd) ? u : -1;
+        s_c[i] = __ldg(cr + w0 + i);
+      }
+      __syncthreads();  // staged lists (and, on the first pass, the zeroed row)
+      if (warp == 0) {
+        for (int b = 0; b < n; b += 32) {
+          const int i = b + lane;
+          const int u = i < n ? s_u[i] : -1;
+          const double c = i < n ? s_c[i] : 0.0;
+          const unsigned peers = __match_any_sync(0xffffffffu, u);
+          double acc = c;
+          if (__any_sync(0xffffffffu, u >= 0 && peers != (1u << lane))) {
+            // repeated atoms in this window: each group's lowest lane sums the
+            // group's coefficients in term (lane) order
+            acc = 0.0;
+            for (int l = 0; l < 32; ++l) {
+              const double cl = __shfl_sync(0xffffffffu, c, l);
+              if ((peers >> l) & 1u) acc += cl;
+            }
           }
+          if (u >= 0 && lane == __ffs(peers) - 1) s_v[u + (u >> 4)] += acc;
+          __syncwarp();
         }
       }
-      const int64_t off = plane_offset(r, 16 * static_cast<int64_t>(c), rows_pad);
-#pragma unroll
-      for (int i = 0; i < S; ++i)
-        *reinterpret_cast<uint4*>(planes + i * plane_stride + off) =
-            make_uint4(packed[i][0], packed[i][1], packed[i][2], packed[i][3]);
+      __syncthreads();  // s_u / s_c reused by the next window; s_v complete
     }
+    double m = 0.0;
+    for (int k = tid; k < kp; k += OZ_SPLIT_THREADS) m = fmax(m, fabs(s_v[k + (k >> 4)]));
+    m = block_max_abs(m, s_max);
+    cut_row_planes<S>(s_v, m, r, kp, rows_pad, plane_stride, planes, exps);
     __syncthreads();  // s_v / s_max reused by the next row
   }
 }
@@ -324,6 +414,44 @@ extern "C" int fase_ozaki_split(const double* x, int64_t ldx, const int32_t* idx
     return FASE_ERR_CUDA;
   }
   return check_launch("fase_ozaki_split");
+}
+
+extern "C" int fase_ozaki_split_sparse(const int32_t* sel, int64_t ldsel, const double* coef,
+                                       int64_t ldcoef, int rows, int iters, int kd, int slices,
+                                       int8_t* planes, int64_t kp, int rows_pad, int32_t* exps,
+                                       void* stream) {
+  if (rows < 0 || iters < 0 || kd < 1 || slices < 6 || slices > OZ_MAX_SLICES || kp < kd ||
+      kp % OZ_BK || kp > 16384 || ldsel < iters || ldcoef < iters || rows_pad < rows ||
+      rows_pad % 8) {
+    set_error("fase_ozaki_split_sparse: bad sizes (rows=%d iters=%d kd=%d slices=%d kp=%lld)",
+              rows, iters, kd, slices, static_cast<long long>(kp));
+    return FASE_ERR_SHAPE;
+  }
+  if (rows == 0) return FASE_OK;
+  if ((iters > 0 && (!sel || !coef)) || !planes || !exps || !aligned16(planes)) {
+    set_error("fase_ozaki_split_sparse: null or misaligned pointer");
+    return FASE_ERR_SHAPE;
+  }
+  const dim3 grid(rows < 148 * 8 ? rows : 148 * 8);
+  const int64_t stride = static_cast<int64_t>(rows_pad) * kp;
+  const size_t smem = sizeof(double) * static_cast<size_t>(kp + kp / 16);
+  auto run = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<grid, OZ_SPLIT_THREADS, smem, as_stream(stream)>>>(sel, ldsel, coef, ldcoef, rows,
+                                                               iters, kd, planes, kp, rows_pad,
+                                                               stride, exps);
+    return cudaSuccess;
+  };
+  cudaError_t e = slices == 8 ? run(ozaki_split_sparse_kernel<8>)
+                              : (slices == 7 ? run(ozaki_split_sparse_kernel<7>)
+                                             : run(ozaki_split_sparse_kernel<6>));
+  if (e != cudaSuccess) {
+    set_error("fase_ozaki_split_sparse: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return FASE_ERR_CUDA;
+  }
+  return check_launch("fase_ozaki_split_sparse");
 }
 
 static int ozaki_gemm_impl(const int8_t* a_planes, int a_rows_pad, const int32_t* ea, int m_rows,

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import functools
 import hashlib
+import os
 import struct
 from dataclasses import dataclass
 
@@ -745,8 +746,9 @@ def fase_extrapolate_batch(signals, masks, dictionary: Dictionary, tables=None,
             # large dense batches: support samples only, on the tcgen05 Ozaki path
             sidx, w_s = gram_support(W, M)
             n_s = int(sidx.numel())
-            a = _native.OzakiOperand(B, n_s, 128, dev).split(F, sidx, w_s)
-            b = _native.OzakiOperand(rows, n_s, 64, dev).split(phi, sidx)
+            ns = _native.PRODUCT_SLICES
+            a = _native.OzakiOperand(B, n_s, 128, dev, ns).split(F, sidx, w_s)
+            b = _native.OzakiOperand(rows, n_s, 64, dev, ns).split(phi, sidx)
             _native.ozaki_gemm(a, b, _real_view(R0) if cplx else R0)
         else:
             ws = torch.empty(max(_native.init_products_workspace(M, B) // 8, 2),
@@ -922,11 +924,31 @@ class ExtrapolationPlan:
             # csrc/ozaki.cu) for batches that fill the GPU; Phi's planes once here
             if products == "ozaki" or (products == "auto" and ozaki_worthwhile(self.B, phi_s.shape[0])):
                 rows = phi_s.shape[0]
-                self._ozaki = (_native.OzakiOperand(self.B, n_s, 128, dev),
-                               _native.OzakiOperand(rows, n_s, 64, dev).split(phi_s))
+                ns = _native.PRODUCT_SLICES
+                self._ozaki = (_native.OzakiOperand(self.B, n_s, 128, dev, ns),
+                               _native.OzakiOperand(rows, n_s, 64, dev, ns).split(phi_s))
                 n_prod = 2
-        # (weigh +) products + iterate + synth
-        self.launches_per_run = n_prod + 1 + (1 if self.n_lost and not self.fused_synth else 0)
+        # Synthesis of the lost samples as one Ozaki product, g = V Phi_lost^T,
+        # V the batch's sparse models scattered to dense coefficient rows
+        # (fase_ozaki_split_sparse), when the B x L output fills the GPU with
+        # one 128 x 64 tile per SM (config 4: 4,096 x 576): the per-block
+        # gathers of phi rows stream 9.5 GB from L2 per batch, the product reads
+        # Phi_lost's planes once per tile. Real dictionaries; FASE_SYNTH=paste
+        # keeps the per-block kernel (measurement knob).
+        self._synth_oz = None
+        synth_mode = os.environ.get("FASE_SYNTH", "auto")
+        if (not cplx and self.n_lost and not self.fused_synth and K <= 16384
+                and synth_mode != "paste"
+                and (synth_mode == "ozaki" or ozaki_worthwhile(self.B, self.n_lost))):
+            ns = _native.PRODUCT_SLICES
+            phi_t = self.phi_lost[:K, : self.n_lost].t().contiguous()
+            self._synth_oz = (_native.OzakiOperand(self.B, K, 128, dev, ns),
+                              _native.OzakiOperand(self.n_lost, K, 64, dev, ns).split(phi_t))
+            torch.cuda.current_stream(dev).synchronize()  # phi_t freed after its split
+            del phi_t
+        # (weigh +) products + iterate + synth (split + product on the Ozaki path)
+        n_synth = (2 if self._synth_oz is not None else 1) if self.n_lost and not self.fused_synth else 0
+        self.launches_per_run = n_prod + 1 + n_synth
 
     def _scratch(self, slot: int = 0) -> dict:
         """Per-slot work buffers (R0, products scratch, max |Im g|): slot 0 is the
@@ -936,6 +958,7 @@ class ExtrapolationPlan:
             return {"R0": self.R0, "ws": self.ws,
                     "X": self._support[3] if self._support is not None else None,
                     "oz": self._ozaki[0] if self._ozaki is not None else None,
+                    "soz": self._synth_oz[0] if self._synth_oz is not None else None,
                     "max_imag": self.max_imag}
         if not hasattr(self, "_slot1"):
             oz = None
@@ -946,6 +969,9 @@ class ExtrapolationPlan:
                 "R0": torch.empty_like(self.R0), "ws": torch.empty_like(self.ws),
                 "X": torch.empty_like(self._support[3]) if self._support is not None else None,
                 "oz": oz,
+                "soz": (_native.OzakiOperand(self.B, self.K, 128, self.device,
+                                             self._synth_oz[0].slices)
+                        if self._synth_oz is not None else None),
                 "max_imag": torch.zeros_like(self.max_imag) if self.max_imag is not None else None}
         return self._slot1
 
@@ -1028,9 +1054,20 @@ class ExtrapolationPlan:
         else:
             _native.iterate(self.G, self.D, sc["R0"], self.K, self.I, self.config.gamma, sel,
                             proj, coef, l2_hot=hot)
-        if self.n_lost:
-            _native.synth_paste(self.phi_lost, sel, coef, self.I, self.lost_seq, lost,
-                                n_shared=self.n_lost, dst=self.lost_pos)
+        self._synth(sel, coef, lost, slot)
+
+    def _synth(self, sel, coef, lost, slot: int = 0):
+        """Lost samples of real models (separate from the recursion): the Ozaki
+        product when the plan set it up, else fase_synth_paste (bit-exact
+        sequential order)."""
+        if not self.n_lost:
+            return
+        if self._synth_oz is not None:
+            a = self._scratch(slot)["soz"].split_sparse(sel, coef, self.I)
+            _native.ozaki_gemm(a, self._synth_oz[1], lost)
+            return
+        _native.synth_paste(self.phi_lost, sel, coef, self.I, self.lost_seq, lost,
+                            n_shared=self.n_lost, dst=self.lost_pos)
 
     def run(self, signals=None):
         """Enqueue one batch. ``signals``: None (use ``self.F`` as filled by the
