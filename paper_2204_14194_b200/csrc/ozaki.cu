@@ -29,6 +29,7 @@
 // mbarrier. TMEM holds s accumulators of 64 columns; all eight
 // warps run the epilogue.
 
+#include <climits>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -74,8 +75,8 @@ constexpr int OZ_SPLIT_THREADS = 256;
 // row r: e = smallest integer with max|v| < 2^e (m = max|v| over the row, block-
 // uniform), then each thread cuts 16 consecutive k into S truncated base-2^7
 // digits of v * 2^-e (each step exact) and stores one 16-byte chunk per plane.
-template <int S>
-__device__ __forceinline__ void cut_row_planes(const double* s_v, double m, int r, int64_t kp,
+template <int S, class Get>
+__device__ __forceinline__ void cut_row_planes(Get get, double m, int r, int64_t kp,
                                                int64_t rows_pad, int64_t plane_stride,
                                                int8_t* __restrict__ planes,
                                                int32_t* __restrict__ exps) {
@@ -91,7 +92,7 @@ __device__ __forceinline__ void cut_row_planes(const double* s_v, double m, int 
       for (int i = 0; i < S; ++i) packed[i][q] = 0u;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        double y = s_v[17 * c + 4 * q + b];
+        double y = get(c, 4 * q + b);
         if (y == 0.0) continue;  // all digits 0 (most entries of sparse model rows)
         y = scalbn(y, -e);       // |y| < 1, exact
 #pragma unroll
@@ -138,17 +139,33 @@ __global__ void __launch_bounds__(OZ_SPLIT_THREADS) ozaki_split_kernel(
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     const double* xr = x + static_cast<int64_t>(r) * ldx;
     double m = 0.0;
-    for (int k = tid; k < kp; k += OZ_SPLIT_THREADS) {
-      double v = 0.0;
-      if (k < kd) {
-        v = __ldg(xr + (idx ? __ldg(idx + k) : k));
-        if (w) v = mul_rn(v, __ldg(w + k));
+    // eight independent gathers in flight per thread (the index loads, then
+    // the values: one dependent global round trip per eight elements)
+    constexpr int U = 8;
+    for (int k0 = tid; k0 < kp; k0 += U * OZ_SPLIT_THREADS) {
+      int col[U];
+      double v[U], wk[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int k = k0 + j * OZ_SPLIT_THREADS;
+        col[j] = k < kd ? (idx ? __ldg(idx + k) : k) : -1;
+        wk[j] = (w && k < kd) ? __ldg(w + k) : 1.0;
       }
-      s_v[k + (k >> 4)] = v;
-      m = fmax(m, fabs(v));
+#pragma unroll
+      for (int j = 0; j < U; ++j) v[j] = col[j] >= 0 ? __ldg(xr + col[j]) : 0.0;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int k = k0 + j * OZ_SPLIT_THREADS;
+        if (w) v[j] = mul_rn(v[j], wk[j]);
+        if (k < kp) {
+          s_v[k + (k >> 4)] = v[j];
+          m = fmax(m, fabs(v[j]));
+        }
+      }
     }
     m = block_max_abs(m, s_max);
-    cut_row_planes<S>(s_v, m, r, kp, rows_pad, plane_stride, planes, exps);
+    cut_row_planes<S>([&](int c, int j) { return s_v[17 * c + j]; }, m, r, kp, rows_pad,
+                      plane_stride, planes, exps);
     __syncthreads();  // s_v / s_max reused by the next row
   }
 }
@@ -158,63 +175,73 @@ __global__ void __launch_bounds__(OZ_SPLIT_THREADS) ozaki_split_kernel(
 // (terms with sel < 0 -- a run stopped by degeneracy -- or sel >= kd add
 // nothing). Synthesis of the lost samples of a shared geometry is then one
 // Ozaki product g = V Phi_lost^T (fase_ozaki_gemm).
-// Scatter: the (sel, coef) lists are staged in shared memory by the whole
-// CTA; warp 0 adds them in windows of 32 terms, in term order. A window whose
-// atoms are all distinct adds lane-parallel (distinct addresses); repeated
-// atoms inside a window (__match_any_sync) are first summed in term order by
-// the group's lowest lane. Deterministic: the same sums in the same order on
-// every run.
-constexpr int OZ_SPARSE_WINDOW = 1024;  // terms staged per pass
-
+// Shared memory holds a slot map (kp int32: the term that first names atom k,
+// or -1) and the terms, not the dense row, so several CTAs share an SM. Every
+// term claims its atom (atomicMin of the term index); when no atom is named
+// twice each slot's value is its term's coefficient; repeated terms are
+// flagged in a bit mask, and one thread walks the set bits in term order,
+// adding each into its atom's first occurrence -- the same sums in the same
+// order as a sequential scatter, on every run. The cut reads v[k] through the
+// map.
 template <int S>
 __global__ void __launch_bounds__(OZ_SPLIT_THREADS) ozaki_split_sparse_kernel(
     const int32_t* __restrict__ sel, int64_t ldsel, const double* __restrict__ coef,
     int64_t ldcoef, int rows, int iters, int kd, int8_t* __restrict__ planes, int64_t kp,
     int64_t rows_pad, int64_t plane_stride, int32_t* __restrict__ exps) {
-  extern __shared__ double s_v[];  // kp + kp/16
+  extern __shared__ double s_dyn[];
+  double* s_val = s_dyn;                                   // iters values
+  int* s_u = reinterpret_cast<int*>(s_val + iters);        // iters atoms
+  int* s_slot = reinterpret_cast<int*>(                    // kp slots, 16-byte aligned
+      (reinterpret_cast<uintptr_t>(s_u + iters) + 15) & ~static_cast<uintptr_t>(15));
+  unsigned* s_rep = reinterpret_cast<unsigned*>(s_slot + kp);  // (iters + 31) / 32 words
   __shared__ double s_max[OZ_SPLIT_THREADS / 32];
-  __shared__ double s_c[OZ_SPARSE_WINDOW];
-  __shared__ int s_u[OZ_SPARSE_WINDOW];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ int s_dup;
+  const int tid = threadIdx.x;
+  const int rep_words = (iters + 31) >> 5;
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
-    for (int k = tid; k < kp; k += OZ_SPLIT_THREADS) s_v[k + (k >> 4)] = 0.0;
+    for (int k = 4 * tid; k < kp; k += 4 * OZ_SPLIT_THREADS)
+      *reinterpret_cast<int4*>(s_slot + k) = make_int4(INT_MAX, INT_MAX, INT_MAX, INT_MAX);
+    for (int i = tid; i < rep_words; i += OZ_SPLIT_THREADS) s_rep[i] = 0u;
+    if (tid == 0) s_dup = 0;
     const int32_t* sr = sel + static_cast<int64_t>(r) * ldsel;
     const double* cr = coef + static_cast<int64_t>(r) * ldcoef;
-    for (int w0 = 0; w0 < iters; w0 += OZ_SPARSE_WINDOW) {
-      const int n = min(OZ_SPARSE_WINDOW, iters - w0);
-      for (int i = tid; i < n; i += OZ_SPLIT_THREADS) {
-        const int u = __ldg(sr + w0 + i);
-        s_u[i] = (u >= 0 && u < kd) ? u : -1;
-        s_c[i] = __ldg(cr + w0 + i);
+    for (int t = tid; t < iters; t += OZ_SPLIT_THREADS) {
+      const int u = __ldg(sr + t);
+      s_u[t] = (u >= 0 && u < kd) ? u : -1;
+      s_val[t] = __ldg(cr + t);
+    }
+    __syncthreads();
+    for (int t = tid; t < iters; t += OZ_SPLIT_THREADS)
+      if (s_u[t] >= 0) atomicMin(s_slot + s_u[t], t);
+    __syncthreads();
+    for (int t = tid; t < iters; t += OZ_SPLIT_THREADS)
+      if (s_u[t] >= 0 && s_slot[s_u[t]] != t) {
+        atomicOr(s_rep + (t >> 5), 1u << (t & 31));
+        s_dup = 1;
       }
-      __syncthreads();  // staged lists (and, on the first pass, the zeroed row)
-      if (warp == 0) {
-        for (int b = 0; b < n; b += 32) {
-          const int i = b + lane;
-          const int u = i < n ? s_u[i] : -1;
-          const double c = i < n ? s_c[i] : 0.0;
-          const unsigned peers = __match_any_sync(0xffffffffu, u);
-          double acc = c;
-          if (__any_sync(0xffffffffu, u >= 0 && peers != (1u << lane))) {
-            // repeated atoms in this window: each group's lowest lane sums the
-            // group's coefficients in term (lane) order
-            acc = 0.0;
-            for (int l = 0; l < 32; ++l) {
-              const double cl = __shfl_sync(0xffffffffu, c, l);
-              if ((peers >> l) & 1u) acc += cl;
-            }
+    __syncthreads();
+    if (s_dup) {  // repeated atoms: each added, in term order, into the first occurrence
+      if (tid == 0)
+        for (int i = 0; i < rep_words; ++i)
+          for (unsigned bits = s_rep[i]; bits; bits &= bits - 1u) {
+            const int t = 32 * i + __ffs(bits) - 1;
+            const int o = s_slot[s_u[t]];
+            s_val[o] = s_val[o] + s_val[t];
+            s_u[t] = -1;  // folded into its first occurrence
           }
-          if (u >= 0 && lane == __ffs(peers) - 1) s_v[u + (u >> 4)] += acc;
-          __syncwarp();
-        }
-      }
-      __syncthreads();  // s_u / s_c reused by the next window; s_v complete
+      __syncthreads();
     }
     double m = 0.0;
-    for (int k = tid; k < kp; k += OZ_SPLIT_THREADS) m = fmax(m, fabs(s_v[k + (k >> 4)]));
+    for (int t = tid; t < iters; t += OZ_SPLIT_THREADS)
+      if (s_u[t] >= 0) m = fmax(m, fabs(s_val[t]));
     m = block_max_abs(m, s_max);
-    cut_row_planes<S>(s_v, m, r, kp, rows_pad, plane_stride, planes, exps);
-    __syncthreads();  // s_v / s_max reused by the next row
+    cut_row_planes<S>(
+        [&](int c, int j) {
+          const int o = s_slot[16 * c + j];
+          return o == INT_MAX ? 0.0 : s_val[o];
+        },
+        m, r, kp, rows_pad, plane_stride, planes, exps);
+    __syncthreads();  // shared arrays reused by the next row
   }
 }
 
@@ -434,7 +461,13 @@ extern "C" int fase_ozaki_split_sparse(const int32_t* sel, int64_t ldsel, const 
   }
   const dim3 grid(rows < 148 * 8 ? rows : 148 * 8);
   const int64_t stride = static_cast<int64_t>(rows_pad) * kp;
-  const size_t smem = sizeof(double) * static_cast<size_t>(kp + kp / 16);
+  const size_t smem = static_cast<size_t>(iters) * 12 + 16 + 4 * static_cast<size_t>(kp) +
+                      4 * static_cast<size_t>((iters + 31) / 32);
+  if (smem > 200 * 1024) {
+    set_error("fase_ozaki_split_sparse: %d terms x %lld atoms exceed shared memory", iters,
+              static_cast<long long>(kp));
+    return FASE_ERR_SHAPE;
+  }
   auto run = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
