@@ -228,9 +228,9 @@ __device__ __forceinline__ void fence_mbar_init() {
 // already ordered (FASE_ISSUE_FENCE=0 drops it)
 // Scaled recursion variants (bits; see iterate.cu): 1 signed running max,
 // 2 D prefetch, 4 fused update (iterate.cu and iterate_cluster.cu), 8 tie-dump
-// shortcut, 16 issue-warp offset
+// shortcut, 16 issue-warp offset, 32 integer running max (24-32 elements per thread)
 #ifndef FASE_SCALED_LEAN
-#define FASE_SCALED_LEAN 13
+#define FASE_SCALED_LEAN 45
 #endif
 #ifndef FASE_ISSUE_FENCE
 #define FASE_ISSUE_FENCE 1

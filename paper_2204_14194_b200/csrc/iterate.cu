@@ -55,6 +55,9 @@ constexpr unsigned kNone = 0xffffffffu;
 #ifndef FASE_SCALED_SEG
 #define FASE_SCALED_SEG 3
 #endif
+#ifndef FASE_INTMAX_MIN_EPT
+#define FASE_INTMAX_MIN_EPT 24
+#endif
 #ifndef FASE_SCALED_CHAINS
 #define FASE_SCALED_CHAINS 1
 #endif
@@ -106,6 +109,9 @@ constexpr unsigned kNone = 0xffffffffu;
 //  2: D of the predicted atom is loaded by every thread right after the block
 //     max, so the tie winner no longer reads D from global memory between the
 //     two barriers (measured: no gain on config 4, config 1 0.4% slower: off)
+// 32: integer running max (kIntMax in the kernel: keys of the high words, the
+//     exact top and tie rule resolved by one warp while the row copy is in
+//     flight), on shapes of at least FASE_INTMAX_MIN_EPT elements per thread
 // (FASE_SCALED_LEAN is defined in common.cuh: the cluster recursion follows bit 4 too)
 #ifdef FASE_ITERATE_STATS
 __device__ unsigned long long g_stats[8];  // measurement build: chunked-path counters
@@ -185,6 +191,24 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   __shared__ double s_r_all[NB][NW];
   __shared__ double s_d_all[NB][NW];
   __shared__ __align__(16) double s_dump_all[NB][NW][kDsmem ? 1 : 2][EPT];  // tie-pass winner's registers
+  // kIntMax (scaled, FASE_SCALED_LEAN & 32): the update keeps, per thread, only
+  // the largest key (high word of |R'| with its five low bits replaced by the
+  // element's position): one logic op per element and one 3-input integer max
+  // per pair instead of a compare and three selects per element. The largest
+  // key of the block names the row to stage; the exact top and the tie rule
+  // are then resolved, while that copy is in flight, by the warp holding every
+  // element within one key unit (2^-15 relative) of the largest: each such
+  // lane's registers are spread over the warp's lanes through shared memory.
+  // Any other situation (two such warps, a wide tie quantum, zero / subnormal /
+  // non-finite maxima) takes an exact per-thread scan and one more barrier.
+  // Dead atoms and the padding hold R' = 0 here (their table columns are 0).
+  // Shapes of 24 to 32 elements per thread (K > 5120): config 4 recursion 11.85 ->
+  // 11.35 ms on one box, every selection unchanged; the 64-register 18-element
+  // shape of config 1 measured 3.5% slower (0.698 -> 0.722 ms: its resolution
+  // spills) and keeps the compare / select running max.
+  constexpr bool kIntMax = kScaled && (FASE_SCALED_LEAN & 32) && EPT >= FASE_INTMAX_MIN_EPT && EPT <= 32 && SPEC == 0;
+  __shared__ unsigned s_wk[kIntMax ? NW : 1];  // kIntMax: the warps' largest keys
+  __shared__ double s_ftop;                    // kIntMax: the exact top of a resolved iteration
   // The staged row arrives in kSeg segments, each on its own mbarrier, so the
   // update can start on the first segment while the rest is still in flight.
   constexpr int kSegMax = kScaled ? FASE_SCALED_SEG : 3;
@@ -317,8 +341,8 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       // R' = R * D; dead atoms and the padding hold NaN (never selected)
       const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
       const double d0 = k < K ? D[k] : 0.0, d1 = k + 1 < K ? D[k + 1] : 0.0;
-      r[j][0] = d0 != 0.0 ? mul_rn(R0[k], d0) : kNaN;
-      r[j][1] = d1 != 0.0 ? mul_rn(R0[k + 1], d1) : kNaN;
+      r[j][0] = d0 != 0.0 ? mul_rn(R0[k], d0) : (kIntMax ? 0.0 : kNaN);
+      r[j][1] = d1 != 0.0 ? mul_rn(R0[k + 1], d1) : (kIntMax ? 0.0 : kNaN);
       const double m0 = fabs(r[j][0]);
       if (m0 > best) {
         best = m0;
@@ -394,8 +418,63 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
 #pragma unroll
   for (int rr = 0; rr < kSp; ++rr) runner[rr] = kNone;
 
+  // kIntMax: a live atom (dead ones and the padding hold R' = 0 there)
+  auto live = [&](int k) { return k < K && __ldg(D + k) != 0.0; };
+  // kIntMax: this thread's largest key; key = (high word & mask) | position, one LOP3
+  constexpr unsigned kKeyMask = 0x7fffffe0u;
+  auto key_of = [&](double x, unsigned pos) -> unsigned {
+    unsigned d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(d) : "r"(__double2hiint(x)), "r"(pos), "r"(kKeyMask));
+    return d;
+  };
+  unsigned tkey = 0u;
+  if constexpr (kIntMax) {
+#pragma unroll
+    for (int j = 0; j < EP; ++j)
+      tkey = __vimax3_u32(tkey, key_of(r[j][0], 31u - 2 * j), key_of(r[j][1], 30u - 2 * j));
+  }
+  // kIntMax, exact path: this thread's exact max, its signed value and lowest index
+  auto rescan = [&]() {
+    double cb = -0.0;
+    unsigned ca = kNone;
+#pragma unroll
+    for (int j = 0; j < EP; ++j) {
+      if (fabs(r[j][0]) > fabs(cb)) {
+        cb = r[j][0];
+        ca = static_cast<unsigned>(2 * (j * NT + t));
+      }
+      if (fabs(r[j][1]) > fabs(cb)) {
+        cb = r[j][1];
+        ca = static_cast<unsigned>(2 * (j * NT + t) + 1);
+      }
+    }
+    best = ca == kNone ? kDead : fabs(cb);
+    bsig = cb;
+    barg = ca;
+    if (ca == kNone) {  // rare: no metric > 0 here -- the lowest live atom (metric 0), if any
+#pragma unroll
+      for (int j = EP - 1; j >= 0; --j) {
+        const int k = 2 * (j * NT + t);
+        if (live(k + 1)) {
+          best = 0.0;
+          bsig = r[j][1];
+          barg = static_cast<unsigned>(k + 1);
+        }
+        if (live(k)) {
+          best = 0.0;
+          bsig = r[j][0];
+          barg = static_cast<unsigned>(k);
+        }
+      }
+    }
+  };
+
   for (int it = 0; it < a.I; ++it) {
+    long long top_key = 0;
+    unsigned guess = kNone;
+    long long wkey = LLONG_MIN;
     // ---- exact warp max and the lowest index attaining it
+    auto publish_exact = [&]() {
     {
       const long long key = __double_as_longlong(best);
       const int kh = static_cast<int>(key >> 32);
@@ -408,11 +487,9 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         s_arg[warp] = wa;
       }
     }
-    block_sync();
+    };
     // ---- block max: every warp reduces the NW slots in parallel (lane l reads slot l)
-    long long top_key;
-    unsigned guess;
-    long long wkey;
+    auto block_exact = [&](unsigned& guess_out) {
     {
       const long long sk = lane < NW ? s_key[lane] : LLONG_MIN;
       const unsigned sa = lane < NW ? s_arg[lane] : kNone;
@@ -421,14 +498,14 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       const unsigned l = static_cast<unsigned>(sk);
       const int bh = __reduce_max_sync(0xffffffffu, h);
       const unsigned bl = __reduce_max_sync(0xffffffffu, h == bh ? l : 0u);
-      guess = __reduce_min_sync(0xffffffffu, (h == bh && l == bl) ? sa : kNone);
+      guess_out = __reduce_min_sync(0xffffffffu, (h == bh && l == bl) ? sa : kNone);
       top_key = (static_cast<long long>(bh) << 32) | bl;
       if constexpr (SPEC > 0) {
         // the best maxima of the other warps (warp 0; thread 0 stages their rows)
         if (warp == 0) {
 #pragma unroll
           for (int rr = 0; rr < SPEC; ++rr) {
-            bool taken = sa == guess;
+            bool taken = sa == guess_out;
 #pragma unroll
             for (int q2 = 0; q2 < rr; ++q2) taken = taken || sa == runner[q2];
             const long long k2 = taken ? LLONG_MIN : sk;
@@ -448,10 +525,10 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         // of the best two other warps' maxima into L2 now, a whole iteration
         // ahead (bulk prefetches: no registers or shared memory held).
         if (warp == 0) {
-          unsigned prev = guess;
+          unsigned prev = guess_out;
 #pragma unroll
           for (int rr = 0; rr < FASE_RUNNER_PREFETCH; ++rr) {
-            const long long k2 = (sa == guess || sa == prev) ? LLONG_MIN : sk;
+            const long long k2 = (sa == guess_out || sa == prev) ? LLONG_MIN : sk;
             const int h2 = static_cast<int>(k2 >> 32);
             const unsigned l2 = static_cast<unsigned>(k2);
             const int b2 = __reduce_max_sync(0xffffffffu, h2);
@@ -467,6 +544,30 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
           }
         }
       }
+    }
+    };
+    bool fastb = false;  // kIntMax: one warp resolves this iteration (block-uniform)
+    unsigned sk_l = 0u;  // kIntMax: warp `lane`'s largest key
+    unsigned kb = 0u;    // kIntMax: the block's largest key
+    if constexpr (kIntMax) {
+      const unsigned wk = __reduce_max_sync(0xffffffffu, tkey);
+      const int wl = __ffs(__ballot_sync(0xffffffffu, tkey == wk)) - 1;
+      if (lane == 0) {
+        const int e = 31 - static_cast<int>(wk & 31u);
+        s_wk[warp] = wk;
+        s_arg[warp] = 2u * static_cast<unsigned>((e >> 1) * NT + warp * 32 + wl) + (e & 1);
+      }
+      block_sync();
+      sk_l = lane < NW ? s_wk[lane] : 0u;
+      const unsigned sa = lane < NW ? s_arg[lane] : kNone;
+      kb = __reduce_max_sync(0xffffffffu, sk_l);
+      guess = __reduce_min_sync(0xffffffffu, sk_l == kb ? sa : kNone);
+      guess = guess < static_cast<unsigned>(K) ? guess : 0u;  // (an all-zero block: any row)
+      top_key = 1;  // (known after the resolution below)
+    } else {
+      publish_exact();
+      block_sync();
+      block_exact(guess);
     }
     if (top_key < 0) {  // every atom degenerate (NoSelectableAtomError): mark and stop
       for (int k = it + t; k < a.I; k += NT) {
@@ -614,6 +715,118 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       }
     }
     constexpr bool kLeanD = kScaled && (FASE_SCALED_LEAN & 2);
+    if constexpr (kIntMax) {
+      const unsigned kb27 = kb >> 5;
+      const unsigned nearw = __ballot_sync(0xffffffffu, lane < NW && (sk_l >> 5) + 1u >= kb27);
+      const int wstar = __ffs(nearw) - 1;
+      // every element that can reach the tie threshold lies within one key
+      // unit (2^(e-15) for a top in [2^e, 2^(e+1))) of the largest when the
+      // quantum max(q, 1e-13 * top) is below that unit: compared through the
+      // exponent fields
+      fastb = __popc(nearw) == 1 && kb >= 0x02000000u && kb < 0x7ff00000u &&
+              __double2hiint(q) < static_cast<int>(((kb >> 20) - 15u) << 20);
+      if (fastb) {
+        if (warp == wstar) {
+          // the lanes holding an element within one key unit of the largest
+          const unsigned nearl = __ballot_sync(0xffffffffu, (tkey >> 5) + 1u >= kb27);
+          unsigned cu = kNone;
+          double rv = 0.0, topx = 0.0;
+          if ((nearl & (nearl - 1u)) == 0u) {  // one lane: its registers over the lanes
+            const int c = __ffs(nearl) - 1;
+            if (lane == c) {
+#pragma unroll
+              for (int j = 0; j < EP; ++j)
+                *reinterpret_cast<double2*>(&s_dump[warp][0][2 * j]) = make_double2(r[j][0], r[j][1]);
+            }
+            __syncwarp();
+            const double v = lane < EPT ? s_dump[warp][0][lane] : 0.0;
+            const unsigned hv = (static_cast<unsigned>(__double2hiint(v)) & 0x7fffffffu) >> 5;
+            const unsigned nb = __ballot_sync(0xffffffffu, hv + 1u >= kb27);
+            if ((nb & (nb - 1u)) == 0u) {  // one element: the top and the pick
+              const int e = __ffs(nb) - 1;
+              rv = __shfl_sync(0xffffffffu, v, e);
+              topx = fabs(rv);
+              cu = 2u * static_cast<unsigned>((e >> 1) * NT + warp * 32 + c) + (e & 1);
+            }
+          }
+          if (cu == kNone) {  // several elements: exact top, then the lowest index at the threshold
+            long long tk = 0;
+            for (unsigned m = nearl; m; m &= m - 1u) {
+              const int c = __ffs(m) - 1;
+              __syncwarp();
+              if (lane == c) {
+#pragma unroll
+                for (int j = 0; j < EP; ++j)
+                  *reinterpret_cast<double2*>(&s_dump[warp][0][2 * j]) = make_double2(r[j][0], r[j][1]);
+              }
+              __syncwarp();
+              const double v = lane < EPT ? s_dump[warp][0][lane] : 0.0;
+              const long long key = __double_as_longlong(fabs(v));
+              const int kh = static_cast<int>(key >> 32);
+              const unsigned kl = static_cast<unsigned>(key);
+              const int wh = __reduce_max_sync(0xffffffffu, kh);
+              const unsigned wl2 = __reduce_max_sync(0xffffffffu, kh == wh ? kl : 0u);
+              const long long k2 = (static_cast<long long>(wh) << 32) | wl2;
+              tk = k2 > tk ? k2 : tk;
+            }
+            topx = __longlong_as_double(tk);
+            const double thrx = sub_rn(topx, fmax(q, mul_rn(1e-13, topx)));  // as below (finite top)
+            for (unsigned m = nearl; m; m &= m - 1u) {
+              const int c = __ffs(m) - 1;
+              __syncwarp();
+              if (lane == c) {
+#pragma unroll
+                for (int j = 0; j < EP; ++j)
+                  *reinterpret_cast<double2*>(&s_dump[warp][0][2 * j]) = make_double2(r[j][0], r[j][1]);
+              }
+              __syncwarp();
+              const double v = lane < EPT ? s_dump[warp][0][lane] : 0.0;
+              const unsigned hit = __ballot_sync(0xffffffffu, fabs(v) >= thrx);
+              if (hit) {
+                const int e = __ffs(hit) - 1;
+                const unsigned ci = 2u * static_cast<unsigned>((e >> 1) * NT + warp * 32 + c) + (e & 1);
+                const double cv = __shfl_sync(0xffffffffu, v, e);
+                if (ci < cu) {
+                  cu = ci;
+                  rv = cv;
+                }
+              }
+            }
+          }
+          FASE_ASSERT(cu < static_cast<unsigned>(K));
+          if (lane == 0) {  // projection, coefficient and the iteration's outputs
+            const double pf = mul_rn(rv, __ldg(D + cu));
+            const double cf = mul_rn(a.gamma, pf);
+            s_u[0] = cu;
+            s_r[0] = pf;
+            s_d[0] = cf;
+            s_ftop = topx;
+            sel[it] = static_cast<int32_t>(cu);
+            proj[it] = pf;
+            coef[it] = cf;
+          }
+        }
+        block_sync();
+        top_key = __double_as_longlong(s_ftop);
+      } else {
+        rescan();
+        publish_exact();
+        block_sync();
+        unsigned exact_guess;
+        block_exact(exact_guess);
+        if (top_key < 0) {  // every atom degenerate: retire the copy, then mark and stop as above
+#pragma unroll
+          for (int sg = 0; sg < kSeg; ++sg) mbar_wait(&s_bar[sg], it & 1);
+          for (int k = it + t; k < a.I; k += NT) {
+            sel[k] = -1;
+            proj[k] = 0.0;
+            coef[k] = 0.0;
+          }
+          write_synth(b);
+          return;
+        }
+      }
+    }
     // kLeanD: D of the predicted atom, in flight during the tie pass and the
     // second barrier (the guess is in range here: a degenerate top returned)
     const double dguess = kLeanD ? __ldg(D + guess) : 0.0;
@@ -633,14 +846,18 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       thr = sub_rn(top, q);
     }
 
+    unsigned u = 0u;
+    int uw = 0;
+    if (!(kIntMax && fastb)) {
     // ---- lowest index reaching the threshold (only warps whose max reaches it)
     unsigned cand = kNone;
     if (wkey >= 0 && __longlong_as_double(wkey) >= thr) {  // warp-uniform
 #pragma unroll
       for (int j = EP - 1; j >= 0; --j) {
         const double2 m = metrics(j, dpair_if(j));
-        if (m.y >= thr) cand = 2 * (j * NT + t) + 1;
-        if (m.x >= thr) cand = 2 * (j * NT + t);
+        // (kIntMax: dead atoms hold 0, which reaches a threshold <= 0)
+        if (m.y >= thr && (!kIntMax || thr > 0.0 || live(2 * (j * NT + t) + 1))) cand = 2 * (j * NT + t) + 1;
+        if (m.x >= thr && (!kIntMax || thr > 0.0 || live(2 * (j * NT + t)))) cand = 2 * (j * NT + t);
       }
     }
     const unsigned wmin = __reduce_min_sync(0xffffffffu, cand);
@@ -676,14 +893,15 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       }
     }
     block_sync();
-    unsigned u;
-    int uw;
     {
       const unsigned su = lane < NW ? s_u[lane] : kNone;
       u = __reduce_min_sync(0xffffffffu, su);
       uw = __ffs(__ballot_sync(0xffffffffu, su == u)) - 1;
     }
     FASE_ASSERT(u < static_cast<unsigned>(K) && uw >= 0 && uw < NW);
+    } else {
+      u = s_u[0];  // resolved above (one barrier back)
+    }
     if constexpr (kChunked) {
       for (int ch = 0; ch < nch; ++ch) FASE_ASSERT(cids[ch] >= 0);
     }
@@ -699,9 +917,10 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     }
     const double ru = s_r[uw];
     const double du = kLeanD ? (u == guess ? dguess : __ldg(D + u)) : s_d[uw];
-    const double p = kScaled ? mul_rn(ru, du) : mul_rn(ru, mul_rn(du, du));
-    const double c = mul_rn(a.gamma, p);
-    if (t == 0) {
+    // (kIntMax, resolved above: the two slots hold the projection and the coefficient)
+    const double p = (kIntMax && fastb) ? ru : (kScaled ? mul_rn(ru, du) : mul_rn(ru, mul_rn(du, du)));
+    const double c = (kIntMax && fastb) ? du : mul_rn(a.gamma, p);
+    if (t == 0 && !(kIntMax && fastb)) {
       out_row(a.sel, sel)[it] = static_cast<int32_t>(u);
       out_row(a.proj, proj)[it] = p;
       out_row(a.coef, coef)[it] = c;
@@ -723,6 +942,7 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     auto update = [&](auto row_pair, auto staged, auto pre) {
       double cb[kChains];
       unsigned ca[kChains];
+      unsigned tk = 0u;  // kIntMax: the running largest key
 #pragma unroll
       for (int h = 0; h < kChains; ++h) {
         cb[h] = kLeanMax ? -0.0 : kDead;
@@ -744,6 +964,10 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
         } else {
           r[j][0] = sub_rn(r[j][0], mul_rn(c, g.x));
           r[j][1] = sub_rn(r[j][1], mul_rn(c, g.y));
+        }
+        if constexpr (kIntMax) {
+          tk = __vimax3_u32(tk, key_of(r[j][0], 31u - 2 * j), key_of(r[j][1], 30u - 2 * j));
+          continue;
         }
         const int h = j % kChains;
         if constexpr (kLeanMax) {
@@ -768,6 +992,10 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
           cb[h] = m1;
           ca[h] = static_cast<unsigned>(2 * (j * NT + t) + 1);
         }
+      }
+      if constexpr (kIntMax) {
+        tkey = tk;
+        return;
       }
       if constexpr (kLeanMax) {
         bsig = cb[0];

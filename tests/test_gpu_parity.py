@@ -481,6 +481,42 @@ def test_scaled_recursion_zero_metrics_and_dead_atoms(blocks):
             assert (sel != 0).all()
 
 
+@pytest.mark.parametrize("K", [6000, 8192])
+def test_scaled_recursion_integer_max_shapes(K):
+    """The 24- and 32-element shapes of the scaled recursion (K > 5,120) track
+    integer keys of the high words and resolve the exact top and the tie rule
+    in one warp (csrc/iterate.cu, kIntMax). Exact ties between duplicated atoms
+    held by one thread, by two lanes of a warp, by two warps and far apart,
+    dead atoms, padding (K = 6,000 of 6,144 positions) and an all-zero block:
+    the selections must be the bit-exact kernel's -- the lowest index of every
+    tie set (reference.py:55-85)."""
+    rng = np.random.default_rng(21)
+    vals = rng.standard_normal((K, 8, 8))
+    mask = wl.central_loss_mask(8, 8, 2, 2)
+    vals[1] = vals[0]            # elements 0 and 1 of thread 0
+    vals[56] = vals[40]          # threads 20 and 28: two lanes of warp 0
+    vals[164] = vals[100]        # threads 50 and 82: warps 1 and 2
+    vals[4000] = vals[5]         # far apart
+    for k in (2, 4001):          # dead: atoms living only on lost samples
+        vals[k] = 0.0
+        vals[k][mask] = rng.standard_normal(int(mask.sum()))
+    d = Dictionary(vals)
+    blocks = 160                 # more than one block per SM: the one-CTA kernels
+    sig = rng.uniform(0, 255, (blocks, 8, 8))
+    sig[7] = 0.0                 # all-zero metrics
+    cfg = ExtrapConfig(48, 0.5, 0.8)
+    a = fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion="exact")
+    b = fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion="scaled")
+    sa, sb = a.selected.cpu().numpy(), b.selected.cpu().numpy()
+    same = (sa == sb).all(axis=1)
+    assert int(same.sum()) == blocks, np.flatnonzero(~same)
+    assert not np.isin(sb, [1, 56, 164, 4000, 2, 4001]).any()
+    assert np.isin(sb, [0, 40, 100, 5]).any()      # the tie sets were reached
+    assert (sb[7] == 0).all() and (b.coefficients[7].cpu().numpy() == 0.0).all()
+    scale = a.coefficients.abs().amax(dim=1).clamp_min(1e-300)
+    assert float(((a.coefficients - b.coefficients).abs().amax(dim=1) / scale).max()) < 1e-10
+
+
 def test_stale_tables_detected():
     d = generate_dictionary("dct", 4, 4)
     mask = wl.central_loss_mask(4, 4, 2, 2)
