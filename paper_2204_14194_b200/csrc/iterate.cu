@@ -720,11 +720,11 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       const unsigned nearw = __ballot_sync(0xffffffffu, lane < NW && (sk_l >> 5) + 1u >= kb27);
       const int wstar = __ffs(nearw) - 1;
       // every element that can reach the tie threshold lies within one key
-      // unit (2^(e-15) for a top in [2^e, 2^(e+1))) of the largest when the
-      // quantum max(q, 1e-13 * top) is below that unit: compared through the
-      // exponent fields
+      // unit of the largest when the quantum max(q, 1e-13 * top) is below
+      // 2^(e-16) for a top in [2^e, 2^(e+1)) -- half a unit there, a whole one
+      // just below 2^e: compared through the exponent fields
       fastb = __popc(nearw) == 1 && kb >= 0x02000000u && kb < 0x7ff00000u &&
-              __double2hiint(q) < static_cast<int>(((kb >> 20) - 15u) << 20);
+              __double2hiint(q) < static_cast<int>(((kb >> 20) - 16u) << 20);
       if (fastb) {
         if (warp == wstar) {
           // the lanes holding an element within one key unit of the largest

@@ -482,7 +482,7 @@ def test_scaled_recursion_zero_metrics_and_dead_atoms(blocks):
 
 
 @pytest.mark.parametrize("K", [6000, 8192])
-def test_scaled_recursion_integer_max_shapes(K):
+def test_scaled_recursion_integer_max_shapes(monkeypatch, K):
     """The 24- and 32-element shapes of the scaled recursion (K > 5,120) track
     integer keys of the high words and resolve the exact top and the tie rule
     in one warp (csrc/iterate.cu, kIntMax). Exact ties between duplicated atoms
@@ -504,12 +504,24 @@ def test_scaled_recursion_integer_max_shapes(K):
     blocks = 160                 # more than one block per SM: the one-CTA kernels
     sig = rng.uniform(0, 255, (blocks, 8, 8))
     sig[7] = 0.0                 # all-zero metrics
+    sig[9] = 37.5 * vals[300]    # one atom's multiple: the top halves every iteration until the
+    #                              ratcheted quantum exceeds it (threshold <= 0: every live atom ties)
     cfg = ExtrapConfig(48, 0.5, 0.8)
     a = fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion="exact")
     b = fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion="scaled")
     sa, sb = a.selected.cpu().numpy(), b.selected.cpu().numpy()
     same = (sa == sb).all(axis=1)
+    same[9] = True               # (threshold-wide tie sets: compared bit for bit below instead)
     assert int(same.sum()) == blocks, np.flatnonzero(~same)
+    assert (sb[9, :8] == 300).all() and (sb[9] >= 0).all() and not np.isin(sb[9], [2, 4001]).any()
+    if K == 8192:
+        # the compare / select scaled kernel (128 x 64 shape: no integer keys) on the same
+        # table layout: the integer-key kernel must agree bit for bit, block 9 included
+        monkeypatch.setenv("FASE_SCALED_VARIANT", "128x64x2")
+        c = fase_extrapolate_batch(sig, mask, d, None, cfg, device=DEV, recursion="scaled")
+        monkeypatch.delenv("FASE_SCALED_VARIANT")
+        assert torch.equal(b.selected, c.selected)
+        assert torch.equal(b.coefficients, c.coefficients)
     assert not np.isin(sb, [1, 56, 164, 4000, 2, 4001]).any()
     assert np.isin(sb, [0, 40, 100, 5]).any()      # the tie sets were reached
     assert (sb[7] == 0).all() and (b.coefficients[7].cpu().numpy() == 0.0).all()
