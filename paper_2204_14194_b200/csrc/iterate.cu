@@ -55,6 +55,12 @@ constexpr unsigned kNone = 0xffffffffu;
 #ifndef FASE_SCALED_SEG
 #define FASE_SCALED_SEG 3
 #endif
+// (measurement: output rows re-derived at their use in the integer-key kernels; it
+// halves the 18-element shape's spills, yet config 1 stays 1.4% slower with integer
+// keys (0.690 vs 0.680 ms) and config 4 loses 1%: off, profiles/r02d/ab_intmax.txt)
+#ifndef FASE_INTMAX_OUTROW
+#define FASE_INTMAX_OUTROW 0
+#endif
 #ifndef FASE_INTMAX_MIN_EPT
 #define FASE_INTMAX_MIN_EPT 24
 #endif
@@ -403,6 +409,10 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
     if constexpr (kChunked) {
       asm volatile("" : "+l"(base));
       return base + static_cast<int64_t>(s_blk[half]) * a.ldo;
+    } else if constexpr (kIntMax && FASE_INTMAX_OUTROW) {
+      // (one lane writes the outputs: re-derived at the use, not held across the loop)
+      asm volatile("" : "+l"(base));
+      return base + static_cast<int64_t>(blockIdx.x) * a.ldo;
     } else {
       return hoisted;
     }
@@ -801,9 +811,9 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
             s_r[0] = pf;
             s_d[0] = cf;
             s_ftop = topx;
-            sel[it] = static_cast<int32_t>(cu);
-            proj[it] = pf;
-            coef[it] = cf;
+            out_row(a.sel, sel)[it] = static_cast<int32_t>(cu);
+            out_row(a.proj, proj)[it] = pf;
+            out_row(a.coef, coef)[it] = cf;
           }
         }
         block_sync();
@@ -818,9 +828,9 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
 #pragma unroll
           for (int sg = 0; sg < kSeg; ++sg) mbar_wait(&s_bar[sg], it & 1);
           for (int k = it + t; k < a.I; k += NT) {
-            sel[k] = -1;
-            proj[k] = 0.0;
-            coef[k] = 0.0;
+            out_row(a.sel, sel)[k] = -1;
+            out_row(a.proj, proj)[k] = 0.0;
+            out_row(a.coef, coef)[k] = 0.0;
           }
           write_synth(b);
           return;
