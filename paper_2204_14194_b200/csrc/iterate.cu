@@ -214,6 +214,9 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
   // spills) and keeps the compare / select running max.
   constexpr bool kIntMax = kScaled && (FASE_SCALED_LEAN & 32) && EPT >= FASE_INTMAX_MIN_EPT && EPT <= 32 && SPEC == 0;
   __shared__ unsigned s_wk[kIntMax ? NW : 1];  // kIntMax: the warps' largest keys
+  // ... and their atoms (not s_arg: the exact path republishes s_arg one barrier later,
+  // while slower warps may still be reading these)
+  __shared__ unsigned s_wa[kIntMax ? NW : 1];
   __shared__ double s_ftop;                    // kIntMax: the exact top of a resolved iteration
   // The staged row arrives in kSeg segments, each on its own mbarrier, so the
   // update can start on the first segment while the rest is still in flight.
@@ -565,11 +568,11 @@ __global__ void __launch_bounds__(NT * NB, MINB) fase_iterate_kernel(const fase_
       if (lane == 0) {
         const int e = 31 - static_cast<int>(wk & 31u);
         s_wk[warp] = wk;
-        s_arg[warp] = 2u * static_cast<unsigned>((e >> 1) * NT + warp * 32 + wl) + (e & 1);
+        s_wa[warp] = 2u * static_cast<unsigned>((e >> 1) * NT + warp * 32 + wl) + (e & 1);
       }
       block_sync();
       sk_l = lane < NW ? s_wk[lane] : 0u;
-      const unsigned sa = lane < NW ? s_arg[lane] : kNone;
+      const unsigned sa = lane < NW ? s_wa[lane] : kNone;
       kb = __reduce_max_sync(0xffffffffu, sk_l);
       guess = __reduce_min_sync(0xffffffffu, sk_l == kb ? sa : kNone);
       guess = guess < static_cast<unsigned>(K) ? guess : 0u;  // (an all-zero block: any row)
